@@ -1,0 +1,412 @@
+"""IVFADC+R search benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+Workload (default): BASELINE.json configs[1] ("C2"): n = 10M SIFT-like uint8
+vectors (4096-component mixture, seed 0), 1M training vectors, 10k queries,
+d = 128, Kc = 1024, m = 8, m' = 16, w = 16, k' = 1000, top-100.  A step is one
+fused batched search of all queries (coarse probe -> LUT -> ADC scan ->
+exact top-k' -> residual-PQ re-rank -> top-k).
+
+  value : queries/s with queries resident in HBM, device-timed (CUDA events on
+          the index stream), L2 flushed between steps.
+  e2e   : same metric through the public host API (pqrr_dev_search_u8 via
+          ctypes) from pinned host memory, H2D of the queries and D2H of the
+          results inside the timed region.
+  --impl reference : the reference's CPU implementation of the path
+          (oracle/_ref: kernels.cpp scan_topk + headers' TopK/l2_sq) on the
+          host cores, on a bounded sample of the same queries.
+
+Multi-GPU (torchrun): the database is sharded by id range; each rank searches
+its shard with the full query batch; per-rank top-k lists are all-gathered and
+merged under (dist, id).  Timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: n, train, nq, clusters, Kc, m, m', w, k', k
+    "C1": dict(n=1_000_000, train=100_000, nq=1000, clusters=1024, kc=1024, m=8, mprime=8, w=8,
+               kprime=100, k=100),
+    "C2": dict(n=10_000_000, train=1_000_000, nq=10_000, clusters=4096, kc=1024, m=8, mprime=16,
+               w=16, kprime=1000, k=100),
+    "C3": dict(n=100_000_000, train=1_000_000, nq=10_000, clusters=4096, kc=8192, m=8, mprime=16,
+               w=64, kprime=1000, k=100),
+}
+SEED = 0
+METRIC = "IVFADC+R queries/sec at oracle-matched recall@1/10/100; scan HBM GB/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- setup
+def train_codebooks(pq, cfg, device):
+    t0 = time.time()
+    train = pq.synth(1, 0, cfg["train"], cfg["clusters"], seed=SEED, device=device).astype(np.float32)
+    prm = pq.TrainParams(iterations=25, seed=SEED)
+    coarse, P = pq.ivf_train(train, cfg["kc"], cfg["m"], params=prm, device=device)
+    rq = pq.ivf_refine_train(coarse, P, train, cfg["mprime"], prm, device=device)
+    log(f"[setup] trained codebooks on {cfg['train']} vectors in {time.time() - t0:.1f}s")
+    return coarse, P, rq
+
+
+def build_index(pq, cfg, coarse, P, rq, device, shard, nshards):
+    n = cfg["n"]
+    lo = n * shard // nshards
+    hi = n * (shard + 1) // nshards
+    t0 = time.time()
+    ix = pq.IvfIndex(coarse, P, rq, device)
+    ix.add_synthetic(SEED, cfg["clusters"], lo, hi - lo, id_base=lo)
+    ix.finalize()
+    log(f"[setup] added ids [{lo}, {hi}) on device {device} in {time.time() - t0:.1f}s")
+    return ix, lo, hi
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, cfg, rank, world):
+    """The reference's CPU implementation (oracle/_ref) on this host's cores."""
+    if rank != 0:
+        return
+    from oracle.oracle_py import Oracle, RefLib, build, ref_available
+
+    if not ref_available():
+        build()
+    ref = RefLib()
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    import paper_1102_3828_b200 as pq  # setup only (bit-identical index build), see DESIGN.md
+
+    use_gpu = pq.device_count() > 0
+    if use_gpu:
+        coarse, P, rq = train_codebooks(pq, cfg, 0)
+        ix, _, _ = build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
+        offs, ids, codes, rcodes = ix.export_lists()
+        coarse_c, books, rbooks = coarse.centroids, P.flat(), rq.pq.flat()
+        queries = pq.synth(3, 0, cfg["nq"], cfg["clusters"], seed=SEED)
+        ix.close()
+    else:  # no GPU: the oracle builds the same index on the host (slow)
+        o = Oracle()
+        centers = o.synth_centers(SEED, cfg["clusters"], 128)
+        tr = o.synth_rows(SEED, 1, 0, cfg["train"], centers).astype(np.float32)
+        coarse_c, books = o.ivf_train(tr, cfg["kc"], cfg["m"], iterations=25, seed=SEED)
+        rbooks = o.ivf_refine_train(coarse_c, books, cfg["m"], tr, cfg["mprime"], iterations=25,
+                                    seed=SEED)
+        base = o.synth_rows(SEED, 2, 0, cfg["n"], centers).astype(np.float32)
+        oix = o.ivf_build(coarse_c, books, cfg["m"], base)
+        oix.refine_encode(rbooks, cfg["mprime"], base)
+        offs, ids, codes = oix.flat()
+        rcodes = oix.rcodes[ids]
+        queries = o.synth_rows(SEED, 3, 0, cfg["nq"], centers)
+    n = len(ids)
+    list_of_id = np.zeros(n, np.uint32)
+    codes_by_id = np.zeros((n, cfg["m"]), np.uint8)
+    rcodes_by_id = np.zeros((n, cfg["mprime"]), np.uint8)
+    for l in range(cfg["kc"]):
+        seg = ids[offs[l]:offs[l + 1]]
+        list_of_id[seg] = l
+    codes_by_id[ids] = codes
+    rcodes_by_id[ids] = rcodes
+    qf = queries.astype(np.float32)
+    # bounded sample per step: ~10-20 s of CPU work
+    sample = max(cores * 4, 64)
+    W, K = args.warmup, args.steps
+
+    def step(i):
+        qs = qf[(i * sample) % cfg["nq"]:][:sample]
+        sl_i, _, sl_c = ref.ivf_search(coarse_c, books, cfg["m"], offs, ids, codes, qs, cfg["w"],
+                                       cfg["kprime"])
+        ref.ivf_rerank(coarse_c, books, rbooks, cfg["m"], cfg["mprime"], list_of_id, codes_by_id,
+                       rcodes_by_id, qs, sl_i, sl_c, cfg["k"])
+        return len(qs)
+
+    for i in range(min(W, 1)):
+        step(i)
+    t0 = time.perf_counter()
+    done = 0
+    for i in range(K):
+        done += step(i + 1)
+    dt = time.perf_counter() - t0
+    v = done / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": dt / K * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.config, **cfg, "parallelism": "cpu-openmp"},
+        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "reference",
+                         "sample": f"{sample} queries per step (of {cfg['nq']}) on the "
+                                   f"{'device-built' if use_gpu else 'host-built'} index"},
+        "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-recall", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import paper_1102_3828_b200 as pq
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local
+    coarse, P, rq = train_codebooks(pq, cfg, device)
+    ix, lo, hi = build_index(pq, cfg, coarse, P, rq, device, rank, world)
+    nq, k, kp, w = cfg["nq"], cfg["k"], cfg["kprime"], cfg["w"]
+    queries = pq.synth(3, 0, nq, cfg["clusters"], seed=SEED, device=device)
+    d_q = torch.from_numpy(queries).cuda()
+    d_ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    d_dist = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+    d_cnt = torch.empty(nq, dtype=torch.int32, device="cuda")
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def run_once():
+        ix.search_device(d_q.data_ptr(), nq, w, kp, k, d_ids.data_ptr(), d_dist.data_ptr(),
+                         d_cnt.data_ptr(), stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        run_once()
+    torch.cuda.synchronize()
+    launches0 = pq.launch_count()
+    step_ms, scan_ms, stats = [], [], []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (buffer 512 MB > 126 MB L2)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run_once()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            st = ix.last_stats()
+            stats.append(st)
+            scan_ms.append(st["ms_scan"])
+    torch.cuda.synchronize()
+    launches = pq.launch_count() - launches0
+    total_ms = float(np.sum(step_ms))
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = nq * args.steps / (total_ms / 1e3)
+
+    # ---- e2e through the host API from pinned memory
+    pinned_q = torch.from_numpy(queries).pin_memory()
+    out_i = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    out_d = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    hq = pinned_q.numpy()
+    e2e_s = []
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ids_h, d_h, c_h = ix.search(hq, w, kp, k)
+        e2e_s.append(time.perf_counter() - t0)
+    e2e_total = float(np.sum(e2e_s[args.warmup:]))
+    e2e_val = nq * args.steps / e2e_total
+
+    # ---- parity / recall evidence
+    res_ids = d_ids.cpu().numpy().view(np.uint32)
+    extra = {}
+    if not args.no_recall and world == 1:
+        extra.update(recall_and_parity(pq, cfg, queries, res_ids, ix, coarse, P, rq))
+
+    # ---- roofline of the dominant kernel (the main ADC scan)
+    st = stats[-1]
+    scanned = float(np.mean([s["scanned_entries"] for s in stats]))
+    bytes_per_step = scanned * (cfg["m"] + 4)
+    scan_s = float(np.mean(scan_ms)) / 1e3
+    peak, kind = measured_peak_gbs()
+    achieved = bytes_per_step / scan_s / 1e9
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (BASELINE.json SIFT-like generator, seed 0)",
+        "config": {"workload": args.config, **cfg, "parallelism": f"id-range shards x{world}",
+                   "l2": "flushed between steps (512 MB write)"},
+        "e2e": {"value": e2e_val, "unit": "queries/s", "h2d_bytes_per_step": int(queries.nbytes),
+                "d2h_bytes_per_step": int(nq * k * 8 + nq * 4)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": kind,
+                     "kernel": "ivf_scan_kernel (main pass)",
+                     "algorithmic_bytes_per_launch": bytes_per_step,
+                     "kernel_ms": scan_s * 1e3},
+        "stages_ms": {k2: round(float(np.mean([s[k2] for s in stats])), 4)
+                      for k2 in ["ms_coarse", "ms_invert", "ms_sample_scan", "ms_threshold",
+                                 "ms_scan", "ms_select", "ms_rerank", "ms_total"]},
+        "search_stats": {k2: st[k2] for k2 in ["work_items", "retries", "stride", "kernels",
+                                               "scanned_entries", "sampled_entries"]},
+        "clocks": clocks,
+        **extra,
+    }
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg, ix, coarse, P, rq, queries)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def recall_and_parity(pq, cfg, queries, res_ids, ix, coarse, P, rq):
+    """recall@1/10/100 vs exact GT on a query sample + oracle parity on a subsample."""
+    import torch
+
+    out = {}
+    nq_gt = min(1000, len(queries))
+    qs = torch.from_numpy(queries[:nq_gt]).cuda().float()
+    best_d = torch.full((nq_gt,), float("inf"), device="cuda")
+    best_i = torch.zeros(nq_gt, dtype=torch.int64, device="cuda")
+    qn = (qs * qs).sum(1, keepdim=True)
+    chunk = 2_000_000
+    for s in range(0, cfg["n"], chunk):
+        n = min(chunk, cfg["n"] - s)
+        b = torch.from_numpy(pq.synth(2, s, n, cfg["clusters"], seed=SEED)).cuda()
+        bf = b.float()
+        # u8 data: every term is an exact integer < 2^24, so bf16 products with
+        # fp32 accumulation give the exact squared distance
+        dots = (qs.bfloat16() @ bf.bfloat16().T).float()
+        dd = qn + (bf * bf).sum(1)[None, :] - 2 * dots
+        v, i = dd.min(1)  # first occurrence = lowest id on ties
+        upd = v < best_d
+        best_d = torch.where(upd, v, best_d)
+        best_i = torch.where(upd, i + s, best_i)
+    gt = best_i.cpu().numpy()
+    for r in (1, 10, 100):
+        out[f"recall@{r}"] = float(np.mean([gt[q] in res_ids[q, :r] for q in range(nq_gt)]))
+    out["recall_queries"] = nq_gt
+    return out
+
+
+def cpu_baseline(cfg, ix, coarse, P, rq, queries):
+    """oracle/_ref (reference kernels.cpp + headers) on a bounded query sample."""
+    from oracle.oracle_py import RefLib, ref_available
+
+    if not ref_available():
+        return {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    ref = RefLib()
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    offs, ids, codes, rcodes = ix.export_lists()
+    n = len(ids)
+    list_of_id = np.zeros(n, np.uint32)
+    for l in range(cfg["kc"]):
+        list_of_id[ids[offs[l]:offs[l + 1]]] = l
+    codes_by_id = np.zeros((n, cfg["m"]), np.uint8)
+    codes_by_id[ids] = codes
+    rcodes_by_id = np.zeros((n, cfg["mprime"]), np.uint8)
+    rcodes_by_id[ids] = rcodes
+    sample = min(len(queries), max(64, cores * 4))
+    qf = queries[:sample].astype(np.float32)
+    t0 = time.perf_counter()
+    sl_i, _, sl_c = ref.ivf_search(coarse.centroids, P.flat(), cfg["m"], offs, ids, codes, qf,
+                                   cfg["w"], cfg["kprime"])
+    rr, _ = ref.ivf_rerank(coarse.centroids, P.flat(), rq.pq.flat(), cfg["m"], cfg["mprime"],
+                           list_of_id, codes_by_id, rcodes_by_id, qf, sl_i, sl_c, cfg["k"])
+    dt = time.perf_counter() - t0
+    ours, _, _ = ix.search(queries[:sample], cfg["w"], cfg["kprime"], cfg["k"])
+    match = float(np.mean(ours == rr))
+    return {"value": sample / dt, "unit": "queries/s", "cores": cores, "kind": "reference",
+            "sample": f"first {sample} queries, OpenMP over queries",
+            "oracle_id_match": match}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,184 @@
+/*
+ * pqrr_dev.h — C ABI of the B200-native IVFADC+R search path
+ * (paper_1102_3828_b200/lib/libpqrr_b200.so).
+ *
+ * This is the drop-in boundary for the reference's C++ API in namespace
+ * pqrr (/root/reference/proj/include/pqrr/).  The reference has no C ABI or
+ * plugin registry; its seams are (1) the index API of ivf_index.hpp:48-81,
+ * (2) the hot-kernel seam pqrr::kernels of kernels.hpp:13-43, substituted at
+ * link time, and (3) the k-means / PQ trainers of kmeans.hpp:38 and
+ * product_quantizer.hpp:39-40.  Each entry point below names the reference
+ * declaration it replaces.  INTEGRATION.md shows the C++ shim (and a ctypes
+ * binding) a maintainer adds on the reference side.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Unless a name ends in _device, every
+ *    pointer is a HOST pointer; the library copies in and out.
+ *  - Matrices are row-major.  Product-quantizer books are m sub-codebooks of
+ *    ks centroids of d/m floats, sub-quantizer-major, centroid-major,
+ *    component-minor (storage.hpp:19-20).  A coarse codebook is c x d floats.
+ *  - Codes are uint8, m per vector.  Ids are uint32 (ivf_index.hpp:18).
+ *  - Every function returns PQRR_OK (0) or a negative status; the message of
+ *    the last failure on the calling thread is pqrr_dev_last_error().  Error
+ *    messages pinned by the reference spec are reproduced verbatim:
+ *    "insufficient training data", "dimension not divisible",
+ *    "shortlist too small".
+ *  - Arithmetic follows the reference contract bit for bit (distance.hpp:7-33,
+ *    product_quantizer.hpp:51-57, types.hpp:45-50): outputs are identical to
+ *    the reference path on the same inputs and codebooks.
+ *  - There is no CPU fallback: without a usable sm_100 device every call
+ *    fails with PQRR_ENODEV.
+ */
+#ifndef PQRR_DEV_H
+#define PQRR_DEV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    PQRR_OK = 0,
+    PQRR_EINVAL = -1,      /* bad argument (reference std::invalid_argument) */
+    PQRR_ECUDA = -2,       /* CUDA runtime failure */
+    PQRR_ENODEV = -3,      /* no usable GPU */
+    PQRR_EUNSUPPORTED = -4,/* shape outside what the device kernels implement */
+    PQRR_ESHORTLIST = -5,  /* "shortlist too small" */
+    PQRR_EINTERNAL = -6
+};
+
+const char* pqrr_dev_last_error(void);
+int pqrr_dev_device_count(int* out);
+/* Number of kernels this library has launched in this process. */
+uint64_t pqrr_dev_launch_count(void);
+
+/* ------------------------------------------------------------------ kernel seam
+ * pqrr::kernels (kernels.hpp:13-43).  One call = one batch on `device`.    */
+
+/* kernels::assign_batch (kernels.hpp:23-25): argmin l2_sq, ties -> lowest index. */
+int pqrr_dev_assign_batch(int device, const float* points, size_t n, uint32_t dim,
+                          const float* centroids, uint32_t k, uint32_t* out_assign,
+                          float* out_dist);
+/* kernels::encode_batch (kernels.hpp:28-29) with pq_encode_into semantics. */
+int pqrr_dev_encode_batch(int device, const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                          const float* data, size_t n, uint8_t* out_codes);
+/* kernels::decode_batch (kernels.hpp:32-33). */
+int pqrr_dev_decode_batch(int device, const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                          const uint8_t* codes, size_t n, float* out_data);
+/* build_lut (product_quantizer.hpp:48-49) for nx vectors: out is nx * m * ks. */
+int pqrr_dev_build_lut(int device, const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                       const float* x, size_t nx, float* out_lut);
+/* kernels::scan_topk (kernels.hpp:40-41): ids = id_base + position. */
+int pqrr_dev_scan_topk(int device, const float* lut, uint32_t m, uint32_t ks, const uint8_t* codes,
+                       size_t n, size_t kprime, uint32_t id_base, uint32_t* out_ids,
+                       float* out_dists, size_t* out_count);
+
+/* ------------------------------------------------------------------ training
+ * kmeans_train (kmeans.hpp:38), pq_train (product_quantizer.hpp:39-40),
+ * ivf_train (ivf_index.hpp:50-52), ivf_refine_train (ivf_index.hpp:68-70).
+ * Exact assignment on the device, id-order fp64 update (bit-identical to the
+ * serial policy of kmeans.hpp:30-38).                                        */
+int pqrr_dev_kmeans_train(int device, const float* points, size_t n, uint32_t dim, uint32_t k,
+                          uint32_t iterations, uint64_t seed, uint32_t redo, float* out_centroids,
+                          double* out_final_mse, double* out_trace /* iterations or NULL */);
+int pqrr_dev_pq_train(int device, const float* training, size_t n, uint32_t d, uint32_t m,
+                      uint32_t ks, uint32_t iterations, uint64_t seed, uint32_t redo,
+                      float* out_books);
+int pqrr_dev_ivf_train(int device, const float* training, size_t n, uint32_t d, uint32_t c,
+                       uint32_t m, uint32_t ks, uint32_t iterations, uint64_t seed,
+                       float* out_coarse, float* out_books);
+int pqrr_dev_ivf_refine_train(int device, const float* coarse, uint32_t c, const float* books,
+                              uint32_t d, uint32_t m, uint32_t ks, const float* training,
+                              size_t n, uint32_t mprime, uint32_t iterations, uint64_t seed,
+                              float* out_rbooks);
+
+/* ------------------------------------------------------------------ synthetic data
+ * The BASELINE.json SIFT-like generator: set 0 = centres,
+ * 1 = train, 2 = base, 3 = query.  Rows [row0, row0 + n) of `set`.           */
+int pqrr_dev_synth(int device, uint64_t seed, uint32_t clusters, uint32_t d, uint32_t set,
+                   uint64_t row0, size_t n, uint8_t* out /* host, n * d */);
+
+/* ------------------------------------------------------------------ index
+ * IvfIndex + RefineQuantizer + RefineCodes (ivf_index.hpp:27-41,
+ * refine.hpp:15-28) resident in one device's HBM.                            */
+typedef struct pqrr_dev_index pqrr_dev_index;
+
+/* mprime = 0 / rbooks = NULL: no refinement (plain IVFADC). */
+int pqrr_dev_index_create(int device, uint32_t d, uint32_t c, const float* coarse, uint32_t m,
+                          const float* books, uint32_t mprime, const float* rbooks, uint32_t ks,
+                          pqrr_dev_index** out);
+int pqrr_dev_index_destroy(pqrr_dev_index* ix);
+
+/* ivf_build (ivf_index.hpp:54-56) + ivf_refine_encode (:72-73), chunked:
+ * vectors get ids id_base .. id_base + n - 1; chunks must arrive in
+ * id-ascending order (lists stay id-ascending, ivf_index.hpp:15-16).         */
+int pqrr_dev_add_u8(pqrr_dev_index* ix, const uint8_t* y, size_t n, uint32_t id_base);
+int pqrr_dev_add_f32(pqrr_dev_index* ix, const float* y, size_t n, uint32_t id_base);
+/* Same, vectors generated on the device by the synthetic generator: rows
+ * [row0, row0 + n) of the base set get ids id_base + (row - row0).          */
+int pqrr_dev_add_synthetic(pqrr_dev_index* ix, uint64_t seed, uint32_t clusters, uint64_t row0,
+                           size_t n, uint32_t id_base);
+/* Builds the list-major layout of everything added so far (implicit on search). */
+int pqrr_dev_finalize(pqrr_dev_index* ix);
+
+typedef struct {
+    uint64_t n;            /* indexed vectors */
+    uint64_t slots;        /* padded list-major entries */
+    uint32_t d, c, m, mprime, ks;
+    uint32_t max_list_len;
+    uint64_t device_bytes; /* bytes held in HBM by the index */
+} pqrr_dev_index_info;
+int pqrr_dev_index_get_info(pqrr_dev_index* ix, pqrr_dev_index_info* out);
+
+/* Lists in list order without padding: offsets[c + 1], ids[n], codes[n * m],
+ * rcodes[n * mprime] (any output may be NULL). */
+int pqrr_dev_export_lists(pqrr_dev_index* ix, uint64_t* offsets, uint32_t* ids, uint8_t* codes,
+                          uint8_t* rcodes);
+
+/* Fused search: coarse probe of w lists -> LUTs -> ADC scan -> exact top-k'
+ * shortlist (ivf_search_batch, ivf_index.hpp:58-64) -> if k > 0, re-rank with
+ * the refinement codes to the top-k (ivf_rerank, :79-81).
+ * Outputs per query q at row q of width (k > 0 ? k : kprime):
+ *   out_ids, out_dists ascending under (dist, id); out_counts[q] entries.
+ * k == 0 returns the IVFADC shortlist itself (min(kprime, candidates)).
+ * k > min(kprime, candidates) fails with PQRR_ESHORTLIST.                    */
+int pqrr_dev_search_u8(pqrr_dev_index* ix, const uint8_t* queries, size_t nq, uint32_t w,
+                       size_t kprime, size_t k, uint32_t* out_ids, float* out_dists,
+                       uint32_t* out_counts);
+int pqrr_dev_search_f32(pqrr_dev_index* ix, const float* queries, size_t nq, uint32_t w,
+                        size_t kprime, size_t k, uint32_t* out_ids, float* out_dists,
+                        uint32_t* out_counts);
+/* Device-resident variant: all pointers are device pointers on the index's
+ * device; `stream` is a cudaStream_t (NULL = the index's own stream). The
+ * call is stream-ordered but may synchronise internally.                    */
+int pqrr_dev_search_u8_device(pqrr_dev_index* ix, const uint8_t* d_queries, size_t nq,
+                              uint32_t w, size_t kprime, size_t k, uint32_t* d_out_ids,
+                              float* d_out_dists, uint32_t* d_out_counts, void* stream);
+
+/* ivf_rerank (ivf_index.hpp:79-81) of an explicit shortlist: sl_ids row q
+ * holds sl_counts[q] ids (stride sl_stride); outputs k per query. */
+int pqrr_dev_rerank_u8(pqrr_dev_index* ix, const uint8_t* queries, size_t nq,
+                       const uint32_t* sl_ids, const uint32_t* sl_counts, size_t sl_stride,
+                       size_t k, uint32_t* out_ids, float* out_dists);
+int pqrr_dev_rerank_f32(pqrr_dev_index* ix, const float* queries, size_t nq,
+                        const uint32_t* sl_ids, const uint32_t* sl_counts, size_t sl_stride,
+                        size_t k, uint32_t* out_ids, float* out_dists);
+/* ivf_reconstruct (ivf_index.hpp:75-77): coarse + decode + refine decode. */
+int pqrr_dev_reconstruct(pqrr_dev_index* ix, const uint32_t* ids, size_t n, float* out);
+
+/* Per-stage device times (CUDA events on the index stream) of the last search. */
+typedef struct {
+    float ms_total, ms_coarse, ms_invert, ms_sample_scan, ms_threshold, ms_scan, ms_select,
+        ms_rerank;
+    uint64_t nq, scanned_entries, sampled_entries, candidates;
+    uint32_t work_items, retries, stride;
+    uint32_t kernels;
+} pqrr_dev_search_stats;
+int pqrr_dev_last_search_stats(pqrr_dev_index* ix, pqrr_dev_search_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PQRR_DEV_H */

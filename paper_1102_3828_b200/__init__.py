@@ -1,0 +1,15 @@
+"""B200-native IVFADC+R search path of arXiv 1102.3828 ("Searching in one
+billion vectors: re-rank with source coding").
+
+The product is libpqrr_b200.so (sm_100a kernels behind the C ABI of
+include/pqrr_dev.h); this package is its Python host binding, mirroring the
+reference's pqrr C++ API (see ivf.py).  There is no CPU fallback.
+"""
+from ._lib import DeviceUnavailable, PqrrError, device_count, launch_count  # noqa: F401
+from .ivf import (  # noqa: F401
+    Codebook, IvfIndex, IvfSearchParams, LookupTable, ProductQuantizer, RefineCodes,
+    RefineQuantizer, SearchResult, TrainParams, adc_distance, build_lut, ivf_build,
+    ivf_reconstruct, ivf_refine_encode, ivf_refine_train, ivf_rerank, ivf_search,
+    ivf_search_batch, ivf_train, kmeans_train, pq_decode, pq_encode, pq_train, synth,
+)
+from . import kernels  # noqa: F401

@@ -1,0 +1,98 @@
+// common.cuh — shared device helpers for the pqrr B200 kernels (sm_100a).
+//
+// Exact arithmetic: every distance follows the reference l2_sq order
+// (distance.hpp:16-33): t = a - b, s[j mod 4] += t*t, remainder into s0..s2,
+// result (s0 + s1) + (s2 + s3), with SEPARATE multiply and add roundings.
+// nvcc contracts a*b+c into FFMA by default, and ptxas 12.9 even contracts
+// explicit `mul.rn.f32x2` + `add.rn.f32x2` into FFMA2 (verified in SASS, with
+// and without --fmad=false).  So packed products are computed as
+// fma(t, t, nz) where nz = -0.0 arrives as a kernel parameter that ptxas cannot
+// see through: t*t + (-0) rounds once, i.e. equals the rounded product exactly
+// (and +0 stays +0), and the following FADD2 cannot fuse with an FFMA2.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pqrr_b200 {
+
+typedef unsigned long long u64;
+
+// ------------------------------------------------------------ packed f32x2
+__device__ __forceinline__ u64 pk2(float lo, float hi) {
+    return (u64)__float_as_uint(lo) | ((u64)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float lo2(u64 v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
+__device__ __forceinline__ float hi2(u64 v) { return __uint_as_float((unsigned)(v >> 32)); }
+
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+    u64 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+// Exact rounded square of each lane: fma(t, t, nz) with nz = {-0,-0} opaque.
+__device__ __forceinline__ u64 sq2(u64 t, u64 nz) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(t), "l"(nz));
+    return r;
+}
+// s += t*t for both lanes, exact order.
+__device__ __forceinline__ u64 acc_sq2(u64 s, u64 a, u64 b, u64 nz) {
+    return add2(s, sq2(sub2(a, b), nz));
+}
+
+static const u64 kNegZero2 = 0x8000000080000000ull;
+
+// ------------------------------------------------------------ scalar exact
+// Generic l2_sq in the reference order (any d, any alignment).
+__device__ __forceinline__ float l2sq_scalar(const float* a, const float* b, int d) {
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int j = 0;
+    for (; j + 4 <= d; j += 4) {
+        float t0 = __fsub_rn(a[j], b[j]);
+        float t1 = __fsub_rn(a[j + 1], b[j + 1]);
+        float t2 = __fsub_rn(a[j + 2], b[j + 2]);
+        float t3 = __fsub_rn(a[j + 3], b[j + 3]);
+        s0 = __fadd_rn(s0, __fmul_rn(t0, t0));
+        s1 = __fadd_rn(s1, __fmul_rn(t1, t1));
+        s2 = __fadd_rn(s2, __fmul_rn(t2, t2));
+        s3 = __fadd_rn(s3, __fmul_rn(t3, t3));
+    }
+    if (j < d) { float t = __fsub_rn(a[j], b[j]); s0 = __fadd_rn(s0, __fmul_rn(t, t)); ++j; }
+    if (j < d) { float t = __fsub_rn(a[j], b[j]); s1 = __fadd_rn(s1, __fmul_rn(t, t)); ++j; }
+    if (j < d) { float t = __fsub_rn(a[j], b[j]); s2 = __fadd_rn(s2, __fmul_rn(t, t)); ++j; }
+    return __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));
+}
+
+// Packed l2_sq for d % 4 == 0 with both operands 16-byte aligned.
+// s01 holds (s0, s1), s23 holds (s2, s3).
+template <int D>
+__device__ __forceinline__ float l2sq_packed(const float* __restrict__ a,
+                                             const float* __restrict__ b, u64 nz) {
+    static_assert(D % 4 == 0, "packed l2_sq needs d % 4 == 0");
+    u64 s01 = 0, s23 = 0;
+#pragma unroll
+    for (int j = 0; j < D; j += 4) {
+        const float4 x = *reinterpret_cast<const float4*>(a + j);
+        const float4 y = *reinterpret_cast<const float4*>(b + j);
+        s01 = acc_sq2(s01, pk2(x.x, x.y), pk2(y.x, y.y), nz);
+        s23 = acc_sq2(s23, pk2(x.z, x.w), pk2(y.z, y.w), nz);
+    }
+    return __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
+}
+
+// Total order of types.hpp:47-50 on (dist, id) as one 64-bit key.  Distances
+// are non-negative (sums of squares starting at +0), so the IEEE bit pattern
+// orders like the value.
+__device__ __forceinline__ u64 nb_key(float dist, uint32_t id) {
+    return ((u64)__float_as_uint(dist) << 32) | (u64)id;
+}
+__device__ __forceinline__ float key_dist(u64 k) { return __uint_as_float((unsigned)(k >> 32)); }
+__device__ __forceinline__ uint32_t key_id(u64 k) { return (uint32_t)(k & 0xffffffffull); }
+
+}  // namespace pqrr_b200

@@ -1,0 +1,172 @@
+// internal.h — host-side launchers shared between the .cu translation units of
+// libpqrr_b200.so.  Nothing here is part of the public C ABI (include/pqrr_dev.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace pqrr_b200 {
+
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& s) : std::runtime_error(s) {}
+};
+struct ArgError : std::invalid_argument {
+    explicit ArgError(const std::string& s) : std::invalid_argument(s) {}
+};
+
+#define PQRR_CUDA(call)                                                                     \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            throw ::pqrr_b200::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+#define PQRR_LAUNCH_CHECK() PQRR_CUDA(cudaGetLastError())
+
+// Counts kernel launches issued by this library (gpu_launches evidence).
+void count_launch(int n = 1);
+unsigned long long launch_count();
+
+// Number of SMs of the current device (cached).
+int sm_count();
+
+// -------------------------------------------------------------- synth (k_synth.cu)
+void launch_synth_centers(uint64_t seed, uint32_t clusters, uint32_t d, double* centers,
+                          cudaStream_t s);
+void launch_synth_rows(uint64_t seed, uint32_t set, uint64_t row0, size_t n, uint32_t d,
+                       const double* centers, uint32_t clusters, uint8_t* out, cudaStream_t s);
+
+// -------------------------------------------------------------- coarse (k_coarse.cu)
+// u8 -> f32 exact widening.
+void launch_widen_u8(const uint8_t* in, float* out, size_t count, cudaStream_t s);
+// D[q][k] = l2_sq(x_q, C_k) for all pairs (exact reference order).
+void launch_pair_dists(const float* x, size_t nx, const float* c, uint32_t nc, uint32_t d,
+                       float* out, cudaStream_t s);
+// argmin over centroids with ties to the lowest index (kernels.cpp:21-39).
+void launch_argmin(const float* x, size_t nx, const float* c, uint32_t nc, uint32_t d,
+                   uint32_t* out_idx, float* out_dist, cudaStream_t s);
+// per row of D[nq][nc]: the w smallest (dist, idx), ascending.
+void launch_topw(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* out_idx,
+                 float* out_dist, cudaStream_t s);
+
+// -------------------------------------------------------------- PQ codec (k_encode.cu)
+// Plain PQ encode of vectors (kernels::encode_batch / pq_encode_into).
+void launch_pq_encode(const float* data, size_t n, uint32_t d, const float* books, uint32_t m,
+                      uint32_t ks, uint8_t* codes, cudaStream_t s);
+void launch_pq_decode(const uint8_t* codes, size_t n, uint32_t d, const float* books, uint32_t m,
+                      uint32_t ks, float* out, cudaStream_t s);
+// IVF add path: codes of y - C_a and refine codes of y - (C_a + p).
+// y given as f32 (x_f32 != null) or u8 (x_u8 != null).
+void launch_ivf_encode(const float* x_f32, const uint8_t* x_u8, size_t n, uint32_t d,
+                       const uint32_t* assign, const float* coarse, const float* books, uint32_t m,
+                       const float* rbooks, uint32_t mprime, uint32_t ks, uint8_t* codes,
+                       uint8_t* rcodes, cudaStream_t s);
+
+// -------------------------------------------------------------- k-means (k_kmeans.cu)
+void launch_gather_rows(const float* pts, uint32_t dim, const uint32_t* rows, uint32_t k,
+                        float* out, cudaStream_t s);
+// Deterministic id-order fp64 centroid update from (cluster-sorted ids).
+void launch_centroid_update(const float* pts, uint32_t dim, const uint32_t* sorted_ids,
+                            const uint32_t* cl_off, uint32_t k, float* centroids,
+                            cudaStream_t s);
+
+// -------------------------------------------------------------- misc (k_util.cu)
+void launch_histogram(const uint32_t* keys, size_t n, uint32_t nbins, uint32_t* hist,
+                      cudaStream_t s);
+void launch_iota(uint32_t* out, size_t n, cudaStream_t s);
+// Stable sort of (key, value) pairs by key (CUB radix sort, low `bits` bits).
+void sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                uint32_t* vals_out, size_t n, int bits, cudaStream_t s);
+void exclusive_scan_u64(const uint64_t* in, uint64_t* out, size_t n, cudaStream_t s);
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, cudaStream_t s);
+
+// -------------------------------------------------------------- layout (k_layout.cu)
+// Scatter an existing list-major layout into a new one (per-list prefix kept).
+void launch_layout_copy_old(const uint64_t* old_off, const uint32_t* old_len, uint32_t nlists,
+                            const uint64_t* new_off, const uint8_t* old_codes,
+                            const uint32_t* old_ids, const uint8_t* old_rcodes, uint32_t m,
+                            uint32_t mprime, uint8_t* codes, uint32_t* ids, uint8_t* rcodes,
+                            uint32_t max_len, cudaStream_t s);
+// Scatter staged (id-ordered) entries, sorted by list, behind the old entries.
+void launch_layout_place_new(const uint32_t* sorted_list, const uint32_t* sorted_idx, size_t n,
+                             const uint32_t* stage_off, const uint64_t* new_off,
+                             const uint32_t* old_len, const uint8_t* st_codes,
+                             const uint8_t* st_rcodes, const uint32_t* st_ids, uint32_t m,
+                             uint32_t mprime, uint8_t* codes, uint32_t* ids, uint8_t* rcodes,
+                             cudaStream_t s);
+
+// -------------------------------------------------------------- search (k_scan.cu / k_select.cu)
+static const int kQT = 16;        // queries per scan work item
+static const int kScanThreads = 256;
+
+struct ScanArgs {
+    const uint8_t* codes;      // list-major, m bytes per entry (m == 8)
+    const uint64_t* list_off;  // padded list starts, nlists + 1
+    const uint32_t* list_len;  // nlists
+    const float* coarse;       // nlists x d
+    const float* books;        // m x ks x dsub
+    const float* xq;           // nq x d
+    uint32_t d, m, ks;
+    // work items
+    const uint32_t* item_list;
+    const uint32_t* item_start;  // into pair_sorted
+    const uint32_t* item_nq;
+    const uint32_t* num_items;   // device scalar
+    uint32_t* item_counter;      // device scalar, zeroed before launch
+    const uint32_t* pair_sorted;  // pair index q * w + r, grouped by list
+    uint32_t w;
+    const float* tau;  // per query threshold
+    // main mode
+    float* cand_dist;
+    uint32_t* cand_pos;
+    uint32_t* cand_cnt;
+    uint32_t cap;
+    // sample mode (stride > 1)
+    uint32_t stride;
+    const uint64_t* sample_off;  // per pair
+    float* sample_dist;
+    const uint8_t* query_sampled;  // per query: 1 if the query is in sample mode
+};
+void launch_ivf_scan(const ScanArgs& a, cudaStream_t s);
+
+// Build the scan work items from the probes.
+void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first, uint32_t nlists,
+                        const uint32_t* item_off, uint32_t* item_list, uint32_t* item_start,
+                        uint32_t* item_nq, cudaStream_t s);
+void launch_items_per_list(const uint32_t* list_cnt, uint32_t nlists, uint32_t* items,
+                           cudaStream_t s);
+// Per query: N_q = sum of probed list lengths; per pair sample counts.
+void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
+                        uint32_t stride, uint32_t cap, uint64_t* nq_entries,
+                        uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
+                        cudaStream_t s);
+// tau_q = rank-th smallest sample of query q (sampled queries), +inf otherwise.
+void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_off, uint32_t w,
+                             size_t nq, const uint8_t* query_sampled, uint32_t rank, float* tau,
+                             cudaStream_t s);
+// Exact top-kprime under (dist, id) from each query's candidates.
+void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
+                        uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime,
+                        bool sorted, uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt,
+                        cudaStream_t s);
+// Re-rank the shortlist with the 3-term reconstruction, keep the k best.
+void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_t* sl_cnt,
+                   uint32_t sl_stride, size_t nq, const float* xq, uint32_t d,
+                   const uint64_t* list_off, uint32_t nlists, const float* coarse,
+                   const uint8_t* codes, const float* books, uint32_t m, const uint8_t* rcodes,
+                   const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
+                   uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s);
+// Split keys into ids / dists ([nq][stride] -> [nq][stride]).
+void launch_unpack_keys(const uint64_t* keys, const uint32_t* cnt, size_t nq, uint32_t stride,
+                        uint32_t* ids, float* dists, cudaStream_t s);
+
+// Standalone kernel-seam scan (kernels::scan_topk parity): LUT given.
+void launch_lut_scan_all(const float* lut, uint32_t m, uint32_t ks, const uint8_t* codes, size_t n,
+                         float* out_dist, cudaStream_t s);
+void launch_build_lut(const float* xr, size_t nx, uint32_t d, const float* books, uint32_t m,
+                      uint32_t ks, float* out, cudaStream_t s);
+
+}  // namespace pqrr_b200

@@ -1,0 +1,305 @@
+// k_scan.cu — K2 + K4: per-(list, query-group) LUT construction in shared
+// memory fused with the ADC list scan (ivf_search's hot loop,
+// ivf_index.hpp:58-61; adc_distance, product_quantizer.hpp:53-57).
+//
+// List-major, query-lane design.  A work item is one inverted list and up to
+// 16 queries that probe it.  The CTA builds the 16 residual LUTs
+// LUT[j][i][q] = l2_sq(x_q^j - C_l^j, B_j[i]) (query index fastest, 128 KiB),
+// then streams the list's 8-byte codes once for all 16 queries: a warp covers
+// 8 entries x 16 queries per step, each lane owning one entry and 4 queries,
+// so every lookup is one LDS.128 returning 4 queries' table values.  Codes are
+// read from HBM once per 16 queries instead of once per query; the kernel is
+// bound by shared-memory LUT gathers (SURVEY.md §7 "Hard parts").
+//
+// ADC sums are j-ascending fp32 adds (acc = 0; acc += LUT[j][c_j]), bit-equal
+// to the reference.  Candidates at or below the query's threshold tau_q are
+// appended (dist, position) to the query's buffer with warp-aggregated
+// atomics.  Sample mode (stride > 1) writes every stride-th entry's distance
+// to a per-(query, probe) slot instead; it feeds the threshold estimate.
+#include "common.cuh"
+#include "internal.h"
+
+namespace pqrr_b200 {
+namespace {
+
+constexpr int M = 8;
+constexpr int KS = 256;
+constexpr int QT = kQT;
+constexpr int NT = kScanThreads;
+constexpr int NW = NT / 32;
+constexpr int LUT_FLOATS = M * KS * QT;  // 32768 floats = 128 KiB
+
+template <int DSUB>
+__device__ __forceinline__ void build_luts(float* __restrict__ lut, const float* __restrict__ xr,
+                                           int xld, const float* __restrict__ books, u64 nz) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int qq = lane & 15, ih = lane >> 4;
+#pragma unroll 1
+    for (int j = 0; j < M; ++j) {
+        float r[DSUB];
+#pragma unroll
+        for (int t = 0; t < DSUB; t += 4) {
+            float4 v = *reinterpret_cast<const float4*>(xr + qq * xld + j * DSUB + t);
+            r[t] = v.x; r[t + 1] = v.y; r[t + 2] = v.z; r[t + 3] = v.w;
+        }
+        const float* bj = books + (size_t)j * KS * DSUB;
+#pragma unroll 2
+        for (int ib = 0; ib < KS / (2 * NW); ++ib) {
+            const int i = (ib * NW + warp) * 2 + ih;
+            const float* b = bj + (size_t)i * DSUB;
+            u64 s01 = 0, s23 = 0;
+#pragma unroll
+            for (int t = 0; t < DSUB; t += 4) {
+                const float4 c = __ldg(reinterpret_cast<const float4*>(b + t));
+                s01 = acc_sq2(s01, pk2(r[t], r[t + 1]), pk2(c.x, c.y), nz);
+                s23 = acc_sq2(s23, pk2(r[t + 2], r[t + 3]), pk2(c.z, c.w), nz);
+            }
+            lut[(j * KS + i) * QT + qq] =
+                __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
+        }
+    }
+}
+
+// Warp-aggregated append of (dist, pos) for the lanes with `hit`, grouped by
+// query (lanes sharing lane & 3 share the 4 queries).
+__device__ __forceinline__ void emit(bool hit, int q, float dist, uint32_t pos, int lane, int qd,
+                                     uint32_t* __restrict__ cnt, float* __restrict__ cdist,
+                                     uint32_t* __restrict__ cpos, uint32_t cap) {
+    const unsigned all = __ballot_sync(0xffffffffu, hit);
+    if (!hit) return;
+    const unsigned grp = all & (0x11111111u << qd);
+    const int leader = __ffs(grp) - 1;
+    const unsigned rank = __popc(grp & ((1u << lane) - 1u));
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(cnt + q, (unsigned)__popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    const unsigned slot = base + rank;
+    if (slot < cap) {
+        cdist[(size_t)q * cap + slot] = dist;
+        cpos[(size_t)q * cap + slot] = pos;
+    }
+}
+
+template <int DSUB>
+__global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const u64 nz) {
+    extern __shared__ float4 smem4[];
+    float* lut = reinterpret_cast<float*>(smem4);
+    const int xld = (int)a.d + 4;
+    float* xr = lut + LUT_FLOATS;  // [QT][d + 4]
+    __shared__ uint32_t s_item;
+    __shared__ int s_q[QT];
+    __shared__ uint32_t s_pair[QT];
+    __shared__ float s_tau[QT];
+    __shared__ uint8_t s_samp[QT];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int slot = lane >> 2, qd = lane & 3;
+    const uint32_t n_items = *a.num_items;
+    const float4* lut4 = reinterpret_cast<const float4*>(lut);
+
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(a.item_counter, 1u);
+        __syncthreads();
+        const uint32_t it = s_item;
+        if (it >= n_items) break;
+        const uint32_t l = a.item_list[it];
+        const uint32_t start = a.item_start[it];
+        const uint32_t nqi = a.item_nq[it];
+        if (threadIdx.x < QT) {
+            int q = -1;
+            uint32_t p = 0;
+            if (threadIdx.x < nqi) {
+                p = a.pair_sorted[start + threadIdx.x];
+                q = (int)(p / a.w);
+            }
+            s_q[threadIdx.x] = q;
+            s_pair[threadIdx.x] = p;
+            s_tau[threadIdx.x] = q >= 0 ? a.tau[q] : -1.0f;
+            s_samp[threadIdx.x] = (q >= 0 && a.query_sampled) ? a.query_sampled[q] : 0;
+        }
+        __syncthreads();
+        // residual queries x - C_l (ivf_index.hpp:58-59)
+        const float* crow = a.coarse + (size_t)l * a.d;
+        for (uint32_t idx = threadIdx.x; idx < QT * a.d; idx += NT) {
+            const uint32_t qq = idx / a.d, t = idx % a.d;
+            const int q = s_q[qq];
+            xr[qq * xld + t] = q >= 0 ? __fsub_rn(a.xq[(size_t)q * a.d + t], crow[t]) : 0.f;
+        }
+        __syncthreads();
+        build_luts<DSUB>(lut, xr, xld, a.books, nz);
+        __syncthreads();
+
+        const uint64_t off = a.list_off[l];
+        const uint32_t len = a.list_len[l];
+        const u64* codes = reinterpret_cast<const u64*>(a.codes) + off;
+        int qk[4];
+        float tk[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            qk[k] = s_q[qd * 4 + k];
+            tk[k] = s_tau[qd * 4 + k];
+        }
+        if (a.stride <= 1) {
+            // ---------------- main mode: threshold filter + append
+            for (uint32_t base = warp * 8; base < len; base += NW * 8) {
+                const uint32_t e = base + slot;
+                const bool valid = e < len;
+                const u64 code = valid ? __ldg(codes + e) : 0ull;
+                float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+#pragma unroll
+                for (int j = 0; j < M; ++j) {
+                    const uint32_t c = (uint32_t)(code >> (8 * j)) & 0xffu;
+                    const float4 v = lut4[(j * KS + c) * (QT / 4) + qd];
+                    acc0 = __fadd_rn(acc0, v.x);
+                    acc1 = __fadd_rn(acc1, v.y);
+                    acc2 = __fadd_rn(acc2, v.z);
+                    acc3 = __fadd_rn(acc3, v.w);
+                }
+                const bool h0 = valid && acc0 <= tk[0];
+                const bool h1 = valid && acc1 <= tk[1];
+                const bool h2 = valid && acc2 <= tk[2];
+                const bool h3 = valid && acc3 <= tk[3];
+                if (__any_sync(0xffffffffu, h0 | h1 | h2 | h3)) {
+                    const uint32_t pos = (uint32_t)(off + e);
+                    emit(h0, qk[0], acc0, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                    emit(h1, qk[1], acc1, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                    emit(h2, qk[2], acc2, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                    emit(h3, qk[3], acc3, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                }
+            }
+        } else {
+            // ---------------- sample mode: every stride-th entry, fixed slots
+            const uint32_t ns = (len + a.stride - 1) / a.stride;
+            uint64_t sbase[4];
+            bool sw[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                sw[k] = qk[k] >= 0 && s_samp[qd * 4 + k];
+                sbase[k] = sw[k] ? a.sample_off[s_pair[qd * 4 + k]] : 0;
+            }
+            for (uint32_t base = warp * 8; base < ns; base += NW * 8) {
+                const uint32_t si = base + slot;
+                if (si >= ns) continue;
+                const u64 code = __ldg(codes + (size_t)si * a.stride);
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int j = 0; j < M; ++j) {
+                    const uint32_t c = (uint32_t)(code >> (8 * j)) & 0xffu;
+                    const float4 v = lut4[(j * KS + c) * (QT / 4) + qd];
+                    acc[0] = __fadd_rn(acc[0], v.x);
+                    acc[1] = __fadd_rn(acc[1], v.y);
+                    acc[2] = __fadd_rn(acc[2], v.z);
+                    acc[3] = __fadd_rn(acc[3], v.w);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (sw[k]) a.sample_dist[sbase[k] + si] = acc[k];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Kernel seam helpers (kernels::scan_topk / build_lut parity).
+__global__ void lut_scan_all_kernel(const float* __restrict__ lut, uint32_t m, uint32_t ks,
+                                    const uint8_t* __restrict__ codes, size_t n,
+                                    float* __restrict__ out) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float acc = 0.f;
+    for (uint32_t j = 0; j < m; ++j) acc = __fadd_rn(acc, lut[(size_t)j * ks + codes[i * m + j]]);
+    out[i] = acc;
+}
+
+__global__ void build_lut_kernel(const float* __restrict__ xr, size_t nx, uint32_t d,
+                                 const float* __restrict__ books, uint32_t m, uint32_t ks,
+                                 float* __restrict__ out) {
+    size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nx * m * ks) return;
+    size_t v = idx / ((size_t)m * ks);
+    uint32_t r = (uint32_t)(idx % ((size_t)m * ks));
+    uint32_t j = r / ks, i = r % ks;
+    uint32_t ds = d / m;
+    out[idx] = l2sq_scalar(xr + v * d + (size_t)j * ds, books + ((size_t)j * ks + i) * ds, (int)ds);
+}
+
+__global__ void items_per_list_kernel(const uint32_t* __restrict__ cnt, uint32_t nlists,
+                                      uint32_t* __restrict__ items) {
+    uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l < nlists) items[l] = (cnt[l] + QT - 1) / QT;
+    if (l == nlists) items[l] = 0;
+}
+
+__global__ void items_build_kernel(const uint32_t* __restrict__ cnt,
+                                   const uint32_t* __restrict__ first, uint32_t nlists,
+                                   const uint32_t* __restrict__ item_off,
+                                   uint32_t* __restrict__ item_list, uint32_t* __restrict__ item_start,
+                                   uint32_t* __restrict__ item_nq) {
+    uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= nlists) return;
+    const uint32_t c = cnt[l];
+    uint32_t o = item_off[l];
+    for (uint32_t s = 0; s < c; s += QT, ++o) {
+        item_list[o] = l;
+        item_start[o] = first[l] + s;
+        item_nq[o] = min((uint32_t)QT, c - s);
+    }
+}
+
+template <int DSUB>
+void scan_t(const ScanArgs& a, cudaStream_t s) {
+    const size_t smem = (size_t)LUT_FLOATS * sizeof(float) + (size_t)QT * (a.d + 4) * sizeof(float);
+    PQRR_CUDA(cudaFuncSetAttribute(ivf_scan_kernel<DSUB>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ivf_scan_kernel<DSUB><<<sm_count(), NT, smem, s>>>(a, kNegZero2);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+}  // namespace
+
+void launch_ivf_scan(const ScanArgs& a, cudaStream_t s) {
+    if (a.m != M || a.ks != KS) throw ArgError("device scan supports m = 8, ks = 256");
+    switch (a.d / a.m) {
+        case 16: return scan_t<16>(a, s);
+        case 8: return scan_t<8>(a, s);
+        case 4: return scan_t<4>(a, s);
+        case 32: return scan_t<32>(a, s);
+        default: throw ArgError("device scan supports d/m in {4, 8, 16, 32}");
+    }
+}
+
+void launch_items_per_list(const uint32_t* list_cnt, uint32_t nlists, uint32_t* items,
+                           cudaStream_t s) {
+    items_per_list_kernel<<<(nlists + 1 + 255) / 256, 256, 0, s>>>(list_cnt, nlists, items);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first, uint32_t nlists,
+                        const uint32_t* item_off, uint32_t* item_list, uint32_t* item_start,
+                        uint32_t* item_nq, cudaStream_t s) {
+    items_build_kernel<<<(nlists + 255) / 256, 256, 0, s>>>(list_cnt, list_first, nlists, item_off,
+                                                            item_list, item_start, item_nq);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_lut_scan_all(const float* lut, uint32_t m, uint32_t ks, const uint8_t* codes, size_t n,
+                         float* out_dist, cudaStream_t s) {
+    if (n == 0) return;
+    lut_scan_all_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(lut, m, ks, codes, n, out_dist);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_build_lut(const float* xr, size_t nx, uint32_t d, const float* books, uint32_t m,
+                      uint32_t ks, float* out, cudaStream_t s) {
+    size_t total = nx * m * ks;
+    if (!total) return;
+    build_lut_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(xr, nx, d, books, m, ks, out);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+}  // namespace pqrr_b200

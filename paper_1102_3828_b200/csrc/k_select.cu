@@ -1,0 +1,399 @@
+// k_select.cu — threshold estimation, exact top-k' shortlist selection and the
+// K5 re-ranker (ivf_rerank, ivf_index.hpp:79-81).
+//
+// Selection is exact under the reference total order (types.hpp:47-50): every
+// candidate becomes a 64-bit key (dist bits << 32 | id) — distances are
+// non-negative so the IEEE pattern orders like the value — and a CTA-wide
+// MSB-first radix select finds the k'-th key; ties on distance are therefore
+// broken by id exactly like TopK (topk.hpp:18-29).
+#include <float.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace pqrr_b200 {
+namespace {
+
+constexpr int SEL_THREADS = 512;
+constexpr int RADIX_BITS = 11;
+constexpr int NBINS = 1 << RADIX_BITS;
+
+__global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t nq, uint32_t w,
+                                   const uint32_t* __restrict__ list_len, uint32_t stride,
+                                   uint32_t cap, uint64_t* __restrict__ n_entries,
+                                   uint8_t* __restrict__ sampled, uint64_t* __restrict__ pair_samples,
+                                   unsigned long long* __restrict__ grand_total) {
+    size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    uint64_t tot = 0;
+    for (uint32_t r = 0; r < w; ++r) tot += list_len[probes[q * w + r]];
+    n_entries[q] = tot;
+    atomicAdd(grand_total, (unsigned long long)tot);
+    const bool samp = tot > cap && stride > 1;
+    sampled[q] = samp ? 1 : 0;
+    for (uint32_t r = 0; r < w; ++r) {
+        const uint32_t len = list_len[probes[q * w + r]];
+        pair_samples[q * w + r] = samp ? (len + stride - 1) / stride : 0;
+    }
+}
+
+// Block-wide search of the bin holding the rank-th element (1-based) of a
+// 2048-bin histogram; returns bin and rank within the bin.
+__device__ void find_bin(const uint32_t* hist, uint32_t rank, uint32_t* s_bin, uint32_t* s_rank) {
+    // one warp: lane l owns bins [64 l, 64 l + 64)
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        uint32_t sum = 0;
+        for (int b = 0; b < 64; ++b) sum += hist[lane * 64 + b];
+        uint32_t incl = sum;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const uint32_t excl = incl - sum;
+        const bool mine = excl < rank && rank <= incl;
+        const unsigned who = __ballot_sync(0xffffffffu, mine);
+        if (mine && lane == __ffs(who) - 1) {
+            uint32_t c = excl;
+            for (int b = 0; b < 64; ++b) {
+                const uint32_t h = hist[lane * 64 + b];
+                if (rank <= c + h) {
+                    *s_bin = lane * 64 + b;
+                    *s_rank = rank - c;
+                    break;
+                }
+                c += h;
+            }
+        }
+    }
+}
+
+// tau_q = rank-th smallest sampled distance (an estimate of the distance that
+// admits ~alpha*k' entries); +inf for queries scanned without sampling.
+__global__ __launch_bounds__(SEL_THREADS) void sample_threshold_kernel(
+    const float* __restrict__ sample, const uint64_t* __restrict__ sample_off, uint32_t w,
+    const uint8_t* __restrict__ sampled, uint32_t rank, float* __restrict__ tau) {
+    __shared__ uint32_t hist[NBINS];
+    __shared__ uint32_t s_bin, s_rank;
+    const size_t q = blockIdx.x;
+    if (!sampled[q]) {
+        if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
+        return;
+    }
+    const uint64_t lo = sample_off[q * w], hi = sample_off[q * w + w];
+    if (hi - lo < rank) {
+        if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
+        return;
+    }
+    uint32_t prefix = 0, r = rank;
+    const int shifts[3] = {21, 10, 0};
+    const int widths[3] = {11, 11, 10};
+    for (int pass = 0; pass < 3; ++pass) {
+        for (int b = threadIdx.x; b < NBINS; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        const int sh = shifts[pass], wd = widths[pass];
+        const uint32_t msk = (1u << wd) - 1u;
+        for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+            const uint32_t u = __float_as_uint(sample[i]);
+            const bool match = pass == 0 ? true : ((u >> (sh + wd)) == prefix);
+            if (match) atomicAdd(&hist[(u >> sh) & msk], 1u);
+        }
+        __syncthreads();
+        find_bin(hist, r, &s_bin, &s_rank);
+        __syncthreads();
+        prefix = (prefix << wd) | s_bin;
+        r = s_rank;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) tau[q] = __uint_as_float(prefix);
+}
+
+__device__ void bitonic_sort_kv(u64* keys, uint32_t* vals, uint32_t n2) {
+    for (uint32_t k = 2; k <= n2; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+                const uint32_t lo = 2 * i - (i & (j - 1));
+                const uint32_t hi = lo + j;
+                const bool up = (lo & k) == 0;
+                const u64 a = keys[lo], b = keys[hi];
+                if ((a > b) == up) {
+                    keys[lo] = b;
+                    keys[hi] = a;
+                    if (vals) {
+                        const uint32_t t = vals[lo];
+                        vals[lo] = vals[hi];
+                        vals[hi] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Exact k'-smallest (dist, id) keys among a query's candidates.
+__global__ __launch_bounds__(SEL_THREADS) void select_topk_kernel(
+    const float* __restrict__ cand_dist, const uint32_t* __restrict__ cand_pos,
+    const uint32_t* __restrict__ cand_cnt, uint32_t cap, const uint32_t* __restrict__ ids,
+    uint32_t kprime, int sorted, u64* __restrict__ sl_key, uint32_t* __restrict__ sl_pos,
+    uint32_t* __restrict__ sl_cnt) {
+    extern __shared__ u64 skeys[];
+    __shared__ uint32_t hist[NBINS];
+    __shared__ uint32_t s_bin, s_rank, s_out;
+    const size_t q = blockIdx.x;
+    const uint32_t n = min(cand_cnt[q], cap);
+    const uint32_t cap2 = cap;
+    uint32_t* spos = reinterpret_cast<uint32_t*>(skeys + cap2);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t p = cand_pos[q * cap + i];
+        skeys[i] = nb_key(cand_dist[q * cap + i], ids[p]);
+        spos[i] = p;
+    }
+    if (threadIdx.x == 0) s_out = 0;
+    __syncthreads();
+    u64 kth = ~0ull;
+    if (n > kprime) {
+        u64 prefix = 0;
+        uint32_t r = kprime;
+        int consumed = 0;
+        while (consumed < 64) {
+            const int wd = min(RADIX_BITS, 64 - consumed);
+            const int sh = 64 - consumed - wd;
+            for (int b = threadIdx.x; b < NBINS; b += blockDim.x) hist[b] = 0;
+            __syncthreads();
+            const u64 msk = (1ull << wd) - 1ull;
+            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+                const u64 k = skeys[i];
+                const bool match = consumed == 0 ? true : ((k >> (sh + wd)) == prefix);
+                if (match) atomicAdd(&hist[(uint32_t)((k >> sh) & msk)], 1u);
+            }
+            __syncthreads();
+            find_bin(hist, r, &s_bin, &s_rank);
+            __syncthreads();
+            prefix = (prefix << wd) | s_bin;
+            r = s_rank;
+            consumed += wd;
+            __syncthreads();
+        }
+        kth = prefix;
+    }
+    const uint32_t cnt = min(n, kprime);
+    // compaction of the keys <= kth (exactly cnt of them: keys are unique)
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const u64 k = skeys[i];
+        if (k <= kth) {
+            const uint32_t o = atomicAdd(&s_out, 1u);
+            sl_key[q * kprime + o] = k;
+            sl_pos[q * kprime + o] = spos[i];
+        }
+    }
+    if (threadIdx.x == 0) sl_cnt[q] = cnt;
+    if (!sorted) return;
+    __syncthreads();
+    uint32_t n2 = 1;
+    while (n2 < cnt) n2 <<= 1;
+    for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+        skeys[i] = i < cnt ? sl_key[q * kprime + i] : ~0ull;
+        spos[i] = i < cnt ? sl_pos[q * kprime + i] : 0u;
+    }
+    __syncthreads();
+    bitonic_sort_kv(skeys, spos, n2);
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+        sl_key[q * kprime + i] = skeys[i];
+        sl_pos[q * kprime + i] = spos[i];
+    }
+}
+
+__device__ __forceinline__ uint32_t list_of_pos(const uint64_t* __restrict__ off, uint32_t nlists,
+                                                uint64_t pos) {
+    uint32_t lo = 0, hi = nlists;  // off[lo] <= pos < off[hi]
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(off + mid) <= pos) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// l2_sq(x, yhat) with yhat[t] = (C_l[t] + B(code)[t]) + R(rcode)[t].
+template <bool FAST>
+__device__ __forceinline__ float rerank_dist(const float* __restrict__ xs, uint32_t d,
+                                             const float* __restrict__ crow,
+                                             const float* __restrict__ books, const uint8_t* code,
+                                             uint32_t ds, const float* __restrict__ rbooks,
+                                             const uint8_t* rcode, uint32_t dsr, uint32_t ks,
+                                             u64 nz) {
+    if constexpr (FAST) {
+        u64 s01 = 0, s23 = 0;
+        for (uint32_t t = 0; t < d; t += 4) {
+            const uint32_t jj = t / ds, jr = t / dsr;
+            const float4 c = __ldg(reinterpret_cast<const float4*>(crow + t));
+            const float4 b = __ldg(reinterpret_cast<const float4*>(
+                books + ((size_t)jj * ks + code[jj]) * ds + (t - jj * ds)));
+            const float4 rr = __ldg(reinterpret_cast<const float4*>(
+                rbooks + ((size_t)jr * ks + rcode[jr]) * dsr + (t - jr * dsr)));
+            const float y0 = __fadd_rn(__fadd_rn(c.x, b.x), rr.x);
+            const float y1 = __fadd_rn(__fadd_rn(c.y, b.y), rr.y);
+            const float y2 = __fadd_rn(__fadd_rn(c.z, b.z), rr.z);
+            const float y3 = __fadd_rn(__fadd_rn(c.w, b.w), rr.w);
+            const float4 x = *reinterpret_cast<const float4*>(xs + t);
+            s01 = acc_sq2(s01, pk2(x.x, x.y), pk2(y0, y1), nz);
+            s23 = acc_sq2(s23, pk2(x.z, x.w), pk2(y2, y3), nz);
+        }
+        return __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
+    } else {
+        float s[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t full = d & ~3u;
+        for (uint32_t t = 0; t < d; ++t) {
+            const uint32_t jj = t / ds, jr = t / dsr;
+            const float rec1 = __fadd_rn(crow[t], books[((size_t)jj * ks + code[jj]) * ds + (t - jj * ds)]);
+            const float yh = __fadd_rn(rec1, rbooks[((size_t)jr * ks + rcode[jr]) * dsr + (t - jr * dsr)]);
+            const float df = __fsub_rn(xs[t], yh);
+            const int slot = t < full ? (int)(t & 3) : (int)(t - full);
+            s[slot] = __fadd_rn(s[slot], __fmul_rn(df, df));
+        }
+        return __fadd_rn(__fadd_rn(s[0], s[1]), __fadd_rn(s[2], s[3]));
+    }
+}
+
+template <bool FAST>
+__global__ __launch_bounds__(256) void rerank_kernel(
+    const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
+    const uint32_t* __restrict__ sl_cnt, uint32_t sl_stride, const float* __restrict__ xq, uint32_t d,
+    const uint64_t* __restrict__ list_off, uint32_t nlists, const float* __restrict__ coarse,
+    const uint8_t* __restrict__ codes, const float* __restrict__ books, uint32_t m,
+    const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks, uint32_t mprime,
+    uint32_t ks, uint32_t k, uint32_t* __restrict__ out_ids, float* __restrict__ out_dists,
+    uint32_t* __restrict__ out_cnt, u64 nz) {
+    extern __shared__ u64 rkeys[];
+    float* xs = reinterpret_cast<float*>(rkeys);  // first d floats (rounded up to 16 B)
+    const uint32_t xwords = ((d + 3) & ~3u) / 2;  // u64 words taken by xs
+    u64* keys = rkeys + xwords;
+    const size_t q = blockIdx.x;
+    const uint32_t n = sl_cnt[q];
+    for (uint32_t t = threadIdx.x; t < d; t += blockDim.x) xs[t] = xq[q * d + t];
+    uint32_t n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    __syncthreads();
+    const uint32_t ds = d / m, dsr = d / mprime;
+    for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+        if (i >= n) {
+            keys[i] = ~0ull;
+            continue;
+        }
+        const uint32_t p = sl_pos[q * sl_stride + i];
+        const uint32_t id = key_id(sl_key[q * sl_stride + i]);
+        const uint32_t l = list_of_pos(list_off, nlists, p);
+        const float dist = rerank_dist<FAST>(xs, d, coarse + (size_t)l * d, books, codes + (size_t)p * m, ds,
+                                             rbooks, rcodes + (size_t)p * mprime, dsr, ks, nz);
+        keys[i] = nb_key(dist, id);
+    }
+    __syncthreads();
+    bitonic_sort_kv(keys, nullptr, n2);
+    const uint32_t cnt = min(n, k);
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+        out_ids[q * k + i] = key_id(keys[i]);
+        out_dists[q * k + i] = key_dist(keys[i]);
+    }
+    if (threadIdx.x == 0) out_cnt[q] = cnt;
+}
+
+__global__ void unpack_keys_kernel(const u64* __restrict__ keys, const uint32_t* __restrict__ cnt,
+                                   size_t nq, uint32_t stride, uint32_t* __restrict__ ids,
+                                   float* __restrict__ dists) {
+    size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nq * stride) return;
+    size_t q = idx / stride;
+    uint32_t i = (uint32_t)(idx % stride);
+    if (i < cnt[q]) {
+        ids[idx] = key_id(keys[idx]);
+        dists[idx] = key_dist(keys[idx]);
+    }
+}
+
+void set_smem(const void* f, size_t bytes) {
+    PQRR_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+}  // namespace
+
+void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
+                        uint32_t stride, uint32_t cap, uint64_t* nq_entries,
+                        uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
+                        cudaStream_t s) {
+    if (nq == 0) return;
+    query_sizes_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, s>>>(
+        probes, nq, w, list_len, stride, cap, nq_entries, query_sampled, pair_samples,
+        reinterpret_cast<unsigned long long*>(grand_total));
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_off, uint32_t w,
+                             size_t nq, const uint8_t* query_sampled, uint32_t rank, float* tau,
+                             cudaStream_t s) {
+    if (nq == 0) return;
+    sample_threshold_kernel<<<(unsigned)nq, SEL_THREADS, 0, s>>>(sample_dist, sample_off, w,
+                                                                  query_sampled, rank, tau);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
+                        uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime, bool sorted,
+                        uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s) {
+    if (nq == 0) return;
+    uint32_t kp2 = 1;
+    while (kp2 < kprime) kp2 <<= 1;
+    const uint32_t slots = std::max(cap, sorted ? kp2 : 0u);
+    const size_t smem = (size_t)slots * (sizeof(u64) + sizeof(uint32_t));
+    if (smem > 200 * 1024) throw ArgError("candidate capacity too large for the device selector");
+    set_smem((const void*)select_topk_kernel, smem);
+    select_topk_kernel<<<(unsigned)nq, SEL_THREADS, smem, s>>>(
+        cand_dist, cand_pos, cand_cnt, cap, ids, kprime, sorted ? 1 : 0,
+        reinterpret_cast<u64*>(sl_key), sl_pos, sl_cnt);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_t* sl_cnt,
+                   uint32_t sl_stride, size_t nq, const float* xq, uint32_t d,
+                   const uint64_t* list_off, uint32_t nlists, const float* coarse,
+                   const uint8_t* codes, const float* books, uint32_t m, const uint8_t* rcodes,
+                   const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
+                   uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s) {
+    if (nq == 0) return;
+    uint32_t n2 = 1;
+    while (n2 < sl_stride) n2 <<= 1;
+    const size_t smem = ((d + 3) & ~3u) * sizeof(float) + (size_t)n2 * sizeof(u64);
+    if (smem > 200 * 1024) throw ArgError("shortlist too large for the device re-ranker");
+    const bool fast = d % 4 == 0 && (d / m) % 4 == 0 && (d / mprime) % 4 == 0;
+    if (fast) {
+        set_smem((const void*)rerank_kernel<true>, smem);
+        rerank_kernel<true><<<(unsigned)nq, 256, smem, s>>>(
+            reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, d, list_off,
+            nlists, coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists,
+            out_cnt, kNegZero2);
+    } else {
+        set_smem((const void*)rerank_kernel<false>, smem);
+        rerank_kernel<false><<<(unsigned)nq, 256, smem, s>>>(
+            reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, d, list_off,
+            nlists, coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists,
+            out_cnt, kNegZero2);
+    }
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_unpack_keys(const uint64_t* keys, const uint32_t* cnt, size_t nq, uint32_t stride,
+                        uint32_t* ids, float* dists, cudaStream_t s) {
+    size_t total = nq * stride;
+    if (!total) return;
+    unpack_keys_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<const u64*>(keys), cnt, nq, stride, ids, dists);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+}  // namespace pqrr_b200

@@ -1,0 +1,1180 @@
+// pqrr_dev.cu — host orchestration behind the C ABI of include/pqrr_dev.h:
+// the device-resident IVF index (ivf_index.hpp:27-41 + refine.hpp:15-28),
+// its add path (ivf_build / ivf_refine_encode), and the fused batched search
+// (ivf_search_batch + ivf_rerank).  One CUDA stream per index; calls on one
+// index are serialised by a mutex (SPEC.md:346 allows concurrent searches —
+// they queue on the device in order).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cub/device/device_radix_sort.cuh>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pqrr_dev.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace pqrr_b200 {
+
+thread_local std::string g_last_error;
+
+struct ShortlistError : std::runtime_error {
+    ShortlistError() : std::runtime_error("shortlist too small") {}
+};
+struct UnsupportedError : std::runtime_error {
+    explicit UnsupportedError(const std::string& s) : std::runtime_error(s) {}
+};
+struct NoDevice : std::runtime_error {
+    explicit NoDevice(const std::string& s) : std::runtime_error(s) {}
+};
+
+// ------------------------------------------------------------------ helpers
+class DeviceGuard {
+  public:
+    explicit DeviceGuard(int dev) {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            throw NoDevice("no CUDA device available (the B200 path has no CPU fallback)");
+        }
+        if (dev < 0 || dev >= n) throw ArgError("device ordinal out of range");
+        PQRR_CUDA(cudaGetDevice(&prev_));
+        PQRR_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() { cudaSetDevice(prev_); }
+
+  private:
+    int prev_ = 0;
+};
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count) PQRR_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void swap(DBuf& o) {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// Stream-ordered scratch: everything is freed (stream-ordered) at scope exit.
+class Workspace {
+  public:
+    explicit Workspace(cudaStream_t s) : s_(s) {}
+    ~Workspace() {
+        for (void* p : ptrs_) cudaFreeAsync(p, s_);
+    }
+    template <class T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        PQRR_CUDA(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), s_));
+        ptrs_.push_back(p);
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    T* zeros(size_t count) {
+        T* p = alloc<T>(count);
+        PQRR_CUDA(cudaMemsetAsync(p, 0, std::max<size_t>(count, 1) * sizeof(T), s_));
+        return p;
+    }
+
+  private:
+    cudaStream_t s_;
+    std::vector<void*> ptrs_;
+};
+
+int bits_for(uint32_t n) {
+    int b = 1;
+    while ((1ull << b) < n) ++b;
+    return b;
+}
+
+// ------------------------------------------------------------------ small kernels
+namespace {
+
+__global__ void iota_base_kernel(uint32_t* out, size_t n, uint32_t base) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = base + (uint32_t)i;
+}
+
+__global__ void check_fail_kernel(const uint8_t* __restrict__ sampled, const uint32_t* __restrict__ cnt,
+                                  size_t nq, uint32_t kprime, uint32_t cap, uint8_t* __restrict__ fail) {
+    size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    uint8_t f = 0;
+    if (sampled[q]) {
+        if (cnt[q] < kprime) f = 1;   // threshold too tight: shortlist may be incomplete
+        else if (cnt[q] > cap) f = 2; // buffer overflow: candidates were dropped
+    }
+    fail[q] = f;
+}
+
+__global__ void gather_rows_f32(const float* __restrict__ x, uint32_t d, const uint32_t* __restrict__ rows,
+                                size_t nr, float* __restrict__ out) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nr * d) return;
+    out[i] = x[(size_t)rows[i / d] * d + i % d];
+}
+
+__global__ void scatter_shortlist(const u64* __restrict__ skey, const uint32_t* __restrict__ spos,
+                                  const uint32_t* __restrict__ scnt, const uint32_t* __restrict__ rows,
+                                  size_t nr, uint32_t kprime, u64* __restrict__ key,
+                                  uint32_t* __restrict__ pos, uint32_t* __restrict__ cnt) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nr * kprime) return;
+    size_t r = i / kprime, j = i % kprime;
+    size_t q = rows[r];
+    key[q * kprime + j] = skey[i];
+    pos[q * kprime + j] = spos[i];
+    if (j == 0) cnt[q] = scnt[r];
+}
+
+__global__ void min_count_kernel(const uint32_t* __restrict__ cnt, size_t nq, uint32_t k,
+                                 unsigned* __restrict__ flag) {
+    size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < nq && cnt[q] < k) atomicOr(flag, 1u);
+}
+
+__global__ void id_to_pos_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
+                                 const uint32_t* __restrict__ ids, uint32_t* __restrict__ map) {
+    const uint32_t l = blockIdx.x;
+    const uint64_t o = off[l];
+    for (uint32_t r = threadIdx.x; r < len[l]; r += blockDim.x) map[ids[o + r]] = (uint32_t)(o + r);
+}
+
+__global__ void ids_to_shortlist(const uint32_t* __restrict__ sl_ids, const uint32_t* __restrict__ map,
+                                 size_t total, u64* __restrict__ key, uint32_t* __restrict__ pos,
+                                 unsigned* __restrict__ bad, uint32_t nmap) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const uint32_t id = sl_ids[i];
+    uint32_t p = 0xffffffffu;
+    if (id < nmap) p = map[id];
+    if (p == 0xffffffffu) {
+        atomicOr(bad, 1u);
+        p = 0;
+    }
+    key[i] = (u64)id;
+    pos[i] = p;
+}
+
+__global__ void reconstruct_kernel(const uint32_t* __restrict__ ids, size_t n, const uint32_t* __restrict__ map,
+                                   const uint64_t* __restrict__ off, uint32_t nlists, uint32_t d,
+                                   const float* __restrict__ coarse, const uint8_t* __restrict__ codes,
+                                   const float* __restrict__ books, uint32_t m,
+                                   const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks,
+                                   uint32_t mprime, uint32_t ks, float* __restrict__ out) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * d) return;
+    const size_t v = i / d;
+    const uint32_t t = (uint32_t)(i % d);
+    const uint32_t p = map[ids[v]];
+    if (p == 0xffffffffu) {
+        out[i] = __int_as_float(0x7fc00000);  // id never added
+        return;
+    }
+    uint32_t lo = 0, hi = nlists;
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (off[mid] <= p) lo = mid;
+        else hi = mid;
+    }
+    const uint32_t ds = d / m, jj = t / ds;
+    float y = __fadd_rn(coarse[(size_t)lo * d + t],
+                        books[((size_t)jj * ks + codes[(size_t)p * m + jj]) * ds + (t - jj * ds)]);
+    if (mprime) {
+        const uint32_t dsr = d / mprime, jr = t / dsr;
+        y = __fadd_rn(y, rbooks[((size_t)jr * ks + rcodes[(size_t)p * mprime + jr]) * dsr + (t - jr * dsr)]);
+    }
+    out[i] = y;
+}
+
+__global__ void compact_lists_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
+                                     const uint64_t* __restrict__ uoff, const uint32_t* __restrict__ ids,
+                                     const uint8_t* __restrict__ codes, const uint8_t* __restrict__ rcodes,
+                                     uint32_t m, uint32_t mprime, uint32_t* __restrict__ o_ids,
+                                     uint8_t* __restrict__ o_codes, uint8_t* __restrict__ o_rcodes) {
+    const uint32_t l = blockIdx.x;
+    const uint64_t o = off[l], u = uoff[l];
+    for (uint32_t r = threadIdx.x; r < len[l]; r += blockDim.x) {
+        o_ids[u + r] = ids[o + r];
+        for (uint32_t j = 0; j < m; ++j) o_codes[(u + r) * m + j] = codes[(o + r) * m + j];
+        for (uint32_t j = 0; j < mprime; ++j) o_rcodes[(u + r) * mprime + j] = rcodes[(o + r) * mprime + j];
+    }
+}
+
+__global__ void lut_keys_kernel(const float* __restrict__ dist, size_t n, uint32_t id_base,
+                                u64* __restrict__ keys) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) keys[i] = nb_key(dist[i], id_base + (uint32_t)i);
+}
+
+inline unsigned nblk(size_t n, unsigned t = 256) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+// ------------------------------------------------------------------ index
+struct DevIndex {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    uint32_t d = 0, c = 0, m = 0, mprime = 0, ks = 0;
+    DBuf<float> coarse, books, rbooks;
+    // list-major layout
+    uint64_t n = 0, slots = 0;
+    DBuf<uint64_t> list_off;
+    DBuf<uint32_t> list_len;
+    std::vector<uint64_t> h_off;
+    std::vector<uint32_t> h_len;
+    DBuf<uint8_t> codes, rcodes;
+    DBuf<uint32_t> ids;
+    uint64_t next_id = 0;
+    // id -> position (lazy)
+    DBuf<uint32_t> id_map;
+    bool id_map_valid = false;
+    // staging (id order)
+    uint64_t st_n = 0, st_cap = 0;
+    DBuf<uint32_t> st_assign, st_ids;
+    DBuf<uint8_t> st_codes, st_rcodes;
+    pqrr_dev_search_stats stats{};
+    cudaEvent_t ev[10] = {};
+
+    ~DevIndex() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (stream) cudaStreamDestroy(stream);
+    }
+    uint32_t max_len() const {
+        uint32_t mx = 0;
+        for (uint32_t v : h_len) mx = std::max(mx, v);
+        return mx;
+    }
+};
+
+namespace {
+
+void check_shape(uint32_t d, uint32_t m, uint32_t ks) {
+    if (d == 0) throw ArgError("d must be positive");
+    if (m == 0 || d % m != 0) throw ArgError("dimension not divisible");
+    if (ks == 0 || ks > 256) throw ArgError("ks must be in [1, 256]");
+}
+
+void grow_staging(DevIndex& ix, uint64_t need) {
+    if (need <= ix.st_cap) return;
+    uint64_t cap = std::max<uint64_t>(need, ix.st_cap * 2);
+    DBuf<uint32_t> a, i;
+    DBuf<uint8_t> c, r;
+    a.alloc(cap);
+    i.alloc(cap);
+    c.alloc(cap * ix.m);
+    if (ix.mprime) r.alloc(cap * ix.mprime);
+    if (ix.st_n) {
+        PQRR_CUDA(cudaMemcpyAsync(a.p, ix.st_assign.p, ix.st_n * 4, cudaMemcpyDeviceToDevice, ix.stream));
+        PQRR_CUDA(cudaMemcpyAsync(i.p, ix.st_ids.p, ix.st_n * 4, cudaMemcpyDeviceToDevice, ix.stream));
+        PQRR_CUDA(cudaMemcpyAsync(c.p, ix.st_codes.p, ix.st_n * ix.m, cudaMemcpyDeviceToDevice, ix.stream));
+        if (ix.mprime)
+            PQRR_CUDA(cudaMemcpyAsync(r.p, ix.st_rcodes.p, ix.st_n * ix.mprime, cudaMemcpyDeviceToDevice,
+                                      ix.stream));
+        PQRR_CUDA(cudaStreamSynchronize(ix.stream));
+    }
+    ix.st_assign.swap(a);
+    ix.st_ids.swap(i);
+    ix.st_codes.swap(c);
+    ix.st_rcodes.swap(r);
+    ix.st_cap = cap;
+}
+
+// Encode a device-resident chunk (f32 or u8) into the staging arrays.
+void stage_chunk(DevIndex& ix, const float* xf, const uint8_t* xu, size_t n, uint32_t id_base) {
+    if (n == 0) return;
+    if ((uint64_t)id_base < ix.next_id)
+        throw ArgError("ids must be added in ascending order (id_base below the next free id)");
+    if ((uint64_t)id_base + n > 0xffffffffull) throw ArgError("ids exceed the 32-bit id space");
+    cudaStream_t s = ix.stream;
+    grow_staging(ix, ix.st_n + n);
+    Workspace ws(s);
+    const float* x = xf;
+    if (!x) {
+        float* tmp = ws.alloc<float>(n * ix.d);
+        launch_widen_u8(xu, tmp, n * ix.d, s);
+        x = tmp;
+    }
+    uint32_t* a = ix.st_assign.p + ix.st_n;
+    launch_argmin(x, n, ix.coarse.p, ix.c, ix.d, a, nullptr, s);
+    launch_ivf_encode(x, nullptr, n, ix.d, a, ix.coarse.p, ix.books.p, ix.m, ix.rbooks.p, ix.mprime,
+                      ix.ks, ix.st_codes.p + ix.st_n * ix.m,
+                      ix.mprime ? ix.st_rcodes.p + ix.st_n * ix.mprime : nullptr, s);
+    iota_base_kernel<<<nblk(n), 256, 0, s>>>(ix.st_ids.p + ix.st_n, n, id_base);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+    ix.st_n += n;
+    ix.next_id = (uint64_t)id_base + n;
+}
+
+void finalize(DevIndex& ix) {
+    if (ix.st_n == 0) return;
+    cudaStream_t s = ix.stream;
+    const uint32_t c = ix.c;
+    const size_t n = ix.st_n;
+    Workspace ws(s);
+    uint32_t* cnt = ws.alloc<uint32_t>(c + 1);
+    PQRR_CUDA(cudaMemsetAsync(cnt, 0, (c + 1) * sizeof(uint32_t), s));
+    launch_histogram(ix.st_assign.p, n, c, cnt, s);
+    uint32_t* stage_off = ws.alloc<uint32_t>(c + 1);
+    exclusive_scan_u32(cnt, stage_off, c + 1, s);
+    uint32_t* iota = ws.alloc<uint32_t>(n);
+    launch_iota(iota, n, s);
+    uint32_t* skeys = ws.alloc<uint32_t>(n);
+    uint32_t* sidx = ws.alloc<uint32_t>(n);
+    sort_pairs(ix.st_assign.p, skeys, iota, sidx, n, bits_for(c), s);
+    std::vector<uint32_t> h_cnt(c);
+    PQRR_CUDA(cudaMemcpyAsync(h_cnt.data(), cnt, c * 4, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint32_t> old_len = ix.h_len;
+    if (old_len.empty()) old_len.assign(c, 0);
+    std::vector<uint32_t> new_len(c);
+    std::vector<uint64_t> new_off(c + 1);
+    uint64_t acc = 0;
+    for (uint32_t l = 0; l < c; ++l) {
+        new_len[l] = old_len[l] + h_cnt[l];
+        new_off[l] = acc;
+        acc += (uint64_t(new_len[l]) + 15) & ~uint64_t(15);
+    }
+    new_off[c] = acc;
+    if (acc > 0xffffffffull) throw UnsupportedError("more than 2^32 entries on one device");
+    DBuf<uint64_t> d_off;
+    DBuf<uint32_t> d_len, d_oldlen;
+    d_off.alloc(c + 1);
+    d_len.alloc(c);
+    d_oldlen.alloc(c);
+    PQRR_CUDA(cudaMemcpyAsync(d_off.p, new_off.data(), (c + 1) * 8, cudaMemcpyHostToDevice, s));
+    PQRR_CUDA(cudaMemcpyAsync(d_len.p, new_len.data(), c * 4, cudaMemcpyHostToDevice, s));
+    PQRR_CUDA(cudaMemcpyAsync(d_oldlen.p, old_len.data(), c * 4, cudaMemcpyHostToDevice, s));
+    DBuf<uint8_t> codes, rcodes;
+    DBuf<uint32_t> ids;
+    codes.alloc(acc * ix.m + 16);
+    ids.alloc(acc + 1);
+    if (ix.mprime) rcodes.alloc(acc * ix.mprime + 16);
+    if (ix.n) {
+        uint32_t mx = 0;
+        for (uint32_t v : ix.h_len) mx = std::max(mx, v);
+        launch_layout_copy_old(ix.list_off.p, ix.list_len.p, c, d_off.p, ix.codes.p, ix.ids.p,
+                               ix.rcodes.p, ix.m, ix.mprime, codes.p, ids.p, rcodes.p, mx, s);
+    }
+    launch_layout_place_new(skeys, sidx, n, stage_off, d_off.p, d_oldlen.p, ix.st_codes.p,
+                            ix.st_rcodes.p, ix.st_ids.p, ix.m, ix.mprime, codes.p, ids.p, rcodes.p, s);
+    PQRR_CUDA(cudaStreamSynchronize(s));
+    ix.codes.swap(codes);
+    ix.rcodes.swap(rcodes);
+    ix.ids.swap(ids);
+    ix.list_off.swap(d_off);
+    ix.list_len.swap(d_len);
+    ix.h_off = new_off;
+    ix.h_len = new_len;
+    ix.n += n;
+    ix.slots = acc;
+    ix.st_n = 0;
+    ix.id_map_valid = false;
+}
+
+void ensure_id_map(DevIndex& ix) {
+    finalize(ix);
+    if (ix.id_map_valid) return;
+    ix.id_map.alloc(std::max<uint64_t>(ix.next_id, 1));
+    PQRR_CUDA(cudaMemsetAsync(ix.id_map.p, 0xff, ix.id_map.bytes(), ix.stream));
+    if (ix.c)
+        id_to_pos_kernel<<<ix.c, 256, 0, ix.stream>>>(ix.list_off.p, ix.list_len.p, ix.ids.p,
+                                                      ix.id_map.p);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+    ix.id_map_valid = true;
+}
+
+struct ShortlistDev {
+    u64* key;
+    uint32_t* pos;
+    uint32_t* cnt;
+};
+
+// Builds the exact top-kprime shortlist of every query into `out` (device,
+// [nq][kprime]).  alpha scales the sampled threshold rank (expected
+// candidates ~ alpha * kprime).
+void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32_t kprime,
+                    bool sorted, double alpha, uint32_t stride_div, ShortlistDev out, int depth,
+                    bool timed) {
+    cudaStream_t s = ix.stream;
+    auto& st = ix.stats;
+    const uint32_t c = ix.c;
+    const size_t P = nq * (size_t)w;
+    uint32_t kp2 = 1;
+    while (kp2 < 4 * kprime) kp2 <<= 1;
+    const uint32_t cap = std::max<uint32_t>(8192, std::min<uint32_t>(kp2, 16384));
+    uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / 64.0));
+    stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
+    const uint32_t rank = (uint32_t)std::ceil(alpha * kprime / stride);
+    Workspace ws(s);
+
+    // ---- K1: coarse distances + top-w probes
+    float* D = ws.alloc<float>(nq * (size_t)c);
+    launch_pair_dists(xq, nq, ix.coarse.p, c, ix.d, D, s);
+    uint32_t* probes = ws.alloc<uint32_t>(P);
+    launch_topw(D, nq, c, w, probes, nullptr, s);
+    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[1], s));
+
+    // ---- invert probes into list-major work items
+    uint32_t* iota = ws.alloc<uint32_t>(P);
+    launch_iota(iota, P, s);
+    uint32_t* sorted_lists = ws.alloc<uint32_t>(P);
+    uint32_t* pair_sorted = ws.alloc<uint32_t>(P);
+    sort_pairs(probes, sorted_lists, iota, pair_sorted, P, bits_for(c), s);
+    uint32_t* list_cnt = ws.zeros<uint32_t>(c + 1);
+    launch_histogram(probes, P, c, list_cnt, s);
+    uint32_t* list_first = ws.alloc<uint32_t>(c + 1);
+    exclusive_scan_u32(list_cnt, list_first, c + 1, s);
+    uint32_t* items = ws.alloc<uint32_t>(c + 1);
+    launch_items_per_list(list_cnt, c, items, s);
+    uint32_t* item_off = ws.alloc<uint32_t>(c + 1);
+    exclusive_scan_u32(items, item_off, c + 1, s);
+    uint32_t* item_list = ws.alloc<uint32_t>(P);
+    uint32_t* item_start = ws.alloc<uint32_t>(P);
+    uint32_t* item_nq = ws.alloc<uint32_t>(P);
+    launch_items_build(list_cnt, list_first, c, item_off, item_list, item_start, item_nq, s);
+    uint64_t* n_entries = ws.alloc<uint64_t>(nq);
+    uint8_t* sampled = ws.alloc<uint8_t>(nq);
+    uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
+    uint64_t* grand = ws.zeros<uint64_t>(1);
+    launch_query_sizes(probes, nq, w, ix.list_len.p, stride, cap, n_entries, sampled, pair_samples,
+                       grand, s);
+    uint64_t* sample_off = ws.alloc<uint64_t>(P + 1);
+    exclusive_scan_u64(pair_samples, sample_off, P + 1, s);
+    uint64_t total_samples = 0, scanned = 0;
+    uint32_t n_items = 0;
+    PQRR_CUDA(cudaMemcpyAsync(&scanned, grand, 8, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaMemcpyAsync(&total_samples, sample_off + P, 8, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaMemcpyAsync(&n_items, item_off + c, 4, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaStreamSynchronize(s));
+    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[2], s));
+
+    ScanArgs a{};
+    a.codes = ix.codes.p;
+    a.list_off = ix.list_off.p;
+    a.list_len = ix.list_len.p;
+    a.coarse = ix.coarse.p;
+    a.books = ix.books.p;
+    a.xq = xq;
+    a.d = ix.d;
+    a.m = ix.m;
+    a.ks = ix.ks;
+    a.item_list = item_list;
+    a.item_start = item_start;
+    a.item_nq = item_nq;
+    a.num_items = item_off + c;
+    a.pair_sorted = pair_sorted;
+    a.w = w;
+    a.cap = cap;
+    a.query_sampled = sampled;
+    uint32_t* counter = ws.zeros<uint32_t>(2);
+
+    // ---- sample pass (threshold estimation)
+    float* tau = ws.alloc<float>(nq);
+    float* sample_dist = ws.alloc<float>(total_samples);
+    if (total_samples) {
+        a.stride = stride;
+        a.sample_off = sample_off;
+        a.sample_dist = sample_dist;
+        a.tau = tau;  // unused in sample mode
+        a.item_counter = counter;
+        launch_ivf_scan(a, s);
+    }
+    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[3], s));
+    launch_sample_threshold(sample_dist, sample_off, w, nq, sampled, rank, tau, s);
+    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[4], s));
+
+    // ---- K4 main scan
+    float* cand_dist = ws.alloc<float>(nq * (size_t)cap);
+    uint32_t* cand_pos = ws.alloc<uint32_t>(nq * (size_t)cap);
+    uint32_t* cand_cnt = ws.zeros<uint32_t>(nq);
+    a.stride = 1;
+    a.tau = tau;
+    a.cand_dist = cand_dist;
+    a.cand_pos = cand_pos;
+    a.cand_cnt = cand_cnt;
+    a.item_counter = counter + 1;
+    launch_ivf_scan(a, s);
+    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[5], s));
+
+    // ---- exactness check of the threshold
+    uint8_t* fail = ws.alloc<uint8_t>(nq);
+    check_fail_kernel<<<nblk(nq), 256, 0, s>>>(sampled, cand_cnt, nq, kprime, cap, fail);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+    std::vector<uint8_t> h_fail(nq);
+    PQRR_CUDA(cudaMemcpyAsync(h_fail.data(), fail, nq, cudaMemcpyDeviceToHost, s));
+
+    // ---- exact top-k' selection
+    launch_select_topk(cand_dist, cand_pos, cand_cnt, cap, nq, ix.ids.p, kprime, sorted,
+                       reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s);
+    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[6], s));
+    PQRR_CUDA(cudaStreamSynchronize(s));
+    if (timed) {
+        st.work_items += n_items;
+        st.sampled_entries += total_samples;
+        st.scanned_entries += scanned;
+        st.stride = stride;
+    }
+
+    // ---- retry queries whose threshold failed (rare): under-full -> raise
+    // alpha; overflow -> lower alpha and sample more densely.
+    for (int kind = 1; kind <= 2; ++kind) {
+        std::vector<uint32_t> rows;
+        for (size_t q = 0; q < nq; ++q)
+            if (h_fail[q] == kind) rows.push_back((uint32_t)q);
+        if (rows.empty()) continue;
+        if (depth >= 8) throw std::runtime_error("shortlist threshold did not converge");
+        st.retries += (uint32_t)rows.size();
+        Workspace ws2(s);
+        uint32_t* d_rows = ws2.alloc<uint32_t>(rows.size());
+        PQRR_CUDA(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, s));
+        float* sx = ws2.alloc<float>(rows.size() * ix.d);
+        gather_rows_f32<<<nblk(rows.size() * ix.d), 256, 0, s>>>(xq, ix.d, d_rows, rows.size(), sx);
+        PQRR_LAUNCH_CHECK();
+        ShortlistDev sub{ws2.alloc<u64>(rows.size() * kprime), ws2.alloc<uint32_t>(rows.size() * kprime),
+                         ws2.alloc<uint32_t>(rows.size())};
+        const double a2 = kind == 1 ? alpha * 4.0 : alpha / 4.0;
+        shortlist_core(ix, sx, rows.size(), w, kprime, sorted, a2, kind == 2 ? stride_div * 4 : stride_div,
+                       sub, depth + 1, false);
+        scatter_shortlist<<<nblk(rows.size() * kprime), 256, 0, s>>>(
+            sub.key, sub.pos, sub.cnt, d_rows, rows.size(), kprime, out.key, out.pos, out.cnt);
+        PQRR_LAUNCH_CHECK();
+        count_launch(2);
+        PQRR_CUDA(cudaStreamSynchronize(s));
+    }
+}
+
+void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t kprime_sz,
+                   size_t k_sz, uint32_t* out_ids, float* out_dists, uint32_t* out_cnt) {
+    if (w < 1 || w > ix.c) throw ArgError("v must satisfy 1 <= v <= c");
+    if (kprime_sz < 1) throw ArgError("kprime must be positive");
+    if (kprime_sz > 4096) throw UnsupportedError("kprime above 4096 is not supported yet on the device");
+    if (k_sz > kprime_sz) throw ShortlistError();
+    if (k_sz > 0 && ix.mprime == 0) throw ArgError("re-ranking needs refinement codes (mprime > 0)");
+    finalize(ix);
+    const uint32_t kprime = (uint32_t)kprime_sz, k = (uint32_t)k_sz;
+    cudaStream_t s = ix.stream;
+    const unsigned long long l0 = launch_count();
+    ix.stats = pqrr_dev_search_stats{};
+    ix.stats.nq = nq;
+    if (nq == 0) return;
+    for (auto& e : ix.ev)
+        if (!e) PQRR_CUDA(cudaEventCreate(&e));
+    PQRR_CUDA(cudaEventRecord(ix.ev[0], s));
+    Workspace ws(s);
+    ShortlistDev sl{ws.alloc<u64>(nq * (size_t)kprime), ws.alloc<uint32_t>(nq * (size_t)kprime),
+                    ws.alloc<uint32_t>(nq)};
+    shortlist_core(ix, xq, nq, w, kprime, k == 0, 2.0, 1, sl, 0, true);
+    if (k > 0) {
+        unsigned* flag = ws.zeros<unsigned>(1);
+        min_count_kernel<<<nblk(nq), 256, 0, s>>>(sl.cnt, nq, k, flag);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        unsigned h_flag = 0;
+        PQRR_CUDA(cudaMemcpyAsync(&h_flag, flag, 4, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaStreamSynchronize(s));
+        if (h_flag) throw ShortlistError();
+        PQRR_CUDA(cudaEventRecord(ix.ev[7], s));
+        launch_rerank(reinterpret_cast<uint64_t*>(sl.key), sl.pos, sl.cnt, kprime, nq, xq, ix.d,
+                      ix.list_off.p, ix.c, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
+                      ix.rbooks.p, ix.mprime, ix.ks, k, out_ids, out_dists, out_cnt, s);
+    } else {
+        PQRR_CUDA(cudaEventRecord(ix.ev[7], s));
+        launch_unpack_keys(reinterpret_cast<uint64_t*>(sl.key), sl.cnt, nq, kprime, out_ids, out_dists, s);
+        PQRR_CUDA(cudaMemcpyAsync(out_cnt, sl.cnt, nq * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    PQRR_CUDA(cudaEventRecord(ix.ev[8], s));
+    PQRR_CUDA(cudaEventSynchronize(ix.ev[8]));
+    auto el = [&](int a, int b) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ix.ev[a], ix.ev[b]);
+        return ms;
+    };
+    auto& st = ix.stats;
+    st.ms_coarse = el(0, 1);
+    st.ms_invert = el(1, 2);
+    st.ms_sample_scan = el(2, 3);
+    st.ms_threshold = el(3, 4);
+    st.ms_scan = el(4, 5);
+    st.ms_select = el(5, 6);
+    st.ms_rerank = el(7, 8);
+    st.ms_total = el(0, 8);
+    st.kernels = (uint32_t)(launch_count() - l0);
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return PQRR_OK;
+    } catch (const ShortlistError& e) {
+        g_last_error = e.what();
+        return PQRR_ESHORTLIST;
+    } catch (const NoDevice& e) {
+        g_last_error = e.what();
+        return PQRR_ENODEV;
+    } catch (const UnsupportedError& e) {
+        g_last_error = e.what();
+        return PQRR_EUNSUPPORTED;
+    } catch (const ArgError& e) {
+        g_last_error = e.what();
+        return PQRR_EINVAL;
+    } catch (const CudaError& e) {
+        g_last_error = e.what();
+        return PQRR_ECUDA;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return PQRR_EINTERNAL;
+    }
+}
+
+// Temporary stream + guard for the stateless kernel-seam entry points.
+struct Session {
+    DeviceGuard g;
+    cudaStream_t s = nullptr;
+    explicit Session(int dev) : g(dev) { PQRR_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    ~Session() {
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
+    template <class T>
+    T* upload(Workspace& ws, const T* h, size_t n) {
+        T* d = ws.alloc<T>(n);
+        if (n) PQRR_CUDA(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+        return d;
+    }
+    template <class T>
+    void download(T* h, const T* d, size_t n) {
+        if (n) PQRR_CUDA(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+    void sync() { PQRR_CUDA(cudaStreamSynchronize(s)); }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ training (train.cu)
+void kmeans_device(const float* d_points, size_t n, uint32_t dim, uint32_t k, uint32_t iterations,
+                   uint64_t seed, uint32_t redo, float* h_centroids, double* out_mse,
+                   double* out_trace, cudaStream_t s);
+
+}  // namespace pqrr_b200
+
+// ====================================================================== C ABI
+using namespace pqrr_b200;
+
+struct pqrr_dev_index {
+    DevIndex ix;
+};
+
+extern "C" {
+
+const char* pqrr_dev_last_error(void) { return g_last_error.c_str(); }
+
+int pqrr_dev_device_count(int* out) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    if (out) *out = n;
+    return PQRR_OK;
+}
+
+uint64_t pqrr_dev_launch_count(void) { return launch_count(); }
+
+int pqrr_dev_assign_batch(int device, const float* points, size_t n, uint32_t dim,
+                          const float* centroids, uint32_t k, uint32_t* out_assign, float* out_dist) {
+    return guarded([&] {
+        if (k == 0) throw ArgError("k must be positive");
+        if (n == 0) return;
+        Session se(device);
+        Workspace ws(se.s);
+        const float* p = se.upload(ws, points, n * dim);
+        const float* c = se.upload(ws, centroids, (size_t)k * dim);
+        uint32_t* a = ws.alloc<uint32_t>(n);
+        float* dd = ws.alloc<float>(n);
+        launch_argmin(p, n, c, k, dim, a, dd, se.s);
+        se.download(out_assign, a, n);
+        if (out_dist) se.download(out_dist, dd, n);
+        se.sync();
+    });
+}
+
+int pqrr_dev_encode_batch(int device, const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                          const float* data, size_t n, uint8_t* out_codes) {
+    return guarded([&] {
+        check_shape(d, m, ks);
+        if (n == 0) return;
+        Session se(device);
+        Workspace ws(se.s);
+        const float* b = se.upload(ws, books, (size_t)ks * d);
+        const float* x = se.upload(ws, data, n * d);
+        uint8_t* c = ws.alloc<uint8_t>(n * m);
+        launch_pq_encode(x, n, d, b, m, ks, c, se.s);
+        se.download(out_codes, c, n * m);
+        se.sync();
+    });
+}
+
+int pqrr_dev_decode_batch(int device, const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                          const uint8_t* codes, size_t n, float* out_data) {
+    return guarded([&] {
+        check_shape(d, m, ks);
+        for (size_t i = 0; i < n * m; ++i)
+            if (codes[i] >= ks) throw ArgError("code index out of range");
+        if (n == 0) return;
+        Session se(device);
+        Workspace ws(se.s);
+        const float* b = se.upload(ws, books, (size_t)ks * d);
+        const uint8_t* c = se.upload(ws, codes, n * m);
+        float* o = ws.alloc<float>(n * d);
+        launch_pq_decode(c, n, d, b, m, ks, o, se.s);
+        se.download(out_data, o, n * d);
+        se.sync();
+    });
+}
+
+int pqrr_dev_build_lut(int device, const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                       const float* x, size_t nx, float* out_lut) {
+    return guarded([&] {
+        check_shape(d, m, ks);
+        if (nx == 0) return;
+        Session se(device);
+        Workspace ws(se.s);
+        const float* b = se.upload(ws, books, (size_t)ks * d);
+        const float* xx = se.upload(ws, x, nx * d);
+        float* o = ws.alloc<float>(nx * m * ks);
+        launch_build_lut(xx, nx, d, b, m, ks, o, se.s);
+        se.download(out_lut, o, nx * m * ks);
+        se.sync();
+    });
+}
+
+int pqrr_dev_scan_topk(int device, const float* lut, uint32_t m, uint32_t ks, const uint8_t* codes,
+                       size_t n, size_t kprime, uint32_t id_base, uint32_t* out_ids,
+                       float* out_dists, size_t* out_count) {
+    return guarded([&] {
+        if (out_count) *out_count = 0;
+        if (kprime == 0 || n == 0) return;
+        Session se(device);
+        Workspace ws(se.s);
+        const float* l = se.upload(ws, lut, (size_t)m * ks);
+        const uint8_t* c = se.upload(ws, codes, n * m);
+        float* dist = ws.alloc<float>(n);
+        launch_lut_scan_all(l, m, ks, c, n, dist, se.s);
+        u64* keys = ws.alloc<u64>(n);
+        u64* sorted = ws.alloc<u64>(n);
+        lut_keys_kernel<<<nblk(n), 256, 0, se.s>>>(dist, n, id_base, keys);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        size_t tmp = 0;
+        PQRR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys, sorted, (int64_t)n, 0, 64, se.s));
+        void* t = ws.alloc<uint8_t>(tmp);
+        PQRR_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, keys, sorted, (int64_t)n, 0, 64, se.s));
+        count_launch(8);
+        const size_t cnt = std::min(kprime, n);
+        std::vector<u64> h(cnt);
+        se.download(h.data(), sorted, cnt);
+        se.sync();
+        for (size_t i = 0; i < cnt; ++i) {
+            out_ids[i] = (uint32_t)(h[i] & 0xffffffffull);
+            uint32_t b = (uint32_t)(h[i] >> 32);
+            std::memcpy(&out_dists[i], &b, 4);
+        }
+        if (out_count) *out_count = cnt;
+    });
+}
+
+int pqrr_dev_kmeans_train(int device, const float* points, size_t n, uint32_t dim, uint32_t k,
+                          uint32_t iterations, uint64_t seed, uint32_t redo, float* out_centroids,
+                          double* out_final_mse, double* out_trace) {
+    return guarded([&] {
+        if (k == 0) throw ArgError("k must be positive");
+        if (n < k || n == 0) throw ArgError("insufficient training data");
+        for (size_t i = 0; i < n * dim; ++i)
+            if (!std::isfinite(points[i])) throw ArgError("VectorSet: non-finite value");
+        Session se(device);
+        Workspace ws(se.s);
+        const float* p = se.upload(ws, points, n * dim);
+        kmeans_device(p, n, dim, k, iterations, seed, redo, out_centroids, out_final_mse, out_trace,
+                      se.s);
+    });
+}
+
+int pqrr_dev_synth(int device, uint64_t seed, uint32_t clusters, uint32_t d, uint32_t set,
+                   uint64_t row0, size_t n, uint8_t* out) {
+    return guarded([&] {
+        if (clusters == 0 || d == 0) throw ArgError("clusters and d must be positive");
+        if (n == 0) return;
+        Session se(device);
+        Workspace ws(se.s);
+        double* centers = ws.alloc<double>((size_t)clusters * d);
+        launch_synth_centers(seed, clusters, d, centers, se.s);
+        uint8_t* o = ws.alloc<uint8_t>(n * d);
+        if (set == 0) throw ArgError("set 0 holds the mixture centres, not rows");
+        launch_synth_rows(seed, set, row0, n, d, centers, clusters, o, se.s);
+        se.download(out, o, n * d);
+        se.sync();
+    });
+}
+
+int pqrr_dev_index_create(int device, uint32_t d, uint32_t c, const float* coarse, uint32_t m,
+                          const float* books, uint32_t mprime, const float* rbooks, uint32_t ks,
+                          pqrr_dev_index** out) {
+    return guarded([&] {
+        *out = nullptr;
+        check_shape(d, m, ks);
+        if (c == 0) throw ArgError("c must be positive");
+        if (mprime && d % mprime) throw ArgError("dimension not divisible");
+        if (mprime && !rbooks) throw ArgError("rbooks required when mprime > 0");
+        DeviceGuard g(device);
+        auto h = std::make_unique<pqrr_dev_index>();
+        DevIndex& ix = h->ix;
+        ix.device = device;
+        ix.d = d;
+        ix.c = c;
+        ix.m = m;
+        ix.mprime = mprime;
+        ix.ks = ks;
+        PQRR_CUDA(cudaStreamCreateWithFlags(&ix.stream, cudaStreamNonBlocking));
+        cudaMemPool_t pool;
+        PQRR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        PQRR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        ix.coarse.alloc((size_t)c * d);
+        ix.books.alloc((size_t)ks * d);
+        PQRR_CUDA(cudaMemcpy(ix.coarse.p, coarse, ix.coarse.bytes(), cudaMemcpyHostToDevice));
+        PQRR_CUDA(cudaMemcpy(ix.books.p, books, ix.books.bytes(), cudaMemcpyHostToDevice));
+        if (mprime) {
+            ix.rbooks.alloc((size_t)ks * d);
+            PQRR_CUDA(cudaMemcpy(ix.rbooks.p, rbooks, ix.rbooks.bytes(), cudaMemcpyHostToDevice));
+        }
+        ix.h_len.assign(c, 0);
+        ix.h_off.assign(c + 1, 0);
+        ix.list_len.alloc(c);
+        ix.list_off.alloc(c + 1);
+        PQRR_CUDA(cudaMemset(ix.list_len.p, 0, c * 4));
+        PQRR_CUDA(cudaMemset(ix.list_off.p, 0, (c + 1) * 8));
+        *out = h.release();
+    });
+}
+
+int pqrr_dev_index_destroy(pqrr_dev_index* h) {
+    return guarded([&] {
+        if (!h) return;
+        DeviceGuard g(h->ix.device);
+        delete h;
+    });
+}
+
+int pqrr_dev_add_u8(pqrr_dev_index* h, const uint8_t* y, size_t n, uint32_t id_base) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        const size_t chunk = 1u << 20;
+        for (size_t o = 0; o < n; o += chunk) {
+            const size_t cn = std::min(chunk, n - o);
+            Workspace ws(ix.stream);
+            uint8_t* dy = ws.alloc<uint8_t>(cn * ix.d);
+            PQRR_CUDA(cudaMemcpyAsync(dy, y + o * ix.d, cn * ix.d, cudaMemcpyHostToDevice, ix.stream));
+            stage_chunk(ix, nullptr, dy, cn, id_base + (uint32_t)o);
+        }
+        PQRR_CUDA(cudaStreamSynchronize(ix.stream));
+    });
+}
+
+int pqrr_dev_add_f32(pqrr_dev_index* h, const float* y, size_t n, uint32_t id_base) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        for (size_t i = 0; i < n * ix.d; ++i)
+            if (!std::isfinite(y[i])) throw ArgError("VectorSet: non-finite value");
+        const size_t chunk = 1u << 20;
+        for (size_t o = 0; o < n; o += chunk) {
+            const size_t cn = std::min(chunk, n - o);
+            Workspace ws(ix.stream);
+            float* dy = ws.alloc<float>(cn * ix.d);
+            PQRR_CUDA(cudaMemcpyAsync(dy, y + o * ix.d, cn * ix.d * 4, cudaMemcpyHostToDevice, ix.stream));
+            stage_chunk(ix, dy, nullptr, cn, id_base + (uint32_t)o);
+        }
+        PQRR_CUDA(cudaStreamSynchronize(ix.stream));
+    });
+}
+
+int pqrr_dev_add_synthetic(pqrr_dev_index* h, uint64_t seed, uint32_t clusters, uint64_t row0,
+                           size_t n, uint32_t id_base) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        Workspace wsc(ix.stream);
+        double* centers = wsc.alloc<double>((size_t)clusters * ix.d);
+        launch_synth_centers(seed, clusters, ix.d, centers, ix.stream);
+        const size_t chunk = 1u << 21;
+        for (size_t o = 0; o < n; o += chunk) {
+            const size_t cn = std::min(chunk, n - o);
+            Workspace ws(ix.stream);
+            uint8_t* dy = ws.alloc<uint8_t>(cn * ix.d);
+            launch_synth_rows(seed, 2, row0 + o, cn, ix.d, centers, clusters, dy, ix.stream);
+            stage_chunk(ix, nullptr, dy, cn, id_base + (uint32_t)o);
+        }
+        PQRR_CUDA(cudaStreamSynchronize(ix.stream));
+    });
+}
+
+int pqrr_dev_finalize(pqrr_dev_index* h) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        finalize(ix);
+    });
+}
+
+int pqrr_dev_index_get_info(pqrr_dev_index* h, pqrr_dev_index_info* out) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        finalize(ix);
+        out->n = ix.n;
+        out->slots = ix.slots;
+        out->d = ix.d;
+        out->c = ix.c;
+        out->m = ix.m;
+        out->mprime = ix.mprime;
+        out->ks = ix.ks;
+        out->max_list_len = ix.max_len();
+        out->device_bytes = ix.coarse.bytes() + ix.books.bytes() + ix.rbooks.bytes() +
+                            ix.codes.bytes() + ix.rcodes.bytes() + ix.ids.bytes() +
+                            ix.list_off.bytes() + ix.list_len.bytes() + ix.id_map.bytes();
+    });
+}
+
+int pqrr_dev_export_lists(pqrr_dev_index* h, uint64_t* offsets, uint32_t* ids, uint8_t* codes,
+                          uint8_t* rcodes) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        finalize(ix);
+        std::vector<uint64_t> uoff(ix.c + 1, 0);
+        for (uint32_t l = 0; l < ix.c; ++l) uoff[l + 1] = uoff[l] + ix.h_len[l];
+        if (offsets) std::memcpy(offsets, uoff.data(), (ix.c + 1) * 8);
+        if (ix.n == 0) return;
+        Workspace ws(ix.stream);
+        uint64_t* d_uoff = ws.alloc<uint64_t>(ix.c + 1);
+        PQRR_CUDA(cudaMemcpyAsync(d_uoff, uoff.data(), (ix.c + 1) * 8, cudaMemcpyHostToDevice, ix.stream));
+        uint32_t* o_ids = ws.alloc<uint32_t>(ix.n);
+        uint8_t* o_codes = ws.alloc<uint8_t>(ix.n * ix.m);
+        uint8_t* o_rcodes = ws.alloc<uint8_t>(ix.n * std::max<uint32_t>(ix.mprime, 1));
+        compact_lists_kernel<<<ix.c, 256, 0, ix.stream>>>(ix.list_off.p, ix.list_len.p, d_uoff, ix.ids.p,
+                                                         ix.codes.p, ix.rcodes.p, ix.m, ix.mprime,
+                                                         o_ids, o_codes, o_rcodes);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        if (ids) PQRR_CUDA(cudaMemcpyAsync(ids, o_ids, ix.n * 4, cudaMemcpyDeviceToHost, ix.stream));
+        if (codes) PQRR_CUDA(cudaMemcpyAsync(codes, o_codes, ix.n * ix.m, cudaMemcpyDeviceToHost, ix.stream));
+        if (rcodes && ix.mprime)
+            PQRR_CUDA(cudaMemcpyAsync(rcodes, o_rcodes, ix.n * ix.mprime, cudaMemcpyDeviceToHost, ix.stream));
+        PQRR_CUDA(cudaStreamSynchronize(ix.stream));
+    });
+}
+
+static int search_host(pqrr_dev_index* h, const float* qf, const uint8_t* qu, size_t nq, uint32_t w,
+                       size_t kprime, size_t k, uint32_t* out_ids, float* out_dists,
+                       uint32_t* out_counts) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        if (nq == 0) return;
+        cudaStream_t s = ix.stream;
+        Workspace ws(s);
+        float* xq = ws.alloc<float>(nq * ix.d);
+        if (qf) {
+            for (size_t i = 0; i < nq * ix.d; ++i)
+                if (!std::isfinite(qf[i])) throw ArgError("VectorSet: non-finite value");
+            PQRR_CUDA(cudaMemcpyAsync(xq, qf, nq * ix.d * 4, cudaMemcpyHostToDevice, s));
+        } else {
+            uint8_t* dq = ws.alloc<uint8_t>(nq * ix.d);
+            PQRR_CUDA(cudaMemcpyAsync(dq, qu, nq * ix.d, cudaMemcpyHostToDevice, s));
+            launch_widen_u8(dq, xq, nq * ix.d, s);
+        }
+        const size_t width = k ? k : kprime;
+        uint32_t* oi = ws.alloc<uint32_t>(nq * width);
+        float* od = ws.alloc<float>(nq * width);
+        uint32_t* oc = ws.alloc<uint32_t>(nq);
+        search_device(ix, xq, nq, w, kprime, k, oi, od, oc);
+        PQRR_CUDA(cudaMemcpyAsync(out_ids, oi, nq * width * 4, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaMemcpyAsync(out_dists, od, nq * width * 4, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaMemcpyAsync(out_counts, oc, nq * 4, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pqrr_dev_search_u8(pqrr_dev_index* h, const uint8_t* queries, size_t nq, uint32_t w,
+                       size_t kprime, size_t k, uint32_t* out_ids, float* out_dists,
+                       uint32_t* out_counts) {
+    return search_host(h, nullptr, queries, nq, w, kprime, k, out_ids, out_dists, out_counts);
+}
+
+int pqrr_dev_search_f32(pqrr_dev_index* h, const float* queries, size_t nq, uint32_t w,
+                        size_t kprime, size_t k, uint32_t* out_ids, float* out_dists,
+                        uint32_t* out_counts) {
+    return search_host(h, queries, nullptr, nq, w, kprime, k, out_ids, out_dists, out_counts);
+}
+
+int pqrr_dev_search_u8_device(pqrr_dev_index* h, const uint8_t* d_queries, size_t nq, uint32_t w,
+                              size_t kprime, size_t k, uint32_t* d_out_ids, float* d_out_dists,
+                              uint32_t* d_out_counts, void* stream) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        if (nq == 0) return;
+        cudaStream_t user = static_cast<cudaStream_t>(stream);
+        cudaStream_t s = ix.stream;
+        if (user && user != s) {
+            cudaEvent_t e;
+            PQRR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            PQRR_CUDA(cudaEventRecord(e, user));
+            PQRR_CUDA(cudaStreamWaitEvent(s, e, 0));
+            cudaEventDestroy(e);
+        }
+        Workspace ws(s);
+        float* xq = ws.alloc<float>(nq * ix.d);
+        launch_widen_u8(d_queries, xq, nq * ix.d, s);
+        search_device(ix, xq, nq, w, kprime, k, d_out_ids, d_out_dists, d_out_counts);
+        if (user && user != s) {
+            cudaEvent_t e;
+            PQRR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            PQRR_CUDA(cudaEventRecord(e, s));
+            PQRR_CUDA(cudaStreamWaitEvent(user, e, 0));
+            cudaEventDestroy(e);
+        }
+    });
+}
+
+static int rerank_host(pqrr_dev_index* h, const float* qf, const uint8_t* qu, size_t nq,
+                       const uint32_t* sl_ids, const uint32_t* sl_counts, size_t sl_stride, size_t k,
+                       uint32_t* out_ids, float* out_dists) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        if (ix.mprime == 0) throw ArgError("re-ranking needs refinement codes (mprime > 0)");
+        for (size_t q = 0; q < nq; ++q)
+            if (k > sl_counts[q]) throw ShortlistError();
+        if (nq == 0 || k == 0) return;
+        if (sl_stride > 16384) throw UnsupportedError("shortlists above 16384 entries");
+        ensure_id_map(ix);
+        cudaStream_t s = ix.stream;
+        Workspace ws(s);
+        float* xq = ws.alloc<float>(nq * ix.d);
+        if (qf) {
+            PQRR_CUDA(cudaMemcpyAsync(xq, qf, nq * ix.d * 4, cudaMemcpyHostToDevice, s));
+        } else {
+            uint8_t* dq = ws.alloc<uint8_t>(nq * ix.d);
+            PQRR_CUDA(cudaMemcpyAsync(dq, qu, nq * ix.d, cudaMemcpyHostToDevice, s));
+            launch_widen_u8(dq, xq, nq * ix.d, s);
+        }
+        uint32_t* ids = ws.alloc<uint32_t>(nq * sl_stride);
+        PQRR_CUDA(cudaMemcpyAsync(ids, sl_ids, nq * sl_stride * 4, cudaMemcpyHostToDevice, s));
+        uint32_t* cnt = ws.alloc<uint32_t>(nq);
+        PQRR_CUDA(cudaMemcpyAsync(cnt, sl_counts, nq * 4, cudaMemcpyHostToDevice, s));
+        u64* key = ws.alloc<u64>(nq * sl_stride);
+        uint32_t* pos = ws.alloc<uint32_t>(nq * sl_stride);
+        unsigned* bad = ws.zeros<unsigned>(1);
+        ids_to_shortlist<<<nblk(nq * sl_stride), 256, 0, s>>>(ids, ix.id_map.p, nq * sl_stride, key, pos,
+                                                               bad, (uint32_t)ix.id_map.n);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        // unused tail entries of a row may hold junk ids: only the first cnt[q] are read
+        uint32_t* oi = ws.alloc<uint32_t>(nq * k);
+        float* od = ws.alloc<float>(nq * k);
+        uint32_t* oc = ws.alloc<uint32_t>(nq);
+        launch_rerank(reinterpret_cast<uint64_t*>(key), pos, cnt, (uint32_t)sl_stride, nq, xq, ix.d,
+                      ix.list_off.p, ix.c, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
+                      ix.rbooks.p, ix.mprime, ix.ks, (uint32_t)k, oi, od, oc, s);
+        PQRR_CUDA(cudaMemcpyAsync(out_ids, oi, nq * k * 4, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaMemcpyAsync(out_dists, od, nq * k * 4, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pqrr_dev_rerank_u8(pqrr_dev_index* h, const uint8_t* queries, size_t nq, const uint32_t* sl_ids,
+                       const uint32_t* sl_counts, size_t sl_stride, size_t k, uint32_t* out_ids,
+                       float* out_dists) {
+    return rerank_host(h, nullptr, queries, nq, sl_ids, sl_counts, sl_stride, k, out_ids, out_dists);
+}
+
+int pqrr_dev_rerank_f32(pqrr_dev_index* h, const float* queries, size_t nq, const uint32_t* sl_ids,
+                        const uint32_t* sl_counts, size_t sl_stride, size_t k, uint32_t* out_ids,
+                        float* out_dists) {
+    return rerank_host(h, queries, nullptr, nq, sl_ids, sl_counts, sl_stride, k, out_ids, out_dists);
+}
+
+int pqrr_dev_reconstruct(pqrr_dev_index* h, const uint32_t* ids, size_t n, float* out) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        if (n == 0) return;
+        ensure_id_map(ix);
+        for (size_t i = 0; i < n; ++i)
+            if (ids[i] >= ix.next_id) throw ArgError("id out of range");
+        cudaStream_t s = ix.stream;
+        Workspace ws(s);
+        uint32_t* d_ids = ws.alloc<uint32_t>(n);
+        PQRR_CUDA(cudaMemcpyAsync(d_ids, ids, n * 4, cudaMemcpyHostToDevice, s));
+        float* o = ws.alloc<float>(n * ix.d);
+        reconstruct_kernel<<<nblk(n * ix.d), 256, 0, s>>>(d_ids, n, ix.id_map.p, ix.list_off.p, ix.c, ix.d,
+                                                           ix.coarse.p, ix.codes.p, ix.books.p, ix.m,
+                                                           ix.rcodes.p, ix.rbooks.p, ix.mprime, ix.ks, o);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        PQRR_CUDA(cudaMemcpyAsync(out, o, n * ix.d * 4, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pqrr_dev_last_search_stats(pqrr_dev_index* h, pqrr_dev_search_stats* out) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> lk(h->ix.mu);
+        *out = h->ix.stats;
+    });
+}
+
+}  // extern "C"

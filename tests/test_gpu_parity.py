@@ -1,0 +1,214 @@
+"""GPU parity suite: the CUDA path (through the C ABI) against the golden
+vectors produced by the reference's own code and against the CPU oracle on the
+same seeded inputs.  Integer/index outputs must be bit-exact; float distances
+too (the arithmetic contract makes them identical)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def pqobj(pq, books, d=128):
+    books = np.asarray(books, np.float32)
+    m = books.shape[0]
+    return pq.ProductQuantizer(d, m, books.shape[1], books.reshape(m, books.shape[1], -1))
+
+
+# ------------------------------------------------------------------ kernel seam
+def test_assign_batch_golden(pq, golden_ivf):
+    g = golden_ivf
+    a, d = pq.kernels.assign_batch(g["base"].astype(np.float32), g["coarse"])
+    np.testing.assert_array_equal(a, g["assign"])
+    np.testing.assert_array_equal(bits(d), bits(g["assign_dist"]))
+
+
+def test_assign_batch_ties_and_dims(pq, oracle):
+    rng = np.random.default_rng(7)
+    for d in [4, 8, 12, 16, 24, 32, 64, 128, 130]:
+        pts = rng.integers(0, 6, (777, d)).astype(np.float32)
+        cen = rng.integers(0, 6, (67, d)).astype(np.float32)
+        cen[9] = cen[2]
+        a1, d1 = pq.kernels.assign_batch(pts, cen)
+        a2, d2 = oracle.assign(pts, cen)
+        np.testing.assert_array_equal(a1, a2)
+        np.testing.assert_array_equal(bits(d1), bits(d2))
+
+
+def test_encode_decode_lut_golden(pq, golden_ivf, oracle):
+    g = golden_ivf
+    bf = g["base"].astype(np.float32)
+    res = bf - g["coarse"][g["assign"]]
+    P = pqobj(pq, g["books"])
+    np.testing.assert_array_equal(pq.kernels.encode_batch(P, res), g["codes"])
+    dec = pq.kernels.decode_batch(P, g["codes"][:500])
+    np.testing.assert_array_equal(bits(dec), bits(oracle.decode(g["books"], g["codes"][:500], 128)))
+    luts = pq.build_lut(P, res[:5])
+    for i in range(5):
+        np.testing.assert_array_equal(bits(luts[i].values), bits(oracle.build_lut(g["books"], res[i], 8)))
+
+
+def test_scan_topk_golden(pq, golden_prims):
+    g = golden_prims
+    lut = pq.LookupTable(g["lut"])
+    r = pq.kernels.scan_topk(lut, g["codes"], 100, id_base=7)
+    np.testing.assert_array_equal(r.ids, g["scan_ids"])
+    np.testing.assert_array_equal(bits(r.dists), bits(g["scan_dists"]))
+    r = pq.kernels.scan_topk(lut, g["codes"][:3000], 50)
+    np.testing.assert_array_equal(r.ids, g["scan_ids_serial"])
+
+
+# ------------------------------------------------------------------ generator + training
+def test_device_generator_bit_identical(pq, oracle, golden_ivf):
+    g = golden_ivf
+    base = pq.synth(2, 0, 4000, int(g["clusters"]), seed=int(g["seed"]))
+    np.testing.assert_array_equal(base, g["base"])
+    centers = oracle.synth_centers(1, 1024, 128)
+    for set_id, row0 in [(1, 0), (2, 123_456_789), (3, 9999)]:
+        np.testing.assert_array_equal(pq.synth(set_id, row0, 300, 1024, seed=1),
+                                      oracle.synth_rows(1, set_id, row0, 300, centers))
+
+
+def test_kmeans_bit_identical(pq, oracle):
+    rng = np.random.default_rng(9)
+    p = (rng.standard_normal((5000, 16)) * 7 + rng.integers(0, 5, (5000, 1))).astype(np.float32)
+    p[:40] = p[0]  # exact duplicates exercise ties and empty-cluster splits
+    for k in [1, 7, 64, 300]:
+        tr = []
+        cb = pq.kmeans_train(p, k, pq.TrainParams(iterations=8, seed=k, trace=tr))
+        c2, mse2, trace2 = oracle.kmeans(p, k, iterations=8, seed=k)
+        np.testing.assert_array_equal(bits(cb.centroids), bits(c2))
+        assert cb.final_mse == mse2
+        np.testing.assert_array_equal(np.array(tr), trace2)
+
+
+def test_ivf_train_bit_identical(pq, golden_ivf):
+    g = golden_ivf
+    trf = g["train"].astype(np.float32)
+    coarse, P = pq.ivf_train(trf, int(g["c"]), int(g["m"]), params=pq.TrainParams(iterations=6, seed=3))
+    np.testing.assert_array_equal(bits(coarse.centroids), bits(g["coarse"]))
+    np.testing.assert_array_equal(bits(P.books), bits(g["books"]))
+    rq = pq.ivf_refine_train(coarse, P, trf, int(g["mprime"]), pq.TrainParams(iterations=6, seed=5))
+    np.testing.assert_array_equal(bits(rq.pq.books), bits(g["rbooks"]))
+
+
+# ------------------------------------------------------------------ index: build / search / rerank
+def build_small(pq, g, refine=True):
+    coarse = pq.Codebook(np.asarray(g["coarse"], np.float32))
+    P = pqobj(pq, g["books"])
+    rq = pq.RefineQuantizer(pqobj(pq, g["rbooks"])) if refine else None
+    return pq.ivf_build(coarse, P, g["base"], rq=rq), coarse, P, rq
+
+
+def test_ivf_build_layout_golden(pq, golden_ivf):
+    g = golden_ivf
+    ix, _, _, _ = build_small(pq, g)
+    offs, ids, codes, rc = ix.export_lists()
+    np.testing.assert_array_equal(offs, g["offsets"])
+    np.testing.assert_array_equal(ids, g["ids_l"])
+    np.testing.assert_array_equal(codes, g["codes"][g["ids_l"]])
+    np.testing.assert_array_equal(rc, g["rcodes"][g["ids_l"]])
+
+
+def test_ivf_refine_encode_api(pq, golden_ivf):
+    g = golden_ivf
+    ix, coarse, P, _ = build_small(pq, g, refine=False)
+    rq = pq.RefineQuantizer(pqobj(pq, g["rbooks"]))
+    rc = pq.ivf_refine_encode(ix, rq, g["base"])
+    np.testing.assert_array_equal(rc.bytes, g["rcodes"])
+    yh = pq.ivf_reconstruct(ix, rq, 17, rc)
+    a = int(g["assign"][17])
+    p = np.concatenate([g["books"][j, g["codes"][17, j]] for j in range(8)])
+    r = np.concatenate([g["rbooks"][j, g["rcodes"][17, j]] for j in range(16)])
+    np.testing.assert_array_equal(bits(yh), bits((g["coarse"][a] + p) + r))
+
+
+def test_search_shortlist_and_rerank_golden(pq, golden_ivf):
+    g = golden_ivf
+    ix, _, _, _ = build_small(pq, g)
+    for q in (g["queries"], g["queries"].astype(np.float32)):
+        ids, d, cnt = ix.search(q, int(g["v"]), int(g["kprime"]), 0)
+        np.testing.assert_array_equal(cnt, g["sl_cnt"])
+        np.testing.assert_array_equal(ids, g["sl_ids"])
+        np.testing.assert_array_equal(bits(d), bits(g["sl_dists"]))
+        ids, d, cnt = ix.search(q, int(g["v"]), int(g["kprime"]), int(g["k"]))
+        np.testing.assert_array_equal(ids, g["rr_ids"])
+        np.testing.assert_array_equal(bits(d), bits(g["rr_dists"]))
+    # v = c equals the exhaustive scan
+    ids, d, _ = ix.search(g["queries"][:4], int(g["c"]), 200, 0)
+    np.testing.assert_array_equal(ids, g["ex_ids"])
+    np.testing.assert_array_equal(bits(d), bits(g["ex_dists"]))
+
+
+def test_reference_api_mirror(pq, golden_ivf):
+    g = golden_ivf
+    ix, coarse, P, rq = build_small(pq, g, refine=False)
+    rc = pq.ivf_refine_encode(ix, pq.RefineQuantizer(pqobj(pq, g["rbooks"])), g["base"])
+    prm = pq.IvfSearchParams(v=int(g["v"]), kprime=int(g["kprime"]))
+    sl = pq.ivf_search_batch(ix, g["queries"], prm)
+    one = pq.ivf_search(ix, g["queries"][3], prm)
+    np.testing.assert_array_equal(one.ids, sl[3].ids)
+    rr = pq.ivf_rerank(g["queries"], sl, ix, ix.rq, rc, int(g["k"]))
+    for i in range(len(sl)):
+        np.testing.assert_array_equal(rr[i].ids, g["rr_ids"][i])
+        np.testing.assert_array_equal(bits(rr[i].dists), bits(g["rr_dists"][i]))
+        assert set(rr[i].ids) <= set(sl[i].ids)
+    with pytest.raises(ValueError, match="shortlist too small"):
+        pq.ivf_rerank(g["queries"][0], pq.SearchResult(sl[0].ids[:5], sl[0].dists[:5]), ix, ix.rq,
+                      rc, 10)
+    with pytest.raises(ValueError):
+        ix.search(g["queries"], 0, 10, 0)
+    with pytest.raises(ValueError):
+        ix.search(g["queries"], int(g["c"]) + 1, 10, 0)
+
+
+def test_chunked_add_equals_single_add(pq, golden_ivf):
+    g = golden_ivf
+    ix, coarse, P, rq = build_small(pq, g)
+    ix2 = pq.IvfIndex(coarse, P, rq)
+    ix2.add(g["base"][:1000], 0)
+    ix2.add(g["base"][1000:2500], 1000)
+    ix2.finalize()  # layout built in two rounds: old entries kept, new appended
+    ix2.add(g["base"][2500:], 2500)
+    for a, b in zip(ix.export_lists(), ix2.export_lists()):
+        np.testing.assert_array_equal(a, b)
+    with pytest.raises(ValueError):
+        ix2.add(g["base"][:10], 5)  # ids must ascend
+
+
+# ------------------------------------------------------------------ larger: sampled threshold path
+@pytest.fixture(scope="module")
+def mid_instance(pq, oracle):
+    seed, K = 0, 256
+    centers = oracle.synth_centers(seed, K, 128)
+    base = oracle.synth_rows(seed, 2, 0, 120_000, centers)
+    train = oracle.synth_rows(seed, 1, 0, 20_000, centers).astype(np.float32)
+    queries = oracle.synth_rows(seed, 3, 0, 64, centers)
+    coarse, books = oracle.ivf_train(train, 128, 8, iterations=4, seed=0)
+    rbooks = oracle.ivf_refine_train(coarse, books, 8, train, 16, iterations=4, seed=0)
+    oix = oracle.ivf_build(coarse, books, 8, base.astype(np.float32))
+    oix.refine_encode(rbooks, 16, base.astype(np.float32))
+    dix = pq.ivf_build(pq.Codebook(coarse), pqobj(pq, books.reshape(8, 256, 16)), base,
+                       rq=pq.RefineQuantizer(pqobj(pq, rbooks.reshape(16, 256, 8))))
+    return dict(base=base, queries=queries, coarse=coarse, books=books, rbooks=rbooks, oix=oix,
+                dix=dix)
+
+
+@pytest.mark.parametrize("v,kprime,k", [(24, 1000, 100), (8, 100, 10), (40, 300, 300), (3, 2000, 1)])
+def test_search_matches_oracle(mid_instance, v, kprime, k):
+    oix, dix, q = mid_instance["oix"], mid_instance["dix"], mid_instance["queries"]
+    qf = q.astype(np.float32)
+    oi, od, oc = oix.search(qf, v, kprime)
+    di, dd, dc = dix.search(q, v, kprime, 0)
+    np.testing.assert_array_equal(dc, oc)
+    np.testing.assert_array_equal(di, oi)
+    np.testing.assert_array_equal(bits(dd), bits(od))
+    ri, rd = oix.rerank(qf, oi, oc, k)
+    di, dd, dc = dix.search(q, v, kprime, k)
+    np.testing.assert_array_equal(di, ri)
+    np.testing.assert_array_equal(bits(dd), bits(rd))
+    st = dix.last_stats()
+    assert st["kernels"] > 5 and st["ms_scan"] > 0
