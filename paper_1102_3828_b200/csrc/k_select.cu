@@ -292,9 +292,10 @@ __global__ __launch_bounds__(256) void rerank_kernel(
     __syncthreads();
     bitonic_sort_kv(keys, nullptr, n2);
     const uint32_t cnt = min(n, k);
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-        out_ids[q * k + i] = key_id(keys[i]);
-        out_dists[q * k + i] = key_dist(keys[i]);
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+        const bool live = i < cnt;
+        out_ids[q * k + i] = live ? key_id(keys[i]) : 0xffffffffu;
+        out_dists[q * k + i] = live ? key_dist(keys[i]) : __int_as_float(0x7f800000);
     }
     if (threadIdx.x == 0) out_cnt[q] = cnt;
 }
@@ -309,6 +310,9 @@ __global__ void unpack_keys_kernel(const u64* __restrict__ keys, const uint32_t*
     if (i < cnt[q]) {
         ids[idx] = key_id(keys[idx]);
         dists[idx] = key_dist(keys[idx]);
+    } else {  // rows shorter than the width: (UINT32_MAX, +inf) sentinels
+        ids[idx] = 0xffffffffu;
+        dists[idx] = __int_as_float(0x7f800000);
     }
 }
 

@@ -12,10 +12,9 @@ def bits(a):
     return np.ascontiguousarray(a, np.float32).view(np.uint32)
 
 
-def pqobj(pq, books, d=128):
-    books = np.asarray(books, np.float32)
-    m = books.shape[0]
-    return pq.ProductQuantizer(d, m, books.shape[1], books.reshape(m, books.shape[1], -1))
+def pqobj(pq, books, m, d=128, ks=256):
+    books = np.asarray(books, np.float32).reshape(m, ks, d // m)
+    return pq.ProductQuantizer(d, m, ks, books)
 
 
 # ------------------------------------------------------------------ kernel seam
@@ -42,7 +41,7 @@ def test_encode_decode_lut_golden(pq, golden_ivf, oracle):
     g = golden_ivf
     bf = g["base"].astype(np.float32)
     res = bf - g["coarse"][g["assign"]]
-    P = pqobj(pq, g["books"])
+    P = pqobj(pq, g["books"], 8)
     np.testing.assert_array_equal(pq.kernels.encode_batch(P, res), g["codes"])
     dec = pq.kernels.decode_batch(P, g["codes"][:500])
     np.testing.assert_array_equal(bits(dec), bits(oracle.decode(g["books"], g["codes"][:500], 128)))
@@ -90,16 +89,16 @@ def test_ivf_train_bit_identical(pq, golden_ivf):
     trf = g["train"].astype(np.float32)
     coarse, P = pq.ivf_train(trf, int(g["c"]), int(g["m"]), params=pq.TrainParams(iterations=6, seed=3))
     np.testing.assert_array_equal(bits(coarse.centroids), bits(g["coarse"]))
-    np.testing.assert_array_equal(bits(P.books), bits(g["books"]))
+    np.testing.assert_array_equal(bits(P.books.reshape(-1)), bits(g["books"]))
     rq = pq.ivf_refine_train(coarse, P, trf, int(g["mprime"]), pq.TrainParams(iterations=6, seed=5))
-    np.testing.assert_array_equal(bits(rq.pq.books), bits(g["rbooks"]))
+    np.testing.assert_array_equal(bits(rq.pq.books.reshape(-1)), bits(g["rbooks"]))
 
 
 # ------------------------------------------------------------------ index: build / search / rerank
 def build_small(pq, g, refine=True):
     coarse = pq.Codebook(np.asarray(g["coarse"], np.float32))
-    P = pqobj(pq, g["books"])
-    rq = pq.RefineQuantizer(pqobj(pq, g["rbooks"])) if refine else None
+    P = pqobj(pq, g["books"], 8)
+    rq = pq.RefineQuantizer(pqobj(pq, g["rbooks"], 16)) if refine else None
     return pq.ivf_build(coarse, P, g["base"], rq=rq), coarse, P, rq
 
 
@@ -116,13 +115,15 @@ def test_ivf_build_layout_golden(pq, golden_ivf):
 def test_ivf_refine_encode_api(pq, golden_ivf):
     g = golden_ivf
     ix, coarse, P, _ = build_small(pq, g, refine=False)
-    rq = pq.RefineQuantizer(pqobj(pq, g["rbooks"]))
+    rq = pq.RefineQuantizer(pqobj(pq, g["rbooks"], 16))
     rc = pq.ivf_refine_encode(ix, rq, g["base"])
     np.testing.assert_array_equal(rc.bytes, g["rcodes"])
     yh = pq.ivf_reconstruct(ix, rq, 17, rc)
     a = int(g["assign"][17])
-    p = np.concatenate([g["books"][j, g["codes"][17, j]] for j in range(8)])
-    r = np.concatenate([g["rbooks"][j, g["rcodes"][17, j]] for j in range(16)])
+    B = g["books"].reshape(8, 256, 16)
+    R = g["rbooks"].reshape(16, 256, 8)
+    p = np.concatenate([B[j, g["codes"][17, j]] for j in range(8)])
+    r = np.concatenate([R[j, g["rcodes"][17, j]] for j in range(16)])
     np.testing.assert_array_equal(bits(yh), bits((g["coarse"][a] + p) + r))
 
 
@@ -146,7 +147,7 @@ def test_search_shortlist_and_rerank_golden(pq, golden_ivf):
 def test_reference_api_mirror(pq, golden_ivf):
     g = golden_ivf
     ix, coarse, P, rq = build_small(pq, g, refine=False)
-    rc = pq.ivf_refine_encode(ix, pq.RefineQuantizer(pqobj(pq, g["rbooks"])), g["base"])
+    rc = pq.ivf_refine_encode(ix, pq.RefineQuantizer(pqobj(pq, g["rbooks"], 16)), g["base"])
     prm = pq.IvfSearchParams(v=int(g["v"]), kprime=int(g["kprime"]))
     sl = pq.ivf_search_batch(ix, g["queries"], prm)
     one = pq.ivf_search(ix, g["queries"][3], prm)
@@ -191,8 +192,8 @@ def mid_instance(pq, oracle):
     rbooks = oracle.ivf_refine_train(coarse, books, 8, train, 16, iterations=4, seed=0)
     oix = oracle.ivf_build(coarse, books, 8, base.astype(np.float32))
     oix.refine_encode(rbooks, 16, base.astype(np.float32))
-    dix = pq.ivf_build(pq.Codebook(coarse), pqobj(pq, books.reshape(8, 256, 16)), base,
-                       rq=pq.RefineQuantizer(pqobj(pq, rbooks.reshape(16, 256, 8))))
+    dix = pq.ivf_build(pq.Codebook(coarse), pqobj(pq, books, 8), base,
+                       rq=pq.RefineQuantizer(pqobj(pq, rbooks, 16)))
     return dict(base=base, queries=queries, coarse=coarse, books=books, rbooks=rbooks, oix=oix,
                 dix=dix)
 
@@ -204,8 +205,11 @@ def test_search_matches_oracle(mid_instance, v, kprime, k):
     oi, od, oc = oix.search(qf, v, kprime)
     di, dd, dc = dix.search(q, v, kprime, 0)
     np.testing.assert_array_equal(dc, oc)
-    np.testing.assert_array_equal(di, oi)
-    np.testing.assert_array_equal(bits(dd), bits(od))
+    for i in range(len(q)):
+        n = oc[i]
+        np.testing.assert_array_equal(di[i, :n], oi[i, :n])
+        np.testing.assert_array_equal(bits(dd[i, :n]), bits(od[i, :n]))
+        assert np.all(di[i, n:] == 0xFFFFFFFF) and np.all(np.isinf(dd[i, n:]))
     ri, rd = oix.rerank(qf, oi, oc, k)
     di, dd, dc = dix.search(q, v, kprime, k)
     np.testing.assert_array_equal(di, ri)
