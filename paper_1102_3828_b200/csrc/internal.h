@@ -98,9 +98,25 @@ void launch_layout_place_new(const uint32_t* sorted_list, const uint32_t* sorted
                              uint32_t mprime, uint8_t* codes, uint32_t* ids, uint8_t* rcodes,
                              cudaStream_t s);
 
+// Parity-balanced list order (see k_layout.cu) and per-list re-sorting.
+void launch_parity_keys(const uint64_t* off, const uint32_t* len, uint32_t nlists,
+                        const uint8_t* codes, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+void launch_list_id_keys(const uint64_t* off, const uint32_t* len, uint32_t nlists,
+                         const uint32_t* ids, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+void launch_pair_perm(const uint64_t* off, const uint32_t* len, uint32_t nlists,
+                      const uint32_t* skeys, const uint32_t* svals, uint32_t* perm, cudaStream_t s);
+void launch_gather_layout(const uint64_t* off, const uint32_t* len, uint32_t nlists,
+                          const uint32_t* perm, const uint8_t* codes, const uint32_t* ids,
+                          const uint8_t* rcodes, uint32_t m, uint32_t mprime, uint8_t* o_codes,
+                          uint32_t* o_ids, uint8_t* o_rcodes, cudaStream_t s);
+// Stable per-segment sort (CUB segmented radix sort).
+void segmented_sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                          uint32_t* vals_out, size_t n, uint32_t nseg, const uint64_t* seg_begin,
+                          const uint64_t* seg_end, int bits, cudaStream_t s);
+
 // -------------------------------------------------------------- search (k_scan.cu / k_select.cu)
 static const int kQT = 16;        // queries per scan work item
-static const int kScanThreads = 256;
+static const int kScanThreads = 512;
 
 struct ScanArgs {
     const uint8_t* codes;      // list-major, m bytes per entry (m == 8)
@@ -145,13 +161,13 @@ void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uin
                         cudaStream_t s);
 // tau_q = rank-th smallest sample of query q (sampled queries), +inf otherwise.
 void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_off, uint32_t w,
-                             size_t nq, const uint8_t* query_sampled, uint32_t rank, float* tau,
-                             cudaStream_t s);
+                             size_t nq, const uint8_t* query_sampled, uint32_t rank,
+                             uint32_t max_samples, float* tau, cudaStream_t s);
 // Exact top-kprime under (dist, id) from each query's candidates.
 void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
-                        uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime,
-                        bool sorted, uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt,
-                        cudaStream_t s);
+                        uint32_t cap, uint32_t max_n, size_t nq, const uint32_t* ids,
+                        uint32_t kprime, bool sorted, uint64_t* sl_key, uint32_t* sl_pos,
+                        uint32_t* sl_cnt, cudaStream_t s);
 // Re-rank the shortlist with the 3-term reconstruction, keep the k best.
 void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_t* sl_cnt,
                    uint32_t sl_stride, size_t nq, const float* xq, uint32_t d,

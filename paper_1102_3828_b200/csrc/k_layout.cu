@@ -59,7 +59,133 @@ __global__ void place_new_kernel(const uint32_t* __restrict__ sorted_list,
     if (mprime) copy_bytes(rcodes + pos * mprime, st_rcodes + (size_t)idx * mprime, mprime);
 }
 
+// Parity vector of an m = 8 code: bit j = code byte j & 1.  A 16-query LUT row
+// is 64 B, i.e. exactly one half of the 32 banks, and the half is selected by
+// the parity of the code byte; two entries of one warp step collide iff their
+// bytes share parity.
+__global__ void parity_keys_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
+                                   const uint8_t* __restrict__ codes, uint32_t* __restrict__ keys,
+                                   uint32_t* __restrict__ vals) {
+    const uint32_t l = blockIdx.x;
+    const uint64_t o = off[l];
+    for (uint32_t r = threadIdx.x; r < len[l]; r += blockDim.x) {
+        const u64 c = *reinterpret_cast<const u64*>(codes + (o + r) * 8);
+        uint32_t v = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v |= (uint32_t)((c >> (8 * j)) & 1ull) << j;
+        keys[o + r] = v;
+        vals[o + r] = (uint32_t)(o + r);
+    }
+}
+
+// One CTA per list: the list's entries sorted (stably) by parity vector v are
+// re-laid out as complementary pairs (v, ~v) first — every aligned group of 8
+// entries then has exactly 4 even and 4 odd bytes for every sub-quantizer, so
+// each LDS.128 of the scanner is 4 conflict-free wavefronts — then leftovers.
+__global__ void pair_perm_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
+                                 const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+                                 uint32_t* __restrict__ perm) {
+    __shared__ uint32_t cnt[256], start[256], pair_off[128], left_off[256];
+    __shared__ uint32_t s_pairs_total;
+    const uint32_t l = blockIdx.x;
+    const uint64_t o = off[l];
+    const uint32_t n = len[l];
+    for (uint32_t v = threadIdx.x; v < 256; v += blockDim.x) cnt[v] = 0;
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) atomicAdd(&cnt[skeys[o + r]], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0, pacc = 0;
+        for (uint32_t v = 0; v < 256; ++v) {
+            start[v] = acc;
+            acc += cnt[v];
+        }
+        for (uint32_t v = 0; v < 128; ++v) {
+            pair_off[v] = pacc;
+            pacc += 2 * min(cnt[v], cnt[255 - v]);
+        }
+        s_pairs_total = pacc;
+        uint32_t lacc = pacc;
+        for (uint32_t v = 0; v < 256; ++v) {
+            left_off[v] = lacc;
+            const uint32_t p = min(cnt[v], cnt[255 - v]);
+            lacc += cnt[v] - p;
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t v = skeys[o + i];
+        const uint32_t r = i - start[v];
+        const uint32_t p = min(cnt[v], cnt[255 - v]);
+        uint32_t dst;
+        if (r < p) dst = v < 128 ? pair_off[v] + 2 * r : pair_off[255 - v] + 2 * r + 1;
+        else dst = left_off[v] + (r - p);
+        perm[o + dst] = svals[o + i];
+    }
+}
+
+__global__ void gather_layout_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
+                                     const uint32_t* __restrict__ perm, const uint8_t* __restrict__ codes,
+                                     const uint32_t* __restrict__ ids, const uint8_t* __restrict__ rcodes,
+                                     uint32_t m, uint32_t mprime, uint8_t* __restrict__ o_codes,
+                                     uint32_t* __restrict__ o_ids, uint8_t* __restrict__ o_rcodes) {
+    const uint32_t l = blockIdx.x;
+    const uint64_t o = off[l];
+    for (uint32_t r = threadIdx.x; r < len[l]; r += blockDim.x) {
+        const uint64_t dst = o + r, src = perm[o + r];
+        o_ids[dst] = ids[src];
+        copy_bytes(o_codes + dst * m, codes + src * m, m);
+        if (mprime) copy_bytes(o_rcodes + dst * mprime, rcodes + src * mprime, mprime);
+    }
+}
+
+__global__ void list_keys_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
+                                 const uint32_t* __restrict__ ids, uint32_t* __restrict__ keys,
+                                 uint32_t* __restrict__ vals) {
+    const uint32_t l = blockIdx.x;
+    const uint64_t o = off[l];
+    for (uint32_t r = threadIdx.x; r < len[l]; r += blockDim.x) {
+        keys[o + r] = ids[o + r];
+        vals[o + r] = (uint32_t)(o + r);
+    }
+}
+
 }  // namespace
+
+void launch_parity_keys(const uint64_t* off, const uint32_t* len, uint32_t nlists,
+                        const uint8_t* codes, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+    parity_keys_kernel<<<nlists, 256, 0, s>>>(off, len, codes, keys, vals);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_list_id_keys(const uint64_t* off, const uint32_t* len, uint32_t nlists,
+                         const uint32_t* ids, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+    list_keys_kernel<<<nlists, 256, 0, s>>>(off, len, ids, keys, vals);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_pair_perm(const uint64_t* off, const uint32_t* len, uint32_t nlists,
+                      const uint32_t* skeys, const uint32_t* svals, uint32_t* perm, cudaStream_t s) {
+    pair_perm_kernel<<<nlists, 256, 0, s>>>(off, len, skeys, svals, perm);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_gather_layout(const uint64_t* off, const uint32_t* len, uint32_t nlists,
+                          const uint32_t* perm, const uint8_t* codes, const uint32_t* ids,
+                          const uint8_t* rcodes, uint32_t m, uint32_t mprime, uint8_t* o_codes,
+                          uint32_t* o_ids, uint8_t* o_rcodes, cudaStream_t s) {
+    gather_layout_kernel<<<nlists, 256, 0, s>>>(off, len, perm, codes, ids, rcodes, m, mprime, o_codes,
+                                                o_ids, o_rcodes);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void segmented_sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                          uint32_t* vals_out, size_t n, uint32_t nseg, const uint64_t* seg_begin,
+                          const uint64_t* seg_end, int bits, cudaStream_t s);
 
 void launch_layout_copy_old(const uint64_t* old_off, const uint32_t* old_len, uint32_t nlists,
                             const uint64_t* new_off, const uint8_t* old_codes,

@@ -43,7 +43,7 @@ __device__ __forceinline__ void build_luts(float* __restrict__ lut, const float*
             r[t] = v.x; r[t + 1] = v.y; r[t + 2] = v.z; r[t + 3] = v.w;
         }
         const float* bj = books + (size_t)j * KS * DSUB;
-#pragma unroll 2
+#pragma unroll
         for (int ib = 0; ib < KS / (2 * NW); ++ib) {
             const int i = (ib * NW + warp) * 2 + ih;
             const float* b = bj + (size_t)i * DSUB;
@@ -140,31 +140,49 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
             tk[k] = s_tau[qd * 4 + k];
         }
         if (a.stride <= 1) {
-            // ---------------- main mode: threshold filter + append
-            for (uint32_t base = warp * 8; base < len; base += NW * 8) {
-                const uint32_t e = base + slot;
-                const bool valid = e < len;
-                const u64 code = valid ? __ldg(codes + e) : 0ull;
-                float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+            // ---------------- main mode: threshold filter + append.  Codes are
+            // prefetched PF steps ahead in registers so the L2/HBM latency of
+            // the stream hides behind the LUT gathers of earlier steps.
+            constexpr uint32_t S = NW * 8;  // entries per CTA step
+            constexpr int PF = 4;
+            const uint32_t wbase = warp * 8;
+            u64 cbuf[PF];
 #pragma unroll
-                for (int j = 0; j < M; ++j) {
-                    const uint32_t c = (uint32_t)(code >> (8 * j)) & 0xffu;
-                    const float4 v = lut4[(j * KS + c) * (QT / 4) + qd];
-                    acc0 = __fadd_rn(acc0, v.x);
-                    acc1 = __fadd_rn(acc1, v.y);
-                    acc2 = __fadd_rn(acc2, v.z);
-                    acc3 = __fadd_rn(acc3, v.w);
-                }
-                const bool h0 = valid && acc0 <= tk[0];
-                const bool h1 = valid && acc1 <= tk[1];
-                const bool h2 = valid && acc2 <= tk[2];
-                const bool h3 = valid && acc3 <= tk[3];
-                if (__any_sync(0xffffffffu, h0 | h1 | h2 | h3)) {
-                    const uint32_t pos = (uint32_t)(off + e);
-                    emit(h0, qk[0], acc0, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
-                    emit(h1, qk[1], acc1, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
-                    emit(h2, qk[2], acc2, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
-                    emit(h3, qk[3], acc3, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+            for (int k = 0; k < PF; ++k) {
+                const uint32_t e = wbase + k * S + slot;
+                cbuf[k] = e < len ? __ldg(codes + e) : 0ull;
+            }
+            for (uint32_t wb = wbase; wb < len; wb += PF * S) {
+#pragma unroll
+                for (int k = 0; k < PF; ++k) {
+                    const uint32_t eb = wb + k * S;
+                    if (eb >= len) break;  // warp-uniform
+                    const uint32_t e = eb + slot;
+                    const bool valid = e < len;
+                    const u64 code = cbuf[k];
+                    const uint32_t en = e + PF * S;
+                    cbuf[k] = en < len ? __ldg(codes + en) : 0ull;
+                    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+#pragma unroll
+                    for (int j = 0; j < M; ++j) {
+                        const uint32_t c = (uint32_t)(code >> (8 * j)) & 0xffu;
+                        const float4 v = lut4[(j * KS + c) * (QT / 4) + qd];
+                        acc0 = __fadd_rn(acc0, v.x);
+                        acc1 = __fadd_rn(acc1, v.y);
+                        acc2 = __fadd_rn(acc2, v.z);
+                        acc3 = __fadd_rn(acc3, v.w);
+                    }
+                    const bool h0 = valid && acc0 <= tk[0];
+                    const bool h1 = valid && acc1 <= tk[1];
+                    const bool h2 = valid && acc2 <= tk[2];
+                    const bool h3 = valid && acc3 <= tk[3];
+                    if (__any_sync(0xffffffffu, h0 | h1 | h2 | h3)) {
+                        const uint32_t pos = (uint32_t)(off + e);
+                        emit(h0, qk[0], acc0, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                        emit(h1, qk[1], acc1, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                        emit(h2, qk[2], acc2, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                        emit(h3, qk[3], acc3, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                    }
                 }
             }
         } else {

@@ -14,7 +14,7 @@
 namespace pqrr_b200 {
 namespace {
 
-constexpr int SEL_THREADS = 512;
+constexpr int SEL_THREADS = 256;
 constexpr int RADIX_BITS = 11;
 constexpr int NBINS = 1 << RADIX_BITS;
 
@@ -31,15 +31,20 @@ __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t n
     atomicAdd(grand_total, (unsigned long long)tot);
     const bool samp = tot > cap && stride > 1;
     sampled[q] = samp ? 1 : 0;
+    unsigned long long ssum = 0;
     for (uint32_t r = 0; r < w; ++r) {
         const uint32_t len = list_len[probes[q * w + r]];
-        pair_samples[q * w + r] = samp ? (len + stride - 1) / stride : 0;
+        const uint64_t ns = samp ? (len + stride - 1) / stride : 0;
+        pair_samples[q * w + r] = ns;
+        ssum += ns;
     }
+    atomicMax(grand_total + 1, ssum);
 }
 
 // Block-wide search of the bin holding the rank-th element (1-based) of a
 // 2048-bin histogram; returns bin and rank within the bin.
-__device__ void find_bin(const uint32_t* hist, uint32_t rank, uint32_t* s_bin, uint32_t* s_rank) {
+__device__ void find_bin(const uint32_t* hist, uint32_t rank, uint32_t* s_bin, uint32_t* s_rank,
+                         uint32_t* s_cnt = nullptr) {
     // one warp: lane l owns bins [64 l, 64 l + 64)
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
@@ -61,6 +66,7 @@ __device__ void find_bin(const uint32_t* hist, uint32_t rank, uint32_t* s_bin, u
                 if (rank <= c + h) {
                     *s_bin = lane * 64 + b;
                     *s_rank = rank - c;
+                    if (s_cnt) *s_cnt = h;
                     break;
                 }
                 c += h;
@@ -71,20 +77,28 @@ __device__ void find_bin(const uint32_t* hist, uint32_t rank, uint32_t* s_bin, u
 
 // tau_q = rank-th smallest sampled distance (an estimate of the distance that
 // admits ~alpha*k' entries); +inf for queries scanned without sampling.
-__global__ __launch_bounds__(SEL_THREADS) void sample_threshold_kernel(
+__global__ __launch_bounds__(SEL_THREADS, 3) void sample_threshold_kernel(
     const float* __restrict__ sample, const uint64_t* __restrict__ sample_off, uint32_t w,
-    const uint8_t* __restrict__ sampled, uint32_t rank, float* __restrict__ tau) {
+    const uint8_t* __restrict__ sampled, uint32_t rank, uint32_t stage_cap, float* __restrict__ tau) {
+    extern __shared__ uint32_t stage[];  // the query's samples when they fit
     __shared__ uint32_t hist[NBINS];
-    __shared__ uint32_t s_bin, s_rank;
+    __shared__ uint32_t s_bin, s_rank, s_cnt, s_val;
     const size_t q = blockIdx.x;
     if (!sampled[q]) {
         if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
         return;
     }
     const uint64_t lo = sample_off[q * w], hi = sample_off[q * w + w];
-    if (hi - lo < rank) {
+    const uint32_t n = (uint32_t)(hi - lo);
+    if (n < rank) {
         if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
         return;
+    }
+    const bool staged = n <= stage_cap;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(sample) + lo;
+    if (staged) {
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) stage[i] = src[i];
+        src = stage;
     }
     uint32_t prefix = 0, r = rank;
     const int shifts[3] = {21, 10, 0};
@@ -94,16 +108,23 @@ __global__ __launch_bounds__(SEL_THREADS) void sample_threshold_kernel(
         __syncthreads();
         const int sh = shifts[pass], wd = widths[pass];
         const uint32_t msk = (1u << wd) - 1u;
-        for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-            const uint32_t u = __float_as_uint(sample[i]);
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const uint32_t u = src[i];
             const bool match = pass == 0 ? true : ((u >> (sh + wd)) == prefix);
             if (match) atomicAdd(&hist[(u >> sh) & msk], 1u);
         }
         __syncthreads();
-        find_bin(hist, r, &s_bin, &s_rank);
+        find_bin(hist, r, &s_bin, &s_rank, &s_cnt);
         __syncthreads();
         prefix = (prefix << wd) | s_bin;
         r = s_rank;
+        if (s_cnt == 1 && sh > 0) {  // unique value left under this prefix
+            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+                if ((src[i] >> sh) == prefix) s_val = src[i];
+            __syncthreads();
+            prefix = s_val;
+            break;
+        }
         __syncthreads();
     }
     if (threadIdx.x == 0) tau[q] = __uint_as_float(prefix);
@@ -133,18 +154,18 @@ __device__ void bitonic_sort_kv(u64* keys, uint32_t* vals, uint32_t n2) {
 }
 
 // Exact k'-smallest (dist, id) keys among a query's candidates.
-__global__ __launch_bounds__(SEL_THREADS) void select_topk_kernel(
+__global__ __launch_bounds__(SEL_THREADS, 4) void select_topk_kernel(
     const float* __restrict__ cand_dist, const uint32_t* __restrict__ cand_pos,
-    const uint32_t* __restrict__ cand_cnt, uint32_t cap, const uint32_t* __restrict__ ids,
-    uint32_t kprime, int sorted, u64* __restrict__ sl_key, uint32_t* __restrict__ sl_pos,
-    uint32_t* __restrict__ sl_cnt) {
+    const uint32_t* __restrict__ cand_cnt, uint32_t cap, uint32_t slots,
+    const uint32_t* __restrict__ ids, uint32_t kprime, int sorted, u64* __restrict__ sl_key,
+    uint32_t* __restrict__ sl_pos, uint32_t* __restrict__ sl_cnt) {
     extern __shared__ u64 skeys[];
     __shared__ uint32_t hist[NBINS];
-    __shared__ uint32_t s_bin, s_rank, s_out;
+    __shared__ uint32_t s_bin, s_rank, s_out, s_bincnt;
+    __shared__ u64 s_kth;
     const size_t q = blockIdx.x;
     const uint32_t n = min(cand_cnt[q], cap);
-    const uint32_t cap2 = cap;
-    uint32_t* spos = reinterpret_cast<uint32_t*>(skeys + cap2);
+    uint32_t* spos = reinterpret_cast<uint32_t*>(skeys + slots);
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         const uint32_t p = cand_pos[q * cap + i];
         skeys[i] = nb_key(cand_dist[q * cap + i], ids[p]);
@@ -169,11 +190,20 @@ __global__ __launch_bounds__(SEL_THREADS) void select_topk_kernel(
                 if (match) atomicAdd(&hist[(uint32_t)((k >> sh) & msk)], 1u);
             }
             __syncthreads();
-            find_bin(hist, r, &s_bin, &s_rank);
+            find_bin(hist, r, &s_bin, &s_rank, &s_bincnt);
             __syncthreads();
             prefix = (prefix << wd) | s_bin;
             r = s_rank;
             consumed += wd;
+            if (s_bincnt == 1 && consumed < 64) {
+                // the rank-th key is the only one left with this prefix
+                const int rem = 64 - consumed;
+                for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+                    if ((skeys[i] >> rem) == prefix) s_kth = skeys[i];
+                __syncthreads();
+                prefix = s_kth;
+                break;
+            }
             __syncthreads();
         }
         kth = prefix;
@@ -226,6 +256,7 @@ __device__ __forceinline__ float rerank_dist(const float* __restrict__ xs, uint3
                                              u64 nz) {
     if constexpr (FAST) {
         u64 s01 = 0, s23 = 0;
+#pragma unroll 8
         for (uint32_t t = 0; t < d; t += 4) {
             const uint32_t jj = t / ds, jr = t / dsr;
             const float4 c = __ldg(reinterpret_cast<const float4*>(crow + t));
@@ -258,7 +289,7 @@ __device__ __forceinline__ float rerank_dist(const float* __restrict__ xs, uint3
 }
 
 template <bool FAST>
-__global__ __launch_bounds__(256) void rerank_kernel(
+__global__ __launch_bounds__(256, 4) void rerank_kernel(
     const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
     const uint32_t* __restrict__ sl_cnt, uint32_t sl_stride, const float* __restrict__ xq, uint32_t d,
     const uint64_t* __restrict__ list_off, uint32_t nlists, const float* __restrict__ coarse,
@@ -335,27 +366,32 @@ void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uin
 }
 
 void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_off, uint32_t w,
-                             size_t nq, const uint8_t* query_sampled, uint32_t rank, float* tau,
-                             cudaStream_t s) {
+                             size_t nq, const uint8_t* query_sampled, uint32_t rank,
+                             uint32_t max_samples, float* tau, cudaStream_t s) {
     if (nq == 0) return;
-    sample_threshold_kernel<<<(unsigned)nq, SEL_THREADS, 0, s>>>(sample_dist, sample_off, w,
-                                                                  query_sampled, rank, tau);
+    const uint32_t stage_cap = std::min<uint32_t>(max_samples, 16 * 1024);
+    const size_t smem = (size_t)std::max<uint32_t>(stage_cap, 1) * sizeof(uint32_t);
+    set_smem((const void*)sample_threshold_kernel, smem);
+    sample_threshold_kernel<<<(unsigned)nq, SEL_THREADS, smem, s>>>(
+        sample_dist, sample_off, w, query_sampled, rank, stage_cap, tau);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }
 
 void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
-                        uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime, bool sorted,
-                        uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s) {
+                        uint32_t cap, uint32_t max_n, size_t nq, const uint32_t* ids,
+                        uint32_t kprime, bool sorted, uint64_t* sl_key, uint32_t* sl_pos,
+                        uint32_t* sl_cnt, cudaStream_t s) {
     if (nq == 0) return;
     uint32_t kp2 = 1;
     while (kp2 < kprime) kp2 <<= 1;
-    const uint32_t slots = std::max(cap, sorted ? kp2 : 0u);
+    // smem sized by the largest candidate set of this batch (max_n <= cap)
+    const uint32_t slots = std::max(std::max(std::min(max_n, cap), 1u), sorted ? kp2 : 0u);
     const size_t smem = (size_t)slots * (sizeof(u64) + sizeof(uint32_t));
     if (smem > 200 * 1024) throw ArgError("candidate capacity too large for the device selector");
     set_smem((const void*)select_topk_kernel, smem);
     select_topk_kernel<<<(unsigned)nq, SEL_THREADS, smem, s>>>(
-        cand_dist, cand_pos, cand_cnt, cap, ids, kprime, sorted ? 1 : 0,
+        cand_dist, cand_pos, cand_cnt, cap, slots, ids, kprime, sorted ? 1 : 0,
         reinterpret_cast<u64*>(sl_key), sl_pos, sl_cnt);
     PQRR_LAUNCH_CHECK();
     count_launch();

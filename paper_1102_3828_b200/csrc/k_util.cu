@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
 
 #include "common.cuh"
 #include "internal.h"
@@ -87,6 +88,23 @@ void sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* val
                                               (int64_t)n, 0, bits, s));
     PQRR_CUDA(cudaFreeAsync(d_tmp, s));
     count_launch(bits <= 8 ? 2 : 4);
+}
+
+void segmented_sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                          uint32_t* vals_out, size_t n, uint32_t nseg, const uint64_t* seg_begin,
+                          const uint64_t* seg_end, int bits, cudaStream_t s) {
+    if (n == 0 || nseg == 0) return;
+    size_t tmp = 0;
+    PQRR_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, keys_in, keys_out, vals_in,
+                                                       vals_out, (int64_t)n, (int64_t)nseg,
+                                                       seg_begin, seg_end, 0, bits, s));
+    void* d_tmp = nullptr;
+    PQRR_CUDA(cudaMallocAsync(&d_tmp, tmp, s));
+    PQRR_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(d_tmp, tmp, keys_in, keys_out, vals_in,
+                                                       vals_out, (int64_t)n, (int64_t)nseg,
+                                                       seg_begin, seg_end, 0, bits, s));
+    PQRR_CUDA(cudaFreeAsync(d_tmp, s));
+    count_launch(bits <= 8 ? 1 : 4);
 }
 
 void exclusive_scan_u64(const uint64_t* in, uint64_t* out, size_t n, cudaStream_t s) {

@@ -118,9 +118,12 @@ __global__ void iota_base_kernel(uint32_t* out, size_t n, uint32_t base) {
 }
 
 __global__ void check_fail_kernel(const uint8_t* __restrict__ sampled, const uint32_t* __restrict__ cnt,
-                                  size_t nq, uint32_t kprime, uint32_t cap, uint8_t* __restrict__ fail) {
+                                  size_t nq, uint32_t kprime, uint32_t cap, uint8_t* __restrict__ fail,
+                                  unsigned* __restrict__ max_n, unsigned long long* __restrict__ total) {
     size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
+    atomicMax(max_n, min(cnt[q], cap));
+    atomicAdd(total, (unsigned long long)cnt[q]);
     uint8_t f = 0;
     if (sampled[q]) {
         if (cnt[q] < kprime) f = 1;   // threshold too tight: shortlist may be incomplete
@@ -383,6 +386,32 @@ void finalize(DevIndex& ix) {
     }
     launch_layout_place_new(skeys, sidx, n, stage_off, d_off.p, d_oldlen.p, ix.st_codes.p,
                             ix.st_rcodes.p, ix.st_ids.p, ix.m, ix.mprime, codes.p, ids.p, rcodes.p, s);
+    if (ix.m == 8) {
+        // parity-balanced order inside every list (bank-conflict-free LUT gathers)
+        std::vector<uint64_t> h_end(c);
+        for (uint32_t l = 0; l < c; ++l) h_end[l] = new_off[l] + new_len[l];
+        uint64_t* d_end = ws.alloc<uint64_t>(c);
+        PQRR_CUDA(cudaMemcpyAsync(d_end, h_end.data(), c * 8, cudaMemcpyHostToDevice, s));
+        uint32_t* pk = ws.alloc<uint32_t>(acc);
+        uint32_t* pv = ws.alloc<uint32_t>(acc);
+        uint32_t* spk = ws.alloc<uint32_t>(acc);
+        uint32_t* spv = ws.alloc<uint32_t>(acc);
+        uint32_t* perm = ws.alloc<uint32_t>(acc);
+        launch_parity_keys(d_off.p, d_len.p, c, codes.p, pk, pv, s);
+        segmented_sort_pairs(pk, spk, pv, spv, acc, c, d_off.p, d_end, 8, s);
+        launch_pair_perm(d_off.p, d_len.p, c, spk, spv, perm, s);
+        DBuf<uint8_t> codes2, rcodes2;
+        DBuf<uint32_t> ids2;
+        codes2.alloc(acc * ix.m + 16);
+        ids2.alloc(acc + 1);
+        if (ix.mprime) rcodes2.alloc(acc * ix.mprime + 16);
+        launch_gather_layout(d_off.p, d_len.p, c, perm, codes.p, ids.p, rcodes.p, ix.m, ix.mprime,
+                             codes2.p, ids2.p, rcodes2.p, s);
+        PQRR_CUDA(cudaStreamSynchronize(s));
+        codes.swap(codes2);
+        ids.swap(ids2);
+        rcodes.swap(rcodes2);
+    }
     PQRR_CUDA(cudaStreamSynchronize(s));
     ix.codes.swap(codes);
     ix.rcodes.swap(rcodes);
@@ -462,14 +491,14 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     uint64_t* n_entries = ws.alloc<uint64_t>(nq);
     uint8_t* sampled = ws.alloc<uint8_t>(nq);
     uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
-    uint64_t* grand = ws.zeros<uint64_t>(1);
+    uint64_t* grand = ws.zeros<uint64_t>(2);
     launch_query_sizes(probes, nq, w, ix.list_len.p, stride, cap, n_entries, sampled, pair_samples,
                        grand, s);
     uint64_t* sample_off = ws.alloc<uint64_t>(P + 1);
     exclusive_scan_u64(pair_samples, sample_off, P + 1, s);
-    uint64_t total_samples = 0, scanned = 0;
+    uint64_t total_samples = 0, h_grand[2] = {0, 0};
     uint32_t n_items = 0;
-    PQRR_CUDA(cudaMemcpyAsync(&scanned, grand, 8, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaMemcpyAsync(h_grand, grand, 16, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&total_samples, sample_off + P, 8, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&n_items, item_off + c, 4, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaStreamSynchronize(s));
@@ -507,7 +536,8 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         launch_ivf_scan(a, s);
     }
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[3], s));
-    launch_sample_threshold(sample_dist, sample_off, w, nq, sampled, rank, tau, s);
+    launch_sample_threshold(sample_dist, sample_off, w, nq, sampled, rank, (uint32_t)h_grand[1],
+                            tau, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[4], s));
 
     // ---- K4 main scan
@@ -525,21 +555,29 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
 
     // ---- exactness check of the threshold
     uint8_t* fail = ws.alloc<uint8_t>(nq);
-    check_fail_kernel<<<nblk(nq), 256, 0, s>>>(sampled, cand_cnt, nq, kprime, cap, fail);
+    unsigned* maxn = ws.zeros<unsigned>(4);
+    check_fail_kernel<<<nblk(nq), 256, 0, s>>>(sampled, cand_cnt, nq, kprime, cap, fail, maxn,
+                                                reinterpret_cast<unsigned long long*>(maxn + 2));
     PQRR_LAUNCH_CHECK();
     count_launch();
     std::vector<uint8_t> h_fail(nq);
+    unsigned h_maxn[4] = {0, 0, 0, 0};
     PQRR_CUDA(cudaMemcpyAsync(h_fail.data(), fail, nq, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaMemcpyAsync(h_maxn, maxn, 16, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaStreamSynchronize(s));
+    uint64_t total_cand = 0;
+    std::memcpy(&total_cand, h_maxn + 2, 8);
 
     // ---- exact top-k' selection
-    launch_select_topk(cand_dist, cand_pos, cand_cnt, cap, nq, ix.ids.p, kprime, sorted,
+    launch_select_topk(cand_dist, cand_pos, cand_cnt, cap, h_maxn[0], nq, ix.ids.p, kprime, sorted,
                        reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[6], s));
     PQRR_CUDA(cudaStreamSynchronize(s));
     if (timed) {
+        st.candidates += total_cand;
         st.work_items += n_items;
         st.sampled_entries += total_samples;
-        st.scanned_entries += scanned;
+        st.scanned_entries += h_grand[0];
         st.stride = stride;
     }
 
@@ -996,11 +1034,29 @@ int pqrr_dev_export_lists(pqrr_dev_index* h, uint64_t* offsets, uint32_t* ids, u
         Workspace ws(ix.stream);
         uint64_t* d_uoff = ws.alloc<uint64_t>(ix.c + 1);
         PQRR_CUDA(cudaMemcpyAsync(d_uoff, uoff.data(), (ix.c + 1) * 8, cudaMemcpyHostToDevice, ix.stream));
+        // the device order inside a list is parity-balanced; the reference
+        // layout is id-ascending (ivf_index.hpp:15-16): re-sort per list
+        const size_t S = ix.slots;
+        std::vector<uint64_t> h_end(ix.c);
+        for (uint32_t l = 0; l < ix.c; ++l) h_end[l] = ix.h_off[l] + ix.h_len[l];
+        uint64_t* d_end = ws.alloc<uint64_t>(ix.c);
+        PQRR_CUDA(cudaMemcpyAsync(d_end, h_end.data(), ix.c * 8, cudaMemcpyHostToDevice, ix.stream));
+        uint32_t* k0 = ws.alloc<uint32_t>(S);
+        uint32_t* v0 = ws.alloc<uint32_t>(S);
+        uint32_t* k1 = ws.alloc<uint32_t>(S);
+        uint32_t* perm = ws.alloc<uint32_t>(S);
+        launch_list_id_keys(ix.list_off.p, ix.list_len.p, ix.c, ix.ids.p, k0, v0, ix.stream);
+        segmented_sort_pairs(k0, k1, v0, perm, S, ix.c, ix.list_off.p, d_end, 32, ix.stream);
+        uint32_t* t_ids = ws.alloc<uint32_t>(S);
+        uint8_t* t_codes = ws.alloc<uint8_t>(S * ix.m);
+        uint8_t* t_rcodes = ws.alloc<uint8_t>(S * std::max<uint32_t>(ix.mprime, 1));
+        launch_gather_layout(ix.list_off.p, ix.list_len.p, ix.c, perm, ix.codes.p, ix.ids.p,
+                             ix.rcodes.p, ix.m, ix.mprime, t_codes, t_ids, t_rcodes, ix.stream);
         uint32_t* o_ids = ws.alloc<uint32_t>(ix.n);
         uint8_t* o_codes = ws.alloc<uint8_t>(ix.n * ix.m);
         uint8_t* o_rcodes = ws.alloc<uint8_t>(ix.n * std::max<uint32_t>(ix.mprime, 1));
-        compact_lists_kernel<<<ix.c, 256, 0, ix.stream>>>(ix.list_off.p, ix.list_len.p, d_uoff, ix.ids.p,
-                                                         ix.codes.p, ix.rcodes.p, ix.m, ix.mprime,
+        compact_lists_kernel<<<ix.c, 256, 0, ix.stream>>>(ix.list_off.p, ix.list_len.p, d_uoff, t_ids,
+                                                         t_codes, t_rcodes, ix.m, ix.mprime,
                                                          o_ids, o_codes, o_rcodes);
         PQRR_LAUNCH_CHECK();
         count_launch();
