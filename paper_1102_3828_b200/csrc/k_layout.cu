@@ -78,50 +78,103 @@ __global__ void parity_keys_kernel(const uint64_t* __restrict__ off, const uint3
     }
 }
 
-// One CTA per list: the list's entries sorted (stably) by parity vector v are
-// re-laid out as complementary pairs (v, ~v) first — every aligned group of 8
-// entries then has exactly 4 even and 4 odd bytes for every sub-quantizer, so
-// each LDS.128 of the scanner is 4 conflict-free wavefronts — then leftovers.
+// XOR masks of 8 bits ordered by decreasing popcount (Hamming distance 8..1).
+__constant__ uint8_t c_masks[255];
+__constant__ uint16_t c_mask_off[10];  // masks with popcount d: [c_mask_off[8-d], c_mask_off[9-d])
+
+// One CTA per list: the scanner's LDS.128 is served in quarter-warp phases of
+// 8 lanes = 2 consecutive entries (measured: tools/microbench/lds128.cu), so a
+// phase is conflict-free in sub-quantizer j iff the two entries' code bytes
+// differ in parity.  The list's entries, stably sorted by parity vector v, are
+// matched greedily into pairs of maximal Hamming distance (complements first,
+// then distance 7, ...), pairs laid out at even offsets, same-bucket leftovers
+// last.  Every bucket-pair step exhausts a bucket, so the plan has <= 512 rows.
 __global__ void pair_perm_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
                                  const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
                                  uint32_t* __restrict__ perm) {
-    __shared__ uint32_t cnt[256], start[256], pair_off[128], left_off[256];
-    __shared__ uint32_t s_pairs_total;
+    __shared__ uint32_t cnt[256], start[256], taken[256];
+    __shared__ uint32_t p_a[512], p_b[512], p_k[512], p_out[512];
+    __shared__ uint32_t s_np;
     const uint32_t l = blockIdx.x;
     const uint64_t o = off[l];
     const uint32_t n = len[l];
-    for (uint32_t v = threadIdx.x; v < 256; v += blockDim.x) cnt[v] = 0;
+    for (uint32_t v = threadIdx.x; v < 256; v += blockDim.x) {
+        cnt[v] = 0;
+        taken[v] = 0;
+    }
     __syncthreads();
     for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) atomicAdd(&cnt[skeys[o + r]], 1u);
     __syncthreads();
     if (threadIdx.x == 0) {
-        uint32_t acc = 0, pacc = 0;
+        uint32_t acc = 0;
         for (uint32_t v = 0; v < 256; ++v) {
             start[v] = acc;
             acc += cnt[v];
         }
-        for (uint32_t v = 0; v < 128; ++v) {
-            pair_off[v] = pacc;
-            pacc += 2 * min(cnt[v], cnt[255 - v]);
+        uint32_t out = 0, np = 0;
+        for (int d = 8; d >= 1; --d) {
+            const uint32_t m0 = c_mask_off[8 - d], m1 = c_mask_off[9 - d];
+            for (uint32_t v = 0; v < 256; ++v) {
+                for (uint32_t mi = m0; mi < m1 && taken[v] < cnt[v]; ++mi) {
+                    const uint32_t u = v ^ c_masks[mi];
+                    const uint32_t k = min(cnt[v] - taken[v], cnt[u] - taken[u]);
+                    if (k == 0) continue;
+                    p_a[np] = start[v] + taken[v];
+                    p_b[np] = start[u] + taken[u];
+                    p_k[np] = k;
+                    p_out[np] = out;
+                    ++np;
+                    out += 2 * k;
+                    taken[v] += k;
+                    taken[u] += k;
+                }
+            }
         }
-        s_pairs_total = pacc;
-        uint32_t lacc = pacc;
-        for (uint32_t v = 0; v < 256; ++v) {
-            left_off[v] = lacc;
-            const uint32_t p = min(cnt[v], cnt[255 - v]);
-            lacc += cnt[v] - p;
+        for (uint32_t v = 0; v < 256; ++v) {  // same-bucket leftovers
+            const uint32_t k = cnt[v] - taken[v];
+            if (!k) continue;
+            p_a[np] = start[v] + taken[v];
+            p_b[np] = 0xffffffffu;
+            p_k[np] = k;
+            p_out[np] = out;
+            ++np;
+            out += k;
         }
+        s_np = np;
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const uint32_t v = skeys[o + i];
-        const uint32_t r = i - start[v];
-        const uint32_t p = min(cnt[v], cnt[255 - v]);
-        uint32_t dst;
-        if (r < p) dst = v < 128 ? pair_off[v] + 2 * r : pair_off[255 - v] + 2 * r + 1;
-        else dst = left_off[v] + (r - p);
-        perm[o + dst] = svals[o + i];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (uint32_t p = warp; p < s_np; p += nw) {
+        const uint32_t a = p_a[p], b = p_b[p], k = p_k[p], dst = p_out[p];
+        for (uint32_t i = lane; i < k; i += 32) {
+            if (b == 0xffffffffu) {
+                perm[o + dst + i] = svals[o + a + i];
+            } else {
+                perm[o + dst + 2 * i] = svals[o + a + i];
+                perm[o + dst + 2 * i + 1] = svals[o + b + i];
+            }
+        }
     }
+}
+
+void upload_masks() {
+    static int done_dev[64] = {0};
+    int dev = 0;
+    PQRR_CUDA(cudaGetDevice(&dev));
+    if (dev < 64 && done_dev[dev]) return;
+    uint8_t masks[255];
+    uint16_t moff[10];
+    int k = 0;
+    for (int d = 8; d >= 1; --d) {
+        moff[8 - d] = (uint16_t)k;
+        for (int m = 1; m < 256; ++m)
+            if (__builtin_popcount(m) == d) masks[k++] = (uint8_t)m;
+    }
+    moff[8] = (uint16_t)k;
+    moff[9] = (uint16_t)k;
+    PQRR_CUDA(cudaMemcpyToSymbol(c_masks, masks, sizeof(masks)));
+    PQRR_CUDA(cudaMemcpyToSymbol(c_mask_off, moff, sizeof(moff)));
+    if (dev < 64) done_dev[dev] = 1;
 }
 
 __global__ void gather_layout_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
@@ -168,6 +221,7 @@ void launch_list_id_keys(const uint64_t* off, const uint32_t* len, uint32_t nlis
 
 void launch_pair_perm(const uint64_t* off, const uint32_t* len, uint32_t nlists,
                       const uint32_t* skeys, const uint32_t* svals, uint32_t* perm, cudaStream_t s) {
+    upload_masks();
     pair_perm_kernel<<<nlists, 256, 0, s>>>(off, len, skeys, svals, perm);
     PQRR_LAUNCH_CHECK();
     count_launch();
