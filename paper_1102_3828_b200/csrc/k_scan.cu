@@ -29,34 +29,67 @@ constexpr int NT = kScanThreads;
 constexpr int NW = NT / 32;
 constexpr int LUT_FLOATS = M * KS * QT;  // 32768 floats = 128 KiB
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// Sub-codebook j (KS x DSUB floats) -> smem buffer, 16 B per cp.async.
+template <int DSUB>
+__device__ __forceinline__ void stage_book(float* __restrict__ dst, const float* __restrict__ books,
+                                           int j) {
+    constexpr int CH = KS * DSUB / 4;  // 16-byte chunks
+    const float* src = books + (size_t)j * KS * DSUB;
+    for (int c = threadIdx.x; c < CH; c += NT) cp_async16(dst + 4 * c, src + 4 * c);
+    cp_async_commit();
+}
+
+// LUT[j][i][q] for the item's 16 queries.  B_j is double-buffered in shared
+// memory (cp.async of B_{j+1} overlaps the arithmetic of j); every warp reads 2
+// distinct centroid rows per LDS.128 (broadcast) and writes 32 contiguous LUT
+// words.
 template <int DSUB>
 __device__ __forceinline__ void build_luts(float* __restrict__ lut, const float* __restrict__ xr,
-                                           int xld, const float* __restrict__ books, u64 nz) {
+                                           int xld, const float* __restrict__ books,
+                                           float* __restrict__ bbuf, u64 nz) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int qq = lane & 15, ih = lane >> 4;
+    constexpr int BF = KS * DSUB;
+    stage_book<DSUB>(bbuf, books, 0);
 #pragma unroll 1
     for (int j = 0; j < M; ++j) {
+        if (j + 1 < M) {
+            stage_book<DSUB>(bbuf + ((j + 1) & 1) * BF, books, j + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float* bj = bbuf + (j & 1) * BF;
         float r[DSUB];
 #pragma unroll
         for (int t = 0; t < DSUB; t += 4) {
             float4 v = *reinterpret_cast<const float4*>(xr + qq * xld + j * DSUB + t);
             r[t] = v.x; r[t + 1] = v.y; r[t + 2] = v.z; r[t + 3] = v.w;
         }
-        const float* bj = books + (size_t)j * KS * DSUB;
 #pragma unroll
         for (int ib = 0; ib < KS / (2 * NW); ++ib) {
             const int i = (ib * NW + warp) * 2 + ih;
-            const float* b = bj + (size_t)i * DSUB;
+            const float* b = bj + i * DSUB;
             u64 s01 = 0, s23 = 0;
 #pragma unroll
             for (int t = 0; t < DSUB; t += 4) {
-                const float4 c = __ldg(reinterpret_cast<const float4*>(b + t));
+                const float4 c = *reinterpret_cast<const float4*>(b + t);
                 s01 = acc_sq2(s01, pk2(r[t], r[t + 1]), pk2(c.x, c.y), nz);
                 s23 = acc_sq2(s23, pk2(r[t + 2], r[t + 3]), pk2(c.z, c.w), nz);
             }
             lut[(j * KS + i) * QT + qq] =
                 __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
         }
+        __syncthreads();  // buffer (j & 1) is refilled by the prefetch of j + 2
     }
 }
 
@@ -85,7 +118,8 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
     extern __shared__ float4 smem4[];
     float* lut = reinterpret_cast<float*>(smem4);
     const int xld = (int)a.d + 4;
-    float* xr = lut + LUT_FLOATS;  // [QT][d + 4]
+    float* xr = lut + LUT_FLOATS;         // [QT][d + 4]
+    float* bbuf = xr + QT * xld;          // [2][KS][DSUB] sub-codebook ring
     __shared__ uint32_t s_item;
     __shared__ int s_q[QT];
     __shared__ uint32_t s_pair[QT];
@@ -126,8 +160,7 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
             xr[qq * xld + t] = q >= 0 ? __fsub_rn(a.xq[(size_t)q * a.d + t], crow[t]) : 0.f;
         }
         __syncthreads();
-        build_luts<DSUB>(lut, xr, xld, a.books, nz);
-        __syncthreads();
+        build_luts<DSUB>(lut, xr, xld, a.books, bbuf, nz);
 
         const uint64_t off = a.list_off[l];
         const uint32_t len = a.list_len[l];
@@ -266,7 +299,8 @@ __global__ void items_build_kernel(const uint32_t* __restrict__ cnt,
 
 template <int DSUB>
 void scan_t(const ScanArgs& a, cudaStream_t s) {
-    const size_t smem = (size_t)LUT_FLOATS * sizeof(float) + (size_t)QT * (a.d + 4) * sizeof(float);
+    const size_t smem = (size_t)LUT_FLOATS * sizeof(float) + (size_t)QT * (a.d + 4) * sizeof(float) +
+                        2 * (size_t)KS * DSUB * sizeof(float);
     PQRR_CUDA(cudaFuncSetAttribute(ivf_scan_kernel<DSUB>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ivf_scan_kernel<DSUB><<<sm_count(), NT, smem, s>>>(a, kNegZero2);

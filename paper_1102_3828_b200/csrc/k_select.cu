@@ -289,7 +289,7 @@ __device__ __forceinline__ float rerank_dist(const float* __restrict__ xs, uint3
 }
 
 template <bool FAST>
-__global__ __launch_bounds__(256, 4) void rerank_kernel(
+__global__ __launch_bounds__(256, 3) void rerank_kernel(
     const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
     const uint32_t* __restrict__ sl_cnt, uint32_t sl_stride, const float* __restrict__ xq, uint32_t d,
     const uint64_t* __restrict__ list_off, uint32_t nlists, const float* __restrict__ coarse,
@@ -308,17 +308,24 @@ __global__ __launch_bounds__(256, 4) void rerank_kernel(
     while (n2 < n) n2 <<= 1;
     __syncthreads();
     const uint32_t ds = d / m, dsr = d / mprime;
-    for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
-        if (i >= n) {
-            keys[i] = ~0ull;
-            continue;
-        }
-        const uint32_t p = sl_pos[q * sl_stride + i];
-        const uint32_t id = key_id(sl_key[q * sl_stride + i]);
-        const uint32_t l = list_of_pos(list_off, nlists, p);
-        const float dist = rerank_dist<FAST>(xs, d, coarse + (size_t)l * d, books, codes + (size_t)p * m, ds,
-                                             rbooks, rcodes + (size_t)p * mprime, dsr, ks, nz);
-        keys[i] = nb_key(dist, id);
+    for (uint32_t i = n + threadIdx.x; i < n2; i += blockDim.x) keys[i] = ~0ull;
+    // two candidates per thread in flight: their gathers (position, list
+    // search, code bytes, centroid rows) overlap
+    for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 2 * blockDim.x) {
+        const uint32_t i1 = i0 + blockDim.x;
+        const bool has1 = i1 < n;
+        const uint32_t p0 = sl_pos[q * sl_stride + i0];
+        const uint32_t p1 = has1 ? sl_pos[q * sl_stride + i1] : p0;
+        const uint32_t id0 = key_id(sl_key[q * sl_stride + i0]);
+        const uint32_t id1 = has1 ? key_id(sl_key[q * sl_stride + i1]) : 0u;
+        const uint32_t l0 = list_of_pos(list_off, nlists, p0);
+        const uint32_t l1 = list_of_pos(list_off, nlists, p1);
+        const float d0 = rerank_dist<FAST>(xs, d, coarse + (size_t)l0 * d, books, codes + (size_t)p0 * m, ds,
+                                           rbooks, rcodes + (size_t)p0 * mprime, dsr, ks, nz);
+        const float d1 = rerank_dist<FAST>(xs, d, coarse + (size_t)l1 * d, books, codes + (size_t)p1 * m, ds,
+                                           rbooks, rcodes + (size_t)p1 * mprime, dsr, ks, nz);
+        keys[i0] = nb_key(d0, id0);
+        if (has1) keys[i1] = nb_key(d1, id1);
     }
     __syncthreads();
     bitonic_sort_kv(keys, nullptr, n2);
