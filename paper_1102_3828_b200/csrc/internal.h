@@ -130,6 +130,9 @@ struct ScanArgs {
     const uint32_t* item_list;
     const uint32_t* item_start;  // into pair_sorted
     const uint32_t* item_nq;
+    const uint32_t* item_e0;     // entry range of the list covered by the item
+    const uint32_t* item_e1;
+    const uint32_t* item_order;  // items sorted longest first
     const uint32_t* num_items;   // device scalar
     uint32_t* item_counter;      // device scalar, zeroed before launch
     const uint32_t* pair_sorted;  // pair index q * w + r, grouped by list
@@ -149,11 +152,12 @@ struct ScanArgs {
 void launch_ivf_scan(const ScanArgs& a, cudaStream_t s);
 
 // Build the scan work items from the probes.
-void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first, uint32_t nlists,
-                        const uint32_t* item_off, uint32_t* item_list, uint32_t* item_start,
-                        uint32_t* item_nq, cudaStream_t s);
-void launch_items_per_list(const uint32_t* list_cnt, uint32_t nlists, uint32_t* items,
-                           cudaStream_t s);
+void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,
+                        const uint32_t* list_len, uint32_t nlists, const uint32_t* item_off,
+                        uint32_t* item_list, uint32_t* item_start, uint32_t* item_nq,
+                        uint32_t* item_e0, uint32_t* item_e1, uint32_t* sort_key, cudaStream_t s);
+void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, uint32_t nlists,
+                           uint32_t* items, cudaStream_t s);
 // Per query: N_q = sum of probed list lengths; per pair sample counts.
 void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
                         uint32_t stride, uint32_t cap, uint64_t* nq_entries,

@@ -132,11 +132,15 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
     const float4* lut4 = reinterpret_cast<const float4*>(lut);
 
     for (;;) {
-        if (threadIdx.x == 0) s_item = atomicAdd(a.item_counter, 1u);
+        if (threadIdx.x == 0) {
+            const uint32_t c = atomicAdd(a.item_counter, 1u);
+            s_item = c < n_items ? a.item_order[c] : 0xffffffffu;  // longest items first
+        }
         __syncthreads();
         const uint32_t it = s_item;
-        if (it >= n_items) break;
+        if (it == 0xffffffffu) break;
         const uint32_t l = a.item_list[it];
+        const uint32_t e0 = a.item_e0[it], e1 = a.item_e1[it];
         const uint32_t start = a.item_start[it];
         const uint32_t nqi = a.item_nq[it];
         if (threadIdx.x < QT) {
@@ -162,8 +166,9 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
         __syncthreads();
         build_luts<DSUB>(lut, xr, xld, a.books, bbuf, nz);
 
-        const uint64_t off = a.list_off[l];
-        const uint32_t len = a.list_len[l];
+        // this item's entry range [e0, e1) of the list (long lists are chunked)
+        const uint64_t off = a.list_off[l] + e0;
+        const uint32_t len = e1 - e0;
         const u64* codes = reinterpret_cast<const u64*>(a.codes) + off;
         int qk[4];
         float tk[4];
@@ -220,7 +225,7 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
             }
         } else {
             // ---------------- sample mode: every stride-th entry, fixed slots
-            const uint32_t ns = (len + a.stride - 1) / a.stride;
+            const uint32_t ns = (e1 + a.stride - 1) / a.stride - (e0 + a.stride - 1) / a.stride;
             uint64_t sbase[4];
             bool sw[4];
 #pragma unroll
@@ -228,23 +233,43 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
                 sw[k] = qk[k] >= 0 && s_samp[qd * 4 + k];
                 sbase[k] = sw[k] ? a.sample_off[s_pair[qd * 4 + k]] : 0;
             }
-            for (uint32_t base = warp * 8; base < ns; base += NW * 8) {
-                const uint32_t si = base + slot;
-                if (si >= ns) continue;
-                const u64 code = __ldg(codes + (size_t)si * a.stride);
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            // sampled entries of the chunk: global indices i * stride in [e0, e1),
+            // written at their fixed per-(query, probe) slot i
+            const uint32_t i0 = (e0 + a.stride - 1) / a.stride;
+            const u64* lcodes = reinterpret_cast<const u64*>(a.codes) + a.list_off[l];
+            constexpr uint32_t S = NW * 8;
+            constexpr int PF = 4;
+            const uint32_t wbase = warp * 8;
+            u64 cbuf[PF];
 #pragma unroll
-                for (int j = 0; j < M; ++j) {
-                    const uint32_t c = (uint32_t)(code >> (8 * j)) & 0xffu;
-                    const float4 v = lut4[(j * KS + c) * (QT / 4) + qd];
-                    acc[0] = __fadd_rn(acc[0], v.x);
-                    acc[1] = __fadd_rn(acc[1], v.y);
-                    acc[2] = __fadd_rn(acc[2], v.z);
-                    acc[3] = __fadd_rn(acc[3], v.w);
+            for (int k = 0; k < PF; ++k) {
+                const uint32_t si = wbase + k * S + slot;
+                cbuf[k] = si < ns ? __ldg(lcodes + (size_t)(i0 + si) * a.stride) : 0ull;
+            }
+            for (uint32_t wb = wbase; wb < ns; wb += PF * S) {
+#pragma unroll
+                for (int kk = 0; kk < PF; ++kk) {
+                    const uint32_t sb = wb + kk * S;
+                    if (sb >= ns) break;
+                    const uint32_t si = sb + slot;
+                    const u64 code = cbuf[kk];
+                    const uint32_t sn = si + PF * S;
+                    cbuf[kk] = sn < ns ? __ldg(lcodes + (size_t)(i0 + sn) * a.stride) : 0ull;
+                    if (si >= ns) continue;
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int j = 0; j < M; ++j) {
+                        const uint32_t c = (uint32_t)(code >> (8 * j)) & 0xffu;
+                        const float4 v = lut4[(j * KS + c) * (QT / 4) + qd];
+                        acc[0] = __fadd_rn(acc[0], v.x);
+                        acc[1] = __fadd_rn(acc[1], v.y);
+                        acc[2] = __fadd_rn(acc[2], v.z);
+                        acc[3] = __fadd_rn(acc[3], v.w);
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (sw[k]) a.sample_dist[sbase[k] + i0 + si] = acc[k];
                 }
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (sw[k]) a.sample_dist[sbase[k] + si] = acc[k];
             }
         }
         __syncthreads();
@@ -274,26 +299,44 @@ __global__ void build_lut_kernel(const float* __restrict__ xr, size_t nx, uint32
     out[idx] = l2sq_scalar(xr + v * d + (size_t)j * ds, books + ((size_t)j * ks + i) * ds, (int)ds);
 }
 
-__global__ void items_per_list_kernel(const uint32_t* __restrict__ cnt, uint32_t nlists,
+// Work items: (list, group of <= 16 probing queries, chunk of <= kChunk
+// entries).  Chunking bounds the longest item so the longest-first schedule
+// below leaves no tail of one huge list on one SM.
+constexpr uint32_t kChunk = 32768;
+
+__global__ void items_per_list_kernel(const uint32_t* __restrict__ cnt,
+                                      const uint32_t* __restrict__ len, uint32_t nlists,
                                       uint32_t* __restrict__ items) {
     uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l < nlists) items[l] = (cnt[l] + QT - 1) / QT;
+    if (l < nlists) {
+        const uint32_t chunks = max(1u, (len[l] + kChunk - 1) / kChunk);
+        items[l] = ((cnt[l] + QT - 1) / QT) * chunks;
+    }
     if (l == nlists) items[l] = 0;
 }
 
 __global__ void items_build_kernel(const uint32_t* __restrict__ cnt,
-                                   const uint32_t* __restrict__ first, uint32_t nlists,
+                                   const uint32_t* __restrict__ first,
+                                   const uint32_t* __restrict__ len, uint32_t nlists,
                                    const uint32_t* __restrict__ item_off,
                                    uint32_t* __restrict__ item_list, uint32_t* __restrict__ item_start,
-                                   uint32_t* __restrict__ item_nq) {
+                                   uint32_t* __restrict__ item_nq, uint32_t* __restrict__ item_e0,
+                                   uint32_t* __restrict__ item_e1, uint32_t* __restrict__ sort_key) {
     uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= nlists) return;
-    const uint32_t c = cnt[l];
+    const uint32_t c = cnt[l], L = len[l];
+    const uint32_t chunks = max(1u, (L + kChunk - 1) / kChunk);
     uint32_t o = item_off[l];
-    for (uint32_t s = 0; s < c; s += QT, ++o) {
-        item_list[o] = l;
-        item_start[o] = first[l] + s;
-        item_nq[o] = min((uint32_t)QT, c - s);
+    for (uint32_t s = 0; s < c; s += QT) {
+        for (uint32_t ch = 0; ch < chunks; ++ch, ++o) {
+            const uint32_t e0 = ch * kChunk, e1 = min(L, e0 + kChunk);
+            item_list[o] = l;
+            item_start[o] = first[l] + s;
+            item_nq[o] = min((uint32_t)QT, c - s);
+            item_e0[o] = e0;
+            item_e1[o] = e1;
+            sort_key[o] = 0xffffffffu - (e1 - e0);  // ascending sort = longest first
+        }
     }
 }
 
@@ -321,18 +364,20 @@ void launch_ivf_scan(const ScanArgs& a, cudaStream_t s) {
     }
 }
 
-void launch_items_per_list(const uint32_t* list_cnt, uint32_t nlists, uint32_t* items,
-                           cudaStream_t s) {
-    items_per_list_kernel<<<(nlists + 1 + 255) / 256, 256, 0, s>>>(list_cnt, nlists, items);
+void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, uint32_t nlists,
+                           uint32_t* items, cudaStream_t s) {
+    items_per_list_kernel<<<(nlists + 1 + 255) / 256, 256, 0, s>>>(list_cnt, list_len, nlists, items);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }
 
-void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first, uint32_t nlists,
-                        const uint32_t* item_off, uint32_t* item_list, uint32_t* item_start,
-                        uint32_t* item_nq, cudaStream_t s) {
-    items_build_kernel<<<(nlists + 255) / 256, 256, 0, s>>>(list_cnt, list_first, nlists, item_off,
-                                                            item_list, item_start, item_nq);
+void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,
+                        const uint32_t* list_len, uint32_t nlists, const uint32_t* item_off,
+                        uint32_t* item_list, uint32_t* item_start, uint32_t* item_nq,
+                        uint32_t* item_e0, uint32_t* item_e1, uint32_t* sort_key, cudaStream_t s) {
+    items_build_kernel<<<(nlists + 255) / 256, 256, 0, s>>>(list_cnt, list_first, list_len, nlists,
+                                                            item_off, item_list, item_start, item_nq,
+                                                            item_e0, item_e1, sort_key);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

@@ -481,13 +481,9 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     uint32_t* list_first = ws.alloc<uint32_t>(c + 1);
     exclusive_scan_u32(list_cnt, list_first, c + 1, s);
     uint32_t* items = ws.alloc<uint32_t>(c + 1);
-    launch_items_per_list(list_cnt, c, items, s);
+    launch_items_per_list(list_cnt, ix.list_len.p, c, items, s);
     uint32_t* item_off = ws.alloc<uint32_t>(c + 1);
     exclusive_scan_u32(items, item_off, c + 1, s);
-    uint32_t* item_list = ws.alloc<uint32_t>(P);
-    uint32_t* item_start = ws.alloc<uint32_t>(P);
-    uint32_t* item_nq = ws.alloc<uint32_t>(P);
-    launch_items_build(list_cnt, list_first, c, item_off, item_list, item_start, item_nq, s);
     uint64_t* n_entries = ws.alloc<uint64_t>(nq);
     uint8_t* sampled = ws.alloc<uint8_t>(nq);
     uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
@@ -502,6 +498,20 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     PQRR_CUDA(cudaMemcpyAsync(&total_samples, sample_off + P, 8, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&n_items, item_off + c, 4, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaStreamSynchronize(s));
+    // items: (list, query group, entry chunk), scheduled longest first
+    uint32_t* item_list = ws.alloc<uint32_t>(n_items);
+    uint32_t* item_start = ws.alloc<uint32_t>(n_items);
+    uint32_t* item_nq = ws.alloc<uint32_t>(n_items);
+    uint32_t* item_e0 = ws.alloc<uint32_t>(n_items);
+    uint32_t* item_e1 = ws.alloc<uint32_t>(n_items);
+    uint32_t* item_key = ws.alloc<uint32_t>(n_items);
+    uint32_t* item_key2 = ws.alloc<uint32_t>(n_items);
+    uint32_t* item_iota = ws.alloc<uint32_t>(n_items);
+    uint32_t* item_order = ws.alloc<uint32_t>(n_items);
+    launch_items_build(list_cnt, list_first, ix.list_len.p, c, item_off, item_list, item_start,
+                       item_nq, item_e0, item_e1, item_key, s);
+    launch_iota(item_iota, n_items, s);
+    sort_pairs(item_key, item_key2, item_iota, item_order, n_items, 32, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[2], s));
 
     ScanArgs a{};
@@ -517,6 +527,9 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     a.item_list = item_list;
     a.item_start = item_start;
     a.item_nq = item_nq;
+    a.item_e0 = item_e0;
+    a.item_e1 = item_e1;
+    a.item_order = item_order;
     a.num_items = item_off + c;
     a.pair_sorted = pair_sorted;
     a.w = w;
