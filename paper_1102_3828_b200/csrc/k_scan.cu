@@ -113,6 +113,18 @@ __device__ __forceinline__ void emit(bool hit, int q, float dist, uint32_t pos, 
     }
 }
 
+// Plain per-lane append (hits are rare after the threshold: ~2k' per query).
+__device__ __forceinline__ void emit1(bool hit, int q, float dist, uint32_t pos,
+                                      uint32_t* __restrict__ cnt, float* __restrict__ cdist,
+                                      uint32_t* __restrict__ cpos, uint32_t cap) {
+    if (!hit) return;
+    const unsigned slot = atomicAdd(cnt + q, 1u);
+    if (slot < cap) {
+        cdist[(size_t)q * cap + slot] = dist;
+        cpos[(size_t)q * cap + slot] = pos;
+    }
+}
+
 template <int DSUB>
 __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const u64 nz) {
     extern __shared__ float4 smem4[];
@@ -181,46 +193,57 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
             // ---------------- main mode: threshold filter + append.  Codes are
             // prefetched PF steps ahead in registers so the L2/HBM latency of
             // the stream hides behind the LUT gathers of earlier steps.
+            // Two entry-steps (A, B = A + S) per iteration: 8 independent
+            // j-ordered FADD chains per lane and one vote per two steps.
             constexpr uint32_t S = NW * 8;  // entries per CTA step
-            constexpr int PF = 4;
             const uint32_t wbase = warp * 8;
-            u64 cbuf[PF];
-#pragma unroll
-            for (int k = 0; k < PF; ++k) {
-                const uint32_t e = wbase + k * S + slot;
-                cbuf[k] = e < len ? __ldg(codes + e) : 0ull;
+            u64 nA = 0ull, nB = 0ull, fA = 0ull, fB = 0ull;
+            {
+                const uint32_t e = wbase + slot;
+                nA = e < len ? __ldg(codes + e) : 0ull;
+                nB = e + S < len ? __ldg(codes + e + S) : 0ull;
+                fA = e + 2 * S < len ? __ldg(codes + e + 2 * S) : 0ull;
+                fB = e + 3 * S < len ? __ldg(codes + e + 3 * S) : 0ull;
             }
-            for (uint32_t wb = wbase; wb < len; wb += PF * S) {
+            for (uint32_t wb = wbase; wb < len; wb += 2 * S) {
+                const uint32_t eA = wb + slot, eB = eA + S;
+                const bool vA = eA < len, vB = eB < len;
+                const u64 cA = nA, cB = nB;
+                nA = fA;
+                nB = fB;
+                fA = eA + 4 * S < len ? __ldg(codes + eA + 4 * S) : 0ull;
+                fB = eB + 4 * S < len ? __ldg(codes + eB + 4 * S) : 0ull;
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+                float b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
 #pragma unroll
-                for (int k = 0; k < PF; ++k) {
-                    const uint32_t eb = wb + k * S;
-                    if (eb >= len) break;  // warp-uniform
-                    const uint32_t e = eb + slot;
-                    const bool valid = e < len;
-                    const u64 code = cbuf[k];
-                    const uint32_t en = e + PF * S;
-                    cbuf[k] = en < len ? __ldg(codes + en) : 0ull;
-                    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-#pragma unroll
-                    for (int j = 0; j < M; ++j) {
-                        const uint32_t c = (uint32_t)(code >> (8 * j)) & 0xffu;
-                        const float4 v = lut4[(j * KS + c) * (QT / 4) + qd];
-                        acc0 = __fadd_rn(acc0, v.x);
-                        acc1 = __fadd_rn(acc1, v.y);
-                        acc2 = __fadd_rn(acc2, v.z);
-                        acc3 = __fadd_rn(acc3, v.w);
-                    }
-                    const bool h0 = valid && acc0 <= tk[0];
-                    const bool h1 = valid && acc1 <= tk[1];
-                    const bool h2 = valid && acc2 <= tk[2];
-                    const bool h3 = valid && acc3 <= tk[3];
-                    if (__any_sync(0xffffffffu, h0 | h1 | h2 | h3)) {
-                        const uint32_t pos = (uint32_t)(off + e);
-                        emit(h0, qk[0], acc0, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
-                        emit(h1, qk[1], acc1, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
-                        emit(h2, qk[2], acc2, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
-                        emit(h3, qk[3], acc3, pos, lane, qd, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
-                    }
+                for (int j = 0; j < M; ++j) {
+                    const uint32_t ca = (uint32_t)(cA >> (8 * j)) & 0xffu;
+                    const uint32_t cb = (uint32_t)(cB >> (8 * j)) & 0xffu;
+                    const float4 va = lut4[(j * KS + ca) * (QT / 4) + qd];
+                    const float4 vb = lut4[(j * KS + cb) * (QT / 4) + qd];
+                    a0 = __fadd_rn(a0, va.x);
+                    a1 = __fadd_rn(a1, va.y);
+                    a2 = __fadd_rn(a2, va.z);
+                    a3 = __fadd_rn(a3, va.w);
+                    b0 = __fadd_rn(b0, vb.x);
+                    b1 = __fadd_rn(b1, vb.y);
+                    b2 = __fadd_rn(b2, vb.z);
+                    b3 = __fadd_rn(b3, vb.w);
+                }
+                const bool hA0 = vA && a0 <= tk[0], hA1 = vA && a1 <= tk[1];
+                const bool hA2 = vA && a2 <= tk[2], hA3 = vA && a3 <= tk[3];
+                const bool hB0 = vB && b0 <= tk[0], hB1 = vB && b1 <= tk[1];
+                const bool hB2 = vB && b2 <= tk[2], hB3 = vB && b3 <= tk[3];
+                if (__any_sync(0xffffffffu, hA0 | hA1 | hA2 | hA3 | hB0 | hB1 | hB2 | hB3)) {
+                    const uint32_t pA = (uint32_t)(off + eA), pB = (uint32_t)(off + eB);
+                    emit1(hA0, qk[0], a0, pA, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                    emit1(hA1, qk[1], a1, pA, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                    emit1(hA2, qk[2], a2, pA, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                    emit1(hA3, qk[3], a3, pA, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                    emit1(hB0, qk[0], b0, pB, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                    emit1(hB1, qk[1], b1, pB, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                    emit1(hB2, qk[2], b2, pB, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
+                    emit1(hB3, qk[3], b3, pB, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
                 }
             }
         } else {
