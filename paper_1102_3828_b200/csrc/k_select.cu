@@ -338,6 +338,92 @@ __global__ __launch_bounds__(256, 3) void rerank_kernel(
     if (threadIdx.x == 0) out_cnt[q] = cnt;
 }
 
+// Warp-cooperative re-ranker for d = 128 (dsub, dsub' multiples of 4): lane t
+// owns dims 4t..4t+3, so the centroid / code-book rows of one candidate are
+// read as coalesced 512 B / 64 B / 32 B segments instead of 32 scattered rows.
+// The exact reference order of l2_sq (s_k += t_{4g+k}^2 for g = 0..31 in
+// order, distance.hpp:16-33) is kept by transposing the squared differences of
+// 32 candidates through shared memory: lane c then sums candidate c's 32
+// groups sequentially.
+constexpr int RW_WARPS = 4;
+constexpr int RW_LD = 33;  // padded float4 row of the transpose tile
+
+__global__ __launch_bounds__(RW_WARPS * 32) void rerank_warp_kernel(
+    const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
+    const uint32_t* __restrict__ sl_cnt, uint32_t sl_stride, const float* __restrict__ xq,
+    const uint64_t* __restrict__ list_off, uint32_t nlists, const float* __restrict__ coarse,
+    const uint8_t* __restrict__ codes, const float* __restrict__ books, uint32_t m,
+    const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks, uint32_t mprime,
+    uint32_t ks, uint32_t k, uint32_t* __restrict__ out_ids, float* __restrict__ out_dists,
+    uint32_t* __restrict__ out_cnt) {
+    constexpr uint32_t D = 128;
+    extern __shared__ float4 rw_smem[];
+    float4* tiles = rw_smem;                                            // [warps][32][RW_LD]
+    u64* keys = reinterpret_cast<u64*>(rw_smem + RW_WARPS * 32 * RW_LD);  // [n2]
+    const size_t q = blockIdx.x;
+    const uint32_t n = sl_cnt[q];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float4* tile = tiles + warp * 32 * RW_LD;
+    uint32_t n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (uint32_t i = n + threadIdx.x; i < n2; i += blockDim.x) keys[i] = ~0ull;
+    const float4 x4 = reinterpret_cast<const float4*>(xq + q * D)[lane];
+    const uint32_t ds = D / m, dsr = D / mprime;
+    const uint32_t t0 = 4 * lane;
+    const uint32_t jj = t0 / ds, jr = t0 / dsr;
+    const uint32_t bo = t0 - jj * ds, ro = t0 - jr * dsr;
+    for (uint32_t b = warp * 32; b < n; b += RW_WARPS * 32) {
+        const uint32_t c = b + lane;
+        uint32_t my_pos = 0, my_id = 0, my_list = 0;
+        if (c < n) {
+            my_pos = sl_pos[q * sl_stride + c];
+            my_id = key_id(sl_key[q * sl_stride + c]);
+            my_list = list_of_pos(list_off, nlists, my_pos);
+        }
+        const uint32_t nb = min(32u, n - b);
+        for (uint32_t cc = 0; cc < nb; ++cc) {
+            const uint32_t pos = __shfl_sync(0xffffffffu, my_pos, cc);
+            const uint32_t l = __shfl_sync(0xffffffffu, my_list, cc);
+            const uint32_t code = __ldg(codes + (size_t)pos * m + jj);
+            const uint32_t rcode = __ldg(rcodes + (size_t)pos * mprime + jr);
+            const float4 cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D + t0));
+            const float4 bv = __ldg(reinterpret_cast<const float4*>(
+                books + ((size_t)jj * ks + code) * ds + bo));
+            const float4 rv = __ldg(reinterpret_cast<const float4*>(
+                rbooks + ((size_t)jr * ks + rcode) * dsr + ro));
+            const float d0 = __fsub_rn(x4.x, __fadd_rn(__fadd_rn(cv.x, bv.x), rv.x));
+            const float d1 = __fsub_rn(x4.y, __fadd_rn(__fadd_rn(cv.y, bv.y), rv.y));
+            const float d2 = __fsub_rn(x4.z, __fadd_rn(__fadd_rn(cv.z, bv.z), rv.z));
+            const float d3 = __fsub_rn(x4.w, __fadd_rn(__fadd_rn(cv.w, bv.w), rv.w));
+            tile[cc * RW_LD + lane] =
+                make_float4(__fmul_rn(d0, d0), __fmul_rn(d1, d1), __fmul_rn(d2, d2), __fmul_rn(d3, d3));
+        }
+        __syncwarp();
+        if (c < n) {
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll 8
+            for (int g = 0; g < 32; ++g) {
+                const float4 v = tile[lane * RW_LD + g];
+                s0 = __fadd_rn(s0, v.x);
+                s1 = __fadd_rn(s1, v.y);
+                s2 = __fadd_rn(s2, v.z);
+                s3 = __fadd_rn(s3, v.w);
+            }
+            keys[c] = nb_key(__fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3)), my_id);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    bitonic_sort_kv(keys, nullptr, n2);
+    const uint32_t cnt = min(n, k);
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+        const bool live = i < cnt;
+        out_ids[q * k + i] = live ? key_id(keys[i]) : 0xffffffffu;
+        out_dists[q * k + i] = live ? key_dist(keys[i]) : __int_as_float(0x7f800000);
+    }
+    if (threadIdx.x == 0) out_cnt[q] = cnt;
+}
+
 __global__ void unpack_keys_kernel(const u64* __restrict__ keys, const uint32_t* __restrict__ cnt,
                                    size_t nq, uint32_t stride, uint32_t* __restrict__ ids,
                                    float* __restrict__ dists) {
@@ -416,7 +502,14 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
     const size_t smem = ((d + 3) & ~3u) * sizeof(float) + (size_t)n2 * sizeof(u64);
     if (smem > 200 * 1024) throw ArgError("shortlist too large for the device re-ranker");
     const bool fast = d % 4 == 0 && (d / m) % 4 == 0 && (d / mprime) % 4 == 0;
-    if (fast) {
+    if (fast && d == 128) {
+        const size_t wsmem = (size_t)RW_WARPS * 32 * RW_LD * sizeof(float4) + (size_t)n2 * sizeof(u64);
+        if (wsmem > 220 * 1024) throw ArgError("shortlist too large for the device re-ranker");
+        set_smem((const void*)rerank_warp_kernel, wsmem);
+        rerank_warp_kernel<<<(unsigned)nq, RW_WARPS * 32, wsmem, s>>>(
+            reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, list_off, nlists,
+            coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists, out_cnt);
+    } else if (fast) {
         set_smem((const void*)rerank_kernel<true>, smem);
         rerank_kernel<true><<<(unsigned)nq, 256, smem, s>>>(
             reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, d, list_off,
