@@ -372,20 +372,29 @@ __global__ __launch_bounds__(RW_WARPS * 32) void rerank_warp_kernel(
     const uint32_t t0 = 4 * lane;
     const uint32_t jj = t0 / ds, jr = t0 / dsr;
     const uint32_t bo = t0 - jj * ds, ro = t0 - jr * dsr;
+    // per-warp staging of the batch's candidate metadata (list, code bytes)
+    __shared__ uint32_t s_list[RW_WARPS][32];
+    __shared__ __align__(16) uint8_t s_code[RW_WARPS][32][8];
+    __shared__ __align__(16) uint8_t s_rcode[RW_WARPS][32][32];
     for (uint32_t b = warp * 32; b < n; b += RW_WARPS * 32) {
         const uint32_t c = b + lane;
-        uint32_t my_pos = 0, my_id = 0, my_list = 0;
+        uint32_t my_id = 0;
         if (c < n) {
-            my_pos = sl_pos[q * sl_stride + c];
+            const uint32_t pos = sl_pos[q * sl_stride + c];
             my_id = key_id(sl_key[q * sl_stride + c]);
-            my_list = list_of_pos(list_off, nlists, my_pos);
+            s_list[warp][lane] = list_of_pos(list_off, nlists, pos);
+            *reinterpret_cast<u64*>(s_code[warp][lane]) = *reinterpret_cast<const u64*>(codes + (size_t)pos * 8);
+            for (uint32_t w8 = 0; w8 < mprime; w8 += 8)
+                *reinterpret_cast<u64*>(&s_rcode[warp][lane][w8]) =
+                    *reinterpret_cast<const u64*>(rcodes + (size_t)pos * mprime + w8);
         }
+        __syncwarp();
         const uint32_t nb = min(32u, n - b);
+#pragma unroll 4
         for (uint32_t cc = 0; cc < nb; ++cc) {
-            const uint32_t pos = __shfl_sync(0xffffffffu, my_pos, cc);
-            const uint32_t l = __shfl_sync(0xffffffffu, my_list, cc);
-            const uint32_t code = __ldg(codes + (size_t)pos * m + jj);
-            const uint32_t rcode = __ldg(rcodes + (size_t)pos * mprime + jr);
+            const uint32_t l = s_list[warp][cc];
+            const uint32_t code = s_code[warp][cc][jj];
+            const uint32_t rcode = s_rcode[warp][cc][jr];
             const float4 cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D + t0));
             const float4 bv = __ldg(reinterpret_cast<const float4*>(
                 books + ((size_t)jj * ks + code) * ds + bo));
@@ -502,7 +511,7 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
     const size_t smem = ((d + 3) & ~3u) * sizeof(float) + (size_t)n2 * sizeof(u64);
     if (smem > 200 * 1024) throw ArgError("shortlist too large for the device re-ranker");
     const bool fast = d % 4 == 0 && (d / m) % 4 == 0 && (d / mprime) % 4 == 0;
-    if (fast && d == 128) {
+    if (fast && d == 128 && m == 8 && mprime % 8 == 0 && mprime <= 32) {
         const size_t wsmem = (size_t)RW_WARPS * 32 * RW_LD * sizeof(float4) + (size_t)n2 * sizeof(u64);
         if (wsmem > 220 * 1024) throw ArgError("shortlist too large for the device re-ranker");
         set_smem((const void*)rerank_warp_kernel, wsmem);
