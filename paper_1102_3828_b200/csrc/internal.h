@@ -98,6 +98,8 @@ void launch_layout_place_new(const uint32_t* sorted_list, const uint32_t* sorted
                              uint32_t mprime, uint8_t* codes, uint32_t* ids, uint8_t* rcodes,
                              cudaStream_t s);
 
+// position -> list table at 16-entry granularity (list starts are 16-aligned).
+void launch_block_list(const uint64_t* off, uint32_t nlists, uint16_t* bl, cudaStream_t s);
 // Parity-balanced list order (see k_layout.cu) and per-list re-sorting.
 void launch_parity_keys(const uint64_t* off, const uint32_t* len, uint32_t nlists,
                         const uint8_t* codes, uint32_t* keys, uint32_t* vals, cudaStream_t s);
@@ -175,7 +177,7 @@ void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const 
 // Re-rank the shortlist with the 3-term reconstruction, keep the k best.
 void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_t* sl_cnt,
                    uint32_t sl_stride, size_t nq, const float* xq, uint32_t d,
-                   const uint64_t* list_off, uint32_t nlists, const float* coarse,
+                   const uint16_t* block_list, const float* coarse,
                    const uint8_t* codes, const float* books, uint32_t m, const uint8_t* rcodes,
                    const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
                    uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s);

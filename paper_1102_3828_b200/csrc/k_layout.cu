@@ -205,6 +205,24 @@ __global__ void list_keys_kernel(const uint64_t* __restrict__ off, const uint32_
 
 }  // namespace
 
+namespace {
+// block_list[pos >> 4] = list owning position pos (list starts are 16-aligned).
+__global__ void block_list_kernel(const uint64_t* __restrict__ off, uint32_t nlists,
+                                  uint16_t* __restrict__ bl) {
+    const uint32_t l = blockIdx.x;
+    if (l >= nlists) return;
+    const uint64_t b0 = off[l] >> 4, b1 = off[l + 1] >> 4;
+    for (uint64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) bl[b] = (uint16_t)l;
+}
+}  // namespace
+
+void launch_block_list(const uint64_t* off, uint32_t nlists, uint16_t* bl, cudaStream_t s) {
+    if (!nlists) return;
+    block_list_kernel<<<nlists, 256, 0, s>>>(off, nlists, bl);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
 void launch_parity_keys(const uint64_t* off, const uint32_t* len, uint32_t nlists,
                         const uint8_t* codes, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
     parity_keys_kernel<<<nlists, 256, 0, s>>>(off, len, codes, keys, vals);

@@ -8,6 +8,7 @@
 // broken by id exactly like TopK (topk.hpp:18-29).
 #include <float.h>
 
+#include <cstdlib>
 #include "common.cuh"
 #include "internal.h"
 
@@ -235,17 +236,6 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void select_topk_kernel(
     }
 }
 
-__device__ __forceinline__ uint32_t list_of_pos(const uint64_t* __restrict__ off, uint32_t nlists,
-                                                uint64_t pos) {
-    uint32_t lo = 0, hi = nlists;  // off[lo] <= pos < off[hi]
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(off + mid) <= pos) lo = mid;
-        else hi = mid;
-    }
-    return lo;
-}
-
 // l2_sq(x, yhat) with yhat[t] = (C_l[t] + B(code)[t]) + R(rcode)[t].
 template <bool FAST>
 __device__ __forceinline__ float rerank_dist(const float* __restrict__ xs, uint32_t d,
@@ -292,7 +282,7 @@ template <bool FAST>
 __global__ __launch_bounds__(256, 3) void rerank_kernel(
     const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
     const uint32_t* __restrict__ sl_cnt, uint32_t sl_stride, const float* __restrict__ xq, uint32_t d,
-    const uint64_t* __restrict__ list_off, uint32_t nlists, const float* __restrict__ coarse,
+    const uint16_t* __restrict__ block_list, const float* __restrict__ coarse,
     const uint8_t* __restrict__ codes, const float* __restrict__ books, uint32_t m,
     const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks, uint32_t mprime,
     uint32_t ks, uint32_t k, uint32_t* __restrict__ out_ids, float* __restrict__ out_dists,
@@ -318,8 +308,8 @@ __global__ __launch_bounds__(256, 3) void rerank_kernel(
         const uint32_t p1 = has1 ? sl_pos[q * sl_stride + i1] : p0;
         const uint32_t id0 = key_id(sl_key[q * sl_stride + i0]);
         const uint32_t id1 = has1 ? key_id(sl_key[q * sl_stride + i1]) : 0u;
-        const uint32_t l0 = list_of_pos(list_off, nlists, p0);
-        const uint32_t l1 = list_of_pos(list_off, nlists, p1);
+        const uint32_t l0 = block_list[p0 >> 4];
+        const uint32_t l1 = block_list[p1 >> 4];
         const float d0 = rerank_dist<FAST>(xs, d, coarse + (size_t)l0 * d, books, codes + (size_t)p0 * m, ds,
                                            rbooks, rcodes + (size_t)p0 * mprime, dsr, ks, nz);
         const float d1 = rerank_dist<FAST>(xs, d, coarse + (size_t)l1 * d, books, codes + (size_t)p1 * m, ds,
@@ -351,7 +341,7 @@ constexpr int RW_LD = 33;  // padded float4 row of the transpose tile
 __global__ __launch_bounds__(RW_WARPS * 32) void rerank_warp_kernel(
     const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
     const uint32_t* __restrict__ sl_cnt, uint32_t sl_stride, const float* __restrict__ xq,
-    const uint64_t* __restrict__ list_off, uint32_t nlists, const float* __restrict__ coarse,
+    const uint16_t* __restrict__ block_list, const float* __restrict__ coarse,
     const uint8_t* __restrict__ codes, const float* __restrict__ books, uint32_t m,
     const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks, uint32_t mprime,
     uint32_t ks, uint32_t k, uint32_t* __restrict__ out_ids, float* __restrict__ out_dists,
@@ -382,7 +372,7 @@ __global__ __launch_bounds__(RW_WARPS * 32) void rerank_warp_kernel(
         if (c < n) {
             const uint32_t pos = sl_pos[q * sl_stride + c];
             my_id = key_id(sl_key[q * sl_stride + c]);
-            s_list[warp][lane] = list_of_pos(list_off, nlists, pos);
+            s_list[warp][lane] = block_list[pos >> 4];
             *reinterpret_cast<u64*>(s_code[warp][lane]) = *reinterpret_cast<const u64*>(codes + (size_t)pos * 8);
             for (uint32_t w8 = 0; w8 < mprime; w8 += 8)
                 *reinterpret_cast<u64*>(&s_rcode[warp][lane][w8]) =
@@ -501,7 +491,7 @@ void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const 
 
 void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_t* sl_cnt,
                    uint32_t sl_stride, size_t nq, const float* xq, uint32_t d,
-                   const uint64_t* list_off, uint32_t nlists, const float* coarse,
+                   const uint16_t* block_list, const float* coarse,
                    const uint8_t* codes, const float* books, uint32_t m, const uint8_t* rcodes,
                    const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
                    uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s) {
@@ -511,24 +501,29 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
     const size_t smem = ((d + 3) & ~3u) * sizeof(float) + (size_t)n2 * sizeof(u64);
     if (smem > 200 * 1024) throw ArgError("shortlist too large for the device re-ranker");
     const bool fast = d % 4 == 0 && (d / m) % 4 == 0 && (d / mprime) % 4 == 0;
-    if (fast && d == 128 && m == 8 && mprime % 8 == 0 && mprime <= 32) {
+    // PQRR_RERANK=warp selects the warp-cooperative variant (A/B measurements)
+    static const bool want_warp = [] {
+        const char* e = getenv("PQRR_RERANK");
+        return e && std::string(e) == "warp";
+    }();
+    if (want_warp && fast && d == 128 && m == 8 && mprime % 8 == 0 && mprime <= 32) {
         const size_t wsmem = (size_t)RW_WARPS * 32 * RW_LD * sizeof(float4) + (size_t)n2 * sizeof(u64);
         if (wsmem > 220 * 1024) throw ArgError("shortlist too large for the device re-ranker");
         set_smem((const void*)rerank_warp_kernel, wsmem);
         rerank_warp_kernel<<<(unsigned)nq, RW_WARPS * 32, wsmem, s>>>(
-            reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, list_off, nlists,
+            reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, block_list,
             coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists, out_cnt);
     } else if (fast) {
         set_smem((const void*)rerank_kernel<true>, smem);
         rerank_kernel<true><<<(unsigned)nq, 256, smem, s>>>(
-            reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, d, list_off,
-            nlists, coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists,
+            reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, d, block_list,
+            coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists,
             out_cnt, kNegZero2);
     } else {
         set_smem((const void*)rerank_kernel<false>, smem);
         rerank_kernel<false><<<(unsigned)nq, 256, smem, s>>>(
-            reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, d, list_off,
-            nlists, coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists,
+            reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, d, block_list,
+            coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists,
             out_cnt, kNegZero2);
     }
     PQRR_LAUNCH_CHECK();

@@ -251,6 +251,7 @@ struct DevIndex {
     std::vector<uint32_t> h_len;
     DBuf<uint8_t> codes, rcodes;
     DBuf<uint32_t> ids;
+    DBuf<uint16_t> block_list;  // list of each 16-entry block of positions
     uint64_t next_id = 0;
     // id -> position (lazy)
     DBuf<uint32_t> id_map;
@@ -417,6 +418,8 @@ void finalize(DevIndex& ix) {
     ix.rcodes.swap(rcodes);
     ix.ids.swap(ids);
     ix.list_off.swap(d_off);
+    ix.block_list.alloc(acc / 16 + 1);
+    launch_block_list(ix.list_off.p, c, ix.block_list.p, s);
     ix.list_len.swap(d_len);
     ix.h_off = new_off;
     ix.h_len = new_len;
@@ -654,7 +657,7 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
         if (h_flag) throw ShortlistError();
         PQRR_CUDA(cudaEventRecord(ix.ev[7], s));
         launch_rerank(reinterpret_cast<uint64_t*>(sl.key), sl.pos, sl.cnt, kprime, nq, xq, ix.d,
-                      ix.list_off.p, ix.c, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
+                      ix.block_list.p, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
                       ix.rbooks.p, ix.mprime, ix.ks, k, out_ids, out_dists, out_cnt, s);
     } else {
         PQRR_CUDA(cudaEventRecord(ix.ev[7], s));
@@ -905,6 +908,7 @@ int pqrr_dev_index_create(int device, uint32_t d, uint32_t c, const float* coars
         *out = nullptr;
         check_shape(d, m, ks);
         if (c == 0) throw ArgError("c must be positive");
+        if (c > 65536) throw UnsupportedError("more than 65536 coarse centroids");
         if (mprime && d % mprime) throw ArgError("dimension not divisible");
         if (mprime && !rbooks) throw ArgError("rbooks required when mprime > 0");
         DeviceGuard g(device);
@@ -1195,7 +1199,7 @@ static int rerank_host(pqrr_dev_index* h, const float* qf, const uint8_t* qu, si
         float* od = ws.alloc<float>(nq * k);
         uint32_t* oc = ws.alloc<uint32_t>(nq);
         launch_rerank(reinterpret_cast<uint64_t*>(key), pos, cnt, (uint32_t)sl_stride, nq, xq, ix.d,
-                      ix.list_off.p, ix.c, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
+                      ix.block_list.p, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
                       ix.rbooks.p, ix.mprime, ix.ks, (uint32_t)k, oi, od, oc, s);
         PQRR_CUDA(cudaMemcpyAsync(out_ids, oi, nq * k * 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaMemcpyAsync(out_dists, od, nq * k * 4, cudaMemcpyDeviceToHost, s));
