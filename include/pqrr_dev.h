@@ -137,6 +137,13 @@ int pqrr_dev_index_get_info(pqrr_dev_index* ix, pqrr_dev_index_info* out);
 int pqrr_dev_export_lists(pqrr_dev_index* ix, uint64_t* offsets, uint32_t* ids, uint8_t* codes,
                           uint8_t* rcodes);
 
+/* Inverse of pqrr_dev_export_lists: load an existing inverted file into an
+ * EMPTY index (e.g. a host IvfIndex, ivf_index.hpp:27-36, or a PQRR file,
+ * storage.hpp:23-25).  Lists in list order, ids ascending within a list;
+ * rcodes (list order, mprime bytes per entry) may be NULL when mprime = 0. */
+int pqrr_dev_load_lists(pqrr_dev_index* ix, const uint64_t* offsets, const uint32_t* ids,
+                        const uint8_t* codes, const uint8_t* rcodes);
+
 /* Fused search: coarse probe of w lists -> LUTs -> ADC scan -> exact top-k'
  * shortlist (ivf_search_batch, ivf_index.hpp:58-64) -> if k > 0, re-rank with
  * the refinement codes to the top-k (ivf_rerank, :79-81).
@@ -167,6 +174,19 @@ int pqrr_dev_rerank_f32(pqrr_dev_index* ix, const float* queries, size_t nq,
                         size_t k, uint32_t* out_ids, float* out_dists);
 /* ivf_reconstruct (ivf_index.hpp:75-77): coarse + decode + refine decode. */
 int pqrr_dev_reconstruct(pqrr_dev_index* ix, const uint32_t* ids, size_t n, float* out);
+
+/* K7 — merge of per-shard ranked lists (multi-GPU id-range sharding, after an
+ * all-gather): inputs [parts][nq][width] ids / dists and [parts][nq] counts;
+ * output the top-k per query under (dist, id) (types.hpp:47-50).  Host
+ * pointers, or device pointers on `device` for the _device variant
+ * (stream-ordered on `stream`, a cudaStream_t; NULL = legacy default).     */
+int pqrr_dev_merge_topk(int device, const uint32_t* ids, const float* dists,
+                        const uint32_t* counts, size_t nq, uint32_t parts, uint32_t width,
+                        uint32_t k, uint32_t* out_ids, float* out_dists, uint32_t* out_counts);
+int pqrr_dev_merge_topk_device(int device, const uint32_t* ids, const float* dists,
+                               const uint32_t* counts, size_t nq, uint32_t parts, uint32_t width,
+                               uint32_t k, uint32_t* out_ids, float* out_dists,
+                               uint32_t* out_counts, void* stream);
 
 /* Per-stage device times (CUDA events on the index stream) of the last search. */
 typedef struct {

@@ -12,4 +12,4 @@ from .ivf import (  # noqa: F401
     ivf_reconstruct, ivf_refine_encode, ivf_refine_train, ivf_rerank, ivf_search,
     ivf_search_batch, ivf_train, kmeans_train, pq_decode, pq_encode, pq_train, synth,
 )
-from . import kernels  # noqa: F401
+from . import ivf, kernels, sharded  # noqa: F401

@@ -100,6 +100,9 @@ _sig("pqrr_dev_rerank_u8", [_vp, _u8p, _sz, _u32p, _u32p, _sz, _sz, _u32p, _f32p
 _sig("pqrr_dev_rerank_f32", [_vp, _f32p, _sz, _u32p, _u32p, _sz, _sz, _u32p, _f32p])
 _sig("pqrr_dev_reconstruct", [_vp, _u32p, _sz, _f32p])
 _sig("pqrr_dev_last_search_stats", [_vp, C.POINTER(SearchStats)])
+_sig("pqrr_dev_load_lists", [_vp, _u64p, _u32p, _u8p, _vp])
+_sig("pqrr_dev_merge_topk", [_int, _u32p, _f32p, _u32p, _sz, _u32, _u32, _u32, _u32p, _f32p, _u32p])
+_sig("pqrr_dev_merge_topk_device", [_int, _vp, _vp, _vp, _sz, _u32, _u32, _u32, _vp, _vp, _vp, _vp])
 
 # Symbols include/pqrr_dev.h declares (checked by the CPU test suite).
 EXPORTED = [
@@ -111,7 +114,8 @@ EXPORTED = [
     "pqrr_dev_add_synthetic", "pqrr_dev_finalize", "pqrr_dev_index_get_info",
     "pqrr_dev_export_lists", "pqrr_dev_search_u8", "pqrr_dev_search_f32",
     "pqrr_dev_search_u8_device", "pqrr_dev_rerank_u8", "pqrr_dev_rerank_f32",
-    "pqrr_dev_reconstruct", "pqrr_dev_last_search_stats",
+    "pqrr_dev_reconstruct", "pqrr_dev_last_search_stats", "pqrr_dev_load_lists",
+    "pqrr_dev_merge_topk", "pqrr_dev_merge_topk_device",
 ]
 
 

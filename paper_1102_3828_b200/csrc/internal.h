@@ -181,6 +181,10 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
                    const uint8_t* codes, const float* books, uint32_t m, const uint8_t* rcodes,
                    const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
                    uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s);
+// Merge per-shard ranked lists [parts][nq][width] into the top-k (K7).
+void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* counts, size_t nq,
+                       uint32_t parts, uint32_t width, uint32_t k, uint32_t* out_ids,
+                       float* out_dists, uint32_t* out_cnt, cudaStream_t s);
 // Split keys into ids / dists ([nq][stride] -> [nq][stride]).
 void launch_unpack_keys(const uint64_t* keys, const uint32_t* cnt, size_t nq, uint32_t stride,
                         uint32_t* ids, float* dists, cudaStream_t s);

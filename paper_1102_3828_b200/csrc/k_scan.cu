@@ -93,26 +93,6 @@ __device__ __forceinline__ void build_luts(float* __restrict__ lut, const float*
     }
 }
 
-// Warp-aggregated append of (dist, pos) for the lanes with `hit`, grouped by
-// query (lanes sharing lane & 3 share the 4 queries).
-__device__ __forceinline__ void emit(bool hit, int q, float dist, uint32_t pos, int lane, int qd,
-                                     uint32_t* __restrict__ cnt, float* __restrict__ cdist,
-                                     uint32_t* __restrict__ cpos, uint32_t cap) {
-    const unsigned all = __ballot_sync(0xffffffffu, hit);
-    if (!hit) return;
-    const unsigned grp = all & (0x11111111u << qd);
-    const int leader = __ffs(grp) - 1;
-    const unsigned rank = __popc(grp & ((1u << lane) - 1u));
-    unsigned base = 0;
-    if (lane == leader) base = atomicAdd(cnt + q, (unsigned)__popc(grp));
-    base = __shfl_sync(grp, base, leader);
-    const unsigned slot = base + rank;
-    if (slot < cap) {
-        cdist[(size_t)q * cap + slot] = dist;
-        cpos[(size_t)q * cap + slot] = pos;
-    }
-}
-
 // Plain per-lane append (hits are rare after the threshold: ~2k' per query).
 __device__ __forceinline__ void emit1(bool hit, int q, float dist, uint32_t pos,
                                       uint32_t* __restrict__ cnt, float* __restrict__ cdist,

@@ -423,6 +423,41 @@ __global__ __launch_bounds__(RW_WARPS * 32) void rerank_warp_kernel(
     if (threadIdx.x == 0) out_cnt[q] = cnt;
 }
 
+// K7: merge of per-shard ranked lists (all-gathered [parts][nq][width]) into
+// the global top-k under (dist, id) — one CTA per query, bitonic in smem.
+__global__ __launch_bounds__(256) void merge_topk_kernel(
+    const uint32_t* __restrict__ ids, const float* __restrict__ dists,
+    const uint32_t* __restrict__ counts, size_t nq, uint32_t parts, uint32_t width, uint32_t k,
+    uint32_t n2, uint32_t* __restrict__ out_ids, float* __restrict__ out_dists,
+    uint32_t* __restrict__ out_cnt) {
+    extern __shared__ u64 mkeys[];
+    const size_t q = blockIdx.x;
+    __shared__ uint32_t s_total;
+    if (threadIdx.x == 0) s_total = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+        u64 key = ~0ull;
+        if (i < parts * width) {
+            const uint32_t p = i / width, j = i % width;
+            const size_t row = (size_t)p * nq + q;
+            if (j < counts[row]) {
+                key = nb_key(dists[row * width + j], ids[row * width + j]);
+                atomicAdd(&s_total, 1u);
+            }
+        }
+        mkeys[i] = key;
+    }
+    __syncthreads();
+    bitonic_sort_kv(mkeys, nullptr, n2);
+    const uint32_t cnt = min(s_total, k);
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+        const bool live = i < cnt;
+        out_ids[q * k + i] = live ? key_id(mkeys[i]) : 0xffffffffu;
+        out_dists[q * k + i] = live ? key_dist(mkeys[i]) : __int_as_float(0x7f800000);
+    }
+    if (threadIdx.x == 0) out_cnt[q] = cnt;
+}
+
 __global__ void unpack_keys_kernel(const u64* __restrict__ keys, const uint32_t* __restrict__ cnt,
                                    size_t nq, uint32_t stride, uint32_t* __restrict__ ids,
                                    float* __restrict__ dists) {
@@ -526,6 +561,21 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
             coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists,
             out_cnt, kNegZero2);
     }
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* counts, size_t nq,
+                       uint32_t parts, uint32_t width, uint32_t k, uint32_t* out_ids,
+                       float* out_dists, uint32_t* out_cnt, cudaStream_t s) {
+    if (nq == 0) return;
+    uint32_t n2 = 1;
+    while (n2 < parts * width) n2 <<= 1;
+    const size_t smem = (size_t)n2 * sizeof(u64);
+    if (smem > 200 * 1024) throw ArgError("parts * width too large for the device merge");
+    set_smem((const void*)merge_topk_kernel, smem);
+    merge_topk_kernel<<<(unsigned)nq, 256, smem, s>>>(ids, dists, counts, nq, parts, width, k, n2,
+                                                      out_ids, out_dists, out_cnt);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

@@ -1243,6 +1243,84 @@ int pqrr_dev_reconstruct(pqrr_dev_index* h, const uint32_t* ids, size_t n, float
     });
 }
 
+int pqrr_dev_load_lists(pqrr_dev_index* h, const uint64_t* offsets, const uint32_t* ids,
+                        const uint8_t* codes, const uint8_t* rcodes) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        if (ix.n || ix.st_n) throw ArgError("load_lists needs an empty index");
+        if (ix.mprime && !rcodes) throw ArgError("rcodes required when mprime > 0");
+        const uint64_t n = offsets[ix.c];
+        if (n == 0) return;
+        if (n > 0xffffffffull) throw UnsupportedError("more than 2^32 entries on one device");
+        std::vector<uint32_t> assign(n);
+        uint64_t max_id = 0;
+        for (uint32_t l = 0; l < ix.c; ++l) {
+            if (offsets[l + 1] < offsets[l]) throw ArgError("corrupt file");
+            for (uint64_t i = offsets[l]; i < offsets[l + 1]; ++i) {
+                assign[i] = l;
+                if (i > offsets[l] && ids[i] <= ids[i - 1]) throw ArgError("corrupt file");
+                max_id = std::max<uint64_t>(max_id, ids[i]);
+            }
+        }
+        grow_staging(ix, n);
+        cudaStream_t s = ix.stream;
+        PQRR_CUDA(cudaMemcpyAsync(ix.st_assign.p, assign.data(), n * 4, cudaMemcpyHostToDevice, s));
+        PQRR_CUDA(cudaMemcpyAsync(ix.st_ids.p, ids, n * 4, cudaMemcpyHostToDevice, s));
+        PQRR_CUDA(cudaMemcpyAsync(ix.st_codes.p, codes, n * ix.m, cudaMemcpyHostToDevice, s));
+        if (ix.mprime)
+            PQRR_CUDA(cudaMemcpyAsync(ix.st_rcodes.p, rcodes, n * ix.mprime, cudaMemcpyHostToDevice, s));
+        ix.st_n = n;
+        ix.next_id = max_id + 1;
+        finalize(ix);
+    });
+}
+
+static int merge_impl(int device, const uint32_t* ids, const float* dists, const uint32_t* counts,
+                      size_t nq, uint32_t parts, uint32_t width, uint32_t k, uint32_t* out_ids,
+                      float* out_dists, uint32_t* out_counts, bool on_device, void* stream) {
+    return guarded([&] {
+        if (nq == 0 || k == 0) return;
+        if (parts == 0 || width == 0) throw ArgError("parts and width must be positive");
+        DeviceGuard g(device);
+        if (on_device) {
+            launch_merge_topk(ids, dists, counts, nq, parts, width, k, out_ids, out_dists, out_counts,
+                              static_cast<cudaStream_t>(stream));
+            return;
+        }
+        Session se(device);
+        Workspace ws(se.s);
+        const size_t tot = (size_t)parts * nq * width;
+        const uint32_t* di = se.upload(ws, ids, tot);
+        const float* dd = se.upload(ws, dists, tot);
+        const uint32_t* dc = se.upload(ws, counts, (size_t)parts * nq);
+        uint32_t* oi = ws.alloc<uint32_t>(nq * k);
+        float* od = ws.alloc<float>(nq * k);
+        uint32_t* oc = ws.alloc<uint32_t>(nq);
+        launch_merge_topk(di, dd, dc, nq, parts, width, k, oi, od, oc, se.s);
+        se.download(out_ids, oi, nq * k);
+        se.download(out_dists, od, nq * k);
+        se.download(out_counts, oc, nq);
+        se.sync();
+    });
+}
+
+int pqrr_dev_merge_topk(int device, const uint32_t* ids, const float* dists, const uint32_t* counts,
+                        size_t nq, uint32_t parts, uint32_t width, uint32_t k, uint32_t* out_ids,
+                        float* out_dists, uint32_t* out_counts) {
+    return merge_impl(device, ids, dists, counts, nq, parts, width, k, out_ids, out_dists, out_counts,
+                      false, nullptr);
+}
+
+int pqrr_dev_merge_topk_device(int device, const uint32_t* ids, const float* dists,
+                               const uint32_t* counts, size_t nq, uint32_t parts, uint32_t width,
+                               uint32_t k, uint32_t* out_ids, float* out_dists, uint32_t* out_counts,
+                               void* stream) {
+    return merge_impl(device, ids, dists, counts, nq, parts, width, k, out_ids, out_dists, out_counts,
+                      true, stream);
+}
+
 int pqrr_dev_last_search_stats(pqrr_dev_index* h, pqrr_dev_search_stats* out) {
     return guarded([&] {
         std::lock_guard<std::mutex> lk(h->ix.mu);

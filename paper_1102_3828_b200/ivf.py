@@ -316,6 +316,16 @@ class IvfIndex:
                                         rc.ctypes.data if rc is not None else None))
         return offs, ids, codes, rc
 
+    def load_lists(self, offsets, ids, codes, rcodes=None) -> None:
+        """Inverse of export_lists (an existing inverted file into an empty index)."""
+        rc = None
+        if rcodes is not None:
+            rc = np.ascontiguousarray(rcodes, np.uint8)
+        check(lib.pqrr_dev_load_lists(self.h, np.ascontiguousarray(offsets, np.uint64),
+                                      np.ascontiguousarray(ids, np.uint32),
+                                      np.ascontiguousarray(codes, np.uint8),
+                                      rc.ctypes.data if rc is not None else None))
+
     @property
     def lists(self):
         offs, ids, codes, _ = self.export_lists()
@@ -446,6 +456,19 @@ def ivf_rerank(x, shortlist, index: IvfIndex, rq: RefineQuantizer, codes: Refine
         check(lib.pqrr_dev_rerank_f32(index.h, _f32(q), nq, sl_ids, sl_cnt, stride, k, ids, dists))
     res = [SearchResult(ids[i, :k].copy(), dists[i, :k].copy()) for i in range(nq)]
     return res[0] if single else res
+
+
+def merge_topk(ids, dists, counts, k: int, device: int = DEFAULT_DEVICE):
+    """K7 on the device: per-shard ranked lists [parts, nq, width] -> top-k (dist, id)."""
+    ids = np.ascontiguousarray(ids, np.uint32)
+    dists = np.ascontiguousarray(dists, np.float32)
+    counts = np.ascontiguousarray(counts, np.uint32)
+    parts, nq, width = ids.shape
+    oi = np.zeros((nq, k), np.uint32)
+    od = np.zeros((nq, k), np.float32)
+    oc = np.zeros(nq, np.uint32)
+    check(lib.pqrr_dev_merge_topk(device, ids, dists, counts, nq, parts, width, k, oi, od, oc))
+    return oi, od, oc
 
 
 # ----------------------------------------------------------------------- data

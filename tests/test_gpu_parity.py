@@ -216,3 +216,52 @@ def test_search_matches_oracle(mid_instance, v, kprime, k):
     np.testing.assert_array_equal(bits(dd), bits(rd))
     st = dix.last_stats()
     assert st["kernels"] > 5 and st["ms_scan"] > 0
+
+
+# ------------------------------------------------------------------ reference-side C++ drop-in
+def test_reference_api_shim():
+    """integration/test_shim: a caller of the reference's own pqrr:: API
+    (compiled against /root/reference headers, prebuilt) linked to the drop-in."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration",
+                       "build", "test_shim")
+    if not os.path.exists(exe):
+        pytest.skip("integration/build/test_shim not built (needs the reference headers)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "SHIM OK" in out.stdout, out.stdout + out.stderr
+
+
+# ------------------------------------------------------------------ K7 merge + list import
+def test_merge_topk_kernel_matches_host_merge(pq):
+    from paper_1102_3828_b200.sharded import merge_topk_host
+
+    rng = np.random.default_rng(12)
+    parts, nq, width, k = 4, 33, 50, 20
+    ids = rng.permutation(parts * nq * width).astype(np.uint32).reshape(parts, nq, width)
+    d = rng.integers(0, 40, (parts, nq, width)).astype(np.float32)  # many exact ties
+    d.sort(axis=2)
+    counts = rng.integers(0, width + 1, (parts, nq)).astype(np.uint32)
+    counts[:, 0] = 0  # a query with no candidates at all
+    oi, od, oc = pq.ivf.merge_topk(ids, d, counts, k)
+    ei, ed, ec = merge_topk_host(ids, d, counts, k)
+    np.testing.assert_array_equal(oc, ec)
+    for q in range(nq):
+        n = ec[q]
+        np.testing.assert_array_equal(oi[q, :n], ei[q, :n])
+        np.testing.assert_array_equal(od[q, :n], ed[q, :n])
+
+
+def test_load_lists_round_trip(pq, golden_ivf):
+    g = golden_ivf
+    ix, coarse, P, rq = build_small(pq, g)
+    offs, ids, codes, rc = ix.export_lists()
+    ix2 = pq.IvfIndex(coarse, P, rq)
+    ix2.load_lists(offs, ids, codes, rc)
+    for a, b in zip(ix.export_lists(), ix2.export_lists()):
+        np.testing.assert_array_equal(a, b)
+    a = ix.search(g["queries"], int(g["v"]), int(g["kprime"]), int(g["k"]))
+    b = ix2.search(g["queries"], int(g["v"]), int(g["kprime"]), int(g["k"]))
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
