@@ -236,6 +236,124 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void select_topk_kernel(
     }
 }
 
+// Radix select over 32-bit keys produced by `key(i)` for the entries `pred(i)`
+// accepts; returns the rank-th smallest key and its rank among equal keys.
+template <class KeyF, class PredF>
+__device__ void radix_select32(uint32_t n, uint32_t rank, KeyF key, PredF pred, uint32_t* hist,
+                               uint32_t* s_bin, uint32_t* s_rank, uint32_t* s_cnt, uint32_t* s_val,
+                               uint32_t& out_key, uint32_t& out_rank, uint32_t& out_cnt) {
+    uint32_t prefix = 0, r = rank, cnt = 0;
+    const int shifts[3] = {21, 10, 0};
+    const int widths[3] = {11, 11, 10};
+    for (int pass = 0; pass < 3; ++pass) {
+        for (int b = threadIdx.x; b < NBINS; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        const int sh = shifts[pass], wd = widths[pass];
+        const uint32_t msk = (1u << wd) - 1u;
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+            if (!pred(i)) continue;
+            const uint32_t u = key(i);
+            if (pass == 0 || (u >> (sh + wd)) == prefix) atomicAdd(&hist[(u >> sh) & msk], 1u);
+        }
+        __syncthreads();
+        find_bin(hist, r, s_bin, s_rank, s_cnt);
+        __syncthreads();
+        prefix = (prefix << wd) | *s_bin;
+        r = *s_rank;
+        cnt = *s_cnt;
+        if (cnt == 1 && sh > 0) {  // a single key left under this prefix
+            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+                if (pred(i) && (key(i) >> sh) == prefix) *s_val = key(i);
+            __syncthreads();
+            prefix = *s_val;
+            break;
+        }
+        __syncthreads();
+    }
+    out_key = prefix;
+    out_rank = r;
+    out_cnt = cnt;
+}
+
+// Exact top-k' for candidate sets too large for shared memory (k' up to 1e4):
+// radix select on the distance bits streamed from global memory, then the
+// boundary distance's ties resolved by a second radix select on ids; ids are
+// gathered only for the selected entries and the ties.
+__global__ __launch_bounds__(SEL_THREADS, 4) void select_large_kernel(
+    const float* __restrict__ cand_dist, const uint32_t* __restrict__ cand_pos,
+    const uint32_t* __restrict__ cand_cnt, uint32_t cap, const uint32_t* __restrict__ ids,
+    uint32_t kprime, u64* __restrict__ sl_key, uint32_t* __restrict__ sl_pos,
+    uint32_t* __restrict__ sl_cnt) {
+    __shared__ uint32_t hist[NBINS];
+    __shared__ uint32_t s_bin, s_rank, s_cnt, s_val, s_out;
+    const size_t q = blockIdx.x;
+    const uint32_t n = min(cand_cnt[q], cap);
+    const uint32_t* db = reinterpret_cast<const uint32_t*>(cand_dist) + q * cap;
+    const uint32_t* pb = cand_pos + q * cap;
+    if (threadIdx.x == 0) s_out = 0;
+    uint32_t dstar = 0xffffffffu, r = 0, ceq = 0;
+    if (n > kprime) {
+        radix_select32(n, kprime, [&](uint32_t i) { return db[i]; }, [](uint32_t) { return true; },
+                       hist, &s_bin, &s_rank, &s_cnt, &s_val, dstar, r, ceq);
+    }
+    __syncthreads();
+    // entries strictly below the boundary distance are all in
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t u = db[i];
+        if (n <= kprime || u < dstar) {
+            const uint32_t p = pb[i];
+            const uint32_t o = atomicAdd(&s_out, 1u);
+            sl_key[q * kprime + o] = ((u64)u << 32) | ids[p];
+            sl_pos[q * kprime + o] = p;
+        }
+    }
+    if (n > kprime) {
+        // r of the entries at exactly dstar, smallest ids first (types.hpp:47-50)
+        uint32_t idstar = 0xffffffffu, r2 = 0, c2 = 0;
+        const bool all_ties = (r == ceq);
+        if (!all_ties) {
+            radix_select32(n, r, [&](uint32_t i) { return ids[pb[i]]; },
+                           [&](uint32_t i) { return db[i] == dstar; }, hist, &s_bin, &s_rank,
+                           &s_cnt, &s_val, idstar, r2, c2);
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+            if (db[i] != dstar) continue;
+            const uint32_t p = pb[i];
+            const uint32_t id = ids[p];
+            if (all_ties || id <= idstar) {
+                const uint32_t o = atomicAdd(&s_out, 1u);
+                sl_key[q * kprime + o] = ((u64)dstar << 32) | id;
+                sl_pos[q * kprime + o] = p;
+            }
+        }
+    }
+    if (threadIdx.x == 0) sl_cnt[q] = min(n, kprime);
+}
+
+// In-place ascending sort of each query's selected (key, pos) rows.
+__global__ __launch_bounds__(256) void sort_rows_kernel(u64* __restrict__ sl_key,
+                                                        uint32_t* __restrict__ sl_pos,
+                                                        const uint32_t* __restrict__ sl_cnt,
+                                                        uint32_t kprime) {
+    extern __shared__ u64 rkeys2[];
+    const size_t q = blockIdx.x;
+    const uint32_t cnt = sl_cnt[q];
+    uint32_t n2 = 1;
+    while (n2 < cnt) n2 <<= 1;
+    uint32_t* rpos = reinterpret_cast<uint32_t*>(rkeys2 + n2);
+    for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+        rkeys2[i] = i < cnt ? sl_key[q * kprime + i] : ~0ull;
+        rpos[i] = i < cnt ? sl_pos[q * kprime + i] : 0u;
+    }
+    __syncthreads();
+    bitonic_sort_kv(rkeys2, rpos, n2);
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+        sl_key[q * kprime + i] = rkeys2[i];
+        sl_pos[q * kprime + i] = rpos[i];
+    }
+}
+
 // l2_sq(x, yhat) with yhat[t] = (C_l[t] + B(code)[t]) + R(rcode)[t].
 template <bool FAST>
 __device__ __forceinline__ float rerank_dist(const float* __restrict__ xs, uint32_t d,
@@ -515,7 +633,24 @@ void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const 
     // smem sized by the largest candidate set of this batch (max_n <= cap)
     const uint32_t slots = std::max(std::max(std::min(max_n, cap), 1u), sorted ? kp2 : 0u);
     const size_t smem = (size_t)slots * (sizeof(u64) + sizeof(uint32_t));
-    if (smem > 200 * 1024) throw ArgError("candidate capacity too large for the device selector");
+    if (smem > 96 * 1024) {
+        // large k' (C4: 1e4): candidates stay in global memory
+        select_large_kernel<<<(unsigned)nq, SEL_THREADS, 0, s>>>(
+            cand_dist, cand_pos, cand_cnt, cap, ids, kprime, reinterpret_cast<u64*>(sl_key), sl_pos,
+            sl_cnt);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        if (sorted) {
+            const size_t ssm = (size_t)kp2 * (sizeof(u64) + sizeof(uint32_t));
+            if (ssm > 200 * 1024) throw ArgError("kprime too large for a sorted device shortlist");
+            set_smem((const void*)sort_rows_kernel, ssm);
+            sort_rows_kernel<<<(unsigned)nq, 256, ssm, s>>>(reinterpret_cast<u64*>(sl_key), sl_pos,
+                                                           sl_cnt, kprime);
+            PQRR_LAUNCH_CHECK();
+            count_launch();
+        }
+        return;
+    }
     set_smem((const void*)select_topk_kernel, smem);
     select_topk_kernel<<<(unsigned)nq, SEL_THREADS, smem, s>>>(
         cand_dist, cand_pos, cand_cnt, cap, slots, ids, kprime, sorted ? 1 : 0,

@@ -458,9 +458,9 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     auto& st = ix.stats;
     const uint32_t c = ix.c;
     const size_t P = nq * (size_t)w;
-    uint32_t kp2 = 1;
-    while (kp2 < 4 * kprime) kp2 <<= 1;
-    const uint32_t cap = std::max<uint32_t>(8192, std::min<uint32_t>(kp2, 16384));
+    // candidate buffer per query: >= 4k' (the sampled threshold targets ~2k');
+    // beyond 8192 the selector streams candidates from global memory
+    const uint32_t cap = std::max<uint32_t>(8192, ((4 * kprime + 1023) / 1024) * 1024);
     uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / 64.0));
     stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
     const uint32_t rank = (uint32_t)std::ceil(alpha * kprime / stride);
@@ -629,7 +629,7 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
                    size_t k_sz, uint32_t* out_ids, float* out_dists, uint32_t* out_cnt) {
     if (w < 1 || w > ix.c) throw ArgError("v must satisfy 1 <= v <= c");
     if (kprime_sz < 1) throw ArgError("kprime must be positive");
-    if (kprime_sz > 4096) throw UnsupportedError("kprime above 4096 is not supported yet on the device");
+    if (kprime_sz > 16384) throw UnsupportedError("kprime above 16384 is not supported on the device");
     if (k_sz > kprime_sz) throw ShortlistError();
     if (k_sz > 0 && ix.mprime == 0) throw ArgError("re-ranking needs refinement codes (mprime > 0)");
     finalize(ix);

@@ -198,7 +198,8 @@ def mid_instance(pq, oracle):
                 dix=dix)
 
 
-@pytest.mark.parametrize("v,kprime,k", [(24, 1000, 100), (8, 100, 10), (40, 300, 300), (3, 2000, 1)])
+@pytest.mark.parametrize("v,kprime,k", [(24, 1000, 100), (8, 100, 10), (40, 300, 300), (3, 2000, 1),
+                                        (64, 5000, 100), (40, 10000, 100)])
 def test_search_matches_oracle(mid_instance, v, kprime, k):
     oix, dix, q = mid_instance["oix"], mid_instance["dix"], mid_instance["queries"]
     qf = q.astype(np.float32)
