@@ -162,13 +162,14 @@ void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, u
                            uint32_t* items, cudaStream_t s);
 // Per query: N_q = sum of probed list lengths; per pair sample counts.
 void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
-                        uint32_t stride, uint32_t cap, uint64_t* nq_entries,
+                        uint32_t stride, uint32_t strat, uint32_t cap, uint64_t* nq_entries,
                         uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
                         cudaStream_t s);
 // tau_q = rank-th smallest sample of query q (sampled queries), +inf otherwise.
 void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_off, uint32_t w,
-                             size_t nq, const uint8_t* query_sampled, uint32_t rank,
-                             uint32_t max_samples, float* tau, cudaStream_t s);
+                             size_t nq, const uint8_t* query_sampled, float alpha_k,
+                             const uint64_t* n_entries, uint32_t max_samples, float* tau,
+                             cudaStream_t s);
 // Exact top-kprime under (dist, id) from each query's candidates.
 void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
                         uint32_t cap, uint32_t max_n, size_t nq, const uint32_t* ids,

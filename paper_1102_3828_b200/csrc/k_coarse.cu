@@ -227,6 +227,132 @@ __global__ __launch_bounds__(512) void topw_kernel(const float* __restrict__ D, 
     }
 }
 
+// Top-w by radix select (K1 epilogue for probe selection): the w-th smallest
+// distance D* is found with three 11/11/10-bit histogram passes over the row
+// staged in smem; the row's entries below D* plus the lowest-index entries
+// equal to D* (ties -> lowest centroid index) are compacted and
+// only those w keys are sorted.  Replaces a full sort of Kc keys per query.
+constexpr int TW_THREADS = 256;
+
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t* s_total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (int i = 0; i < TW_THREADS / 32; ++i) {
+            const uint32_t t = s_warp[i];
+            s_warp[i] = acc;
+            acc += t;
+        }
+        *s_total = acc;
+    }
+    __syncthreads();
+    return s_warp[warp] + incl - v;
+}
+
+__global__ __launch_bounds__(TW_THREADS) void topw_radix_kernel(const float* __restrict__ D,
+                                                                uint32_t nc, uint32_t w, uint32_t w2,
+                                                                uint32_t* __restrict__ out_idx,
+                                                                float* __restrict__ out_dist) {
+    extern __shared__ uint32_t tw_smem[];
+    uint32_t* bits = tw_smem;                                 // [nc]
+    u64* sel = reinterpret_cast<u64*>(tw_smem + ((nc + 1) & ~1u));  // [w2]
+    __shared__ uint32_t hist[2048];
+    __shared__ uint32_t s_bin, s_rank, s_cnt, s_out, s_total, s_warp[TW_THREADS / 32];
+    const size_t q = blockIdx.x;
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(D + q * nc);
+    for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) bits[i] = row[i];
+    for (uint32_t i = threadIdx.x; i < w2; i += blockDim.x) sel[i] = ~0ull;
+    if (threadIdx.x == 0) s_out = 0;
+    __syncthreads();
+    uint32_t prefix = 0, r = w;
+    const int shifts[3] = {21, 10, 0}, widths[3] = {11, 11, 10};
+    for (int pass = 0; pass < 3; ++pass) {
+        for (int b = threadIdx.x; b < 2048; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        const int sh = shifts[pass], wd = widths[pass];
+        const uint32_t msk = (1u << wd) - 1u;
+        for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+            const uint32_t u = bits[i];
+            if (pass == 0 || (u >> (sh + wd)) == prefix) atomicAdd(&hist[(u >> sh) & msk], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // bin holding rank r: lane l owns 64 bins
+            const int lane = threadIdx.x;
+            uint32_t sum = 0;
+            for (int b = 0; b < 64; ++b) sum += hist[lane * 64 + b];
+            uint32_t incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const uint32_t excl = incl - sum;
+            const bool mine = excl < r && r <= incl;
+            const unsigned who = __ballot_sync(0xffffffffu, mine);
+            if (mine && lane == __ffs(who) - 1) {
+                uint32_t cacc = excl;
+                for (int b = 0; b < 64; ++b) {
+                    const uint32_t h = hist[lane * 64 + b];
+                    if (r <= cacc + h) {
+                        s_bin = lane * 64 + b;
+                        s_rank = r - cacc;
+                        s_cnt = h;
+                        break;
+                    }
+                    cacc += h;
+                }
+            }
+        }
+        __syncthreads();
+        prefix = (prefix << wd) | s_bin;
+        r = s_rank;
+        __syncthreads();
+    }
+    const uint32_t dstar = prefix;  // exact w-th smallest distance bits; r of its ties are in
+    // strictly smaller entries: any order
+    for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x)
+        if (bits[i] < dstar) sel[atomicAdd(&s_out, 1u)] = ((u64)bits[i] << 32) | i;
+    // ties at dstar: the r lowest indices, in index order (contiguous chunks per thread)
+    const uint32_t chunk = (nc + TW_THREADS - 1) / TW_THREADS;
+    const uint32_t lo = threadIdx.x * chunk, hi = min(nc, lo + chunk);
+    uint32_t mine = 0;
+    for (uint32_t i = lo; i < hi; ++i) mine += bits[i] == dstar;
+    __syncthreads();
+    const uint32_t before = block_excl_scan(mine, s_warp, &s_total);
+    const uint32_t base_lt = w - r;
+    uint32_t k = before;
+    for (uint32_t i = lo; i < hi && k < r; ++i)
+        if (bits[i] == dstar) sel[base_lt + k++] = ((u64)dstar << 32) | i;
+    __syncthreads();
+    // sort the w selected keys (w2 = next pow2)
+    for (uint32_t kk = 2; kk <= w2; kk <<= 1) {
+        for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < w2 / 2; i += blockDim.x) {
+                const uint32_t a0 = 2 * i - (i & (j - 1)), a1 = a0 + j;
+                const bool up = (a0 & kk) == 0;
+                const u64 x = sel[a0], y = sel[a1];
+                if ((x > y) == up) {
+                    sel[a0] = y;
+                    sel[a1] = x;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < w; i += blockDim.x) {
+        out_idx[q * w + i] = key_id(sel[i]);
+        if (out_dist) out_dist[q * w + i] = key_dist(sel[i]);
+    }
+}
+
 template <int D>
 void pair_dists_t(const float* x, size_t nx, const float* c, uint32_t nc, float* out,
                   cudaStream_t s) {
@@ -307,6 +433,19 @@ void launch_argmin(const float* x, size_t nx, const float* c, uint32_t nc, uint3
 void launch_topw(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* out_idx,
                  float* out_dist, cudaStream_t s) {
     if (nq == 0) return;
+    if (w < nc) {
+        uint32_t w2 = 1;
+        while (w2 < w) w2 <<= 1;
+        const size_t smem = (size_t)((nc + 1) & ~1u) * 4 + (size_t)w2 * 8;
+        if (smem <= 200 * 1024) {
+            PQRR_CUDA(cudaFuncSetAttribute(topw_radix_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            topw_radix_kernel<<<(unsigned)nq, TW_THREADS, smem, s>>>(D, nc, w, w2, out_idx, out_dist);
+            PQRR_LAUNCH_CHECK();
+            count_launch();
+            return;
+        }
+    }
     uint32_t n2 = 1;
     while (n2 < nc) n2 <<= 1;
     size_t smem = (size_t)n2 * sizeof(u64);

@@ -21,7 +21,7 @@ constexpr int NBINS = 1 << RADIX_BITS;
 
 __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t nq, uint32_t w,
                                    const uint32_t* __restrict__ list_len, uint32_t stride,
-                                   uint32_t cap, uint64_t* __restrict__ n_entries,
+                                   uint32_t strat, uint32_t cap, uint64_t* __restrict__ n_entries,
                                    uint8_t* __restrict__ sampled, uint64_t* __restrict__ pair_samples,
                                    unsigned long long* __restrict__ grand_total) {
     size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -35,7 +35,7 @@ __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t n
     unsigned long long ssum = 0;
     for (uint32_t r = 0; r < w; ++r) {
         const uint32_t len = list_len[probes[q * w + r]];
-        const uint64_t ns = samp ? (len + stride - 1) / stride : 0;
+        const uint64_t ns = (samp && r % strat == 0) ? (len + stride - 1) / stride : 0;
         pair_samples[q * w + r] = ns;
         ssum += ns;
     }
@@ -80,7 +80,8 @@ __device__ void find_bin(const uint32_t* hist, uint32_t rank, uint32_t* s_bin, u
 // admits ~alpha*k' entries); +inf for queries scanned without sampling.
 __global__ __launch_bounds__(SEL_THREADS, 3) void sample_threshold_kernel(
     const float* __restrict__ sample, const uint64_t* __restrict__ sample_off, uint32_t w,
-    const uint8_t* __restrict__ sampled, uint32_t rank, uint32_t stage_cap, float* __restrict__ tau) {
+    const uint8_t* __restrict__ sampled, float alpha_k, const uint64_t* __restrict__ n_entries,
+    uint32_t stage_cap, float* __restrict__ tau) {
     extern __shared__ uint32_t stage[];  // the query's samples when they fit
     __shared__ uint32_t hist[NBINS];
     __shared__ uint32_t s_bin, s_rank, s_cnt, s_val;
@@ -91,7 +92,11 @@ __global__ __launch_bounds__(SEL_THREADS, 3) void sample_threshold_kernel(
     }
     const uint64_t lo = sample_off[q * w], hi = sample_off[q * w + w];
     const uint32_t n = (uint32_t)(hi - lo);
-    if (n < rank) {
+    // the sampled (stratified) probes hold n of the query's N_q entries: the
+    // sample rank matching ~alpha*k' candidates is alpha*k' * n / N_q
+    const double frac = (double)n / (double)max((unsigned long long)n_entries[q], 1ull);
+    const uint32_t rank = (uint32_t)max(1.0, ceil((double)alpha_k * frac));
+    if (n < rank || n == 0) {
         if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
         return;
     }
@@ -599,26 +604,27 @@ void set_smem(const void* f, size_t bytes) {
 }  // namespace
 
 void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
-                        uint32_t stride, uint32_t cap, uint64_t* nq_entries,
+                        uint32_t stride, uint32_t strat, uint32_t cap, uint64_t* nq_entries,
                         uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
                         cudaStream_t s) {
     if (nq == 0) return;
     query_sizes_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, s>>>(
-        probes, nq, w, list_len, stride, cap, nq_entries, query_sampled, pair_samples,
+        probes, nq, w, list_len, stride, strat, cap, nq_entries, query_sampled, pair_samples,
         reinterpret_cast<unsigned long long*>(grand_total));
     PQRR_LAUNCH_CHECK();
     count_launch();
 }
 
 void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_off, uint32_t w,
-                             size_t nq, const uint8_t* query_sampled, uint32_t rank,
-                             uint32_t max_samples, float* tau, cudaStream_t s) {
+                             size_t nq, const uint8_t* query_sampled, float alpha_k,
+                             const uint64_t* n_entries, uint32_t max_samples, float* tau,
+                             cudaStream_t s) {
     if (nq == 0) return;
     const uint32_t stage_cap = std::min<uint32_t>(max_samples, 16 * 1024);
     const size_t smem = (size_t)std::max<uint32_t>(stage_cap, 1) * sizeof(uint32_t);
     set_smem((const void*)sample_threshold_kernel, smem);
     sample_threshold_kernel<<<(unsigned)nq, SEL_THREADS, smem, s>>>(
-        sample_dist, sample_off, w, query_sampled, rank, stage_cap, tau);
+        sample_dist, sample_off, w, query_sampled, alpha_k, n_entries, stage_cap, tau);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

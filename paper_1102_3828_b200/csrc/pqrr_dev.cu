@@ -152,6 +152,18 @@ __global__ void scatter_shortlist(const u64* __restrict__ skey, const uint32_t* 
     if (j == 0) cnt[q] = scnt[r];
 }
 
+// probes of ranks r = 0, strat, 2*strat, ... as (list, pair id = q*w + r)
+__global__ void strided_pairs_kernel(const uint32_t* __restrict__ probes, size_t nq, uint32_t w,
+                                     uint32_t strat, uint32_t ws, uint32_t* __restrict__ lists,
+                                     uint32_t* __restrict__ pair_ids) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nq * ws) return;
+    const size_t q = i / ws;
+    const uint32_t r = (uint32_t)(i % ws) * strat;
+    lists[i] = probes[q * w + r];
+    pair_ids[i] = (uint32_t)(q * w + r);
+}
+
 __global__ void min_count_kernel(const uint32_t* __restrict__ cnt, size_t nq, uint32_t k,
                                  unsigned* __restrict__ flag) {
     size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -448,6 +460,63 @@ struct ShortlistDev {
     uint32_t* cnt;
 };
 
+// Work items of one pair set (see k_scan.cu): pairs (list, pair id = q*w+r)
+// sorted by list, grouped by <= 16 queries, scheduled longest first.
+struct ItemSet {
+    uint32_t* pair_sorted = nullptr;
+    uint32_t* list_cnt = nullptr;
+    uint32_t* list_first = nullptr;
+    uint32_t* item_off = nullptr;
+    uint32_t n_items = 0, c = 0;
+    uint32_t *item_list = nullptr, *item_start = nullptr, *item_nq = nullptr;
+    uint32_t *item_e0 = nullptr, *item_e1 = nullptr, *item_order = nullptr;
+    void apply(ScanArgs& a) const {
+        a.item_list = item_list;
+        a.item_start = item_start;
+        a.item_nq = item_nq;
+        a.item_e0 = item_e0;
+        a.item_e1 = item_e1;
+        a.item_order = item_order;
+        a.num_items = item_off + c;
+        a.pair_sorted = pair_sorted;
+    }
+};
+
+ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_ids, size_t np,
+                     uint32_t c, const uint32_t* list_len, cudaStream_t s) {
+    ItemSet it;
+    it.c = c;
+    uint32_t* sorted_lists = ws.alloc<uint32_t>(np);
+    it.pair_sorted = ws.alloc<uint32_t>(np);
+    sort_pairs(lists, sorted_lists, pair_ids, it.pair_sorted, np, bits_for(c), s);
+    it.list_cnt = ws.zeros<uint32_t>(c + 1);
+    launch_histogram(lists, np, c, it.list_cnt, s);
+    it.list_first = ws.alloc<uint32_t>(c + 1);
+    exclusive_scan_u32(it.list_cnt, it.list_first, c + 1, s);
+    uint32_t* items = ws.alloc<uint32_t>(c + 1);
+    launch_items_per_list(it.list_cnt, list_len, c, items, s);
+    it.item_off = ws.alloc<uint32_t>(c + 1);
+    exclusive_scan_u32(items, it.item_off, c + 1, s);
+    return it;
+}
+
+void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_len, cudaStream_t s) {
+    const uint32_t n = it.n_items;
+    it.item_list = ws.alloc<uint32_t>(n);
+    it.item_start = ws.alloc<uint32_t>(n);
+    it.item_nq = ws.alloc<uint32_t>(n);
+    it.item_e0 = ws.alloc<uint32_t>(n);
+    it.item_e1 = ws.alloc<uint32_t>(n);
+    uint32_t* key = ws.alloc<uint32_t>(n);
+    uint32_t* key2 = ws.alloc<uint32_t>(n);
+    uint32_t* iota = ws.alloc<uint32_t>(n);
+    it.item_order = ws.alloc<uint32_t>(n);
+    launch_items_build(it.list_cnt, it.list_first, list_len, c, it.item_off, it.item_list,
+                       it.item_start, it.item_nq, it.item_e0, it.item_e1, key, s);
+    launch_iota(iota, n, s);
+    sort_pairs(key, key2, iota, it.item_order, n, 32, s);
+}
+
 // Builds the exact top-kprime shortlist of every query into `out` (device,
 // [nq][kprime]).  alpha scales the sampled threshold rank (expected
 // candidates ~ alpha * kprime).
@@ -461,9 +530,11 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // candidate buffer per query: >= 4k' (the sampled threshold targets ~2k');
     // beyond 8192 the selector streams candidates from global memory
     const uint32_t cap = std::max<uint32_t>(8192, ((4 * kprime + 1023) / 1024) * 1024);
-    uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / 64.0));
+    // sample density: ~64 samples expected below the alpha*k'-th distance; the
+    // sampled probe ranks hold ~1/strat of the candidates (strat set below)
+    const uint32_t strat_h = w >= 8 ? 4 : 1;
+    uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / (64.0 * strat_h)));
     stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
-    const uint32_t rank = (uint32_t)std::ceil(alpha * kprime / stride);
     Workspace ws(s);
 
     // ---- K1: coarse distances + top-w probes
@@ -473,48 +544,37 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     launch_topw(D, nq, c, w, probes, nullptr, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[1], s));
 
-    // ---- invert probes into list-major work items
-    uint32_t* iota = ws.alloc<uint32_t>(P);
-    launch_iota(iota, P, s);
-    uint32_t* sorted_lists = ws.alloc<uint32_t>(P);
-    uint32_t* pair_sorted = ws.alloc<uint32_t>(P);
-    sort_pairs(probes, sorted_lists, iota, pair_sorted, P, bits_for(c), s);
-    uint32_t* list_cnt = ws.zeros<uint32_t>(c + 1);
-    launch_histogram(probes, P, c, list_cnt, s);
-    uint32_t* list_first = ws.alloc<uint32_t>(c + 1);
-    exclusive_scan_u32(list_cnt, list_first, c + 1, s);
-    uint32_t* items = ws.alloc<uint32_t>(c + 1);
-    launch_items_per_list(list_cnt, ix.list_len.p, c, items, s);
-    uint32_t* item_off = ws.alloc<uint32_t>(c + 1);
-    exclusive_scan_u32(items, item_off, c + 1, s);
+    // ---- invert probes into list-major work items: all pairs (main pass) and
+    // the stratified subset of probe ranks r % strat == 0 (sample pass)
+    const uint32_t strat = w >= 8 ? 4 : 1;
+    const uint32_t ws_ = (w + strat - 1) / strat;
+    const size_t Ps = nq * (size_t)ws_;
+    uint32_t* pair_ids = ws.alloc<uint32_t>(P);
+    launch_iota(pair_ids, P, s);
+    uint32_t* sp_lists = ws.alloc<uint32_t>(Ps);
+    uint32_t* sp_ids = ws.alloc<uint32_t>(Ps);
+    strided_pairs_kernel<<<nblk(Ps), 256, 0, s>>>(probes, nq, w, strat, ws_, sp_lists, sp_ids);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+    ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, s);
+    ItemSet is = items_phase1(ws, sp_lists, sp_ids, Ps, c, ix.list_len.p, s);
     uint64_t* n_entries = ws.alloc<uint64_t>(nq);
     uint8_t* sampled = ws.alloc<uint8_t>(nq);
     uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
     uint64_t* grand = ws.zeros<uint64_t>(2);
-    launch_query_sizes(probes, nq, w, ix.list_len.p, stride, cap, n_entries, sampled, pair_samples,
-                       grand, s);
+    launch_query_sizes(probes, nq, w, ix.list_len.p, stride, strat, cap, n_entries, sampled,
+                       pair_samples, grand, s);
     uint64_t* sample_off = ws.alloc<uint64_t>(P + 1);
     exclusive_scan_u64(pair_samples, sample_off, P + 1, s);
     uint64_t total_samples = 0, h_grand[2] = {0, 0};
-    uint32_t n_items = 0;
     PQRR_CUDA(cudaMemcpyAsync(h_grand, grand, 16, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&total_samples, sample_off + P, 8, cudaMemcpyDeviceToHost, s));
-    PQRR_CUDA(cudaMemcpyAsync(&n_items, item_off + c, 4, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaMemcpyAsync(&is.n_items, is.item_off + c, 4, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaStreamSynchronize(s));
-    // items: (list, query group, entry chunk), scheduled longest first
-    uint32_t* item_list = ws.alloc<uint32_t>(n_items);
-    uint32_t* item_start = ws.alloc<uint32_t>(n_items);
-    uint32_t* item_nq = ws.alloc<uint32_t>(n_items);
-    uint32_t* item_e0 = ws.alloc<uint32_t>(n_items);
-    uint32_t* item_e1 = ws.alloc<uint32_t>(n_items);
-    uint32_t* item_key = ws.alloc<uint32_t>(n_items);
-    uint32_t* item_key2 = ws.alloc<uint32_t>(n_items);
-    uint32_t* item_iota = ws.alloc<uint32_t>(n_items);
-    uint32_t* item_order = ws.alloc<uint32_t>(n_items);
-    launch_items_build(list_cnt, list_first, ix.list_len.p, c, item_off, item_list, item_start,
-                       item_nq, item_e0, item_e1, item_key, s);
-    launch_iota(item_iota, n_items, s);
-    sort_pairs(item_key, item_key2, item_iota, item_order, n_items, 32, s);
+    const uint32_t n_items = im.n_items;
+    items_phase2(ws, im, c, ix.list_len.p, s);
+    if (total_samples) items_phase2(ws, is, c, ix.list_len.p, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[2], s));
 
     ScanArgs a{};
@@ -527,14 +587,6 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     a.d = ix.d;
     a.m = ix.m;
     a.ks = ix.ks;
-    a.item_list = item_list;
-    a.item_start = item_start;
-    a.item_nq = item_nq;
-    a.item_e0 = item_e0;
-    a.item_e1 = item_e1;
-    a.item_order = item_order;
-    a.num_items = item_off + c;
-    a.pair_sorted = pair_sorted;
     a.w = w;
     a.cap = cap;
     a.query_sampled = sampled;
@@ -544,6 +596,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     float* tau = ws.alloc<float>(nq);
     float* sample_dist = ws.alloc<float>(total_samples);
     if (total_samples) {
+        is.apply(a);
         a.stride = stride;
         a.sample_off = sample_off;
         a.sample_dist = sample_dist;
@@ -552,14 +605,15 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         launch_ivf_scan(a, s);
     }
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[3], s));
-    launch_sample_threshold(sample_dist, sample_off, w, nq, sampled, rank, (uint32_t)h_grand[1],
-                            tau, s);
+    launch_sample_threshold(sample_dist, sample_off, w, nq, sampled, (float)(alpha * kprime),
+                            n_entries, (uint32_t)h_grand[1], tau, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[4], s));
 
     // ---- K4 main scan
     float* cand_dist = ws.alloc<float>(nq * (size_t)cap);
     uint32_t* cand_pos = ws.alloc<uint32_t>(nq * (size_t)cap);
     uint32_t* cand_cnt = ws.zeros<uint32_t>(nq);
+    im.apply(a);
     a.stride = 1;
     a.tau = tau;
     a.cand_dist = cand_dist;
