@@ -11,6 +11,8 @@
 // all banks (rows padded to D+4 floats).
 #include <float.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -433,7 +435,8 @@ void launch_argmin(const float* x, size_t nx, const float* c, uint32_t nc, uint3
 void launch_topw(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* out_idx,
                  float* out_dist, cudaStream_t s) {
     if (nq == 0) return;
-    if (w < nc) {
+    static const bool force_sort = getenv("PQRR_TOPW") != nullptr;
+    if (w < nc && !force_sort) {
         uint32_t w2 = 1;
         while (w2 < w) w2 <<= 1;
         const size_t smem = (size_t)((nc + 1) & ~1u) * 4 + (size_t)w2 * 8;

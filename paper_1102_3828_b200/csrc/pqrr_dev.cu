@@ -532,7 +532,11 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     const uint32_t cap = std::max<uint32_t>(8192, ((4 * kprime + 1023) / 1024) * 1024);
     // sample density: ~64 samples expected below the alpha*k'-th distance; the
     // sampled probe ranks hold ~1/strat of the candidates (strat set below)
-    const uint32_t strat_h = w >= 8 ? 4 : 1;
+    static const int strat_env = [] {
+        const char* e = getenv("PQRR_STRAT");
+        return e ? atoi(e) : 0;
+    }();
+    const uint32_t strat_h = strat_env > 0 ? (uint32_t)strat_env : (w >= 8 ? 4 : 1);
     uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / (64.0 * strat_h)));
     stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
     Workspace ws(s);
@@ -546,7 +550,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
 
     // ---- invert probes into list-major work items: all pairs (main pass) and
     // the stratified subset of probe ranks r % strat == 0 (sample pass)
-    const uint32_t strat = w >= 8 ? 4 : 1;
+    const uint32_t strat = strat_h;
     const uint32_t ws_ = (w + strat - 1) / strat;
     const size_t Ps = nq * (size_t)ws_;
     uint32_t* pair_ids = ws.alloc<uint32_t>(P);
