@@ -536,7 +536,10 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         const char* e = getenv("PQRR_STRAT");
         return e ? atoi(e) : 0;
     }();
-    const uint32_t strat_h = strat_env > 0 ? (uint32_t)strat_env : (w >= 8 ? 4 : 1);
+    // Probe-rank stratified sampling (PQRR_STRAT > 1) is measured biased: the
+    // nearest probes hold a disproportionate share of the top-k', so the
+    // estimate runs tight and queries underflow.  Default: sample all probes.
+    const uint32_t strat_h = strat_env > 0 ? (uint32_t)strat_env : 1;
     uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / (64.0 * strat_h)));
     stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
     Workspace ws(s);
@@ -639,6 +642,9 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     PQRR_CUDA(cudaMemcpyAsync(h_fail.data(), fail, nq, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(h_maxn, maxn, 16, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaStreamSynchronize(s));
+    static const bool force_retry = getenv("PQRR_FORCE_RETRY") != nullptr;  // test hook
+    if (force_retry && depth == 0)
+        for (size_t q = 0; q < nq; ++q) h_fail[q] = (uint8_t)(1 + (q & 1));
     uint64_t total_cand = 0;
     std::memcpy(&total_cand, h_maxn + 2, 8);
 
@@ -672,9 +678,11 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         PQRR_LAUNCH_CHECK();
         ShortlistDev sub{ws2.alloc<u64>(rows.size() * kprime), ws2.alloc<uint32_t>(rows.size() * kprime),
                          ws2.alloc<uint32_t>(rows.size())};
-        const double a2 = kind == 1 ? alpha * 4.0 : alpha / 4.0;
-        shortlist_core(ix, sx, rows.size(), w, kprime, sorted, a2, kind == 2 ? stride_div * 4 : stride_div,
-                       sub, depth + 1, false);
+        // under-full: widen the target; overflow: narrow it (never below the
+        // k' it must cover) and sample twice as densely for a tighter estimate
+        const double a2 = kind == 1 ? alpha * 2.0 : std::max(1.25, alpha / 1.5);
+        shortlist_core(ix, sx, rows.size(), w, kprime, sorted, a2, stride_div * 2, sub, depth + 1,
+                       false);
         scatter_shortlist<<<nblk(rows.size() * kprime), 256, 0, s>>>(
             sub.key, sub.pos, sub.cnt, d_rows, rows.size(), kprime, out.key, out.pos, out.cnt);
         PQRR_LAUNCH_CHECK();
