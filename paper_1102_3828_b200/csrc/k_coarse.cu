@@ -436,7 +436,9 @@ void launch_topw(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* o
                  float* out_dist, cudaStream_t s) {
     if (nq == 0) return;
     static const bool force_sort = getenv("PQRR_TOPW") != nullptr;
-    if (w < nc && !force_sort) {
+    // radix select wins for large Kc (8192: 5.65 -> 2.33 ms per 10k queries);
+    // the full bitonic sort is faster for Kc <= 2048 (measured 0.54 vs 0.61 ms)
+    if (w < nc && nc > 2048 && !force_sort) {
         uint32_t w2 = 1;
         while (w2 < w) w2 <<= 1;
         const size_t smem = (size_t)((nc + 1) & ~1u) * 4 + (size_t)w2 * 8;

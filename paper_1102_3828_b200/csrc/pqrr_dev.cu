@@ -558,13 +558,16 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     const size_t Ps = nq * (size_t)ws_;
     uint32_t* pair_ids = ws.alloc<uint32_t>(P);
     launch_iota(pair_ids, P, s);
-    uint32_t* sp_lists = ws.alloc<uint32_t>(Ps);
-    uint32_t* sp_ids = ws.alloc<uint32_t>(Ps);
-    strided_pairs_kernel<<<nblk(Ps), 256, 0, s>>>(probes, nq, w, strat, ws_, sp_lists, sp_ids);
-    PQRR_LAUNCH_CHECK();
-    count_launch();
     ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, s);
-    ItemSet is = items_phase1(ws, sp_lists, sp_ids, Ps, c, ix.list_len.p, s);
+    ItemSet is = im;  // sample pass: same items unless stratified
+    if (strat > 1) {
+        uint32_t* sp_lists = ws.alloc<uint32_t>(Ps);
+        uint32_t* sp_ids = ws.alloc<uint32_t>(Ps);
+        strided_pairs_kernel<<<nblk(Ps), 256, 0, s>>>(probes, nq, w, strat, ws_, sp_lists, sp_ids);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        is = items_phase1(ws, sp_lists, sp_ids, Ps, c, ix.list_len.p, s);
+    }
     uint64_t* n_entries = ws.alloc<uint64_t>(nq);
     uint8_t* sampled = ws.alloc<uint8_t>(nq);
     uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
@@ -577,11 +580,12 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     PQRR_CUDA(cudaMemcpyAsync(h_grand, grand, 16, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&total_samples, sample_off + P, 8, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
-    PQRR_CUDA(cudaMemcpyAsync(&is.n_items, is.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+    if (strat > 1) PQRR_CUDA(cudaMemcpyAsync(&is.n_items, is.item_off + c, 4, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaStreamSynchronize(s));
     const uint32_t n_items = im.n_items;
     items_phase2(ws, im, c, ix.list_len.p, s);
-    if (total_samples) items_phase2(ws, is, c, ix.list_len.p, s);
+    if (strat == 1) is = im;
+    else if (total_samples) items_phase2(ws, is, c, ix.list_len.p, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[2], s));
 
     ScanArgs a{};
