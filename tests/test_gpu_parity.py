@@ -219,6 +219,27 @@ def test_search_matches_oracle(mid_instance, v, kprime, k):
     assert st["kernels"] > 5 and st["ms_scan"] > 0
 
 
+def test_large_coarse_radix_probe_selection(pq, oracle):
+    """Kc > 2048 takes the radix-select top-w path; duplicated centroids force
+    exact coarse-distance ties that must resolve to the lowest list index."""
+    rng = np.random.default_rng(21)
+    base = rng.integers(0, 50, (30000, 128)).astype(np.uint8)
+    coarse = base[rng.choice(30000, 4096, replace=False)].astype(np.float32)
+    coarse[100:140] = coarse[7]
+    books = (rng.standard_normal((8, 256, 16)) * 8).astype(np.float32)
+    P = pqobj(pq, books, 8)
+    dix = pq.ivf_build(pq.Codebook(coarse), P, base)
+    oix = oracle.ivf_build(coarse, books.reshape(-1), 8, base.astype(np.float32))
+    q = np.vstack([base[:20], coarse[7:8].astype(np.uint8)])
+    for v, kp in [(64, 200), (200, 1000)]:
+        oi, od, oc = oix.search(q.astype(np.float32), v, kp)
+        di, dd, dc = dix.search(q, v, kp, 0)
+        np.testing.assert_array_equal(dc, oc)
+        for i in range(len(q)):
+            np.testing.assert_array_equal(di[i, :oc[i]], oi[i, :oc[i]])
+            np.testing.assert_array_equal(bits(dd[i, :oc[i]]), bits(od[i, :oc[i]]))
+
+
 # ------------------------------------------------------------------ reference-side C++ drop-in
 def test_reference_api_shim():
     """integration/test_shim: a caller of the reference's own pqrr:: API
