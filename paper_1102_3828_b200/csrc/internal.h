@@ -135,6 +135,10 @@ struct ScanArgs {
     const uint32_t* item_e0;     // entry range of the list covered by the item
     const uint32_t* item_e1;
     const uint32_t* item_order;  // items sorted longest first
+    // LUT reuse across passes: 0 = build, 1 = build + store to lut_cache
+    // (sample pass), 2 = bulk-load from lut_cache (main pass)
+    int lut_mode;
+    float* lut_cache;            // [items][8 * 256 * 16] floats
     const uint32_t* num_items;   // device scalar
     uint32_t* item_counter;      // device scalar, zeroed before launch
     const uint32_t* pair_sorted;  // pair index q * w + r, grouped by list

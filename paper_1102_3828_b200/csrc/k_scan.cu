@@ -118,10 +118,19 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
     __shared__ float s_tau[QT];
     __shared__ uint8_t s_samp[QT];
 
+    __shared__ __align__(8) unsigned long long s_bar;  // TMA completion barrier (lut_mode 2)
+    unsigned bar_phase = 0;
+
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int slot = lane >> 2, qd = lane & 3;
     const uint32_t n_items = *a.num_items;
     const float4* lut4 = reinterpret_cast<const float4*>(lut);
+    if (threadIdx.x == 0) {
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
 
     for (;;) {
         if (threadIdx.x == 0) {
@@ -148,15 +157,45 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
             s_samp[threadIdx.x] = (q >= 0 && a.query_sampled) ? a.query_sampled[q] : 0;
         }
         __syncthreads();
-        // residual queries x - C_l (ivf_index.hpp:58-59)
-        const float* crow = a.coarse + (size_t)l * a.d;
-        for (uint32_t idx = threadIdx.x; idx < QT * a.d; idx += NT) {
-            const uint32_t qq = idx / a.d, t = idx % a.d;
-            const int q = s_q[qq];
-            xr[qq * xld + t] = q >= 0 ? __fsub_rn(a.xq[(size_t)q * a.d + t], crow[t]) : 0.f;
+        if (a.lut_mode == 2) {
+            // main pass after a sample pass: the item's LUT was cached in HBM
+            // by the sample pass; one TMA bulk copy brings it back (128 KiB)
+            if (threadIdx.x == 0) {
+                const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(lut);
+                const float* src = a.lut_cache + (size_t)it * LUT_FLOATS;
+                // order the previous item's generic smem reads before async-proxy writes
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             ::"r"(bar), "r"((unsigned)(LUT_FLOATS * 4)) : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                    ::"r"(dst), "l"(src), "r"((unsigned)(LUT_FLOATS * 4)), "r"(bar) : "memory");
+            }
+            const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
+            unsigned done = 0;
+            while (!done) {
+                asm volatile(
+                    "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                    : "=r"(done) : "r"(bar), "r"(bar_phase) : "memory");
+            }
+            bar_phase ^= 1u;
+        } else {
+            // residual queries x - C_l (ivf_index.hpp:58-59)
+            const float* crow = a.coarse + (size_t)l * a.d;
+            for (uint32_t idx = threadIdx.x; idx < QT * a.d; idx += NT) {
+                const uint32_t qq = idx / a.d, t = idx % a.d;
+                const int q = s_q[qq];
+                xr[qq * xld + t] = q >= 0 ? __fsub_rn(a.xq[(size_t)q * a.d + t], crow[t]) : 0.f;
+            }
+            __syncthreads();
+            build_luts<DSUB>(lut, xr, xld, a.books, bbuf, nz);
+            if (a.lut_mode == 1) {  // sample pass: keep the LUT for the main pass
+                float4* dst = reinterpret_cast<float4*>(a.lut_cache + (size_t)it * LUT_FLOATS);
+                const float4* src4 = reinterpret_cast<const float4*>(lut);
+                for (int i = threadIdx.x; i < LUT_FLOATS / 4; i += NT) __stcs(dst + i, src4[i]);
+            }
         }
-        __syncthreads();
-        build_luts<DSUB>(lut, xr, xld, a.books, bbuf, nz);
 
         // this item's entry range [e0, e1) of the list (long lists are chunked)
         const uint64_t off = a.list_off[l] + e0;

@@ -606,8 +606,19 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // ---- sample pass (threshold estimation)
     float* tau = ws.alloc<float>(nq);
     float* sample_dist = ws.alloc<float>(total_samples);
+    // LUT reuse: the sample pass stores each item's LUT, the main pass
+    // bulk-loads it (same item set when not stratified; bounded by free HBM)
+    a.lut_mode = 0;
+    a.lut_cache = nullptr;
+    if (total_samples && strat == 1) {
+        size_t free_b = 0, total_b = 0;
+        PQRR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const size_t need = (size_t)n_items * 8 * 256 * 16 * sizeof(float);
+        if (ix.m == 8 && ix.ks == 256 && need < free_b / 2) a.lut_cache = ws.alloc<float>(need / 4);
+    }
     if (total_samples) {
         is.apply(a);
+        a.lut_mode = a.lut_cache ? 1 : 0;
         a.stride = stride;
         a.sample_off = sample_off;
         a.sample_dist = sample_dist;
@@ -625,6 +636,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     uint32_t* cand_pos = ws.alloc<uint32_t>(nq * (size_t)cap);
     uint32_t* cand_cnt = ws.zeros<uint32_t>(nq);
     im.apply(a);
+    a.lut_mode = (total_samples && a.lut_cache) ? 2 : 0;
     a.stride = 1;
     a.tau = tau;
     a.cand_dist = cand_dist;
