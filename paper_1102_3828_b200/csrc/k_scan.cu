@@ -136,6 +136,8 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
         if (threadIdx.x == 0) {
             const uint32_t c = atomicAdd(a.item_counter, 1u);
             s_item = c < n_items ? a.item_order[c] : 0xffffffffu;  // longest items first
+            // the previous item's bulk LUT store must have read smem before reuse
+            if (a.lut_mode == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
         __syncthreads();
         const uint32_t it = s_item;
@@ -190,10 +192,19 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
             }
             __syncthreads();
             build_luts<DSUB>(lut, xr, xld, a.books, bbuf, nz);
-            if (a.lut_mode == 1) {  // sample pass: keep the LUT for the main pass
-                float4* dst = reinterpret_cast<float4*>(a.lut_cache + (size_t)it * LUT_FLOATS);
-                const float4* src4 = reinterpret_cast<const float4*>(lut);
-                for (int i = threadIdx.x; i < LUT_FLOATS / 4; i += NT) __stcs(dst + i, src4[i]);
+            if (a.lut_mode == 1) {
+                // sample pass: keep the LUT for the main pass with an async TMA
+                // bulk store that overlaps this item's sampled scan; it is
+                // waited for (read side) before the LUT smem is rewritten
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    const unsigned src = (unsigned)__cvta_generic_to_shared(lut);
+                    float* dst = a.lut_cache + (size_t)it * LUT_FLOATS;
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                                 ::"l"(dst), "r"(src), "r"((unsigned)(LUT_FLOATS * 4)) : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
             }
         }
 
@@ -316,6 +327,8 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
         }
         __syncthreads();
     }
+    // drain outstanding bulk LUT stores before the CTA retires
+    if (threadIdx.x == 0 && a.lut_mode == 1) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Kernel seam helpers (kernels::scan_topk / build_lut parity).
