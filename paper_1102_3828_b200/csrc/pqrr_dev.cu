@@ -264,6 +264,7 @@ struct DevIndex {
     DBuf<uint8_t> codes, rcodes;
     DBuf<uint32_t> ids;
     DBuf<uint16_t> block_list;  // list of each 16-entry block of positions
+    DBuf<float> lut_cache;      // per-item LUTs shared by the sample and main passes
     uint64_t next_id = 0;
     // id -> position (lazy)
     DBuf<uint32_t> id_map;
@@ -614,7 +615,13 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         size_t free_b = 0, total_b = 0;
         PQRR_CUDA(cudaMemGetInfo(&free_b, &total_b));
         const size_t need = (size_t)n_items * 8 * 256 * 16 * sizeof(float);
-        if (ix.m == 8 && ix.ks == 256 && need < free_b / 2) a.lut_cache = ws.alloc<float>(need / 4);
+        // persistent (index-owned) buffer: a per-search allocation of several
+        // GB was measured to pay first-touch costs on every batch
+        if (ix.m == 8 && ix.ks == 256) {
+            if (ix.lut_cache.bytes() < need && need - ix.lut_cache.bytes() < free_b / 2)
+                ix.lut_cache.alloc(need / 4);
+            if (ix.lut_cache.bytes() >= need) a.lut_cache = ix.lut_cache.p;
+        }
     }
     if (total_samples) {
         is.apply(a);
