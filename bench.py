@@ -42,6 +42,8 @@ CONFIGS = {
                w=16, kprime=1000, k=100),
     "C3": dict(n=100_000_000, train=1_000_000, nq=10_000, clusters=4096, kc=8192, m=8, mprime=16,
                w=64, kprime=1000, k=100),
+    "C4": dict(n=1_000_000_000, train=1_000_000, nq=10_000, clusters=4096, kc=8192, m=8,
+               mprime=32, w=64, kprime=10_000, k=100),
 }
 SEED = 0
 METRIC = "IVFADC+R queries/sec at oracle-matched recall@1/10/100; scan HBM GB/s"

@@ -400,6 +400,17 @@ void finalize(DevIndex& ix) {
     }
     launch_layout_place_new(skeys, sidx, n, stage_off, d_off.p, d_oldlen.p, ix.st_codes.p,
                             ix.st_rcodes.p, ix.st_ids.p, ix.m, ix.mprime, codes.p, ids.p, rcodes.p, s);
+    // Staging (and the previous layout) are dead once placed: release them
+    // before the pairing copy so a 1B-entry build peaks near 2.5x the index.
+    PQRR_CUDA(cudaStreamSynchronize(s));
+    ix.st_assign.release();
+    ix.st_ids.release();
+    ix.st_codes.release();
+    ix.st_rcodes.release();
+    ix.st_cap = 0;
+    ix.codes.release();
+    ix.ids.release();
+    ix.rcodes.release();
     if (ix.m == 8) {
         // parity-balanced order inside every list (bank-conflict-free LUT gathers)
         std::vector<uint64_t> h_end(c);
