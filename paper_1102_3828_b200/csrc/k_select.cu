@@ -546,6 +546,78 @@ __global__ __launch_bounds__(RW_WARPS * 32) void rerank_warp_kernel(
     if (threadIdx.x == 0) out_cnt[q] = cnt;
 }
 
+// K5a: refined distances of every shortlist entry, one thread per candidate
+// (no shared memory, full occupancy: the random code / code-book gathers are
+// latency bound).  Rows shorter than the stride are padded with +inf keys.
+template <bool FAST>
+__global__ __launch_bounds__(256) void rerank_dist_kernel(
+    const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
+    const uint32_t* __restrict__ sl_cnt, uint32_t stride, size_t nq, const float* __restrict__ xq,
+    uint32_t d, const uint16_t* __restrict__ block_list, const float* __restrict__ coarse,
+    const uint8_t* __restrict__ codes, const float* __restrict__ books, uint32_t m,
+    const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks, uint32_t mprime,
+    uint32_t ks, float* __restrict__ rdist, uint32_t* __restrict__ rid, u64 nz) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nq * stride) return;
+    const size_t q = t / stride;
+    const uint32_t i = (uint32_t)(t % stride);
+    if (i >= sl_cnt[q]) return;
+    const uint32_t p = sl_pos[t];
+    const uint32_t l = block_list[p >> 4];
+    rid[t] = key_id(sl_key[t]);
+    rdist[t] = rerank_dist<FAST>(xq + q * d, d, coarse + (size_t)l * d, books, codes + (size_t)p * m,
+                                 d / m, rbooks, rcodes + (size_t)p * mprime, d / mprime, ks, nz);
+}
+
+// K5b: top-k of (rdist, rid) rows under (dist, id): radix select on the
+// distance bits (rows streamed from L2), ties at the boundary broken by id,
+// then the k winners sorted in shared memory.
+__global__ __launch_bounds__(SEL_THREADS) void rerank_topk_kernel(
+    const float* __restrict__ rdist, const uint32_t* __restrict__ rid,
+    const uint32_t* __restrict__ cnt_in, uint32_t stride, uint32_t k, uint32_t k2,
+    uint32_t* __restrict__ out_ids, float* __restrict__ out_dists, uint32_t* __restrict__ out_cnt) {
+    extern __shared__ u64 tk_keys[];
+    __shared__ uint32_t hist[NBINS];
+    __shared__ uint32_t s_bin, s_rank, s_cnt, s_val, s_out;
+    const size_t q = blockIdx.x;
+    const uint32_t n = cnt_in[q];
+    const uint32_t* db = reinterpret_cast<const uint32_t*>(rdist) + q * stride;
+    const uint32_t* ib = rid + q * stride;
+    for (uint32_t i = threadIdx.x; i < k2; i += blockDim.x) tk_keys[i] = ~0ull;
+    if (threadIdx.x == 0) s_out = 0;
+    __syncthreads();
+    uint32_t dstar = 0xffffffffu, r = 0, ceq = 0;
+    if (n > k)
+        radix_select32(n, k, [&](uint32_t i) { return db[i]; }, [](uint32_t) { return true; }, hist,
+                       &s_bin, &s_rank, &s_cnt, &s_val, dstar, r, ceq);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t u = db[i];
+        if (n <= k || u < dstar) tk_keys[atomicAdd(&s_out, 1u)] = ((u64)u << 32) | ib[i];
+    }
+    if (n > k) {
+        uint32_t idstar = 0xffffffffu, r2 = 0, c2 = 0;
+        const bool all_ties = (r == ceq);
+        if (!all_ties)
+            radix_select32(n, r, [&](uint32_t i) { return ib[i]; },
+                           [&](uint32_t i) { return db[i] == dstar; }, hist, &s_bin, &s_rank, &s_cnt,
+                           &s_val, idstar, r2, c2);
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+            if (db[i] == dstar && (all_ties || ib[i] <= idstar))
+                tk_keys[atomicAdd(&s_out, 1u)] = ((u64)dstar << 32) | ib[i];
+    }
+    __syncthreads();
+    bitonic_sort_kv(tk_keys, nullptr, k2);
+    const uint32_t cnt = min(n, k);
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+        const bool live = i < cnt;
+        out_ids[q * k + i] = live ? key_id(tk_keys[i]) : 0xffffffffu;
+        out_dists[q * k + i] = live ? key_dist(tk_keys[i]) : __int_as_float(0x7f800000);
+    }
+    if (threadIdx.x == 0) out_cnt[q] = cnt;
+}
+
 // K7: merge of per-shard ranked lists (all-gathered [parts][nq][width]) into
 // the global top-k under (dist, id) — one CTA per query, bitonic in smem.
 __global__ __launch_bounds__(256) void merge_topk_kernel(
@@ -677,11 +749,40 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
     const size_t smem = ((d + 3) & ~3u) * sizeof(float) + (size_t)n2 * sizeof(u64);
     if (smem > 200 * 1024) throw ArgError("shortlist too large for the device re-ranker");
     const bool fast = d % 4 == 0 && (d / m) % 4 == 0 && (d / mprime) % 4 == 0;
-    // PQRR_RERANK=warp selects the warp-cooperative variant (A/B measurements)
-    static const bool want_warp = [] {
+    // default: split K5a (distances, full occupancy) + K5b (top-k);
+    // PQRR_RERANK=cta|warp select the single-kernel variants (A/B measurements)
+    static const std::string impl = [] {
         const char* e = getenv("PQRR_RERANK");
-        return e && std::string(e) == "warp";
+        return std::string(e ? e : "split");
     }();
+    const bool want_warp = impl == "warp";
+    uint32_t k2 = 1;
+    while (k2 < k) k2 <<= 1;
+    if (impl == "split" && (size_t)k2 * 8 <= 200 * 1024) {
+        const size_t tot = nq * (size_t)sl_stride;
+        float* rd = nullptr;
+        uint32_t* ri = nullptr;
+        PQRR_CUDA(cudaMallocAsync(&rd, tot * sizeof(float), s));
+        PQRR_CUDA(cudaMallocAsync(&ri, tot * sizeof(uint32_t), s));
+        const unsigned g = (unsigned)((tot + 255) / 256);
+        if (fast)
+            rerank_dist_kernel<true><<<g, 256, 0, s>>>(
+                reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, nq, xq, d,
+                block_list, coarse, codes, books, m, rcodes, rbooks, mprime, ks, rd, ri, kNegZero2);
+        else
+            rerank_dist_kernel<false><<<g, 256, 0, s>>>(
+                reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, nq, xq, d,
+                block_list, coarse, codes, books, m, rcodes, rbooks, mprime, ks, rd, ri, kNegZero2);
+        PQRR_LAUNCH_CHECK();
+        set_smem((const void*)rerank_topk_kernel, (size_t)k2 * 8);
+        rerank_topk_kernel<<<(unsigned)nq, SEL_THREADS, (size_t)k2 * 8, s>>>(
+            rd, ri, sl_cnt, sl_stride, k, k2, out_ids, out_dists, out_cnt);
+        PQRR_LAUNCH_CHECK();
+        PQRR_CUDA(cudaFreeAsync(rd, s));
+        PQRR_CUDA(cudaFreeAsync(ri, s));
+        count_launch(2);
+        return;
+    }
     if (want_warp && fast && d == 128 && m == 8 && mprime % 8 == 0 && mprime <= 32) {
         const size_t wsmem = (size_t)RW_WARPS * 32 * RW_LD * sizeof(float4) + (size_t)n2 * sizeof(u64);
         if (wsmem > 220 * 1024) throw ArgError("shortlist too large for the device re-ranker");
