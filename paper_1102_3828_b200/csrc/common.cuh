@@ -86,17 +86,6 @@ __device__ __forceinline__ float l2sq_packed(const float* __restrict__ a,
     return __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
 }
 
-// Warp-aggregated shared-memory histogram increment: lanes hitting the same
-// bin combine into one atomic.  Radix passes over distances of one query
-// concentrate on a handful of bins (shared exponent / leading mantissa bits)
-// and would otherwise serialize on same-address atomics.
-__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bin, bool active) {
-    const unsigned mask = __activemask();
-    const unsigned peers = __match_any_sync(mask, active ? bin : 0xffffffffu);
-    if (active && (int)(threadIdx.x & 31) == __ffs(peers) - 1)
-        atomicAdd(&hist[bin], (unsigned)__popc(peers));
-}
-
 // Total order of types.hpp:47-50 on (dist, id) as one 64-bit key.  Distances
 // are non-negative (sums of squares starting at +0), so the IEEE bit pattern
 // orders like the value.

@@ -283,7 +283,7 @@ __global__ __launch_bounds__(TW_THREADS) void topw_radix_kernel(const float* __r
         const uint32_t msk = (1u << wd) - 1u;
         for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
             const uint32_t u = bits[i];
-            hist_add(hist, (u >> sh) & msk, pass == 0 || (u >> (sh + wd)) == prefix);
+            if (pass == 0 || (u >> (sh + wd)) == prefix) atomicAdd(&hist[(u >> sh) & msk], 1u);
         }
         __syncthreads();
         if (threadIdx.x < 32) {  // bin holding rank r: lane l owns 64 bins

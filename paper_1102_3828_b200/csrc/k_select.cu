@@ -117,7 +117,7 @@ __global__ __launch_bounds__(SEL_THREADS, 3) void sample_threshold_kernel(
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
             const uint32_t u = src[i];
             const bool match = pass == 0 ? true : ((u >> (sh + wd)) == prefix);
-            hist_add(hist, (u >> sh) & msk, match);
+            if (match) atomicAdd(&hist[(u >> sh) & msk], 1u);
         }
         __syncthreads();
         find_bin(hist, r, &s_bin, &s_rank, &s_cnt);
@@ -193,7 +193,7 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void select_topk_kernel(
             for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
                 const u64 k = skeys[i];
                 const bool match = consumed == 0 ? true : ((k >> (sh + wd)) == prefix);
-                hist_add(hist, (uint32_t)((k >> sh) & msk), match);
+                if (match) atomicAdd(&hist[(uint32_t)((k >> sh) & msk)], 1u);
             }
             __syncthreads();
             find_bin(hist, r, &s_bin, &s_rank, &s_bincnt);
@@ -256,9 +256,9 @@ __device__ void radix_select32(uint32_t n, uint32_t rank, KeyF key, PredF pred, 
         const int sh = shifts[pass], wd = widths[pass];
         const uint32_t msk = (1u << wd) - 1u;
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-            const bool ok = pred(i);
-            const uint32_t u = ok ? key(i) : 0u;
-            hist_add(hist, (u >> sh) & msk, ok && (pass == 0 || (u >> (sh + wd)) == prefix));
+            if (!pred(i)) continue;
+            const uint32_t u = key(i);
+            if (pass == 0 || (u >> (sh + wd)) == prefix) atomicAdd(&hist[(u >> sh) & msk], 1u);
         }
         __syncthreads();
         find_bin(hist, r, s_bin, s_rank, s_cnt);
