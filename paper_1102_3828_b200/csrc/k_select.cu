@@ -76,15 +76,43 @@ __device__ void find_bin(const uint32_t* hist, uint32_t rank, uint32_t* s_bin, u
     }
 }
 
+// Applies f to every u32 of src[0, n) with 16-byte loads, 4 in flight per
+// thread (the passes over the sample are latency bound).  src may start at any
+// 4-byte alignment.
+template <class F>
+__device__ __forceinline__ void for_each_u32(const uint32_t* __restrict__ src, uint32_t n, F f) {
+    const uint32_t head = min((uint32_t)((4 - ((reinterpret_cast<uintptr_t>(src) >> 2) & 3)) & 3), n);
+    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) f(__ldg(src + i));
+    const uint32_t nv = (n - head) / 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    uint32_t v = threadIdx.x;
+    for (; v + 3 * blockDim.x < nv; v += 4 * blockDim.x) {
+        uint4 x[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) x[t] = __ldg(s4 + v + t * blockDim.x);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) { f(x[t].x); f(x[t].y); f(x[t].z); f(x[t].w); }
+    }
+    for (; v < nv; v += blockDim.x) {
+        const uint4 x = __ldg(s4 + v);
+        f(x.x); f(x.y); f(x.z); f(x.w);
+    }
+    for (uint32_t i = head + 4 * nv + threadIdx.x; i < n; i += blockDim.x) f(__ldg(src + i));
+}
+
 // tau_q = rank-th smallest sampled distance (an estimate of the distance that
 // admits ~alpha*k' entries); +inf for queries scanned without sampling.
-__global__ __launch_bounds__(SEL_THREADS, 3) void sample_threshold_kernel(
+// Pass 0 histograms the top 11 bits straight from global memory; a second
+// (L2-resident) read compacts the selected bin into shared memory when it
+// fits stage_cap, and the remaining 11- and 10-bit passes run over that small
+// set only.  A bin larger than stage_cap keeps reading global memory.
+__global__ __launch_bounds__(SEL_THREADS, 4) void sample_threshold_kernel(
     const float* __restrict__ sample, const uint64_t* __restrict__ sample_off, uint32_t w,
     const uint8_t* __restrict__ sampled, float alpha_k, const uint64_t* __restrict__ n_entries,
     uint32_t stage_cap, float* __restrict__ tau) {
-    extern __shared__ uint32_t stage[];  // the query's samples when they fit
+    extern __shared__ uint32_t stage[];  // the selected top-bits bin
     __shared__ uint32_t hist[NBINS];
-    __shared__ uint32_t s_bin, s_rank, s_cnt, s_val;
+    __shared__ uint32_t s_bin, s_rank, s_cnt, s_val, s_fill;
     const size_t q = blockIdx.x;
     if (!sampled[q]) {
         if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
@@ -100,37 +128,45 @@ __global__ __launch_bounds__(SEL_THREADS, 3) void sample_threshold_kernel(
         if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
         return;
     }
-    const bool staged = n <= stage_cap;
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(sample) + lo;
-    if (staged) {
-        // 16-byte loads, 4 in flight per thread (the staging is latency bound)
-        const uint32_t head = (uint32_t)((4 - (lo & 3)) & 3);  // floats to 16-B alignment
-        for (uint32_t i = threadIdx.x; i < min(head, n); i += blockDim.x) stage[i] = src[i];
-        const uint32_t nv = n > head ? (n - head) / 4 : 0;
-        const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
-#pragma unroll 4
-        for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) {
-            const uint4 x = __ldg(s4 + v);
-            stage[head + 4 * v] = x.x;
-            stage[head + 4 * v + 1] = x.y;
-            stage[head + 4 * v + 2] = x.z;
-            stage[head + 4 * v + 3] = x.w;
-        }
-        for (uint32_t i = head + 4 * nv + threadIdx.x; i < n; i += blockDim.x) stage[i] = src[i];
+    const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(sample) + lo;
+    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) hist[b] = 0;
+    if (threadIdx.x == 0) s_fill = 0;
+    __syncthreads();
+    for_each_u32(gsrc, n, [&](uint32_t u) { atomicAdd(&hist[u >> 21], 1u); });
+    __syncthreads();
+    find_bin(hist, rank, &s_bin, &s_rank, &s_cnt);
+    __syncthreads();
+    uint32_t prefix = s_bin, r = s_rank;
+    const uint32_t cnt = s_cnt;
+    const uint32_t* src = gsrc;
+    uint32_t ns = n;
+    if (cnt <= stage_cap) {
+        const uint32_t top = prefix;
+        for_each_u32(gsrc, n, [&](uint32_t u) {
+            if ((u >> 21) == top) stage[atomicAdd(&s_fill, 1u)] = u;
+        });
+        __syncthreads();
         src = stage;
+        ns = cnt;
     }
-    uint32_t prefix = 0, r = rank;
-    const int shifts[3] = {21, 10, 0};
-    const int widths[3] = {11, 11, 10};
-    for (int pass = 0; pass < 3; ++pass) {
+    const int shifts[2] = {10, 0};
+    const int widths[2] = {11, 10};
+    bool done = false;
+    if (cnt == 1) {  // the bin holds a single value: it is the answer
+        for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x)
+            if ((src[i] >> 21) == prefix) s_val = src[i];
+        __syncthreads();
+        prefix = s_val;
+        done = true;
+    }
+    for (int pass = 0; pass < 2 && !done; ++pass) {
         for (int b = threadIdx.x; b < NBINS; b += blockDim.x) hist[b] = 0;
         __syncthreads();
         const int sh = shifts[pass], wd = widths[pass];
         const uint32_t msk = (1u << wd) - 1u;
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
             const uint32_t u = src[i];
-            const bool match = pass == 0 ? true : ((u >> (sh + wd)) == prefix);
-            if (match) atomicAdd(&hist[(u >> sh) & msk], 1u);
+            if ((u >> (sh + wd)) == prefix) atomicAdd(&hist[(u >> sh) & msk], 1u);
         }
         __syncthreads();
         find_bin(hist, r, &s_bin, &s_rank, &s_cnt);
@@ -138,7 +174,7 @@ __global__ __launch_bounds__(SEL_THREADS, 3) void sample_threshold_kernel(
         prefix = (prefix << wd) | s_bin;
         r = s_rank;
         if (s_cnt == 1 && sh > 0) {  // unique value left under this prefix
-            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+            for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x)
                 if ((src[i] >> sh) == prefix) s_val = src[i];
             __syncthreads();
             prefix = s_val;
@@ -705,7 +741,7 @@ void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_of
                              const uint64_t* n_entries, uint32_t max_samples, float* tau,
                              cudaStream_t s) {
     if (nq == 0) return;
-    const uint32_t stage_cap = std::min<uint32_t>(max_samples, 16 * 1024);
+    const uint32_t stage_cap = std::min<uint32_t>(max_samples, 8 * 1024);
     const size_t smem = (size_t)std::max<uint32_t>(stage_cap, 1) * sizeof(uint32_t);
     set_smem((const void*)sample_threshold_kernel, smem);
     sample_threshold_kernel<<<(unsigned)nq, SEL_THREADS, smem, s>>>(
