@@ -135,10 +135,13 @@ struct ScanArgs {
     const uint32_t* item_e0;     // entry range of the list covered by the item
     const uint32_t* item_e1;
     const uint32_t* item_order;  // items sorted longest first
-    // LUT reuse across passes: 0 = build, 1 = build + store to lut_cache
-    // (sample pass), 2 = bulk-load from lut_cache (main pass)
-    int lut_mode;
-    float* lut_cache;            // [items][8 * 256 * 16] floats
+    // pass 0 = exact main scan (LUT rebuilt, candidates <= tau emitted with
+    // their exact distance); pass 1 = LUT pass: build each item's exact LUT,
+    // write the sampled distances (sample_dist != null) and, when q8_cache is
+    // set, the item's 8-bit LUT + per-query (scale, sum of minima) for K4f.
+    int pass;
+    uint8_t* q8_cache;           // [items][8][256][16] bytes
+    float* q8_param;             // [items][16][2]: scale s, sum_j min_j
     const uint32_t* num_items;   // device scalar
     uint32_t* item_counter;      // device scalar, zeroed before launch
     const uint32_t* pair_sorted;  // pair index q * w + r, grouped by list
@@ -149,7 +152,7 @@ struct ScanArgs {
     uint32_t* cand_pos;
     uint32_t* cand_cnt;
     uint32_t cap;
-    // sample mode (stride > 1)
+    // sample mode (pass 1, sample_dist != null)
     uint32_t stride;
     const uint64_t* sample_off;  // per pair
     float* sample_dist;
@@ -157,16 +160,54 @@ struct ScanArgs {
 };
 void launch_ivf_scan(const ScanArgs& a, cudaStream_t s);
 
+// K4f: the main scan as a conservative 4-bit filter over 64-query items
+// (k_filter.cu).  Candidates are emitted as (position, probe rank); K4r
+// recomputes their exact distances.
+static const int kFQ = 64;  // queries per filter item (4 LUT-pass items)
+struct FilterArgs {
+    const uint8_t* codes;
+    const uint64_t* list_off;
+    const uint32_t* item_list;   // 64-query items
+    const uint32_t* item_start;
+    const uint32_t* item_nq;
+    const uint32_t* item_order;
+    const uint32_t* num_items;
+    uint32_t* item_counter;
+    const uint32_t* list_len;
+    const uint32_t* list_first;  // first pair of each list in pair_sorted
+    const uint32_t* sub_item_off;  // first 16-query item of each list
+    const uint32_t* pair_sorted;
+    uint32_t w;
+    const float* tau;
+    const uint8_t* q8_cache;
+    const float* q8_param;
+    uint32_t* cand_aux;  // probe rank of each candidate
+    uint32_t* cand_pos;
+    uint32_t* cand_cnt;
+    uint32_t cap;
+    int pass_all;  // debug: every probed entry is a candidate
+};
+void launch_ivf_filter(const FilterArgs& a, cudaStream_t s);
+// K4r: exact ADC distance of every filter candidate (reference order), and
+// the per-query count of candidates at or below tau.
+bool recheck_supported(uint32_t d, uint32_t m, uint32_t w);
+void launch_recheck(const float* xq, uint32_t d, uint32_t m, const float* coarse,
+                    const float* books, const uint32_t* probes, uint32_t w, const uint8_t* codes,
+                    const uint32_t* cand_cnt, uint32_t cap, const uint32_t* cand_pos,
+                    float* cand_dist, const float* tau, size_t nq, uint32_t* cand_le,
+                    cudaStream_t s);
+
 // Build the scan work items from the probes.
 void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,
                         const uint32_t* list_len, uint32_t nlists, const uint32_t* item_off,
                         uint32_t* item_list, uint32_t* item_start, uint32_t* item_nq,
-                        uint32_t* item_e0, uint32_t* item_e1, uint32_t* sort_key, cudaStream_t s);
+                        uint32_t* item_e0, uint32_t* item_e1, uint32_t* sort_key, uint32_t qt,
+                        cudaStream_t s);
 void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, uint32_t nlists,
-                           uint32_t* items, cudaStream_t s);
+                           uint32_t* items, uint32_t qt, cudaStream_t s);
 // Per query: N_q = sum of probed list lengths; per pair sample counts.
 void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
-                        uint32_t stride, uint32_t strat, uint32_t cap, uint64_t* nq_entries,
+                        uint32_t stride, uint32_t cap, uint64_t* nq_entries,
                         uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
                         cudaStream_t s);
 // tau_q = rank-th smallest sample of query q (sampled queries), +inf otherwise.

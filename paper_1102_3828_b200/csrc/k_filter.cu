@@ -1,0 +1,543 @@
+// k_filter.cu — K4f + K4r: the main IVFADC scan (ivf_search's hot loop,
+// ivf_index.hpp:58-61) as a conservative 4-bit filter followed by an exact
+// recheck of the survivors.
+//
+// The exact scan (k_scan.cu, pass 0) is bound by shared-memory LUT gathers:
+// 8 x 4 bytes per (entry, query).  Here a work item is one list and up to 64
+// probing queries (four LUT-pass items), and the item's LUT holds 5-bit
+// values in bytes, laid out [j][code][64 queries]: a lane's LDS.128 returns 16
+// queries' values (8 bytes of gathers per entry-query instead of 32), and a
+// 64-byte row keeps the parity-paired list order conflict-free exactly like
+// the fp32 [j][code][16] layout.
+//
+// Conservativeness.  For query q and list l with exact LUT L_j[c] (the same
+// values the exact scan sums), m_j = min_c L_j[c] and scale s (k_scan.cu
+// quantize_item): v8_j[c] * s <= L_j[c] - m_j.  With Delta = 256 s / mult,
+// v5 = min(31, (v8 * mult) >> 8) gives v5 * Delta <= L_j - m_j, so
+//     sum_j L_j[c_j] >= sum_j m_j + Delta * sum_j v5_j[c_j].
+// The fp32 ADC d = fl(...fl(fl(0 + L_0) + L_1)...) of non-negative terms is
+// >= (1 - 8u) sum_j L_j, so d <= tau implies
+//     sum_j v5_j <= T = floor((tau (1+e) - sum_m (1-e)) / Delta (1+e)),
+// e = 2^-18 covering every rounding.  The filter keeps sum_j v5_j <= T, a
+// superset of {d <= tau}; K4r recomputes d exactly for the survivors, so the
+// exact shortlist is unchanged.  Delta targets (tau - sum_m) / 80: T ~ 80, an
+// average of ~10 per subspace at the threshold, well below the clamp at 31.
+// Byte sums stay <= 8 * 31 = 248 (no carries); the per-byte unsigned test
+// x <= T is SWAR: r = (T | 0x80) - (x & 0x7f) never borrows, and bit 7 of
+// (x ^ T) ? T : r is set exactly when x <= T.  Dead slots (no entry of the
+// list can reach tau) get an all-31 column and T = 0.
+#include <float.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace pqrr_b200 {
+namespace {
+
+constexpr int M = 8;
+constexpr int KS = 256;
+constexpr int FQ = kFQ;      // queries per filter item
+constexpr int SUBQ = kQT;    // queries per LUT-pass item
+constexpr int NSUB = FQ / SUBQ;
+constexpr int FT = 512;
+constexpr int FW = FT / 32;
+constexpr int LUT8_BYTES = M * KS * FQ;      // 128 KiB
+constexpr int Q8_BLOCK = M * KS * SUBQ;      // 32 KiB per LUT-pass item
+constexpr float kBandDiv = 80.f;              // Delta ~ (tau - sum_m) / 80
+
+// Per query slot: multiplier / additive term of the v8 -> v5 conversion and
+// the threshold byte T (255 = everything passes).
+struct SlotParam {
+    uint32_t mult, add, t;
+};
+__device__ __forceinline__ SlotParam slot_params(float tau, float sc, float summ) {
+    const float e_up = 1.000003814697265625f, e_dn = 0.999996185302734375f;  // 1 +- 2^-18
+    if (!(tau < __int_as_float(0x7f800000))) return {0u, 0u, 255u};  // unsampled: all pass
+    const float num = __fsub_rn(__fmul_rn(tau, e_up), __fmul_rn(summ, e_dn));
+    if (!(num >= 0.f)) return {0u, 31u, 0u};  // even the closest reconstruction is beyond tau
+    if (!(sc > 0.f)) return {0u, 0u, 255u};   // v8 == 0 everywhere and sum_m <= tau
+    // mult = floor(256 sc / Delta_target) in [1, 256]
+    const float mf = floorf(__fdiv_rn(__fmul_rn(256.f, sc), __fdiv_rn(num, kBandDiv)));
+    const uint32_t mult = mf >= 256.f ? 256u : (mf < 1.f ? 1u : (uint32_t)mf);
+    // T = floor(num / Delta), Delta = 256 sc / mult
+    const float tf = __fmul_rn(__fdiv_rn(__fmul_rn(num, (float)mult), __fmul_rn(256.f, sc)), e_up);
+    const float t = floorf(tf);
+    return {mult, 0u, t >= 255.f ? 255u : (uint32_t)t};
+}
+
+// Four v8 bytes -> v5 bytes: min(31, (b * mult_b >> 8) + add_b).
+__device__ __forceinline__ uint32_t v5_of(uint32_t word, const uint32_t* mult, const uint32_t* add) {
+    uint32_t out = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const uint32_t v = ((((word >> (8 * b)) & 0xffu) * mult[b]) >> 8) + add[b];
+        out |= min(v, 31u) << (8 * b);
+    }
+    return out;
+}
+
+// Bit 7 of each byte set where x <= t (unsigned bytes, see the header).
+__device__ __forceinline__ uint32_t le_bytes(uint32_t x, uint32_t t, uint32_t t_hi) {
+    const uint32_t r = t_hi - (x & 0x7f7f7f7fu);
+    const uint32_t d = x ^ t;
+    return ((d & t) | (~d & r)) & 0x80808080u;
+}
+
+// Candidates are staged per item in shared memory as (entry << 6 | slot) and
+// written out grouped by query slot at the end of the item, so each (query,
+// list) run is contiguous in the query's buffer (K4r keeps the run's residual
+// in registers).  A full stage falls back to a direct append.
+constexpr int STAGE = 16384;  // staged candidates per item (64 KiB)
+
+__device__ __forceinline__ void append_direct(int slot, uint32_t pos, const int* s_q,
+                                              const uint32_t* s_r, const FilterArgs& a) {
+    const int q = s_q[slot];
+    const unsigned o = atomicAdd(a.cand_cnt + q, 1u);
+    if (o < a.cap) {
+        a.cand_pos[(size_t)q * a.cap + o] = pos;
+        a.cand_aux[(size_t)q * a.cap + o] = s_r[slot];
+    }
+}
+
+__device__ __forceinline__ void emit_bits(uint32_t bits, int base, uint32_t e, uint32_t off32,
+                                          bool stage_ok, uint32_t* stage, uint32_t* s_nst,
+                                          const int* s_q, const uint32_t* s_r, const FilterArgs& a) {
+    while (bits) {
+        const int b = __ffs(bits) - 1;  // bit 7 of byte b / 8
+        bits &= bits - 1;
+        const int slot = base + (b >> 3);
+        const uint32_t k = stage_ok ? atomicAdd(s_nst, 1u) : (uint32_t)STAGE;
+        if (k < (uint32_t)STAGE)
+            stage[k] = (e << 6) | (uint32_t)slot;
+        else
+            append_direct(slot, off32 + e, s_q, s_r, a);
+    }
+}
+
+__global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
+    extern __shared__ uint4 smem_f[];
+    uint8_t* lut8 = reinterpret_cast<uint8_t*>(smem_f);  // [M][KS][FQ]
+    const uint4* lut8v = smem_f;
+    __shared__ uint32_t s_item, s_any;
+    __shared__ int s_q[FQ];
+    __shared__ uint32_t s_r[FQ];
+    __shared__ __align__(16) uint8_t s_t[FQ];
+    __shared__ uint32_t s_mult[FQ], s_add[FQ];
+    __shared__ uint32_t s_nst, s_scnt[FQ], s_sbase[FQ];
+    uint32_t* stage = reinterpret_cast<uint32_t*>(lut8 + LUT8_BYTES);
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int slot = lane >> 2, qd = lane & 3;
+    const uint32_t n_items = *a.num_items;
+
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const uint32_t c = atomicAdd(a.item_counter, 1u);
+            s_item = c < n_items ? a.item_order[c] : 0xffffffffu;
+            s_any = 0;
+            s_nst = 0;
+        }
+        __syncthreads();
+        const uint32_t it = s_item;
+        if (it == 0xffffffffu) break;
+        const uint32_t l = a.item_list[it];
+        const uint32_t start = a.item_start[it];
+        const uint32_t nqi = a.item_nq[it];
+        const uint32_t sub0 = a.sub_item_off[l] + (start - a.list_first[l]) / SUBQ;
+        if (threadIdx.x < FQ) {
+            const uint32_t t = threadIdx.x;
+            int q = -1;
+            uint32_t r = 0;
+            SlotParam sp{0u, 31u, 0u};  // empty slot: dead
+            if (t < nqi) {
+                const uint32_t p = a.pair_sorted[start + t];
+                q = (int)(p / a.w);
+                r = p % a.w;
+                const float* prm = a.q8_param + ((size_t)(sub0 + t / SUBQ) * SUBQ + t % SUBQ) * 2;
+                sp = slot_params(a.tau[q], prm[0], prm[1]);
+                if (a.pass_all) sp = {0u, 0u, 255u};
+            }
+            s_q[t] = q;
+            s_r[t] = r;
+            s_mult[t] = sp.mult;
+            s_add[t] = sp.add;
+            s_t[t] = (uint8_t)sp.t;
+            if (sp.add == 0u) s_any = 1;
+        }
+        __syncthreads();
+        if (!s_any) continue;  // no query of the item can have a candidate in this list
+
+        // ---- 5-bit LUT of the item from the LUT pass's 8-bit blocks
+        {
+            const uint32_t nsub = (nqi + SUBQ - 1) / SUBQ;
+            const int sub = threadIdx.x & 3;  // fixed per thread (FT % 4 == 0)
+            uint32_t mu[SUBQ], ad[SUBQ];
+#pragma unroll
+            for (int i = 0; i < SUBQ; ++i) {
+                mu[i] = s_mult[sub * SUBQ + i];
+                ad[i] = s_add[sub * SUBQ + i];
+            }
+            const uint4* src = reinterpret_cast<const uint4*>(a.q8_cache + (size_t)(sub0 + sub) * Q8_BLOCK);
+            const bool live = (uint32_t)sub < nsub;
+            constexpr int ROWS = M * KS;
+            constexpr int PER = ROWS / (FT / 4);  // rows per thread
+#pragma unroll 4
+            for (int i = 0; i < PER; ++i) {
+                const int row = (threadIdx.x >> 2) + i * (FT / 4);
+                uint4 v = live ? __ldg(src + row) : make_uint4(0, 0, 0, 0);
+                v.x = v5_of(v.x, mu + 0, ad + 0);
+                v.y = v5_of(v.y, mu + 4, ad + 4);
+                v.z = v5_of(v.z, mu + 8, ad + 8);
+                v.w = v5_of(v.w, mu + 12, ad + 12);
+                reinterpret_cast<uint4*>(lut8)[row * NSUB + sub] = v;
+            }
+        }
+        __syncthreads();
+
+        const uint64_t off = a.list_off[l];
+        const uint32_t len = a.list_len[l];
+        const uint32_t off32 = (uint32_t)off;
+        const bool stage_ok = len < (1u << 26);
+        const u64* codes = reinterpret_cast<const u64*>(a.codes) + off;
+        const uint4 tb = reinterpret_cast<const uint4*>(s_t)[qd];
+        const uint4 th = make_uint4(tb.x | 0x80808080u, tb.y | 0x80808080u, tb.z | 0x80808080u,
+                                    tb.w | 0x80808080u);
+        constexpr uint32_t S = FW * 8;
+        const uint32_t wbase = warp * 8;
+        u64 nA, nB, fA, fB;
+        {
+            const uint32_t e = wbase + slot;
+            nA = e < len ? __ldg(codes + e) : 0ull;
+            nB = e + S < len ? __ldg(codes + e + S) : 0ull;
+            fA = e + 2 * S < len ? __ldg(codes + e + 2 * S) : 0ull;
+            fB = e + 3 * S < len ? __ldg(codes + e + 3 * S) : 0ull;
+        }
+        for (uint32_t wb = wbase; wb < len; wb += 2 * S) {
+            const uint32_t eA = wb + slot, eB = eA + S;
+            const bool vA = eA < len, vB = eB < len;
+            const u64 cA = nA, cB = nB;
+            nA = fA;
+            nB = fB;
+            fA = eA + 4 * S < len ? __ldg(codes + eA + 4 * S) : 0ull;
+            fB = eB + 4 * S < len ? __ldg(codes + eB + 4 * S) : 0ull;
+            uint32_t a0 = 0u, a1 = 0u, a2 = 0u, a3 = 0u;
+            uint32_t b0 = 0u, b1 = 0u, b2 = 0u, b3 = 0u;
+            const uint32_t cAl = (uint32_t)cA, cAh = (uint32_t)(cA >> 32);
+            const uint32_t cBl = (uint32_t)cB, cBh = (uint32_t)(cB >> 32);
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+                const uint32_t ca = ((j < 4 ? cAl : cAh) >> (8 * (j & 3))) & 0xffu;
+                const uint32_t cb = ((j < 4 ? cBl : cBh) >> (8 * (j & 3))) & 0xffu;
+                const uint4 va = lut8v[(j * KS + ca) * NSUB + qd];
+                const uint4 vb = lut8v[(j * KS + cb) * NSUB + qd];
+                a0 += va.x; a1 += va.y; a2 += va.z; a3 += va.w;
+                b0 += vb.x; b1 += vb.y; b2 += vb.z; b3 += vb.w;
+            }
+            const uint32_t pa0 = vA ? le_bytes(a0, tb.x, th.x) : 0u, pa1 = vA ? le_bytes(a1, tb.y, th.y) : 0u;
+            const uint32_t pa2 = vA ? le_bytes(a2, tb.z, th.z) : 0u, pa3 = vA ? le_bytes(a3, tb.w, th.w) : 0u;
+            const uint32_t pb0 = vB ? le_bytes(b0, tb.x, th.x) : 0u, pb1 = vB ? le_bytes(b1, tb.y, th.y) : 0u;
+            const uint32_t pb2 = vB ? le_bytes(b2, tb.z, th.z) : 0u, pb3 = vB ? le_bytes(b3, tb.w, th.w) : 0u;
+            if (__any_sync(0xffffffffu, (pa0 | pa1 | pa2 | pa3 | pb0 | pb1 | pb2 | pb3) != 0u)) {
+                const int base = qd * 16;
+                emit_bits(pa0, base + 0, eA, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
+                emit_bits(pa1, base + 4, eA, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
+                emit_bits(pa2, base + 8, eA, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
+                emit_bits(pa3, base + 12, eA, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
+                emit_bits(pb0, base + 0, eB, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
+                emit_bits(pb1, base + 4, eB, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
+                emit_bits(pb2, base + 8, eB, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
+                emit_bits(pb3, base + 12, eB, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
+            }
+        }
+        // ---- flush the staged candidates grouped by slot
+        if (threadIdx.x < FQ) s_scnt[threadIdx.x] = 0;
+        __syncthreads();
+        const uint32_t nst = min(s_nst, (uint32_t)STAGE);
+        for (uint32_t i = threadIdx.x; i < nst; i += FT) atomicAdd(&s_scnt[stage[i] & 63u], 1u);
+        __syncthreads();
+        if (threadIdx.x < FQ) {
+            const uint32_t cnt = s_scnt[threadIdx.x];
+            s_sbase[threadIdx.x] = cnt ? atomicAdd(a.cand_cnt + s_q[threadIdx.x], cnt) : 0u;
+            s_scnt[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < nst; i += FT) {
+            const uint32_t v = stage[i];
+            const uint32_t sl = v & 63u;
+            const uint32_t o = s_sbase[sl] + atomicAdd(&s_scnt[sl], 1u);
+            if (o < a.cap) {
+                const size_t q = (size_t)s_q[sl];
+                a.cand_pos[q * a.cap + o] = off32 + (v >> 6);
+                a.cand_aux[q * a.cap + o] = s_r[sl];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// K4r: one CTA per query.  The query's residuals x - C_l for its w probes are
+// staged in shared memory; each candidate's distance is the j-ascending fp32
+// sum of l2_sq(residual_j, B_j[c_j]) in the reference order — bit-identical to
+// the LUT value the exact scan would have added (build_luts, k_scan.cu).
+template <int DSUB>
+__global__ __launch_bounds__(256) void recheck_kernel(
+    const float* __restrict__ xq, uint32_t d, const float* __restrict__ coarse,
+    const float* __restrict__ books, const uint32_t* __restrict__ probes, uint32_t w,
+    const u64* __restrict__ codes, const uint32_t* __restrict__ cand_cnt, uint32_t cap,
+    const uint32_t* __restrict__ cand_pos, float* __restrict__ cand_dist,
+    const float* __restrict__ tau, uint32_t* __restrict__ cand_le, const u64 nz) {
+    extern __shared__ float4 smem_r[];
+    float* res = reinterpret_cast<float*>(smem_r);  // [w][d]
+    __shared__ uint32_t s_le;
+    const size_t q = blockIdx.x;
+    const uint32_t n = min(cand_cnt[q], cap);
+    if (threadIdx.x == 0) s_le = 0;
+    if (n == 0) {
+        if (threadIdx.x == 0) cand_le[q] = 0;
+        return;
+    }
+    for (uint32_t idx = threadIdx.x; idx < w * d; idx += blockDim.x) {
+        const uint32_t r = idx / d, t = idx % d;
+        const uint32_t l = probes[q * w + r];
+        res[idx] = __fsub_rn(xq[q * d + t], coarse[(size_t)l * d + t]);
+    }
+    __syncthreads();
+    const float tq = tau[q];
+    uint32_t le = 0;
+    const uint32_t* aux = reinterpret_cast<const uint32_t*>(cand_dist) + q * cap;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t pos = cand_pos[q * cap + i];
+        const uint32_t r = aux[i];
+        const u64 code = __ldg(codes + pos);
+        const float* rr = res + (size_t)r * d;
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            const uint32_t c = (uint32_t)(code >> (8 * j)) & 0xffu;
+            acc = __fadd_rn(acc, l2sq_packed<DSUB>(rr + j * DSUB, books + ((size_t)j * KS + c) * DSUB, nz));
+        }
+        cand_dist[q * cap + i] = acc;
+        le += acc <= tq ? 1u : 0u;
+    }
+    atomicAdd(&s_le, le);
+    __syncthreads();
+    if (threadIdx.x == 0) cand_le[q] = s_le;
+}
+
+// K4r, shared-memory variant (d/m <= 16): persistent CTAs hold the whole
+// codebook (8 x 256 x DSUB floats) in shared memory and walk the queries.
+// Per query the w residuals are staged with chunk swizzle
+// phys = c ^ ((c >> 3) & 3) (16-byte chunks), and a warp rechecks 4
+// candidates per step with 8 lanes each (lane = subspace j): the 8 lanes of a
+// quarter-warp read residual chunk p of 8 different subspaces at 8 distinct
+// bank groups, and codebook rows (stored with the same per-subspace swizzle)
+// at ~2 wavefronts.  Each lane computes l2_sq(residual_j, B_j[c_j]) in the
+// reference order; the 8 values are gathered by shuffles and summed
+// j-ascending — the same fp32 operations as the exact scan's LUT + ADC.
+template <int DSUB>
+__global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
+    const float* __restrict__ xq, uint32_t d, const float* __restrict__ coarse,
+    const float* __restrict__ books, const uint32_t* __restrict__ probes, uint32_t w,
+    const u64* __restrict__ codes, const uint32_t* __restrict__ cand_cnt, uint32_t cap,
+    const uint32_t* __restrict__ cand_pos, float* __restrict__ cand_dist,
+    const float* __restrict__ tau, size_t nq, uint32_t* __restrict__ cand_le,
+    uint32_t* __restrict__ counter, const u64 nz) {
+    constexpr int CH = DSUB / 4;  // 16-byte chunks per subspace row
+    extern __shared__ float4 smem_k[];
+    float4* bk = smem_k;                      // [M][KS][CH], swizzled
+    float4* res = smem_k + M * KS * CH;       // [w][d / 4], swizzled
+    __shared__ uint32_t s_q, s_le;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = lane & 7, slot = lane >> 3;
+    const uint32_t dch = d / 4;
+    // swizzled chunk index within a row of subspace j (CH chunks per subspace)
+    auto sw = [](uint32_t c) { return CH >= 4 ? (c ^ ((c >> 3) & 3)) : c; };
+    for (uint32_t i = threadIdx.x; i < (uint32_t)(M * KS * CH); i += blockDim.x) {
+        const uint32_t row = i / CH, c = i % CH;  // row = j * KS + code
+        const uint32_t jj = row / KS;
+        const uint32_t lc = jj * CH + c;  // logical chunk within a d-row
+        bk[row * CH + (sw(lc) - jj * CH)] = reinterpret_cast<const float4*>(books)[i];
+    }
+    for (;;) {
+        __syncthreads();  // previous query done (and books staged)
+        if (threadIdx.x == 0) {
+            s_q = atomicAdd(counter, 1u);
+            s_le = 0;
+        }
+        __syncthreads();
+        const size_t q = s_q;
+        if (q >= nq) break;
+        const uint32_t n = min(cand_cnt[q], cap);
+        if (n == 0) {
+            if (threadIdx.x == 0) cand_le[q] = 0;
+            continue;
+        }
+        for (uint32_t i = threadIdx.x; i < w * dch; i += blockDim.x) {
+            const uint32_t r = i / dch, c = i % dch;
+            const uint32_t l = probes[q * w + r];
+            const float4 x = reinterpret_cast<const float4*>(xq + q * d)[c];
+            const float4 y = reinterpret_cast<const float4*>(coarse + (size_t)l * d)[c];
+            res[r * dch + sw(c)] = make_float4(__fsub_rn(x.x, y.x), __fsub_rn(x.y, y.y),
+                                               __fsub_rn(x.z, y.z), __fsub_rn(x.w, y.w));
+        }
+        __syncthreads();
+        const float tq = tau[q];
+        const uint32_t* aux = reinterpret_cast<const uint32_t*>(cand_dist) + q * cap;
+        uint32_t le = 0;
+        // each warp takes 16 candidates per iteration (4 rounds of 4); the
+        // position / probe-rank loads of the next iteration are issued before
+        // this one's arithmetic, the codes of all 4 rounds together.  Slots of
+        // odd parity read the second 8-byte half of every chunk first, so the
+        // two candidates of a half-warp never share a bank; the halves feed the
+        // separate (s0,s1) / (s2,s3) accumulators, so the order is unchanged.
+        // The residual chunk stays in registers while the probe rank repeats
+        // (K4f writes each (query, list) run contiguously).
+        constexpr int U = 4;
+        constexpr uint32_t STEP = 16 * 4 * U;
+        const uint32_t hA = (uint32_t)slot & 1u;
+        uint32_t npos[U], nr[U];
+        auto fetch = [&](uint32_t b) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = min(b + u * 4 + slot, n - 1);
+                npos[u] = cand_pos[q * cap + i];
+                nr[u] = aux[i];
+            }
+        };
+        const u64* res64 = reinterpret_cast<const u64*>(res);
+        const u64* bk64 = reinterpret_cast<const u64*>(bk);
+        u64 xa[CH], xb[CH];  // residual chunk halves (hA first)
+        uint32_t cur_r = 0xffffffffu;
+        fetch(warp * 4 * U);
+        for (uint32_t base = warp * 4 * U; base < n; base += STEP) {
+            uint32_t pos[U], rr[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                pos[u] = npos[u];
+                rr[u] = nr[u];
+            }
+            if (base + STEP < n) fetch(base + STEP);
+            u64 code[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) code[u] = __ldg(codes + pos[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = base + u * 4 + slot;
+                if (rr[u] != cur_r) {
+                    cur_r = rr[u];
+#pragma unroll
+                    for (int p = 0; p < CH; ++p) {
+                        const uint32_t pc = sw(j * CH + p);
+                        xa[p] = res64[(cur_r * dch + pc) * 2 + hA];
+                        xb[p] = res64[(cur_r * dch + pc) * 2 + (hA ^ 1u)];
+                    }
+                }
+                const uint32_t c = (uint32_t)(code[u] >> (8 * j)) & 0xffu;
+                const u64* brow = bk64 + (size_t)(j * KS + c) * CH * 2;
+                u64 sa = 0, sb = 0;
+#pragma unroll
+                for (int p = 0; p < CH; ++p) {
+                    const uint32_t pc = sw(j * CH + p) - j * CH;
+                    sa = acc_sq2(sa, xa[p], brow[pc * 2 + hA], nz);
+                    sb = acc_sq2(sb, xb[p], brow[pc * 2 + (hA ^ 1u)], nz);
+                }
+                const u64 s01 = hA ? sb : sa, s23 = hA ? sa : sb;
+                const float Lj = __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
+                float acc = 0.f;
+#pragma unroll
+                for (int jj = 0; jj < M; ++jj)
+                    acc = __fadd_rn(acc, __shfl_sync(0xffffffffu, Lj, (lane & ~7) | jj));
+                if (i < n && j == 0) {
+                    cand_dist[q * cap + i] = acc;
+                    le += acc <= tq ? 1u : 0u;
+                }
+            }
+        }
+        if (le) atomicAdd(&s_le, le);
+        __syncthreads();
+        if (threadIdx.x == 0) cand_le[q] = s_le;
+    }
+}
+
+template <int DSUB>
+void recheck_t(const float* xq, uint32_t d, const float* coarse, const float* books,
+               const uint32_t* probes, uint32_t w, const uint8_t* codes, const uint32_t* cand_cnt,
+               uint32_t cap, const uint32_t* cand_pos, float* cand_dist, const float* tau, size_t nq,
+               uint32_t* cand_le, cudaStream_t s) {
+    const size_t smem = (size_t)w * d * sizeof(float);
+    PQRR_CUDA(cudaFuncSetAttribute(recheck_kernel<DSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<size_t>(smem, 1)));
+    recheck_kernel<DSUB><<<(unsigned)nq, 256, smem, s>>>(
+        xq, d, coarse, books, probes, w, reinterpret_cast<const u64*>(codes), cand_cnt, cap, cand_pos,
+        cand_dist, tau, cand_le, kNegZero2);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+}  // namespace
+
+void launch_ivf_filter(const FilterArgs& a, cudaStream_t s) {
+    const int smem = LUT8_BYTES + STAGE * (int)sizeof(uint32_t);
+    PQRR_CUDA(cudaFuncSetAttribute(ivf_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ivf_filter_kernel<<<sm_count(), FT, smem, s>>>(a);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+bool recheck_supported(uint32_t d, uint32_t m, uint32_t w) {
+    if (m != M) return false;
+    const uint32_t ds = d / m;
+    if (ds != 4 && ds != 8 && ds != 16 && ds != 32) return false;
+    return (size_t)w * d * sizeof(float) <= 200 * 1024;
+}
+
+template <int DSUB>
+bool recheck_smem_t(const float* xq, uint32_t d, const float* coarse, const float* books,
+                    const uint32_t* probes, uint32_t w, const uint8_t* codes, const uint32_t* cand_cnt,
+                    uint32_t cap, const uint32_t* cand_pos, float* cand_dist, const float* tau,
+                    size_t nq, uint32_t* cand_le, cudaStream_t s) {
+    const size_t smem = (size_t)M * KS * DSUB * sizeof(float) + (size_t)w * d * sizeof(float);
+    if (smem > 220 * 1024) return false;
+    PQRR_CUDA(cudaFuncSetAttribute(recheck_smem_kernel<DSUB>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    uint32_t* counter = nullptr;
+    PQRR_CUDA(cudaMallocAsync(&counter, sizeof(uint32_t), s));
+    PQRR_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), s));
+    recheck_smem_kernel<DSUB><<<sm_count(), 512, smem, s>>>(
+        xq, d, coarse, books, probes, w, reinterpret_cast<const u64*>(codes), cand_cnt, cap, cand_pos,
+        cand_dist, tau, nq, cand_le, counter, kNegZero2);
+    PQRR_LAUNCH_CHECK();
+    PQRR_CUDA(cudaFreeAsync(counter, s));
+    count_launch();
+    return true;
+}
+
+void launch_recheck(const float* xq, uint32_t d, uint32_t m, const float* coarse,
+                    const float* books, const uint32_t* probes, uint32_t w, const uint8_t* codes,
+                    const uint32_t* cand_cnt, uint32_t cap, const uint32_t* cand_pos,
+                    float* cand_dist, const float* tau, size_t nq, uint32_t* cand_le,
+                    cudaStream_t s) {
+    if (!nq) return;
+    static const bool plain = getenv("PQRR_RECHECK") && std::string(getenv("PQRR_RECHECK")) == "global";
+    if (!plain && d / m == 16 &&
+        recheck_smem_t<16>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist,
+                           tau, nq, cand_le, s))
+        return;
+    if (!plain && d / m == 8 &&
+        recheck_smem_t<8>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist,
+                          tau, nq, cand_le, s))
+        return;
+    switch (d / m) {
+        case 16: return recheck_t<16>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s);
+        case 8: return recheck_t<8>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s);
+        case 4: return recheck_t<4>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s);
+        case 32: return recheck_t<32>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s);
+        default: throw ArgError("recheck supports d/m in {4, 8, 16, 32}");
+    }
+}
+
+}  // namespace pqrr_b200

@@ -16,6 +16,8 @@
 // appended (dist, position) to the query's buffer with warp-aggregated
 // atomics.  Sample mode (stride > 1) writes every stride-th entry's distance
 // to a per-(query, probe) slot instead; it feeds the threshold estimate.
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -105,39 +107,103 @@ __device__ __forceinline__ void emit1(bool hit, int q, float dist, uint32_t pos,
     }
 }
 
+// Per (query lane, subspace) minimum and range of the item's exact LUT, then
+// the 8-bit LUT the K4f filter derives its 4-bit tables from:
+//   v8 = min(255, floor((L - min_j) / s)),  s = max_j range_j / 255
+// computed so that v8 * s <= L - min_j holds in exact arithmetic (the
+// (1 - 2^-20) factor covers the three roundings), which keeps the filter's
+// lower bound conservative.  The block goes to q8 (32 KiB) through `stage`;
+// per query lane (s, sum_j min_j) goes to param.
+__device__ __forceinline__ void quantize_item(const float* __restrict__ lut, uint32_t* __restrict__ stage,
+                                              float* __restrict__ s_mn, float* __restrict__ s_mx,
+                                              float* __restrict__ s_min, float* __restrict__ s_rng,
+                                              float* __restrict__ s_inv,
+                                              float* __restrict__ param) {
+    const int t = threadIdx.x;
+    {
+        const int qq = t & 15, part = (t >> 4) & 3, jj = t >> 6;
+        const int rot = part & 1;  // the two half-warps read rows of opposite parity: no conflicts
+        float mn = __int_as_float(0x7f800000), mx = 0.f;
+#pragma unroll 8
+        for (int ii = 0; ii < 64; ++ii) {
+            const int i = part * 64 + ((ii + rot) & 63);
+            const float v = lut[(jj * KS + i) * QT + qq];
+            mn = fminf(mn, v);
+            mx = fmaxf(mx, v);
+        }
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 16));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        if ((t & 31) < 16) {
+            s_mn[(t >> 5) * 16 + qq] = mn;
+            s_mx[(t >> 5) * 16 + qq] = mx;
+        }
+    }
+    __syncthreads();
+    if (t < M * QT) {
+        const int jj = t >> 4, qq = t & 15;
+        const float mn = fminf(s_mn[(2 * jj) * 16 + qq], s_mn[(2 * jj + 1) * 16 + qq]);
+        const float mx = fmaxf(s_mx[(2 * jj) * 16 + qq], s_mx[(2 * jj + 1) * 16 + qq]);
+        s_min[jj * 16 + qq] = mn;
+        s_rng[jj * 16 + qq] = __fsub_rn(mx, mn);
+    }
+    __syncthreads();
+    if (t < QT) {
+        float rng = 0.f, sm = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+            rng = fmaxf(rng, s_rng[jj * 16 + t]);
+            sm = __fadd_rn(sm, s_min[jj * 16 + t]);
+        }
+        const float sc = __fdiv_rn(rng, 255.f);
+        s_inv[t] = sc > 0.f ? __frcp_rn(sc) : 0.f;
+        param[2 * t] = sc;
+        param[2 * t + 1] = sm;
+    }
+    __syncthreads();
+    const float4* lut4 = reinterpret_cast<const float4*>(lut);
+    const int g = t & 3;
+    const float4 inv = *reinterpret_cast<const float4*>(s_inv + 4 * g);
+    const float shrink = 0.99999904632568359375f;  // 1 - 2^-20
+#pragma unroll 4
+    for (int row = t >> 2; row < M * KS; row += NT / 4) {
+        const float4 v = lut4[row * 4 + g];
+        const float4 mn = *reinterpret_cast<const float4*>(s_min + (row >> 8) * 16 + 4 * g);
+        auto q8 = [&](float L, float m, float iv) -> uint32_t {
+            const float x = fminf(__fmul_rn(__fmul_rn(__fsub_rn(L, m), iv), shrink), 255.f);
+            return __float2uint_rz(x);
+        };
+        stage[row * 4 + g] = q8(v.x, mn.x, inv.x) | (q8(v.y, mn.y, inv.y) << 8) |
+                             (q8(v.z, mn.z, inv.z) << 16) | (q8(v.w, mn.w, inv.w) << 24);
+    }
+}
+
 template <int DSUB>
 __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const u64 nz) {
     extern __shared__ float4 smem4[];
     float* lut = reinterpret_cast<float*>(smem4);
     const int xld = (int)a.d + 4;
     float* xr = lut + LUT_FLOATS;         // [QT][d + 4]
-    float* bbuf = xr + QT * xld;          // [2][KS][DSUB] sub-codebook ring
+    float* bbuf = xr + QT * xld;          // [2][KS][DSUB] sub-codebook ring; q8 staging after the build
     __shared__ uint32_t s_item;
     __shared__ int s_q[QT];
     __shared__ uint32_t s_pair[QT];
     __shared__ float s_tau[QT];
     __shared__ uint8_t s_samp[QT];
-
-    __shared__ __align__(8) unsigned long long s_bar;  // TMA completion barrier (lut_mode 2)
-    unsigned bar_phase = 0;
+    __shared__ __align__(16) float s_mn[NW * 16], s_mx[NW * 16], s_min[M * QT], s_rng[M * QT],
+        s_inv[QT];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int slot = lane >> 2, qd = lane & 3;
     const uint32_t n_items = *a.num_items;
     const float4* lut4 = reinterpret_cast<const float4*>(lut);
-    if (threadIdx.x == 0) {
-        const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
+    const bool store_q8 = a.pass == 1 && a.q8_cache != nullptr;
 
     for (;;) {
         if (threadIdx.x == 0) {
             const uint32_t c = atomicAdd(a.item_counter, 1u);
             s_item = c < n_items ? a.item_order[c] : 0xffffffffu;  // longest items first
-            // the previous item's bulk LUT store must have read smem before reuse
-            if (a.lut_mode == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            // the previous item's bulk q8 store must have read smem before reuse
+            if (store_q8) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
         __syncthreads();
         const uint32_t it = s_item;
@@ -155,34 +221,11 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
             }
             s_q[threadIdx.x] = q;
             s_pair[threadIdx.x] = p;
-            s_tau[threadIdx.x] = q >= 0 ? a.tau[q] : -1.0f;
+            s_tau[threadIdx.x] = (q >= 0 && a.pass == 0) ? a.tau[q] : -1.0f;
             s_samp[threadIdx.x] = (q >= 0 && a.query_sampled) ? a.query_sampled[q] : 0;
         }
         __syncthreads();
-        if (a.lut_mode == 2) {
-            // main pass after a sample pass: the item's LUT was cached in HBM
-            // by the sample pass; one TMA bulk copy brings it back (128 KiB)
-            if (threadIdx.x == 0) {
-                const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
-                const unsigned dst = (unsigned)__cvta_generic_to_shared(lut);
-                const float* src = a.lut_cache + (size_t)it * LUT_FLOATS;
-                // order the previous item's generic smem reads before async-proxy writes
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                             ::"r"(bar), "r"((unsigned)(LUT_FLOATS * 4)) : "memory");
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                    ::"r"(dst), "l"(src), "r"((unsigned)(LUT_FLOATS * 4)), "r"(bar) : "memory");
-            }
-            const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
-            unsigned done = 0;
-            while (!done) {
-                asm volatile(
-                    "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                    : "=r"(done) : "r"(bar), "r"(bar_phase) : "memory");
-            }
-            bar_phase ^= 1u;
-        } else {
+        {
             // residual queries x - C_l (ivf_index.hpp:58-59)
             const float* crow = a.coarse + (size_t)l * a.d;
             for (uint32_t idx = threadIdx.x; idx < QT * a.d; idx += NT) {
@@ -192,17 +235,19 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
             }
             __syncthreads();
             build_luts<DSUB>(lut, xr, xld, a.books, bbuf, nz);
-            if (a.lut_mode == 1) {
-                // sample pass: keep the LUT for the main pass with an async TMA
-                // bulk store that overlaps this item's sampled scan; it is
-                // waited for (read side) before the LUT smem is rewritten
+            if (store_q8) {
+                uint32_t* stage = reinterpret_cast<uint32_t*>(bbuf);
+                quantize_item(lut, stage, s_mn, s_mx, s_min, s_rng, s_inv, a.q8_param + (size_t)it * 2 * QT);
+                // async TMA bulk store of the 32 KiB block; it overlaps this
+                // item's sampled scan and is waited for (read side) before the
+                // staging buffer is rewritten
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncthreads();
                 if (threadIdx.x == 0) {
-                    const unsigned src = (unsigned)__cvta_generic_to_shared(lut);
-                    float* dst = a.lut_cache + (size_t)it * LUT_FLOATS;
+                    const unsigned src = (unsigned)__cvta_generic_to_shared(stage);
+                    uint8_t* dst = a.q8_cache + (size_t)it * (M * KS * QT);
                     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                                 ::"l"(dst), "r"(src), "r"((unsigned)(LUT_FLOATS * 4)) : "memory");
+                                 ::"l"(dst), "r"(src), "r"((unsigned)(M * KS * QT)) : "memory");
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
             }
@@ -219,7 +264,7 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
             qk[k] = s_q[qd * 4 + k];
             tk[k] = s_tau[qd * 4 + k];
         }
-        if (a.stride <= 1) {
+        if (a.pass == 0) {
             // ---------------- main mode: threshold filter + append.  Codes are
             // prefetched PF steps ahead in registers so the L2/HBM latency of
             // the stream hides behind the LUT gathers of earlier steps.
@@ -276,7 +321,7 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
                     emit1(hB3, qk[3], b3, pB, a.cand_cnt, a.cand_dist, a.cand_pos, a.cap);
                 }
             }
-        } else {
+        } else if (a.sample_dist) {
             // ---------------- sample mode: every stride-th entry, fixed slots
             const uint32_t ns = (e1 + a.stride - 1) / a.stride - (e0 + a.stride - 1) / a.stride;
             uint64_t sbase[4];
@@ -327,8 +372,8 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
         }
         __syncthreads();
     }
-    // drain outstanding bulk LUT stores before the CTA retires
-    if (threadIdx.x == 0 && a.lut_mode == 1) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // drain outstanding bulk q8 stores before the CTA retires
+    if (threadIdx.x == 0 && store_q8) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Kernel seam helpers (kernels::scan_topk / build_lut parity).
@@ -361,11 +406,11 @@ constexpr uint32_t kChunk = 1u << 30;  // chunking measured slower on C2 (extra 
 
 __global__ void items_per_list_kernel(const uint32_t* __restrict__ cnt,
                                       const uint32_t* __restrict__ len, uint32_t nlists,
-                                      uint32_t* __restrict__ items) {
+                                      uint32_t* __restrict__ items, uint32_t qt) {
     uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l < nlists) {
         const uint32_t chunks = max(1u, (len[l] + kChunk - 1) / kChunk);
-        items[l] = ((cnt[l] + QT - 1) / QT) * chunks;
+        items[l] = ((cnt[l] + qt - 1) / qt) * chunks;
     }
     if (l == nlists) items[l] = 0;
 }
@@ -376,18 +421,19 @@ __global__ void items_build_kernel(const uint32_t* __restrict__ cnt,
                                    const uint32_t* __restrict__ item_off,
                                    uint32_t* __restrict__ item_list, uint32_t* __restrict__ item_start,
                                    uint32_t* __restrict__ item_nq, uint32_t* __restrict__ item_e0,
-                                   uint32_t* __restrict__ item_e1, uint32_t* __restrict__ sort_key) {
+                                   uint32_t* __restrict__ item_e1, uint32_t* __restrict__ sort_key,
+                                   uint32_t qt) {
     uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= nlists) return;
     const uint32_t c = cnt[l], L = len[l];
     const uint32_t chunks = max(1u, (L + kChunk - 1) / kChunk);
     uint32_t o = item_off[l];
-    for (uint32_t s = 0; s < c; s += QT) {
+    for (uint32_t s = 0; s < c; s += qt) {
         for (uint32_t ch = 0; ch < chunks; ++ch, ++o) {
             const uint32_t e0 = ch * kChunk, e1 = min(L, e0 + kChunk);
             item_list[o] = l;
             item_start[o] = first[l] + s;
-            item_nq[o] = min((uint32_t)QT, c - s);
+            item_nq[o] = min(qt, c - s);
             item_e0[o] = e0;
             item_e1[o] = e1;
             sort_key[o] = 0xffffffffu - (e1 - e0);  // ascending sort = longest first
@@ -397,8 +443,9 @@ __global__ void items_build_kernel(const uint32_t* __restrict__ cnt,
 
 template <int DSUB>
 void scan_t(const ScanArgs& a, cudaStream_t s) {
-    const size_t smem = (size_t)LUT_FLOATS * sizeof(float) + (size_t)QT * (a.d + 4) * sizeof(float) +
-                        2 * (size_t)KS * DSUB * sizeof(float);
+    // the sub-codebook ring doubles as the 32 KiB q8 staging buffer
+    const size_t ring = std::max<size_t>(2 * (size_t)KS * DSUB * sizeof(float), (size_t)M * KS * QT);
+    const size_t smem = (size_t)LUT_FLOATS * sizeof(float) + (size_t)QT * (a.d + 4) * sizeof(float) + ring;
     PQRR_CUDA(cudaFuncSetAttribute(ivf_scan_kernel<DSUB>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ivf_scan_kernel<DSUB><<<sm_count(), NT, smem, s>>>(a, kNegZero2);
@@ -420,8 +467,9 @@ void launch_ivf_scan(const ScanArgs& a, cudaStream_t s) {
 }
 
 void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, uint32_t nlists,
-                           uint32_t* items, cudaStream_t s) {
-    items_per_list_kernel<<<(nlists + 1 + 255) / 256, 256, 0, s>>>(list_cnt, list_len, nlists, items);
+                           uint32_t* items, uint32_t qt, cudaStream_t s) {
+    items_per_list_kernel<<<(nlists + 1 + 255) / 256, 256, 0, s>>>(list_cnt, list_len, nlists, items,
+                                                                   qt);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }
@@ -429,10 +477,11 @@ void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, u
 void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,
                         const uint32_t* list_len, uint32_t nlists, const uint32_t* item_off,
                         uint32_t* item_list, uint32_t* item_start, uint32_t* item_nq,
-                        uint32_t* item_e0, uint32_t* item_e1, uint32_t* sort_key, cudaStream_t s) {
+                        uint32_t* item_e0, uint32_t* item_e1, uint32_t* sort_key, uint32_t qt,
+                        cudaStream_t s) {
     items_build_kernel<<<(nlists + 255) / 256, 256, 0, s>>>(list_cnt, list_first, list_len, nlists,
                                                             item_off, item_list, item_start, item_nq,
-                                                            item_e0, item_e1, sort_key);
+                                                            item_e0, item_e1, sort_key, qt);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

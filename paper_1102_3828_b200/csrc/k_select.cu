@@ -21,7 +21,7 @@ constexpr int NBINS = 1 << RADIX_BITS;
 
 __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t nq, uint32_t w,
                                    const uint32_t* __restrict__ list_len, uint32_t stride,
-                                   uint32_t strat, uint32_t cap, uint64_t* __restrict__ n_entries,
+                                   uint32_t cap, uint64_t* __restrict__ n_entries,
                                    uint8_t* __restrict__ sampled, uint64_t* __restrict__ pair_samples,
                                    unsigned long long* __restrict__ grand_total) {
     size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -35,7 +35,7 @@ __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t n
     unsigned long long ssum = 0;
     for (uint32_t r = 0; r < w; ++r) {
         const uint32_t len = list_len[probes[q * w + r]];
-        const uint64_t ns = (samp && r % strat == 0) ? (len + stride - 1) / stride : 0;
+        const uint64_t ns = samp ? (len + stride - 1) / stride : 0;
         pair_samples[q * w + r] = ns;
         ssum += ns;
     }
@@ -120,8 +120,8 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void sample_threshold_kernel(
     }
     const uint64_t lo = sample_off[q * w], hi = sample_off[q * w + w];
     const uint32_t n = (uint32_t)(hi - lo);
-    // the sampled (stratified) probes hold n of the query's N_q entries: the
-    // sample rank matching ~alpha*k' candidates is alpha*k' * n / N_q
+    // the n samples stand for the query's N_q entries: the sample rank
+    // matching ~alpha*k' candidates is alpha*k' * n / N_q
     const double frac = (double)n / (double)max((unsigned long long)n_entries[q], 1ull);
     const uint32_t rank = (uint32_t)max(1.0, ceil((double)alpha_k * frac));
     if (n < rank || n == 0) {
@@ -725,12 +725,12 @@ void set_smem(const void* f, size_t bytes) {
 }  // namespace
 
 void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
-                        uint32_t stride, uint32_t strat, uint32_t cap, uint64_t* nq_entries,
+                        uint32_t stride, uint32_t cap, uint64_t* nq_entries,
                         uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
                         cudaStream_t s) {
     if (nq == 0) return;
     query_sizes_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, s>>>(
-        probes, nq, w, list_len, stride, strat, cap, nq_entries, query_sampled, pair_samples,
+        probes, nq, w, list_len, stride, cap, nq_entries, query_sampled, pair_samples,
         reinterpret_cast<unsigned long long*>(grand_total));
     PQRR_LAUNCH_CHECK();
     count_launch();

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cub/device/device_radix_sort.cuh>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -117,17 +118,21 @@ __global__ void iota_base_kernel(uint32_t* out, size_t n, uint32_t base) {
     if (i < n) out[i] = base + (uint32_t)i;
 }
 
+// le (optional): per query, how many candidates have an exact distance <= tau
+// (the filter path keeps a superset of those in the buffer).
 __global__ void check_fail_kernel(const uint8_t* __restrict__ sampled, const uint32_t* __restrict__ cnt,
-                                  size_t nq, uint32_t kprime, uint32_t cap, uint8_t* __restrict__ fail,
-                                  unsigned* __restrict__ max_n, unsigned long long* __restrict__ total) {
+                                  const uint32_t* __restrict__ le, size_t nq, uint32_t kprime,
+                                  uint32_t cap, uint8_t* __restrict__ fail, unsigned* __restrict__ max_n,
+                                  unsigned long long* __restrict__ total) {
     size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
     atomicMax(max_n, min(cnt[q], cap));
     atomicAdd(total, (unsigned long long)cnt[q]);
     uint8_t f = 0;
     if (sampled[q]) {
-        if (cnt[q] < kprime) f = 1;   // threshold too tight: shortlist may be incomplete
-        else if (cnt[q] > cap) f = 2; // buffer overflow: candidates were dropped
+        const uint32_t exact = le ? le[q] : cnt[q];
+        if (cnt[q] > cap) f = 2;            // buffer overflow: candidates were dropped
+        else if (exact < kprime) f = 1;     // threshold too tight: shortlist may be incomplete
     }
     fail[q] = f;
 }
@@ -150,18 +155,6 @@ __global__ void scatter_shortlist(const u64* __restrict__ skey, const uint32_t* 
     key[q * kprime + j] = skey[i];
     pos[q * kprime + j] = spos[i];
     if (j == 0) cnt[q] = scnt[r];
-}
-
-// probes of ranks r = 0, strat, 2*strat, ... as (list, pair id = q*w + r)
-__global__ void strided_pairs_kernel(const uint32_t* __restrict__ probes, size_t nq, uint32_t w,
-                                     uint32_t strat, uint32_t ws, uint32_t* __restrict__ lists,
-                                     uint32_t* __restrict__ pair_ids) {
-    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nq * ws) return;
-    const size_t q = i / ws;
-    const uint32_t r = (uint32_t)(i % ws) * strat;
-    lists[i] = probes[q * w + r];
-    pair_ids[i] = (uint32_t)(q * w + r);
 }
 
 __global__ void min_count_kernel(const uint32_t* __restrict__ cnt, size_t nq, uint32_t k,
@@ -264,7 +257,8 @@ struct DevIndex {
     DBuf<uint8_t> codes, rcodes;
     DBuf<uint32_t> ids;
     DBuf<uint16_t> block_list;  // list of each 16-entry block of positions
-    DBuf<float> lut_cache;      // per-item LUTs shared by the sample and main passes
+    DBuf<uint8_t> q8_cache;     // per LUT-pass item 8-bit LUT (32 KiB) for the K4f filter
+    DBuf<float> q8_param;       // per LUT-pass item and query lane: (scale, sum of minima)
     uint64_t next_id = 0;
     // id -> position (lazy)
     DBuf<uint32_t> id_map;
@@ -479,7 +473,7 @@ struct ItemSet {
     uint32_t* list_cnt = nullptr;
     uint32_t* list_first = nullptr;
     uint32_t* item_off = nullptr;
-    uint32_t n_items = 0, c = 0;
+    uint32_t n_items = 0, c = 0, qt = 0;
     uint32_t *item_list = nullptr, *item_start = nullptr, *item_nq = nullptr;
     uint32_t *item_e0 = nullptr, *item_e1 = nullptr, *item_order = nullptr;
     void apply(ScanArgs& a) const {
@@ -494,19 +488,30 @@ struct ItemSet {
     }
 };
 
+// Pairs (list, pair id) sorted by list, per-list pair counts / first pair, and
+// the per-list item counts + offsets for items of <= qt queries.  `share`
+// reuses another set's sorted pairs (same pairs, different qt).
 ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_ids, size_t np,
-                     uint32_t c, const uint32_t* list_len, cudaStream_t s) {
+                     uint32_t c, const uint32_t* list_len, uint32_t qt, cudaStream_t s,
+                     const ItemSet* share = nullptr) {
     ItemSet it;
     it.c = c;
-    uint32_t* sorted_lists = ws.alloc<uint32_t>(np);
-    it.pair_sorted = ws.alloc<uint32_t>(np);
-    sort_pairs(lists, sorted_lists, pair_ids, it.pair_sorted, np, bits_for(c), s);
-    it.list_cnt = ws.zeros<uint32_t>(c + 1);
-    launch_histogram(lists, np, c, it.list_cnt, s);
-    it.list_first = ws.alloc<uint32_t>(c + 1);
-    exclusive_scan_u32(it.list_cnt, it.list_first, c + 1, s);
+    it.qt = qt;
+    if (share) {
+        it.pair_sorted = share->pair_sorted;
+        it.list_cnt = share->list_cnt;
+        it.list_first = share->list_first;
+    } else {
+        uint32_t* sorted_lists = ws.alloc<uint32_t>(np);
+        it.pair_sorted = ws.alloc<uint32_t>(np);
+        sort_pairs(lists, sorted_lists, pair_ids, it.pair_sorted, np, bits_for(c), s);
+        it.list_cnt = ws.zeros<uint32_t>(c + 1);
+        launch_histogram(lists, np, c, it.list_cnt, s);
+        it.list_first = ws.alloc<uint32_t>(c + 1);
+        exclusive_scan_u32(it.list_cnt, it.list_first, c + 1, s);
+    }
     uint32_t* items = ws.alloc<uint32_t>(c + 1);
-    launch_items_per_list(it.list_cnt, list_len, c, items, s);
+    launch_items_per_list(it.list_cnt, list_len, c, items, qt, s);
     it.item_off = ws.alloc<uint32_t>(c + 1);
     exclusive_scan_u32(items, it.item_off, c + 1, s);
     return it;
@@ -524,7 +529,7 @@ void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_l
     uint32_t* iota = ws.alloc<uint32_t>(n);
     it.item_order = ws.alloc<uint32_t>(n);
     launch_items_build(it.list_cnt, it.list_first, list_len, c, it.item_off, it.item_list,
-                       it.item_start, it.item_nq, it.item_e0, it.item_e1, key, s);
+                       it.item_start, it.item_nq, it.item_e0, it.item_e1, key, it.qt, s);
     launch_iota(iota, n, s);
     sort_pairs(key, key2, iota, it.item_order, n, 32, s);
 }
@@ -539,20 +544,22 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     auto& st = ix.stats;
     const uint32_t c = ix.c;
     const size_t P = nq * (size_t)w;
-    // candidate buffer per query: >= 4k' (the sampled threshold targets ~2k');
-    // beyond 8192 the selector streams candidates from global memory
-    const uint32_t cap = std::max<uint32_t>(8192, ((4 * kprime + 1023) / 1024) * 1024);
-    // sample density: ~64 samples expected below the alpha*k'-th distance; the
-    // sampled probe ranks hold ~1/strat of the candidates (strat set below)
-    static const int strat_env = [] {
-        const char* e = getenv("PQRR_STRAT");
-        return e ? atoi(e) : 0;
+    // K4f (filter + exact recheck) unless disabled or out of its envelope:
+    // m = 8, ks = 256, w*d residuals in shared memory, and an 8-bit LUT cache
+    // of 32 KiB per item (index-owned: a per-search allocation of GBs was
+    // measured to pay first-touch costs on every batch)
+    static const bool exact_env = [] {
+        const char* e = getenv("PQRR_SCAN");
+        return e && std::string(e) == "exact";
     }();
-    // Probe-rank stratified sampling (PQRR_STRAT > 1) is measured biased: the
-    // nearest probes hold a disproportionate share of the top-k', so the
-    // estimate runs tight and queries underflow.  Default: sample all probes.
-    const uint32_t strat_h = strat_env > 0 ? (uint32_t)strat_env : 1;
-    uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / (64.0 * strat_h)));
+    const bool filter_ok = !exact_env && ix.m == 8 && ix.ks == 256 && recheck_supported(ix.d, ix.m, w);
+    // candidate buffer per query: the sampled threshold targets ~2k' entries;
+    // >= 4k' for the exact scan, >= 8k' for the filter's superset; beyond
+    // 8192 the selector streams candidates from global memory
+    const uint32_t cap_mul = filter_ok ? 8 : 4;
+    const uint32_t cap = std::max<uint32_t>(8192, ((cap_mul * kprime + 1023) / 1024) * 1024);
+    // sample density: ~64 samples expected below the alpha*k'-th distance
+    uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / 64.0));
     stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
     Workspace ws(s);
 
@@ -563,41 +570,43 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     launch_topw(D, nq, c, w, probes, nullptr, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[1], s));
 
-    // ---- invert probes into list-major work items: all pairs (main pass) and
-    // the stratified subset of probe ranks r % strat == 0 (sample pass)
-    const uint32_t strat = strat_h;
-    const uint32_t ws_ = (w + strat - 1) / strat;
-    const size_t Ps = nq * (size_t)ws_;
+    // ---- invert probes into list-major work items: 16-query items for the
+    // LUT pass (and the exact scan), 64-query items for the K4f filter
     uint32_t* pair_ids = ws.alloc<uint32_t>(P);
     launch_iota(pair_ids, P, s);
-    ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, s);
-    ItemSet is = im;  // sample pass: same items unless stratified
-    if (strat > 1) {
-        uint32_t* sp_lists = ws.alloc<uint32_t>(Ps);
-        uint32_t* sp_ids = ws.alloc<uint32_t>(Ps);
-        strided_pairs_kernel<<<nblk(Ps), 256, 0, s>>>(probes, nq, w, strat, ws_, sp_lists, sp_ids);
-        PQRR_LAUNCH_CHECK();
-        count_launch();
-        is = items_phase1(ws, sp_lists, sp_ids, Ps, c, ix.list_len.p, s);
-    }
+    ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s);
+    ItemSet if64 = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kFQ, s, &im);
     uint64_t* n_entries = ws.alloc<uint64_t>(nq);
     uint8_t* sampled = ws.alloc<uint8_t>(nq);
     uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
     uint64_t* grand = ws.zeros<uint64_t>(2);
-    launch_query_sizes(probes, nq, w, ix.list_len.p, stride, strat, cap, n_entries, sampled,
-                       pair_samples, grand, s);
+    launch_query_sizes(probes, nq, w, ix.list_len.p, stride, cap, n_entries, sampled, pair_samples,
+                       grand, s);
     uint64_t* sample_off = ws.alloc<uint64_t>(P + 1);
     exclusive_scan_u64(pair_samples, sample_off, P + 1, s);
     uint64_t total_samples = 0, h_grand[2] = {0, 0};
     PQRR_CUDA(cudaMemcpyAsync(h_grand, grand, 16, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&total_samples, sample_off + P, 8, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
-    if (strat > 1) PQRR_CUDA(cudaMemcpyAsync(&is.n_items, is.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaMemcpyAsync(&if64.n_items, if64.item_off + c, 4, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaStreamSynchronize(s));
     const uint32_t n_items = im.n_items;
+
+    bool use_filter = filter_ok;
+    if (use_filter) {
+        const size_t need = (size_t)n_items * 8 * 256 * kQT;
+        if (ix.q8_cache.bytes() < need) {
+            size_t free_b = 0, total_b = 0;
+            PQRR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            if (need - ix.q8_cache.bytes() < free_b / 2) {
+                ix.q8_cache.alloc(need);
+                ix.q8_param.alloc((size_t)n_items * kQT * 2);
+            }
+        }
+        use_filter = ix.q8_cache.bytes() >= need;
+    }
     items_phase2(ws, im, c, ix.list_len.p, s);
-    if (strat == 1) is = im;
-    else if (total_samples) items_phase2(ws, is, c, ix.list_len.p, s);
+    if (use_filter) items_phase2(ws, if64, c, ix.list_len.p, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[2], s));
 
     ScanArgs a{};
@@ -615,32 +624,19 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     a.query_sampled = sampled;
     uint32_t* counter = ws.zeros<uint32_t>(2);
 
-    // ---- sample pass (threshold estimation)
+    // ---- K2 LUT pass: per item the exact LUT -> sampled distances (threshold
+    // estimation) and, for the filter, the 8-bit LUT block
     float* tau = ws.alloc<float>(nq);
     float* sample_dist = ws.alloc<float>(total_samples);
-    // LUT reuse: the sample pass stores each item's LUT, the main pass
-    // bulk-loads it (same item set when not stratified; bounded by free HBM)
-    a.lut_mode = 0;
-    a.lut_cache = nullptr;
-    if (total_samples && strat == 1) {
-        size_t free_b = 0, total_b = 0;
-        PQRR_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        const size_t need = (size_t)n_items * 8 * 256 * 16 * sizeof(float);
-        // persistent (index-owned) buffer: a per-search allocation of several
-        // GB was measured to pay first-touch costs on every batch
-        if (ix.m == 8 && ix.ks == 256) {
-            if (ix.lut_cache.bytes() < need && need - ix.lut_cache.bytes() < free_b / 2)
-                ix.lut_cache.alloc(need / 4);
-            if (ix.lut_cache.bytes() >= need) a.lut_cache = ix.lut_cache.p;
-        }
-    }
-    if (total_samples) {
-        is.apply(a);
-        a.lut_mode = a.lut_cache ? 1 : 0;
+    if (total_samples || use_filter) {
+        im.apply(a);
+        a.pass = 1;
+        a.q8_cache = use_filter ? ix.q8_cache.p : nullptr;
+        a.q8_param = use_filter ? ix.q8_param.p : nullptr;
         a.stride = stride;
         a.sample_off = sample_off;
-        a.sample_dist = sample_dist;
-        a.tau = tau;  // unused in sample mode
+        a.sample_dist = total_samples ? sample_dist : nullptr;
+        a.tau = tau;  // unused in the LUT pass
         a.item_counter = counter;
         launch_ivf_scan(a, s);
     }
@@ -649,26 +645,86 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
                             n_entries, (uint32_t)h_grand[1], tau, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[4], s));
 
-    // ---- K4 main scan
+    // ---- K4 main scan: candidates (d <= tau, or the filter's superset)
     float* cand_dist = ws.alloc<float>(nq * (size_t)cap);
     uint32_t* cand_pos = ws.alloc<uint32_t>(nq * (size_t)cap);
     uint32_t* cand_cnt = ws.zeros<uint32_t>(nq);
-    im.apply(a);
-    a.lut_mode = (total_samples && a.lut_cache) ? 2 : 0;
-    a.stride = 1;
-    a.tau = tau;
-    a.cand_dist = cand_dist;
-    a.cand_pos = cand_pos;
-    a.cand_cnt = cand_cnt;
-    a.item_counter = counter + 1;
-    launch_ivf_scan(a, s);
+    uint32_t* cand_le = nullptr;
+    if (use_filter) {
+        FilterArgs f{};
+        f.codes = ix.codes.p;
+        f.list_off = ix.list_off.p;
+        f.list_len = ix.list_len.p;
+        f.item_list = if64.item_list;
+        f.item_start = if64.item_start;
+        f.item_nq = if64.item_nq;
+        f.item_order = if64.item_order;
+        f.num_items = if64.item_off + c;
+        f.item_counter = counter + 1;
+        f.list_first = im.list_first;
+        f.sub_item_off = im.item_off;
+        f.pair_sorted = im.pair_sorted;
+        f.w = w;
+        f.tau = tau;
+        f.q8_cache = ix.q8_cache.p;
+        f.q8_param = ix.q8_param.p;
+        f.cand_aux = reinterpret_cast<uint32_t*>(cand_dist);
+        f.cand_pos = cand_pos;
+        f.cand_cnt = cand_cnt;
+        f.cap = cap;
+        static const bool pass_all = getenv("PQRR_FILTER_ALL") != nullptr;  // debug hook
+        f.pass_all = pass_all ? 1 : 0;
+        launch_ivf_filter(f, s);
+        cand_le = ws.alloc<uint32_t>(nq);
+        launch_recheck(xq, ix.d, ix.m, ix.coarse.p, ix.books.p, probes, w, ix.codes.p, cand_cnt, cap,
+                       cand_pos, cand_dist, tau, nq, cand_le, s);
+        static const char* dump = getenv("PQRR_DEBUG_DUMP");  // debug hook: raw filter state
+        if (dump && depth == 0) {
+            PQRR_CUDA(cudaStreamSynchronize(s));
+            auto put = [&](const char* name, const void* src, size_t bytes) {
+                std::vector<char> h(bytes);
+                if (bytes) PQRR_CUDA(cudaMemcpy(h.data(), src, bytes, cudaMemcpyDeviceToHost));
+                std::string path = std::string(dump) + "/" + name;
+                FILE* fp = fopen(path.c_str(), "wb");
+                if (fp) {
+                    fwrite(h.data(), 1, bytes, fp);
+                    fclose(fp);
+                }
+            };
+            put("tau.bin", tau, nq * 4);
+            put("probes.bin", probes, P * 4);
+            put("cand_cnt.bin", cand_cnt, nq * 4);
+            put("cand_le.bin", cand_le, nq * 4);
+            put("q8_param.bin", ix.q8_param.p, (size_t)n_items * kQT * 8);
+            put("q8_cache.bin", ix.q8_cache.p, (size_t)n_items * 8 * 256 * kQT);
+            put("item_list.bin", im.item_list, n_items * 4);
+            put("item_start.bin", im.item_start, n_items * 4);
+            put("item_nq.bin", im.item_nq, n_items * 4);
+            put("pair_sorted.bin", im.pair_sorted, P * 4);
+            put("cand_pos.bin", cand_pos, nq * (size_t)cap * 4);
+            put("cand_dist.bin", cand_dist, nq * (size_t)cap * 4);
+        }
+    } else {
+        im.apply(a);
+        a.pass = 0;
+        a.q8_cache = nullptr;
+        a.q8_param = nullptr;
+        a.stride = 1;
+        a.sample_dist = nullptr;
+        a.tau = tau;
+        a.cand_dist = cand_dist;
+        a.cand_pos = cand_pos;
+        a.cand_cnt = cand_cnt;
+        a.item_counter = counter + 1;
+        launch_ivf_scan(a, s);
+    }
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[5], s));
 
     // ---- exactness check of the threshold
     uint8_t* fail = ws.alloc<uint8_t>(nq);
     unsigned* maxn = ws.zeros<unsigned>(4);
-    check_fail_kernel<<<nblk(nq), 256, 0, s>>>(sampled, cand_cnt, nq, kprime, cap, fail, maxn,
-                                                reinterpret_cast<unsigned long long*>(maxn + 2));
+    check_fail_kernel<<<nblk(nq), 256, 0, s>>>(sampled, cand_cnt, cand_le, nq, kprime, cap, fail,
+                                                maxn, reinterpret_cast<unsigned long long*>(maxn + 2));
     PQRR_LAUNCH_CHECK();
     count_launch();
     std::vector<uint8_t> h_fail(nq);
