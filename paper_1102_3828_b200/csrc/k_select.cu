@@ -595,6 +595,105 @@ __global__ __launch_bounds__(RW_WARPS * 32) void rerank_warp_kernel(
     if (threadIdx.x == 0) out_cnt[q] = cnt;
 }
 
+// K5a (cooperative, d = 128, m = 8, ks = 256): refined distances of every
+// shortlist entry.  Persistent CTAs keep the PQ code book (128 KiB) in shared
+// memory; a warp takes 32 candidates of one query at a time.  Lane g owns
+// dims 4g..4g+3: the coarse row (512 B) and refinement rows are read as
+// coalesced segments, the code-book row from shared memory, and
+//   yhat = (C_l + B(code)) + R(rcode),  sq = (x - yhat)^2
+// goes to a padded 8-candidate tile.  Lanes (candidate, k) then sum
+// sq[4g + k] for g = 0..31 sequentially — the reference 4-accumulator order of
+// l2_sq (distance.hpp:16-33) — and (s0 + s1) + (s2 + s3) is formed by
+// shuffles.  Metadata (position, id, list, code bytes) of the 32 candidates is
+// loaded by all lanes at once so its dependent latency is paid once per 32.
+constexpr int RC_WARPS = 16;
+constexpr int RC_TLD = 132;  // tile row stride (floats): conflict-free transposed reads
+
+template <int DSR>
+__global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
+    const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
+    const uint32_t* __restrict__ sl_cnt, uint32_t stride, size_t nq, const float* __restrict__ xq,
+    const uint16_t* __restrict__ block_list, const float* __restrict__ coarse,
+    const uint8_t* __restrict__ codes, const float* __restrict__ books,
+    const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks,
+    float* __restrict__ rdist, uint32_t* __restrict__ rid) {
+    constexpr int D = 128, MP = D / DSR;  // m' = D / DSR
+    constexpr int META = 32 + 64 + 8 * MP;  // words per warp: list[32], code[32] u64, rcode[32][MP] B
+    extern __shared__ float4 rc_smem[];
+    float4* bk = rc_smem;                                            // [8][256][4] float4
+    float* tiles = reinterpret_cast<float*>(rc_smem + 8 * 256 * 4);  // [warps][8][RC_TLD]
+    uint32_t* meta = reinterpret_cast<uint32_t*>(tiles + RC_WARPS * 8 * RC_TLD);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* m_list = meta + warp * META;
+    u64* m_code = reinterpret_cast<u64*>(m_list + 32);
+    uint8_t* m_rcode = reinterpret_cast<uint8_t*>(m_list + 32 + 64);
+    float* tile = tiles + warp * 8 * RC_TLD;
+    for (uint32_t i = threadIdx.x; i < 8 * 256 * 4; i += blockDim.x)
+        bk[i] = __ldg(reinterpret_cast<const float4*>(books) + i);
+    __syncthreads();
+
+    const uint32_t g = lane;
+    const uint32_t jj = g / 4, bo = g % 4;                  // book row part (float4 index)
+    const uint32_t jr = (4 * g) / DSR, ro = (4 * g) % DSR;  // refinement row, float offset
+    const uint32_t cpq = (stride + 31) / 32;
+    const size_t total = nq * (size_t)cpq;
+    const size_t tw = (size_t)gridDim.x * RC_WARPS;
+    for (size_t ch = (size_t)blockIdx.x * RC_WARPS + warp; ch < total; ch += tw) {
+        const size_t q = ch / cpq;
+        const uint32_t i0 = (uint32_t)(ch % cpq) * 32;
+        const uint32_t n = sl_cnt[q];
+        if (i0 >= n) continue;
+        const uint32_t nb = min(32u, n - i0);
+        const size_t t0 = q * stride + i0;
+        if ((uint32_t)lane < nb) {
+            const uint32_t pos = sl_pos[t0 + lane];
+            rid[t0 + lane] = key_id(sl_key[t0 + lane]);
+            m_list[lane] = block_list[pos >> 4];
+            m_code[lane] = *reinterpret_cast<const u64*>(codes + (size_t)pos * 8);
+            if constexpr (MP % 16 == 0) {
+                const uint4* rsrc = reinterpret_cast<const uint4*>(rcodes + (size_t)pos * MP);
+#pragma unroll
+                for (int v = 0; v < MP / 16; ++v) reinterpret_cast<uint4*>(m_rcode + lane * MP)[v] = rsrc[v];
+            } else {
+                *reinterpret_cast<u64*>(m_rcode + lane * MP) =
+                    *reinterpret_cast<const u64*>(rcodes + (size_t)pos * MP);
+            }
+        }
+        const float4 x = reinterpret_cast<const float4*>(xq + q * D)[g];
+        __syncwarp();
+        for (uint32_t sb = 0; sb < nb; sb += 8) {
+#pragma unroll 4
+            for (int c = 0; c < 8; ++c) {
+                const uint32_t ci = min(sb + c, nb - 1);
+                const uint32_t l = m_list[ci];
+                const uint32_t code = (uint32_t)(m_code[ci] >> (8 * jj)) & 0xffu;
+                const uint32_t rcode = m_rcode[ci * MP + jr];
+                const float4 cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + g);
+                const float4 bv = bk[(jj * 256 + code) * 4 + bo];
+                const float4 rv = __ldg(reinterpret_cast<const float4*>(
+                    rbooks + ((size_t)jr * 256 + rcode) * DSR + ro));
+                const float d0 = __fsub_rn(x.x, __fadd_rn(__fadd_rn(cv.x, bv.x), rv.x));
+                const float d1 = __fsub_rn(x.y, __fadd_rn(__fadd_rn(cv.y, bv.y), rv.y));
+                const float d2 = __fsub_rn(x.z, __fadd_rn(__fadd_rn(cv.z, bv.z), rv.z));
+                const float d3 = __fsub_rn(x.w, __fadd_rn(__fadd_rn(cv.w, bv.w), rv.w));
+                *reinterpret_cast<float4*>(tile + c * RC_TLD + 4 * g) =
+                    make_float4(__fmul_rn(d0, d0), __fmul_rn(d1, d1), __fmul_rn(d2, d2), __fmul_rn(d3, d3));
+            }
+            __syncwarp();
+            const int cc = lane >> 2, k = lane & 3;
+            float sacc = 0.f;
+#pragma unroll 8
+            for (int gg = 0; gg < 32; ++gg) sacc = __fadd_rn(sacc, tile[cc * RC_TLD + 4 * gg + k]);
+            const float s1 = __shfl_down_sync(0xffffffffu, sacc, 1);
+            const float pair = __fadd_rn(sacc, s1);  // lanes k = 0: s0+s1, k = 2: s2+s3
+            const float p23 = __shfl_down_sync(0xffffffffu, pair, 2);
+            const float dist = __fadd_rn(pair, p23);
+            if (k == 0 && sb + cc < nb) rdist[t0 + sb + cc] = dist;
+            __syncwarp();
+        }
+    }
+}
+
 // K5a: refined distances of every shortlist entry, one thread per candidate
 // (no shared memory, full occupancy: the random code / code-book gathers are
 // latency bound).  Rows shorter than the stride are padded with +inf keys.
@@ -798,15 +897,47 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
     const size_t smem = ((d + 3) & ~3u) * sizeof(float) + (size_t)n2 * sizeof(u64);
     if (smem > 200 * 1024) throw ArgError("shortlist too large for the device re-ranker");
     const bool fast = d % 4 == 0 && (d / m) % 4 == 0 && (d / mprime) % 4 == 0;
-    // default: one CTA per query (measured fastest: C2 2.24 ms vs 2.56 split,
-    // 3.2 warp); PQRR_RERANK=split|warp select the alternatives (A/B runs)
+    // default: cooperative distances (d = 128, m = 8, ks = 256) + radix top-k;
+    // PQRR_RERANK=cta|split|warp select the older kernels (A/B runs)
     static const std::string impl = [] {
         const char* e = getenv("PQRR_RERANK");
-        return std::string(e ? e : "cta");
+        return std::string(e ? e : "coop");
     }();
     const bool want_warp = impl == "warp";
     uint32_t k2 = 1;
     while (k2 < k) k2 <<= 1;
+    const uint32_t dsr = mprime ? d / mprime : 0;
+    const bool coop_ok = impl == "coop" && d == 128 && m == 8 && ks == 256 && mprime * dsr == d &&
+                         (dsr == 4 || dsr == 8 || dsr == 16) && (size_t)k2 * 8 <= 200 * 1024;
+    if (coop_ok) {
+        const size_t tot = nq * (size_t)sl_stride;
+        float* rd = nullptr;
+        uint32_t* ri = nullptr;
+        PQRR_CUDA(cudaMallocAsync(&rd, tot * sizeof(float), s));
+        PQRR_CUDA(cudaMallocAsync(&ri, tot * sizeof(uint32_t), s));
+        const uint32_t mp = d / dsr;
+        const size_t csmem = (size_t)8 * 256 * 16 * sizeof(float) +
+                             (size_t)RC_WARPS * 8 * RC_TLD * sizeof(float) +
+                             (size_t)RC_WARPS * (32 + 64 + 8 * mp) * sizeof(uint32_t);
+        auto go = [&](auto kern) {
+            set_smem((const void*)kern, csmem);
+            kern<<<sm_count(), RC_WARPS * 32, csmem, s>>>(
+                reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, nq, xq, block_list,
+                coarse, codes, books, rcodes, rbooks, rd, ri);
+        };
+        if (dsr == 8) go(rerank_coop_kernel<8>);
+        else if (dsr == 4) go(rerank_coop_kernel<4>);
+        else go(rerank_coop_kernel<16>);
+        PQRR_LAUNCH_CHECK();
+        set_smem((const void*)rerank_topk_kernel, (size_t)k2 * 8);
+        rerank_topk_kernel<<<(unsigned)nq, SEL_THREADS, (size_t)k2 * 8, s>>>(
+            rd, ri, sl_cnt, sl_stride, k, k2, out_ids, out_dists, out_cnt);
+        PQRR_LAUNCH_CHECK();
+        PQRR_CUDA(cudaFreeAsync(rd, s));
+        PQRR_CUDA(cudaFreeAsync(ri, s));
+        count_launch(2);
+        return;
+    }
     if (impl == "split" && (size_t)k2 * 8 <= 200 * 1024) {
         const size_t tot = nq * (size_t)sl_stride;
         float* rd = nullptr;
