@@ -297,7 +297,7 @@ def main():
             step_ms.append(e0.elapsed_time(e1))
             st = ix.last_stats()
             stats.append(st)
-            scan_ms.append(st["ms_scan"])
+            scan_ms.append(st["ms_filter"] if st["ms_filter"] > 0 else st["ms_scan"])
     torch.cuda.synchronize()
     launches = pq.launch_count() - launches0
     total_ms = float(np.sum(step_ms))
@@ -341,32 +341,38 @@ def main():
     if not args.no_recall and world == 1:
         extra.update(recall_and_parity(pq, cfg, queries, res_ids, ix, coarse, P, rq))
 
-    # ---- roofline of the dominant kernel (the main ADC scan)
+    # ---- roofline of the dominant kernel: the main ADC scan (K4f filter; the
+    # fp32 exact scan when the filter is disabled)
     st = stats[-1]
+    filt = st["ms_filter"] > 0
     scanned = float(np.mean([s["scanned_entries"] for s in stats]))
     bytes_per_step = scanned * (cfg["m"] + 4)
     scan_s = float(np.mean(scan_ms)) / 1e3
     peak, kind = measured_peak_gbs()
     achieved = bytes_per_step / scan_s / 1e9
     clocks = clk.summary()
-    # The scan is list-major: its physical DRAM traffic is tiny and its real
-    # bound is shared-memory LUT gathers: m lookups per
-    # scanned (entry, query) against one 128-B wavefront (32 fp32 lookups) per
-    # clock per SM at the measured SM clock.
+    # The scan is list-major: its physical DRAM traffic is small and its real
+    # bound is shared-memory LUT gathers: m lookups per scanned
+    # (entry, query).  K4f gathers 1-byte (5-bit) table entries, 16 queries per
+    # LDS.128, against the 128 B/clk/SM shared-memory pipe; the exact fp32 scan
+    # gathers 4 bytes per lookup (32 lookups/clk/SM).
     import torch as _t
 
     n_sm = _t.cuda.get_device_properties(local).multi_processor_count
     f_sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
     lookups = scanned * cfg["m"]
-    smem_ach = lookups / scan_s / (n_sm * f_sm)
+    lk_per_clk = lookups / scan_s / (n_sm * f_sm)
+    lut_bytes = 1.0 if filt else 4.0
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "scan_traffic.json")) as f:
             tj = json.load(f)
-        if tj.get("config") == args.config:
+        if tj.get("config") == args.config and tj.get("kernel", "").startswith(
+                "ivf_filter" if filt else "ivf_scan"):
             traffic = tj["dram_bytes_per_launch"]
     except Exception:
         pass
+    kname = "ivf_filter_kernel (K4f, 5-bit LUT filter)" if filt else "ivf_scan_kernel (exact main pass)"
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -379,18 +385,24 @@ def main():
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": kind,
-                     "kernel": "ivf_scan_kernel (main pass)",
+                     "kernel": kname,
                      "algorithmic_bytes_per_launch": bytes_per_step,
                      "kernel_ms": scan_s * 1e3,
                      "note": "list-major scan: B_q = sum len*(m+4) per query (SURVEY §8d); "
                              "frac > 1 = reuse across the batch; true bound = smem gathers"},
-        "roofline_smem": {"bound": "smem LUT gathers", "achieved": smem_ach, "peak": 32.0,
-                          "unit": "fp32 lookups/clk/SM", "frac": smem_ach / 32.0,
-                          "lookups_per_launch": lookups, "sm_count": n_sm,
+        "roofline_smem": {"bound": "smem LUT gathers", "achieved": lk_per_clk * lut_bytes,
+                          "peak": 128.0, "unit": "B/clk/SM", "frac": lk_per_clk * lut_bytes / 128.0,
+                          "lookups_per_launch": lookups, "bytes_per_lookup": lut_bytes,
+                          "lookups_per_clk_per_sm": lk_per_clk,
+                          "fp32_gather_bound_lookups_per_clk": 32.0,
+                          "vs_fp32_gather_bound": lk_per_clk / 32.0, "sm_count": n_sm,
                           "sm_clock_mhz": f_sm / 1e6},
+        "filter": {"candidates_per_query": float(np.mean([s["candidates"] for s in stats])) / nq,
+                   "exact_le_tau_per_query": float(np.mean([s["exact_candidates"] for s in stats])) / nq}
+        if filt else None,
         "stages_ms": {k2: round(float(np.mean([s[k2] for s in stats])), 4)
                       for k2 in ["ms_coarse", "ms_invert", "ms_sample_scan", "ms_threshold",
-                                 "ms_scan", "ms_select", "ms_rerank", "ms_total"]},
+                                 "ms_filter", "ms_scan", "ms_select", "ms_rerank", "ms_total"]},
         "search_stats": {k2: st[k2] for k2 in ["work_items", "retries", "stride", "kernels",
                                                "scanned_entries", "sampled_entries"]},
         "clocks": clocks,

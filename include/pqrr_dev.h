@@ -195,6 +195,8 @@ typedef struct {
     uint64_t nq, scanned_entries, sampled_entries, candidates;
     uint32_t work_items, retries, stride;
     uint32_t kernels;
+    float ms_filter;           /* K4f alone (ms_scan = K4f + K4r, or the exact scan) */
+    uint64_t exact_candidates; /* candidates with exact ADC <= tau (K4f path) */
 } pqrr_dev_search_stats;
 int pqrr_dev_last_search_stats(pqrr_dev_index* ix, pqrr_dev_search_stats* out);
 

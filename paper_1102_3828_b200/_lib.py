@@ -52,7 +52,8 @@ class SearchStats(C.Structure):
                 ("nq", C.c_uint64), ("scanned_entries", C.c_uint64),
                 ("sampled_entries", C.c_uint64), ("candidates", C.c_uint64),
                 ("work_items", C.c_uint32), ("retries", C.c_uint32), ("stride", C.c_uint32),
-                ("kernels", C.c_uint32)]
+                ("kernels", C.c_uint32), ("ms_filter", C.c_float),
+                ("exact_candidates", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

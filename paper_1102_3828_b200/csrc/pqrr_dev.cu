@@ -123,11 +123,13 @@ __global__ void iota_base_kernel(uint32_t* out, size_t n, uint32_t base) {
 __global__ void check_fail_kernel(const uint8_t* __restrict__ sampled, const uint32_t* __restrict__ cnt,
                                   const uint32_t* __restrict__ le, size_t nq, uint32_t kprime,
                                   uint32_t cap, uint8_t* __restrict__ fail, unsigned* __restrict__ max_n,
-                                  unsigned long long* __restrict__ total) {
+                                  unsigned long long* __restrict__ total,
+                                  unsigned long long* __restrict__ total_le) {
     size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
     atomicMax(max_n, min(cnt[q], cap));
     atomicAdd(total, (unsigned long long)cnt[q]);
+    if (le) atomicAdd(total_le, (unsigned long long)le[q]);
     uint8_t f = 0;
     if (sampled[q]) {
         const uint32_t exact = le ? le[q] : cnt[q];
@@ -675,6 +677,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         static const bool pass_all = getenv("PQRR_FILTER_ALL") != nullptr;  // debug hook
         f.pass_all = pass_all ? 1 : 0;
         launch_ivf_filter(f, s);
+        if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[9], s));
         cand_le = ws.alloc<uint32_t>(nq);
         launch_recheck(xq, ix.d, ix.m, ix.coarse.p, ix.books.p, probes, w, ix.codes.p, cand_cnt, cap,
                        cand_pos, cand_dist, tau, nq, cand_le, s);
@@ -722,21 +725,23 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
 
     // ---- exactness check of the threshold
     uint8_t* fail = ws.alloc<uint8_t>(nq);
-    unsigned* maxn = ws.zeros<unsigned>(4);
+    unsigned* maxn = ws.zeros<unsigned>(6);
     check_fail_kernel<<<nblk(nq), 256, 0, s>>>(sampled, cand_cnt, cand_le, nq, kprime, cap, fail,
-                                                maxn, reinterpret_cast<unsigned long long*>(maxn + 2));
+                                                maxn, reinterpret_cast<unsigned long long*>(maxn + 2),
+                                                reinterpret_cast<unsigned long long*>(maxn + 4));
     PQRR_LAUNCH_CHECK();
     count_launch();
     std::vector<uint8_t> h_fail(nq);
-    unsigned h_maxn[4] = {0, 0, 0, 0};
+    unsigned h_maxn[6] = {0, 0, 0, 0, 0, 0};
     PQRR_CUDA(cudaMemcpyAsync(h_fail.data(), fail, nq, cudaMemcpyDeviceToHost, s));
-    PQRR_CUDA(cudaMemcpyAsync(h_maxn, maxn, 16, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaMemcpyAsync(h_maxn, maxn, 24, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaStreamSynchronize(s));
     static const bool force_retry = getenv("PQRR_FORCE_RETRY") != nullptr;  // test hook
     if (force_retry && depth == 0)
         for (size_t q = 0; q < nq; ++q) h_fail[q] = (uint8_t)(1 + (q & 1));
-    uint64_t total_cand = 0;
+    uint64_t total_cand = 0, total_le = 0;
     std::memcpy(&total_cand, h_maxn + 2, 8);
+    std::memcpy(&total_le, h_maxn + 4, 8);
 
     // ---- exact top-k' selection
     launch_select_topk(cand_dist, cand_pos, cand_cnt, cap, h_maxn[0], nq, ix.ids.p, kprime, sorted,
@@ -745,6 +750,12 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     PQRR_CUDA(cudaStreamSynchronize(s));
     if (timed) {
         st.candidates += total_cand;
+        st.exact_candidates += use_filter ? total_le : total_cand;
+        if (use_filter) {
+            float fm = 0.f;
+            cudaEventElapsedTime(&fm, ix.ev[4], ix.ev[9]);
+            st.ms_filter = fm;
+        }
         st.work_items += n_items;
         st.sampled_entries += total_samples;
         st.scanned_entries += h_grand[0];
