@@ -344,14 +344,26 @@ class IvfIndex:
         return lo, po
 
     # -- search
-    def search(self, queries, v: int, kprime: int, k: int = 0):
-        """Batched fused search; returns (ids, dists, counts) arrays of width k or kprime."""
+    def search(self, queries, v: int, kprime: int, k: int = 0, out=None):
+        """Batched fused search; returns (ids, dists, counts) arrays of width k or kprime.
+
+        ``out`` (optional) = caller-owned (ids uint32 [nq, width], dists float32
+        [nq, width], counts uint32 [nq]) C-contiguous arrays written in place —
+        e.g. page-locked buffers reused across batches, so the device-to-host
+        copy of the results runs at full PCIe / C2C bandwidth."""
         q = _vectorset(queries, self.pq.d)
         nq = q.shape[0]
         width = k if k else kprime
-        ids = np.zeros((nq, width), np.uint32)
-        dists = np.zeros((nq, width), np.float32)
-        counts = np.zeros(nq, np.uint32)
+        if out is None:
+            ids = np.zeros((nq, width), np.uint32)
+            dists = np.zeros((nq, width), np.float32)
+            counts = np.zeros(nq, np.uint32)
+        else:
+            ids, dists, counts = out
+            for a, dt, shp in ((ids, np.uint32, (nq, width)), (dists, np.float32, (nq, width)),
+                               (counts, np.uint32, (nq,))):
+                if a.dtype != dt or a.shape != shp or not a.flags["C_CONTIGUOUS"]:
+                    raise ValueError("out arrays: expected C-contiguous %s %s" % (np.dtype(dt), shp))
         if q.dtype == np.uint8:
             check(lib.pqrr_dev_search_u8(self.h, np.ascontiguousarray(q), nq, v, kprime, k, ids, dists,
                                          counts))

@@ -217,6 +217,32 @@ def test_search_matches_oracle(mid_instance, v, kprime, k):
     np.testing.assert_array_equal(bits(dd), bits(rd))
     st = dix.last_stats()
     assert st["kernels"] > 5 and st["ms_scan"] > 0
+    # K4f keeps a superset of the exact candidates (<= tau)
+    assert st["exact_candidates"] <= st["candidates"]
+    # caller-owned output buffers give the same results
+    out = (np.empty((len(q), k), np.uint32), np.empty((len(q), k), np.float32),
+           np.empty(len(q), np.uint32))
+    oi2, od2, oc2 = dix.search(q, v, kprime, k, out=out)
+    assert oi2 is out[0] and od2 is out[1] and oc2 is out[2]
+    np.testing.assert_array_equal(out[0], ri)
+    np.testing.assert_array_equal(bits(out[1]), bits(rd))
+    with pytest.raises(ValueError):
+        dix.search(q, v, kprime, k, out=(out[0].astype(np.int64), out[1], out[2]))
+
+
+def test_exact_scan_fallback_matches_oracle():
+    """PQRR_SCAN=exact (read once per process) keeps the fp32 list-major scan:
+    run the mid-size comparison in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PQRR_SCAN="exact")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "dbg_filter.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [x for x in r.stdout.splitlines() if "bad=" in x]
+    assert len(lines) == 3 and all("bad=0" in x and "env=exact" in x for x in lines), r.stdout
 
 
 def test_large_coarse_radix_probe_selection(pq, oracle):
