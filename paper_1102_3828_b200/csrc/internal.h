@@ -159,6 +159,9 @@ struct ScanArgs {
     const uint8_t* query_sampled;  // per query: 1 if the query is in sample mode
 };
 void launch_ivf_scan(const ScanArgs& a, cudaStream_t s);
+// K2 LUT pass (pass 1) as a warp-specialised kernel (k_lutpass.cu).
+bool lut_pass_supported(uint32_t d, uint32_t m, uint32_t ks);
+void launch_lut_pass(const ScanArgs& a, cudaStream_t s);
 
 // K4f: the main scan as a conservative 4-bit filter over 64-query items
 // (k_filter.cu).  Candidates are emitted as (position, probe rank); K4r

@@ -442,8 +442,13 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
 #pragma unroll
                 for (int p = 0; p < CH; ++p) {
                     const uint32_t pc = sw(j * CH + p) - j * CH;
-                    sa = acc_sq2(sa, xa[p], brow[pc * 2 + hA], nz);
-                    sb = acc_sq2(sb, xb[p], brow[pc * 2 + (hA ^ 1u)], nz);
+                    if (p == 0) {  // 0 + x == x for the rounded square x >= +0
+                        sa = sq2(sub2(xa[p], brow[pc * 2 + hA]), nz);
+                        sb = sq2(sub2(xb[p], brow[pc * 2 + (hA ^ 1u)]), nz);
+                    } else {
+                        sa = acc_sq2(sa, xa[p], brow[pc * 2 + hA], nz);
+                        sb = acc_sq2(sb, xb[p], brow[pc * 2 + (hA ^ 1u)], nz);
+                    }
                 }
                 const u64 s01 = hA ? sb : sa, s23 = hA ? sa : sb;
                 const float Lj = __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));

@@ -52,11 +52,17 @@ __device__ __forceinline__ void stage_book(float* __restrict__ dst, const float*
 // LUT[j][i][q] for the item's 16 queries.  B_j is double-buffered in shared
 // memory (cp.async of B_{j+1} overlaps the arithmetic of j); every warp reads 2
 // distinct centroid rows per LDS.128 (broadcast) and writes 32 contiguous LUT
-// words.
-template <int DSUB>
+// words.  The first square of each accumulator is not added to +0: 0 + x == x
+// exactly for the x >= +0 a rounded square is.  With MM, the minimum and
+// maximum of every (j, query lane) sub-table are reduced on the fly into
+// s_mnu / s_mxu (float bits; the values are >= +0, so the bit patterns order
+// like the values).
+template <int DSUB, bool MM>
 __device__ __forceinline__ void build_luts(float* __restrict__ lut, const float* __restrict__ xr,
                                            int xld, const float* __restrict__ books,
-                                           float* __restrict__ bbuf, u64 nz) {
+                                           float* __restrict__ bbuf, u64 nz,
+                                           unsigned* __restrict__ s_mnu = nullptr,
+                                           unsigned* __restrict__ s_mxu = nullptr) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int qq = lane & 15, ih = lane >> 4;
     constexpr int BF = KS * DSUB;
@@ -77,6 +83,7 @@ __device__ __forceinline__ void build_luts(float* __restrict__ lut, const float*
             float4 v = *reinterpret_cast<const float4*>(xr + qq * xld + j * DSUB + t);
             r[t] = v.x; r[t + 1] = v.y; r[t + 2] = v.z; r[t + 3] = v.w;
         }
+        float mn = __int_as_float(0x7f800000), mx = 0.f;
 #pragma unroll
         for (int ib = 0; ib < KS / (2 * NW); ++ib) {
             const int i = (ib * NW + warp) * 2 + ih;
@@ -85,11 +92,28 @@ __device__ __forceinline__ void build_luts(float* __restrict__ lut, const float*
 #pragma unroll
             for (int t = 0; t < DSUB; t += 4) {
                 const float4 c = *reinterpret_cast<const float4*>(b + t);
-                s01 = acc_sq2(s01, pk2(r[t], r[t + 1]), pk2(c.x, c.y), nz);
-                s23 = acc_sq2(s23, pk2(r[t + 2], r[t + 3]), pk2(c.z, c.w), nz);
+                if (t == 0) {
+                    s01 = sq2(sub2(pk2(r[t], r[t + 1]), pk2(c.x, c.y)), nz);
+                    s23 = sq2(sub2(pk2(r[t + 2], r[t + 3]), pk2(c.z, c.w)), nz);
+                } else {
+                    s01 = acc_sq2(s01, pk2(r[t], r[t + 1]), pk2(c.x, c.y), nz);
+                    s23 = acc_sq2(s23, pk2(r[t + 2], r[t + 3]), pk2(c.z, c.w), nz);
+                }
             }
-            lut[(j * KS + i) * QT + qq] =
-                __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
+            const float v = __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
+            lut[(j * KS + i) * QT + qq] = v;
+            if (MM) {
+                mn = fminf(mn, v);
+                mx = fmaxf(mx, v);
+            }
+        }
+        if (MM) {
+            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 16));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+            if (ih == 0) {
+                atomicMin(s_mnu + j * QT + qq, __float_as_uint(mn));
+                atomicMax(s_mxu + j * QT + qq, __float_as_uint(mx));
+            }
         }
         __syncthreads();  // buffer (j & 1) is refilled by the prefetch of j + 2
     }
@@ -115,36 +139,15 @@ __device__ __forceinline__ void emit1(bool hit, int q, float dist, uint32_t pos,
 // lower bound conservative.  The block goes to q8 (32 KiB) through `stage`;
 // per query lane (s, sum_j min_j) goes to param.
 __device__ __forceinline__ void quantize_item(const float* __restrict__ lut, uint32_t* __restrict__ stage,
-                                              float* __restrict__ s_mn, float* __restrict__ s_mx,
+                                              const unsigned* __restrict__ s_mnu,
+                                              const unsigned* __restrict__ s_mxu,
                                               float* __restrict__ s_min, float* __restrict__ s_rng,
-                                              float* __restrict__ s_inv,
-                                              float* __restrict__ param) {
+                                              float* __restrict__ s_inv, float* __restrict__ param) {
     const int t = threadIdx.x;
-    {
-        const int qq = t & 15, part = (t >> 4) & 3, jj = t >> 6;
-        const int rot = part & 1;  // the two half-warps read rows of opposite parity: no conflicts
-        float mn = __int_as_float(0x7f800000), mx = 0.f;
-#pragma unroll 8
-        for (int ii = 0; ii < 64; ++ii) {
-            const int i = part * 64 + ((ii + rot) & 63);
-            const float v = lut[(jj * KS + i) * QT + qq];
-            mn = fminf(mn, v);
-            mx = fmaxf(mx, v);
-        }
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 16));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-        if ((t & 31) < 16) {
-            s_mn[(t >> 5) * 16 + qq] = mn;
-            s_mx[(t >> 5) * 16 + qq] = mx;
-        }
-    }
-    __syncthreads();
     if (t < M * QT) {
-        const int jj = t >> 4, qq = t & 15;
-        const float mn = fminf(s_mn[(2 * jj) * 16 + qq], s_mn[(2 * jj + 1) * 16 + qq]);
-        const float mx = fmaxf(s_mx[(2 * jj) * 16 + qq], s_mx[(2 * jj + 1) * 16 + qq]);
-        s_min[jj * 16 + qq] = mn;
-        s_rng[jj * 16 + qq] = __fsub_rn(mx, mn);
+        const float mn = __uint_as_float(s_mnu[t]), mx = __uint_as_float(s_mxu[t]);
+        s_min[t] = mn;  // [j][q]
+        s_rng[t] = __fsub_rn(mx, mn);
     }
     __syncthreads();
     if (t < QT) {
@@ -189,8 +192,8 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
     __shared__ uint32_t s_pair[QT];
     __shared__ float s_tau[QT];
     __shared__ uint8_t s_samp[QT];
-    __shared__ __align__(16) float s_mn[NW * 16], s_mx[NW * 16], s_min[M * QT], s_rng[M * QT],
-        s_inv[QT];
+    __shared__ __align__(16) float s_min[M * QT], s_rng[M * QT], s_inv[QT];
+    __shared__ unsigned s_mnu[M * QT], s_mxu[M * QT];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int slot = lane >> 2, qd = lane & 3;
@@ -233,11 +236,16 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
                 const int q = s_q[qq];
                 xr[qq * xld + t] = q >= 0 ? __fsub_rn(a.xq[(size_t)q * a.d + t], crow[t]) : 0.f;
             }
+            if (store_q8 && threadIdx.x < M * QT) {
+                s_mnu[threadIdx.x] = 0x7f800000u;
+                s_mxu[threadIdx.x] = 0u;
+            }
             __syncthreads();
-            build_luts<DSUB>(lut, xr, xld, a.books, bbuf, nz);
+            if (store_q8) build_luts<DSUB, true>(lut, xr, xld, a.books, bbuf, nz, s_mnu, s_mxu);
+            else build_luts<DSUB, false>(lut, xr, xld, a.books, bbuf, nz);
             if (store_q8) {
                 uint32_t* stage = reinterpret_cast<uint32_t*>(bbuf);
-                quantize_item(lut, stage, s_mn, s_mx, s_min, s_rng, s_inv, a.q8_param + (size_t)it * 2 * QT);
+                quantize_item(lut, stage, s_mnu, s_mxu, s_min, s_rng, s_inv, a.q8_param + (size_t)it * 2 * QT);
                 // async TMA bulk store of the 32 KiB block; it overlaps this
                 // item's sampled scan and is waited for (read side) before the
                 // staging buffer is rewritten

@@ -640,7 +640,9 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         a.sample_dist = total_samples ? sample_dist : nullptr;
         a.tau = tau;  // unused in the LUT pass
         a.item_counter = counter;
-        launch_ivf_scan(a, s);
+        static const bool old_lut = getenv("PQRR_LUTPASS") && std::string(getenv("PQRR_LUTPASS")) == "old";
+        if (!old_lut && lut_pass_supported(ix.d, ix.m, ix.ks)) launch_lut_pass(a, s);
+        else launch_ivf_scan(a, s);
     }
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[3], s));
     launch_sample_threshold(sample_dist, sample_off, w, nq, sampled, (float)(alpha * kprime),
