@@ -234,6 +234,16 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
 void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* counts, size_t nq,
                        uint32_t parts, uint32_t width, uint32_t k, uint32_t* out_ids,
                        float* out_dists, uint32_t* out_cnt, cudaStream_t s);
+// Warp-per-query selections (k_wselect.cu); the bool variants return false
+// outside their envelope (caller falls back to the CTA kernels).
+bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* out_idx,
+                      float* out_dist, cudaStream_t s);
+void launch_select_warp(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
+                        uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime,
+                        uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s);
+bool launch_rerank_topk_warp(const float* rdist, const uint32_t* rid, const uint32_t* cnt,
+                             uint32_t stride, size_t nq, uint32_t k, uint32_t* out_ids,
+                             float* out_dists, uint32_t* out_cnt, cudaStream_t s);
 // Split keys into ids / dists ([nq][stride] -> [nq][stride]).
 void launch_unpack_keys(const uint64_t* keys, const uint32_t* cnt, size_t nq, uint32_t stride,
                         uint32_t* ids, float* dists, cudaStream_t s);

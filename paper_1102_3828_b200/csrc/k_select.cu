@@ -9,6 +9,7 @@
 #include <float.h>
 
 #include <cstdlib>
+#include <string>
 #include "common.cuh"
 #include "internal.h"
 
@@ -854,6 +855,11 @@ void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const 
                         uint32_t kprime, bool sorted, uint64_t* sl_key, uint32_t* sl_pos,
                         uint32_t* sl_cnt, cudaStream_t s) {
     if (nq == 0) return;
+    static const bool old_select = getenv("PQRR_SELECT") && std::string(getenv("PQRR_SELECT")) == "cta";
+    if (!sorted && !old_select) {  // unsorted shortlist (re-ranked next): warp per query
+        launch_select_warp(cand_dist, cand_pos, cand_cnt, cap, nq, ids, kprime, sl_key, sl_pos, sl_cnt, s);
+        return;
+    }
     uint32_t kp2 = 1;
     while (kp2 < kprime) kp2 <<= 1;
     // smem sized by the largest candidate set of this batch (max_n <= cap)
@@ -929,13 +935,16 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
         else if (dsr == 4) go(rerank_coop_kernel<4>);
         else go(rerank_coop_kernel<16>);
         PQRR_LAUNCH_CHECK();
-        set_smem((const void*)rerank_topk_kernel, (size_t)k2 * 8);
-        rerank_topk_kernel<<<(unsigned)nq, SEL_THREADS, (size_t)k2 * 8, s>>>(
-            rd, ri, sl_cnt, sl_stride, k, k2, out_ids, out_dists, out_cnt);
-        PQRR_LAUNCH_CHECK();
+        count_launch();
+        if (!launch_rerank_topk_warp(rd, ri, sl_cnt, sl_stride, nq, k, out_ids, out_dists, out_cnt, s)) {
+            set_smem((const void*)rerank_topk_kernel, (size_t)k2 * 8);
+            rerank_topk_kernel<<<(unsigned)nq, SEL_THREADS, (size_t)k2 * 8, s>>>(
+                rd, ri, sl_cnt, sl_stride, k, k2, out_ids, out_dists, out_cnt);
+            PQRR_LAUNCH_CHECK();
+            count_launch();
+        }
         PQRR_CUDA(cudaFreeAsync(rd, s));
         PQRR_CUDA(cudaFreeAsync(ri, s));
-        count_launch(2);
         return;
     }
     if (impl == "split" && (size_t)k2 * 8 <= 200 * 1024) {

@@ -1,0 +1,405 @@
+// k_wselect.cu — warp-per-query exact selections (one query per warp, no
+// block-wide barriers):
+//   * topw_warp_kernel      K1 epilogue: the w nearest coarse centroids of a
+//                           query under (dist, index) (ties -> lowest index,
+//                           SPEC.md:125), w <= 64, sorted;
+//   * select_warp_kernel    exact top-k' of a query's candidates under the
+//                           reference order (dist, id) (types.hpp:47-50,
+//                           topk.hpp:18-29), unsorted;
+//   * rerank_topk_warp_kernel  top-k of the re-ranked distances under
+//                           (dist, id), sorted, with sentinels past the count.
+// All three find the boundary key with a 4-pass 8-bit radix select on the
+// distance bits (non-negative floats order like their bit patterns) using a
+// warp-private 256-bin histogram in shared memory, then compact the keys below
+// the boundary plus the boundary's tied entries in (index / id) order.
+#include "common.cuh"
+#include "internal.h"
+
+namespace pqrr_b200 {
+namespace {
+
+constexpr int WS_WARPS = 8;  // queries per CTA
+constexpr uint32_t TIE_CAP = 256;  // boundary ties sorted in shared memory
+
+// Rank-th (1-based) smallest of n 32-bit keys key(i); on return `kth` is that
+// key and `r_eq` the number of entries equal to it that belong to the
+// rank smallest (1 <= r_eq).  The leading bits shared by the smallest and the
+// largest key are skipped (a query's candidate distances sit in a narrow band,
+// and equal leading digits would pile every lane's atomic onto one bin); the
+// remaining bits are resolved 8 at a time.
+template <class KeyF>
+__device__ __forceinline__ void warp_radix_select(uint32_t n, uint32_t rank, KeyF key,
+                                                  uint32_t* __restrict__ hist, uint32_t& kth,
+                                                  uint32_t& r_eq) {
+    const int lane = threadIdx.x & 31;
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    for (uint32_t i = lane; i < n; i += 32) {
+        const uint32_t u = key(i);
+        kmin = min(kmin, u);
+        kmax = max(kmax, u);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (kmin == kmax) {  // all keys equal
+        kth = kmin;
+        r_eq = rank;
+        return;
+    }
+    int consumed = __clz(kmin ^ kmax);  // leading bits common to every key
+    uint32_t prefix = consumed ? kmin >> (32 - consumed) : 0u;
+    uint32_t r = rank;
+#pragma unroll 1
+    while (consumed < 32) {
+        const int wd = min(8, 32 - consumed);
+        const int sh = 32 - consumed - wd;
+        const uint32_t msk = (1u << wd) - 1u;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
+        __syncwarp();
+        for (uint32_t i = lane; i < n; i += 32) {
+            const uint32_t u = key(i);
+            if (consumed == 0 || (u >> (sh + wd)) == prefix) atomicAdd(&hist[(u >> sh) & msk], 1u);
+        }
+        __syncwarp();
+        uint32_t h[8], sum = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            h[b] = hist[lane * 8 + b];
+            sum += h[b];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const uint32_t excl = incl - sum;
+        const bool mine = excl < r && r <= incl;
+        const int owner = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        uint32_t bin = 0, before = excl, bcnt = 0;
+        if (mine) {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                if (r > before + h[b]) {
+                    before += h[b];
+                } else {
+                    bin = lane * 8 + b;
+                    bcnt = h[b];
+                    break;
+                }
+            }
+        }
+        bin = __shfl_sync(0xffffffffu, bin, owner);
+        before = __shfl_sync(0xffffffffu, before, owner);
+        bcnt = __shfl_sync(0xffffffffu, bcnt, owner);
+        prefix = (prefix << wd) | bin;
+        r -= before;
+        consumed += wd;
+        __syncwarp();
+        if (bcnt == 1 && consumed < 32) {  // a single key left under this prefix
+            uint32_t v = 0;
+            for (uint32_t i = lane; i < n; i += 32) {
+                const uint32_t u = key(i);
+                if ((u >> (32 - consumed)) == prefix) v = u;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+            prefix = v;
+            break;
+        }
+    }
+    kth = prefix;
+    r_eq = r;
+}
+
+// In-warp bitonic sort of n2 (power of two, <= 1024) 64-bit keys in smem.
+__device__ __forceinline__ void warp_bitonic(u64* keys, uint32_t n2) {
+    const int lane = threadIdx.x & 31;
+    for (uint32_t k = 2; k <= n2; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = lane; i < n2 / 2; i += 32) {
+                const uint32_t lo = 2 * i - (i & (j - 1));
+                const uint32_t hi = lo + j;
+                const bool up = (lo & k) == 0;
+                const u64 a = keys[lo], b = keys[hi];
+                if ((a > b) == up) {
+                    keys[lo] = b;
+                    keys[hi] = a;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__global__ __launch_bounds__(WS_WARPS * 32) void topw_warp_kernel(const float* __restrict__ D, size_t nq,
+                                                                   uint32_t nc, uint32_t w,
+                                                                   uint32_t* __restrict__ out_idx,
+                                                                   float* __restrict__ out_dist) {
+    __shared__ uint32_t hist_all[WS_WARPS][256];
+    __shared__ u64 keys_all[WS_WARPS][64];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t q = (size_t)blockIdx.x * WS_WARPS + warp;
+    if (q >= nq) return;
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(D + q * nc);
+    uint32_t kth, r_eq;
+    warp_radix_select(nc, w, [&](uint32_t i) { return __ldg(row + i); }, hist_all[warp], kth, r_eq);
+    // compaction in index order: all keys < kth, then the first r_eq equal ones
+    u64* keys = keys_all[warp];
+    uint32_t n_out = 0, eq_taken = 0;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    constexpr int U = 8;
+    for (uint32_t base = 0; base < nc; base += 32 * U) {
+        uint32_t uu[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const uint32_t i = base + k * 32 + lane;
+            uu[k] = i < nc ? __ldg(row + i) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const uint32_t i = base + k * 32 + lane;
+            const uint32_t u = uu[k];
+            const bool lt = i < nc && u < kth;
+            const bool eq = i < nc && u == kth;
+            const unsigned meq = __ballot_sync(0xffffffffu, eq);
+            const uint32_t eq_rank = eq_taken + __popc(meq & lt_mask);
+            const bool take = lt || (eq && eq_rank < r_eq);
+            const unsigned mtake = __ballot_sync(0xffffffffu, take);
+            if (take) keys[n_out + __popc(mtake & lt_mask)] = ((u64)u << 32) | i;
+            n_out += __popc(mtake);
+            eq_taken += __popc(meq);
+        }
+    }
+    uint32_t w2 = 1;
+    while (w2 < w) w2 <<= 1;
+    for (uint32_t i = w + lane; i < w2; i += 32) keys[i] = ~0ull;
+    __syncwarp();
+    warp_bitonic(keys, w2);
+    for (uint32_t i = lane; i < w; i += 32) {
+        out_idx[q * w + i] = key_id(keys[i]);
+        if (out_dist) out_dist[q * w + i] = key_dist(keys[i]);
+    }
+}
+
+// Shortlist selection (unsorted): candidates (dist, pos) of query q, ids
+// gathered for the selected entries only.  Ties at the boundary distance are
+// resolved by id with a small warp loop (they are rare).
+__global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
+    const float* __restrict__ cand_dist, const uint32_t* __restrict__ cand_pos,
+    const uint32_t* __restrict__ cand_cnt, uint32_t cap, size_t nq, const uint32_t* __restrict__ ids,
+    uint32_t kprime, u64* __restrict__ sl_key, uint32_t* __restrict__ sl_pos,
+    uint32_t* __restrict__ sl_cnt) {
+    __shared__ uint32_t hist_all[WS_WARPS][256];
+    __shared__ u64 tie_all[WS_WARPS][TIE_CAP];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t q = (size_t)blockIdx.x * WS_WARPS + warp;
+    if (q >= nq) return;
+    const uint32_t n = min(cand_cnt[q], cap);
+    const uint32_t* dq = reinterpret_cast<const uint32_t*>(cand_dist) + q * cap;
+    const uint32_t* pq = cand_pos + q * cap;
+    u64* ok = sl_key + q * kprime;
+    uint32_t* op = sl_pos + q * kprime;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    if (n <= kprime) {
+        for (uint32_t i = lane; i < n; i += 32) {
+            const uint32_t p = pq[i];
+            ok[i] = ((u64)dq[i] << 32) | ids[p];
+            op[i] = p;
+        }
+        if (lane == 0) sl_cnt[q] = n;
+        return;
+    }
+    uint32_t kth, r_eq;
+    warp_radix_select(n, kprime, [&](uint32_t i) { return dq[i]; }, hist_all[warp], kth, r_eq);
+    // one pass, 8 chunks of 32 per iteration (loads hoisted): entries strictly
+    // below the boundary go out directly; entries at the boundary distance go
+    // to a per-warp tie buffer as (id, pos) (exact ADC ties are common: equal
+    // codes in one list); the r_eq smallest ids among them are taken after.
+    constexpr int U = 8;
+    u64* tie = tie_all[warp];
+    uint32_t n_out = 0, n_eq = 0;
+    for (uint32_t base = 0; base < n; base += 32 * U) {
+        uint32_t u[U], p[U], id[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const uint32_t i = base + k * 32 + lane;
+            u[k] = i < n ? dq[i] : 0xffffffffu;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const uint32_t i = base + k * 32 + lane;
+            p[k] = (i < n && u[k] <= kth) ? pq[i] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) id[k] = u[k] <= kth ? ids[p[k]] : 0u;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const bool lt = u[k] < kth, eq = u[k] == kth;  // padding lanes carry 0xffffffff
+            const unsigned mlt = __ballot_sync(0xffffffffu, lt), meq = __ballot_sync(0xffffffffu, eq);
+            if (lt) {
+                const uint32_t o = n_out + __popc(mlt & lt_mask);
+                ok[o] = ((u64)u[k] << 32) | id[k];
+                op[o] = p[k];
+            }
+            if (eq) {
+                const uint32_t t = n_eq + __popc(meq & lt_mask);
+                if (t < TIE_CAP) tie[t] = ((u64)id[k] << 32) | p[k];
+            }
+            n_out += __popc(mlt);
+            n_eq += __popc(meq);
+        }
+    }
+    __syncwarp();
+    if (n_eq <= TIE_CAP) {
+        if (n_eq != r_eq) {
+            uint32_t t2 = 1;
+            while (t2 < n_eq) t2 <<= 1;
+            for (uint32_t i = n_eq + lane; i < t2; i += 32) tie[i] = ~0ull;
+            __syncwarp();
+            warp_bitonic(tie, t2);
+        }
+        for (uint32_t t = lane; t < r_eq; t += 32) {
+            ok[n_out + t] = ((u64)kth << 32) | (uint32_t)(tie[t] >> 32);
+            op[n_out + t] = (uint32_t)tie[t];
+        }
+    } else {
+        // many ties (duplicate vectors): radix-select the r_eq-th smallest id
+        // among them (non-tied entries map to 0xffffffff, above every id)
+        uint32_t idk, dummy;
+        warp_radix_select(n, r_eq, [&](uint32_t i) { return dq[i] == kth ? ids[pq[i]] : 0xffffffffu; },
+                          hist_all[warp], idk, dummy);
+        uint32_t nt = 0;
+        for (uint32_t base = 0; base < n; base += 32) {
+            const uint32_t i = base + lane;
+            uint32_t pp = 0, idd = 0xffffffffu;
+            if (i < n && dq[i] == kth) {
+                pp = pq[i];
+                idd = ids[pp];
+            }
+            const bool take = idd <= idk && idd != 0xffffffffu;
+            const unsigned m = __ballot_sync(0xffffffffu, take);
+            if (take) {
+                const uint32_t o = n_out + nt + __popc(m & lt_mask);
+                ok[o] = ((u64)kth << 32) | idd;
+                op[o] = pp;
+            }
+            nt += __popc(m);
+        }
+    }
+    if (lane == 0) sl_cnt[q] = kprime;
+}
+
+// Re-rank top-k: (rdist, rid) rows of width `stride`, n = cnt[q] valid.
+__global__ __launch_bounds__(WS_WARPS * 32) void rerank_topk_warp_kernel(
+    const float* __restrict__ rdist, const uint32_t* __restrict__ rid,
+    const uint32_t* __restrict__ cnt_in, uint32_t stride, size_t nq, uint32_t k, uint32_t k2,
+    uint32_t* __restrict__ out_ids, float* __restrict__ out_dists, uint32_t* __restrict__ out_cnt) {
+    extern __shared__ u64 wkeys[];  // [WS_WARPS][k2]
+    __shared__ uint32_t hist_all[WS_WARPS][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t q = (size_t)blockIdx.x * WS_WARPS + warp;
+    if (q >= nq) return;
+    u64* keys = wkeys + (size_t)warp * k2;
+    const uint32_t n = cnt_in[q];
+    const uint32_t* db = reinterpret_cast<const uint32_t*>(rdist) + q * stride;
+    const uint32_t* ib = rid + q * stride;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t n_out = 0;
+    if (n <= k) {
+        for (uint32_t i = lane; i < n; i += 32) keys[i] = ((u64)db[i] << 32) | ib[i];
+        n_out = n;
+    } else {
+        uint32_t kth, r_eq;
+        warp_radix_select(n, k, [&](uint32_t i) { return db[i]; }, hist_all[warp], kth, r_eq);
+        uint32_t n_eq = 0;
+        for (uint32_t base = 0; base < n; base += 32) {
+            const uint32_t i = base + lane;
+            const uint32_t u = i < n ? db[i] : 0xffffffffu;
+            const bool lt = i < n && u < kth;
+            const unsigned m = __ballot_sync(0xffffffffu, lt);
+            if (lt) keys[n_out + __popc(m & lt_mask)] = ((u64)u << 32) | ib[i];
+            n_out += __popc(m);
+            n_eq += __popc(__ballot_sync(0xffffffffu, i < n && u == kth));
+        }
+        if (n_eq == r_eq) {
+            for (uint32_t base = 0; base < n; base += 32) {
+                const uint32_t i = base + lane;
+                const bool eq = i < n && db[i] == kth;
+                const unsigned m = __ballot_sync(0xffffffffu, eq);
+                if (eq) keys[n_out + __popc(m & lt_mask)] = ((u64)kth << 32) | ib[i];
+                n_out += __popc(m);
+            }
+        } else {
+            // the r_eq smallest ids among the ties (radix select on ids)
+            uint32_t idk, dummy;
+            warp_radix_select(n, r_eq, [&](uint32_t i) { return db[i] == kth ? ib[i] : 0xffffffffu; },
+                              hist_all[warp], idk, dummy);
+            uint32_t nt = 0;
+            for (uint32_t base = 0; base < n; base += 32) {
+                const uint32_t i = base + lane;
+                const bool take = i < n && db[i] == kth && ib[i] <= idk;
+                const unsigned m = __ballot_sync(0xffffffffu, take);
+                if (take) keys[n_out + nt + __popc(m & lt_mask)] = ((u64)kth << 32) | ib[i];
+                nt += __popc(m);
+            }
+            n_out += r_eq;
+        }
+    }
+    __syncwarp();
+    for (uint32_t i = n_out + lane; i < k2; i += 32) keys[i] = ~0ull;
+    __syncwarp();
+    warp_bitonic(keys, k2);
+    const uint32_t cnt = min(n, k);
+    for (uint32_t i = lane; i < k; i += 32) {
+        const bool live = i < cnt;
+        out_ids[q * k + i] = live ? key_id(keys[i]) : 0xffffffffu;
+        out_dists[q * k + i] = live ? key_dist(keys[i]) : __int_as_float(0x7f800000);
+    }
+    if (lane == 0) out_cnt[q] = cnt;
+}
+
+}  // namespace
+
+bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* out_idx,
+                      float* out_dist, cudaStream_t s) {
+    if (w > 64 || w == 0 || w > nc) return false;
+    topw_warp_kernel<<<(unsigned)((nq + WS_WARPS - 1) / WS_WARPS), WS_WARPS * 32, 0, s>>>(
+        D, nq, nc, w, out_idx, out_dist);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+    return true;
+}
+
+void launch_select_warp(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
+                        uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime,
+                        uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s) {
+    if (nq == 0) return;
+    select_warp_kernel<<<(unsigned)((nq + WS_WARPS - 1) / WS_WARPS), WS_WARPS * 32, 0, s>>>(
+        cand_dist, cand_pos, cand_cnt, cap, nq, ids, kprime, reinterpret_cast<u64*>(sl_key), sl_pos,
+        sl_cnt);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
+
+bool launch_rerank_topk_warp(const float* rdist, const uint32_t* rid, const uint32_t* cnt,
+                             uint32_t stride, size_t nq, uint32_t k, uint32_t* out_ids,
+                             float* out_dists, uint32_t* out_cnt, cudaStream_t s) {
+    uint32_t k2 = 1;
+    while (k2 < k) k2 <<= 1;
+    const size_t smem = (size_t)WS_WARPS * k2 * sizeof(u64);
+    if (k2 > 1024 || smem > 96 * 1024) return false;
+    if (smem > 48 * 1024)
+        PQRR_CUDA(cudaFuncSetAttribute(rerank_topk_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    rerank_topk_warp_kernel<<<(unsigned)((nq + WS_WARPS - 1) / WS_WARPS), WS_WARPS * 32, smem, s>>>(
+        rdist, rid, cnt, stride, nq, k, k2, out_ids, out_dists, out_cnt);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+    return true;
+}
+
+}  // namespace pqrr_b200

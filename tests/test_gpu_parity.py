@@ -313,3 +313,32 @@ def test_load_lists_round_trip(pq, golden_ivf):
     b = ix2.search(g["queries"], int(g["v"]), int(g["kprime"]), int(g["k"]))
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
+
+
+def test_massive_boundary_ties_match_oracle(pq, oracle):
+    """600 copies of one vector in the base and the same vector as a query: the
+    k'-th (and k-th) boundary falls inside > 256 exact distance ties, which the
+    selectors must resolve by id exactly like the reference's TopK."""
+    seed, K = 3, 64
+    centers = oracle.synth_centers(seed, K, 128)
+    base = oracle.synth_rows(seed, 2, 0, 30_000, centers)
+    train = oracle.synth_rows(seed, 1, 0, 8_000, centers).astype(np.float32)
+    dup = base[123].copy()
+    base[5000:5600] = dup  # ids 5000..5599 are identical vectors
+    queries = np.concatenate([dup[None], oracle.synth_rows(seed, 3, 0, 15, centers)])
+    coarse, books = oracle.ivf_train(train, 32, 8, iterations=3, seed=0)
+    rbooks = oracle.ivf_refine_train(coarse, books, 8, train, 16, iterations=3, seed=0)
+    oix = oracle.ivf_build(coarse, books, 8, base.astype(np.float32))
+    oix.refine_encode(rbooks, 16, base.astype(np.float32))
+    dix = pq.ivf_build(pq.Codebook(coarse), pqobj(pq, books, 8), base,
+                       rq=pq.RefineQuantizer(pqobj(pq, rbooks, 16)))
+    qf = queries.astype(np.float32)
+    for v, kprime, k in [(4, 300, 100), (32, 300, 250)]:
+        oi, od, oc = oix.search(qf, v, kprime)
+        ri, rd = oix.rerank(qf, oi, oc, k)
+        di, dd, dc = dix.search(queries, v, kprime, k)
+        np.testing.assert_array_equal(di, ri)
+        np.testing.assert_array_equal(bits(dd), bits(rd))
+        # the duplicated query's shortlist is all ties: ids 123, 5000, 5001, ... in order
+        expect = np.concatenate([[123], np.arange(5000, 5000 + k - 1)])
+        assert np.all(ri[0, :k] == expect)
