@@ -103,21 +103,6 @@ __device__ __forceinline__ void append_direct(int slot, uint32_t pos, const int*
     }
 }
 
-__device__ __forceinline__ void emit_bits(uint32_t bits, int base, uint32_t e, uint32_t off32,
-                                          bool stage_ok, uint32_t* stage, uint32_t* s_nst,
-                                          const int* s_q, const uint32_t* s_r, const FilterArgs& a) {
-    while (bits) {
-        const int b = __ffs(bits) - 1;  // bit 7 of byte b / 8
-        bits &= bits - 1;
-        const int slot = base + (b >> 3);
-        const uint32_t k = stage_ok ? atomicAdd(s_nst, 1u) : (uint32_t)STAGE;
-        if (k < (uint32_t)STAGE)
-            stage[k] = (e << 6) | (uint32_t)slot;
-        else
-            append_direct(slot, off32 + e, s_q, s_r, a);
-    }
-}
-
 __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
     extern __shared__ uint4 smem_f[];
     uint8_t* lut8 = reinterpret_cast<uint8_t*>(smem_f);  // [M][KS][FQ]
@@ -237,20 +222,28 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
                 a0 += va.x; a1 += va.y; a2 += va.z; a3 += va.w;
                 b0 += vb.x; b1 += vb.y; b2 += vb.z; b3 += vb.w;
             }
-            const uint32_t pa0 = vA ? le_bytes(a0, tb.x, th.x) : 0u, pa1 = vA ? le_bytes(a1, tb.y, th.y) : 0u;
-            const uint32_t pa2 = vA ? le_bytes(a2, tb.z, th.z) : 0u, pa3 = vA ? le_bytes(a3, tb.w, th.w) : 0u;
-            const uint32_t pb0 = vB ? le_bytes(b0, tb.x, th.x) : 0u, pb1 = vB ? le_bytes(b1, tb.y, th.y) : 0u;
-            const uint32_t pb2 = vB ? le_bytes(b2, tb.z, th.z) : 0u, pb3 = vB ? le_bytes(b3, tb.w, th.w) : 0u;
-            if (__any_sync(0xffffffffu, (pa0 | pa1 | pa2 | pa3 | pb0 | pb1 | pb2 | pb3) != 0u)) {
-                const int base = qd * 16;
-                emit_bits(pa0, base + 0, eA, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
-                emit_bits(pa1, base + 4, eA, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
-                emit_bits(pa2, base + 8, eA, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
-                emit_bits(pa3, base + 12, eA, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
-                emit_bits(pb0, base + 0, eB, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
-                emit_bits(pb1, base + 4, eB, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
-                emit_bits(pb2, base + 8, eB, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
-                emit_bits(pb3, base + 12, eB, off32, stage_ok, stage, &s_nst, s_q, s_r, a);
+            // pass bits sit at bit 7 of each byte; gather them into one lane mask
+            // (bit 16 s + 4 t + b: step s, word t, byte b -> query slot
+            // qd * 16 + 4 t + b).  (x >> 7) * 0x00204081 moves bits 0/8/16/24 to
+            // bits 21..24 without carries.
+            auto m4 = [](uint32_t x) { return (((x >> 7) * 0x00204081u) >> 21) & 0xfu; };
+            const uint32_t mA = vA ? (m4(le_bytes(a0, tb.x, th.x)) | (m4(le_bytes(a1, tb.y, th.y)) << 4) |
+                                      (m4(le_bytes(a2, tb.z, th.z)) << 8) | (m4(le_bytes(a3, tb.w, th.w)) << 12))
+                                   : 0u;
+            const uint32_t mB = vB ? (m4(le_bytes(b0, tb.x, th.x)) | (m4(le_bytes(b1, tb.y, th.y)) << 4) |
+                                      (m4(le_bytes(b2, tb.z, th.z)) << 8) | (m4(le_bytes(b3, tb.w, th.w)) << 12))
+                                   : 0u;
+            uint32_t mask = mA | (mB << 16);
+            while (mask) {
+                const int bpos = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int sl = qd * 16 + (bpos & 15);
+                const uint32_t e = bpos < 16 ? eA : eB;
+                const uint32_t k = stage_ok ? atomicAdd(&s_nst, 1u) : (uint32_t)STAGE;
+                if (k < (uint32_t)STAGE)
+                    stage[k] = (e << 6) | (uint32_t)sl;
+                else
+                    append_direct(sl, off32 + e, s_q, s_r, a);
             }
         }
         // ---- flush the staged candidates grouped by slot
