@@ -189,6 +189,7 @@ struct FilterArgs {
     uint32_t* cand_cnt;
     uint32_t cap;
     int pass_all;  // debug: every probed entry is a candidate
+    float band_div;  // Delta target = (tau - sum of minima) / band_div
 };
 void launch_ivf_filter(const FilterArgs& a, cudaStream_t s);
 // K4r: exact ADC distance of every filter candidate (reference order), and

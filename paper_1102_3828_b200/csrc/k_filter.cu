@@ -20,8 +20,9 @@
 //     sum_j v5_j <= T = floor((tau (1+e) - sum_m (1-e)) / Delta (1+e)),
 // e = 2^-18 covering every rounding.  The filter keeps sum_j v5_j <= T, a
 // superset of {d <= tau}; K4r recomputes d exactly for the survivors, so the
-// exact shortlist is unchanged.  Delta targets (tau - sum_m) / 80: T ~ 80, an
-// average of ~10 per subspace at the threshold, well below the clamp at 31.
+// exact shortlist is unchanged.  Delta targets (tau - sum_m) / band_div
+// (default 100, FilterArgs): T ~ 100, an average of ~12 per subspace at the
+// threshold, well below the clamp at 31.
 // Byte sums stay <= 8 * 31 = 248 (no carries); the per-byte unsigned test
 // x <= T is SWAR: r = (T | 0x80) - (x & 0x7f) never borrows, and bit 7 of
 // (x ^ T) ? T : r is set exactly when x <= T.  Dead slots (no entry of the
@@ -47,21 +48,20 @@ constexpr int FT = 512;
 constexpr int FW = FT / 32;
 constexpr int LUT8_BYTES = M * KS * FQ;      // 128 KiB
 constexpr int Q8_BLOCK = M * KS * SUBQ;      // 32 KiB per LUT-pass item
-constexpr float kBandDiv = 80.f;              // Delta ~ (tau - sum_m) / 80
 
 // Per query slot: multiplier / additive term of the v8 -> v5 conversion and
 // the threshold byte T (255 = everything passes).
 struct SlotParam {
     uint32_t mult, add, t;
 };
-__device__ __forceinline__ SlotParam slot_params(float tau, float sc, float summ) {
+__device__ __forceinline__ SlotParam slot_params(float tau, float sc, float summ, float band_div) {
     const float e_up = 1.000003814697265625f, e_dn = 0.999996185302734375f;  // 1 +- 2^-18
     if (!(tau < __int_as_float(0x7f800000))) return {0u, 0u, 255u};  // unsampled: all pass
     const float num = __fsub_rn(__fmul_rn(tau, e_up), __fmul_rn(summ, e_dn));
     if (!(num >= 0.f)) return {0u, 31u, 0u};  // even the closest reconstruction is beyond tau
     if (!(sc > 0.f)) return {0u, 0u, 255u};   // v8 == 0 everywhere and sum_m <= tau
     // mult = floor(256 sc / Delta_target) in [1, 256]
-    const float mf = floorf(__fdiv_rn(__fmul_rn(256.f, sc), __fdiv_rn(num, kBandDiv)));
+    const float mf = floorf(__fdiv_rn(__fmul_rn(256.f, sc), __fdiv_rn(num, band_div)));
     const uint32_t mult = mf >= 256.f ? 256u : (mf < 1.f ? 1u : (uint32_t)mf);
     // T = floor(num / Delta), Delta = 256 sc / mult
     const float tf = __fmul_rn(__fdiv_rn(__fmul_rn(num, (float)mult), __fmul_rn(256.f, sc)), e_up);
@@ -143,7 +143,7 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
                 q = (int)(p / a.w);
                 r = p % a.w;
                 const float* prm = a.q8_param + ((size_t)(sub0 + t / SUBQ) * SUBQ + t % SUBQ) * 2;
-                sp = slot_params(a.tau[q], prm[0], prm[1]);
+                sp = slot_params(a.tau[q], prm[0], prm[1], a.band_div);
                 if (a.pass_all) sp = {0u, 0u, 255u};
             }
             s_q[t] = q;

@@ -678,6 +678,11 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         f.cap = cap;
         static const bool pass_all = getenv("PQRR_FILTER_ALL") != nullptr;  // debug hook
         f.pass_all = pass_all ? 1 : 0;
+        const char* bd_env = getenv("PQRR_BANDDIV");  // tuning hook (read per search)
+        // 100: measured flat at C2 (80..120) and better than 80 at C4 (k' = 1e4);
+        // >= 160 saturates the 5-bit values and overflows candidate buffers
+        const float band_div = bd_env ? (float)atof(bd_env) : 100.f;
+        f.band_div = band_div;
         launch_ivf_filter(f, s);
         if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[9], s));
         cand_le = ws.alloc<uint32_t>(nq);
