@@ -31,7 +31,9 @@ __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t n
     for (uint32_t r = 0; r < w; ++r) tot += list_len[probes[q * w + r]];
     n_entries[q] = tot;
     atomicAdd(grand_total, (unsigned long long)tot);
-    const bool samp = tot > cap && stride > 1;
+    // every query whose candidates may not fit the buffer gets a threshold
+    // (stride 1 samples every entry: still exact, only slower)
+    const bool samp = tot > cap;
     sampled[q] = samp ? 1 : 0;
     unsigned long long ssum = 0;
     for (uint32_t r = 0; r < w; ++r) {
@@ -610,7 +612,12 @@ __global__ __launch_bounds__(RW_WARPS * 32) void rerank_warp_kernel(
 constexpr int RC_WARPS = 16;
 constexpr int RC_TLD = 132;  // tile row stride (floats): conflict-free transposed reads
 
-template <int DSR>
+// RB_SMEM: the refinement code book (m' rows of d/m' floats per candidate)
+// is the shared-memory table and the PQ code book is read through L1 — for
+// m' >= 16 the refinement rows are the smaller, more numerous segments (m' = 32:
+// 32 separate 16-B rows per candidate), so keeping them on-chip saves the most
+// L1 wavefronts.
+template <int DSR, bool RB_SMEM>
 __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
     const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
     const uint32_t* __restrict__ sl_cnt, uint32_t stride, size_t nq, const float* __restrict__ xq,
@@ -630,7 +637,7 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
     uint8_t* m_rcode = reinterpret_cast<uint8_t*>(m_list + 32 + 64);
     float* tile = tiles + warp * 8 * RC_TLD;
     for (uint32_t i = threadIdx.x; i < 8 * 256 * 4; i += blockDim.x)
-        bk[i] = __ldg(reinterpret_cast<const float4*>(books) + i);
+        bk[i] = __ldg(reinterpret_cast<const float4*>(RB_SMEM ? rbooks : books) + i);
     __syncthreads();
 
     const uint32_t g = lane;
@@ -670,9 +677,14 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
                 const uint32_t code = (uint32_t)(m_code[ci] >> (8 * jj)) & 0xffu;
                 const uint32_t rcode = m_rcode[ci * MP + jr];
                 const float4 cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + g);
-                const float4 bv = bk[(jj * 256 + code) * 4 + bo];
-                const float4 rv = __ldg(reinterpret_cast<const float4*>(
-                    rbooks + ((size_t)jr * 256 + rcode) * DSR + ro));
+                float4 bv, rv;
+                if constexpr (RB_SMEM) {
+                    bv = __ldg(reinterpret_cast<const float4*>(books + ((size_t)jj * 256 + code) * 16) + bo);
+                    rv = bk[((jr * 256 + rcode) * DSR + ro) / 4];
+                } else {
+                    bv = bk[(jj * 256 + code) * 4 + bo];
+                    rv = __ldg(reinterpret_cast<const float4*>(rbooks + ((size_t)jr * 256 + rcode) * DSR + ro));
+                }
                 const float d0 = __fsub_rn(x.x, __fadd_rn(__fadd_rn(cv.x, bv.x), rv.x));
                 const float d1 = __fsub_rn(x.y, __fadd_rn(__fadd_rn(cv.y, bv.y), rv.y));
                 const float d2 = __fsub_rn(x.z, __fadd_rn(__fadd_rn(cv.z, bv.z), rv.z));
@@ -931,9 +943,17 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
                 reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, nq, xq, block_list,
                 coarse, codes, books, rcodes, rbooks, rd, ri);
         };
-        if (dsr == 8) go(rerank_coop_kernel<8>);
-        else if (dsr == 4) go(rerank_coop_kernel<4>);
-        else go(rerank_coop_kernel<16>);
+        static const bool rb_smem = !(getenv("PQRR_RERANK_TABLE") &&
+                                      std::string(getenv("PQRR_RERANK_TABLE")) == "pq");
+        if (rb_smem) {
+            if (dsr == 8) go(rerank_coop_kernel<8, true>);
+            else if (dsr == 4) go(rerank_coop_kernel<4, true>);
+            else go(rerank_coop_kernel<16, true>);
+        } else {
+            if (dsr == 8) go(rerank_coop_kernel<8, false>);
+            else if (dsr == 4) go(rerank_coop_kernel<4, false>);
+            else go(rerank_coop_kernel<16, false>);
+        }
         PQRR_LAUNCH_CHECK();
         count_launch();
         if (!launch_rerank_topk_warp(rd, ri, sl_cnt, sl_stride, nq, k, out_ids, out_dists, out_cnt, s)) {

@@ -131,10 +131,11 @@ __global__ void check_fail_kernel(const uint8_t* __restrict__ sampled, const uin
     atomicAdd(total, (unsigned long long)cnt[q]);
     if (le) atomicAdd(total_le, (unsigned long long)le[q]);
     uint8_t f = 0;
-    if (sampled[q]) {
+    if (cnt[q] > cap) {
+        f = 2;  // buffer overflow: candidates were dropped
+    } else if (sampled[q]) {
         const uint32_t exact = le ? le[q] : cnt[q];
-        if (cnt[q] > cap) f = 2;            // buffer overflow: candidates were dropped
-        else if (exact < kprime) f = 1;     // threshold too tight: shortlist may be incomplete
+        if (exact < kprime) f = 1;  // threshold too tight: shortlist may be incomplete
     }
     fail[q] = f;
 }
@@ -541,7 +542,7 @@ void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_l
 // candidates ~ alpha * kprime).
 void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32_t kprime,
                     bool sorted, double alpha, uint32_t stride_div, ShortlistDev out, int depth,
-                    bool timed) {
+                    bool timed, uint32_t cap_shift = 0) {
     cudaStream_t s = ix.stream;
     auto& st = ix.stats;
     const uint32_t c = ix.c;
@@ -559,7 +560,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // >= 4k' for the exact scan, >= 8k' for the filter's superset; beyond
     // 8192 the selector streams candidates from global memory
     const uint32_t cap_mul = filter_ok ? 8 : 4;
-    const uint32_t cap = std::max<uint32_t>(8192, ((cap_mul * kprime + 1023) / 1024) * 1024);
+    const uint32_t cap = std::max<uint32_t>(8192, ((cap_mul * kprime + 1023) / 1024) * 1024) << cap_shift;
     // sample density: ~64 samples expected below the alpha*k'-th distance
     uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / 64.0));
     stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
@@ -789,8 +790,10 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         // under-full: widen the target; overflow: narrow it (never below the
         // k' it must cover) and sample twice as densely for a tighter estimate
         const double a2 = kind == 1 ? alpha * 2.0 : std::max(1.25, alpha / 1.5);
+        // an overflow also doubles the candidate buffer (the filter's superset
+        // of the entries <= tau, not tau itself, may be what does not fit)
         shortlist_core(ix, sx, rows.size(), w, kprime, sorted, a2, stride_div * 2, sub, depth + 1,
-                       false);
+                       false, cap_shift + (kind == 2 ? 1u : 0u));
         scatter_shortlist<<<nblk(rows.size() * kprime), 256, 0, s>>>(
             sub.key, sub.pos, sub.cnt, d_rows, rows.size(), kprime, out.key, out.pos, out.cnt);
         PQRR_LAUNCH_CHECK();

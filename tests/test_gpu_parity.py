@@ -230,19 +230,44 @@ def test_search_matches_oracle(mid_instance, v, kprime, k):
         dix.search(q, v, kprime, k, out=(out[0].astype(np.int64), out[1], out[2]))
 
 
-def test_exact_scan_fallback_matches_oracle():
-    """PQRR_SCAN=exact (read once per process) keeps the fp32 list-major scan:
-    run the mid-size comparison in a subprocess."""
+def _mid_search_subprocess(**env_over):
+    """Runs tools/dbg_filter.py (three mid-size searches against the oracle) in a
+    subprocess with the given environment (the switches are read once per
+    process) and returns its result lines."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PQRR_SCAN="exact")
+    env = dict(os.environ, **env_over)
     r = subprocess.run([sys.executable, os.path.join(root, "tools", "dbg_filter.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [x for x in r.stdout.splitlines() if "bad=" in x]
-    assert len(lines) == 3 and all("bad=0" in x and "env=exact" in x for x in lines), r.stdout
+    assert len(lines) == 3, r.stdout
+    return lines
+
+
+def test_exact_scan_fallback_matches_oracle():
+    """PQRR_SCAN=exact keeps the fp32 list-major scan."""
+    lines = _mid_search_subprocess(PQRR_SCAN="exact")
+    assert all("bad=0" in x and "env=exact" in x for x in lines), lines
+
+
+@pytest.mark.parametrize("scan", ["exact", "filter"])
+def test_forced_retries_stay_exact(scan):
+    """PQRR_FORCE_RETRY marks every query as failed once (odd: overflow, even:
+    under-full).  The retry policy (alpha, denser samples down to stride 1,
+    doubled buffer on overflow) must reproduce the oracle exactly; a band
+    divisor of 160 additionally forces genuine filter overflows."""
+    env = {"PQRR_FORCE_RETRY": "1"}
+    if scan == "exact":
+        env["PQRR_SCAN"] = "exact"
+    lines = _mid_search_subprocess(**env)
+    assert all("bad=0" in x for x in lines), lines
+    if scan == "filter":
+        lines = _mid_search_subprocess(PQRR_BANDDIV="160")
+        assert all("bad=0" in x for x in lines), lines
+        assert any("retries=0" not in x for x in lines), lines
 
 
 def test_large_coarse_radix_probe_selection(pq, oracle):
