@@ -101,27 +101,30 @@ __device__ __forceinline__ void build_luts_mm(float* __restrict__ lut, const flo
         }
         csync();
         const float* bj = bbuf + (j & 1) * BF;
-        float r[DSUB];
+        // operands as packed f32x2 pairs: one 16-byte load gives (t, t+1) and
+        // (t+2, t+3) ready for the packed arithmetic (LDS.128, not 2 x LDS.64)
+        u64 r01[DSUB / 4], r23[DSUB / 4];
 #pragma unroll
-        for (int t = 0; t < DSUB; t += 4) {
-            const float4 v = *reinterpret_cast<const float4*>(xr + qq * xld + j * DSUB + t);
-            r[t] = v.x; r[t + 1] = v.y; r[t + 2] = v.z; r[t + 3] = v.w;
+        for (int t4 = 0; t4 < DSUB / 4; ++t4) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(xr + qq * xld + j * DSUB + 4 * t4);
+            r01[t4] = v.x;
+            r23[t4] = v.y;
         }
         float mn = __int_as_float(0x7f800000), mx = 0.f;
 #pragma unroll
         for (int ib = 0; ib < KS / (2 * NCW); ++ib) {
             const int i = (ib * NCW + warp) * 2 + ih;
-            const float* b = bj + i * DSUB;
+            const ulonglong2* b = reinterpret_cast<const ulonglong2*>(bj + i * DSUB);
             u64 s01 = 0, s23 = 0;
 #pragma unroll
-            for (int t = 0; t < DSUB; t += 4) {
-                const float4 c = *reinterpret_cast<const float4*>(b + t);
-                if (t == 0) {  // 0 + x == x for the rounded square x >= +0
-                    s01 = sq2(sub2(pk2(r[t], r[t + 1]), pk2(c.x, c.y)), nz);
-                    s23 = sq2(sub2(pk2(r[t + 2], r[t + 3]), pk2(c.z, c.w)), nz);
+            for (int t4 = 0; t4 < DSUB / 4; ++t4) {
+                const ulonglong2 c = b[t4];
+                if (t4 == 0) {  // 0 + x == x for the rounded square x >= +0
+                    s01 = sq2(sub2(r01[t4], c.x), nz);
+                    s23 = sq2(sub2(r23[t4], c.y), nz);
                 } else {
-                    s01 = acc_sq2(s01, pk2(r[t], r[t + 1]), pk2(c.x, c.y), nz);
-                    s23 = acc_sq2(s23, pk2(r[t + 2], r[t + 3]), pk2(c.z, c.w), nz);
+                    s01 = acc_sq2(s01, r01[t4], c.x, nz);
+                    s23 = acc_sq2(s23, r23[t4], c.y, nz);
                 }
             }
             const float v = __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
