@@ -391,7 +391,6 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
         // (K4f writes each (query, list) run contiguously).
         constexpr int U = 4;
         constexpr uint32_t STEP = 16 * 4 * U;
-        const uint32_t hA = (uint32_t)slot & 1u;
         uint32_t npos[U], nr[U];
         auto fetch = [&](uint32_t b) {
 #pragma unroll
@@ -401,9 +400,12 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
                 nr[u] = aux[i];
             }
         };
-        const u64* res64 = reinterpret_cast<const u64*>(res);
-        const u64* bk64 = reinterpret_cast<const u64*>(bk);
-        u64 xa[CH], xb[CH];  // residual chunk halves (hA first)
+        // 16-byte loads: a quarter-warp is one candidate's 8 sub-spaces, so the
+        // swizzled residual chunks sit in 8 distinct bank groups and the
+        // code-book rows collide only by row parity
+        const ulonglong2* res128 = reinterpret_cast<const ulonglong2*>(res);
+        const ulonglong2* bk128 = reinterpret_cast<const ulonglong2*>(bk);
+        u64 xa[CH], xb[CH];  // residual chunk halves (t, t+1) / (t+2, t+3)
         uint32_t cur_r = 0xffffffffu;
         fetch(warp * 4 * U);
         for (uint32_t base = warp * 4 * U; base < n; base += STEP) {
@@ -424,26 +426,26 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
                     cur_r = rr[u];
 #pragma unroll
                     for (int p = 0; p < CH; ++p) {
-                        const uint32_t pc = sw(j * CH + p);
-                        xa[p] = res64[(cur_r * dch + pc) * 2 + hA];
-                        xb[p] = res64[(cur_r * dch + pc) * 2 + (hA ^ 1u)];
+                        const ulonglong2 v = res128[cur_r * dch + sw(j * CH + p)];
+                        xa[p] = v.x;
+                        xb[p] = v.y;
                     }
                 }
                 const uint32_t c = (uint32_t)(code[u] >> (8 * j)) & 0xffu;
-                const u64* brow = bk64 + (size_t)(j * KS + c) * CH * 2;
+                const ulonglong2* brow = bk128 + (size_t)(j * KS + c) * CH;
                 u64 sa = 0, sb = 0;
 #pragma unroll
                 for (int p = 0; p < CH; ++p) {
-                    const uint32_t pc = sw(j * CH + p) - j * CH;
+                    const ulonglong2 bv = brow[sw(j * CH + p) - j * CH];
                     if (p == 0) {  // 0 + x == x for the rounded square x >= +0
-                        sa = sq2(sub2(xa[p], brow[pc * 2 + hA]), nz);
-                        sb = sq2(sub2(xb[p], brow[pc * 2 + (hA ^ 1u)]), nz);
+                        sa = sq2(sub2(xa[p], bv.x), nz);
+                        sb = sq2(sub2(xb[p], bv.y), nz);
                     } else {
-                        sa = acc_sq2(sa, xa[p], brow[pc * 2 + hA], nz);
-                        sb = acc_sq2(sb, xb[p], brow[pc * 2 + (hA ^ 1u)], nz);
+                        sa = acc_sq2(sa, xa[p], bv.x, nz);
+                        sb = acc_sq2(sb, xb[p], bv.y, nz);
                     }
                 }
-                const u64 s01 = hA ? sb : sa, s23 = hA ? sa : sb;
+                const u64 s01 = sa, s23 = sb;
                 const float Lj = __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
                 float acc = 0.f;
 #pragma unroll
