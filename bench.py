@@ -44,7 +44,11 @@ CONFIGS = {
                w=64, kprime=1000, k=100),
     "C4": dict(n=1_000_000_000, train=1_000_000, nq=10_000, clusters=4096, kc=8192, m=8,
                mprime=32, w=64, kprime=10_000, k=100),
+    # batch-size sweep (BASELINE configs[4], quoted at 8 GPUs; here one GPU holds all 1B)
+    "C5": dict(n=1_000_000_000, train=1_000_000, nq=65_536, clusters=4096, kc=8192, m=8,
+               mprime=16, w=128, kprime=1000, k=100),
 }
+C5_BATCHES = [1, 16, 256, 4096, 65536]
 SEED = 0
 METRIC = "IVFADC+R queries/sec at oracle-matched recall@1/10/100; scan HBM GB/s"
 
@@ -241,6 +245,8 @@ def main():
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
+    if args.config == "C5":
+        return run_sweep(args, cfg, rank, world)
 
     import torch
     import paper_1102_3828_b200 as pq
@@ -417,6 +423,93 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def run_sweep(args, cfg, rank, world):
+    """C5: latency and queries/s per query-batch size on one index (device-
+    resident queries timed with CUDA events; e2e through the host API with
+    pinned input / result buffers, wall clock)."""
+    import torch
+    import paper_1102_3828_b200 as pq
+
+    if world > 1:
+        raise SystemExit("C5 sweep: single-GPU mode (one GPU holds the 1B index)")
+    torch.cuda.set_device(0)
+    coarse, P, rq = train_codebooks(pq, cfg, 0)
+    ix, _, _ = build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
+    k, kp, w = cfg["k"], cfg["kprime"], cfg["w"]
+    allq = pq.synth(3, 0, max(C5_BATCHES), cfg["clusters"], seed=SEED, device=0)
+    d_all = torch.from_numpy(allq).cuda()
+    h_all = torch.from_numpy(allq).pin_memory()
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    rows = []
+    launches0 = pq.launch_count()
+    with ClockSampler(0) as clk:
+        for B in C5_BATCHES:
+            reps = max(3, min(30, int(200_000 // B)))
+            d_ids = torch.empty((B, k), dtype=torch.int32, device="cuda")
+            d_dist = torch.empty((B, k), dtype=torch.float32, device="cuda")
+            d_cnt = torch.empty(B, dtype=torch.int32, device="cuda")
+
+            def once():
+                ix.search_device(d_all.data_ptr(), B, w, kp, k, d_ids.data_ptr(), d_dist.data_ptr(),
+                                 d_cnt.data_ptr(), stream.cuda_stream)
+
+            for _ in range(max(3, args.warmup)):
+                once()
+            torch.cuda.synchronize()
+            ms = []
+            for _ in range(reps):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                once()
+                e1.record(stream)
+                e1.synchronize()
+                ms.append(e0.elapsed_time(e1))
+            st = ix.last_stats()
+            hq = h_all[:B].numpy()
+            h_out = (torch.empty((B, k), dtype=torch.int32).pin_memory().numpy().view(np.uint32),
+                     torch.empty((B, k), dtype=torch.float32).pin_memory().numpy(),
+                     torch.empty((B,), dtype=torch.int32).pin_memory().numpy().view(np.uint32))
+            for _ in range(3):
+                ix.search(hq, w, kp, k, out=h_out)
+            es = []
+            for _ in range(reps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                ix.search(hq, w, kp, k, out=h_out)
+                es.append(time.perf_counter() - t0)
+            lat = float(np.median(ms))
+            e2e_lat = float(np.median(es)) * 1e3
+            rows.append({"batch": B, "latency_ms": lat, "qps": B / (lat / 1e3),
+                         "e2e_latency_ms": e2e_lat, "e2e_qps": B / (e2e_lat / 1e3), "reps": reps,
+                         "retries": st["retries"], "stages_ms": {kk: round(v, 4) for kk, v in st.items()
+                                                                  if kk.startswith("ms_")}})
+            log(f"[C5] batch {B}: {lat:.3f} ms device, {e2e_lat:.3f} ms e2e, {B / (lat / 1e3):.0f} q/s")
+    launches = pq.launch_count() - launches0
+    top = rows[-1]
+    peak, kind = measured_peak_gbs()
+    line = {
+        "metric": METRIC, "value": top["qps"], "unit": "queries/s", "n_gpus": 1,
+        "steps": top["reps"], "warmup": max(3, args.warmup), "ms_per_step": top["latency_ms"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (BASELINE.json SIFT-like generator, seed 0)",
+        "config": {"workload": "C5", **{kk: v for kk, v in cfg.items() if kk != "nq"},
+                   "batches": C5_BATCHES, "parallelism": "single GPU (quoted config: 8 GPUs)",
+                   "l2": "flushed between steps (512 MB write)"},
+        "e2e": {"value": top["e2e_qps"], "unit": "queries/s",
+                "h2d_bytes_per_step": int(top["batch"] * 128),
+                "d2h_bytes_per_step": int(top["batch"] * (k * 8 + 4))},
+        "gpu_launches": int(launches),
+        "sweep": rows,
+        "peak_hbm_gbs": peak, "peak_kind": kind,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
 
 
 def recall_and_parity(pq, cfg, queries, res_ids, ix, coarse, P, rq):

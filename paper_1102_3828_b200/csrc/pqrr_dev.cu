@@ -271,7 +271,7 @@ struct DevIndex {
     DBuf<uint32_t> st_assign, st_ids;
     DBuf<uint8_t> st_codes, st_rcodes;
     pqrr_dev_search_stats stats{};
-    cudaEvent_t ev[10] = {};
+    cudaEvent_t ev[11] = {};
 
     ~DevIndex() {
         for (auto& e : ev)
@@ -566,6 +566,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
     Workspace ws(s);
 
+    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[0], s));
     // ---- K1: coarse distances + top-w probes
     float* D = ws.alloc<float>(nq * (size_t)c);
     launch_pair_dists(xq, nq, ix.coarse.p, c, ix.d, D, s);
@@ -759,11 +760,19 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     if (timed) {
         st.candidates += total_cand;
         st.exact_candidates += use_filter ? total_le : total_cand;
-        if (use_filter) {
-            float fm = 0.f;
-            cudaEventElapsedTime(&fm, ix.ev[4], ix.ev[9]);
-            st.ms_filter = fm;
-        }
+        // stage times (accumulated over the chunks of a large batch)
+        auto el = [&](int a, int b) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ix.ev[a], ix.ev[b]);
+            return ms;
+        };
+        st.ms_coarse += el(0, 1);
+        st.ms_invert += el(1, 2);
+        st.ms_sample_scan += el(2, 3);
+        st.ms_threshold += el(3, 4);
+        st.ms_scan += el(4, 5);
+        st.ms_select += el(5, 6);
+        if (use_filter) st.ms_filter += el(4, 9);
         st.work_items += n_items;
         st.sampled_entries += total_samples;
         st.scanned_entries += h_grand[0];
@@ -818,11 +827,28 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
     if (nq == 0) return;
     for (auto& e : ix.ev)
         if (!e) PQRR_CUDA(cudaEventCreate(&e));
-    PQRR_CUDA(cudaEventRecord(ix.ev[0], s));
+    PQRR_CUDA(cudaEventRecord(ix.ev[10], s));
     Workspace ws(s);
     ShortlistDev sl{ws.alloc<u64>(nq * (size_t)kprime), ws.alloc<uint32_t>(nq * (size_t)kprime),
                     ws.alloc<uint32_t>(nq)};
-    shortlist_core(ix, xq, nq, w, kprime, k == 0, 2.0, 1, sl, 0, true);
+    // Large batches run in chunks sized to the free device memory: per query
+    // the sampled distances (~2 w avg_len / stride floats: uniform sampling of
+    // the k'-quantile needs many samples when k' << N_q), the 8-bit LUT blocks,
+    // the candidate buffers and the coarse distance row.
+    {
+        const double avg_len = ix.c ? (double)ix.n / ix.c : 0.0;
+        const double stride = std::max(1.0, std::floor(2.0 * kprime / 64.0));
+        const double per_q = 2.0 * w * avg_len / stride * 4.0 + (w / 16.0 + 1.0) * 32768.0 +
+                             std::max(8192.0, 8.0 * kprime) * 8.0 + ix.c * 4.0 + w * 64.0;
+        size_t free_b = 0, total_b = 0;
+        PQRR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const size_t chunk = std::min(nq, std::max<size_t>(256, (size_t)(0.5 * (double)free_b / per_q)));
+        for (size_t c0 = 0; c0 < nq; c0 += chunk) {
+            const size_t nc = std::min(chunk, nq - c0);
+            ShortlistDev part{sl.key + c0 * kprime, sl.pos + c0 * kprime, sl.cnt + c0};
+            shortlist_core(ix, xq + c0 * ix.d, nc, w, kprime, k == 0, 2.0, 1, part, 0, true);
+        }
+    }
     if (k > 0) {
         unsigned* flag = ws.zeros<unsigned>(1);
         min_count_kernel<<<nblk(nq), 256, 0, s>>>(sl.cnt, nq, k, flag);
@@ -849,14 +875,8 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
         return ms;
     };
     auto& st = ix.stats;
-    st.ms_coarse = el(0, 1);
-    st.ms_invert = el(1, 2);
-    st.ms_sample_scan = el(2, 3);
-    st.ms_threshold = el(3, 4);
-    st.ms_scan = el(4, 5);
-    st.ms_select = el(5, 6);
     st.ms_rerank = el(7, 8);
-    st.ms_total = el(0, 8);
+    st.ms_total = el(10, 8);
     st.kernels = (uint32_t)(launch_count() - l0);
 }
 
