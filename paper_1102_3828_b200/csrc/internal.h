@@ -117,6 +117,18 @@ void segmented_sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, const uin
                           const uint64_t* seg_end, int bits, cudaStream_t s);
 
 // -------------------------------------------------------------- search (k_scan.cu / k_select.cu)
+// Importance-weighted threshold sampling: probe rank r (0 = nearest list) of
+// w is sampled at stride << sample_tier(r, w): the nearest eighth of the
+// probes at the base stride, then 2x, 4x and 8x for the farther quarter /
+// half.  Each sample stands for its stride's worth of entries, so the
+// threshold is a weighted quantile (unbiased); the near probes, which hold
+// most entries below the threshold, keep the full density.  Tiers are
+// contiguous ranges of r, i.e. of a query's sample slots.
+__host__ __device__ inline uint32_t sample_tier(uint32_t r, uint32_t w, int tiered) {
+    if (!tiered) return 0;
+    const uint32_t r8 = 8 * r;
+    return r8 < w ? 0u : (r8 < 2 * w ? 1u : (r8 < 4 * w ? 2u : 3u));
+}
 static const int kQT = 16;        // queries per scan work item
 static const int kScanThreads = 512;
 
@@ -153,7 +165,8 @@ struct ScanArgs {
     uint32_t* cand_cnt;
     uint32_t cap;
     // sample mode (pass 1, sample_dist != null)
-    uint32_t stride;
+    uint32_t stride;             // base stride (probe-rank tier 0)
+    int tiered;                  // importance-weighted strides (sample_tier)
     const uint64_t* sample_off;  // per pair
     float* sample_dist;
     const uint8_t* query_sampled;  // per query: 1 if the query is in sample mode
@@ -211,13 +224,13 @@ void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, u
                            uint32_t* items, uint32_t qt, cudaStream_t s);
 // Per query: N_q = sum of probed list lengths; per pair sample counts.
 void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
-                        uint32_t stride, uint32_t cap, uint64_t* nq_entries,
+                        uint32_t stride, int tiered, uint32_t cap, uint64_t* nq_entries,
                         uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
                         cudaStream_t s);
 // tau_q = rank-th smallest sample of query q (sampled queries), +inf otherwise.
 void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_off, uint32_t w,
                              size_t nq, const uint8_t* query_sampled, float alpha_k,
-                             const uint64_t* n_entries, uint32_t max_samples, float* tau,
+                             uint32_t stride, int tiered, uint32_t max_samples, float* tau,
                              cudaStream_t s);
 // Exact top-kprime under (dist, id) from each query's candidates.
 void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
@@ -242,6 +255,9 @@ bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32
 void launch_select_warp(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
                         uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime,
                         uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s);
+void launch_threshold_warp(const float* sample_dist, const uint64_t* sample_off, uint32_t w, size_t nq,
+                           const uint8_t* query_sampled, float alpha_k, uint32_t stride, int tiered,
+                           float* tau, cudaStream_t s);
 bool launch_rerank_topk_warp(const float* rdist, const uint32_t* rid, const uint32_t* cnt,
                              uint32_t stride, size_t nq, uint32_t k, uint32_t* out_ids,
                              float* out_dists, uint32_t* out_cnt, cudaStream_t s);

@@ -37,10 +37,12 @@ constexpr int SCAP = 2048;             // sampled codes staged per item (more: r
 
 struct ItemMeta {
     uint32_t it, l, e0, e1, nqi;
+    uint32_t smin;  // smallest sampling stride among the item's sampled queries
     int q[QT];
     uint32_t pair[QT];
     unsigned long long sbase[QT];
     uint8_t samp[QT];
+    uint8_t sshift[QT];  // the query's stride = smin << sshift (sample_tier)
 };
 
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory"); }
@@ -197,12 +199,18 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 p = a.pair_sorted[start + lane];
                 q = (int)(p / a.w);
             }
+            // per-query sampling stride for this list (probe rank tier)
+            const uint8_t sm = (q >= 0 && a.query_sampled) ? a.query_sampled[q] : 0;
+            const uint32_t tier = (lane < QT && q >= 0) ? sample_tier(p % a.w, a.w, a.tiered) : 7u;
+            uint32_t tmin = (sm && lane < QT) ? tier : 7u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
             if (lane < QT) {
                 mt.q[lane] = q;
                 mt.pair[lane] = p;
-                const uint8_t sm = (q >= 0 && a.query_sampled) ? a.query_sampled[q] : 0;
                 mt.samp[lane] = sm;
                 mt.sbase[lane] = (sampling && sm) ? a.sample_off[p] : 0ull;
+                mt.sshift[lane] = (uint8_t)(sm ? tier - tmin : 0u);
             }
             if (lane == 0) {
                 mt.it = it;
@@ -210,6 +218,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 mt.e0 = e0;
                 mt.e1 = e1;
                 mt.nqi = nqi;
+                mt.smin = tmin < 7u ? (a.stride << tmin) : 0u;
             }
             __syncwarp();
             // rows: 16 query rows + the coarse row, 16 B per cp.async
@@ -219,13 +228,14 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 if (r == QT) cp16(raw + r * a.d + 4 * cc, a.coarse + (size_t)l * a.d + 4 * cc);
                 else if (mt.q[r] >= 0) cp16(raw + r * a.d + 4 * cc, a.xq + (size_t)mt.q[r] * a.d + 4 * cc);
             }
-            // sampled codes of the item's entry range
-            if (sampling) {
-                const uint32_t i0 = (e0 + a.stride - 1) / a.stride;
-                const uint32_t ns = (e1 + a.stride - 1) / a.stride - i0;
+            // sampled codes of the item's entries at the smallest stride among
+            // its sampled queries (items cover whole lists: e0 == 0)
+            if (sampling && tmin < 7u) {
+                const uint32_t smin = a.stride << tmin;
+                const uint32_t ns = (e1 + smin - 1) / smin;
                 const u64* lcodes = reinterpret_cast<const u64*>(a.codes) + a.list_off[l];
                 for (uint32_t si = lane; si < min(ns, (uint32_t)SCAP); si += 32)
-                    cp8(scodes + b * SCAP + si, lcodes + (size_t)(i0 + si) * a.stride);
+                    cp8(scodes + b * SCAP + si, lcodes + (size_t)si * smin);
             }
             cp_commit();
             cp_wait<0>();
@@ -315,24 +325,25 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
         }
-        if (sampling) {
-            // every stride-th entry of [e0, e1) at its fixed per-(query, probe) slot
-            const uint32_t e0 = mt.e0, e1 = mt.e1;
-            const uint32_t i0 = (e0 + a.stride - 1) / a.stride;
-            const uint32_t ns = (e1 + a.stride - 1) / a.stride - i0;
+        if (sampling && mt.smin) {
+            // entries i = si * smin of the list; query lane k samples those with
+            // si % 2^sshift_k == 0 into its slot si >> sshift_k (i / its stride)
+            const uint32_t smin = mt.smin;
+            const uint32_t ns = (mt.e1 + smin - 1) / smin;
             const u64* lcodes = reinterpret_cast<const u64*>(a.codes) + a.list_off[mt.l];
             const u64* sc = scodes + b * SCAP;
-            int qk[4];
             unsigned long long sbase[4];
             bool sw[4];
+            uint32_t sh[4];
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-                qk[kk] = mt.q[qd * 4 + kk];
-                sw[kk] = qk[kk] >= 0 && mt.samp[qd * 4 + kk];
-                sbase[kk] = mt.sbase[qd * 4 + kk];
+                const int qq = qd * 4 + kk;
+                sw[kk] = mt.q[qq] >= 0 && mt.samp[qq];
+                sbase[kk] = mt.sbase[qq];
+                sh[kk] = mt.sshift[qq];
             }
             for (uint32_t si = warp * 8 + slot; si < ns; si += NCW * 8) {
-                const u64 code = si < (uint32_t)SCAP ? sc[si] : __ldg(lcodes + (size_t)(i0 + si) * a.stride);
+                const u64 code = si < (uint32_t)SCAP ? sc[si] : __ldg(lcodes + (size_t)si * smin);
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int j = 0; j < M; ++j) {
@@ -345,7 +356,8 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 }
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                    if (sw[kk]) a.sample_dist[sbase[kk] + i0 + si] = acc[kk];
+                    if (sw[kk] && (si & ((1u << sh[kk]) - 1u)) == 0u)
+                        a.sample_dist[sbase[kk] + (si >> sh[kk])] = acc[kk];
             }
         }
         csync();  // all consumers are done with xr[b], meta[b], scodes[b] and the LUT

@@ -22,7 +22,7 @@ constexpr int NBINS = 1 << RADIX_BITS;
 
 __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t nq, uint32_t w,
                                    const uint32_t* __restrict__ list_len, uint32_t stride,
-                                   uint32_t cap, uint64_t* __restrict__ n_entries,
+                                   int tiered, uint32_t cap, uint64_t* __restrict__ n_entries,
                                    uint8_t* __restrict__ sampled, uint64_t* __restrict__ pair_samples,
                                    unsigned long long* __restrict__ grand_total) {
     size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -38,7 +38,8 @@ __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t n
     unsigned long long ssum = 0;
     for (uint32_t r = 0; r < w; ++r) {
         const uint32_t len = list_len[probes[q * w + r]];
-        const uint64_t ns = samp ? (len + stride - 1) / stride : 0;
+        const uint32_t st = stride << sample_tier(r, w, tiered);
+        const uint64_t ns = samp ? (len + st - 1) / st : 0;
         pair_samples[q * w + r] = ns;
         ssum += ns;
     }
@@ -103,86 +104,104 @@ __device__ __forceinline__ void for_each_u32(const uint32_t* __restrict__ src, u
     for (uint32_t i = head + 4 * nv + threadIdx.x; i < n; i += blockDim.x) f(__ldg(src + i));
 }
 
-// tau_q = rank-th smallest sampled distance (an estimate of the distance that
-// admits ~alpha*k' entries); +inf for queries scanned without sampling.
-// Pass 0 histograms the top 11 bits straight from global memory; a second
-// (L2-resident) read compacts the selected bin into shared memory when it
-// fits stage_cap, and the remaining 11- and 10-bit passes run over that small
-// set only.  A bin larger than stage_cap keeps reading global memory.
+// tau_q: the distance at which the weighted count of samples reaches alpha*k'
+// entries (each sample stands for its pair's stride, see sample_tier); +inf
+// for queries scanned without sampling or with too few entries.  A weighted
+// MSB-first radix select (11/11/10 bits): pass 1 histograms the top bits
+// straight from global memory, the selected bin is compacted into shared
+// memory when it fits stage_cap (with each element's tier), and the remaining
+// passes run over that small set only.
 __global__ __launch_bounds__(SEL_THREADS, 4) void sample_threshold_kernel(
     const float* __restrict__ sample, const uint64_t* __restrict__ sample_off, uint32_t w,
-    const uint8_t* __restrict__ sampled, float alpha_k, const uint64_t* __restrict__ n_entries,
+    const uint8_t* __restrict__ sampled, float alpha_k, uint32_t stride, int tiered,
     uint32_t stage_cap, float* __restrict__ tau) {
-    extern __shared__ uint32_t stage[];  // the selected top-bits bin
+    extern __shared__ uint32_t stage[];  // [stage_cap] values, then [stage_cap] tiers (bytes)
+    uint8_t* stage_t = reinterpret_cast<uint8_t*>(stage + stage_cap);
     __shared__ uint32_t hist[NBINS];
-    __shared__ uint32_t s_bin, s_rank, s_cnt, s_val, s_fill;
+    __shared__ uint32_t s_bin, s_rank, s_fill;
+    __shared__ unsigned long long s_seg[5];
     const size_t q = blockIdx.x;
     if (!sampled[q]) {
         if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
         return;
     }
-    const uint64_t lo = sample_off[q * w], hi = sample_off[q * w + w];
-    const uint32_t n = (uint32_t)(hi - lo);
-    // the n samples stand for the query's N_q entries: the sample rank
-    // matching ~alpha*k' candidates is alpha*k' * n / N_q
-    const double frac = (double)n / (double)max((unsigned long long)n_entries[q], 1ull);
-    const uint32_t rank = (uint32_t)max(1.0, ceil((double)alpha_k * frac));
-    if (n < rank || n == 0) {
+    // tier segments: contiguous ranges of the query's sample slots
+    if (threadIdx.x == 0) {
+        uint32_t r = 0;
+        for (uint32_t t = 0; t < 4; ++t) {
+            while (r < w && sample_tier(r, w, tiered) < t) ++r;
+            s_seg[t] = sample_off[q * w + r];
+        }
+        s_seg[4] = sample_off[q * w + w];
+    }
+    __syncthreads();
+    unsigned long long total = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) total += (s_seg[t + 1] - s_seg[t]) * ((unsigned long long)stride << t);
+    const uint32_t rank = (uint32_t)max(1.0, ceil((double)alpha_k));
+    if (total < rank) {
         if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
         return;
     }
-    const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(sample) + lo;
+    const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(sample);
     for (int b = threadIdx.x; b < NBINS; b += blockDim.x) hist[b] = 0;
     if (threadIdx.x == 0) s_fill = 0;
     __syncthreads();
-    for_each_u32(gsrc, n, [&](uint32_t u) { atomicAdd(&hist[u >> 21], 1u); });
+    for (int t = 0; t < 4; ++t) {
+        const uint32_t wt = stride << t;
+        const uint32_t n = (uint32_t)(s_seg[t + 1] - s_seg[t]);
+        if (n) for_each_u32(gsrc + s_seg[t], n, [&](uint32_t u) { atomicAdd(&hist[u >> 21], wt); });
+    }
     __syncthreads();
-    find_bin(hist, rank, &s_bin, &s_rank, &s_cnt);
+    find_bin(hist, rank, &s_bin, &s_rank);
     __syncthreads();
     uint32_t prefix = s_bin, r = s_rank;
-    const uint32_t cnt = s_cnt;
-    const uint32_t* src = gsrc;
-    uint32_t ns = n;
-    if (cnt <= stage_cap) {
+    // optimistic compaction of the selected bin (with each element's tier);
+    // an overfull stage falls back to reading global memory
+    {
         const uint32_t top = prefix;
-        for_each_u32(gsrc, n, [&](uint32_t u) {
-            if ((u >> 21) == top) stage[atomicAdd(&s_fill, 1u)] = u;
-        });
-        __syncthreads();
-        src = stage;
-        ns = cnt;
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t n = (uint32_t)(s_seg[t + 1] - s_seg[t]);
+            if (n)
+                for_each_u32(gsrc + s_seg[t], n, [&](uint32_t u) {
+                    if ((u >> 21) == top) {
+                        const uint32_t k = atomicAdd(&s_fill, 1u);
+                        if (k < stage_cap) {
+                            stage[k] = u;
+                            stage_t[k] = (uint8_t)t;
+                        }
+                    }
+                });
+        }
+    }
+    __syncthreads();
+    const uint32_t cnt = s_fill;
+    const bool staged = cnt <= stage_cap;
+    if (cnt == 1) {  // the bin holds a single value: it is the answer
+        if (threadIdx.x == 0) tau[q] = __uint_as_float(stage[0]);
+        return;
     }
     const int shifts[2] = {10, 0};
     const int widths[2] = {11, 10};
-    bool done = false;
-    if (cnt == 1) {  // the bin holds a single value: it is the answer
-        for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x)
-            if ((src[i] >> 21) == prefix) s_val = src[i];
-        __syncthreads();
-        prefix = s_val;
-        done = true;
-    }
-    for (int pass = 0; pass < 2 && !done; ++pass) {
+    for (int pass = 0; pass < 2; ++pass) {
         for (int b = threadIdx.x; b < NBINS; b += blockDim.x) hist[b] = 0;
         __syncthreads();
         const int sh = shifts[pass], wd = widths[pass];
         const uint32_t msk = (1u << wd) - 1u;
-        for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
-            const uint32_t u = src[i];
-            if ((u >> (sh + wd)) == prefix) atomicAdd(&hist[(u >> sh) & msk], 1u);
+        auto add = [&](uint32_t u, uint32_t t) {
+            if ((u >> (sh + wd)) == prefix) atomicAdd(&hist[(u >> sh) & msk], stride << t);
+        };
+        if (staged) {
+            for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) add(stage[i], stage_t[i]);
+        } else {
+            for (int t = 0; t < 4; ++t)
+                for (uint64_t i = s_seg[t] + threadIdx.x; i < s_seg[t + 1]; i += blockDim.x) add(gsrc[i], t);
         }
         __syncthreads();
-        find_bin(hist, r, &s_bin, &s_rank, &s_cnt);
+        find_bin(hist, r, &s_bin, &s_rank);
         __syncthreads();
         prefix = (prefix << wd) | s_bin;
         r = s_rank;
-        if (s_cnt == 1 && sh > 0) {  // unique value left under this prefix
-            for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x)
-                if ((src[i] >> sh) == prefix) s_val = src[i];
-            __syncthreads();
-            prefix = s_val;
-            break;
-        }
         __syncthreads();
     }
     if (threadIdx.x == 0) tau[q] = __uint_as_float(prefix);
@@ -837,12 +856,12 @@ void set_smem(const void* f, size_t bytes) {
 }  // namespace
 
 void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
-                        uint32_t stride, uint32_t cap, uint64_t* nq_entries,
+                        uint32_t stride, int tiered, uint32_t cap, uint64_t* nq_entries,
                         uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
                         cudaStream_t s) {
     if (nq == 0) return;
     query_sizes_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, s>>>(
-        probes, nq, w, list_len, stride, cap, nq_entries, query_sampled, pair_samples,
+        probes, nq, w, list_len, stride, tiered, cap, nq_entries, query_sampled, pair_samples,
         reinterpret_cast<unsigned long long*>(grand_total));
     PQRR_LAUNCH_CHECK();
     count_launch();
@@ -850,14 +869,19 @@ void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uin
 
 void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_off, uint32_t w,
                              size_t nq, const uint8_t* query_sampled, float alpha_k,
-                             const uint64_t* n_entries, uint32_t max_samples, float* tau,
+                             uint32_t stride, int tiered, uint32_t max_samples, float* tau,
                              cudaStream_t s) {
     if (nq == 0) return;
+    static const bool cta = getenv("PQRR_THRESHOLD") && std::string(getenv("PQRR_THRESHOLD")) == "cta";
+    if (!cta) {
+        launch_threshold_warp(sample_dist, sample_off, w, nq, query_sampled, alpha_k, stride, tiered, tau, s);
+        return;
+    }
     const uint32_t stage_cap = std::min<uint32_t>(max_samples, 8 * 1024);
-    const size_t smem = (size_t)std::max<uint32_t>(stage_cap, 1) * sizeof(uint32_t);
+    const size_t smem = (size_t)std::max<uint32_t>(stage_cap, 1) * (sizeof(uint32_t) + 1) + 16;
     set_smem((const void*)sample_threshold_kernel, smem);
     sample_threshold_kernel<<<(unsigned)nq, SEL_THREADS, smem, s>>>(
-        sample_dist, sample_off, w, query_sampled, alpha_k, n_entries, stage_cap, tau);
+        sample_dist, sample_off, w, query_sampled, alpha_k, stride, tiered, stage_cap, tau);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

@@ -362,6 +362,140 @@ __global__ __launch_bounds__(WS_WARPS * 32) void rerank_topk_warp_kernel(
     if (lane == 0) out_cnt[q] = cnt;
 }
 
+// Weighted variant for the threshold estimate: the smallest key at which the
+// weights of the keys <= it reach `rank`.  weight(i) > 0, sums fit 32 bits.
+template <class KeyF, class WtF>
+__device__ __forceinline__ uint32_t warp_weighted_select(uint32_t n, uint32_t rank, KeyF key, WtF wt,
+                                                         uint32_t* __restrict__ hist) {
+    const int lane = threadIdx.x & 31;
+    constexpr int U = 8;  // loads in flight per lane
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    for (uint32_t base = 0; base < n; base += 32 * U) {
+        uint32_t v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const uint32_t i = base + k * 32 + lane;
+            v[k] = i < n ? key(i) : kmin;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const uint32_t i = base + k * 32 + lane;
+            if (i < n) {
+                kmin = min(kmin, v[k]);
+                kmax = max(kmax, v[k]);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (kmin == kmax) return kmin;
+    int consumed = __clz(kmin ^ kmax);
+    uint32_t prefix = consumed ? kmin >> (32 - consumed) : 0u;
+    uint32_t r = rank;
+#pragma unroll 1
+    while (consumed < 32) {
+        const int wd = min(8, 32 - consumed);
+        const int sh = 32 - consumed - wd;
+        const uint32_t msk = (1u << wd) - 1u;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
+        __syncwarp();
+        for (uint32_t base = 0; base < n; base += 32 * U) {
+            uint32_t v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const uint32_t i = base + k * 32 + lane;
+                v[k] = i < n ? key(i) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const uint32_t i = base + k * 32 + lane;
+                if (i < n && (consumed == 0 || (v[k] >> (sh + wd)) == prefix))
+                    atomicAdd(&hist[(v[k] >> sh) & msk], wt(i));
+            }
+        }
+        __syncwarp();
+        uint32_t h[8], sum = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            h[b] = hist[lane * 8 + b];
+            sum += h[b];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const uint32_t excl = incl - sum;
+        const bool mine = excl < r && r <= incl;
+        const int owner = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        uint32_t bin = 0, before = excl;
+        if (mine) {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                if (r > before + h[b]) {
+                    before += h[b];
+                } else {
+                    bin = lane * 8 + b;
+                    break;
+                }
+            }
+        }
+        bin = __shfl_sync(0xffffffffu, bin, owner);
+        before = __shfl_sync(0xffffffffu, before, owner);
+        prefix = (prefix << wd) | bin;
+        r -= before;
+        consumed += wd;
+        __syncwarp();
+    }
+    return prefix;
+}
+
+// tau_q (one query per warp): the distance at which the weighted count of the
+// query's samples reaches alpha*k' entries; each sample weighs its pair's
+// stride (sample_tier: the tiers are contiguous ranges of the query's slots).
+// +inf for queries scanned without sampling or with too few entries.
+__global__ __launch_bounds__(WS_WARPS * 32) void threshold_warp_kernel(
+    const float* __restrict__ sample, const uint64_t* __restrict__ sample_off, uint32_t w,
+    size_t nq, const uint8_t* __restrict__ sampled, float alpha_k, uint32_t stride, int tiered,
+    float* __restrict__ tau) {
+    __shared__ uint32_t hist_all[WS_WARPS][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t q = (size_t)blockIdx.x * WS_WARPS + warp;
+    if (q >= nq) return;
+    const float inf = __int_as_float(0x7f800000);
+    if (!sampled[q]) {
+        if (lane == 0) tau[q] = inf;
+        return;
+    }
+    // first probe rank of each tier: ceil(w/8), ceil(w/4), ceil(w/2) (sample_tier)
+    uint32_t rb = w;
+    if (tiered && lane >= 1 && lane <= 3) rb = min(w, (w * (1u << (lane - 1)) + 7u) / 8u);
+    if (lane == 0) rb = 0;
+    const uint64_t seg = lane <= 4 ? sample_off[q * w + (lane == 4 ? w : rb)] : 0ull;
+    const uint64_t s0 = __shfl_sync(0xffffffffu, seg, 0), s1 = __shfl_sync(0xffffffffu, seg, 1);
+    const uint64_t s2 = __shfl_sync(0xffffffffu, seg, 2), s3 = __shfl_sync(0xffffffffu, seg, 3);
+    const uint64_t s4 = __shfl_sync(0xffffffffu, seg, 4);
+    const unsigned long long total = ((s1 - s0) + ((s2 - s1) << 1) + ((s3 - s2) << 2) + ((s4 - s3) << 3)) *
+                                     (unsigned long long)stride;
+    const uint32_t rank = (uint32_t)max(1.0, ceil((double)alpha_k));
+    if (total < rank) {
+        if (lane == 0) tau[q] = inf;
+        return;
+    }
+    const uint32_t n = (uint32_t)(s4 - s0);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(sample) + s0;
+    const uint32_t b1 = (uint32_t)(s1 - s0), b2 = (uint32_t)(s2 - s0), b3 = (uint32_t)(s3 - s0);
+    const uint32_t t = warp_weighted_select(
+        n, rank, [&](uint32_t i) { return __ldg(src + i); },
+        [&](uint32_t i) { return stride << ((i >= b1) + (i >= b2) + (i >= b3)); }, hist_all[warp]);
+    if (lane == 0) tau[q] = __uint_as_float(t);
+}
+
 }  // namespace
 
 bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* out_idx,
@@ -402,4 +536,16 @@ bool launch_rerank_topk_warp(const float* rdist, const uint32_t* rid, const uint
     return true;
 }
 
+}  // namespace pqrr_b200
+
+namespace pqrr_b200 {
+void launch_threshold_warp(const float* sample_dist, const uint64_t* sample_off, uint32_t w, size_t nq,
+                           const uint8_t* query_sampled, float alpha_k, uint32_t stride, int tiered,
+                           float* tau, cudaStream_t s) {
+    if (nq == 0) return;
+    threshold_warp_kernel<<<(unsigned)((nq + WS_WARPS - 1) / WS_WARPS), WS_WARPS * 32, 0, s>>>(
+        sample_dist, sample_off, w, nq, query_sampled, alpha_k, stride, tiered, tau);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
 }  // namespace pqrr_b200

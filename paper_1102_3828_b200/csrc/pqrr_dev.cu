@@ -584,8 +584,12 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     uint8_t* sampled = ws.alloc<uint8_t>(nq);
     uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
     uint64_t* grand = ws.zeros<uint64_t>(2);
-    launch_query_sizes(probes, nq, w, ix.list_len.p, stride, cap, n_entries, sampled, pair_samples,
-                       grand, s);
+    // importance-weighted sampling needs the warp-specialised LUT pass
+    static const bool old_lut_env = getenv("PQRR_LUTPASS") && std::string(getenv("PQRR_LUTPASS")) == "old";
+    static const bool uniform_env = getenv("PQRR_SAMPLING") && std::string(getenv("PQRR_SAMPLING")) == "uniform";
+    const int tiered = (!old_lut_env && !uniform_env && w >= 8 && lut_pass_supported(ix.d, ix.m, ix.ks)) ? 1 : 0;
+    launch_query_sizes(probes, nq, w, ix.list_len.p, stride, tiered, cap, n_entries, sampled,
+                       pair_samples, grand, s);
     uint64_t* sample_off = ws.alloc<uint64_t>(P + 1);
     exclusive_scan_u64(pair_samples, sample_off, P + 1, s);
     uint64_t total_samples = 0, h_grand[2] = {0, 0};
@@ -638,6 +642,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         a.q8_cache = use_filter ? ix.q8_cache.p : nullptr;
         a.q8_param = use_filter ? ix.q8_param.p : nullptr;
         a.stride = stride;
+        a.tiered = tiered;
         a.sample_off = sample_off;
         a.sample_dist = total_samples ? sample_dist : nullptr;
         a.tau = tau;  // unused in the LUT pass
@@ -647,8 +652,8 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         else launch_ivf_scan(a, s);
     }
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[3], s));
-    launch_sample_threshold(sample_dist, sample_off, w, nq, sampled, (float)(alpha * kprime),
-                            n_entries, (uint32_t)h_grand[1], tau, s);
+    launch_sample_threshold(sample_dist, sample_off, w, nq, sampled, (float)(alpha * kprime), stride,
+                            tiered, (uint32_t)h_grand[1], tau, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[4], s));
 
     // ---- K4 main scan: candidates (d <= tau, or the filter's superset)

@@ -16,4 +16,4 @@ q = pq.synth(3, 0, cfg["nq"], cfg["clusters"], seed=bench.SEED)
 for i in range(args.searches):
     ix.search(q, cfg["w"], cfg["kprime"], cfg["k"])
     st = ix.last_stats()
-    print(i, {k: round(v, 2) for k, v in st.items() if k.startswith("ms_")}, st["work_items"], flush=True)
+    print(i, {k: round(v, 2) for k, v in st.items() if k.startswith("ms_")}, st["work_items"], "retries", st["retries"], flush=True)
