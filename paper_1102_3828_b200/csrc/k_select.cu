@@ -873,7 +873,9 @@ void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_of
                              cudaStream_t s) {
     if (nq == 0) return;
     static const bool cta = getenv("PQRR_THRESHOLD") && std::string(getenv("PQRR_THRESHOLD")) == "cta";
-    if (!cta) {
+    // warp per query when the batch fills the GPU with warps; a small batch
+    // (C5 latency points) spreads each query's samples over a CTA instead
+    if (!cta && nq >= (size_t)2 * sm_count() * 8) {
         launch_threshold_warp(sample_dist, sample_off, w, nq, query_sampled, alpha_k, stride, tiered, tau, s);
         return;
     }

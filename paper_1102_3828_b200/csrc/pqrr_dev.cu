@@ -845,9 +845,19 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
         const double stride = std::max(1.0, std::floor(2.0 * kprime / 64.0));
         const double per_q = 2.0 * w * avg_len / stride * 4.0 + (w / 16.0 + 1.0) * 32768.0 +
                              std::max(8192.0, 8.0 * kprime) * 8.0 + ix.c * 4.0 + w * 64.0;
-        size_t free_b = 0, total_b = 0;
-        PQRR_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        const size_t chunk = std::min(nq, std::max<size_t>(256, (size_t)(0.5 * (double)free_b / per_q)));
+        // cudaMemGetInfo costs ~1 ms with a large resident index: query it
+        // only when the batch needs a sizeable share of the device
+        static size_t dev_total = 0;
+        if (!dev_total) {
+            size_t f = 0;
+            PQRR_CUDA(cudaMemGetInfo(&f, &dev_total));
+        }
+        size_t chunk = nq;
+        if (per_q * (double)nq > 0.25 * (double)dev_total) {
+            size_t free_b = 0, total_b = 0;
+            PQRR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            chunk = std::min(nq, std::max<size_t>(256, (size_t)(0.5 * (double)free_b / per_q)));
+        }
         for (size_t c0 = 0; c0 < nq; c0 += chunk) {
             const size_t nc = std::min(chunk, nq - c0);
             ShortlistDev part{sl.key + c0 * kprime, sl.pos + c0 * kprime, sl.cnt + c0};
