@@ -186,6 +186,8 @@ struct FilterArgs {
     const uint32_t* item_list;   // 64-query items
     const uint32_t* item_start;
     const uint32_t* item_nq;
+    const uint32_t* item_e0;     // entry range of the list covered by the item
+    const uint32_t* item_e1;
     const uint32_t* item_order;
     const uint32_t* num_items;
     uint32_t* item_counter;
@@ -219,9 +221,9 @@ void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,
                         const uint32_t* list_len, uint32_t nlists, const uint32_t* item_off,
                         uint32_t* item_list, uint32_t* item_start, uint32_t* item_nq,
                         uint32_t* item_e0, uint32_t* item_e1, uint32_t* sort_key, uint32_t qt,
-                        cudaStream_t s);
+                        cudaStream_t s, uint32_t chunk = 1u << 30);
 void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, uint32_t nlists,
-                           uint32_t* items, uint32_t qt, cudaStream_t s);
+                           uint32_t* items, uint32_t qt, cudaStream_t s, uint32_t chunk = 1u << 30);
 // Per query: N_q = sum of probed list lengths; per pair sample counts.
 void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
                         uint32_t stride, int tiered, uint32_t cap, uint64_t* nq_entries,

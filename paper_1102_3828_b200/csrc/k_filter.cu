@@ -183,8 +183,9 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
         }
         __syncthreads();
 
-        const uint64_t off = a.list_off[l];
-        const uint32_t len = a.list_len[l];
+        const uint32_t ie0 = a.item_e0[it];
+        const uint64_t off = a.list_off[l] + ie0;  // this item's entry range [e0, e1)
+        const uint32_t len = a.item_e1[it] - ie0;
         const uint32_t off32 = (uint32_t)off;
         const bool stage_ok = len < (1u << 26);
         const u64* codes = reinterpret_cast<const u64*>(a.codes) + off;

@@ -407,17 +407,18 @@ __global__ void build_lut_kernel(const float* __restrict__ xr, size_t nx, uint32
     out[idx] = l2sq_scalar(xr + v * d + (size_t)j * ds, books + ((size_t)j * ks + i) * ds, (int)ds);
 }
 
-// Work items: (list, group of <= 16 probing queries, chunk of <= kChunk
+// Work items: (list, group of <= qt probing queries, chunk of <= `chunk`
 // entries).  Chunking bounds the longest item so the longest-first schedule
-// below leaves no tail of one huge list on one SM.
-constexpr uint32_t kChunk = 1u << 30;  // chunking measured slower on C2 (extra LUT builds)
+// leaves no tail of one huge list on one SM; it is used for the K4f items of
+// small batches only (the LUT-pass items cover whole lists: chunks would
+// rebuild the same LUT).
 
 __global__ void items_per_list_kernel(const uint32_t* __restrict__ cnt,
                                       const uint32_t* __restrict__ len, uint32_t nlists,
-                                      uint32_t* __restrict__ items, uint32_t qt) {
+                                      uint32_t* __restrict__ items, uint32_t qt, uint32_t chunk) {
     uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l < nlists) {
-        const uint32_t chunks = max(1u, (len[l] + kChunk - 1) / kChunk);
+        const uint32_t chunks = max(1u, (len[l] + chunk - 1) / chunk);
         items[l] = ((cnt[l] + qt - 1) / qt) * chunks;
     }
     if (l == nlists) items[l] = 0;
@@ -430,15 +431,15 @@ __global__ void items_build_kernel(const uint32_t* __restrict__ cnt,
                                    uint32_t* __restrict__ item_list, uint32_t* __restrict__ item_start,
                                    uint32_t* __restrict__ item_nq, uint32_t* __restrict__ item_e0,
                                    uint32_t* __restrict__ item_e1, uint32_t* __restrict__ sort_key,
-                                   uint32_t qt) {
+                                   uint32_t qt, uint32_t chunk) {
     uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= nlists) return;
     const uint32_t c = cnt[l], L = len[l];
-    const uint32_t chunks = max(1u, (L + kChunk - 1) / kChunk);
+    const uint32_t chunks = max(1u, (L + chunk - 1) / chunk);
     uint32_t o = item_off[l];
     for (uint32_t s = 0; s < c; s += qt) {
         for (uint32_t ch = 0; ch < chunks; ++ch, ++o) {
-            const uint32_t e0 = ch * kChunk, e1 = min(L, e0 + kChunk);
+            const uint32_t e0 = ch * chunk, e1 = min(L, e0 + chunk);
             item_list[o] = l;
             item_start[o] = first[l] + s;
             item_nq[o] = min(qt, c - s);
@@ -475,9 +476,9 @@ void launch_ivf_scan(const ScanArgs& a, cudaStream_t s) {
 }
 
 void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, uint32_t nlists,
-                           uint32_t* items, uint32_t qt, cudaStream_t s) {
+                           uint32_t* items, uint32_t qt, cudaStream_t s, uint32_t chunk) {
     items_per_list_kernel<<<(nlists + 1 + 255) / 256, 256, 0, s>>>(list_cnt, list_len, nlists, items,
-                                                                   qt);
+                                                                   qt, chunk);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }
@@ -486,10 +487,10 @@ void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,
                         const uint32_t* list_len, uint32_t nlists, const uint32_t* item_off,
                         uint32_t* item_list, uint32_t* item_start, uint32_t* item_nq,
                         uint32_t* item_e0, uint32_t* item_e1, uint32_t* sort_key, uint32_t qt,
-                        cudaStream_t s) {
+                        cudaStream_t s, uint32_t chunk) {
     items_build_kernel<<<(nlists + 255) / 256, 256, 0, s>>>(list_cnt, list_first, list_len, nlists,
                                                             item_off, item_list, item_start, item_nq,
-                                                            item_e0, item_e1, sort_key, qt);
+                                                            item_e0, item_e1, sort_key, qt, chunk);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

@@ -476,7 +476,7 @@ struct ItemSet {
     uint32_t* list_cnt = nullptr;
     uint32_t* list_first = nullptr;
     uint32_t* item_off = nullptr;
-    uint32_t n_items = 0, c = 0, qt = 0;
+    uint32_t n_items = 0, c = 0, qt = 0, chunk = 1u << 30;
     uint32_t *item_list = nullptr, *item_start = nullptr, *item_nq = nullptr;
     uint32_t *item_e0 = nullptr, *item_e1 = nullptr, *item_order = nullptr;
     void apply(ScanArgs& a) const {
@@ -496,10 +496,11 @@ struct ItemSet {
 // reuses another set's sorted pairs (same pairs, different qt).
 ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_ids, size_t np,
                      uint32_t c, const uint32_t* list_len, uint32_t qt, cudaStream_t s,
-                     const ItemSet* share = nullptr) {
+                     const ItemSet* share = nullptr, uint32_t chunk = 1u << 30) {
     ItemSet it;
     it.c = c;
     it.qt = qt;
+    it.chunk = chunk;
     if (share) {
         it.pair_sorted = share->pair_sorted;
         it.list_cnt = share->list_cnt;
@@ -514,7 +515,7 @@ ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_
         exclusive_scan_u32(it.list_cnt, it.list_first, c + 1, s);
     }
     uint32_t* items = ws.alloc<uint32_t>(c + 1);
-    launch_items_per_list(it.list_cnt, list_len, c, items, qt, s);
+    launch_items_per_list(it.list_cnt, list_len, c, items, qt, s, chunk);
     it.item_off = ws.alloc<uint32_t>(c + 1);
     exclusive_scan_u32(items, it.item_off, c + 1, s);
     return it;
@@ -532,7 +533,7 @@ void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_l
     uint32_t* iota = ws.alloc<uint32_t>(n);
     it.item_order = ws.alloc<uint32_t>(n);
     launch_items_build(it.list_cnt, it.list_first, list_len, c, it.item_off, it.item_list,
-                       it.item_start, it.item_nq, it.item_e0, it.item_e1, key, it.qt, s);
+                       it.item_start, it.item_nq, it.item_e0, it.item_e1, key, it.qt, s, it.chunk);
     launch_iota(iota, n, s);
     sort_pairs(key, key2, iota, it.item_order, n, 32, s);
 }
@@ -579,7 +580,10 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     uint32_t* pair_ids = ws.alloc<uint32_t>(P);
     launch_iota(pair_ids, P, s);
     ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s);
-    ItemSet if64 = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kFQ, s, &im);
+    // small batches (few query-list pairs per SM): K4f items split long lists
+    // into chunks so one list does not serialise on one SM
+    const uint32_t fchunk = P < (size_t)64 * sm_count() ? 16384u : (1u << 30);
+    ItemSet if64 = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kFQ, s, &im, fchunk);
     uint64_t* n_entries = ws.alloc<uint64_t>(nq);
     uint8_t* sampled = ws.alloc<uint8_t>(nq);
     uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
@@ -669,6 +673,8 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         f.item_list = if64.item_list;
         f.item_start = if64.item_start;
         f.item_nq = if64.item_nq;
+        f.item_e0 = if64.item_e0;
+        f.item_e1 = if64.item_e1;
         f.item_order = if64.item_order;
         f.num_items = if64.item_off + c;
         f.item_counter = counter + 1;
