@@ -32,11 +32,21 @@ __device__ __forceinline__ void warp_radix_select(uint32_t n, uint32_t rank, Key
                                                   uint32_t* __restrict__ hist, uint32_t& kth,
                                                   uint32_t& r_eq) {
     const int lane = threadIdx.x & 31;
+    constexpr int U = 8;  // loads in flight per lane
     uint32_t kmin = 0xffffffffu, kmax = 0u;
-    for (uint32_t i = lane; i < n; i += 32) {
-        const uint32_t u = key(i);
-        kmin = min(kmin, u);
-        kmax = max(kmax, u);
+    for (uint32_t base = 0; base < n; base += 32 * U) {
+        uint32_t v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const uint32_t i = base + k * 32 + lane;
+            v[k] = i < n ? key(i) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+            if (base + k * 32 + lane < n) {
+                kmin = min(kmin, v[k]);
+                kmax = max(kmax, v[k]);
+            }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -59,9 +69,17 @@ __device__ __forceinline__ void warp_radix_select(uint32_t n, uint32_t rank, Key
 #pragma unroll
         for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
         __syncwarp();
-        for (uint32_t i = lane; i < n; i += 32) {
-            const uint32_t u = key(i);
-            if (consumed == 0 || (u >> (sh + wd)) == prefix) atomicAdd(&hist[(u >> sh) & msk], 1u);
+        for (uint32_t base = 0; base < n; base += 32 * U) {
+            uint32_t v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const uint32_t i = base + k * 32 + lane;
+                v[k] = i < n ? key(i) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k)
+                if (base + k * 32 + lane < n && (consumed == 0 || (v[k] >> (sh + wd)) == prefix))
+                    atomicAdd(&hist[(v[k] >> sh) & msk], 1u);
         }
         __syncwarp();
         uint32_t h[8], sum = 0;
@@ -101,9 +119,16 @@ __device__ __forceinline__ void warp_radix_select(uint32_t n, uint32_t rank, Key
         __syncwarp();
         if (bcnt == 1 && consumed < 32) {  // a single key left under this prefix
             uint32_t v = 0;
-            for (uint32_t i = lane; i < n; i += 32) {
-                const uint32_t u = key(i);
-                if ((u >> (32 - consumed)) == prefix) v = u;
+            for (uint32_t base = 0; base < n; base += 32 * U) {
+                uint32_t vv[U];
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    const uint32_t i = base + k * 32 + lane;
+                    vv[k] = i < n ? key(i) : 0u;
+                }
+#pragma unroll
+                for (int k = 0; k < U; ++k)
+                    if (base + k * 32 + lane < n && (vv[k] >> (32 - consumed)) == prefix) v = vv[k];
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
