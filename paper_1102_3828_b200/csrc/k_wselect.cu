@@ -160,34 +160,152 @@ __device__ __forceinline__ void warp_bitonic(u64* keys, uint32_t n2) {
     }
 }
 
+// Top-w of a coarse distance row in three passes over the row (the rows of a
+// large batch do not fit L2): min / max, one 8-bit histogram below their
+// common leading bits, then one pass that emits every entry of a lower bin (in
+// index order) and compacts the boundary bin's entries (value, index) into a
+// per-warp buffer, from which a small sort takes the remaining rank.  A
+// boundary bin larger than the buffer falls back to the full radix select.
+constexpr uint32_t TW_BIN_CAP = 256;
+
 __global__ __launch_bounds__(WS_WARPS * 32) void topw_warp_kernel(const float* __restrict__ D, size_t nq,
                                                                    uint32_t nc, uint32_t w,
                                                                    uint32_t* __restrict__ out_idx,
                                                                    float* __restrict__ out_dist) {
     __shared__ uint32_t hist_all[WS_WARPS][256];
     __shared__ u64 keys_all[WS_WARPS][64];
+    __shared__ u64 bin_all[WS_WARPS][TW_BIN_CAP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t q = (size_t)blockIdx.x * WS_WARPS + warp;
     if (q >= nq) return;
     const uint32_t* row = reinterpret_cast<const uint32_t*>(D + q * nc);
-    uint32_t kth, r_eq;
-    warp_radix_select(nc, w, [&](uint32_t i) { return __ldg(row + i); }, hist_all[warp], kth, r_eq);
-    // compaction in index order: all keys < kth, then the first r_eq equal ones
+    uint32_t* hist = hist_all[warp];
     u64* keys = keys_all[warp];
-    uint32_t n_out = 0, eq_taken = 0;
+    u64* binb = bin_all[warp];
     const unsigned lt_mask = (1u << lane) - 1u;
     constexpr int U = 8;
+    // ---- pass 1: min / max
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
     for (uint32_t base = 0; base < nc; base += 32 * U) {
-        uint32_t uu[U];
+        uint32_t v[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             const uint32_t i = base + k * 32 + lane;
-            uu[k] = i < nc ? __ldg(row + i) : 0xffffffffu;
+            v[k] = i < nc ? __ldg(row + i) : 0u;
         }
 #pragma unroll
-        for (int k = 0; k < U; ++k) {
-            const uint32_t i = base + k * 32 + lane;
-            const uint32_t u = uu[k];
+        for (int k = 0; k < U; ++k)
+            if (base + k * 32 + lane < nc) {
+                kmin = min(kmin, v[k]);
+                kmax = max(kmax, v[k]);
+            }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    bool fast = kmin != kmax;
+    uint32_t lo_key = 0, r_bin = 0;
+    int sh = 0;
+    if (fast) {
+        // ---- pass 2: 8-bit histogram of the bits below the common prefix
+        const int consumed = __clz(kmin ^ kmax);
+        const int wd = min(8, 32 - consumed);
+        sh = 32 - consumed - wd;
+        const uint32_t base_key = consumed ? (kmin >> (32 - consumed)) << (32 - consumed) : 0u;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
+        __syncwarp();
+        for (uint32_t base = 0; base < nc; base += 32 * U) {
+            uint32_t v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const uint32_t i = base + k * 32 + lane;
+                v[k] = i < nc ? __ldg(row + i) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k)
+                if (base + k * 32 + lane < nc) atomicAdd(&hist[(v[k] >> sh) & ((1u << wd) - 1u)], 1u);
+        }
+        __syncwarp();
+        uint32_t h[8], sum = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            h[b] = hist[lane * 8 + b];
+            sum += h[b];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t excl = incl - sum;
+        const bool mine = excl < w && w <= incl;
+        const int owner = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        uint32_t bin = 0, before = excl, bc = 0;
+        if (mine) {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                if (w > before + h[b]) {
+                    before += h[b];
+                } else {
+                    bin = lane * 8 + b;
+                    bc = h[b];
+                    break;
+                }
+            }
+        }
+        bin = __shfl_sync(0xffffffffu, bin, owner);
+        before = __shfl_sync(0xffffffffu, before, owner);
+        bc = __shfl_sync(0xffffffffu, bc, owner);
+        lo_key = base_key | (bin << sh);  // first key of the boundary bin
+        r_bin = w - before;               // entries to take from the boundary bin
+        fast = bc <= TW_BIN_CAP;
+    }
+    uint32_t n_out = 0;
+    if (fast) {
+        // ---- pass 3: keys below the boundary bin in index order; the bin's
+        // entries (value, index) to the per-warp buffer
+        const uint32_t hi_key = lo_key + ((1u << sh) - 1u);  // last key of the bin
+        uint32_t nb = 0;
+        for (uint32_t base = 0; base < nc; base += 32 * U) {
+            uint32_t v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const uint32_t i = base + k * 32 + lane;
+                v[k] = i < nc ? __ldg(row + i) : 0xffffffffu;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const uint32_t i = base + k * 32 + lane;
+                const bool valid = i < nc;
+                const bool lt = valid && v[k] < lo_key;
+                const bool inb = valid && v[k] >= lo_key && v[k] <= hi_key;
+                const unsigned mlt = __ballot_sync(0xffffffffu, lt), mb = __ballot_sync(0xffffffffu, inb);
+                if (lt) keys[n_out + __popc(mlt & lt_mask)] = ((u64)v[k] << 32) | i;
+                if (inb) binb[nb + __popc(mb & lt_mask)] = ((u64)v[k] << 32) | i;
+                n_out += __popc(mlt);
+                nb += __popc(mb);
+            }
+        }
+        __syncwarp();
+        uint32_t b2 = 1;
+        while (b2 < nb) b2 <<= 1;
+        for (uint32_t i = nb + lane; i < b2; i += 32) binb[i] = ~0ull;
+        __syncwarp();
+        warp_bitonic(binb, b2);
+        for (uint32_t t = lane; t < r_bin; t += 32) keys[n_out + t] = binb[t];
+        n_out += r_bin;
+    } else {
+        // fallback: full radix select, then compaction in index order
+        uint32_t kth, r_eq;
+        warp_radix_select(nc, w, [&](uint32_t i) { return __ldg(row + i); }, hist, kth, r_eq);
+        uint32_t eq_taken = 0;
+        for (uint32_t base = 0; base < nc; base += 32) {
+            const uint32_t i = base + lane;
+            const uint32_t u = i < nc ? __ldg(row + i) : 0xffffffffu;
             const bool lt = i < nc && u < kth;
             const bool eq = i < nc && u == kth;
             const unsigned meq = __ballot_sync(0xffffffffu, eq);
@@ -201,6 +319,7 @@ __global__ __launch_bounds__(WS_WARPS * 32) void topw_warp_kernel(const float* _
     }
     uint32_t w2 = 1;
     while (w2 < w) w2 <<= 1;
+    __syncwarp();
     for (uint32_t i = w + lane; i < w2; i += 32) keys[i] = ~0ull;
     __syncwarp();
     warp_bitonic(keys, w2);
