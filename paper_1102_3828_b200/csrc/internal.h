@@ -250,6 +250,12 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
 void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* counts, size_t nq,
                        uint32_t parts, uint32_t width, uint32_t k, uint32_t* out_ids,
                        float* out_dists, uint32_t* out_cnt, cudaStream_t s);
+// K1 on the tensor cores with certified exact top-w (k_coarse_tc.cu).
+bool coarse_tc_supported(uint32_t d, uint32_t w);
+void launch_coarse_norms(const float* c, uint32_t n, uint32_t d, float* out, cudaStream_t s);
+void launch_coarse_tc(const float* x, size_t nq, const float* c, uint32_t nc, const float* cnorm,
+                      float cnorm_max, uint32_t w, float* Dt, uint32_t* out_idx, uint32_t* overflow,
+                      cudaStream_t s);
 // Warp-per-query selections (k_wselect.cu); the bool variants return false
 // outside their envelope (caller falls back to the CTA kernels).
 bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* out_idx,

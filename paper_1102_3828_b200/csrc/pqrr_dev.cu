@@ -260,6 +260,8 @@ struct DevIndex {
     DBuf<uint8_t> codes, rcodes;
     DBuf<uint32_t> ids;
     DBuf<uint16_t> block_list;  // list of each 16-entry block of positions
+    DBuf<float> cnorm;          // |C_l|^2 (tensor-core K1), cnorm_max their maximum
+    float cnorm_max = 0.f;
     DBuf<uint8_t> q8_cache;     // per LUT-pass item 8-bit LUT (32 KiB) for the K4f filter
     DBuf<float> q8_param;       // per LUT-pass item and query lane: (scale, sum of minima)
     uint64_t next_id = 0;
@@ -543,7 +545,7 @@ void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_l
 // candidates ~ alpha * kprime).
 void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32_t kprime,
                     bool sorted, double alpha, uint32_t stride_div, ShortlistDev out, int depth,
-                    bool timed, uint32_t cap_shift = 0) {
+                    bool timed, uint32_t cap_shift = 0, bool exact_coarse = false) {
     cudaStream_t s = ix.stream;
     auto& st = ix.stats;
     const uint32_t c = ix.c;
@@ -568,11 +570,29 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     Workspace ws(s);
 
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[0], s));
-    // ---- K1: coarse distances + top-w probes
+    // ---- K1: coarse distances + top-w probes.  Kc >= 2048: tensor-core
+    // distances with a certified candidate set recomputed exactly
+    // (k_coarse_tc.cu); a query whose candidate set overflows restarts the
+    // batch on the exact CUDA-core path (checked at the first readback below)
     float* D = ws.alloc<float>(nq * (size_t)c);
-    launch_pair_dists(xq, nq, ix.coarse.p, c, ix.d, D, s);
     uint32_t* probes = ws.alloc<uint32_t>(P);
-    launch_topw(D, nq, c, w, probes, nullptr, s);
+    static const bool exact_coarse_env = getenv("PQRR_COARSE") && std::string(getenv("PQRR_COARSE")) == "exact";
+    const bool coarse_tc = !exact_coarse && !exact_coarse_env && c >= 2048 && coarse_tc_supported(ix.d, w);
+    uint32_t* coarse_ovf = ws.zeros<uint32_t>(1);
+    if (coarse_tc) {
+        if (!ix.cnorm.p) {
+            ix.cnorm.alloc(c);
+            launch_coarse_norms(ix.coarse.p, c, ix.d, ix.cnorm.p, s);
+            std::vector<float> h(c);
+            PQRR_CUDA(cudaMemcpyAsync(h.data(), ix.cnorm.p, c * sizeof(float), cudaMemcpyDeviceToHost, s));
+            PQRR_CUDA(cudaStreamSynchronize(s));
+            ix.cnorm_max = *std::max_element(h.begin(), h.end());
+        }
+        launch_coarse_tc(xq, nq, ix.coarse.p, c, ix.cnorm.p, ix.cnorm_max, w, D, probes, coarse_ovf, s);
+    } else {
+        launch_pair_dists(xq, nq, ix.coarse.p, c, ix.d, D, s);
+        launch_topw(D, nq, c, w, probes, nullptr, s);
+    }
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[1], s));
 
     // ---- invert probes into list-major work items: 16-query items for the
@@ -601,7 +621,13 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     PQRR_CUDA(cudaMemcpyAsync(&total_samples, sample_off + P, 8, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&if64.n_items, if64.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+    uint32_t h_ovf = 0;
+    if (coarse_tc) PQRR_CUDA(cudaMemcpyAsync(&h_ovf, coarse_ovf, 4, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaStreamSynchronize(s));
+    if (h_ovf) {  // rare: a certified candidate set did not fit; redo on the exact path
+        shortlist_core(ix, xq, nq, w, kprime, sorted, alpha, stride_div, out, depth, timed, cap_shift, true);
+        return;
+    }
     const uint32_t n_items = im.n_items;
 
     bool use_filter = filter_ok;
