@@ -549,6 +549,11 @@ def cpu_baseline(cfg, ix, coarse, P, rq, queries):
     if not ref_available():
         return {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
                 "sample": "unavailable: oracle/_ref not built"}
+    if cfg["n"] > 200_000_000:
+        # the reference's CPU search needs the whole index in its host layout
+        # (export = ~100 GB of device scratch + > 80 GB of host arrays at 1B)
+        return {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
+                "sample": f"skipped: n = {cfg['n']} exceeds the host-side export budget (C2 carries the baseline)"}
     ref = RefLib()
     cores = os.cpu_count() or 1
     ref.set_threads(cores)

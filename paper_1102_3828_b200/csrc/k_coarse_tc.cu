@@ -5,11 +5,14 @@
 //
 // 1. coarse_gemm_kernel: D~[q][c] = |x_q|^2 + |c|^2 - 2 <x_q, c> with the dot
 //    products on the tensor cores (mma.sync m16n8k8 TF32, fp32 accumulation).
-//    The query components are u8 values, exact in TF32; the centroids round to
-//    TF32 (relative 2^-11).  |<x,c>| <= (|x|^2 + |c|^2) / 2 bounds every error
-//    term: the rounding (2^-12), the fp32 accumulation (< 2^-16), the epilogue
-//    and the reference's own fp32 l2_sq (< 40 u), so
-//        |D~ - d_ref| <= delta = 2^-10 (|x|^2 + |c|^2).
+//    The centroids round to TF32 (cvt.rna, relative 2^-11).  Queries from u8
+//    are exact in TF32; float queries round too.  sum_i |x_i c_i| <=
+//    (|x|^2 + |c|^2) / 2 bounds every error term: the operand rounding (2^-11
+//    per rounded operand), the fp32 accumulation (< 2^-16), the epilogue and
+//    the reference's own fp32 l2_sq (< 40 u), so
+//        |D~ - d_ref| <= delta = 2^-10 (|x|^2 + |c|^2)   (u8 queries)
+//        |D~ - d_ref| <= delta = 2^-9  (|x|^2 + |c|^2)   (any float query);
+//    the certify kernel picks the scale per query by checking its components.
 // 2. topw_certify_kernel (one query per warp): T~ >= the w-th smallest D~;
 //    every true top-w centroid c has D~_c <= d_w + delta_c and
 //    d_w <= T~ + delta_max, so the candidate set {c : D~_c <= T~ + 2 delta_max}
@@ -268,11 +271,21 @@ __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
     // back to a float: T~ (>= the w-th smallest D~), candidate bound T~ + 2 delta_max
     const uint32_t tu = (tkey & 0x80000000u) ? (tkey & 0x7fffffffu) : ~tkey;
     float nx = 0.f;
+    bool tf32_exact = true;  // zero or normal with the low 13 mantissa bits clear
 #pragma unroll
-    for (int t = 0; t < 4; ++t) nx = fmaf(xs[4 * lane + t], xs[4 * lane + t], nx);
+    for (int t = 0; t < 4; ++t) {
+        const float v = xs[4 * lane + t];
+        const uint32_t b = __float_as_uint(v);
+        tf32_exact &= (b & 0x1fffu) == 0 && ((b & 0x7f800000u) != 0 || (b & 0x7fffffffu) == 0);
+        nx = fmaf(v, v, nx);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nx += __shfl_xor_sync(0xffffffffu, nx, o);
-    const float delta_max = 9.765625e-04f * (nx + cnorm_max) * 1.01f;  // 2^-10, + slack for this sum
+    // 2^-10 when the query is exact in TF32 (u8 queries); 2^-9 when its
+    // components round too (float queries through pqrr_dev_search_f32); + 1%
+    // slack for this sum and an absolute floor for underflowing products
+    const float dscale = __all_sync(0xffffffffu, tf32_exact) ? 9.765625e-04f : 1.953125e-03f;
+    const float delta_max = dscale * (nx + cnorm_max) * 1.01f + 0x1p-100f;
     const float bound = __uint_as_float(tu) + 2.f * delta_max;
     // ---- pass 3: candidates D~ <= bound (index order)
     uint32_t ncand = 0;

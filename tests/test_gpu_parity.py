@@ -291,6 +291,39 @@ def test_large_coarse_radix_probe_selection(pq, oracle):
             np.testing.assert_array_equal(bits(dd[i, :oc[i]]), bits(od[i, :oc[i]]))
 
 
+@pytest.mark.parametrize("kc", [2048, 4096])
+def test_tensor_core_coarse_certified_probes(pq, oracle, kc):
+    """Kc >= 2048 with d = 128 takes the TF32 coarse GEMM + certify path
+    (k_coarse_tc.cu).  Fractional centroids make the TF32 rounding real, a
+    ragged batch spans several 64-query GEMM tiles, and centroid pairs that
+    differ by one ulp in one coordinate put near-ties inside the error bound;
+    the probes (hence every shortlist) must still be the exact ones."""
+    rng = np.random.default_rng(kc)
+    base = rng.integers(0, 120, (30000, 128)).astype(np.uint8)
+    coarse = (base[rng.choice(30000, kc, replace=False)].astype(np.float32)
+              + rng.standard_normal((kc, 128)).astype(np.float32) * 3.3)
+    for a, b in [(11, 900), (12, 901), (13, 1500)]:
+        coarse[b] = coarse[a]
+        coarse[b, a % 128] = np.nextafter(coarse[a, a % 128], np.float32(np.inf))
+    books = (rng.standard_normal((8, 256, 16)) * 6).astype(np.float32)
+    dix = pq.ivf_build(pq.Codebook(coarse), pqobj(pq, books, 8), base)
+    oix = oracle.ivf_build(coarse, books.reshape(-1), 8, base.astype(np.float32))
+    q = np.vstack([base[rng.choice(30000, 170, replace=False)],
+                   np.clip(np.rint(coarse[[11, 12, 13]]), 0, 255).astype(np.uint8)])
+    # float queries with fractional components (not exact in TF32: the wider
+    # error bound applies), one of them half-way between two near-tied centroids
+    qf = (q.astype(np.float32) + rng.standard_normal(q.shape).astype(np.float32) * 0.37)
+    qf[-1] = (coarse[11] + coarse[900]) * np.float32(0.5)
+    for qq in (q, qf):
+        for v, kp in [(1, 50), (16, 300), (96, 1000)]:
+            oi, od, oc = oix.search(qq.astype(np.float32), v, kp)
+            di, dd, dc = dix.search(qq, v, kp, 0)
+            np.testing.assert_array_equal(dc, oc)
+            for i in range(len(q)):
+                np.testing.assert_array_equal(di[i, :oc[i]], oi[i, :oc[i]])
+                np.testing.assert_array_equal(bits(dd[i, :oc[i]]), bits(od[i, :oc[i]]))
+
+
 # ------------------------------------------------------------------ reference-side C++ drop-in
 def test_reference_api_shim():
     """integration/test_shim: a caller of the reference's own pqrr:: API
