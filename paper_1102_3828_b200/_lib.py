@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libpqrr_b200.so")
+# PQRR_LIB_PATH: an alternative build of the same library (A/B timing runs)
+LIB_PATH = os.environ.get("PQRR_LIB_PATH") or os.path.join(HERE, "lib", "libpqrr_b200.so")
 
 PQRR_OK = 0
 PQRR_EINVAL = -1

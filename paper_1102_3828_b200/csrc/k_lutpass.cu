@@ -30,10 +30,11 @@ constexpr int KS = 256;
 constexpr int QT = kQT;
 constexpr int NC = kScanThreads;  // consumer threads
 constexpr int NCW = NC / 32;      // consumer warps
-constexpr int NTH = NC + 32;      // + one producer warp
+constexpr int NTH = NC + 64;      // + the item producer warp + the book warp
 constexpr int LUT_FLOATS = M * KS * QT;
 constexpr int Q8_BYTES = M * KS * QT;  // 32 KiB
-constexpr int SCAP = 2048;             // sampled codes staged per item (more: read from global)
+constexpr int SCAP = 1024;             // sampled codes staged per item (more: read from global)
+constexpr int RING = 3;                // code-book slices in flight
 
 struct ItemMeta {
     uint32_t it, l, e0, e1, nqi;
@@ -74,75 +75,100 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int DSUB>
-__device__ __forceinline__ void stage_book(float* __restrict__ dst, const float* __restrict__ books, int j) {
-    constexpr int CH = KS * DSUB / 4;
-    const float* src = books + (size_t)j * KS * DSUB;
-    for (int c = threadIdx.x; c < CH; c += NC) cp16(dst + 4 * c, src + 4 * c);
-    cp_commit();
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+    unsigned done;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    return done != 0;
 }
 
-// Exact LUTs of the item (see build_luts in k_scan.cu; consumer threads only)
-// with the per-(j, q) minimum / maximum reduced into s_mnu / s_mxu.
+// Exact LUTs of the item (the reference order of l2_sq; consumer threads only)
+// with the per-(j, q) minimum / maximum reduced into s_mnu / s_mxu.  The
+// code-book slice of sub-space j arrives in a RING-slot ring filled by the
+// book warp (TMA bulk copies, full / empty mbarriers), so the consumers never
+// meet at a block barrier inside the build.  Register blocking: a thread
+// computes 2 queries x CI codes per sub-space, so every code-book row it
+// loads serves two entries (a broadcast LDS.128 still costs one wavefront per
+// quarter warp); the LUT is written with conflict-free 8-byte stores.
 template <int DSUB>
-__device__ __forceinline__ void build_luts_mm(float* __restrict__ lut, const float* __restrict__ xr,
-                                              int xld, const float* __restrict__ books,
-                                              float* __restrict__ bbuf, u64 nz, bool mm,
-                                              unsigned* __restrict__ s_mnu, unsigned* __restrict__ s_mxu) {
+__device__ __forceinline__ void build_luts_ring(float* __restrict__ lut, const float* __restrict__ xr,
+                                                int xld, const float* __restrict__ ring,
+                                                unsigned long long* bfull, unsigned long long* bempty,
+                                                uint32_t& gslice, u64 nz, bool mm,
+                                                unsigned* __restrict__ s_mnu, unsigned* __restrict__ s_mxu) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int qq = lane & 15, ih = lane >> 4;
+    const int qa = 2 * (lane & 7), ic = lane >> 3;
     constexpr int BF = KS * DSUB;
-    stage_book<DSUB>(bbuf, books, 0);
+    constexpr int NCODE = KS / NCW;  // codes per warp and sub-space
+    constexpr int CI = NCODE / 4;    // codes per thread and sub-space
+    constexpr int T4 = DSUB / 4;
 #pragma unroll 1
-    for (int j = 0; j < M; ++j) {
-        if (j + 1 < M) {
-            stage_book<DSUB>(bbuf + ((j + 1) & 1) * BF, books, j + 1);
-            cp_wait<1>();
-        } else {
-            cp_wait<0>();
+    for (int j = 0; j < M; ++j, ++gslice) {
+        const uint32_t slot = gslice % RING;
+        mbar_wait(&bfull[slot], (gslice / RING) & 1u);
+        const float* bj = ring + slot * BF;
+        u64 a01[T4], a23[T4], b01[T4], b23[T4];
+#pragma unroll
+        for (int t4 = 0; t4 < T4; ++t4) {
+            const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(xr + qa * xld + j * DSUB + 4 * t4);
+            const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(xr + (qa + 1) * xld + j * DSUB + 4 * t4);
+            a01[t4] = u.x;
+            a23[t4] = u.y;
+            b01[t4] = w.x;
+            b23[t4] = w.y;
         }
-        csync();
-        const float* bj = bbuf + (j & 1) * BF;
-        // operands as packed f32x2 pairs: one 16-byte load gives (t, t+1) and
-        // (t+2, t+3) ready for the packed arithmetic (LDS.128, not 2 x LDS.64)
-        u64 r01[DSUB / 4], r23[DSUB / 4];
+        float va[CI], vb[CI];
 #pragma unroll
-        for (int t4 = 0; t4 < DSUB / 4; ++t4) {
-            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(xr + qq * xld + j * DSUB + 4 * t4);
-            r01[t4] = v.x;
-            r23[t4] = v.y;
-        }
-        float mn = __int_as_float(0x7f800000), mx = 0.f;
+        for (int ci = 0; ci < CI; ++ci) {
+            const int i = warp * NCODE + ci * 4 + ic;
+            const ulonglong2* bp = reinterpret_cast<const ulonglong2*>(bj + i * DSUB);
+            u64 sa01 = 0, sa23 = 0, sb01 = 0, sb23 = 0;
 #pragma unroll
-        for (int ib = 0; ib < KS / (2 * NCW); ++ib) {
-            const int i = (ib * NCW + warp) * 2 + ih;
-            const ulonglong2* b = reinterpret_cast<const ulonglong2*>(bj + i * DSUB);
-            u64 s01 = 0, s23 = 0;
-#pragma unroll
-            for (int t4 = 0; t4 < DSUB / 4; ++t4) {
-                const ulonglong2 c = b[t4];
+            for (int t4 = 0; t4 < T4; ++t4) {
+                const ulonglong2 c = bp[t4];
                 if (t4 == 0) {  // 0 + x == x for the rounded square x >= +0
-                    s01 = sq2(sub2(r01[t4], c.x), nz);
-                    s23 = sq2(sub2(r23[t4], c.y), nz);
+                    sa01 = sq2(sub2(a01[0], c.x), nz);
+                    sa23 = sq2(sub2(a23[0], c.y), nz);
+                    sb01 = sq2(sub2(b01[0], c.x), nz);
+                    sb23 = sq2(sub2(b23[0], c.y), nz);
                 } else {
-                    s01 = acc_sq2(s01, r01[t4], c.x, nz);
-                    s23 = acc_sq2(s23, r23[t4], c.y, nz);
+                    sa01 = acc_sq2(sa01, a01[t4], c.x, nz);
+                    sa23 = acc_sq2(sa23, a23[t4], c.y, nz);
+                    sb01 = acc_sq2(sb01, b01[t4], c.x, nz);
+                    sb23 = acc_sq2(sb23, b23[t4], c.y, nz);
                 }
             }
-            const float v = __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
-            lut[(j * KS + i) * QT + qq] = v;
-            mn = fminf(mn, v);
-            mx = fmaxf(mx, v);
+            va[ci] = __fadd_rn(__fadd_rn(lo2(sa01), hi2(sa01)), __fadd_rn(lo2(sa23), hi2(sa23)));
+            vb[ci] = __fadd_rn(__fadd_rn(lo2(sb01), hi2(sb01)), __fadd_rn(lo2(sb23), hi2(sb23)));
+        }
+        __syncwarp();  // every lane's reads of the slice are complete
+        if (lane == 0) mbar_arrive(&bempty[slot]);
+        float mna = __int_as_float(0x7f800000), mxa = 0.f, mnb = mna, mxb = 0.f;
+#pragma unroll
+        for (int ci = 0; ci < CI; ++ci) {
+            const int i = warp * NCODE + ci * 4 + ic;
+            *reinterpret_cast<float2*>(lut + (j * KS + i) * QT + qa) = make_float2(va[ci], vb[ci]);
+            mna = fminf(mna, va[ci]);
+            mxa = fmaxf(mxa, va[ci]);
+            mnb = fminf(mnb, vb[ci]);
+            mxb = fmaxf(mxb, vb[ci]);
         }
         if (mm) {
-            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 16));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-            if (ih == 0) {
-                atomicMin(s_mnu + j * QT + qq, __float_as_uint(mn));
-                atomicMax(s_mxu + j * QT + qq, __float_as_uint(mx));
+#pragma unroll
+            for (int o = 8; o < 32; o <<= 1) {
+                mna = fminf(mna, __shfl_xor_sync(0xffffffffu, mna, o));
+                mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, o));
+                mnb = fminf(mnb, __shfl_xor_sync(0xffffffffu, mnb, o));
+                mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, o));
+            }
+            if (ic == 0) {
+                atomicMin(s_mnu + j * QT + qa, __float_as_uint(mna));
+                atomicMax(s_mxu + j * QT + qa, __float_as_uint(mxa));
+                atomicMin(s_mnu + j * QT + qa + 1, __float_as_uint(mnb));
+                atomicMax(s_mxu + j * QT + qa + 1, __float_as_uint(mxb));
             }
         }
-        csync();  // buffer (j & 1) is refilled by the prefetch of j + 2
     }
 }
 
@@ -154,9 +180,10 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
     float* xr0 = lut + LUT_FLOATS;                 // [2][QT][xld] residual queries
     float* raw = xr0 + 2 * QT * xld;               // [QT + 1][d] producer staging
     u64* scodes = reinterpret_cast<u64*>(raw + (QT + 1) * a.d);  // [2][SCAP] sampled codes
-    float* bbuf = reinterpret_cast<float*>(scodes + 2 * SCAP);  // code-book ring / q8 staging
+    float* ring = reinterpret_cast<float*>(scodes + 2 * SCAP);  // [RING][KS * DSUB] code-book slices
     __shared__ ItemMeta meta[2];
-    __shared__ __align__(8) unsigned long long full_bar[2], empty_bar[2];
+    __shared__ __align__(8) unsigned long long full_bar[2], empty_bar[2], bfull[RING], bempty[RING];
+    __shared__ volatile int s_stop;
     __shared__ __align__(16) float s_min[M * QT], s_rng[M * QT], s_inv[QT];
     __shared__ unsigned s_mnu[M * QT], s_mxu[M * QT];
 
@@ -169,9 +196,48 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
             mbar_init(&full_bar[b], 1);
             mbar_init(&empty_bar[b], 1);
         }
+        for (int r = 0; r < RING; ++r) {
+            mbar_init(&bfull[r], 1);
+            mbar_init(&bempty[r], NCW);
+        }
+        s_stop = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+
+    if (warp == NCW + 1) {
+        // ------------------------------------------------------- book warp
+        // streams the code-book slices j = 0..M-1, 0..M-1, ... (the same for
+        // every item) into the ring; a slot is refilled once all consumer
+        // warps released it.  Stops when the consumers saw the last item.
+        if (lane == 0) {
+            constexpr unsigned BYTES = KS * DSUB * sizeof(float);
+            uint32_t n = 0;
+            for (;; ++n) {
+                const uint32_t slot = n % RING;
+                bool stop = false;
+                if (n >= RING) {
+                    while (!mbar_try(&bempty[slot], ((n / RING) - 1) & 1u))
+                        if (s_stop) {
+                            stop = true;
+                            break;
+                        }
+                } else {
+                    stop = s_stop != 0;
+                }
+                if (stop) break;
+                const float* src = a.books + (size_t)(n % M) * KS * DSUB;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             ::"r"(smem_u32(&bfull[slot])), "r"(BYTES) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(smem_u32(ring + slot * KS * DSUB)), "l"(src), "r"(BYTES),
+                               "r"(smem_u32(&bfull[slot])) : "memory");
+            }
+            // the slices still in flight land before the CTA exits
+            for (uint32_t t = n > (uint32_t)RING ? n - RING : 0u; t < n; ++t) mbar_wait(&bfull[t % RING], (t / RING) & 1u);
+        }
+        return;
+    }
 
     if (warp == NCW) {
         // ---------------------------------------------------------- producer
@@ -264,21 +330,29 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
     // -------------------------------------------------------------- consumers
     const int slot = lane >> 2, qd = lane & 3;
     const float4* lut4 = reinterpret_cast<const float4*>(lut);
+    uint32_t gslice = 0;  // code-book slices consumed
     for (uint32_t k = 0;; ++k) {
         const int b = k & 1;
         mbar_wait(&full_bar[b], (k >> 1) & 1);
         const ItemMeta& mt = meta[b];
         const uint32_t it = mt.it;
-        if (it == 0xffffffffu) break;
-        if (threadIdx.x == 0 && store_q8)  // previous bulk store has read the staging buffer
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (it == 0xffffffffu) {
+            if (threadIdx.x == 0) s_stop = 1;
+            break;
+        }
         if (store_q8 && threadIdx.x < M * QT) {
             s_mnu[threadIdx.x] = 0x7f800000u;
             s_mxu[threadIdx.x] = 0u;
         }
         csync();
-        build_luts_mm<DSUB>(lut, xr0 + b * QT * xld, xld, a.books, bbuf, nz, store_q8, s_mnu, s_mxu);
+        build_luts_ring<DSUB>(lut, xr0 + b * QT * xld, xld, ring, bfull, bempty, gslice, nz, store_q8, s_mnu,
+                              s_mxu);
+        csync();  // LUT and the (j, q) minima / maxima complete
+#ifdef LP_NOQUANT  // timing experiment only
+        if (false) {
+#else
         if (store_q8) {
+#endif
             // 8-bit LUT (see quantize_item in k_scan.cu)
             const int t = threadIdx.x;
             if (t < M * QT) {
@@ -301,7 +375,9 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 prm[2 * t + 1] = sm;
             }
             csync();
-            uint32_t* stage = reinterpret_cast<uint32_t*>(bbuf);
+            // 8-bit block straight to global memory: a warp writes 128
+            // contiguous bytes per store
+            uint32_t* stage = reinterpret_cast<uint32_t*>(a.q8_cache + (size_t)it * Q8_BYTES);
             const int g = t & 3;
             const float4 inv = *reinterpret_cast<const float4*>(s_inv + 4 * g);
             const float shrink = 0.99999904632568359375f;  // 1 - 2^-20
@@ -316,16 +392,12 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 stage[row * 4 + g] = q8(v.x, mn.x, inv.x) | (q8(v.y, mn.y, inv.y) << 8) |
                                      (q8(v.z, mn.z, inv.z) << 16) | (q8(v.w, mn.w, inv.w) << 24);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            csync();
-            if (threadIdx.x == 0) {
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                             ::"l"(a.q8_cache + (size_t)it * Q8_BYTES), "r"(smem_u32(stage)),
-                             "r"((unsigned)Q8_BYTES) : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
         }
+#ifdef LP_NOSAMPLE  // timing experiment only
+        if (false) {
+#else
         if (sampling && mt.smin) {
+#endif
             // entries i = si * smin of the list; query lane k samples those with
             // si % 2^sshift_k == 0 into its slot si >> sshift_k (i / its stride)
             const uint32_t smin = mt.smin;
@@ -363,12 +435,11 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
         csync();  // all consumers are done with xr[b], meta[b], scodes[b] and the LUT
         if (threadIdx.x == 0) mbar_arrive(&empty_bar[b]);
     }
-    if (threadIdx.x == 0 && store_q8) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 template <int DSUB>
 void lut_pass_t(const ScanArgs& a, cudaStream_t s) {
-    const size_t ring = std::max<size_t>(2 * (size_t)KS * DSUB * sizeof(float), (size_t)Q8_BYTES);
+    const size_t ring = (size_t)RING * KS * DSUB * sizeof(float);
     const size_t smem = (size_t)LUT_FLOATS * sizeof(float) + 2 * (size_t)QT * (a.d + 4) * sizeof(float) +
                         (size_t)(QT + 1) * a.d * sizeof(float) + 2 * (size_t)SCAP * sizeof(u64) + ring;
     PQRR_CUDA(cudaFuncSetAttribute(lut_pass_kernel<DSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -384,7 +455,7 @@ bool lut_pass_supported(uint32_t d, uint32_t m, uint32_t ks) {
     if (m != M || ks != KS) return false;
     const uint32_t ds = d / m;
     if (ds != 4 && ds != 8 && ds != 16) return false;
-    const size_t ring = std::max<size_t>(2 * (size_t)KS * ds * sizeof(float), (size_t)Q8_BYTES);
+    const size_t ring = (size_t)RING * KS * ds * sizeof(float);
     const size_t smem = (size_t)LUT_FLOATS * 4 + 2 * (size_t)QT * (d + 4) * 4 + (size_t)(QT + 1) * d * 4 +
                         2 * (size_t)SCAP * 8 + ring;
     return smem <= 220 * 1024;
