@@ -75,6 +75,12 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Residual row q of an item: stride d + 4 floats (16 B mod 128 B) plus 16 B
+// for rows 8..15, so the rows a quarter warp reads in the build (0, 2, .., 14
+// or 1, 3, .., 15) fall on 8 distinct 16-byte bank groups.
+__device__ __forceinline__ int xrow(int q, int xld) { return q * xld + ((q >> 3) << 2); }
+constexpr int xbuf(int xld) { return QT * xld + 4; }  // floats per residual buffer
+
 __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
     unsigned done;
     asm volatile(
@@ -111,8 +117,8 @@ __device__ __forceinline__ void build_luts_ring(float* __restrict__ lut, const f
         u64 a01[T4], a23[T4], b01[T4], b23[T4];
 #pragma unroll
         for (int t4 = 0; t4 < T4; ++t4) {
-            const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(xr + qa * xld + j * DSUB + 4 * t4);
-            const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(xr + (qa + 1) * xld + j * DSUB + 4 * t4);
+            const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(xr + xrow(qa, xld) + j * DSUB + 4 * t4);
+            const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(xr + xrow(qa + 1, xld) + j * DSUB + 4 * t4);
             a01[t4] = u.x;
             a23[t4] = u.y;
             b01[t4] = w.x;
@@ -177,8 +183,8 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
     extern __shared__ float4 smem4[];
     const int xld = (int)a.d + 4;
     float* lut = reinterpret_cast<float*>(smem4);
-    float* xr0 = lut + LUT_FLOATS;                 // [2][QT][xld] residual queries
-    float* raw = xr0 + 2 * QT * xld;               // [QT + 1][d] producer staging
+    float* xr0 = lut + LUT_FLOATS;                 // [2][xbuf] residual queries (xrow)
+    float* raw = xr0 + 2 * xbuf(xld);              // [QT + 1][d] producer staging
     u64* scodes = reinterpret_cast<u64*>(raw + (QT + 1) * a.d);  // [2][SCAP] sampled codes
     float* ring = reinterpret_cast<float*>(scodes + 2 * SCAP);  // [RING][KS * DSUB] code-book slices
     __shared__ ItemMeta meta[2];
@@ -307,7 +313,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
             cp_wait<0>();
             __syncwarp();
             // residual queries x - C_l (ivf_index.hpp:58-59) into xr[b]
-            float* xr = xr0 + b * QT * xld;
+            float* xr = xr0 + b * xbuf(xld);
             const float* crow = raw + QT * a.d;
             for (uint32_t i = lane; i < QT * dch; i += 32) {
                 const uint32_t r = i / dch, cc = i % dch;
@@ -319,7 +325,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                     v = make_float4(__fsub_rn(x.x, y.x), __fsub_rn(x.y, y.y), __fsub_rn(x.z, y.z),
                                     __fsub_rn(x.w, y.w));
                 }
-                *reinterpret_cast<float4*>(xr + r * xld + 4 * cc) = v;
+                *reinterpret_cast<float4*>(xr + xrow(r, xld) + 4 * cc) = v;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&full_bar[b]);
@@ -345,7 +351,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
             s_mxu[threadIdx.x] = 0u;
         }
         csync();
-        build_luts_ring<DSUB>(lut, xr0 + b * QT * xld, xld, ring, bfull, bempty, gslice, nz, store_q8, s_mnu,
+        build_luts_ring<DSUB>(lut, xr0 + b * xbuf(xld), xld, ring, bfull, bempty, gslice, nz, store_q8, s_mnu,
                               s_mxu);
         csync();  // LUT and the (j, q) minima / maxima complete
 #ifdef LP_NOQUANT  // timing experiment only
@@ -440,7 +446,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
 template <int DSUB>
 void lut_pass_t(const ScanArgs& a, cudaStream_t s) {
     const size_t ring = (size_t)RING * KS * DSUB * sizeof(float);
-    const size_t smem = (size_t)LUT_FLOATS * sizeof(float) + 2 * (size_t)QT * (a.d + 4) * sizeof(float) +
+    const size_t smem = (size_t)LUT_FLOATS * sizeof(float) + 2 * (size_t)xbuf((int)a.d + 4) * sizeof(float) +
                         (size_t)(QT + 1) * a.d * sizeof(float) + 2 * (size_t)SCAP * sizeof(u64) + ring;
     PQRR_CUDA(cudaFuncSetAttribute(lut_pass_kernel<DSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
@@ -456,7 +462,7 @@ bool lut_pass_supported(uint32_t d, uint32_t m, uint32_t ks) {
     const uint32_t ds = d / m;
     if (ds != 4 && ds != 8 && ds != 16) return false;
     const size_t ring = (size_t)RING * KS * ds * sizeof(float);
-    const size_t smem = (size_t)LUT_FLOATS * 4 + 2 * (size_t)QT * (d + 4) * 4 + (size_t)(QT + 1) * d * 4 +
+    const size_t smem = (size_t)LUT_FLOATS * 4 + 2 * (size_t)xbuf((int)d + 4) * 4 + (size_t)(QT + 1) * d * 4 +
                         2 * (size_t)SCAP * 8 + ring;
     return smem <= 220 * 1024;
 }
