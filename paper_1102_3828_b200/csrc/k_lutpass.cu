@@ -391,12 +391,15 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
             for (int row = t >> 2; row < M * KS; row += NC / 4) {
                 const float4 v = lut4[row * 4 + g];
                 const float4 mn = *reinterpret_cast<const float4*>(s_min + (row >> 8) * QT + 4 * g);
+                // floor(x) for 0 <= x <= 255 without the quarter-rate F2I:
+                // x + 2^23 rounded down has ulp 1, so its low byte is floor(x)
                 auto q8 = [&](float L, float m, float iv) -> uint32_t {
                     const float x = fminf(__fmul_rn(__fmul_rn(__fsub_rn(L, m), iv), shrink), 255.f);
-                    return __float2uint_rz(x);
+                    return __float_as_uint(__fadd_rd(x, 8388608.f));
                 };
-                stage[row * 4 + g] = q8(v.x, mn.x, inv.x) | (q8(v.y, mn.y, inv.y) << 8) |
-                                     (q8(v.z, mn.z, inv.z) << 16) | (q8(v.w, mn.w, inv.w) << 24);
+                const uint32_t p01 = __byte_perm(q8(v.x, mn.x, inv.x), q8(v.y, mn.y, inv.y), 0x0040);
+                const uint32_t p23 = __byte_perm(q8(v.z, mn.z, inv.z), q8(v.w, mn.w, inv.w), 0x0040);
+                stage[row * 4 + g] = __byte_perm(p01, p23, 0x5410);
             }
         }
 #ifdef LP_NOSAMPLE  // timing experiment only

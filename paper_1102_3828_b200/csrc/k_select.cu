@@ -688,21 +688,44 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
         }
         const float4 x = reinterpret_cast<const float4*>(xq + q * D)[g];
         __syncwarp();
+        // shortlists arrive grouped by inverted list (the filter emits per
+        // (query, list) and the selections keep index order): the coarse row
+        // stays in registers until the list changes (warp-uniform branch)
+        uint32_t cur_l = 0xffffffffu;
+        float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+        // the L1 / L2 gathers (the code-book rows not held in shared memory)
+        // of a sub-batch of 8 candidates are issued one sub-batch ahead, so
+        // their latency overlaps the previous sub-batch's sequential sums
+        auto gload = [&](uint32_t ci) -> float4 {
+            if constexpr (RB_SMEM) {
+                const uint32_t code = (uint32_t)(m_code[ci] >> (8 * jj)) & 0xffu;
+                return __ldg(reinterpret_cast<const float4*>(books + ((size_t)jj * 256 + code) * 16) + bo);
+            } else {
+                const uint32_t rcode = m_rcode[ci * MP + jr];
+                return __ldg(reinterpret_cast<const float4*>(rbooks + ((size_t)jr * 256 + rcode) * DSR + ro));
+            }
+        };
+        float4 gv[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) gv[c] = gload(min((uint32_t)c, nb - 1));
         for (uint32_t sb = 0; sb < nb; sb += 8) {
-#pragma unroll 4
+#pragma unroll
             for (int c = 0; c < 8; ++c) {
                 const uint32_t ci = min(sb + c, nb - 1);
                 const uint32_t l = m_list[ci];
-                const uint32_t code = (uint32_t)(m_code[ci] >> (8 * jj)) & 0xffu;
-                const uint32_t rcode = m_rcode[ci * MP + jr];
-                const float4 cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + g);
+                if (l != cur_l) {
+                    cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + g);
+                    cur_l = l;
+                }
                 float4 bv, rv;
                 if constexpr (RB_SMEM) {
-                    bv = __ldg(reinterpret_cast<const float4*>(books + ((size_t)jj * 256 + code) * 16) + bo);
+                    const uint32_t rcode = m_rcode[ci * MP + jr];
+                    bv = gv[c];
                     rv = bk[((jr * 256 + rcode) * DSR + ro) / 4];
                 } else {
+                    const uint32_t code = (uint32_t)(m_code[ci] >> (8 * jj)) & 0xffu;
                     bv = bk[(jj * 256 + code) * 4 + bo];
-                    rv = __ldg(reinterpret_cast<const float4*>(rbooks + ((size_t)jr * 256 + rcode) * DSR + ro));
+                    rv = gv[c];
                 }
                 const float d0 = __fsub_rn(x.x, __fadd_rn(__fadd_rn(cv.x, bv.x), rv.x));
                 const float d1 = __fsub_rn(x.y, __fadd_rn(__fadd_rn(cv.y, bv.y), rv.y));
@@ -710,6 +733,10 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
                 const float d3 = __fsub_rn(x.w, __fadd_rn(__fadd_rn(cv.w, bv.w), rv.w));
                 *reinterpret_cast<float4*>(tile + c * RC_TLD + 4 * g) =
                     make_float4(__fmul_rn(d0, d0), __fmul_rn(d1, d1), __fmul_rn(d2, d2), __fmul_rn(d3, d3));
+            }
+            if (sb + 8 < nb) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) gv[c] = gload(min(sb + 8 + c, nb - 1));
             }
             __syncwarp();
             const int cc = lane >> 2, k = lane & 3;
