@@ -321,9 +321,9 @@ __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
         const float* cr = c + (size_t)ci * D;
         u64 s01 = 0, s23 = 0;
 #pragma unroll 2
-        for (int t = 0; t < D; t += 4) {
-            const float4 xv = *reinterpret_cast<const float4*>(xs + t);
-            const float4 cv = __ldg(reinterpret_cast<const float4*>(cr + t));
+        for (int e = 0; e < D; e += 4) {
+            const float4 xv = *reinterpret_cast<const float4*>(xs + e);
+            const float4 cv = __ldg(reinterpret_cast<const float4*>(cr + e));
             s01 = acc_sq2(s01, pk2(xv.x, xv.y), pk2(cv.x, cv.y), nz);
             s23 = acc_sq2(s23, pk2(xv.z, xv.w), pk2(cv.z, cv.w), nz);
         }
