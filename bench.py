@@ -240,6 +240,8 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recall", action="store_true")
+    ap.add_argument("--shard-mode", default="local", choices=["local", "exact"],
+                    help="N>1: per-shard shortlists (north star) or the single-index-exact flow")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     rank, world, local = dist_env()
@@ -273,7 +275,7 @@ def main():
     if world > 1:
         from paper_1102_3828_b200.sharded import DeviceShardedSearch
 
-        sharded = DeviceShardedSearch(ix, k, kp, w)
+        sharded = DeviceShardedSearch(ix, k, kp, w, mode=args.shard_mode)
 
     def run_once():
         if sharded is not None:  # shard search + NCCL all-gather + K7 merge
@@ -388,6 +390,7 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (BASELINE.json SIFT-like generator, seed 0)",
         "config": {"workload": args.config, **cfg, "parallelism": f"id-range shards x{world}",
+                   "shard_mode": args.shard_mode if world > 1 else "single index",
                    "l2": "flushed between steps (512 MB write)"},
         "e2e": {"value": e2e_val, "unit": "queries/s", "h2d_bytes_per_step": int(queries.nbytes),
                 "d2h_bytes_per_step": int(nq * k * 8 + nq * 4)},
@@ -432,20 +435,36 @@ def run_sweep(args, cfg, rank, world):
     import torch
     import paper_1102_3828_b200 as pq
 
-    if world > 1:
-        raise SystemExit("C5 sweep: single-GPU mode (one GPU holds the 1B index)")
-    torch.cuda.set_device(0)
-    coarse, P, rq = train_codebooks(pq, cfg, 0)
-    ix, _, _ = build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
+    _, _, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = sharded = None
+    if world > 1:  # the quoted C5 setup: 1B ids sharded over the GPUs, queries broadcast
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    coarse, P, rq = train_codebooks(pq, cfg, local)
+    ix, _, _ = build_index(pq, cfg, coarse, P, rq, local, rank, world)
     k, kp, w = cfg["k"], cfg["kprime"], cfg["w"]
-    allq = pq.synth(3, 0, max(C5_BATCHES), cfg["clusters"], seed=SEED, device=0)
+    if world > 1:
+        from paper_1102_3828_b200.sharded import DeviceShardedSearch
+
+        sharded = DeviceShardedSearch(ix, k, kp, w, mode=args.shard_mode)
+
+    def max_over_ranks(vals):
+        if dist is None:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    allq = pq.synth(3, 0, max(C5_BATCHES), cfg["clusters"], seed=SEED, device=local)
     d_all = torch.from_numpy(allq).cuda()
     h_all = torch.from_numpy(allq).pin_memory()
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     rows = []
     launches0 = pq.launch_count()
-    with ClockSampler(0) as clk:
+    with ClockSampler(local) as clk:
         for B in C5_BATCHES:
             reps = max(3, min(30, int(200_000 // B)))
             d_ids = torch.empty((B, k), dtype=torch.int32, device="cuda")
@@ -453,8 +472,24 @@ def run_sweep(args, cfg, rank, world):
             d_cnt = torch.empty(B, dtype=torch.int32, device="cuda")
 
             def once():
+                if sharded is not None:
+                    oi, _, _ = sharded.search(d_all[:B], stream)
+                    d_ids.copy_(oi)
+                    return
                 ix.search_device(d_all.data_ptr(), B, w, kp, k, d_ids.data_ptr(), d_dist.data_ptr(),
                                  d_cnt.data_ptr(), stream.cuda_stream)
+
+            def once_host(hq_t, h_out):
+                """host API: H2D of the batch, search, D2H of the results"""
+                if sharded is None:
+                    ix.search(hq_t.numpy(), w, kp, k, out=h_out)
+                    return
+                dq = hq_t.to("cuda", non_blocking=True)
+                oi, od, oc = sharded.search(dq, stream)
+                h_out[0].copy_(oi, non_blocking=True)
+                h_out[1].copy_(od, non_blocking=True)
+                h_out[2].copy_(oc, non_blocking=True)
+                torch.cuda.synchronize()
 
             for _ in range(max(3, args.warmup)):
                 once()
@@ -462,6 +497,8 @@ def run_sweep(args, cfg, rank, world):
             ms = []
             for _ in range(reps):
                 flush.zero_()
+                if dist is not None:
+                    dist.barrier()
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -469,37 +506,49 @@ def run_sweep(args, cfg, rank, world):
                 e1.record(stream)
                 e1.synchronize()
                 ms.append(e0.elapsed_time(e1))
+            ms = max_over_ranks(ms)
             st = ix.last_stats()
-            hq = h_all[:B].numpy()
-            h_out = (torch.empty((B, k), dtype=torch.int32).pin_memory().numpy().view(np.uint32),
-                     torch.empty((B, k), dtype=torch.float32).pin_memory().numpy(),
-                     torch.empty((B,), dtype=torch.int32).pin_memory().numpy().view(np.uint32))
+            hq = h_all[:B]
+            if sharded is None:
+                h_out = (torch.empty((B, k), dtype=torch.int32).pin_memory().numpy().view(np.uint32),
+                         torch.empty((B, k), dtype=torch.float32).pin_memory().numpy(),
+                         torch.empty((B,), dtype=torch.int32).pin_memory().numpy().view(np.uint32))
+            else:
+                h_out = (torch.empty((B, k), dtype=torch.int32).pin_memory(),
+                         torch.empty((B, k), dtype=torch.float32).pin_memory(),
+                         torch.empty((B,), dtype=torch.int32).pin_memory())
             for _ in range(3):
-                ix.search(hq, w, kp, k, out=h_out)
+                once_host(hq, h_out)
             es = []
             for _ in range(reps):
                 flush.zero_()
                 torch.cuda.synchronize()
+                if dist is not None:
+                    dist.barrier()
                 t0 = time.perf_counter()
-                ix.search(hq, w, kp, k, out=h_out)
+                once_host(hq, h_out)
                 es.append(time.perf_counter() - t0)
+            es = max_over_ranks(es)
             lat = float(np.median(ms))
             e2e_lat = float(np.median(es)) * 1e3
             rows.append({"batch": B, "latency_ms": lat, "qps": B / (lat / 1e3),
                          "e2e_latency_ms": e2e_lat, "e2e_qps": B / (e2e_lat / 1e3), "reps": reps,
                          "retries": st["retries"], "stages_ms": {kk: round(v, 4) for kk, v in st.items()
                                                                   if kk.startswith("ms_")}})
-            log(f"[C5] batch {B}: {lat:.3f} ms device, {e2e_lat:.3f} ms e2e, {B / (lat / 1e3):.0f} q/s")
+            if rank == 0:
+                log(f"[C5] batch {B}: {lat:.3f} ms device, {e2e_lat:.3f} ms e2e, {B / (lat / 1e3):.0f} q/s")
     launches = pq.launch_count() - launches0
     top = rows[-1]
     peak, kind = measured_peak_gbs()
     line = {
-        "metric": METRIC, "value": top["qps"], "unit": "queries/s", "n_gpus": 1,
+        "metric": METRIC, "value": top["qps"], "unit": "queries/s", "n_gpus": world,
         "steps": top["reps"], "warmup": max(3, args.warmup), "ms_per_step": top["latency_ms"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (BASELINE.json SIFT-like generator, seed 0)",
         "config": {"workload": "C5", **{kk: v for kk, v in cfg.items() if kk != "nq"},
-                   "batches": C5_BATCHES, "parallelism": "single GPU (quoted config: 8 GPUs)",
+                   "batches": C5_BATCHES,
+                   "parallelism": (f"id-range shards x{world} ({args.shard_mode} mode)" if world > 1
+                                   else "single GPU holds the 1B index (quoted config: 8 GPUs)"),
                    "l2": "flushed between steps (512 MB write)"},
         "e2e": {"value": top["e2e_qps"], "unit": "queries/s",
                 "h2d_bytes_per_step": int(top["batch"] * 128),
@@ -509,7 +558,10 @@ def run_sweep(args, cfg, rank, world):
         "peak_hbm_gbs": peak, "peak_kind": kind,
         "clocks": clk.summary(),
     }
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
 
 
 def recall_and_parity(pq, cfg, queries, res_ids, ix, coarse, P, rq):

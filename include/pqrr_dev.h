@@ -158,7 +158,7 @@ int pqrr_dev_search_f32(pqrr_dev_index* ix, const float* queries, size_t nq, uin
                         size_t kprime, size_t k, uint32_t* out_ids, float* out_dists,
                         uint32_t* out_counts);
 /* Device-resident variant: all pointers are device pointers on the index's
- * device; `stream` is a cudaStream_t (NULL = the index's own stream). The
+ * device; `stream` is a cudaStream_t (NULL = the legacy default stream). The
  * call is stream-ordered but may synchronise internally.                    */
 int pqrr_dev_search_u8_device(pqrr_dev_index* ix, const uint8_t* d_queries, size_t nq,
                               uint32_t w, size_t kprime, size_t k, uint32_t* d_out_ids,
@@ -172,6 +172,17 @@ int pqrr_dev_rerank_u8(pqrr_dev_index* ix, const uint8_t* queries, size_t nq,
 int pqrr_dev_rerank_f32(pqrr_dev_index* ix, const float* queries, size_t nq,
                         const uint32_t* sl_ids, const uint32_t* sl_counts, size_t sl_stride,
                         size_t k, uint32_t* out_ids, float* out_dists);
+/* Exact multi-shard mode: re-rank the entries of a GLOBAL
+ * shortlist (the merged top-k' of every shard, rows of sl_stride, d_sl_counts[q]
+ * valid) that THIS shard holds; ids held elsewhere are skipped.  Per query the
+ * top-min(k, owned) under (dist, id) land in row q of width k and
+ * d_out_counts[q].  Merging every shard's rows with pqrr_dev_merge_topk gives
+ * the single-index ivf_rerank result (ivf_index.hpp:79-81).  Device pointers,
+ * stream-ordered on `stream` (NULL = the legacy default stream).            */
+int pqrr_dev_rerank_owned_u8_device(pqrr_dev_index* ix, const uint8_t* d_queries, size_t nq,
+                                    const uint32_t* d_sl_ids, const uint32_t* d_sl_counts,
+                                    size_t sl_stride, size_t k, uint32_t* d_out_ids,
+                                    float* d_out_dists, uint32_t* d_out_counts, void* stream);
 /* ivf_reconstruct (ivf_index.hpp:75-77): coarse + decode + refine decode. */
 int pqrr_dev_reconstruct(pqrr_dev_index* ix, const uint32_t* ids, size_t n, float* out);
 

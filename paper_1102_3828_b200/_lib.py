@@ -101,6 +101,7 @@ _sig("pqrr_dev_search_u8_device", [_vp, _vp, _sz, _u32, _sz, _sz, _vp, _vp, _vp,
 _sig("pqrr_dev_rerank_u8", [_vp, _u8p, _sz, _u32p, _u32p, _sz, _sz, _u32p, _f32p])
 _sig("pqrr_dev_rerank_f32", [_vp, _f32p, _sz, _u32p, _u32p, _sz, _sz, _u32p, _f32p])
 _sig("pqrr_dev_reconstruct", [_vp, _u32p, _sz, _f32p])
+_sig("pqrr_dev_rerank_owned_u8_device", [_vp, _vp, _sz, _vp, _vp, _sz, _sz, _vp, _vp, _vp, _vp])
 _sig("pqrr_dev_last_search_stats", [_vp, C.POINTER(SearchStats)])
 _sig("pqrr_dev_load_lists", [_vp, _u64p, _u32p, _u8p, _vp])
 _sig("pqrr_dev_merge_topk", [_int, _u32p, _f32p, _u32p, _sz, _u32, _u32, _u32, _u32p, _f32p, _u32p])
@@ -117,7 +118,7 @@ EXPORTED = [
     "pqrr_dev_export_lists", "pqrr_dev_search_u8", "pqrr_dev_search_f32",
     "pqrr_dev_search_u8_device", "pqrr_dev_rerank_u8", "pqrr_dev_rerank_f32",
     "pqrr_dev_reconstruct", "pqrr_dev_last_search_stats", "pqrr_dev_load_lists",
-    "pqrr_dev_merge_topk", "pqrr_dev_merge_topk_device",
+    "pqrr_dev_merge_topk", "pqrr_dev_merge_topk_device", "pqrr_dev_rerank_owned_u8_device",
 ]
 
 

@@ -860,6 +860,29 @@ __global__ __launch_bounds__(256) void merge_topk_kernel(
     if (threadIdx.x == 0) out_cnt[q] = cnt;
 }
 
+// Large K7 inputs (parts * width above the smem bitonic): pack each query's
+// valid entries of all parts contiguously for select_large_kernel.
+__global__ void merge_pack_kernel(const uint32_t* __restrict__ ids, const float* __restrict__ dists,
+                                  const uint32_t* __restrict__ counts, size_t nq, uint32_t parts,
+                                  uint32_t width, float* __restrict__ cd, uint32_t* __restrict__ cp,
+                                  uint32_t* __restrict__ cid, uint32_t* __restrict__ ccnt) {
+    const size_t q = blockIdx.x;
+    const size_t cap = (size_t)parts * width;
+    uint32_t off = 0;
+    for (uint32_t p = 0; p < parts; ++p) {
+        const size_t row = (size_t)p * nq + q;
+        const uint32_t c = min(counts[row], width);
+        for (uint32_t j = threadIdx.x; j < c; j += blockDim.x) {
+            const size_t o = q * cap + off + j;
+            cd[o] = dists[row * width + j];
+            cid[o] = ids[row * width + j];
+            cp[o] = (uint32_t)o;
+        }
+        off += c;
+    }
+    if (threadIdx.x == 0) ccnt[q] = off;
+}
+
 __global__ void unpack_keys_kernel(const u64* __restrict__ keys, const uint32_t* __restrict__ cnt,
                                    size_t nq, uint32_t stride, uint32_t* __restrict__ ids,
                                    float* __restrict__ dists) {
@@ -1076,7 +1099,41 @@ void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* 
     uint32_t n2 = 1;
     while (n2 < parts * width) n2 <<= 1;
     const size_t smem = (size_t)n2 * sizeof(u64);
-    if (smem > 200 * 1024) throw ArgError("parts * width too large for the device merge");
+    if (smem > 200 * 1024) {
+        // exact multi-shard mode merges k'-wide shortlists (C4: 8 x 1e4): pack,
+        // radix-select from global memory (select_large_kernel), sort the k rows
+        const size_t cap = (size_t)parts * width;
+        if (nq * cap > 0xffffffffull) throw ArgError("nq * parts * width too large for the device merge");
+        uint32_t k2 = 1;
+        while (k2 < k) k2 <<= 1;
+        const size_t ssm = (size_t)k2 * (sizeof(u64) + sizeof(uint32_t));
+        if (ssm > 200 * 1024) throw ArgError("k too large for the device merge");
+        float* cd = nullptr;
+        uint32_t *cp = nullptr, *cid = nullptr, *ccnt = nullptr, *spos = nullptr;
+        u64* skey = nullptr;
+        PQRR_CUDA(cudaMallocAsync(&cd, nq * cap * 4, s));
+        PQRR_CUDA(cudaMallocAsync(&cp, nq * cap * 4, s));
+        PQRR_CUDA(cudaMallocAsync(&cid, nq * cap * 4, s));
+        PQRR_CUDA(cudaMallocAsync(&ccnt, nq * 4, s));
+        PQRR_CUDA(cudaMallocAsync(&skey, nq * k * 8, s));
+        PQRR_CUDA(cudaMallocAsync(&spos, nq * k * 4, s));
+        merge_pack_kernel<<<(unsigned)nq, 256, 0, s>>>(ids, dists, counts, nq, parts, width, cd, cp,
+                                                       cid, ccnt);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        select_large_kernel<<<(unsigned)nq, SEL_THREADS, 0, s>>>(cd, cp, ccnt, (uint32_t)cap, cid, k,
+                                                                 skey, spos, out_cnt);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        set_smem((const void*)sort_rows_kernel, ssm);
+        sort_rows_kernel<<<(unsigned)nq, 256, ssm, s>>>(skey, spos, out_cnt, k);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        launch_unpack_keys(reinterpret_cast<const uint64_t*>(skey), out_cnt, nq, k, out_ids, out_dists, s);
+        for (void* p : {(void*)cd, (void*)cp, (void*)cid, (void*)ccnt, (void*)skey, (void*)spos})
+            PQRR_CUDA(cudaFreeAsync(p, s));
+        return;
+    }
     set_smem((const void*)merge_topk_kernel, smem);
     merge_topk_kernel<<<(unsigned)nq, 256, smem, s>>>(ids, dists, counts, nq, parts, width, k, n2,
                                                       out_ids, out_dists, out_cnt);

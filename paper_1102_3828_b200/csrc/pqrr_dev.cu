@@ -167,20 +167,21 @@ __global__ void min_count_kernel(const uint32_t* __restrict__ cnt, size_t nq, ui
 }
 
 __global__ void id_to_pos_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
-                                 const uint32_t* __restrict__ ids, uint32_t* __restrict__ map) {
+                                 const uint32_t* __restrict__ ids, uint32_t id_lo,
+                                 uint32_t* __restrict__ map) {
     const uint32_t l = blockIdx.x;
     const uint64_t o = off[l];
-    for (uint32_t r = threadIdx.x; r < len[l]; r += blockDim.x) map[ids[o + r]] = (uint32_t)(o + r);
+    for (uint32_t r = threadIdx.x; r < len[l]; r += blockDim.x) map[ids[o + r] - id_lo] = (uint32_t)(o + r);
 }
 
 __global__ void ids_to_shortlist(const uint32_t* __restrict__ sl_ids, const uint32_t* __restrict__ map,
                                  size_t total, u64* __restrict__ key, uint32_t* __restrict__ pos,
-                                 unsigned* __restrict__ bad, uint32_t nmap) {
+                                 unsigned* __restrict__ bad, uint32_t id_lo, uint32_t nmap) {
     size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
     const uint32_t id = sl_ids[i];
     uint32_t p = 0xffffffffu;
-    if (id < nmap) p = map[id];
+    if (id >= id_lo && id - id_lo < nmap) p = map[id - id_lo];
     if (p == 0xffffffffu) {
         atomicOr(bad, 1u);
         p = 0;
@@ -189,7 +190,39 @@ __global__ void ids_to_shortlist(const uint32_t* __restrict__ sl_ids, const uint
     pos[i] = p;
 }
 
-__global__ void reconstruct_kernel(const uint32_t* __restrict__ ids, size_t n, const uint32_t* __restrict__ map,
+// Exact multi-shard mode: keep, per query row of a GLOBAL shortlist, the ids
+// this shard holds (id map hit), compacted in row order; one warp per query.
+__global__ void owned_shortlist_kernel(const uint32_t* __restrict__ sl_ids,
+                                       const uint32_t* __restrict__ sl_cnt, size_t nq, uint32_t stride,
+                                       const uint32_t* __restrict__ map, uint32_t id_lo, uint32_t nmap,
+                                       u64* __restrict__ key, uint32_t* __restrict__ pos,
+                                       uint32_t* __restrict__ cnt) {
+    const size_t q = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned lane = threadIdx.x & 31;
+    if (q >= nq) return;
+    const uint32_t n = sl_cnt[q];
+    uint32_t o = 0;
+    for (uint32_t b = 0; b < n; b += 32) {
+        const uint32_t i = b + lane;
+        uint32_t p = 0xffffffffu, id = 0;
+        if (i < n) {
+            id = sl_ids[q * stride + i];
+            if (id >= id_lo && id - id_lo < nmap) p = map[id - id_lo];
+        }
+        const bool own = p != 0xffffffffu;
+        const unsigned bal = __ballot_sync(0xffffffffu, own);
+        if (own) {
+            const uint32_t j = o + __popc(bal & ((1u << lane) - 1u));
+            key[q * stride + j] = (u64)id;
+            pos[q * stride + j] = p;
+        }
+        o += __popc(bal);
+    }
+    if (lane == 0) cnt[q] = o;
+}
+
+__global__ void reconstruct_kernel(const uint32_t* __restrict__ ids, size_t n, uint32_t id_lo,
+                                   const uint32_t* __restrict__ map,
                                    const uint64_t* __restrict__ off, uint32_t nlists, uint32_t d,
                                    const float* __restrict__ coarse, const uint8_t* __restrict__ codes,
                                    const float* __restrict__ books, uint32_t m,
@@ -199,7 +232,7 @@ __global__ void reconstruct_kernel(const uint32_t* __restrict__ ids, size_t n, c
     if (i >= n * d) return;
     const size_t v = i / d;
     const uint32_t t = (uint32_t)(i % d);
-    const uint32_t p = map[ids[v]];
+    const uint32_t p = map[ids[v] - id_lo];
     if (p == 0xffffffffu) {
         out[i] = __int_as_float(0x7fc00000);  // id never added
         return;
@@ -265,6 +298,7 @@ struct DevIndex {
     DBuf<uint8_t> q8_cache;     // per LUT-pass item 8-bit LUT (32 KiB) for the K4f filter
     DBuf<float> q8_param;       // per LUT-pass item and query lane: (scale, sum of minima)
     uint64_t next_id = 0;
+    uint64_t id_lo = ~0ull;  // smallest id held (id-range shards start above 0)
     // id -> position (lazy)
     DBuf<uint32_t> id_map;
     bool id_map_valid = false;
@@ -344,6 +378,7 @@ void stage_chunk(DevIndex& ix, const float* xf, const uint8_t* xu, size_t n, uin
     PQRR_LAUNCH_CHECK();
     count_launch();
     ix.st_n += n;
+    ix.id_lo = std::min<uint64_t>(ix.id_lo, id_base);
     ix.next_id = (uint64_t)id_base + n;
 }
 
@@ -452,14 +487,16 @@ void finalize(DevIndex& ix) {
     ix.id_map_valid = false;
 }
 
+uint64_t id_lo_of(const DevIndex& ix) { return ix.id_lo == ~0ull ? 0 : ix.id_lo; }
+
 void ensure_id_map(DevIndex& ix) {
     finalize(ix);
     if (ix.id_map_valid) return;
-    ix.id_map.alloc(std::max<uint64_t>(ix.next_id, 1));
+    ix.id_map.alloc(std::max<uint64_t>(ix.next_id - id_lo_of(ix), 1));
     PQRR_CUDA(cudaMemsetAsync(ix.id_map.p, 0xff, ix.id_map.bytes(), ix.stream));
     if (ix.c)
         id_to_pos_kernel<<<ix.c, 256, 0, ix.stream>>>(ix.list_off.p, ix.list_len.p, ix.ids.p,
-                                                      ix.id_map.p);
+                                                      (uint32_t)id_lo_of(ix), ix.id_map.p);
     PQRR_LAUNCH_CHECK();
     count_launch();
     ix.id_map_valid = true;
@@ -1373,6 +1410,14 @@ int pqrr_dev_search_f32(pqrr_dev_index* h, const float* queries, size_t nq, uint
     return search_host(h, queries, nullptr, nq, w, kprime, k, out_ids, out_dists, out_counts);
 }
 
+static void stream_join(cudaStream_t from, cudaStream_t to) {
+    cudaEvent_t e;
+    PQRR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    PQRR_CUDA(cudaEventRecord(e, from));
+    PQRR_CUDA(cudaStreamWaitEvent(to, e, 0));
+    cudaEventDestroy(e);
+}
+
 int pqrr_dev_search_u8_device(pqrr_dev_index* h, const uint8_t* d_queries, size_t nq, uint32_t w,
                               size_t kprime, size_t k, uint32_t* d_out_ids, float* d_out_dists,
                               uint32_t* d_out_counts, void* stream) {
@@ -1381,26 +1426,51 @@ int pqrr_dev_search_u8_device(pqrr_dev_index* h, const uint8_t* d_queries, size_
         std::lock_guard<std::mutex> lk(ix.mu);
         DeviceGuard g(ix.device);
         if (nq == 0) return;
-        cudaStream_t user = static_cast<cudaStream_t>(stream);
+        // NULL = the legacy default stream (torch's default stream has handle 0)
+        cudaStream_t user = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
         cudaStream_t s = ix.stream;
-        if (user && user != s) {
-            cudaEvent_t e;
-            PQRR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            PQRR_CUDA(cudaEventRecord(e, user));
-            PQRR_CUDA(cudaStreamWaitEvent(s, e, 0));
-            cudaEventDestroy(e);
-        }
+        stream_join(user, s);
         Workspace ws(s);
         float* xq = ws.alloc<float>(nq * ix.d);
         launch_widen_u8(d_queries, xq, nq * ix.d, s);
         search_device(ix, xq, nq, w, kprime, k, d_out_ids, d_out_dists, d_out_counts);
-        if (user && user != s) {
-            cudaEvent_t e;
-            PQRR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            PQRR_CUDA(cudaEventRecord(e, s));
-            PQRR_CUDA(cudaStreamWaitEvent(user, e, 0));
-            cudaEventDestroy(e);
-        }
+        stream_join(s, user);
+    });
+}
+
+
+int pqrr_dev_rerank_owned_u8_device(pqrr_dev_index* h, const uint8_t* d_queries, size_t nq,
+                                    const uint32_t* d_sl_ids, const uint32_t* d_sl_counts,
+                                    size_t sl_stride, size_t k, uint32_t* d_out_ids,
+                                    float* d_out_dists, uint32_t* d_out_counts, void* stream) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        if (ix.mprime == 0) throw ArgError("re-ranking needs refinement codes (mprime > 0)");
+        if (nq == 0 || k == 0) return;
+        if (sl_stride > 16384) throw UnsupportedError("shortlists above 16384 entries");
+        ensure_id_map(ix);
+        cudaStream_t user = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+        cudaStream_t s = ix.stream;
+        stream_join(user, s);
+        Workspace ws(s);
+        float* xq = ws.alloc<float>(nq * ix.d);
+        launch_widen_u8(d_queries, xq, nq * ix.d, s);
+        u64* key = ws.alloc<u64>(nq * sl_stride);
+        uint32_t* pos = ws.alloc<uint32_t>(nq * sl_stride);
+        uint32_t* cnt = ws.alloc<uint32_t>(nq);
+        owned_shortlist_kernel<<<nblk(nq * 32), 256, 0, s>>>(d_sl_ids, d_sl_counts, nq,
+                                                             (uint32_t)sl_stride, ix.id_map.p,
+                                                             (uint32_t)id_lo_of(ix),
+                                                             (uint32_t)ix.id_map.n, key, pos, cnt);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        launch_rerank(reinterpret_cast<uint64_t*>(key), pos, cnt, (uint32_t)sl_stride, nq, xq, ix.d,
+                      ix.block_list.p, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
+                      ix.rbooks.p, ix.mprime, ix.ks, (uint32_t)k, d_out_ids, d_out_dists,
+                      d_out_counts, s);
+        stream_join(s, user);
     });
 }
 
@@ -1435,7 +1505,8 @@ static int rerank_host(pqrr_dev_index* h, const float* qf, const uint8_t* qu, si
         uint32_t* pos = ws.alloc<uint32_t>(nq * sl_stride);
         unsigned* bad = ws.zeros<unsigned>(1);
         ids_to_shortlist<<<nblk(nq * sl_stride), 256, 0, s>>>(ids, ix.id_map.p, nq * sl_stride, key, pos,
-                                                               bad, (uint32_t)ix.id_map.n);
+                                                               bad, (uint32_t)id_lo_of(ix),
+                                                               (uint32_t)ix.id_map.n);
         PQRR_LAUNCH_CHECK();
         count_launch();
         // unused tail entries of a row may hold junk ids: only the first cnt[q] are read
@@ -1447,7 +1518,10 @@ static int rerank_host(pqrr_dev_index* h, const float* qf, const uint8_t* qu, si
                       ix.rbooks.p, ix.mprime, ix.ks, (uint32_t)k, oi, od, oc, s);
         PQRR_CUDA(cudaMemcpyAsync(out_ids, oi, nq * k * 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaMemcpyAsync(out_dists, od, nq * k * 4, cudaMemcpyDeviceToHost, s));
+        unsigned h_bad = 0;
+        PQRR_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaStreamSynchronize(s));
+        if (h_bad) throw ArgError("shortlist id not in the index");
     });
 }
 
@@ -1471,13 +1545,13 @@ int pqrr_dev_reconstruct(pqrr_dev_index* h, const uint32_t* ids, size_t n, float
         if (n == 0) return;
         ensure_id_map(ix);
         for (size_t i = 0; i < n; ++i)
-            if (ids[i] >= ix.next_id) throw ArgError("id out of range");
+            if (ids[i] >= ix.next_id || ids[i] < id_lo_of(ix)) throw ArgError("id out of range");
         cudaStream_t s = ix.stream;
         Workspace ws(s);
         uint32_t* d_ids = ws.alloc<uint32_t>(n);
         PQRR_CUDA(cudaMemcpyAsync(d_ids, ids, n * 4, cudaMemcpyHostToDevice, s));
         float* o = ws.alloc<float>(n * ix.d);
-        reconstruct_kernel<<<nblk(n * ix.d), 256, 0, s>>>(d_ids, n, ix.id_map.p, ix.list_off.p, ix.c, ix.d,
+        reconstruct_kernel<<<nblk(n * ix.d), 256, 0, s>>>(d_ids, n, (uint32_t)id_lo_of(ix), ix.id_map.p, ix.list_off.p, ix.c, ix.d,
                                                            ix.coarse.p, ix.codes.p, ix.books.p, ix.m,
                                                            ix.rcodes.p, ix.rbooks.p, ix.mprime, ix.ks, o);
         PQRR_LAUNCH_CHECK();
@@ -1499,13 +1573,14 @@ int pqrr_dev_load_lists(pqrr_dev_index* h, const uint64_t* offsets, const uint32
         if (n == 0) return;
         if (n > 0xffffffffull) throw UnsupportedError("more than 2^32 entries on one device");
         std::vector<uint32_t> assign(n);
-        uint64_t max_id = 0;
+        uint64_t max_id = 0, min_id = ~0ull;
         for (uint32_t l = 0; l < ix.c; ++l) {
             if (offsets[l + 1] < offsets[l]) throw ArgError("corrupt file");
             for (uint64_t i = offsets[l]; i < offsets[l + 1]; ++i) {
                 assign[i] = l;
                 if (i > offsets[l] && ids[i] <= ids[i - 1]) throw ArgError("corrupt file");
                 max_id = std::max<uint64_t>(max_id, ids[i]);
+                min_id = std::min<uint64_t>(min_id, ids[i]);
             }
         }
         grow_staging(ix, n);
@@ -1517,6 +1592,7 @@ int pqrr_dev_load_lists(pqrr_dev_index* h, const uint64_t* offsets, const uint32
             PQRR_CUDA(cudaMemcpyAsync(ix.st_rcodes.p, rcodes, n * ix.mprime, cudaMemcpyHostToDevice, s));
         ix.st_n = n;
         ix.next_id = max_id + 1;
+        ix.id_lo = min_id;
         finalize(ix);
     });
 }

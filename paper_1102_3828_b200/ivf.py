@@ -376,6 +376,15 @@ class IvfIndex:
         check(lib.pqrr_dev_search_u8_device(self.h, d_queries_ptr, nq, v, kprime, k, d_ids_ptr,
                                             d_dists_ptr, d_counts_ptr, stream_ptr or None))
 
+    def rerank_owned_device(self, d_queries_ptr: int, nq: int, d_sl_ids_ptr: int,
+                            d_sl_counts_ptr: int, sl_stride: int, k: int, d_ids_ptr: int,
+                            d_dists_ptr: int, d_counts_ptr: int, stream_ptr: int = 0):
+        """Exact multi-shard mode: re-rank the ids of a global shortlist that this
+        shard holds (device pointers; see pqrr_dev_rerank_owned_u8_device)."""
+        check(lib.pqrr_dev_rerank_owned_u8_device(self.h, d_queries_ptr, nq, d_sl_ids_ptr,
+                                                  d_sl_counts_ptr, sl_stride, k, d_ids_ptr,
+                                                  d_dists_ptr, d_counts_ptr, stream_ptr or None))
+
     def last_stats(self) -> dict:
         st = _lib.SearchStats()
         check(lib.pqrr_dev_last_search_stats(self.h, C.byref(st)))

@@ -7,9 +7,19 @@ each rank runs the fused search on its shard, the per-rank top-k (id, dist)
 lists are all-gathered, and K7 merges them under (dist, id)
 (types.hpp:47-50).  Ids are global, so the merge is a pure k-way merge.
 
-This is the north star's "local mode": each shard keeps its own top-k'
-shortlist, so up to world*k' candidates are re-ranked (results can only be
-as good as or better than one index with one k' shortlist).
+Two modes:
+
+* ``"local"`` — the north star's literal flow: each shard keeps its own top-k'
+  shortlist, so up to world*k' candidates are re-ranked (results can only be
+  as good as or better than one index with one k' shortlist).
+* ``"exact"`` — reproduces the single index (ivf_search_batch + ivf_rerank,
+  ivf_index.hpp:58-64,79-81) bit for bit: every shard returns its local top-k'
+  IVFADC shortlist; the all-gathered shortlists are merged to the global top-k'
+  (the union's k' smallest under (dist, id) are the single index's shortlist,
+  because an entry's ADC distance does not depend on which shard holds it);
+  each shard re-ranks the global-shortlist entries it holds; a second
+  all-gather + merge of the per-shard top-k gives the final list.  Cost: one
+  extra all-gather of Q*k'*8 B per rank.
 
 The collective is torch.distributed (NCCL over NVLink on GPUs; gloo in the
 CPU tests, which plug an oracle searcher into ``local_search``).
@@ -49,26 +59,45 @@ def merge_topk_host(ids: np.ndarray, dists: np.ndarray, counts: np.ndarray, k: i
 class ShardedSearch:
     """Host orchestration of one rank.
 
-    local_search(queries) -> (ids[nq, width], dists[nq, width], counts[nq]) for
-    this rank's shard (the product passes IvfIndex.search; tests pass an
-    oracle).  ``merge`` defaults to the device K7 kernel when a GPU is used.
+    local mode: local_search(queries) -> (ids[nq, width], dists[nq, width],
+    counts[nq]), the shard's re-ranked top-k (the product passes
+    IvfIndex.search; tests pass an oracle).
+    exact mode: local_search returns the shard's IVFADC shortlist (width k'),
+    and local_rerank(queries, sl_ids, sl_counts) re-ranks the global-shortlist
+    entries the shard holds -> (ids[nq, k], dists[nq, k], counts[nq]).
+    ``merge`` defaults to the numpy merge (the GPU path uses the K7 kernel).
     """
 
     def __init__(self, local_search: Callable, width: int, group=None,
-                 merge: Optional[Callable] = None):
+                 merge: Optional[Callable] = None, mode: str = "local",
+                 local_rerank: Optional[Callable] = None, kprime: int = 0):
         import torch.distributed as dist
 
+        if mode not in ("local", "exact"):
+            raise ValueError(f"unknown sharded mode {mode!r}")
+        if mode == "exact" and (local_rerank is None or kprime <= 0):
+            raise ValueError("exact mode needs local_rerank and kprime")
         self.dist = dist
         self.group = group
         self.local_search = local_search
+        self.local_rerank = local_rerank
         self.width = width
+        self.kprime = kprime
+        self.mode = mode
         self.world = dist.get_world_size(group)
         self.merge = merge or merge_topk_host
 
     def search(self, queries):
+        if self.mode == "local":
+            return self._gather_merge(*self.local_search(queries), self.width)
+        sl_i, sl_d, sl_c = self._gather_merge(*self.local_search(queries), self.kprime)
+        if len(sl_c) and int(sl_c.min()) < self.width:
+            raise ValueError("shortlist too small")  # SPEC.md:256, as one index would
+        return self._gather_merge(*self.local_rerank(queries, sl_i, sl_c), self.width)
+
+    def _gather_merge(self, ids, dists, counts, k):
         import torch
 
-        ids, dists, counts = self.local_search(queries)
         ti = torch.from_numpy(np.ascontiguousarray(ids).view(np.int32))
         td = torch.from_numpy(np.ascontiguousarray(dists, np.float32))
         tc = torch.from_numpy(np.ascontiguousarray(counts).view(np.int32))
@@ -81,47 +110,124 @@ class ShardedSearch:
         all_i = np.stack([g.numpy().view(np.uint32) for g in gi])
         all_d = np.stack([g.numpy() for g in gd])
         all_c = np.stack([g.numpy().view(np.uint32) for g in gc])
-        return self.merge(all_i, all_d, all_c, self.width)
+        return self.merge(all_i, all_d, all_c, k)
+
+
+def _merge_device(all_i, all_d, all_c, k, stream):
+    """K7 on stacked [parts, nq, width] device tensors -> top-k (ids, dists, counts)."""
+    import torch
+
+    from ._lib import check, lib
+
+    parts, nq, width = all_i.shape
+    dev = all_i.device
+    out_i = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    out_d = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    out_c = torch.empty(nq, dtype=torch.int32, device=dev)
+    check(lib.pqrr_dev_merge_topk_device(dev.index, all_i.data_ptr(), all_d.data_ptr(),
+                                         all_c.data_ptr(), nq, parts, width, k, out_i.data_ptr(),
+                                         out_d.data_ptr(), out_c.data_ptr(), stream.cuda_stream))
+    return out_i, out_d, out_c
+
+
+def _local_search(ix, d_queries, w, kprime, k, stream):
+    """One shard's fused search; k = 0 returns its IVFADC shortlist (width k')."""
+    import torch
+
+    nq, dev = d_queries.shape[0], d_queries.device
+    width = k or kprime
+    i = torch.empty((nq, width), dtype=torch.int32, device=dev)
+    d = torch.empty((nq, width), dtype=torch.float32, device=dev)
+    c = torch.empty(nq, dtype=torch.int32, device=dev)
+    ix.search_device(d_queries.data_ptr(), nq, w, kprime, k, i.data_ptr(), d.data_ptr(),
+                     c.data_ptr(), stream.cuda_stream)
+    return i, d, c
+
+
+def _rerank_owned(ix, d_queries, sl_i, sl_c, k, stream):
+    import torch
+
+    nq, dev = d_queries.shape[0], d_queries.device
+    i = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    d = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    c = torch.empty(nq, dtype=torch.int32, device=dev)
+    ix.rerank_owned_device(d_queries.data_ptr(), nq, sl_i.data_ptr(), sl_c.data_ptr(),
+                           sl_i.shape[1], k, i.data_ptr(), d.data_ptr(), c.data_ptr(),
+                           stream.cuda_stream)
+    return i, d, c
+
+
+def _check_shortlist(sl_c, k):
+    if sl_c.numel() and int(sl_c.min()) < k:
+        raise ValueError("shortlist too small")  # SPEC.md:256, as one index would
 
 
 class DeviceShardedSearch:
     """GPU rank: device-resident queries, NCCL all-gather into one buffer and
-    the K7 merge kernel on the same stream."""
+    the K7 merge kernel on the same stream (mode as in the module docstring)."""
 
-    def __init__(self, index, k: int, kprime: int, w: int, group=None):
+    def __init__(self, index, k: int, kprime: int, w: int, group=None, mode: str = "local"):
         import torch
         import torch.distributed as dist
 
-        self.ix, self.k, self.kprime, self.w = index, k, kprime, w
+        if mode not in ("local", "exact"):
+            raise ValueError(f"unknown sharded mode {mode!r}")
+        self.ix, self.k, self.kprime, self.w, self.mode = index, k, kprime, w, mode
         self.dist, self.group = dist, group
         self.world = dist.get_world_size(group)
         self.torch = torch
 
-    def search(self, d_queries, stream=None):
-        """d_queries: uint8 CUDA tensor [nq, d] -> (ids, dists, counts) CUDA tensors."""
-        from ._lib import check, lib
-
+    def _gather_merge(self, loc_i, loc_d, loc_c, k, stream):
         torch = self.torch
-        nq = d_queries.shape[0]
-        k = self.k
-        dev = d_queries.device
-        stream = stream or torch.cuda.current_stream(dev)
-        loc_i = torch.empty((nq, k), dtype=torch.int32, device=dev)
-        loc_d = torch.empty((nq, k), dtype=torch.float32, device=dev)
-        loc_c = torch.empty(nq, dtype=torch.int32, device=dev)
-        self.ix.search_device(d_queries.data_ptr(), nq, self.w, self.kprime, k, loc_i.data_ptr(),
-                              loc_d.data_ptr(), loc_c.data_ptr(), stream.cuda_stream)
-        all_i = torch.empty((self.world, nq, k), dtype=torch.int32, device=dev)
-        all_d = torch.empty((self.world, nq, k), dtype=torch.float32, device=dev)
+        nq, width = loc_i.shape
+        dev = loc_i.device
+        all_i = torch.empty((self.world, nq, width), dtype=torch.int32, device=dev)
+        all_d = torch.empty((self.world, nq, width), dtype=torch.float32, device=dev)
         all_c = torch.empty((self.world, nq), dtype=torch.int32, device=dev)
         self.dist.all_gather_into_tensor(all_i, loc_i, group=self.group)
         self.dist.all_gather_into_tensor(all_d, loc_d, group=self.group)
         self.dist.all_gather_into_tensor(all_c, loc_c, group=self.group)
-        out_i = torch.empty((nq, k), dtype=torch.int32, device=dev)
-        out_d = torch.empty((nq, k), dtype=torch.float32, device=dev)
-        out_c = torch.empty(nq, dtype=torch.int32, device=dev)
-        check(lib.pqrr_dev_merge_topk_device(dev.index, all_i.data_ptr(), all_d.data_ptr(),
-                                             all_c.data_ptr(), nq, self.world, k, k,
-                                             out_i.data_ptr(), out_d.data_ptr(), out_c.data_ptr(),
-                                             stream.cuda_stream))
-        return out_i, out_d, out_c
+        return _merge_device(all_i, all_d, all_c, k, stream)
+
+    def search(self, d_queries, stream=None):
+        """d_queries: uint8 CUDA tensor [nq, d] -> (ids, dists, counts) CUDA tensors."""
+        stream = stream or self.torch.cuda.current_stream(d_queries.device)
+        if self.mode == "local":
+            loc = _local_search(self.ix, d_queries, self.w, self.kprime, self.k, stream)
+            return self._gather_merge(*loc, self.k, stream)
+        loc = _local_search(self.ix, d_queries, self.w, self.kprime, 0, stream)
+        sl_i, _, sl_c = self._gather_merge(*loc, self.kprime, stream)
+        _check_shortlist(sl_c, self.k)
+        r = _rerank_owned(self.ix, d_queries, sl_i, sl_c, self.k, stream)
+        return self._gather_merge(*r, self.k, stream)
+
+
+class MultiShardSearch:
+    """Several id-range shards on ONE device in one process (more shards than
+    GPUs, or the one-GPU parity test of the sharded flow): the same steps as
+    DeviceShardedSearch with the all-gather replaced by a device-side stack."""
+
+    def __init__(self, indexes, k: int, kprime: int, w: int, mode: str = "exact"):
+        import torch
+
+        if mode not in ("local", "exact"):
+            raise ValueError(f"unknown sharded mode {mode!r}")
+        self.ixs, self.k, self.kprime, self.w, self.mode = list(indexes), k, kprime, w, mode
+        self.torch = torch
+
+    def _stack_merge(self, parts, k, stream):
+        t = self.torch
+        return _merge_device(t.stack([p[0] for p in parts]), t.stack([p[1] for p in parts]),
+                             t.stack([p[2] for p in parts]), k, stream)
+
+    def search(self, d_queries, stream=None):
+        stream = stream or self.torch.cuda.current_stream(d_queries.device)
+        if self.mode == "local":
+            return self._stack_merge([_local_search(ix, d_queries, self.w, self.kprime, self.k,
+                                                    stream) for ix in self.ixs], self.k, stream)
+        sl_i, _, sl_c = self._stack_merge([_local_search(ix, d_queries, self.w, self.kprime, 0,
+                                                         stream) for ix in self.ixs],
+                                          self.kprime, stream)
+        _check_shortlist(sl_c, self.k)
+        return self._stack_merge([_rerank_owned(ix, d_queries, sl_i, sl_c, self.k, stream)
+                                  for ix in self.ixs], self.k, stream)

@@ -400,3 +400,94 @@ def test_massive_boundary_ties_match_oracle(pq, oracle):
         # the duplicated query's shortlist is all ties: ids 123, 5000, 5001, ... in order
         expect = np.concatenate([[123], np.arange(5000, 5000 + k - 1)])
         assert np.all(ri[0, :k] == expect)
+
+
+def test_merge_topk_large_path_matches_sort(pq):
+    """K7 above the smem bitonic (parts * width > 25600: exact multi-shard mode
+    merges k'-wide shortlists): pack + global radix select + row sort."""
+    rng = np.random.default_rng(21)
+    parts, nq, width, k = 8, 6, 5000, 3000
+    ids = rng.permutation(parts * nq * width).astype(np.uint32).reshape(parts, nq, width)
+    d = rng.integers(0, 3000, (parts, nq, width)).astype(np.float32)  # many exact ties
+    d.sort(axis=2)
+    counts = rng.integers(0, width + 1, (parts, nq)).astype(np.uint32)
+    counts[:, 0] = 0
+    counts[:, 1] = 100  # fewer candidates than k
+    oi, od, oc = pq.ivf.merge_topk(ids, d, counts, k)
+    for q in range(nq):
+        keys = sorted((float(d[p, q, j]), int(ids[p, q, j])) for p in range(parts)
+                      for j in range(counts[p, q]))[:k]
+        assert oc[q] == len(keys)
+        np.testing.assert_array_equal(oi[q, :len(keys)], np.array([i for _, i in keys], np.uint32))
+        np.testing.assert_array_equal(od[q, :len(keys)], np.array([x for x, _ in keys], np.float32))
+
+
+@pytest.mark.parametrize("nshards,v,kprime,k", [(2, 16, 300, 100), (3, 8, 1000, 50), (2, 40, 10000, 100)])
+def test_exact_sharded_mode_equals_single_index(pq, mid_instance, nshards, v, kprime, k):
+    """SURVEY §8e exact mode on one GPU: id-range shards (own device indexes,
+    global ids), per-shard k' shortlists merged to the global top-k', owned
+    re-rank, final merge == the single-index oracle bit for bit."""
+    import torch
+
+    from paper_1102_3828_b200.sharded import MultiShardSearch, shard_range
+
+    mi = mid_instance
+    base, q = mi["base"], mi["queries"]
+    shards = []
+    for r in range(nshards):
+        lo, hi = shard_range(len(base), r, nshards)
+        ix = pq.IvfIndex(pq.Codebook(mi["coarse"]), pqobj(pq, mi["books"], 8),
+                         pq.RefineQuantizer(pqobj(pq, mi["rbooks"], 16)))
+        ix.add(base[lo:hi], id_base=lo)
+        ix.finalize()
+        shards.append(ix)
+    ms = MultiShardSearch(shards, k, kprime, v, mode="exact")
+    dq = torch.from_numpy(q).cuda()
+    oi, od, oc = ms.search(dq)
+    torch.cuda.synchronize()
+    qf = q.astype(np.float32)
+    si, _, sc = mi["oix"].search(qf, v, kprime)
+    ri, rd = mi["oix"].rerank(qf, si, sc, k)
+    np.testing.assert_array_equal(oi.cpu().numpy().view(np.uint32), ri)
+    np.testing.assert_array_equal(bits(od.cpu().numpy()), bits(rd))
+    assert (oc.cpu().numpy() == k).all()
+    # local mode runs too and returns ranked, duplicate-free rows
+    li, ld, lc = MultiShardSearch(shards, k, kprime, v, mode="local").search(dq)
+    li = li.cpu().numpy()
+    for r in range(len(q)):
+        assert len(set(li[r].tolist())) == k
+    # shortlist ids a shard does not hold are rejected by the explicit re-rank
+    from paper_1102_3828_b200._lib import check, lib
+    with pytest.raises(Exception, match="not in the index"):
+        check(lib.pqrr_dev_rerank_u8(shards[-1].h, np.ascontiguousarray(q[:1]), 1,
+                                     np.zeros((1, 1), np.uint32), np.ones(1, np.uint32), 1, 1,
+                                     np.zeros((1, 1), np.uint32), np.zeros((1, 1), np.float32)))
+
+
+@pytest.mark.parametrize("mode", ["exact", "local"])
+def test_device_sharded_search_nccl_world1(pq, mid_instance, mode):
+    """DeviceShardedSearch through a real NCCL group (world size 1 — gpurun has
+    one GPU): all_gather_into_tensor + K7 on the stream; equals the index."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1102_3828_b200.sharded import DeviceShardedSearch
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        mi = mid_instance
+        q = mi["queries"]
+        ds = DeviceShardedSearch(mi["dix"], 100, 1000, 24, mode=mode)
+        oi, od, oc = ds.search(torch.from_numpy(q).cuda())
+        ri, rd, rc = mi["dix"].search(q, 24, 1000, 100)
+        np.testing.assert_array_equal(oi.cpu().numpy().view(np.uint32), ri)
+        np.testing.assert_array_equal(bits(od.cpu().numpy()), bits(rd))
+    finally:
+        dist.destroy_process_group()
