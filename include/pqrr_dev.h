@@ -186,6 +186,29 @@ int pqrr_dev_rerank_owned_u8_device(pqrr_dev_index* ix, const uint8_t* d_queries
 /* ivf_reconstruct (ivf_index.hpp:75-77): coarse + decode + refine decode. */
 int pqrr_dev_reconstruct(pqrr_dev_index* ix, const uint32_t* ids, size_t n, float* out);
 
+/* ------------------------------------------------------------------ ADC / ADC+R
+ * Exhaustive first stage (adc_index.hpp:13-31) and its re-ranking
+ * (refine.hpp:30-53).  An ADC index is an index handle with one all-zero
+ * coarse centroid, bit-identical to the ADC definitions:
+ *   adc_build        -> pqrr_dev_adc_index_create + pqrr_dev_add_* + pqrr_dev_finalize
+ *   adc_search[_batch] -> pqrr_dev_search_*(w = 1, k = 0); with k > 0 the
+ *                       search is fused with the ADC+R re-rank (refine.hpp:50-53)
+ *   refine_encode    -> create with mprime > 0 (codes of y - decode(encode(y)))
+ *   rerank           -> pqrr_dev_rerank_u8/_f32
+ * refine_train (refine.hpp:33-36), residual (refine.hpp:30-31) and
+ * reconstruct (refine.hpp:42-45) are stand-alone.                                                              */
+int pqrr_dev_adc_index_create(int device, uint32_t d, uint32_t m, const float* books,
+                              uint32_t mprime, const float* rbooks, uint32_t ks,
+                              pqrr_dev_index** out);
+int pqrr_dev_refine_train(int device, const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                          const float* training, size_t n, uint32_t mprime, uint32_t iterations,
+                          uint64_t seed, float* out_rbooks);
+int pqrr_dev_residual(int device, const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                      const float* y, size_t n, float* out);
+int pqrr_dev_reconstruct_codes(int device, const float* books, uint32_t d, uint32_t m,
+                               const float* rbooks, uint32_t mprime, uint32_t ks,
+                               const uint8_t* codes, const uint8_t* rcodes, size_t n, float* out);
+
 /* K7 — merge of per-shard ranked lists (multi-GPU id-range sharding, after an
  * all-gather): inputs [parts][nq][width] ids / dists and [parts][nq] counts;
  * output the top-k per query under (dist, id) (types.hpp:47-50).  Host

@@ -96,6 +96,18 @@ class Oracle:
         _sig(L, "orc_sincos_2pi", None, [C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double)])
         _sig(L, "orc_synth_centers", C.c_int, [_u64, _u32, _u32, _f64p])
         _sig(L, "orc_synth_rows", C.c_int, [_u64, _u32, _u64, _sz, _u32, _f64p, _u32, _u8p])
+        _sig(L, "orc_adc_encode", C.c_int, [_f32p, _u32, _u32, _u32, _f32p, _sz, _u8p])
+        _sig(L, "orc_adc_search_batch", C.c_int,
+             [_f32p, _u32, _u32, _u32, _u8p, _sz, _f32p, _sz, _sz, _u32p, _f32p, _u32p])
+        _sig(L, "orc_refine_train", C.c_int,
+             [_f32p, _u32, _u32, _u32, _f32p, _sz, _u32, _u32, _u64, _f32p])
+        _sig(L, "orc_adc_refine_encode", C.c_int,
+             [_f32p, _u32, _u32, _f32p, _u32, _u32, _f32p, _sz, _u8p])
+        _sig(L, "orc_adc_reconstruct", C.c_int,
+             [_f32p, _u32, _u32, _f32p, _u32, _u32, _u8p, _u8p, _f32p])
+        _sig(L, "orc_adc_rerank_batch", C.c_int,
+             [_f32p, _u32, _u32, _f32p, _u32, _u32, _u8p, _u8p, _f32p, _sz, _u32p, _u32p, _sz,
+              _sz, _u32p, _f32p])
 
     def _chk(self, rc):
         if rc != 0:
@@ -206,6 +218,66 @@ class Oracle:
                                                 d, m, ks, training, n, mprime, iterations, seed,
                                                 rbooks))
         return rbooks
+
+    # ---- ADC / ADC+R (adc_index.hpp:13-31, refine.hpp:30-53)
+    def adc_build(self, books, m, base, ks=256):
+        base = np.ascontiguousarray(base, np.float32)
+        n, d = base.shape
+        out = np.zeros((n, m), np.uint8)
+        self._chk(self.lib.orc_adc_encode(np.ascontiguousarray(books, np.float32).reshape(-1), d, m,
+                                          ks, base, n, out))
+        return out
+
+    def adc_search(self, books, m, codes, queries, kprime, ks=256):
+        queries = np.ascontiguousarray(queries, np.float32)
+        codes = np.ascontiguousarray(codes, np.uint8)
+        nq, d = queries.shape
+        ids = np.zeros((nq, kprime), np.uint32)
+        dists = np.zeros((nq, kprime), np.float32)
+        counts = np.zeros(nq, np.uint32)
+        self._chk(self.lib.orc_adc_search_batch(np.ascontiguousarray(books, np.float32).reshape(-1),
+                                                d, m, ks, codes, codes.shape[0], queries, nq,
+                                                kprime, ids, dists, counts))
+        return ids, dists, counts
+
+    def refine_train(self, books, m, training, mprime, ks=256, iterations=25, seed=0):
+        training = np.ascontiguousarray(training, np.float32)
+        n, d = training.shape
+        out = np.zeros(mprime * ks * (d // mprime), np.float32)
+        self._chk(self.lib.orc_refine_train(np.ascontiguousarray(books, np.float32).reshape(-1), d,
+                                            m, ks, training, n, mprime, iterations, seed, out))
+        return out
+
+    def adc_refine_encode(self, books, m, rbooks, mprime, base, ks=256):
+        base = np.ascontiguousarray(base, np.float32)
+        n, d = base.shape
+        out = np.zeros((n, mprime), np.uint8)
+        self._chk(self.lib.orc_adc_refine_encode(
+            np.ascontiguousarray(books, np.float32).reshape(-1), d, m,
+            np.ascontiguousarray(rbooks, np.float32).reshape(-1), mprime, ks, base, n, out))
+        return out
+
+    def adc_reconstruct(self, books, m, rbooks, mprime, code, rcode, d=128, ks=256):
+        out = np.zeros(d, np.float32)
+        self._chk(self.lib.orc_adc_reconstruct(
+            np.ascontiguousarray(books, np.float32).reshape(-1), d, m,
+            np.ascontiguousarray(rbooks, np.float32).reshape(-1), mprime, ks,
+            np.ascontiguousarray(code, np.uint8), np.ascontiguousarray(rcode, np.uint8), out))
+        return out
+
+    def adc_rerank(self, books, m, rbooks, mprime, codes, rcodes, queries, sl_ids, sl_counts, k,
+                   ks=256):
+        queries = np.ascontiguousarray(queries, np.float32)
+        sl_ids = np.ascontiguousarray(sl_ids, np.uint32)
+        nq, d = queries.shape
+        ids = np.zeros((nq, k), np.uint32)
+        dists = np.zeros((nq, k), np.float32)
+        self._chk(self.lib.orc_adc_rerank_batch(
+            np.ascontiguousarray(books, np.float32).reshape(-1), d, m,
+            np.ascontiguousarray(rbooks, np.float32).reshape(-1), mprime, ks,
+            np.ascontiguousarray(codes, np.uint8), np.ascontiguousarray(rcodes, np.uint8), queries,
+            nq, sl_ids, np.ascontiguousarray(sl_counts, np.uint32), sl_ids.shape[1], k, ids, dists))
+        return ids, dists
 
     def ivf_build(self, coarse, books, m, base, ks=256) -> "OracleIvf":
         return OracleIvf(self, coarse, books, m, base, ks)

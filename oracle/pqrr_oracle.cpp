@@ -670,6 +670,128 @@ int orc_ivf_rerank_batch(const orc_ivf* ix, const float* queries, size_t nq,
     return 0;
 }
 
+// ================================================================= ADC / ADC+R
+// adc_index.hpp:13-31 and refine.hpp:30-53 restated directly (no coarse
+// quantizer): codes are pq_encode(y) in id order; adc_search builds ONE LUT on
+// x and returns the min(kprime, n) smallest adc_distance under (dist, id)
+// (SPEC.md:165-172); refine residual r = y - pq_decode(pq_encode(y))
+// (refine.hpp:30-31); reconstruct = decode_c + decode_r (refine.hpp:42-45);
+// rerank = l2_sq(x, reconstruct) -> k smallest (refine.hpp:47-53).
+
+int orc_adc_encode(const float* books, uint32_t d, uint32_t m, uint32_t ks, const float* base,
+                   size_t n, uint8_t* out_codes) {
+    if (m == 0 || d % m) return fail("dimension not divisible");
+    const PQ pq{d, m, ks, books};
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < int64_t(n); ++i)
+        pq_encode_into(pq, base + size_t(i) * d, out_codes + size_t(i) * m);
+    return 0;
+}
+
+int orc_adc_search_batch(const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                         const uint8_t* codes, size_t n, const float* queries, size_t nq,
+                         size_t kprime, uint32_t* out_ids, float* out_dists, uint32_t* counts) {
+    const PQ pq{d, m, ks, books};
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t q = 0; q < int64_t(nq); ++q) {
+        std::vector<float> lut(size_t(m) * ks);
+        build_lut(pq, queries + size_t(q) * d, lut.data());
+        TopK heap(kprime);
+        for (size_t i = 0; i < n; ++i)
+            heap.push(uint32_t(i), adc_distance(lut.data(), m, ks, codes + i * m));
+        auto r = heap.take_sorted();
+        for (size_t i = 0; i < r.size(); ++i) {
+            out_ids[size_t(q) * kprime + i] = r[i].id;
+            out_dists[size_t(q) * kprime + i] = r[i].dist;
+        }
+        counts[q] = uint32_t(r.size());
+    }
+    return 0;
+}
+
+// refine.hpp:30-31 residual of each row; used by refine_train and refine_encode
+static void adc_residuals(const PQ& pq, const float* y, size_t n, float* res) {
+    const uint32_t d = pq.d;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < int64_t(n); ++i) {
+        std::vector<float> p(d);
+        uint8_t code[256];
+        pq_encode_into(pq, y + size_t(i) * d, code);
+        pq_decode_into(pq, code, p.data());
+        for (uint32_t t = 0; t < d; ++t) res[size_t(i) * d + t] = y[size_t(i) * d + t] - p[t];
+    }
+}
+
+// refine.hpp:33-36: pq_train on the residual set, 8 bits per sub-quantizer.
+int orc_refine_train(const float* books, uint32_t d, uint32_t m, uint32_t ks, const float* training,
+                     size_t n, uint32_t mprime, uint32_t iterations, uint64_t seed,
+                     float* out_rbooks) {
+    try {
+        if (m == 0 || d % m || mprime == 0 || d % mprime)
+            throw std::invalid_argument("dimension not divisible");
+        std::vector<float> res(n * d);
+        adc_residuals(PQ{d, m, ks, books}, training, n, res.data());
+        auto b = pq_train(res.data(), n, d, mprime, ks, iterations, seed, 1);
+        std::memcpy(out_rbooks, b.data(), b.size() * sizeof(float));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e.what());
+    }
+}
+
+// refine.hpp:38-40: id-aligned encode_r(y - decode(encode(y))).
+int orc_adc_refine_encode(const float* books, uint32_t d, uint32_t m, const float* rbooks,
+                          uint32_t mprime, uint32_t ks, const float* base, size_t n,
+                          uint8_t* out_rcodes) {
+    if (mprime == 0 || d % mprime) return fail("dimension not divisible");
+    std::vector<float> res(n * d);
+    adc_residuals(PQ{d, m, ks, books}, base, n, res.data());
+    const PQ rq{d, mprime, ks, rbooks};
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < int64_t(n); ++i)
+        pq_encode_into(rq, res.data() + size_t(i) * d, out_rcodes + size_t(i) * mprime);
+    return 0;
+}
+
+// refine.hpp:42-45
+int orc_adc_reconstruct(const float* books, uint32_t d, uint32_t m, const float* rbooks,
+                        uint32_t mprime, uint32_t ks, const uint8_t* code, const uint8_t* rcode,
+                        float* out) {
+    std::vector<float> p(d), r(d);
+    pq_decode_into(PQ{d, m, ks, books}, code, p.data());
+    pq_decode_into(PQ{d, mprime, ks, rbooks}, rcode, r.data());
+    for (uint32_t t = 0; t < d; ++t) out[t] = p[t] + r[t];
+    return 0;
+}
+
+// refine.hpp:47-53 ("shortlist too small" when k exceeds the shortlist).
+int orc_adc_rerank_batch(const float* books, uint32_t d, uint32_t m, const float* rbooks,
+                         uint32_t mprime, uint32_t ks, const uint8_t* codes, const uint8_t* rcodes,
+                         const float* queries, size_t nq, const uint32_t* sl_ids,
+                         const uint32_t* sl_counts, size_t sl_stride, size_t k, uint32_t* out_ids,
+                         float* out_dists) {
+    for (size_t q = 0; q < nq; ++q)
+        if (k > sl_counts[q]) return fail("shortlist too small");
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t q = 0; q < int64_t(nq); ++q) {
+        const float* x = queries + size_t(q) * d;
+        std::vector<float> yh(d);
+        TopK h(k);
+        for (uint32_t i = 0; i < sl_counts[q]; ++i) {
+            const uint32_t id = sl_ids[size_t(q) * sl_stride + i];
+            orc_adc_reconstruct(books, d, m, rbooks, mprime, ks, codes + size_t(id) * m,
+                                rcodes + size_t(id) * mprime, yh.data());
+            h.push(id, l2_sq(x, yh.data(), d));
+        }
+        auto r = h.take_sorted();
+        for (size_t i = 0; i < r.size(); ++i) {
+            out_ids[size_t(q) * k + i] = r[i].id;
+            out_dists[size_t(q) * k + i] = r[i].dist;
+        }
+    }
+    return 0;
+}
+
 int orc_coarse_probe(const float* coarse, uint32_t c, uint32_t d, const float* queries, size_t nq,
                      uint32_t v, uint32_t* out_lists, float* out_dists) {
     if (v < 1 || v > c) return fail("v must satisfy 1 <= v <= c");

@@ -85,6 +85,26 @@ int orc_ivf_rerank_batch(const orc_ivf* ix, const float* queries, size_t nq,
                          const uint32_t* sl_ids, const uint32_t* sl_counts, size_t sl_stride,
                          size_t k, uint32_t* out_ids, float* out_dists);
 /* Coarse probe selection alone (for parity of the first kernel): v ids per query. */
+/* ADC / ADC+R (adc_index.hpp:13-31, refine.hpp:30-53), restated directly. */
+int orc_adc_encode(const float* books, uint32_t d, uint32_t m, uint32_t ks, const float* base,
+                   size_t n, uint8_t* out_codes);
+int orc_adc_search_batch(const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                         const uint8_t* codes, size_t n, const float* queries, size_t nq,
+                         size_t kprime, uint32_t* out_ids, float* out_dists, uint32_t* counts);
+int orc_refine_train(const float* books, uint32_t d, uint32_t m, uint32_t ks, const float* training,
+                     size_t n, uint32_t mprime, uint32_t iterations, uint64_t seed,
+                     float* out_rbooks);
+int orc_adc_refine_encode(const float* books, uint32_t d, uint32_t m, const float* rbooks,
+                          uint32_t mprime, uint32_t ks, const float* base, size_t n,
+                          uint8_t* out_rcodes);
+int orc_adc_reconstruct(const float* books, uint32_t d, uint32_t m, const float* rbooks,
+                        uint32_t mprime, uint32_t ks, const uint8_t* code, const uint8_t* rcode,
+                        float* out);
+int orc_adc_rerank_batch(const float* books, uint32_t d, uint32_t m, const float* rbooks,
+                         uint32_t mprime, uint32_t ks, const uint8_t* codes, const uint8_t* rcodes,
+                         const float* queries, size_t nq, const uint32_t* sl_ids,
+                         const uint32_t* sl_counts, size_t sl_stride, size_t k, uint32_t* out_ids,
+                         float* out_dists);
 int orc_coarse_probe(const float* coarse, uint32_t c, uint32_t d, const float* queries,
                      size_t nq, uint32_t v, uint32_t* out_lists, float* out_dists);
 

@@ -12,4 +12,8 @@ from .ivf import (  # noqa: F401
     ivf_reconstruct, ivf_refine_encode, ivf_refine_train, ivf_rerank, ivf_search,
     ivf_search_batch, ivf_train, kmeans_train, pq_decode, pq_encode, pq_train, synth,
 )
-from . import ivf, kernels, sharded  # noqa: F401
+from .adc import (  # noqa: F401
+    AdcIndex, adc_build, adc_search, adc_search_batch, reconstruct, refine_encode, refine_train,
+    rerank, residual,
+)
+from . import adc, ivf, kernels, sharded  # noqa: F401

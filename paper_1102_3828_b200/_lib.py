@@ -106,6 +106,11 @@ _sig("pqrr_dev_last_search_stats", [_vp, C.POINTER(SearchStats)])
 _sig("pqrr_dev_load_lists", [_vp, _u64p, _u32p, _u8p, _vp])
 _sig("pqrr_dev_merge_topk", [_int, _u32p, _f32p, _u32p, _sz, _u32, _u32, _u32, _u32p, _f32p, _u32p])
 _sig("pqrr_dev_merge_topk_device", [_int, _vp, _vp, _vp, _sz, _u32, _u32, _u32, _vp, _vp, _vp, _vp])
+_sig("pqrr_dev_adc_index_create", [_int, _u32, _u32, _f32p, _u32, _vp, _u32, C.POINTER(_vp)])
+_sig("pqrr_dev_refine_train", [_int, _f32p, _u32, _u32, _u32, _f32p, _sz, _u32, _u32, _u64, _f32p])
+_sig("pqrr_dev_residual", [_int, _f32p, _u32, _u32, _u32, _f32p, _sz, _f32p])
+_sig("pqrr_dev_reconstruct_codes", [_int, _f32p, _u32, _u32, _f32p, _u32, _u32, _u8p, _u8p, _sz,
+                                    _f32p])
 
 # Symbols include/pqrr_dev.h declares (checked by the CPU test suite).
 EXPORTED = [
@@ -119,6 +124,8 @@ EXPORTED = [
     "pqrr_dev_search_u8_device", "pqrr_dev_rerank_u8", "pqrr_dev_rerank_f32",
     "pqrr_dev_reconstruct", "pqrr_dev_last_search_stats", "pqrr_dev_load_lists",
     "pqrr_dev_merge_topk", "pqrr_dev_merge_topk_device", "pqrr_dev_rerank_owned_u8_device",
+    "pqrr_dev_adc_index_create", "pqrr_dev_refine_train", "pqrr_dev_residual",
+    "pqrr_dev_reconstruct_codes",
 ]
 
 

@@ -221,6 +221,34 @@ __global__ void owned_shortlist_kernel(const uint32_t* __restrict__ sl_ids,
     if (lane == 0) cnt[q] = o;
 }
 
+// refine.hpp:42-45: yhat = decode_c(code) + decode_r(rcode) (ADC+R estimate).
+__global__ void reconstruct_codes_kernel(const uint8_t* __restrict__ codes,
+                                         const uint8_t* __restrict__ rcodes, size_t n, uint32_t d,
+                                         const float* __restrict__ books, uint32_t m,
+                                         const float* __restrict__ rbooks, uint32_t mprime,
+                                         uint32_t ks, float* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * d) return;
+    const size_t v = i / d;
+    const uint32_t t = (uint32_t)(i % d);
+    const uint32_t ds = d / m, j = t / ds, dsr = d / mprime, jr = t / dsr;
+    const float p = books[((size_t)j * ks + codes[v * m + j]) * ds + (t - j * ds)];
+    const float r = rbooks[((size_t)jr * ks + rcodes[v * mprime + jr]) * dsr + (t - jr * dsr)];
+    out[i] = __fadd_rn(p, r);
+}
+
+// refine.hpp:30-31: r = y - decode(code), code = encode(y).
+__global__ void pq_residual_kernel(const float* __restrict__ y, const uint8_t* __restrict__ codes,
+                                   size_t n, uint32_t d, const float* __restrict__ books, uint32_t m,
+                                   uint32_t ks, float* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * d) return;
+    const size_t v = i / d;
+    const uint32_t t = (uint32_t)(i % d);
+    const uint32_t ds = d / m, j = t / ds;
+    out[i] = __fsub_rn(y[i], books[((size_t)j * ks + codes[v * m + j]) * ds + (t - j * ds)]);
+}
+
 __global__ void reconstruct_kernel(const uint32_t* __restrict__ ids, size_t n, uint32_t id_lo,
                                    const uint32_t* __restrict__ map,
                                    const uint64_t* __restrict__ off, uint32_t nlists, uint32_t d,
@@ -1594,6 +1622,72 @@ int pqrr_dev_load_lists(pqrr_dev_index* h, const uint64_t* offsets, const uint32
         ix.next_id = max_id + 1;
         ix.id_lo = min_id;
         finalize(ix);
+    });
+}
+
+// ---------------------------------------------------------------- ADC / ADC+R
+// The exhaustive index (adc_index.hpp:13-31) is the IVF machinery with ONE
+// all-zero coarse centroid: y - 0 = y and x - 0 = x exactly in fp32, and
+// (0 + p) + q_r = p + q_r, so codes, LUTs, ADC sums, refinement residuals and
+// re-rank distances are the ADC / ADC+R ones bit for bit.
+int pqrr_dev_adc_index_create(int device, uint32_t d, uint32_t m, const float* books,
+                              uint32_t mprime, const float* rbooks, uint32_t ks,
+                              pqrr_dev_index** out) {
+    std::vector<float> zero(std::max<uint32_t>(d, 1), 0.f);
+    return pqrr_dev_index_create(device, d, 1, zero.data(), m, books, mprime, rbooks, ks, out);
+}
+
+int pqrr_dev_refine_train(int device, const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                          const float* training, size_t n, uint32_t mprime, uint32_t iterations,
+                          uint64_t seed, float* out_rbooks) {
+    std::vector<float> zero(std::max<uint32_t>(d, 1), 0.f);
+    return pqrr_dev_ivf_refine_train(device, zero.data(), 1, books, d, m, ks, training, n, mprime,
+                                     iterations, seed, out_rbooks);
+}
+
+int pqrr_dev_residual(int device, const float* books, uint32_t d, uint32_t m, uint32_t ks,
+                      const float* y, size_t n, float* out) {
+    return guarded([&] {
+        check_shape(d, m, ks);
+        if (n == 0) return;
+        Session se(device);
+        Workspace ws(se.s);
+        const float* b = se.upload(ws, books, (size_t)ks * d);
+        const float* dy = se.upload(ws, y, n * d);
+        uint8_t* c = ws.alloc<uint8_t>(n * m);
+        launch_pq_encode(dy, n, d, b, m, ks, c, se.s);
+        float* o = ws.alloc<float>(n * d);
+        pq_residual_kernel<<<nblk(n * d), 256, 0, se.s>>>(dy, c, n, d, b, m, ks, o);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        se.download(out, o, n * d);
+        se.sync();
+    });
+}
+
+int pqrr_dev_reconstruct_codes(int device, const float* books, uint32_t d, uint32_t m,
+                               const float* rbooks, uint32_t mprime, uint32_t ks,
+                               const uint8_t* codes, const uint8_t* rcodes, size_t n, float* out) {
+    return guarded([&] {
+        check_shape(d, m, ks);
+        if (mprime == 0 || d % mprime) throw ArgError("dimension not divisible");
+        for (size_t i = 0; i < n * m; ++i)
+            if (codes[i] >= ks) throw ArgError("code index out of range");
+        for (size_t i = 0; i < n * mprime; ++i)
+            if (rcodes[i] >= ks) throw ArgError("code index out of range");
+        if (n == 0) return;
+        Session se(device);
+        Workspace ws(se.s);
+        const float* b = se.upload(ws, books, (size_t)ks * d);
+        const float* rb = se.upload(ws, rbooks, (size_t)ks * d);
+        const uint8_t* c = se.upload(ws, codes, n * m);
+        const uint8_t* rc = se.upload(ws, rcodes, n * mprime);
+        float* o = ws.alloc<float>(n * d);
+        reconstruct_codes_kernel<<<nblk(n * d), 256, 0, se.s>>>(c, rc, n, d, b, m, rb, mprime, ks, o);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        se.download(out, o, n * d);
+        se.sync();
     });
 }
 

@@ -48,3 +48,8 @@ def pq():
     import paper_1102_3828_b200 as p
 
     return p
+
+
+@pytest.fixture(scope="session")
+def golden_adc():
+    return dict(np.load(os.path.join(GOLDEN, "adc_small.npz")))

@@ -110,5 +110,49 @@ def main():
     print("golden fixtures written to", OUT)
 
 
+def main_adc():
+    """adc_small.npz: exhaustive ADC / ADC+R (adc_index.hpp, refine.hpp:30-53).
+    Expected outputs from the reference's code: codes = kernels::encode_batch(y),
+    shortlist = kernels::scan_topk(build_lut(x), all codes) (what adc_search
+    computes), residual codes = encode_batch(y - decode(code)),
+    re-rank = l2_sq(x, decode + decode_r) through the reference l2_sq and TopK."""
+    build(ref=True)
+    o = Oracle()
+    r = RefLib()
+    seed, K, d = 0, 64, 128
+    centers = o.synth_centers(seed, K, d)
+    base = o.synth_rows(seed, 2, 0, 12000, centers)
+    train = o.synth_rows(seed, 1, 0, 3000, centers).astype(np.float32)
+    queries = o.synth_rows(seed, 3, 0, 16, centers)
+    m, mprime = 8, 8
+    books = o.pq_train(train, m, iterations=6, seed=11)
+    rbooks = o.refine_train(books, m, train, mprime, iterations=6, seed=12)
+    bf, qf = base.astype(np.float32), queries.astype(np.float32)
+    codes = r.encode(books, bf, m)
+    dec = r.decode(books, codes, d)
+    rcodes = r.encode(rbooks, bf - dec, mprime)
+    rdec = r.decode(rbooks, rcodes, d)
+    kprime, k = 200, 20
+    r.set_threads(4)  # n >= 8192: scan_topk's partitioned merge path
+    sl = [r.scan_topk(r.build_lut(books, x, m), codes, kprime) for x in qf]
+    sl_ids = np.stack([a for a, _ in sl])
+    sl_d = np.stack([b for _, b in sl])
+    yhat = dec + rdec
+    rr = []
+    for q in range(len(qf)):
+        dd = np.array([r.l2_sq(qf[q], yhat[i]) for i in sl_ids[q]], np.float32)
+        rr.append(r.topk(sl_ids[q], dd, k))
+    np.savez_compressed(
+        os.path.join(OUT, "adc_small.npz"), base=base, queries=queries, books=books,
+        rbooks=rbooks, m=m, mprime=mprime, codes=codes, rcodes=rcodes, kprime=kprime, k=k,
+        sl_ids=sl_ids, sl_dists=sl_d, rr_ids=np.stack([a for a, _ in rr]),
+        rr_dists=np.stack([b for _, b in rr]))
+    print("adc fixture written to", OUT)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["adc"]:
+        main_adc()
+    else:
+        main()
+        main_adc()

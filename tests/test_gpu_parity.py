@@ -491,3 +491,82 @@ def test_device_sharded_search_nccl_world1(pq, mid_instance, mode):
         np.testing.assert_array_equal(bits(od.cpu().numpy()), bits(rd))
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ ADC / ADC+R (exhaustive)
+def test_adc_golden(pq, golden_adc, oracle):
+    """adc_build / adc_search_batch / refine_encode / rerank (adc_index.hpp,
+    refine.hpp:30-53) on the device == the reference kernels' outputs."""
+    g = golden_adc
+    m, mp, kp, k = int(g["m"]), int(g["mprime"]), int(g["kprime"]), int(g["k"])
+    P = pqobj(pq, g["books"], m)
+    R = pq.RefineQuantizer(pqobj(pq, g["rbooks"], mp))
+    ix = pq.adc_build(P, g["base"])
+    np.testing.assert_array_equal(ix.codes, g["codes"])
+    res = pq.adc_search_batch(ix, g["queries"], kp)
+    for q, r in enumerate(res):
+        np.testing.assert_array_equal(r.ids, g["sl_ids"][q])
+        np.testing.assert_array_equal(bits(r.dists), bits(g["sl_dists"][q]))
+    one = pq.adc_search(ix, g["queries"][3], kp)
+    np.testing.assert_array_equal(one.ids, g["sl_ids"][3])
+    codes = pq.refine_encode(ix, R, g["base"])
+    np.testing.assert_array_equal(codes.bytes, g["rcodes"])
+    rr = pq.rerank(g["queries"], res, ix, R, codes, k)
+    for q, r in enumerate(rr):
+        np.testing.assert_array_equal(r.ids, g["rr_ids"][q])
+        np.testing.assert_array_equal(bits(r.dists), bits(g["rr_dists"][q]))
+    # fused ADC+R search (shortlist + re-rank in one call)
+    fi, fd, fc = ix.search(g["queries"], kp, k)
+    np.testing.assert_array_equal(fi, g["rr_ids"])
+    np.testing.assert_array_equal(bits(fd), bits(g["rr_dists"]))
+    with pytest.raises(ValueError, match="shortlist too small"):
+        pq.rerank(g["queries"][0], pq.SearchResult(res[0].ids[:3], res[0].dists[:3]), ix, R, codes, 4)
+    # stand-alone helpers: residual, reconstruct, refine_train
+    bf = g["base"][:500].astype(np.float32)
+    dec = oracle.decode(g["books"], g["codes"][:500], 128)
+    np.testing.assert_array_equal(bits(pq.residual(bf, P)), bits(bf - dec))
+    rec = pq.reconstruct(P, R, g["codes"][:500], g["rcodes"][:500])
+    for i in (0, 7, 499):
+        np.testing.assert_array_equal(bits(rec[i]), bits(oracle.adc_reconstruct(
+            g["books"], m, g["rbooks"], mp, g["codes"][i], g["rcodes"][i])))
+    tr = g["base"][:4000].astype(np.float32)
+    R2 = pq.refine_train(P, tr, 16, pq.TrainParams(iterations=3, seed=4))
+    np.testing.assert_array_equal(R2.pq.flat(), oracle.refine_train(g["books"], m, tr, 16,
+                                                                    iterations=3, seed=4))
+
+
+@pytest.mark.parametrize("m,mp,kp,k", [(8, 16, 1000, 100), (8, 8, 300, 50), (8, 32, 5000, 100)])
+def test_adc_matches_oracle_large(pq, oracle, mid_instance, m, mp, kp, k):
+    """120k-vector exhaustive ADC+R vs the oracle: the single list runs through
+    K4f/K4r in 16k-entry work items."""
+    mi = mid_instance
+    base, q = mi["base"], mi["queries"][:32]
+    train = base[:20000].astype(np.float32)
+    books = oracle.pq_train(train, m, iterations=3, seed=m)
+    rbooks = oracle.refine_train(books, m, train, mp, iterations=3, seed=mp)
+    P, R = pqobj(pq, books, m), pq.RefineQuantizer(pqobj(pq, rbooks, mp))
+    ix = pq.adc_build(P, base, rq=R)
+    bf, qf = base.astype(np.float32), q.astype(np.float32)
+    ocodes = oracle.adc_build(books, m, bf)
+    np.testing.assert_array_equal(ix.codes, ocodes)
+    oi, od, oc = oracle.adc_search(books, m, ocodes, qf, kp)
+    di, dd, dc = ix.search(q, kp, 0)
+    np.testing.assert_array_equal(di, oi)
+    np.testing.assert_array_equal(bits(dd), bits(od))
+    orc = oracle.adc_refine_encode(books, m, rbooks, mp, bf)
+    np.testing.assert_array_equal(ix.refine_codes.bytes, orc)
+    ri, rd = oracle.adc_rerank(books, m, rbooks, mp, ocodes, orc, qf, oi, oc, k)
+    fi, fd, _ = ix.search(q, kp, k)
+    np.testing.assert_array_equal(fi, ri)
+    np.testing.assert_array_equal(bits(fd), bits(rd))
+
+
+def test_adc_scan_needs_m8(pq, golden_adc):
+    """The device scan kernels are specialised to m = 8 (every BASELINE config);
+    other m build and encode but fail loudly at search (no CPU fallback)."""
+    rng = np.random.default_rng(3)
+    books = rng.standard_normal((16, 256, 8)).astype(np.float32)
+    ix = pq.adc_build(pqobj(pq, books, 16), golden_adc["base"][:1000])
+    assert ix.codes.shape == (1000, 16)
+    with pytest.raises(ValueError, match="m = 8"):
+        ix.search(golden_adc["queries"], 10, 0)

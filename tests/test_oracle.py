@@ -221,3 +221,49 @@ def test_recall_examples(oracle):
     gt = np.array([5], np.uint32)
     assert oracle.recall_at_r(ids, cnt, gt, 1) == 0.0
     assert oracle.recall_at_r(ids, cnt, gt, 2) == 1.0
+
+
+# ------------------------------------------------------------------ ADC / ADC+R
+def test_adc_oracle_matches_reference_golden(oracle, golden_adc):
+    """adc_index.hpp / refine.hpp:30-53 restatement vs the reference's kernels
+    (encode_batch, scan_topk over all codes, decode, l2_sq, TopK)."""
+    g = golden_adc
+    m, mp, kp, k = int(g["m"]), int(g["mprime"]), int(g["kprime"]), int(g["k"])
+    bf, qf = g["base"].astype(np.float32), g["queries"].astype(np.float32)
+    codes = oracle.adc_build(g["books"], m, bf)
+    np.testing.assert_array_equal(codes, g["codes"])
+    ids, d, cnt = oracle.adc_search(g["books"], m, codes, qf, kp)
+    assert (cnt == kp).all()
+    np.testing.assert_array_equal(ids, g["sl_ids"])
+    np.testing.assert_array_equal(bits(d), bits(g["sl_dists"]))
+    rc = oracle.adc_refine_encode(g["books"], m, g["rbooks"], mp, bf)
+    np.testing.assert_array_equal(rc, g["rcodes"])
+    ri, rd = oracle.adc_rerank(g["books"], m, g["rbooks"], mp, codes, rc, qf, ids, cnt, k)
+    np.testing.assert_array_equal(ri, g["rr_ids"])
+    np.testing.assert_array_equal(bits(rd), bits(g["rr_dists"]))
+
+
+def test_spec_adc_full_sort_and_shortlist_bound(oracle, golden_adc):
+    """SPEC.md:172 (adc_search with k' = n equals a naive full sort of the
+    adc_distances, ties by id) and acceptance #7 (recall@1 of
+    ADC+R never exceeds recall@k' of ADC on identical queries)."""
+    g = golden_adc
+    m, mp = int(g["m"]), int(g["mprime"])
+    bf, qf = g["base"][:3000].astype(np.float32), g["queries"].astype(np.float32)
+    codes = oracle.adc_build(g["books"], m, bf)
+    n = len(codes)
+    ids, d, cnt = oracle.adc_search(g["books"], m, codes, qf[:3], n)
+    for q in range(3):
+        lut = oracle.build_lut(g["books"], qf[q], m)
+        full = np.array([oracle.adc_distance(lut, c) for c in codes], np.float32)
+        order = np.lexsort((np.arange(n), full))
+        np.testing.assert_array_equal(ids[q], order)
+        np.testing.assert_array_equal(bits(d[q]), bits(full[order]))
+    gt, _ = oracle.exact_nearest(bf, qf)
+    rc = oracle.adc_refine_encode(g["books"], m, g["rbooks"], mp, bf)
+    for kp in (5, 20, 100):
+        sl, _, sc = oracle.adc_search(g["books"], m, codes, qf, kp)
+        ri, _ = oracle.adc_rerank(g["books"], m, g["rbooks"], mp, codes, rc, qf, sl, sc, 1)
+        r1 = np.mean(ri[:, 0] == gt)
+        rk = np.mean([gt[q] in sl[q] for q in range(len(qf))])
+        assert r1 <= rk
