@@ -137,6 +137,10 @@ int pqrr_dev_index_get_info(pqrr_dev_index* ix, pqrr_dev_index_info* out);
 int pqrr_dev_export_lists(pqrr_dev_index* ix, uint64_t* offsets, uint32_t* ids, uint8_t* codes,
                           uint8_t* rcodes);
 
+/* Trained parameters held by the index (coarse[c*d], books[ks*d],
+ * rbooks[ks*d] when mprime > 0; any may be NULL). */
+int pqrr_dev_export_codebooks(pqrr_dev_index* ix, float* coarse, float* books, float* rbooks);
+
 /* Inverse of pqrr_dev_export_lists: load an existing inverted file into an
  * EMPTY index (e.g. a host IvfIndex, ivf_index.hpp:27-36, or a PQRR file,
  * storage.hpp:23-25).  Lists in list order, ids ascending within a list;
@@ -208,6 +212,27 @@ int pqrr_dev_residual(int device, const float* books, uint32_t d, uint32_t m, ui
 int pqrr_dev_reconstruct_codes(int device, const float* books, uint32_t d, uint32_t m,
                                const float* rbooks, uint32_t mprime, uint32_t ks,
                                const uint8_t* codes, const uint8_t* rcodes, size_t n, float* out);
+
+/* ------------------------------------------------------------------ persistence
+ * The "PQRR" container (storage.hpp:14-28): magic "PQRR",
+ * version byte 1, little-endian.  Host files; index loads create a device
+ * index on `device`.  Truncated / oversized / malformed files fail with
+ * PQRR_EINVAL "corrupt file".  Layouts: DESIGN.md §10.
+ *   save_quantizer / load_quantizer   (also codebooks: m = 1, ks = k)
+ *   save_adc_index / load_adc_index   (save_adc_index(ix, rq, codes, path))
+ *   save_index / load_index           (save_ivf_index / load_ivf_index)
+ *   probe_index_kind                  (probe_index_kind, storage.hpp:59-62)
+ * load_quantizer with books = NULL returns the shape only.                  */
+enum { PQRR_INDEX_ADC = 0, PQRR_INDEX_IVF = 1 };
+int pqrr_dev_save_quantizer(const char* path, uint32_t d, uint32_t m, uint32_t ks,
+                            const float* books);
+int pqrr_dev_load_quantizer(const char* path, uint32_t* d, uint32_t* m, uint32_t* ks,
+                            float* books);
+int pqrr_dev_save_index(pqrr_dev_index* ix, const char* path);
+int pqrr_dev_load_index(int device, const char* path, pqrr_dev_index** out);
+int pqrr_dev_save_adc_index(pqrr_dev_index* ix, const char* path);
+int pqrr_dev_load_adc_index(int device, const char* path, pqrr_dev_index** out);
+int pqrr_dev_probe_index_kind(const char* path, int* kind);
 
 /* K7 — merge of per-shard ranked lists (multi-GPU id-range sharding, after an
  * all-gather): inputs [parts][nq][width] ids / dists and [parts][nq] counts;

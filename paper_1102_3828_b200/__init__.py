@@ -16,4 +16,9 @@ from .adc import (  # noqa: F401
     AdcIndex, adc_build, adc_search, adc_search_batch, reconstruct, refine_encode, refine_train,
     rerank, residual,
 )
-from . import adc, ivf, kernels, sharded  # noqa: F401
+from .storage import (  # noqa: F401
+    IndexKind, LoadedAdcIndex, LoadedIvfIndex, load_adc_index, load_codebook, load_ivf_index,
+    load_quantizer, probe_index_kind, save_adc_index, save_codebook, save_ivf_index,
+    save_quantizer,
+)
+from . import adc, ivf, kernels, sharded, storage  # noqa: F401

@@ -26,6 +26,9 @@ struct ArgError : std::invalid_argument {
     } while (0)
 #define PQRR_LAUNCH_CHECK() PQRR_CUDA(cudaGetLastError())
 
+// Sets the calling thread's pqrr_dev_last_error() text; returns `code`.
+int report_error(int code, const std::string& msg);
+
 // Counts kernel launches issued by this library (gpu_launches evidence).
 void count_launch(int n = 1);
 unsigned long long launch_count();

@@ -24,6 +24,11 @@ namespace pqrr_b200 {
 
 thread_local std::string g_last_error;
 
+int report_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
 struct ShortlistError : std::runtime_error {
     ShortlistError() : std::runtime_error("shortlist too small") {}
 };
@@ -1586,6 +1591,18 @@ int pqrr_dev_reconstruct(pqrr_dev_index* h, const uint32_t* ids, size_t n, float
         count_launch();
         PQRR_CUDA(cudaMemcpyAsync(out, o, n * ix.d * 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pqrr_dev_export_codebooks(pqrr_dev_index* h, float* coarse, float* books, float* rbooks) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        if (coarse) PQRR_CUDA(cudaMemcpy(coarse, ix.coarse.p, ix.coarse.bytes(), cudaMemcpyDeviceToHost));
+        if (books) PQRR_CUDA(cudaMemcpy(books, ix.books.p, ix.books.bytes(), cudaMemcpyDeviceToHost));
+        if (rbooks && ix.mprime)
+            PQRR_CUDA(cudaMemcpy(rbooks, ix.rbooks.p, ix.rbooks.bytes(), cudaMemcpyDeviceToHost));
     });
 }
 

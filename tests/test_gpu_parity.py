@@ -570,3 +570,81 @@ def test_adc_scan_needs_m8(pq, golden_adc):
     assert ix.codes.shape == (1000, 16)
     with pytest.raises(ValueError, match="m = 8"):
         ix.search(golden_adc["queries"], 10, 0)
+
+
+# ------------------------------------------------------------------ PQRR container (device indexes)
+def test_ivf_index_file_round_trip(pq, golden_ivf, tmp_path):
+    """save_ivf_index of a device-built index == the restatement's bytes of the
+    reference layout (lists id-ascending, refine codes id-aligned); the loaded
+    index searches and re-ranks exactly like the golden vectors."""
+    from oracle import storage_py as S
+
+    g = golden_ivf
+    m, mp = int(g["m"]), int(g["mprime"])
+    P, R = pqobj(pq, g["books"], m), pq.RefineQuantizer(pqobj(pq, g["rbooks"], mp))
+    ix = pq.ivf_build(pq.Codebook(g["coarse"]), P, g["base"])
+    codes = pq.ivf_refine_encode(ix, R, g["base"])
+    f = tmp_path / "ivf.pqrr"
+    pq.save_ivf_index(ix, R, codes, f)
+    raw = f.read_bytes()
+    assert raw == S.ivf_file(g["books"], 128, m, 256, g["coarse"], g["offsets"], g["ids_l"],
+                             g["codes"][g["ids_l"]], g["rbooks"], mp, g["rcodes"])
+    assert pq.probe_index_kind(f) == pq.IndexKind.ivf
+    L = pq.load_ivf_index(f)
+    np.testing.assert_array_equal(L.refine_codes.bytes, g["rcodes"])
+    v, kp, k = int(g["v"]), int(g["kprime"]), int(g["k"])
+    si, sd, sc = L.index.search(g["queries"], v, kp, 0)
+    for q in range(len(sc)):
+        n = sc[q]
+        np.testing.assert_array_equal(si[q, :n], g["sl_ids"][q, :n])
+    ri, rd, _ = L.index.search(g["queries"], v, kp, k)
+    np.testing.assert_array_equal(ri, g["rr_ids"])
+    np.testing.assert_array_equal(bits(rd), bits(g["rr_dists"]))
+    pq.save_ivf_index(L.index, L.refine_quantizer, L.refine_codes, tmp_path / "again.pqrr")
+    assert (tmp_path / "again.pqrr").read_bytes() == raw
+    # without refinement
+    ix0 = pq.ivf_build(pq.Codebook(g["coarse"]), P, g["base"])
+    pq.save_ivf_index(ix0, None, None, tmp_path / "plain.pqrr")
+    assert (tmp_path / "plain.pqrr").read_bytes() == S.ivf_file(
+        g["books"], 128, m, 256, g["coarse"], g["offsets"], g["ids_l"], g["codes"][g["ids_l"]])
+    for cut in (1, 100, len(raw) // 2):
+        (tmp_path / "t.pqrr").write_bytes(raw[:-cut])
+        with pytest.raises(ValueError, match="corrupt file"):
+            pq.load_ivf_index(tmp_path / "t.pqrr")
+    # a list whose ids are not ascending is rejected
+    hdr = 17 + 256 * 128 * 4 + 4 + 32 * 128 * 4 + 32 * 8
+    lens = np.frombuffer(raw[hdr - 32 * 8:hdr], "<u8")
+    l0 = int(np.argmax(lens >= 2))
+    e0 = hdr + int(lens[:l0].sum()) * (4 + m)
+    swapped = bytearray(raw)
+    swapped[e0:e0 + 4], swapped[e0 + 12:e0 + 16] = raw[e0 + 12:e0 + 16], raw[e0:e0 + 4]
+    (tmp_path / "s.pqrr").write_bytes(bytes(swapped))
+    with pytest.raises(ValueError, match="corrupt file"):
+        pq.load_ivf_index(tmp_path / "s.pqrr")
+
+
+def test_adc_index_file_round_trip(pq, golden_adc, tmp_path):
+    from oracle import storage_py as S
+
+    g = golden_adc
+    m, mp, kp, k = int(g["m"]), int(g["mprime"]), int(g["kprime"]), int(g["k"])
+    P, R = pqobj(pq, g["books"], m), pq.RefineQuantizer(pqobj(pq, g["rbooks"], mp))
+    ix = pq.adc_build(P, g["base"])
+    codes = pq.refine_encode(ix, R, g["base"])
+    f = tmp_path / "adc.pqrr"
+    pq.save_adc_index(ix, R, codes, f)
+    raw = f.read_bytes()
+    assert raw == S.adc_file(g["books"], 128, m, 256, g["codes"], g["rbooks"], mp, g["rcodes"])
+    assert pq.probe_index_kind(f) == pq.IndexKind.adc
+    L = pq.load_adc_index(f)
+    np.testing.assert_array_equal(L.index.codes, g["codes"])
+    np.testing.assert_array_equal(L.refine_codes.bytes, g["rcodes"])
+    fi, fd, _ = L.index.search(g["queries"], kp, k)
+    np.testing.assert_array_equal(fi, g["rr_ids"])
+    np.testing.assert_array_equal(bits(fd), bits(g["rr_dists"]))
+    (tmp_path / "t.pqrr").write_bytes(raw[:-1])
+    with pytest.raises(ValueError, match="corrupt file"):
+        pq.load_adc_index(tmp_path / "t.pqrr")
+    with pytest.raises(ValueError, match="not an ADC index"):
+        ivf = pq.ivf_build(pq.Codebook(np.ones((2, 128), np.float32)), P, g["base"][:100])
+        pq.save_adc_index(ivf, None, None, tmp_path / "x.pqrr")

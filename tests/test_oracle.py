@@ -267,3 +267,63 @@ def test_spec_adc_full_sort_and_shortlist_bound(oracle, golden_adc):
         r1 = np.mean(ri[:, 0] == gt)
         rk = np.mean([gt[q] in sl[q] for q in range(len(qf))])
         assert r1 <= rk
+
+
+# ------------------------------------------------------------------ PQRR container (host code)
+def test_quantizer_file_bytes_and_corruption(pq, tmp_path, golden_ivf):
+    """storage.cu save/load_quantizer (host-only, no GPU) vs the independent
+    restatement oracle/storage_py.py: identical bytes, exact round trip, and
+    "corrupt file" on truncated / oversized / bad-magic / bad-version input."""
+    from oracle import storage_py as S
+
+    g = golden_ivf
+    P = pq.ProductQuantizer(128, 8, 256, g["books"].reshape(8, 256, 16))
+    f = tmp_path / "pq.pqrr"
+    pq.save_quantizer(P, f)
+    raw = f.read_bytes()
+    assert raw == S.quantizer_block(g["books"], 128, 8, 256)
+    assert len(raw) == 4 + 1 + 12 + 256 * 128 * 4
+    P2 = pq.load_quantizer(f)
+    assert (P2.d, P2.m, P2.ks) == (128, 8, 256)
+    np.testing.assert_array_equal(bits(P2.books), bits(P.books))
+    pq.save_quantizer(P2, tmp_path / "again.pqrr")  # determinism: same bytes
+    assert (tmp_path / "again.pqrr").read_bytes() == raw
+    cb = pq.Codebook(g["coarse"])
+    pq.save_codebook(cb, tmp_path / "cb.pqrr")
+    assert (tmp_path / "cb.pqrr").read_bytes() == S.quantizer_block(g["coarse"], 128, 1, 32)
+    np.testing.assert_array_equal(pq.load_codebook(tmp_path / "cb.pqrr").centroids, g["coarse"])
+    with pytest.raises(ValueError, match="corrupt file"):
+        pq.load_codebook(f)  # m = 8: not a plain codebook
+    bad = {"trunc": raw[:-1], "long": raw + b"\0", "magic": b"PQRS" + raw[4:],
+           "version": raw[:4] + b"\x02" + raw[5:], "empty": b"", "dims": raw[:5] +
+           np.array([128, 7, 256], "<u4").tobytes() + raw[17:]}
+    for name, b in bad.items():
+        p = tmp_path / f"{name}.pqrr"
+        p.write_bytes(b)
+        with pytest.raises(ValueError, match="corrupt file"):
+            pq.load_quantizer(p)
+        with pytest.raises(ValueError, match="corrupt file"):
+            S.read_quantizer(b)
+    with pytest.raises(Exception, match="cannot open"):
+        pq.load_quantizer(tmp_path / "missing.pqrr")
+
+
+def test_probe_index_kind_host(pq, tmp_path, golden_ivf, golden_adc):
+    """storage.hpp:59-62 on files written by the restatement (no GPU)."""
+    from oracle import storage_py as S
+
+    g, a = golden_ivf, golden_adc
+    ivf = S.ivf_file(g["books"], 128, 8, 256, g["coarse"], g["offsets"], g["ids_l"],
+                     g["codes"][g["ids_l"]], g["rbooks"], 16, g["rcodes"])
+    adc = S.adc_file(a["books"], 128, 8, 256, a["codes"], a["rbooks"], 8, a["rcodes"])
+    for name, b, kind in [("ivf", ivf, pq.IndexKind.ivf), ("adc", adc, pq.IndexKind.adc),
+                          ("ivf0", S.ivf_file(g["books"], 128, 8, 256, g["coarse"], g["offsets"],
+                                               g["ids_l"], g["codes"][g["ids_l"]]),
+                           pq.IndexKind.ivf),
+                          ("adc0", S.adc_file(a["books"], 128, 8, 256, a["codes"]), pq.IndexKind.adc)]:
+        p = tmp_path / f"{name}.pqrr"
+        p.write_bytes(b)
+        assert pq.probe_index_kind(p) == kind
+        p.write_bytes(b[:-3])
+        with pytest.raises(ValueError, match="corrupt file"):
+            pq.probe_index_kind(p)
