@@ -137,6 +137,12 @@ int pqrr_dev_index_get_info(pqrr_dev_index* ix, pqrr_dev_index_info* out);
 int pqrr_dev_export_lists(pqrr_dev_index* ix, uint64_t* offsets, uint32_t* ids, uint8_t* codes,
                           uint8_t* rcodes);
 
+/* The lists `lists[0..nl)` only (e.g. the probed lists of a query sample, for
+ * an oracle check at 1B without exporting the index): offsets[nl + 1] (always
+ * filled), then ids / codes / rcodes of each list id-ascending (NULL = skip). */
+int pqrr_dev_export_lists_subset(pqrr_dev_index* ix, const uint32_t* lists, uint32_t nl,
+                                 uint64_t* offsets, uint32_t* ids, uint8_t* codes,
+                                 uint8_t* rcodes);
 /* Trained parameters held by the index (coarse[c*d], books[ks*d],
  * rbooks[ks*d] when mprime > 0; any may be NULL). */
 int pqrr_dev_export_codebooks(pqrr_dev_index* ix, float* coarse, float* books, float* rbooks);

@@ -408,18 +408,32 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
         const ulonglong2* bk128 = reinterpret_cast<const ulonglong2*>(bk);
         u64 xa[CH], xb[CH];  // residual chunk halves (t, t+1) / (t+2, t+3)
         uint32_t cur_r = 0xffffffffu;
+        // software pipeline: positions run two iterations ahead, codes one
+        // (the random 8-byte code gathers are the kernel's long-latency loads)
+        u64 ncode[U];
         fetch(warp * 4 * U);
-        for (uint32_t base = warp * 4 * U; base < n; base += STEP) {
-            uint32_t pos[U], rr[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                pos[u] = npos[u];
-                rr[u] = nr[u];
-            }
-            if (base + STEP < n) fetch(base + STEP);
+        for (int u = 0; u < U; ++u) ncode[u] = __ldg(codes + npos[u]);
+        uint32_t cpos_r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) cpos_r[u] = nr[u];
+        if (warp * 4 * U + STEP < n) fetch(warp * 4 * U + STEP);
+        for (uint32_t base = warp * 4 * U; base < n; base += STEP) {
+            uint32_t rr[U];
             u64 code[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) code[u] = __ldg(codes + pos[u]);
+            for (int u = 0; u < U; ++u) {
+                code[u] = ncode[u];
+                rr[u] = cpos_r[u];
+            }
+            if (base + STEP < n) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    ncode[u] = __ldg(codes + npos[u]);
+                    cpos_r[u] = nr[u];
+                }
+                if (base + 2 * STEP < n) fetch(base + 2 * STEP);
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const uint32_t i = base + u * 4 + slot;

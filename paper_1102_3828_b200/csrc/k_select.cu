@@ -665,27 +665,60 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
     const uint32_t cpq = (stride + 31) / 32;
     const size_t total = nq * (size_t)cpq;
     const size_t tw = (size_t)gridDim.x * RC_WARPS;
-    for (size_t ch = (size_t)blockIdx.x * RC_WARPS + warp; ch < total; ch += tw) {
-        const size_t q = ch / cpq;
-        const uint32_t i0 = (uint32_t)(ch % cpq) * 32;
-        const uint32_t n = sl_cnt[q];
-        if (i0 >= n) continue;
-        const uint32_t nb = min(32u, n - i0);
+    // chunk metadata (id, list, code, refinement code) is prefetched into
+    // registers one chunk ahead: its dependent gather chain (position ->
+    // block list / codes / refinement codes) overlaps the current chunk
+    constexpr int RCV = MP % 16 == 0 ? MP / 16 : 1;
+    auto next_valid = [&](size_t c) -> size_t {
+        for (; c < total; c += tw)
+            if ((uint32_t)(c % cpq) * 32 < sl_cnt[c / cpq]) break;
+        return c;
+    };
+    uint32_t p_id = 0, p_list = 0;
+    u64 p_code = 0;
+    uint4 p_rc[RCV];
+    auto prefetch = [&](size_t c) {
+        const size_t q = c / cpq;
+        const uint32_t i0 = (uint32_t)(c % cpq) * 32;
+        const uint32_t nb = min(32u, sl_cnt[q] - i0);
         const size_t t0 = q * stride + i0;
         if ((uint32_t)lane < nb) {
             const uint32_t pos = sl_pos[t0 + lane];
-            rid[t0 + lane] = key_id(sl_key[t0 + lane]);
-            m_list[lane] = block_list[pos >> 4];
-            m_code[lane] = *reinterpret_cast<const u64*>(codes + (size_t)pos * 8);
+            p_id = key_id(sl_key[t0 + lane]);
+            p_list = block_list[pos >> 4];
+            p_code = *reinterpret_cast<const u64*>(codes + (size_t)pos * 8);
             if constexpr (MP % 16 == 0) {
                 const uint4* rsrc = reinterpret_cast<const uint4*>(rcodes + (size_t)pos * MP);
 #pragma unroll
-                for (int v = 0; v < MP / 16; ++v) reinterpret_cast<uint4*>(m_rcode + lane * MP)[v] = rsrc[v];
+                for (int v = 0; v < RCV; ++v) p_rc[v] = rsrc[v];
             } else {
-                *reinterpret_cast<u64*>(m_rcode + lane * MP) =
-                    *reinterpret_cast<const u64*>(rcodes + (size_t)pos * MP);
+                const u64 r = *reinterpret_cast<const u64*>(rcodes + (size_t)pos * MP);
+                p_rc[0] = make_uint4((uint32_t)r, (uint32_t)(r >> 32), 0u, 0u);
             }
         }
+    };
+    size_t nch = next_valid((size_t)blockIdx.x * RC_WARPS + warp);
+    if (nch < total) prefetch(nch);
+    for (size_t ch = nch; ch < total; ch = nch) {
+        const size_t q = ch / cpq;
+        const uint32_t i0 = (uint32_t)(ch % cpq) * 32;
+        const uint32_t n = sl_cnt[q];
+        const uint32_t nb = min(32u, n - i0);
+        const size_t t0 = q * stride + i0;
+        __syncwarp();  // the previous chunk's metadata reads are done
+        if ((uint32_t)lane < nb) {
+            rid[t0 + lane] = p_id;
+            m_list[lane] = p_list;
+            m_code[lane] = p_code;
+            if constexpr (MP % 16 == 0) {
+#pragma unroll
+                for (int v = 0; v < RCV; ++v) reinterpret_cast<uint4*>(m_rcode + lane * MP)[v] = p_rc[v];
+            } else {
+                *reinterpret_cast<u64*>(m_rcode + lane * MP) = ((u64)p_rc[0].y << 32) | p_rc[0].x;
+            }
+        }
+        nch = next_valid(ch + tw);
+        if (nch < total) prefetch(nch);
         const float4 x = reinterpret_cast<const float4*>(xq + q * D)[g];
         __syncwarp();
         // shortlists arrive grouped by inverted list (the filter emits per

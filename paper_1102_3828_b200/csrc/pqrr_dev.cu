@@ -635,7 +635,10 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     const uint32_t cap_mul = filter_ok ? 8 : 4;
     const uint32_t cap = std::max<uint32_t>(8192, ((cap_mul * kprime + 1023) / 1024) * 1024) << cap_shift;
     // sample density: ~64 samples expected below the alpha*k'-th distance
-    uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / 64.0));
+    // tuning hook (read per search): expected samples below the target rank
+    const char* spq_env = getenv("PQRR_SAMPLES");
+    const double spq = spq_env ? std::max(1.0, atof(spq_env)) : 64.0;
+    uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / spq));
     stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
     Workspace ws(s);
 
@@ -918,6 +921,13 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     }
 }
 
+// Target candidates per query = alpha * k' (the sampled threshold rank);
+// tuning hook PQRR_ALPHA (read per search).
+double default_alpha() {
+    const char* e = getenv("PQRR_ALPHA");
+    return e ? std::max(1.05, atof(e)) : 2.0;
+}
+
 void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t kprime_sz,
                    size_t k_sz, uint32_t* out_ids, float* out_dists, uint32_t* out_cnt) {
     if (w < 1 || w > ix.c) throw ArgError("v must satisfy 1 <= v <= c");
@@ -963,7 +973,7 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
         for (size_t c0 = 0; c0 < nq; c0 += chunk) {
             const size_t nc = std::min(chunk, nq - c0);
             ShortlistDev part{sl.key + c0 * kprime, sl.pos + c0 * kprime, sl.cnt + c0};
-            shortlist_core(ix, xq + c0 * ix.d, nc, w, kprime, k == 0, 2.0, 1, part, 0, true);
+            shortlist_core(ix, xq + c0 * ix.d, nc, w, kprime, k == 0, default_alpha(), 1, part, 0, true);
         }
     }
     if (k > 0) {
@@ -1591,6 +1601,51 @@ int pqrr_dev_reconstruct(pqrr_dev_index* h, const uint32_t* ids, size_t n, float
         count_launch();
         PQRR_CUDA(cudaMemcpyAsync(out, o, n * ix.d * 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pqrr_dev_export_lists_subset(pqrr_dev_index* h, const uint32_t* lists, uint32_t nl,
+                                 uint64_t* offsets, uint32_t* ids, uint8_t* codes,
+                                 uint8_t* rcodes) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        finalize(ix);
+        offsets[0] = 0;
+        for (uint32_t i = 0; i < nl; ++i) {
+            if (lists[i] >= ix.c) throw ArgError("list out of range");
+            offsets[i + 1] = offsets[i] + ix.h_len[lists[i]];
+        }
+        if (!ids && !codes && !rcodes) return;
+        const uint32_t m = ix.m, mp = ix.mprime;
+        std::vector<uint32_t> t_ids, perm;
+        std::vector<uint8_t> t_codes, t_rc;
+        for (uint32_t i = 0; i < nl; ++i) {
+            const uint32_t l = lists[i], len = ix.h_len[l];
+            const uint64_t o = ix.h_off[l];
+            if (!len) continue;
+            t_ids.resize(len);
+            t_codes.resize((size_t)len * m);
+            t_rc.resize((size_t)len * mp);
+            PQRR_CUDA(cudaMemcpy(t_ids.data(), ix.ids.p + o, (size_t)len * 4, cudaMemcpyDeviceToHost));
+            PQRR_CUDA(cudaMemcpy(t_codes.data(), ix.codes.p + o * m, (size_t)len * m,
+                                 cudaMemcpyDeviceToHost));
+            if (mp && rcodes)
+                PQRR_CUDA(cudaMemcpy(t_rc.data(), ix.rcodes.p + o * mp, (size_t)len * mp,
+                                     cudaMemcpyDeviceToHost));
+            // the device order inside a list is parity-paired: back to id order
+            perm.resize(len);
+            for (uint32_t r = 0; r < len; ++r) perm[r] = r;
+            std::sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) { return t_ids[a] < t_ids[b]; });
+            const uint64_t d0 = offsets[i];
+            for (uint32_t r = 0; r < len; ++r) {
+                const uint32_t sidx = perm[r];
+                if (ids) ids[d0 + r] = t_ids[sidx];
+                if (codes) std::memcpy(codes + (d0 + r) * m, &t_codes[(size_t)sidx * m], m);
+                if (rcodes && mp) std::memcpy(rcodes + (d0 + r) * mp, &t_rc[(size_t)sidx * mp], mp);
+            }
+        }
     });
 }
 

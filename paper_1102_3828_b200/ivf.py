@@ -316,6 +316,22 @@ class IvfIndex:
                                         rc.ctypes.data if rc is not None else None))
         return offs, ids, codes, rc
 
+    def export_lists_subset(self, lists):
+        """(offsets[len(lists)+1], ids, codes, rcodes or None) of the given lists,
+        each id-ascending (host copies of those lists only)."""
+        lists = np.ascontiguousarray(lists, np.uint32)
+        offs = np.zeros(len(lists) + 1, np.uint64)
+        check(lib.pqrr_dev_export_lists_subset(self.h, lists, len(lists), offs, None, None, None))
+        n = int(offs[-1])
+        mp = self.info()["mprime"]
+        ids = np.zeros(n, np.uint32)
+        codes = np.zeros((n, self.pq.m), np.uint8)
+        rc = np.zeros((n, mp), np.uint8) if mp else None
+        check(lib.pqrr_dev_export_lists_subset(self.h, lists, len(lists), offs, ids.ctypes.data,
+                                               codes.ctypes.data,
+                                               rc.ctypes.data if rc is not None else None))
+        return offs, ids, codes, rc
+
     def load_lists(self, offsets, ids, codes, rcodes=None) -> None:
         """Inverse of export_lists (an existing inverted file into an empty index)."""
         rc = None

@@ -648,3 +648,17 @@ def test_adc_index_file_round_trip(pq, golden_adc, tmp_path):
     with pytest.raises(ValueError, match="not an ADC index"):
         ivf = pq.ivf_build(pq.Codebook(np.ones((2, 128), np.float32)), P, g["base"][:100])
         pq.save_adc_index(ivf, None, None, tmp_path / "x.pqrr")
+
+
+def test_export_lists_subset(pq, golden_ivf):
+    g = golden_ivf
+    ix = pq.ivf_build(pq.Codebook(g["coarse"]), pqobj(pq, g["books"], 8), g["base"],
+                      rq=pq.RefineQuantizer(pqobj(pq, g["rbooks"], 16)))
+    offs, ids, codes, rc = ix.export_lists()
+    sub = np.array([5, 0, 31, 7], np.uint32)
+    so, si, sc, sr = ix.export_lists_subset(sub)
+    for i, l in enumerate(sub):
+        a, b = offs[l], offs[l + 1]
+        np.testing.assert_array_equal(si[so[i]:so[i + 1]], ids[a:b])
+        np.testing.assert_array_equal(sc[so[i]:so[i + 1]], codes[a:b])
+        np.testing.assert_array_equal(sr[so[i]:so[i + 1]], rc[a:b])
