@@ -103,27 +103,104 @@ __device__ __forceinline__ void append_direct(int slot, uint32_t pos, const int*
     }
 }
 
+// The scan of one item's entry range with NQD 16-slot quads per entry
+// (NQD = 4: 64 slots, 8 entries per warp step; 2: 32 slots, 16 entries; 1:
+// 16 slots, 32 entries).  The 5-bit LUT row always holds 4 16-byte quads;
+// quad c carries slot group c % NQD (replicated 4 / NQD times), and lane
+// L = 8p + 4h + c reads quad c for entry 2 (p (4 / NQD) + c / NQD) + h of the
+// step: the two lanes of a quarter warp that read the same quad position get
+// the two entries of a parity pair, so every LDS.128 stays conflict-free
+// exactly as in the 64-slot layout.
+template <int NQD>
+__device__ __forceinline__ void filter_scan(const FilterArgs& a, const uint4* __restrict__ lut8v,
+                                            const uint8_t* s_t, const int* s_q, const uint32_t* s_r,
+                                            uint32_t* s_nst, uint32_t* stage, const u64* codes,
+                                            uint32_t len, uint32_t off32, bool stage_ok) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = lane & 3, h = (lane >> 2) & 1, p = lane >> 3;
+    const int grp = c % NQD;  // the lane's slot group
+    const uint32_t eoff = 2 * (p * (4 / NQD) + c / NQD) + h;
+    constexpr uint32_t EPW = 32 / NQD;  // entries per warp step
+    const uint4 tb = reinterpret_cast<const uint4*>(s_t)[grp];
+    const uint4 th = make_uint4(tb.x | 0x80808080u, tb.y | 0x80808080u, tb.z | 0x80808080u,
+                                tb.w | 0x80808080u);
+    constexpr uint32_t S = FW * EPW;
+    const uint32_t wbase = warp * EPW;
+    u64 nA, nB, fA, fB;
+    {
+        const uint32_t e = wbase + eoff;
+        nA = e < len ? __ldg(codes + e) : 0ull;
+        nB = e + S < len ? __ldg(codes + e + S) : 0ull;
+        fA = e + 2 * S < len ? __ldg(codes + e + 2 * S) : 0ull;
+        fB = e + 3 * S < len ? __ldg(codes + e + 3 * S) : 0ull;
+    }
+    for (uint32_t wb = wbase; wb < len; wb += 2 * S) {
+        const uint32_t eA = wb + eoff, eB = eA + S;
+        const bool vA = eA < len, vB = eB < len;
+        const u64 cA = nA, cB = nB;
+        nA = fA;
+        nB = fB;
+        fA = eA + 4 * S < len ? __ldg(codes + eA + 4 * S) : 0ull;
+        fB = eB + 4 * S < len ? __ldg(codes + eB + 4 * S) : 0ull;
+        uint32_t a0 = 0u, a1 = 0u, a2 = 0u, a3 = 0u;
+        uint32_t b0 = 0u, b1 = 0u, b2 = 0u, b3 = 0u;
+        const uint32_t cAl = (uint32_t)cA, cAh = (uint32_t)(cA >> 32);
+        const uint32_t cBl = (uint32_t)cB, cBh = (uint32_t)(cB >> 32);
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            const uint32_t ca = ((j < 4 ? cAl : cAh) >> (8 * (j & 3))) & 0xffu;
+            const uint32_t cb = ((j < 4 ? cBl : cBh) >> (8 * (j & 3))) & 0xffu;
+            const uint4 va = lut8v[(j * KS + ca) * NSUB + c];
+            const uint4 vb = lut8v[(j * KS + cb) * NSUB + c];
+            a0 += va.x; a1 += va.y; a2 += va.z; a3 += va.w;
+            b0 += vb.x; b1 += vb.y; b2 += vb.z; b3 += vb.w;
+        }
+        // pass bits sit at bit 7 of each byte; gather them into one lane mask
+        // (bit 16 s + 4 t + b: step s, word t, byte b -> slot grp * 16 + 4 t
+        // + b).  (x >> 7) * 0x00204081 moves bits 0/8/16/24 to bits 21..24
+        // without carries.
+        auto m4 = [](uint32_t x) { return (((x >> 7) * 0x00204081u) >> 21) & 0xfu; };
+        const uint32_t mA = vA ? (m4(le_bytes(a0, tb.x, th.x)) | (m4(le_bytes(a1, tb.y, th.y)) << 4) |
+                                  (m4(le_bytes(a2, tb.z, th.z)) << 8) | (m4(le_bytes(a3, tb.w, th.w)) << 12))
+                               : 0u;
+        const uint32_t mB = vB ? (m4(le_bytes(b0, tb.x, th.x)) | (m4(le_bytes(b1, tb.y, th.y)) << 4) |
+                                  (m4(le_bytes(b2, tb.z, th.z)) << 8) | (m4(le_bytes(b3, tb.w, th.w)) << 12))
+                               : 0u;
+        uint32_t mask = mA | (mB << 16);
+        while (mask) {
+            const int bpos = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int sl = grp * 16 + (bpos & 15);
+            const uint32_t e = bpos < 16 ? eA : eB;
+            const uint32_t k = stage_ok ? atomicAdd(s_nst, 1u) : (uint32_t)STAGE;
+            if (k < (uint32_t)STAGE)
+                stage[k] = (e << 6) | (uint32_t)sl;
+            else
+                append_direct(sl, off32 + e, s_q, s_r, a);
+        }
+    }
+}
+
 __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
     extern __shared__ uint4 smem_f[];
     uint8_t* lut8 = reinterpret_cast<uint8_t*>(smem_f);  // [M][KS][FQ]
     const uint4* lut8v = smem_f;
-    __shared__ uint32_t s_item, s_any;
-    __shared__ int s_q[FQ];
-    __shared__ uint32_t s_r[FQ];
+    __shared__ uint32_t s_item, s_live;
+    __shared__ int s_q[FQ], s_q0[FQ];
+    __shared__ uint32_t s_r[FQ], s_r0[FQ];
     __shared__ __align__(16) uint8_t s_t[FQ];
-    __shared__ uint32_t s_mult[FQ], s_add[FQ];
+    __shared__ uint8_t s_t0[FQ];
+    __shared__ uint32_t s_mult[FQ], s_add[FQ], s_mult0[FQ], s_add0[FQ];
     __shared__ uint32_t s_nst, s_scnt[FQ], s_sbase[FQ];
     uint32_t* stage = reinterpret_cast<uint32_t*>(lut8 + LUT8_BYTES);
 
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int slot = lane >> 2, qd = lane & 3;
     const uint32_t n_items = *a.num_items;
 
     for (;;) {
         if (threadIdx.x == 0) {
             const uint32_t c = atomicAdd(a.item_counter, 1u);
             s_item = c < n_items ? a.item_order[c] : 0xffffffffu;
-            s_any = 0;
+            s_live = 0;
             s_nst = 0;
         }
         __syncthreads();
@@ -146,34 +223,66 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
                 sp = slot_params(a.tau[q], prm[0], prm[1], a.band_div);
                 if (a.pass_all) sp = {0u, 0u, 255u};
             }
-            s_q[t] = q;
-            s_r[t] = r;
-            s_mult[t] = sp.mult;
-            s_add[t] = sp.add;
-            s_t[t] = (uint8_t)sp.t;
-            if (sp.add == 0u) s_any = 1;
+            s_q0[t] = q;
+            s_r0[t] = r;
+            s_mult0[t] = sp.mult;
+            s_add0[t] = sp.add;
+            s_t0[t] = (uint8_t)sp.t;
+            // a 16-slot block is live when one of its queries can reach tau
+            if (sp.add == 0u) atomicOr(&s_live, 1u << (t / SUBQ));
         }
         __syncthreads();
-        if (!s_any) continue;  // no query of the item can have a candidate in this list
+        const uint32_t live = s_live;
+        if (!live) continue;  // no query of the item can have a candidate in this list
+        // live blocks, compacted: NQD = 1 / 2 quads when one / two blocks are
+        // live (dead blocks cost no lookups), else the 4 blocks as they are
+        const int nlive = __popc(live);
+        const int nqd = nlive == 1 ? 1 : (nlive == 2 ? 2 : 4);
+        int lb[NSUB];
+        {
+            int k = 0;
+#pragma unroll
+            for (int b = 0; b < NSUB; ++b) {
+                lb[b] = b;
+            }
+            if (nqd < 4) {
+#pragma unroll
+                for (int b = 0; b < NSUB; ++b)
+                    if (live & (1u << b)) lb[k++] = b;
+            }
+        }
+        if (threadIdx.x < FQ) {
+            const int t = threadIdx.x;
+            const int src = lb[(t / SUBQ) % nqd] * SUBQ + t % SUBQ;
+            s_q[t] = s_q0[src];
+            s_r[t] = s_r0[src];
+            s_mult[t] = s_mult0[src];
+            s_add[t] = s_add0[src];
+            s_t[t] = s_t0[src];
+        }
+        __syncthreads();
 
-        // ---- 5-bit LUT of the item from the LUT pass's 8-bit blocks
+        // ---- 5-bit LUT of the item from the LUT pass's 8-bit blocks; quad
+        // position c holds slot group c % nqd (source block lb[c % nqd])
         {
             const uint32_t nsub = (nqi + SUBQ - 1) / SUBQ;
-            const int sub = threadIdx.x & 3;  // fixed per thread (FT % 4 == 0)
+            const int sub = threadIdx.x & 3;  // quad position, fixed per thread (FT % 4 == 0)
+            const int grp = sub % nqd;
+            const int sblk = lb[grp];
             uint32_t mu[SUBQ], ad[SUBQ];
 #pragma unroll
             for (int i = 0; i < SUBQ; ++i) {
-                mu[i] = s_mult[sub * SUBQ + i];
-                ad[i] = s_add[sub * SUBQ + i];
+                mu[i] = s_mult[grp * SUBQ + i];
+                ad[i] = s_add[grp * SUBQ + i];
             }
-            const uint4* src = reinterpret_cast<const uint4*>(a.q8_cache + (size_t)(sub0 + sub) * Q8_BLOCK);
-            const bool live = (uint32_t)sub < nsub;
+            const uint4* src = reinterpret_cast<const uint4*>(a.q8_cache + (size_t)(sub0 + sblk) * Q8_BLOCK);
+            const bool lv = (uint32_t)sblk < nsub;
             constexpr int ROWS = M * KS;
             constexpr int PER = ROWS / (FT / 4);  // rows per thread
 #pragma unroll 4
             for (int i = 0; i < PER; ++i) {
                 const int row = (threadIdx.x >> 2) + i * (FT / 4);
-                uint4 v = live ? __ldg(src + row) : make_uint4(0, 0, 0, 0);
+                uint4 v = lv ? __ldg(src + row) : make_uint4(0, 0, 0, 0);
                 v.x = v5_of(v.x, mu + 0, ad + 0);
                 v.y = v5_of(v.y, mu + 4, ad + 4);
                 v.z = v5_of(v.z, mu + 8, ad + 8);
@@ -189,64 +298,12 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
         const uint32_t off32 = (uint32_t)off;
         const bool stage_ok = len < (1u << 26);
         const u64* codes = reinterpret_cast<const u64*>(a.codes) + off;
-        const uint4 tb = reinterpret_cast<const uint4*>(s_t)[qd];
-        const uint4 th = make_uint4(tb.x | 0x80808080u, tb.y | 0x80808080u, tb.z | 0x80808080u,
-                                    tb.w | 0x80808080u);
-        constexpr uint32_t S = FW * 8;
-        const uint32_t wbase = warp * 8;
-        u64 nA, nB, fA, fB;
-        {
-            const uint32_t e = wbase + slot;
-            nA = e < len ? __ldg(codes + e) : 0ull;
-            nB = e + S < len ? __ldg(codes + e + S) : 0ull;
-            fA = e + 2 * S < len ? __ldg(codes + e + 2 * S) : 0ull;
-            fB = e + 3 * S < len ? __ldg(codes + e + 3 * S) : 0ull;
-        }
-        for (uint32_t wb = wbase; wb < len; wb += 2 * S) {
-            const uint32_t eA = wb + slot, eB = eA + S;
-            const bool vA = eA < len, vB = eB < len;
-            const u64 cA = nA, cB = nB;
-            nA = fA;
-            nB = fB;
-            fA = eA + 4 * S < len ? __ldg(codes + eA + 4 * S) : 0ull;
-            fB = eB + 4 * S < len ? __ldg(codes + eB + 4 * S) : 0ull;
-            uint32_t a0 = 0u, a1 = 0u, a2 = 0u, a3 = 0u;
-            uint32_t b0 = 0u, b1 = 0u, b2 = 0u, b3 = 0u;
-            const uint32_t cAl = (uint32_t)cA, cAh = (uint32_t)(cA >> 32);
-            const uint32_t cBl = (uint32_t)cB, cBh = (uint32_t)(cB >> 32);
-#pragma unroll
-            for (int j = 0; j < M; ++j) {
-                const uint32_t ca = ((j < 4 ? cAl : cAh) >> (8 * (j & 3))) & 0xffu;
-                const uint32_t cb = ((j < 4 ? cBl : cBh) >> (8 * (j & 3))) & 0xffu;
-                const uint4 va = lut8v[(j * KS + ca) * NSUB + qd];
-                const uint4 vb = lut8v[(j * KS + cb) * NSUB + qd];
-                a0 += va.x; a1 += va.y; a2 += va.z; a3 += va.w;
-                b0 += vb.x; b1 += vb.y; b2 += vb.z; b3 += vb.w;
-            }
-            // pass bits sit at bit 7 of each byte; gather them into one lane mask
-            // (bit 16 s + 4 t + b: step s, word t, byte b -> query slot
-            // qd * 16 + 4 t + b).  (x >> 7) * 0x00204081 moves bits 0/8/16/24 to
-            // bits 21..24 without carries.
-            auto m4 = [](uint32_t x) { return (((x >> 7) * 0x00204081u) >> 21) & 0xfu; };
-            const uint32_t mA = vA ? (m4(le_bytes(a0, tb.x, th.x)) | (m4(le_bytes(a1, tb.y, th.y)) << 4) |
-                                      (m4(le_bytes(a2, tb.z, th.z)) << 8) | (m4(le_bytes(a3, tb.w, th.w)) << 12))
-                                   : 0u;
-            const uint32_t mB = vB ? (m4(le_bytes(b0, tb.x, th.x)) | (m4(le_bytes(b1, tb.y, th.y)) << 4) |
-                                      (m4(le_bytes(b2, tb.z, th.z)) << 8) | (m4(le_bytes(b3, tb.w, th.w)) << 12))
-                                   : 0u;
-            uint32_t mask = mA | (mB << 16);
-            while (mask) {
-                const int bpos = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int sl = qd * 16 + (bpos & 15);
-                const uint32_t e = bpos < 16 ? eA : eB;
-                const uint32_t k = stage_ok ? atomicAdd(&s_nst, 1u) : (uint32_t)STAGE;
-                if (k < (uint32_t)STAGE)
-                    stage[k] = (e << 6) | (uint32_t)sl;
-                else
-                    append_direct(sl, off32 + e, s_q, s_r, a);
-            }
-        }
+        if (nqd == 1)
+            filter_scan<1>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, codes, len, off32, stage_ok);
+        else if (nqd == 2)
+            filter_scan<2>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, codes, len, off32, stage_ok);
+        else
+            filter_scan<4>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, codes, len, off32, stage_ok);
         // ---- flush the staged candidates grouped by slot
         if (threadIdx.x < FQ) s_scnt[threadIdx.x] = 0;
         __syncthreads();

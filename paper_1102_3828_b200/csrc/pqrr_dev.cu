@@ -566,9 +566,20 @@ struct ItemSet {
 // Pairs (list, pair id) sorted by list, per-list pair counts / first pair, and
 // the per-list item counts + offsets for items of <= qt queries.  `share`
 // reuses another set's sorted pairs (same pairs, different qt).
+// Sort key of a pair: (list, probe rank).  Within a list the pairs are
+// ordered by the query's probe rank, so the near probes (where a query's
+// shortlist lives) fill the first 16-query blocks and the far probes, which
+// rarely reach the threshold, the last ones: K4f then skips whole dead
+// blocks (ivf_filter_kernel).
+__global__ void pair_key_kernel(const uint32_t* __restrict__ lists, const uint32_t* __restrict__ pair_ids,
+                                size_t np, uint32_t w, int wbits, uint32_t* __restrict__ key) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < np) key[i] = (lists[i] << wbits) | (pair_ids[i] % w);
+}
+
 ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_ids, size_t np,
                      uint32_t c, const uint32_t* list_len, uint32_t qt, cudaStream_t s,
-                     const ItemSet* share = nullptr, uint32_t chunk = 1u << 30) {
+                     const ItemSet* share = nullptr, uint32_t chunk = 1u << 30, uint32_t w = 1) {
     ItemSet it;
     it.c = c;
     it.qt = qt;
@@ -578,9 +589,18 @@ ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_
         it.list_cnt = share->list_cnt;
         it.list_first = share->list_first;
     } else {
-        uint32_t* sorted_lists = ws.alloc<uint32_t>(np);
+        uint32_t* sorted_keys = ws.alloc<uint32_t>(np);
         it.pair_sorted = ws.alloc<uint32_t>(np);
-        sort_pairs(lists, sorted_lists, pair_ids, it.pair_sorted, np, bits_for(c), s);
+        const int wbits = w > 1 ? bits_for(w) : 0;
+        if (wbits && bits_for(c) + wbits <= 32) {
+            uint32_t* key = ws.alloc<uint32_t>(np);
+            pair_key_kernel<<<nblk(np), 256, 0, s>>>(lists, pair_ids, np, w, wbits, key);
+            PQRR_LAUNCH_CHECK();
+            count_launch();
+            sort_pairs(key, sorted_keys, pair_ids, it.pair_sorted, np, bits_for(c) + wbits, s);
+        } else {
+            sort_pairs(lists, sorted_keys, pair_ids, it.pair_sorted, np, bits_for(c), s);
+        }
         it.list_cnt = ws.zeros<uint32_t>(c + 1);
         launch_histogram(lists, np, c, it.list_cnt, s);
         it.list_first = ws.alloc<uint32_t>(c + 1);
@@ -672,7 +692,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // LUT pass (and the exact scan), 64-query items for the K4f filter
     uint32_t* pair_ids = ws.alloc<uint32_t>(P);
     launch_iota(pair_ids, P, s);
-    ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s);
+    ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w);
     // small batches (few query-list pairs per SM): K4f items split long lists
     // into chunks so one list does not serialise on one SM
     const uint32_t fchunk = P < (size_t)64 * sm_count() ? 16384u : (1u << 30);
