@@ -566,20 +566,32 @@ struct ItemSet {
 // Pairs (list, pair id) sorted by list, per-list pair counts / first pair, and
 // the per-list item counts + offsets for items of <= qt queries.  `share`
 // reuses another set's sorted pairs (same pairs, different qt).
-// Sort key of a pair: (list, probe rank).  Within a list the pairs are
-// ordered by the query's probe rank, so the near probes (where a query's
-// shortlist lives) fill the first 16-query blocks and the far probes, which
-// rarely reach the threshold, the last ones: K4f then skips whole dead
-// blocks (ivf_filter_kernel).
+// Sort key of a pair (q, l): (list, coarse-distance gap d(q, l) - d(q, l_0)
+// to the query's nearest probe, top 16 bits of its float pattern).  Within a
+// list the pairs are ordered by that gap, so the pairs likely to reach the
+// query's threshold (small gap) fill the first 16-query blocks and the others
+// the last ones: K4f then skips whole dead blocks (ivf_filter_kernel).  The
+// order affects only speed (every ranking is by (dist, id)).  D holds the
+// coarse distances (approximate on the tensor-core path: fine for a sort).
 __global__ void pair_key_kernel(const uint32_t* __restrict__ lists, const uint32_t* __restrict__ pair_ids,
-                                size_t np, uint32_t w, int wbits, uint32_t* __restrict__ key) {
+                                size_t np, uint32_t w, const float* __restrict__ D, uint32_t c,
+                                uint32_t* __restrict__ key) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < np) key[i] = (lists[i] << wbits) | (pair_ids[i] % w);
+    if (i >= np) return;
+    const uint32_t p = pair_ids[i];
+    const size_t q = p / w;
+    const float gap = fmaxf(__fsub_rn(D[q * c + lists[i]], D[q * c + lists[q * w]]), 0.f);
+    // the sampling tier of the probe rank first (a 16-query block then shares
+    // one sampling stride in the LUT pass), then the gap (bits 30..17 of a
+    // non-negative float: 14 bits, monotone)
+    const uint32_t tier = sample_tier(p % w, w, 1);
+    key[i] = (lists[i] << 16) | (tier << 14) | (__float_as_uint(gap) >> 17);
 }
 
 ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_ids, size_t np,
                      uint32_t c, const uint32_t* list_len, uint32_t qt, cudaStream_t s,
-                     const ItemSet* share = nullptr, uint32_t chunk = 1u << 30, uint32_t w = 1) {
+                     const ItemSet* share = nullptr, uint32_t chunk = 1u << 30, uint32_t w = 1,
+                     const float* D = nullptr) {
     ItemSet it;
     it.c = c;
     it.qt = qt;
@@ -591,13 +603,12 @@ ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_
     } else {
         uint32_t* sorted_keys = ws.alloc<uint32_t>(np);
         it.pair_sorted = ws.alloc<uint32_t>(np);
-        const int wbits = w > 1 ? bits_for(w) : 0;
-        if (wbits && bits_for(c) + wbits <= 32) {
+        if (D && bits_for(c) <= 16) {
             uint32_t* key = ws.alloc<uint32_t>(np);
-            pair_key_kernel<<<nblk(np), 256, 0, s>>>(lists, pair_ids, np, w, wbits, key);
+            pair_key_kernel<<<nblk(np), 256, 0, s>>>(lists, pair_ids, np, w, D, c, key);
             PQRR_LAUNCH_CHECK();
             count_launch();
-            sort_pairs(key, sorted_keys, pair_ids, it.pair_sorted, np, bits_for(c) + wbits, s);
+            sort_pairs(key, sorted_keys, pair_ids, it.pair_sorted, np, 16 + bits_for(c), s);
         } else {
             sort_pairs(lists, sorted_keys, pair_ids, it.pair_sorted, np, bits_for(c), s);
         }
@@ -692,7 +703,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // LUT pass (and the exact scan), 64-query items for the K4f filter
     uint32_t* pair_ids = ws.alloc<uint32_t>(P);
     launch_iota(pair_ids, P, s);
-    ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w);
+    ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w, D);
     // small batches (few query-list pairs per SM): K4f items split long lists
     // into chunks so one list does not serialise on one SM
     const uint32_t fchunk = P < (size_t)64 * sm_count() ? 16384u : (1u << 30);

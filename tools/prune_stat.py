@@ -18,7 +18,8 @@ coarse, P, rq = bench.train_codebooks(pq, cfg, 0)
 ix, _, _ = bench.build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
 q = pq.synth(3, 0, args.nq, cfg["clusters"], seed=bench.SEED)
 ids, d, c = ix.search(q, cfg["w"], cfg["kprime"], 0)
-probes, _ = Oracle().coarse_probe(coarse.centroids, q.astype(np.float32), cfg["w"])
+probes, pdist = Oracle().coarse_probe(coarse.centroids, q.astype(np.float32), cfg["w"])
+feat = []  # (live, rank, gap, ratio, sum_m - d_coarse)
 offs, _, _, _ = ix.export_lists_subset(np.arange(cfg["kc"], dtype=np.uint32))
 lens = np.diff(offs).astype(np.int64)
 tot_pairs = tot_entries = skip_pairs = skip_entries = 0
@@ -31,6 +32,8 @@ for i in range(args.nq):
         sm = np.float32(0)
         for j in range(cfg["m"]):
             sm = np.float32(sm + lut.values[j].min())
+        feat.append((sm <= tau, r, pdist[i, r] - pdist[i, 0], pdist[i, r] / max(pdist[i, 0], 1e-9),
+                     pdist[i, r] / tau))
         tot_pairs += 1
         tot_entries += lens[l]
         if sm > tau:
@@ -39,3 +42,18 @@ for i in range(args.nq):
             by_rank[r] += 1
 print(args.config, f"pairs skippable {skip_pairs / tot_pairs:.3f}, entries {skip_entries / tot_entries:.3f}")
 print("skippable share by probe rank (per 8):", np.round(by_rank.reshape(-1, 8).mean(1) / args.nq, 2).tolist())
+
+f = np.array(feat, dtype=np.float64)
+live = f[:, 0] > 0
+
+
+def auc(score):  # P(score(live) < score(dead)): lower score should mean live
+    o = np.argsort(score, kind="stable")
+    rk = np.empty(len(score))
+    rk[o] = np.arange(len(score))
+    nl, nd = live.sum(), (~live).sum()
+    return 1 - (rk[live].sum() - nl * (nl - 1) / 2) / (nl * nd)
+
+
+for k, name in [(1, "rank"), (2, "gap d(q,l)-d(q,l0)"), (3, "ratio d(q,l)/d(q,l0)"), (4, "d(q,l)/tau")]:
+    print(f"AUC {name}: {auc(f[:, k]):.3f}")
