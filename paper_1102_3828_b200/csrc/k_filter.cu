@@ -402,6 +402,9 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
     float4* bk = smem_k;                      // [M][KS][CH], swizzled
     float4* res = smem_k + M * KS * CH;       // [w][d / 4], swizzled
     __shared__ uint32_t s_q, s_le;
+    // per-warp exchange of the 8 sub-space terms of 4 x 4 candidates:
+    // [round u][slot][j], rows of 36 floats (conflict-free writes and reads)
+    __shared__ __align__(16) float s_x[16][4 * 36];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = lane & 7, slot = lane >> 3;
     const uint32_t dch = d / 4;
@@ -519,15 +522,24 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
                 }
                 const u64 s01 = sa, s23 = sb;
                 const float Lj = __fadd_rn(__fadd_rn(lo2(s01), hi2(s01)), __fadd_rn(lo2(s23), hi2(s23)));
-                float acc = 0.f;
-#pragma unroll
-                for (int jj = 0; jj < M; ++jj)
-                    acc = __fadd_rn(acc, __shfl_sync(0xffffffffu, Lj, (lane & ~7) | jj));
-                if (i < n && j == 0) {
+                (void)i;
+                s_x[warp][u * 36 + slot * 8 + j] = Lj;
+            }
+            __syncwarp();
+            // lane j < 4 of a quarter warp sums round u = j's 8 terms
+            // j-ascending (adc_distance, product_quantizer.hpp:53-57)
+            if (j < U) {
+                const float4 t0 = *reinterpret_cast<const float4*>(&s_x[warp][j * 36 + slot * 8]);
+                const float4 t1 = *reinterpret_cast<const float4*>(&s_x[warp][j * 36 + slot * 8 + 4]);
+                float acc = __fadd_rn(__fadd_rn(__fadd_rn(t0.x, t0.y), t0.z), t0.w);  // 0 + L0 == L0
+                acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, t1.x), t1.y), t1.z), t1.w);
+                const uint32_t i = base + j * 4 + slot;
+                if (i < n) {
                     cand_dist[q * cap + i] = acc;
                     le += acc <= tq ? 1u : 0u;
                 }
             }
+            __syncwarp();
         }
         if (le) atomicAdd(&s_le, le);
         __syncthreads();
@@ -573,7 +585,7 @@ bool recheck_smem_t(const float* xq, uint32_t d, const float* coarse, const floa
                     uint32_t cap, const uint32_t* cand_pos, float* cand_dist, const float* tau,
                     size_t nq, uint32_t* cand_le, cudaStream_t s) {
     const size_t smem = (size_t)M * KS * DSUB * sizeof(float) + (size_t)w * d * sizeof(float);
-    if (smem > 220 * 1024) return false;
+    if (smem > 216 * 1024) return false;  // + ~9.3 KiB static (s_x) <= 227 KiB
     PQRR_CUDA(cudaFuncSetAttribute(recheck_smem_kernel<DSUB>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     uint32_t* counter = nullptr;
