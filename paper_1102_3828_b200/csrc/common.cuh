@@ -95,4 +95,19 @@ __device__ __forceinline__ u64 nb_key(float dist, uint32_t id) {
 __device__ __forceinline__ float key_dist(u64 k) { return __uint_as_float((unsigned)(k >> 32)); }
 __device__ __forceinline__ uint32_t key_id(u64 k) { return (uint32_t)(k & 0xffffffffull); }
 
+// 8-bit LUT block of a LUT-pass item (K2 -> K4f): LANE-major, 16 query lanes
+// x (M * KS) row bytes, so K4f can copy any lane's 2 KiB column with
+// coalesced 16-byte loads.  r0..r3 hold rows 4 rq .. 4 rq + 3, each the bytes
+// of lanes 4 g .. 4 g + 3; a 4 x 4 byte transpose gives each lane's 4 rows.
+__device__ __forceinline__ void q8_put_rows(uint32_t* __restrict__ block, int g, int rq, uint32_t r0,
+                                            uint32_t r1, uint32_t r2, uint32_t r3) {
+    constexpr int LANE_WORDS = 8 * 256 / 4;  // one lane's column (M = 8, KS = 256)
+    const uint32_t lo01 = __byte_perm(r0, r1, 0x5140), hi01 = __byte_perm(r0, r1, 0x7362);
+    const uint32_t lo23 = __byte_perm(r2, r3, 0x5140), hi23 = __byte_perm(r2, r3, 0x7362);
+    block[(4 * g + 0) * LANE_WORDS + rq] = __byte_perm(lo01, lo23, 0x5410);
+    block[(4 * g + 1) * LANE_WORDS + rq] = __byte_perm(lo01, lo23, 0x7632);
+    block[(4 * g + 2) * LANE_WORDS + rq] = __byte_perm(hi01, hi23, 0x5410);
+    block[(4 * g + 3) * LANE_WORDS + rq] = __byte_perm(hi01, hi23, 0x7632);
+}
+
 }  // namespace pqrr_b200

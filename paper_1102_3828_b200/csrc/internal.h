@@ -198,6 +198,7 @@ struct FilterArgs {
     const uint32_t* list_first;  // first pair of each list in pair_sorted
     const uint32_t* sub_item_off;  // first 16-query item of each list
     const uint32_t* pair_sorted;
+    const uint32_t* live_pos;    // per list, the positions (into pair_sorted) of its live pairs
     uint32_t w;
     const float* tau;
     const uint8_t* q8_cache;
@@ -210,6 +211,14 @@ struct FilterArgs {
     float band_div;  // Delta target = (tau - sum of minima) / band_div
 };
 void launch_ivf_filter(const FilterArgs& a, cudaStream_t s);
+// Live-pair compaction before K4f: a pair (q, l) is live when its LUT's sum of
+// sub-table minima can reach tau_q (no entry of l is at or below tau_q
+// otherwise).  Writes, per list, the positions of its live pairs from
+// list_first[l] on (live_pos) and rewrites the 64-query K4f items
+// (item_start / item_nq) over the live pairs only.
+void launch_live_pairs(const FilterArgs& a, const uint32_t* list_cnt, uint32_t nlists,
+                       uint32_t* live_pos, uint32_t* live_cnt, const uint32_t* item_off,
+                       uint32_t* item_start, uint32_t* item_nq, uint32_t chunk, cudaStream_t s);
 // K4r: exact ADC distance of every filter candidate (reference order), and
 // the per-query count of candidates at or below tau.
 bool recheck_supported(uint32_t d, uint32_t m, uint32_t w);

@@ -69,6 +69,14 @@ __device__ __forceinline__ SlotParam slot_params(float tau, float sc, float summ
     return {mult, 0u, t >= 255.f ? 255u : (uint32_t)t};
 }
 
+// A pair can have a candidate (dist <= tau) only if sum_m <= tau (within the
+// roundings slot_params covers); the same test as slot_params' dead case.
+__device__ __forceinline__ bool pair_live(float tau, float summ) {
+    const float e_up = 1.000003814697265625f, e_dn = 0.999996185302734375f;  // 1 +- 2^-18
+    if (!(tau < __int_as_float(0x7f800000))) return true;
+    return __fsub_rn(__fmul_rn(tau, e_up), __fmul_rn(summ, e_dn)) >= 0.f;
+}
+
 // Four v8 bytes -> v5 bytes: min(31, (b * mult_b >> 8) + add_b).
 __device__ __forceinline__ uint32_t v5_of(uint32_t word, const uint32_t* mult, const uint32_t* add) {
     uint32_t out = 0;
@@ -103,6 +111,38 @@ __device__ __forceinline__ void append_direct(int slot, uint32_t pos, const int*
     }
 }
 
+// Writes the staged candidates (entry << 6 | slot) of the item to the
+// queries' buffers grouped by slot, so each (query, list) run is contiguous
+// (K4r keeps the run's residual in registers).  Block-wide; resets the stage.
+__device__ __forceinline__ void flush_stage(const FilterArgs& a, const uint32_t* stage, uint32_t* s_nst,
+                                            uint32_t* s_scnt, uint32_t* s_sbase, const int* s_q,
+                                            const uint32_t* s_r, uint32_t off32) {
+    if (threadIdx.x < FQ) s_scnt[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t nst = min(*s_nst, (uint32_t)STAGE);
+    for (uint32_t i = threadIdx.x; i < nst; i += FT) atomicAdd(&s_scnt[stage[i] & 63u], 1u);
+    __syncthreads();
+    if (threadIdx.x < FQ) {
+        const uint32_t cnt = s_scnt[threadIdx.x];
+        s_sbase[threadIdx.x] = cnt ? atomicAdd(a.cand_cnt + s_q[threadIdx.x], cnt) : 0u;
+        s_scnt[threadIdx.x] = 0;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nst; i += FT) {
+        const uint32_t v = stage[i];
+        const uint32_t sl = v & 63u;
+        const uint32_t o = s_sbase[sl] + atomicAdd(&s_scnt[sl], 1u);
+        if (o < a.cap) {
+            const size_t q = (size_t)s_q[sl];
+            a.cand_pos[q * a.cap + o] = off32 + (v >> 6);
+            a.cand_aux[q * a.cap + o] = s_r[sl];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *s_nst = 0;
+    __syncthreads();
+}
+
 // The scan of one item's entry range with NQD 16-slot quads per entry
 // (NQD = 4: 64 slots, 8 entries per warp step; 2: 32 slots, 16 entries; 1:
 // 16 slots, 32 entries).  The 5-bit LUT row always holds 4 16-byte quads;
@@ -114,8 +154,9 @@ __device__ __forceinline__ void append_direct(int slot, uint32_t pos, const int*
 template <int NQD>
 __device__ __forceinline__ void filter_scan(const FilterArgs& a, const uint4* __restrict__ lut8v,
                                             const uint8_t* s_t, const int* s_q, const uint32_t* s_r,
-                                            uint32_t* s_nst, uint32_t* stage, const u64* codes,
-                                            uint32_t len, uint32_t off32, bool stage_ok) {
+                                            uint32_t* s_nst, uint32_t* stage, uint32_t* s_scnt,
+                                            uint32_t* s_sbase, const u64* codes, uint32_t len,
+                                            uint32_t off32, bool stage_ok) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c = lane & 3, h = (lane >> 2) & 1, p = lane >> 3;
     const int grp = c % NQD;  // the lane's slot group
@@ -134,7 +175,13 @@ __device__ __forceinline__ void filter_scan(const FilterArgs& a, const uint4* __
         fA = e + 2 * S < len ? __ldg(codes + e + 2 * S) : 0ull;
         fB = e + 3 * S < len ? __ldg(codes + e + 3 * S) : 0ull;
     }
-    for (uint32_t wb = wbase; wb < len; wb += 2 * S) {
+    // every warp runs the same number of steps (entries past len are masked),
+    // so the stage can be flushed at block barriers every FLUSH_EVERY steps
+    // once it is half full (a dense item would overflow it otherwise)
+    constexpr uint32_t FLUSH_EVERY = 8;
+    const uint32_t nsteps = (len + 2 * S - 1) / (2 * S);
+    for (uint32_t step = 0; step < nsteps; ++step) {
+        const uint32_t wb = wbase + step * 2 * S;
         const uint32_t eA = wb + eoff, eB = eA + S;
         const bool vA = eA < len, vB = eB < len;
         const u64 cA = nA, cB = nB;
@@ -178,6 +225,10 @@ __device__ __forceinline__ void filter_scan(const FilterArgs& a, const uint4* __
             else
                 append_direct(sl, off32 + e, s_q, s_r, a);
         }
+        if (step % FLUSH_EVERY == FLUSH_EVERY - 1 && step + 1 < nsteps) {
+            __syncthreads();
+            if (*s_nst >= (uint32_t)STAGE / 2) flush_stage(a, stage, s_nst, s_scnt, s_sbase, s_q, s_r, off32);
+        }
     }
 }
 
@@ -185,12 +236,12 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
     extern __shared__ uint4 smem_f[];
     uint8_t* lut8 = reinterpret_cast<uint8_t*>(smem_f);  // [M][KS][FQ]
     const uint4* lut8v = smem_f;
-    __shared__ uint32_t s_item, s_live;
-    __shared__ int s_q[FQ], s_q0[FQ];
-    __shared__ uint32_t s_r[FQ], s_r0[FQ];
+    __shared__ uint32_t s_item;
+    __shared__ int s_q[FQ];
+    __shared__ uint32_t s_r[FQ];
     __shared__ __align__(16) uint8_t s_t[FQ];
-    __shared__ uint8_t s_t0[FQ];
-    __shared__ uint32_t s_mult[FQ], s_add[FQ], s_mult0[FQ], s_add0[FQ];
+    __shared__ uint32_t s_mult[FQ], s_add[FQ];
+    __shared__ uint64_t s_src[FQ];  // byte offset of the slot's lane column in q8_cache
     __shared__ uint32_t s_nst, s_scnt[FQ], s_sbase[FQ];
     uint32_t* stage = reinterpret_cast<uint32_t*>(lut8 + LUT8_BYTES);
 
@@ -200,97 +251,93 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
         if (threadIdx.x == 0) {
             const uint32_t c = atomicAdd(a.item_counter, 1u);
             s_item = c < n_items ? a.item_order[c] : 0xffffffffu;
-            s_live = 0;
             s_nst = 0;
         }
         __syncthreads();
         const uint32_t it = s_item;
         if (it == 0xffffffffu) break;
+        const uint32_t nqi = a.item_nq[it];
+        if (nqi == 0) {  // every pair of this item's group is dead (launch_live_pairs)
+            __syncthreads();  // all threads read s_item before thread 0 claims the next item
+            continue;
+        }
         const uint32_t l = a.item_list[it];
         const uint32_t start = a.item_start[it];
-        const uint32_t nqi = a.item_nq[it];
-        const uint32_t sub0 = a.sub_item_off[l] + (start - a.list_first[l]) / SUBQ;
         if (threadIdx.x < FQ) {
             const uint32_t t = threadIdx.x;
             int q = -1;
             uint32_t r = 0;
             SlotParam sp{0u, 31u, 0u};  // empty slot: dead
+            uint64_t src = 0;
             if (t < nqi) {
-                const uint32_t p = a.pair_sorted[start + t];
+                const uint32_t pos = a.live_pos[start + t];
+                const uint32_t li = pos - a.list_first[l];
+                const uint32_t blk = a.sub_item_off[l] + li / SUBQ, ln = li % SUBQ;
+                const uint32_t p = a.pair_sorted[pos];
                 q = (int)(p / a.w);
                 r = p % a.w;
-                const float* prm = a.q8_param + ((size_t)(sub0 + t / SUBQ) * SUBQ + t % SUBQ) * 2;
+                const float* prm = a.q8_param + ((size_t)blk * SUBQ + ln) * 2;
                 sp = slot_params(a.tau[q], prm[0], prm[1], a.band_div);
                 if (a.pass_all) sp = {0u, 0u, 255u};
+                src = (uint64_t)blk * Q8_BLOCK + (uint64_t)ln * (M * KS);
             }
-            s_q0[t] = q;
-            s_r0[t] = r;
-            s_mult0[t] = sp.mult;
-            s_add0[t] = sp.add;
-            s_t0[t] = (uint8_t)sp.t;
-            // a 16-slot block is live when one of its queries can reach tau
-            if (sp.add == 0u) atomicOr(&s_live, 1u << (t / SUBQ));
+            s_q[t] = q;
+            s_r[t] = r;
+            s_mult[t] = sp.mult;
+            s_add[t] = sp.add;
+            s_t[t] = (uint8_t)sp.t;
+            s_src[t] = src;
         }
         __syncthreads();
-        const uint32_t live = s_live;
-        if (!live) continue;  // no query of the item can have a candidate in this list
-        // live blocks, compacted: NQD = 1 / 2 quads when one / two blocks are
-        // live (dead blocks cost no lookups), else the 4 blocks as they are
-        const int nlive = __popc(live);
-        const int nqd = nlive == 1 ? 1 : (nlive == 2 ? 2 : 4);
-        int lb[NSUB];
-        {
-            int k = 0;
-#pragma unroll
-            for (int b = 0; b < NSUB; ++b) {
-                lb[b] = b;
-            }
-            if (nqd < 4) {
-#pragma unroll
-                for (int b = 0; b < NSUB; ++b)
-                    if (live & (1u << b)) lb[k++] = b;
-            }
-        }
-        if (threadIdx.x < FQ) {
-            const int t = threadIdx.x;
-            const int src = lb[(t / SUBQ) % nqd] * SUBQ + t % SUBQ;
-            s_q[t] = s_q0[src];
-            s_r[t] = s_r0[src];
-            s_mult[t] = s_mult0[src];
-            s_add[t] = s_add0[src];
-            s_t[t] = s_t0[src];
-        }
-        __syncthreads();
+        // NQD = 1 / 2 / 4 quads of 16 slots per entry (filter_scan)
+        const int nqd = nqi <= 16 ? 1 : (nqi <= 32 ? 2 : 4);
 
-        // ---- 5-bit LUT of the item from the LUT pass's 8-bit blocks; quad
-        // position c holds slot group c % nqd (source block lb[c % nqd])
+        // ---- 5-bit LUT of the item: the live slots' 8-bit lane columns
+        // (lane-major LUT-pass blocks, q8_put_rows) are staged 32 at a time in
+        // shared memory (2052-byte stride: conflict-free byte reads), then
+        // transposed into [j][code][quad] rows; quad position c holds slot
+        // group c % nqd
         {
-            const uint32_t nsub = (nqi + SUBQ - 1) / SUBQ;
-            const int sub = threadIdx.x & 3;  // quad position, fixed per thread (FT % 4 == 0)
-            const int grp = sub % nqd;
-            const int sblk = lb[grp];
-            uint32_t mu[SUBQ], ad[SUBQ];
+            uint8_t* colbuf = reinterpret_cast<uint8_t*>(stage);  // [32][2052]
+            uint32_t* colw = stage;
+            constexpr int CST = M * KS + 4;  // bytes per staged column
+            const int nsl = 16 * nqd;
+            for (int h = 0; 32 * h < nsl; ++h) {
+                const int ns = min(32, nsl - 32 * h);
+                for (int x = threadIdx.x; x < ns * (M * KS / 16); x += FT) {
+                    const int sl = x / (M * KS / 16), ch = x % (M * KS / 16);
+                    if ((uint32_t)(32 * h + sl) < nqi) {
+                        const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.q8_cache + s_src[32 * h + sl]) + ch);
+                        uint32_t* d = colw + sl * (CST / 4) + ch * 4;
+                        d[0] = v.x;
+                        d[1] = v.y;
+                        d[2] = v.z;
+                        d[3] = v.w;
+                    }
+                }
+                __syncthreads();
+                const int sq = threadIdx.x & 7;
+                if (4 * sq < ns) {
+                    const int s0 = 32 * h + 4 * sq;  // first slot of this thread's word
+                    uint32_t mu[4], ad[4];
 #pragma unroll
-            for (int i = 0; i < SUBQ; ++i) {
-                mu[i] = s_mult[grp * SUBQ + i];
-                ad[i] = s_add[grp * SUBQ + i];
-            }
-            const uint4* src = reinterpret_cast<const uint4*>(a.q8_cache + (size_t)(sub0 + sblk) * Q8_BLOCK);
-            const bool lv = (uint32_t)sblk < nsub;
-            constexpr int ROWS = M * KS;
-            constexpr int PER = ROWS / (FT / 4);  // rows per thread
-#pragma unroll 4
-            for (int i = 0; i < PER; ++i) {
-                const int row = (threadIdx.x >> 2) + i * (FT / 4);
-                uint4 v = lv ? __ldg(src + row) : make_uint4(0, 0, 0, 0);
-                v.x = v5_of(v.x, mu + 0, ad + 0);
-                v.y = v5_of(v.y, mu + 4, ad + 4);
-                v.z = v5_of(v.z, mu + 8, ad + 8);
-                v.w = v5_of(v.w, mu + 12, ad + 12);
-                reinterpret_cast<uint4*>(lut8)[row * NSUB + sub] = v;
+                    for (int k = 0; k < 4; ++k) {
+                        mu[k] = s_mult[s0 + k];
+                        ad[k] = s_add[s0 + k];
+                    }
+                    const int quad = s0 / 16, byte0 = s0 % 16;
+                    for (int row = threadIdx.x >> 3; row < M * KS; row += FT / 8) {
+                        const uint8_t* cb = colbuf + (4 * sq) * CST + row;
+                        const uint32_t word = (uint32_t)cb[0] | ((uint32_t)cb[CST] << 8) |
+                                              ((uint32_t)cb[2 * CST] << 16) | ((uint32_t)cb[3 * CST] << 24);
+                        const uint32_t v5 = v5_of(word, mu, ad);
+                        for (int c = quad; c < NSUB; c += nqd)
+                            *reinterpret_cast<uint32_t*>(lut8 + row * FQ + c * 16 + byte0) = v5;
+                    }
+                }
+                __syncthreads();
             }
         }
-        __syncthreads();
 
         const uint32_t ie0 = a.item_e0[it];
         const uint64_t off = a.list_off[l] + ie0;  // this item's entry range [e0, e1)
@@ -299,34 +346,14 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
         const bool stage_ok = len < (1u << 26);
         const u64* codes = reinterpret_cast<const u64*>(a.codes) + off;
         if (nqd == 1)
-            filter_scan<1>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, codes, len, off32, stage_ok);
+            filter_scan<1>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, s_scnt, s_sbase, codes, len, off32, stage_ok);
         else if (nqd == 2)
-            filter_scan<2>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, codes, len, off32, stage_ok);
+            filter_scan<2>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, s_scnt, s_sbase, codes, len, off32, stage_ok);
         else
-            filter_scan<4>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, codes, len, off32, stage_ok);
-        // ---- flush the staged candidates grouped by slot
-        if (threadIdx.x < FQ) s_scnt[threadIdx.x] = 0;
+            filter_scan<4>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, s_scnt, s_sbase, codes, len, off32, stage_ok);
+        // ---- flush the remaining staged candidates
         __syncthreads();
-        const uint32_t nst = min(s_nst, (uint32_t)STAGE);
-        for (uint32_t i = threadIdx.x; i < nst; i += FT) atomicAdd(&s_scnt[stage[i] & 63u], 1u);
-        __syncthreads();
-        if (threadIdx.x < FQ) {
-            const uint32_t cnt = s_scnt[threadIdx.x];
-            s_sbase[threadIdx.x] = cnt ? atomicAdd(a.cand_cnt + s_q[threadIdx.x], cnt) : 0u;
-            s_scnt[threadIdx.x] = 0;
-        }
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < nst; i += FT) {
-            const uint32_t v = stage[i];
-            const uint32_t sl = v & 63u;
-            const uint32_t o = s_sbase[sl] + atomicAdd(&s_scnt[sl], 1u);
-            if (o < a.cap) {
-                const size_t q = (size_t)s_q[sl];
-                a.cand_pos[q * a.cap + o] = off32 + (v >> 6);
-                a.cand_aux[q * a.cap + o] = s_r[sl];
-            }
-        }
-        __syncthreads();
+        flush_stage(a, stage, &s_nst, s_scnt, s_sbase, s_q, s_r, off32);
     }
 }
 
@@ -564,12 +591,67 @@ void recheck_t(const float* xq, uint32_t d, const float* coarse, const float* bo
 
 }  // namespace
 
+// Per list (one warp): positions of the live pairs, compacted in list order.
+__global__ void live_pairs_kernel(const FilterArgs a, const uint32_t* __restrict__ list_cnt,
+                                  uint32_t nlists, uint32_t* __restrict__ live_pos,
+                                  uint32_t* __restrict__ live_cnt) {
+    const uint32_t l = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (l >= nlists) return;
+    const uint32_t n = list_cnt[l], f = a.list_first[l], b0 = a.sub_item_off[l];
+    uint32_t o = 0;
+    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        bool live = false;
+        if (i < n) {
+            const uint32_t p = a.pair_sorted[f + i];
+            const float* prm = a.q8_param + ((size_t)(b0 + i / SUBQ) * SUBQ + i % SUBQ) * 2;
+            live = a.pass_all || pair_live(a.tau[p / a.w], prm[1]);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, live);
+        if (live) live_pos[f + o + __popc(bal & ((1u << lane) - 1u))] = f + i;
+        o += __popc(bal);
+    }
+    if (lane == 0) live_cnt[l] = o;
+}
+
+// The K4f items of a list (groups of FQ pairs x entry chunks, items_build
+// order) re-pointed at its live pairs; groups past the live count are empty.
+__global__ void live_items_kernel(const FilterArgs a, const uint32_t* __restrict__ list_cnt,
+                                  const uint32_t* __restrict__ live_cnt, uint32_t nlists,
+                                  const uint32_t* __restrict__ item_off, uint32_t* __restrict__ item_start,
+                                  uint32_t* __restrict__ item_nq, uint32_t chunk) {
+    const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= nlists) return;
+    const uint32_t c = list_cnt[l], lc = live_cnt[l], L = a.list_len[l];
+    const uint32_t chunks = max(1u, (L + chunk - 1) / chunk);
+    uint32_t o = item_off[l];
+    for (uint32_t g = 0; g < c; g += FQ)
+        for (uint32_t ch = 0; ch < chunks; ++ch, ++o) {
+            item_start[o] = a.list_first[l] + g;
+            item_nq[o] = g < lc ? min((uint32_t)FQ, lc - g) : 0u;
+        }
+}
+
 void launch_ivf_filter(const FilterArgs& a, cudaStream_t s) {
-    const int smem = LUT8_BYTES + STAGE * (int)sizeof(uint32_t);
+    // + 1 KiB: 32 staged 2052-byte lane columns (the LUT build) exceed the
+    // 64 KiB candidate stage
+    const int smem = LUT8_BYTES + STAGE * (int)sizeof(uint32_t) + 1024;
     PQRR_CUDA(cudaFuncSetAttribute(ivf_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     ivf_filter_kernel<<<sm_count(), FT, smem, s>>>(a);
     PQRR_LAUNCH_CHECK();
     count_launch();
+}
+
+void launch_live_pairs(const FilterArgs& a, const uint32_t* list_cnt, uint32_t nlists,
+                       uint32_t* live_pos, uint32_t* live_cnt, const uint32_t* item_off,
+                       uint32_t* item_start, uint32_t* item_nq, uint32_t chunk, cudaStream_t s) {
+    live_pairs_kernel<<<(nlists * 32 + 255) / 256, 256, 0, s>>>(a, list_cnt, nlists, live_pos, live_cnt);
+    PQRR_LAUNCH_CHECK();
+    live_items_kernel<<<(nlists + 255) / 256, 256, 0, s>>>(a, list_cnt, live_cnt, nlists, item_off,
+                                                          item_start, item_nq, chunk);
+    PQRR_LAUNCH_CHECK();
+    count_launch(2);
 }
 
 bool recheck_supported(uint32_t d, uint32_t m, uint32_t w) {

@@ -381,25 +381,31 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 prm[2 * t + 1] = sm;
             }
             csync();
-            // 8-bit block straight to global memory: a warp writes 128
-            // contiguous bytes per store
-            uint32_t* stage = reinterpret_cast<uint32_t*>(a.q8_cache + (size_t)it * Q8_BYTES);
+            // 8-bit block straight to global memory, lane-major (q8_put_rows):
+            // a thread quantises 4 rows x 4 lanes and writes 4 lane words;
+            // a warp's stores cover 4 lanes x 32 contiguous bytes
+            uint32_t* block = reinterpret_cast<uint32_t*>(a.q8_cache + (size_t)it * Q8_BYTES);
             const int g = t & 3;
             const float4 inv = *reinterpret_cast<const float4*>(s_inv + 4 * g);
             const float shrink = 0.99999904632568359375f;  // 1 - 2^-20
-#pragma unroll 4
-            for (int row = t >> 2; row < M * KS; row += NC / 4) {
-                const float4 v = lut4[row * 4 + g];
-                const float4 mn = *reinterpret_cast<const float4*>(s_min + (row >> 8) * QT + 4 * g);
-                // floor(x) for 0 <= x <= 255 without the quarter-rate F2I:
-                // x + 2^23 rounded down has ulp 1, so its low byte is floor(x)
-                auto q8 = [&](float L, float m, float iv) -> uint32_t {
-                    const float x = fminf(__fmul_rn(__fmul_rn(__fsub_rn(L, m), iv), shrink), 255.f);
-                    return __float_as_uint(__fadd_rd(x, 8388608.f));
-                };
-                const uint32_t p01 = __byte_perm(q8(v.x, mn.x, inv.x), q8(v.y, mn.y, inv.y), 0x0040);
-                const uint32_t p23 = __byte_perm(q8(v.z, mn.z, inv.z), q8(v.w, mn.w, inv.w), 0x0040);
-                stage[row * 4 + g] = __byte_perm(p01, p23, 0x5410);
+            // floor(x) for 0 <= x <= 255 without the quarter-rate F2I:
+            // x + 2^23 rounded down has ulp 1, so its low byte is floor(x)
+            auto q8 = [&](float L, float m, float iv) -> uint32_t {
+                const float x = fminf(__fmul_rn(__fmul_rn(__fsub_rn(L, m), iv), shrink), 255.f);
+                return __float_as_uint(__fadd_rd(x, 8388608.f));
+            };
+#pragma unroll 2
+            for (int rq = t >> 2; rq < M * KS / 4; rq += NC / 4) {
+                const float4 mn = *reinterpret_cast<const float4*>(s_min + (rq >> 6) * QT + 4 * g);
+                uint32_t rw[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float4 v = lut4[(4 * rq + i) * 4 + g];
+                    const uint32_t p01 = __byte_perm(q8(v.x, mn.x, inv.x), q8(v.y, mn.y, inv.y), 0x0040);
+                    const uint32_t p23 = __byte_perm(q8(v.z, mn.z, inv.z), q8(v.w, mn.w, inv.w), 0x0040);
+                    rw[i] = __byte_perm(p01, p23, 0x5410);
+                }
+                q8_put_rows(block, g, rq, rw[0], rw[1], rw[2], rw[3]);
             }
         }
 #ifdef LP_NOSAMPLE  // timing experiment only

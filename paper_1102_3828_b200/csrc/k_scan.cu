@@ -167,16 +167,21 @@ __device__ __forceinline__ void quantize_item(const float* __restrict__ lut, uin
     const int g = t & 3;
     const float4 inv = *reinterpret_cast<const float4*>(s_inv + 4 * g);
     const float shrink = 0.99999904632568359375f;  // 1 - 2^-20
-#pragma unroll 4
-    for (int row = t >> 2; row < M * KS; row += NT / 4) {
-        const float4 v = lut4[row * 4 + g];
-        const float4 mn = *reinterpret_cast<const float4*>(s_min + (row >> 8) * 16 + 4 * g);
-        auto q8 = [&](float L, float m, float iv) -> uint32_t {
-            const float x = fminf(__fmul_rn(__fmul_rn(__fsub_rn(L, m), iv), shrink), 255.f);
-            return __float2uint_rz(x);
-        };
-        stage[row * 4 + g] = q8(v.x, mn.x, inv.x) | (q8(v.y, mn.y, inv.y) << 8) |
-                             (q8(v.z, mn.z, inv.z) << 16) | (q8(v.w, mn.w, inv.w) << 24);
+    auto q8 = [&](float L, float m, float iv) -> uint32_t {
+        const float x = fminf(__fmul_rn(__fmul_rn(__fsub_rn(L, m), iv), shrink), 255.f);
+        return __float2uint_rz(x);
+    };
+    // lane-major block (q8_put_rows), staged in shared memory for the bulk store
+    for (int rq = t >> 2; rq < M * KS / 4; rq += NT / 4) {
+        const float4 mn = *reinterpret_cast<const float4*>(s_min + (rq >> 6) * 16 + 4 * g);
+        uint32_t rw[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float4 v = lut4[(4 * rq + i) * 4 + g];
+            rw[i] = q8(v.x, mn.x, inv.x) | (q8(v.y, mn.y, inv.y) << 8) | (q8(v.z, mn.z, inv.z) << 16) |
+                    (q8(v.w, mn.w, inv.w) << 24);
+        }
+        q8_put_rows(stage, g, rq, rw[0], rw[1], rw[2], rw[3]);
     }
 }
 

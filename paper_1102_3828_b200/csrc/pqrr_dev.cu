@@ -826,6 +826,13 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         // >= 160 saturates the 5-bit values and overflows candidate buffers
         const float band_div = bd_env ? (float)atof(bd_env) : 100.f;
         f.band_div = band_div;
+        {
+            uint32_t* live_pos = ws.alloc<uint32_t>(P);
+            uint32_t* live_cnt = ws.alloc<uint32_t>(c);
+            f.live_pos = live_pos;
+            launch_live_pairs(f, im.list_cnt, c, live_pos, live_cnt, if64.item_off, if64.item_start,
+                              if64.item_nq, if64.chunk, s);
+        }
         launch_ivf_filter(f, s);
         if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[9], s));
         cand_le = ws.alloc<uint32_t>(nq);
