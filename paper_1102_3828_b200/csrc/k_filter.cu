@@ -591,17 +591,18 @@ void recheck_t(const float* xq, uint32_t d, const float* coarse, const float* bo
 
 }  // namespace
 
-// Per list (one warp): positions of the live pairs, compacted in list order.
-__global__ void live_pairs_kernel(const FilterArgs a, const uint32_t* __restrict__ list_cnt,
-                                  uint32_t nlists, uint32_t* __restrict__ live_pos,
-                                  uint32_t* __restrict__ live_cnt) {
-    const uint32_t l = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (l >= nlists) return;
+// Per list (one CTA): positions of the live pairs, compacted in list order
+// (ballot per warp + a prefix over the CTA's warps per 256-pair chunk).
+__global__ __launch_bounds__(256) void live_pairs_kernel(const FilterArgs a, const uint32_t* __restrict__ list_cnt,
+                                                         uint32_t nlists, uint32_t* __restrict__ live_pos,
+                                                         uint32_t* __restrict__ live_cnt) {
+    __shared__ uint32_t s_wc[8];
+    const uint32_t l = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t n = list_cnt[l], f = a.list_first[l], b0 = a.sub_item_off[l];
     uint32_t o = 0;
-    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
-        const uint32_t i = i0 + lane;
+    for (uint32_t i0 = 0; i0 < n; i0 += 256) {
+        const uint32_t i = i0 + threadIdx.x;
         bool live = false;
         if (i < n) {
             const uint32_t p = a.pair_sorted[f + i];
@@ -609,10 +610,15 @@ __global__ void live_pairs_kernel(const FilterArgs a, const uint32_t* __restrict
             live = a.pass_all || pair_live(a.tau[p / a.w], prm[1]);
         }
         const unsigned bal = __ballot_sync(0xffffffffu, live);
-        if (live) live_pos[f + o + __popc(bal & ((1u << lane) - 1u))] = f + i;
-        o += __popc(bal);
+        if (lane == 0) s_wc[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t before = o;
+        for (int k = 0; k < warp; ++k) before += s_wc[k];
+        if (live) live_pos[f + before + __popc(bal & ((1u << lane) - 1u))] = f + i;
+        for (int k = 0; k < 8; ++k) o += s_wc[k];
+        __syncthreads();
     }
-    if (lane == 0) live_cnt[l] = o;
+    if (threadIdx.x == 0) live_cnt[l] = o;
 }
 
 // The K4f items of a list (groups of FQ pairs x entry chunks, items_build
@@ -646,7 +652,7 @@ void launch_ivf_filter(const FilterArgs& a, cudaStream_t s) {
 void launch_live_pairs(const FilterArgs& a, const uint32_t* list_cnt, uint32_t nlists,
                        uint32_t* live_pos, uint32_t* live_cnt, const uint32_t* item_off,
                        uint32_t* item_start, uint32_t* item_nq, uint32_t chunk, cudaStream_t s) {
-    live_pairs_kernel<<<(nlists * 32 + 255) / 256, 256, 0, s>>>(a, list_cnt, nlists, live_pos, live_cnt);
+    live_pairs_kernel<<<nlists, 256, 0, s>>>(a, list_cnt, nlists, live_pos, live_cnt);
     PQRR_LAUNCH_CHECK();
     live_items_kernel<<<(nlists + 255) / 256, 256, 0, s>>>(a, list_cnt, live_cnt, nlists, item_off,
                                                           item_start, item_nq, chunk);
