@@ -273,8 +273,9 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
             }
             // per-query sampling stride for this list (probe rank tier)
             const uint8_t sm = (q >= 0 && a.query_sampled) ? a.query_sampled[q] : 0;
-            const uint32_t tier = (lane < QT && q >= 0) ? sample_tier(p % a.w, a.w, a.tiered) : 7u;
-            uint32_t tmin = (sm && lane < QT) ? tier : 7u;
+            // the lane's stride shift (tier_shift of its probe rank's tier)
+            const uint32_t tier = (lane < QT && q >= 0) ? tier_shift(sample_tier(p % a.w, a.w, a.tiered), a.w) : 31u;
+            uint32_t tmin = (sm && lane < QT) ? tier : 31u;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
             if (lane < QT) {
@@ -290,7 +291,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 mt.e0 = e0;
                 mt.e1 = e1;
                 mt.nqi = nqi;
-                mt.smin = tmin < 7u ? (a.stride << tmin) : 0u;
+                mt.smin = tmin < 31u ? (a.stride << tmin) : 0u;
             }
             __syncwarp();
             // rows: 16 query rows + the coarse row, 16 B per cp.async
@@ -302,7 +303,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
             }
             // sampled codes of the item's entries at the smallest stride among
             // its sampled queries (items cover whole lists: e0 == 0)
-            if (sampling && tmin < 7u) {
+            if (sampling && tmin < 31u) {
                 const uint32_t smin = a.stride << tmin;
                 const uint32_t ns = (e1 + smin - 1) / smin;
                 const u64* lcodes = reinterpret_cast<const u64*>(a.codes) + a.list_off[l];

@@ -38,7 +38,7 @@ __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t n
     unsigned long long ssum = 0;
     for (uint32_t r = 0; r < w; ++r) {
         const uint32_t len = list_len[probes[q * w + r]];
-        const uint32_t st = stride << sample_tier(r, w, tiered);
+        const uint32_t st = stride << tier_shift(sample_tier(r, w, tiered), w);
         const uint64_t ns = samp ? (len + st - 1) / st : 0;
         pair_samples[q * w + r] = ns;
         ssum += ns;
@@ -137,7 +137,7 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void sample_threshold_kernel(
     __syncthreads();
     unsigned long long total = 0;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) total += (s_seg[t + 1] - s_seg[t]) * ((unsigned long long)stride << t);
+    for (int t = 0; t < 4; ++t) total += (s_seg[t + 1] - s_seg[t]) * ((unsigned long long)stride << tier_shift(t, w));
     const uint32_t rank = (uint32_t)max(1.0, ceil((double)alpha_k));
     if (total < rank) {
         if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
@@ -148,7 +148,7 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void sample_threshold_kernel(
     if (threadIdx.x == 0) s_fill = 0;
     __syncthreads();
     for (int t = 0; t < 4; ++t) {
-        const uint32_t wt = stride << t;
+        const uint32_t wt = stride << tier_shift(t, w);
         const uint32_t n = (uint32_t)(s_seg[t + 1] - s_seg[t]);
         if (n) for_each_u32(gsrc + s_seg[t], n, [&](uint32_t u) { atomicAdd(&hist[u >> 21], wt); });
     }
@@ -189,7 +189,7 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void sample_threshold_kernel(
         const int sh = shifts[pass], wd = widths[pass];
         const uint32_t msk = (1u << wd) - 1u;
         auto add = [&](uint32_t u, uint32_t t) {
-            if ((u >> (sh + wd)) == prefix) atomicAdd(&hist[(u >> sh) & msk], stride << t);
+            if ((u >> (sh + wd)) == prefix) atomicAdd(&hist[(u >> sh) & msk], stride << tier_shift(t, w));
         };
         if (staged) {
             for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) add(stage[i], stage_t[i]);

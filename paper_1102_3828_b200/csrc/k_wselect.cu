@@ -624,7 +624,8 @@ __global__ __launch_bounds__(WS_WARPS * 32) void threshold_warp_kernel(
     const uint64_t s0 = __shfl_sync(0xffffffffu, seg, 0), s1 = __shfl_sync(0xffffffffu, seg, 1);
     const uint64_t s2 = __shfl_sync(0xffffffffu, seg, 2), s3 = __shfl_sync(0xffffffffu, seg, 3);
     const uint64_t s4 = __shfl_sync(0xffffffffu, seg, 4);
-    const unsigned long long total = ((s1 - s0) + ((s2 - s1) << 1) + ((s3 - s2) << 2) + ((s4 - s3) << 3)) *
+    const uint32_t h1 = tier_shift(1, w), h2 = tier_shift(2, w), h3 = tier_shift(3, w);
+    const unsigned long long total = ((s1 - s0) + ((s2 - s1) << h1) + ((s3 - s2) << h2) + ((s4 - s3) << h3)) *
                                      (unsigned long long)stride;
     const uint32_t rank = (uint32_t)max(1.0, ceil((double)alpha_k));
     if (total < rank) {
@@ -636,7 +637,7 @@ __global__ __launch_bounds__(WS_WARPS * 32) void threshold_warp_kernel(
     const uint32_t b1 = (uint32_t)(s1 - s0), b2 = (uint32_t)(s2 - s0), b3 = (uint32_t)(s3 - s0);
     const uint32_t t = warp_weighted_select(
         n, rank, [&](uint32_t i) { return __ldg(src + i); },
-        [&](uint32_t i) { return stride << ((i >= b1) + (i >= b2) + (i >= b3)); }, hist_all[warp]);
+        [&](uint32_t i) { return stride << tier_shift((i >= b1) + (i >= b2) + (i >= b3), w); }, hist_all[warp]);
     if (lane == 0) tau[q] = __uint_as_float(t);
 }
 
