@@ -706,15 +706,26 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
         const uint32_t nb = min(32u, n - i0);
         const size_t t0 = q * stride + i0;
         __syncwarp();  // the previous chunk's metadata reads are done
-        if ((uint32_t)lane < nb) {
-            rid[t0 + lane] = p_id;
-            m_list[lane] = p_list;
-            m_code[lane] = p_code;
+        if ((uint32_t)lane < nb) rid[t0 + lane] = p_id;
+        {
+            // slots past nb repeat the last candidate, so the sub-batch loop
+            // reads 8 valid entries without clamping (duplicates are not stored)
+            const int src = min(lane, (int)nb - 1);
+            const uint32_t pl = __shfl_sync(0xffffffffu, p_list, src);
+            const u64 pc = ((u64)__shfl_sync(0xffffffffu, (uint32_t)(p_code >> 32), src) << 32) |
+                           __shfl_sync(0xffffffffu, (uint32_t)p_code, src);
+            m_list[lane] = pl;
+            m_code[lane] = pc;
+            uint4 rc[RCV];
+#pragma unroll
+            for (int v = 0; v < RCV; ++v)
+                rc[v] = make_uint4(__shfl_sync(0xffffffffu, p_rc[v].x, src), __shfl_sync(0xffffffffu, p_rc[v].y, src),
+                                   __shfl_sync(0xffffffffu, p_rc[v].z, src), __shfl_sync(0xffffffffu, p_rc[v].w, src));
             if constexpr (MP % 16 == 0) {
 #pragma unroll
-                for (int v = 0; v < RCV; ++v) reinterpret_cast<uint4*>(m_rcode + lane * MP)[v] = p_rc[v];
+                for (int v = 0; v < RCV; ++v) reinterpret_cast<uint4*>(m_rcode + lane * MP)[v] = rc[v];
             } else {
-                *reinterpret_cast<u64*>(m_rcode + lane * MP) = ((u64)p_rc[0].y << 32) | p_rc[0].x;
+                *reinterpret_cast<u64*>(m_rcode + lane * MP) = ((u64)rc[0].y << 32) | rc[0].x;
             }
         }
         nch = next_valid(ch + tw);
@@ -729,23 +740,36 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
         // the L1 / L2 gathers (the code-book rows not held in shared memory)
         // of a sub-batch of 8 candidates are issued one sub-batch ahead, so
         // their latency overlaps the previous sub-batch's sequential sums
-        auto gload = [&](uint32_t ci) -> float4 {
+        // 8 candidates' codes with 4 LDS.128 (m_code is 16-byte aligned)
+        auto gload8 = [&](uint32_t sb0, float4* out) {
             if constexpr (RB_SMEM) {
-                const uint32_t code = (uint32_t)(m_code[ci] >> (8 * jj)) & 0xffu;
-                return __ldg(reinterpret_cast<const float4*>(books + ((size_t)jj * 256 + code) * 16) + bo);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const ulonglong2 cc2 = reinterpret_cast<const ulonglong2*>(m_code)[(sb0 >> 1) + h];
+                    const uint32_t c0 = (uint32_t)(cc2.x >> (8 * jj)) & 0xffu;
+                    const uint32_t c1 = (uint32_t)(cc2.y >> (8 * jj)) & 0xffu;
+                    out[2 * h] = __ldg(reinterpret_cast<const float4*>(books + ((size_t)jj * 256 + c0) * 16) + bo);
+                    out[2 * h + 1] = __ldg(reinterpret_cast<const float4*>(books + ((size_t)jj * 256 + c1) * 16) + bo);
+                }
             } else {
-                const uint32_t rcode = m_rcode[ci * MP + jr];
-                return __ldg(reinterpret_cast<const float4*>(rbooks + ((size_t)jr * 256 + rcode) * DSR + ro));
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const uint32_t rcode = m_rcode[(sb0 + c) * MP + jr];
+                    out[c] = __ldg(reinterpret_cast<const float4*>(rbooks + ((size_t)jr * 256 + rcode) * DSR + ro));
+                }
             }
         };
         float4 gv[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) gv[c] = gload(min((uint32_t)c, nb - 1));
+        gload8(0, gv);
         for (uint32_t sb = 0; sb < nb; sb += 8) {
+            // the sub-batch's 8 list ids with 2 LDS.128
+            const uint4 lq0 = reinterpret_cast<const uint4*>(m_list)[sb >> 2];
+            const uint4 lq1 = reinterpret_cast<const uint4*>(m_list)[(sb >> 2) + 1];
+            const uint32_t lids[8] = {lq0.x, lq0.y, lq0.z, lq0.w, lq1.x, lq1.y, lq1.z, lq1.w};
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-                const uint32_t ci = min(sb + c, nb - 1);
-                const uint32_t l = m_list[ci];
+                const uint32_t ci = sb + c;
+                const uint32_t l = lids[c];
                 if (l != cur_l) {
                     cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + g);
                     cur_l = l;
@@ -767,10 +791,7 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
                 *reinterpret_cast<float4*>(tile + c * RC_TLD + 4 * g) =
                     make_float4(__fmul_rn(d0, d0), __fmul_rn(d1, d1), __fmul_rn(d2, d2), __fmul_rn(d3, d3));
             }
-            if (sb + 8 < nb) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) gv[c] = gload(min(sb + 8 + c, nb - 1));
-            }
+            if (sb + 8 < nb) gload8(sb + 8, gv);
             __syncwarp();
             const int cc = lane >> 2, k = lane & 3;
             float sacc = 0.f;
