@@ -270,6 +270,15 @@ def test_forced_retries_stay_exact(scan):
         assert any("retries=0" not in x for x in lines), lines
 
 
+def test_filter_pass_all_stays_exact():
+    """PQRR_FILTER_ALL=1 makes every probed entry of a live pair a K4f
+    survivor: it drives the candidate stage through its periodic flushes and
+    the direct-append fallback, and the buffers through overflow retries; the
+    shortlists must still equal the oracle's."""
+    lines = _mid_search_subprocess(PQRR_FILTER_ALL="1")
+    assert all("bad=0" in x for x in lines), lines
+
+
 def test_large_coarse_radix_probe_selection(pq, oracle):
     """Kc > 2048 takes the radix-select top-w path; duplicated centroids force
     exact coarse-distance ties that must resolve to the lowest list index."""
