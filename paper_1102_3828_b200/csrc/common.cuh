@@ -95,6 +95,14 @@ __device__ __forceinline__ u64 nb_key(float dist, uint32_t id) {
 __device__ __forceinline__ float key_dist(u64 k) { return __uint_as_float((unsigned)(k >> 32)); }
 __device__ __forceinline__ uint32_t key_id(u64 k) { return (uint32_t)(k & 0xffffffffull); }
 
+// A pair can have a candidate (dist <= tau) only if sum_m <= tau (within the
+// roundings slot_params covers); the same test as slot_params' dead case.
+__device__ __forceinline__ bool pair_live(float tau, float summ) {
+    const float e_up = 1.000003814697265625f, e_dn = 0.999996185302734375f;  // 1 +- 2^-18
+    if (!(tau < __int_as_float(0x7f800000))) return true;
+    return __fsub_rn(__fmul_rn(tau, e_up), __fmul_rn(summ, e_dn)) >= 0.f;
+}
+
 // 8-bit LUT block of a LUT-pass item (K2 -> K4f): LANE-major, 16 query lanes
 // x (M * KS) row bytes, so K4f can copy any lane's 2 KiB column with
 // coalesced 16-byte loads.  r0..r3 hold rows 4 rq .. 4 rq + 3, each the bytes

@@ -177,6 +177,12 @@ struct ScanArgs {
     const uint64_t* sample_off;  // per pair
     float* sample_dist;
     const uint8_t* query_sampled;  // per query: 1 if the query is in sample mode
+    // two-phase LUT pass (w >= 32, k_lutpass.cu): q8_mode 1 = bound pass
+    // (per-lane scale and sum of minima only, no 8-bit block); skip_dead = skip
+    // items none of whose lanes can reach tau (pair_live on a bound pass's
+    // q8_param) and write the blocks of the others
+    int q8_mode;
+    int skip_dead;
 };
 void launch_ivf_scan(const ScanArgs& a, cudaStream_t s);
 // K2 LUT pass (pass 1) as a warp-specialised kernel (k_lutpass.cu).
@@ -202,7 +208,8 @@ struct FilterArgs {
     const uint32_t* list_first;  // first pair of each list in pair_sorted
     const uint32_t* sub_item_off;  // first 16-query item of each list
     const uint32_t* pair_sorted;
-    const uint32_t* live_pos;    // per list, the positions (into pair_sorted) of its live pairs
+    const uint32_t* live_slot;   // per list from list_first[l]: q8 slot (block * 16 + lane) of each live pair
+    const uint32_t* live_pair;   // ... and its pair id q * w + r
     uint32_t w;
     const float* tau;
     const uint8_t* q8_cache;
@@ -220,8 +227,18 @@ void launch_ivf_filter(const FilterArgs& a, cudaStream_t s);
 // otherwise).  Writes, per list, the positions of its live pairs from
 // list_first[l] on (live_pos) and rewrites the 64-query K4f items
 // (item_start / item_nq) over the live pairs only.
-void launch_live_pairs(const FilterArgs& a, const uint32_t* list_cnt, uint32_t nlists,
-                       uint32_t* live_pos, uint32_t* live_cnt, const uint32_t* item_off,
+// The pairs come from up to two LUT-pass item sets (near / far probes of the
+// two-phase LUT pass); set k's blocks start at q8 block blk_base[k].
+struct PairSet {
+    const uint32_t* pair_sorted;
+    const uint32_t* list_cnt;
+    const uint32_t* list_first;
+    const uint32_t* sub_item_off;
+    uint32_t blk_base;
+};
+void launch_live_pairs(const FilterArgs& a, PairSet s0, PairSet s1, const uint32_t* all_first,
+                       const uint32_t* all_cnt, uint32_t nlists, uint32_t* live_slot,
+                       uint32_t* live_pair, uint32_t* live_cnt, const uint32_t* item_off,
                        uint32_t* item_start, uint32_t* item_nq, uint32_t chunk, cudaStream_t s);
 // K4r: exact ADC distance of every filter candidate (reference order), and
 // the per-query count of candidates at or below tau.
@@ -244,7 +261,7 @@ void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, u
 void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
                         uint32_t stride, int tiered, uint32_t cap, uint64_t* nq_entries,
                         uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
-                        cudaStream_t s);
+                        cudaStream_t s, uint32_t max_rank = 0xffffffffu);
 // tau_q = rank-th smallest sample of query q (sampled queries), +inf otherwise.
 void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_off, uint32_t w,
                              size_t nq, const uint8_t* query_sampled, float alpha_k,

@@ -69,14 +69,6 @@ __device__ __forceinline__ SlotParam slot_params(float tau, float sc, float summ
     return {mult, 0u, t >= 255.f ? 255u : (uint32_t)t};
 }
 
-// A pair can have a candidate (dist <= tau) only if sum_m <= tau (within the
-// roundings slot_params covers); the same test as slot_params' dead case.
-__device__ __forceinline__ bool pair_live(float tau, float summ) {
-    const float e_up = 1.000003814697265625f, e_dn = 0.999996185302734375f;  // 1 +- 2^-18
-    if (!(tau < __int_as_float(0x7f800000))) return true;
-    return __fsub_rn(__fmul_rn(tau, e_up), __fmul_rn(summ, e_dn)) >= 0.f;
-}
-
 // Four v8 bytes -> v5 bytes: min(31, (b * mult_b >> 8) + add_b).
 __device__ __forceinline__ uint32_t v5_of(uint32_t word, const uint32_t* mult, const uint32_t* add) {
     uint32_t out = 0;
@@ -270,10 +262,9 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
             SlotParam sp{0u, 31u, 0u};  // empty slot: dead
             uint64_t src = 0;
             if (t < nqi) {
-                const uint32_t pos = a.live_pos[start + t];
-                const uint32_t li = pos - a.list_first[l];
-                const uint32_t blk = a.sub_item_off[l] + li / SUBQ, ln = li % SUBQ;
-                const uint32_t p = a.pair_sorted[pos];
+                const uint32_t slot = a.live_slot[start + t];
+                const uint32_t blk = slot / SUBQ, ln = slot % SUBQ;
+                const uint32_t p = a.live_pair[start + t];
                 q = (int)(p / a.w);
                 r = p % a.w;
                 const float* prm = a.q8_param + ((size_t)blk * SUBQ + ln) * 2;
@@ -591,32 +582,46 @@ void recheck_t(const float* xq, uint32_t d, const float* coarse, const float* bo
 
 }  // namespace
 
-// Per list (one CTA): positions of the live pairs, compacted in list order
-// (ballot per warp + a prefix over the CTA's warps per 256-pair chunk).
-__global__ __launch_bounds__(256) void live_pairs_kernel(const FilterArgs a, const uint32_t* __restrict__ list_cnt,
-                                                         uint32_t nlists, uint32_t* __restrict__ live_pos,
+// Per list (one CTA): the live pairs of the list from both pair sets (near /
+// far probes of the two-phase LUT pass; one set otherwise), compacted from
+// all_first[l] on as (q8 slot, pair id).  Ballot per warp + a prefix over the
+// CTA's warps per 256-pair chunk.
+__global__ __launch_bounds__(256) void live_pairs_kernel(const FilterArgs a, PairSet s0, PairSet s1,
+                                                         const uint32_t* __restrict__ all_first,
+                                                         uint32_t* __restrict__ live_slot,
+                                                         uint32_t* __restrict__ live_pair,
                                                          uint32_t* __restrict__ live_cnt) {
     __shared__ uint32_t s_wc[8];
     const uint32_t l = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t n = list_cnt[l], f = a.list_first[l], b0 = a.sub_item_off[l];
+    const uint32_t base = all_first[l];
     uint32_t o = 0;
-    for (uint32_t i0 = 0; i0 < n; i0 += 256) {
-        const uint32_t i = i0 + threadIdx.x;
-        bool live = false;
-        if (i < n) {
-            const uint32_t p = a.pair_sorted[f + i];
-            const float* prm = a.q8_param + ((size_t)(b0 + i / SUBQ) * SUBQ + i % SUBQ) * 2;
-            live = a.pass_all || pair_live(a.tau[p / a.w], prm[1]);
+    for (int set = 0; set < 2; ++set) {
+        const PairSet& ps = set ? s1 : s0;
+        if (!ps.list_cnt) continue;
+        const uint32_t n = ps.list_cnt[l], f = ps.list_first[l], b0 = ps.blk_base + ps.sub_item_off[l];
+        for (uint32_t i0 = 0; i0 < n; i0 += 256) {
+            const uint32_t i = i0 + threadIdx.x;
+            bool live = false;
+            uint32_t p = 0, slot = 0;
+            if (i < n) {
+                p = ps.pair_sorted[f + i];
+                slot = (b0 + i / SUBQ) * SUBQ + i % SUBQ;
+                live = a.pass_all || pair_live(a.tau[p / a.w], a.q8_param[(size_t)slot * 2 + 1]);
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, live);
+            if (lane == 0) s_wc[warp] = __popc(bal);
+            __syncthreads();
+            uint32_t before = o;
+            for (int k = 0; k < warp; ++k) before += s_wc[k];
+            if (live) {
+                const uint32_t d = base + before + __popc(bal & ((1u << lane) - 1u));
+                live_slot[d] = slot;
+                live_pair[d] = p;
+            }
+            for (int k = 0; k < 8; ++k) o += s_wc[k];
+            __syncthreads();
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, live);
-        if (lane == 0) s_wc[warp] = __popc(bal);
-        __syncthreads();
-        uint32_t before = o;
-        for (int k = 0; k < warp; ++k) before += s_wc[k];
-        if (live) live_pos[f + before + __popc(bal & ((1u << lane) - 1u))] = f + i;
-        for (int k = 0; k < 8; ++k) o += s_wc[k];
-        __syncthreads();
     }
     if (threadIdx.x == 0) live_cnt[l] = o;
 }
@@ -624,6 +629,7 @@ __global__ __launch_bounds__(256) void live_pairs_kernel(const FilterArgs a, con
 // The K4f items of a list (groups of FQ pairs x entry chunks, items_build
 // order) re-pointed at its live pairs; groups past the live count are empty.
 __global__ void live_items_kernel(const FilterArgs a, const uint32_t* __restrict__ list_cnt,
+                                  const uint32_t* __restrict__ list_first,
                                   const uint32_t* __restrict__ live_cnt, uint32_t nlists,
                                   const uint32_t* __restrict__ item_off, uint32_t* __restrict__ item_start,
                                   uint32_t* __restrict__ item_nq, uint32_t chunk) {
@@ -634,7 +640,7 @@ __global__ void live_items_kernel(const FilterArgs a, const uint32_t* __restrict
     uint32_t o = item_off[l];
     for (uint32_t g = 0; g < c; g += FQ)
         for (uint32_t ch = 0; ch < chunks; ++ch, ++o) {
-            item_start[o] = a.list_first[l] + g;
+            item_start[o] = list_first[l] + g;
             item_nq[o] = g < lc ? min((uint32_t)FQ, lc - g) : 0u;
         }
 }
@@ -649,12 +655,13 @@ void launch_ivf_filter(const FilterArgs& a, cudaStream_t s) {
     count_launch();
 }
 
-void launch_live_pairs(const FilterArgs& a, const uint32_t* list_cnt, uint32_t nlists,
-                       uint32_t* live_pos, uint32_t* live_cnt, const uint32_t* item_off,
+void launch_live_pairs(const FilterArgs& a, PairSet s0, PairSet s1, const uint32_t* all_first,
+                       const uint32_t* all_cnt, uint32_t nlists, uint32_t* live_slot,
+                       uint32_t* live_pair, uint32_t* live_cnt, const uint32_t* item_off,
                        uint32_t* item_start, uint32_t* item_nq, uint32_t chunk, cudaStream_t s) {
-    live_pairs_kernel<<<nlists, 256, 0, s>>>(a, list_cnt, nlists, live_pos, live_cnt);
+    live_pairs_kernel<<<nlists, 256, 0, s>>>(a, s0, s1, all_first, live_slot, live_pair, live_cnt);
     PQRR_LAUNCH_CHECK();
-    live_items_kernel<<<(nlists + 255) / 256, 256, 0, s>>>(a, list_cnt, live_cnt, nlists, item_off,
+    live_items_kernel<<<(nlists + 255) / 256, 256, 0, s>>>(a, all_cnt, all_first, live_cnt, nlists, item_off,
                                                           item_start, item_nq, chunk);
     PQRR_LAUNCH_CHECK();
     count_launch(2);

@@ -195,7 +195,10 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t n_items = *a.num_items;
-    const bool store_q8 = a.q8_cache != nullptr;
+    // per-lane (scale, sum of minima) whenever q8_param is set; the 8-bit
+    // block too unless this is the bound pass of the two-phase LUT pass
+    const bool store_q8 = a.q8_param != nullptr;
+    const bool store_block = store_q8 && a.q8_cache != nullptr && a.q8_mode == 0;
     const bool sampling = a.sample_dist != nullptr;
     if (threadIdx.x == 0) {
         for (int b = 0; b < 2; ++b) {
@@ -250,26 +253,38 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
         for (uint32_t k = 0;; ++k) {
             const int b = k & 1;
             if (k >= 2) mbar_wait(&empty_bar[b], ((k >> 1) - 1) & 1);
-            uint32_t c = 0;
-            if (lane == 0) c = atomicAdd(a.item_counter, 1u);
-            c = __shfl_sync(0xffffffffu, c, 0);
             ItemMeta& mt = meta[b];
+            uint32_t c, it, l, e0, e1, start, nqi, p;
+            int q;
+            for (;;) {
+                c = 0;
+                if (lane == 0) c = atomicAdd(a.item_counter, 1u);
+                c = __shfl_sync(0xffffffffu, c, 0);
+                if (c >= n_items) break;
+                it = a.item_order[c];  // longest items first
+                l = a.item_list[it];
+                e0 = a.item_e0[it];
+                e1 = a.item_e1[it];
+                start = a.item_start[it];
+                nqi = a.item_nq[it];
+                q = -1;
+                p = 0;
+                if (lane < QT && (uint32_t)lane < nqi) {
+                    p = a.pair_sorted[start + lane];
+                    q = (int)(p / a.w);
+                }
+                if (!a.skip_dead) break;
+                // round 2 of the two-phase pass: only items with a lane that
+                // can reach tau (its bound-pass sum of minima, pair_live)
+                const bool live = q >= 0 && pair_live(a.tau[q], a.q8_param[((size_t)it * QT + lane) * 2 + 1]);
+                if (__any_sync(0xffffffffu, live)) break;
+            }
             if (c >= n_items) {
                 if (lane == 0) {
                     mt.it = 0xffffffffu;
                     mbar_arrive(&full_bar[b]);
                 }
                 break;
-            }
-            const uint32_t it = a.item_order[c];  // longest items first
-            const uint32_t l = a.item_list[it];
-            const uint32_t e0 = a.item_e0[it], e1 = a.item_e1[it];
-            const uint32_t start = a.item_start[it], nqi = a.item_nq[it];
-            int q = -1;
-            uint32_t p = 0;
-            if (lane < QT && (uint32_t)lane < nqi) {
-                p = a.pair_sorted[start + lane];
-                q = (int)(p / a.w);
             }
             // per-query sampling stride for this list (probe rank tier)
             const uint8_t sm = (q >= 0 && a.query_sampled) ? a.query_sampled[q] : 0;
@@ -382,6 +397,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 prm[2 * t + 1] = sm;
             }
             csync();
+            if (store_block) {
             // 8-bit block straight to global memory, lane-major (q8_put_rows):
             // a thread quantises 4 rows x 4 lanes and writes 4 lane words;
             // a warp's stores cover 4 lanes x 32 contiguous bytes
@@ -408,6 +424,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 }
                 q8_put_rows(block, g, rq, rw[0], rw[1], rw[2], rw[3]);
             }
+            }  // store_block
         }
 #ifdef LP_NOSAMPLE  // timing experiment only
         if (false) {

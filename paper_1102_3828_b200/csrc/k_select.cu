@@ -24,7 +24,7 @@ __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t n
                                    const uint32_t* __restrict__ list_len, uint32_t stride,
                                    int tiered, uint32_t cap, uint64_t* __restrict__ n_entries,
                                    uint8_t* __restrict__ sampled, uint64_t* __restrict__ pair_samples,
-                                   unsigned long long* __restrict__ grand_total) {
+                                   unsigned long long* __restrict__ grand_total, uint32_t max_rank) {
     size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
     uint64_t tot = 0;
@@ -39,7 +39,7 @@ __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t n
     for (uint32_t r = 0; r < w; ++r) {
         const uint32_t len = list_len[probes[q * w + r]];
         const uint32_t st = stride << tier_shift(sample_tier(r, w, tiered), w);
-        const uint64_t ns = samp ? (len + st - 1) / st : 0;
+        const uint64_t ns = (samp && r < max_rank) ? (len + st - 1) / st : 0;
         pair_samples[q * w + r] = ns;
         ssum += ns;
     }
@@ -962,11 +962,11 @@ void set_smem(const void* f, size_t bytes) {
 void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
                         uint32_t stride, int tiered, uint32_t cap, uint64_t* nq_entries,
                         uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
-                        cudaStream_t s) {
+                        cudaStream_t s, uint32_t max_rank) {
     if (nq == 0) return;
     query_sizes_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, s>>>(
         probes, nq, w, list_len, stride, tiered, cap, nq_entries, query_sampled, pair_samples,
-        reinterpret_cast<unsigned long long*>(grand_total));
+        reinterpret_cast<unsigned long long*>(grand_total), max_rank);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

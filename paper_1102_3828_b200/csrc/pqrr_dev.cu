@@ -340,7 +340,7 @@ struct DevIndex {
     DBuf<uint32_t> st_assign, st_ids;
     DBuf<uint8_t> st_codes, st_rcodes;
     pqrr_dev_search_stats stats{};
-    cudaEvent_t ev[11] = {};
+    cudaEvent_t ev[12] = {};
 
     ~DevIndex() {
         for (auto& e : ev)
@@ -575,12 +575,12 @@ struct ItemSet {
 // coarse distances (approximate on the tensor-core path: fine for a sort).
 __global__ void pair_key_kernel(const uint32_t* __restrict__ lists, const uint32_t* __restrict__ pair_ids,
                                 size_t np, uint32_t w, const float* __restrict__ D, uint32_t c,
-                                uint32_t* __restrict__ key) {
+                                const uint32_t* __restrict__ probes, uint32_t* __restrict__ key) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
     const uint32_t p = pair_ids[i];
     const size_t q = p / w;
-    const float gap = fmaxf(__fsub_rn(D[q * c + lists[i]], D[q * c + lists[q * w]]), 0.f);
+    const float gap = fmaxf(__fsub_rn(D[q * c + lists[i]], D[q * c + probes[q * w]]), 0.f);
     // the sampling tier of the probe rank first (a 16-query block then shares
     // one sampling stride in the LUT pass), then the gap (bits 30..17 of a
     // non-negative float: 14 bits, monotone)
@@ -588,10 +588,29 @@ __global__ void pair_key_kernel(const uint32_t* __restrict__ lists, const uint32
     key[i] = (lists[i] << 16) | (tier << 14) | (__float_as_uint(gap) >> 17);
 }
 
+// Two-phase LUT pass: pairs of probe rank r < R1 (near) and r >= R1 (far).
+__global__ void split_pairs_kernel(const uint32_t* __restrict__ probes, size_t nq, uint32_t w, uint32_t R1,
+                                   uint32_t* __restrict__ near_lists, uint32_t* __restrict__ near_ids,
+                                   uint32_t* __restrict__ far_lists, uint32_t* __restrict__ far_ids) {
+    const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nq * w) return;
+    const size_t q = p / w;
+    const uint32_t r = (uint32_t)(p % w);
+    if (r < R1) {
+        const size_t k = q * R1 + r;
+        near_lists[k] = probes[p];
+        near_ids[k] = (uint32_t)p;
+    } else {
+        const size_t k = q * (w - R1) + (r - R1);
+        far_lists[k] = probes[p];
+        far_ids[k] = (uint32_t)p;
+    }
+}
+
 ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_ids, size_t np,
                      uint32_t c, const uint32_t* list_len, uint32_t qt, cudaStream_t s,
                      const ItemSet* share = nullptr, uint32_t chunk = 1u << 30, uint32_t w = 1,
-                     const float* D = nullptr) {
+                     const float* D = nullptr, const uint32_t* probes = nullptr) {
     ItemSet it;
     it.c = c;
     it.qt = qt;
@@ -605,7 +624,7 @@ ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_
         it.pair_sorted = ws.alloc<uint32_t>(np);
         if (D && bits_for(c) <= 16) {
             uint32_t* key = ws.alloc<uint32_t>(np);
-            pair_key_kernel<<<nblk(np), 256, 0, s>>>(lists, pair_ids, np, w, D, c, key);
+            pair_key_kernel<<<nblk(np), 256, 0, s>>>(lists, pair_ids, np, w, D, c, probes ? probes : lists, key);
             PQRR_LAUNCH_CHECK();
             count_launch();
             sort_pairs(key, sorted_keys, pair_ids, it.pair_sorted, np, 16 + bits_for(c), s);
@@ -708,6 +727,35 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // into chunks so one list does not serialise on one SM
     const uint32_t fchunk = P < (size_t)64 * sm_count() ? 16384u : (1u << 30);
     ItemSet if64 = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kFQ, s, &im, fchunk);
+    // Two-phase LUT pass (w >= 32): the near probes (rank < w/8, the sampling
+    // tier 0, where the shortlist lives at C3-C5) get the full LUT pass with
+    // sampling, which fixes tau; the far probes get a bound pass (exact LUTs,
+    // only their per-lane sum of minima), and a second full pass builds the
+    // 8-bit blocks of the far items that have a live lane.  tau comes from
+    // the near samples only: a quantile over a subset of the entries, so at
+    // least as large as the full one (never under-full; exactness is still
+    // checked) and equal to it when the near probes hold the entries below it.
+    // the far-probe bound pass costs about as much as a full pass per pair
+    // (the LUT build dominates): it pays from w = 128 (C5) on
+    constexpr uint32_t kTwoPhaseW = 128;
+    static const bool old_lut_env0 = getenv("PQRR_LUTPASS") && std::string(getenv("PQRR_LUTPASS")) == "old";
+    static const bool one_phase_env = getenv("PQRR_LUT_ONE_PHASE") != nullptr;  // A/B switch
+    const bool two_phase = filter_ok && !old_lut_env0 && !one_phase_env && w >= kTwoPhaseW &&
+                           lut_pass_supported(ix.d, ix.m, ix.ks);
+    const uint32_t R1 = two_phase ? (w + 7) / 8 : w;
+    ItemSet im_near, im_far;
+    if (two_phase) {
+        const size_t pn = nq * (size_t)R1, pf = nq * (size_t)(w - R1);
+        uint32_t* nl = ws.alloc<uint32_t>(pn);
+        uint32_t* ni = ws.alloc<uint32_t>(pn);
+        uint32_t* fl = ws.alloc<uint32_t>(pf);
+        uint32_t* fi = ws.alloc<uint32_t>(pf);
+        split_pairs_kernel<<<nblk(P), 256, 0, s>>>(probes, nq, w, R1, nl, ni, fl, fi);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        im_near = items_phase1(ws, nl, ni, pn, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w, D, probes);
+        im_far = items_phase1(ws, fl, fi, pf, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w, D, probes);
+    }
     uint64_t* n_entries = ws.alloc<uint64_t>(nq);
     uint8_t* sampled = ws.alloc<uint8_t>(nq);
     uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
@@ -717,7 +765,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     static const bool uniform_env = getenv("PQRR_SAMPLING") && std::string(getenv("PQRR_SAMPLING")) == "uniform";
     const int tiered = (!old_lut_env && !uniform_env && w >= 8 && lut_pass_supported(ix.d, ix.m, ix.ks)) ? 1 : 0;
     launch_query_sizes(probes, nq, w, ix.list_len.p, stride, tiered, cap, n_entries, sampled,
-                       pair_samples, grand, s);
+                       pair_samples, grand, s, R1);
     uint64_t* sample_off = ws.alloc<uint64_t>(P + 1);
     exclusive_scan_u64(pair_samples, sample_off, P + 1, s);
     uint64_t total_samples = 0, h_grand[2] = {0, 0};
@@ -725,6 +773,10 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     PQRR_CUDA(cudaMemcpyAsync(&total_samples, sample_off + P, 8, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaMemcpyAsync(&if64.n_items, if64.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+    if (two_phase) {
+        PQRR_CUDA(cudaMemcpyAsync(&im_near.n_items, im_near.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaMemcpyAsync(&im_far.n_items, im_far.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+    }
     uint32_t h_ovf = 0;
     if (coarse_tc) PQRR_CUDA(cudaMemcpyAsync(&h_ovf, coarse_ovf, 4, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaStreamSynchronize(s));
@@ -732,7 +784,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         shortlist_core(ix, xq, nq, w, kprime, sorted, alpha, stride_div, out, depth, timed, cap_shift, true);
         return;
     }
-    const uint32_t n_items = im.n_items;
+    const uint32_t n_items = two_phase ? im_near.n_items + im_far.n_items : im.n_items;
 
     bool use_filter = filter_ok;
     if (use_filter) {
@@ -749,6 +801,10 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     }
     items_phase2(ws, im, c, ix.list_len.p, s);
     if (use_filter) items_phase2(ws, if64, c, ix.list_len.p, s);
+    if (two_phase) {
+        items_phase2(ws, im_near, c, ix.list_len.p, s);
+        items_phase2(ws, im_far, c, ix.list_len.p, s);
+    }
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[2], s));
 
     ScanArgs a{};
@@ -771,7 +827,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     float* tau = ws.alloc<float>(nq);
     float* sample_dist = ws.alloc<float>(total_samples);
     if (total_samples || use_filter) {
-        im.apply(a);
+        (two_phase ? im_near : im).apply(a);
         a.pass = 1;
         a.q8_cache = use_filter ? ix.q8_cache.p : nullptr;
         a.q8_param = use_filter ? ix.q8_param.p : nullptr;
@@ -789,6 +845,27 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     launch_sample_threshold(sample_dist, sample_off, w, nq, sampled, (float)(alpha * kprime), stride,
                             tiered, (uint32_t)h_grand[1], tau, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[4], s));
+    if (two_phase && use_filter && im_far.n_items) {
+        // far probes: bound pass (per-lane sum of minima), then the 8-bit
+        // blocks of the far items with a lane that can reach tau
+        ScanArgs b = a;
+        im_far.apply(b);
+        b.pass = 1;
+        b.q8_cache = ix.q8_cache.p + (size_t)im_near.n_items * 8 * 256 * kQT;
+        b.q8_param = ix.q8_param.p + (size_t)im_near.n_items * kQT * 2;
+        b.sample_dist = nullptr;
+        b.tau = tau;
+        uint32_t* cnt2 = ws.zeros<uint32_t>(2);
+        b.item_counter = cnt2;
+        b.q8_mode = 1;
+        b.skip_dead = 0;
+        launch_lut_pass(b, s);
+        b.item_counter = cnt2 + 1;
+        b.q8_mode = 0;
+        b.skip_dead = 1;
+        launch_lut_pass(b, s);
+    }
+    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[11], s));
 
     // ---- K4 main scan: candidates (d <= tau, or the filter's superset)
     float* cand_dist = ws.alloc<float>(nq * (size_t)cap);
@@ -827,11 +904,18 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         const float band_div = bd_env ? (float)atof(bd_env) : 100.f;
         f.band_div = band_div;
         {
-            uint32_t* live_pos = ws.alloc<uint32_t>(P);
+            uint32_t* live_slot = ws.alloc<uint32_t>(P);
+            uint32_t* live_pair = ws.alloc<uint32_t>(P);
             uint32_t* live_cnt = ws.alloc<uint32_t>(c);
-            f.live_pos = live_pos;
-            launch_live_pairs(f, im.list_cnt, c, live_pos, live_cnt, if64.item_off, if64.item_start,
-                              if64.item_nq, if64.chunk, s);
+            f.live_slot = live_slot;
+            f.live_pair = live_pair;
+            const ItemSet& s0 = two_phase ? im_near : im;
+            PairSet p0{s0.pair_sorted, s0.list_cnt, s0.list_first, s0.item_off, 0u};
+            PairSet p1{nullptr, nullptr, nullptr, nullptr, 0u};
+            if (two_phase) p1 = PairSet{im_far.pair_sorted, im_far.list_cnt, im_far.list_first, im_far.item_off,
+                                        im_near.n_items};
+            launch_live_pairs(f, p0, p1, im.list_first, im.list_cnt, c, live_slot, live_pair, live_cnt,
+                              if64.item_off, if64.item_start, if64.item_nq, if64.chunk, s);
         }
         launch_ivf_filter(f, s);
         if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[9], s));
@@ -916,11 +1000,12 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         };
         st.ms_coarse += el(0, 1);
         st.ms_invert += el(1, 2);
-        st.ms_sample_scan += el(2, 3);
+        // the far-probe LUT passes (two-phase) count as LUT-pass time
+        st.ms_sample_scan += el(2, 3) + el(4, 11);
         st.ms_threshold += el(3, 4);
-        st.ms_scan += el(4, 5);
+        st.ms_scan += el(11, 5);
         st.ms_select += el(5, 6);
-        if (use_filter) st.ms_filter += el(4, 9);
+        if (use_filter) st.ms_filter += el(11, 9);
         st.work_items += n_items;
         st.sampled_entries += total_samples;
         st.scanned_entries += h_grand[0];
