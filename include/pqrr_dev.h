@@ -196,6 +196,14 @@ int pqrr_dev_rerank_owned_u8_device(pqrr_dev_index* ix, const uint8_t* d_queries
 /* ivf_reconstruct (ivf_index.hpp:75-77): coarse + decode + refine decode. */
 int pqrr_dev_reconstruct(pqrr_dev_index* ix, const uint32_t* ids, size_t n, float* out);
 
+/* Test seam of the two-phase LUT pass (k_bound.cu): certified lower bounds
+ * (tensor cores) of sum_j min_c l2_sq(x_q - C_l, B_j[c]) for the pairs
+ * (q, l = probes[q w + r]), r >= R1, written to out[q w + r] (other slots are
+ * left untouched).  d = 128, m = 8, ks = 256.                               */
+int pqrr_dev_pair_bounds(int device, const float* queries, size_t nq, uint32_t d, const float* coarse,
+                         uint32_t c, const float* books, uint32_t m, uint32_t ks, const uint32_t* probes,
+                         uint32_t w, uint32_t R1, float* out);
+
 /* ------------------------------------------------------------------ ADC / ADC+R
  * Exhaustive first stage (adc_index.hpp:13-31) and its re-ranking
  * (refine.hpp:30-53).  An ADC index is an index handle with one all-zero

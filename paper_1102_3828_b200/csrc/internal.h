@@ -183,7 +183,13 @@ struct ScanArgs {
     // q8_param) and write the blocks of the others
     int q8_mode;
     int skip_dead;
+    const float* pair_bound;  // skip_dead: per pair id, a lower bound of the sum of minima (k_bound.cu)
 };
+// Certified lower bound (tensor cores) of the sum of LUT minima of the far
+// pairs (probe rank >= R1), per pair id into pair_bound (k_bound.cu).
+bool far_bound_supported(uint32_t d, uint32_t m, uint32_t ks);
+void launch_far_bound(const float* xq, const float* coarse, const float* books, const uint32_t* probes,
+                      size_t nq, uint32_t w, uint32_t R1, float* pair_bound, cudaStream_t s);
 void launch_ivf_scan(const ScanArgs& a, cudaStream_t s);
 // K2 LUT pass (pass 1) as a warp-specialised kernel (k_lutpass.cu).
 bool lut_pass_supported(uint32_t d, uint32_t m, uint32_t ks);
@@ -235,6 +241,7 @@ struct PairSet {
     const uint32_t* list_first;
     const uint32_t* sub_item_off;
     uint32_t blk_base;
+    const float* pair_bound;  // set: a pair is live only if its bound also admits it
 };
 void launch_live_pairs(const FilterArgs& a, PairSet s0, PairSet s1, const uint32_t* all_first,
                        const uint32_t* all_cnt, uint32_t nlists, uint32_t* live_slot,

@@ -607,7 +607,9 @@ __global__ __launch_bounds__(256) void live_pairs_kernel(const FilterArgs a, Pai
             if (i < n) {
                 p = ps.pair_sorted[f + i];
                 slot = (b0 + i / SUBQ) * SUBQ + i % SUBQ;
-                live = a.pass_all || pair_live(a.tau[p / a.w], a.q8_param[(size_t)slot * 2 + 1]);
+                // (a bound-dead pair's item may have been skipped: its q8_param is then unset)
+                live = a.pass_all || ((!ps.pair_bound || pair_live(a.tau[p / a.w], ps.pair_bound[p])) &&
+                                      pair_live(a.tau[p / a.w], a.q8_param[(size_t)slot * 2 + 1]));
             }
             const unsigned bal = __ballot_sync(0xffffffffu, live);
             if (lane == 0) s_wc[warp] = __popc(bal);

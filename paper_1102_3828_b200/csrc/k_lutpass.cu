@@ -276,7 +276,9 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 if (!a.skip_dead) break;
                 // round 2 of the two-phase pass: only items with a lane that
                 // can reach tau (its bound-pass sum of minima, pair_live)
-                const bool live = q >= 0 && pair_live(a.tau[q], a.q8_param[((size_t)it * QT + lane) * 2 + 1]);
+                const float summ = a.pair_bound ? (q >= 0 ? a.pair_bound[p] : 0.f)
+                                                : a.q8_param[((size_t)it * QT + lane) * 2 + 1];
+                const bool live = q >= 0 && pair_live(a.tau[q], summ);
                 if (__any_sync(0xffffffffu, live)) break;
             }
             if (c >= n_items) {

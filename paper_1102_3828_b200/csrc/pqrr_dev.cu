@@ -735,9 +735,8 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // the near samples only: a quantile over a subset of the entries, so at
     // least as large as the full one (never under-full; exactness is still
     // checked) and equal to it when the near probes hold the entries below it.
-    // the far-probe bound pass costs about as much as a full pass per pair
-    // (the LUT build dominates): it pays from w = 128 (C5) on
-    constexpr uint32_t kTwoPhaseW = 128;
+    // far probes are bounded on the tensor cores (k_bound.cu): pays from w = 32
+    constexpr uint32_t kTwoPhaseW = 32;
     static const bool old_lut_env0 = getenv("PQRR_LUTPASS") && std::string(getenv("PQRR_LUTPASS")) == "old";
     static const bool one_phase_env = getenv("PQRR_LUT_ONE_PHASE") != nullptr;  // A/B switch
     const bool two_phase = filter_ok && !old_lut_env0 && !one_phase_env && w >= kTwoPhaseW &&
@@ -845,6 +844,9 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     launch_sample_threshold(sample_dist, sample_off, w, nq, sampled, (float)(alpha * kprime), stride,
                             tiered, (uint32_t)h_grand[1], tau, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[4], s));
+    static const bool fma_bound_env = getenv("PQRR_FAR_BOUND") && std::string(getenv("PQRR_FAR_BOUND")) == "fma";
+    float* pair_bound = (two_phase && use_filter && !fma_bound_env && far_bound_supported(ix.d, ix.m, ix.ks))
+                            ? ws.alloc<float>(P) : nullptr;
     if (two_phase && use_filter && im_far.n_items) {
         // far probes: bound pass (per-lane sum of minima), then the 8-bit
         // blocks of the far items with a lane that can reach tau
@@ -856,10 +858,16 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         b.sample_dist = nullptr;
         b.tau = tau;
         uint32_t* cnt2 = ws.zeros<uint32_t>(2);
-        b.item_counter = cnt2;
-        b.q8_mode = 1;
-        b.skip_dead = 0;
-        launch_lut_pass(b, s);
+        if (pair_bound) {
+            // tensor-core lower bound of every far pair's sum of minima
+            launch_far_bound(xq, ix.coarse.p, ix.books.p, probes, nq, w, R1, pair_bound, s);
+            b.pair_bound = pair_bound;
+        } else {
+            b.item_counter = cnt2;
+            b.q8_mode = 1;  // exact bound pass (sum of minima from the FMA LUT build)
+            b.skip_dead = 0;
+            launch_lut_pass(b, s);
+        }
         b.item_counter = cnt2 + 1;
         b.q8_mode = 0;
         b.skip_dead = 1;
@@ -910,10 +918,10 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
             f.live_slot = live_slot;
             f.live_pair = live_pair;
             const ItemSet& s0 = two_phase ? im_near : im;
-            PairSet p0{s0.pair_sorted, s0.list_cnt, s0.list_first, s0.item_off, 0u};
-            PairSet p1{nullptr, nullptr, nullptr, nullptr, 0u};
+            PairSet p0{s0.pair_sorted, s0.list_cnt, s0.list_first, s0.item_off, 0u, nullptr};
+            PairSet p1{nullptr, nullptr, nullptr, nullptr, 0u, nullptr};
             if (two_phase) p1 = PairSet{im_far.pair_sorted, im_far.list_cnt, im_far.list_first, im_far.item_off,
-                                        im_near.n_items};
+                                        im_near.n_items, pair_bound};
             launch_live_pairs(f, p0, p1, im.list_first, im.list_cnt, c, live_slot, live_pair, live_cnt,
                               if64.item_off, if64.item_start, if64.item_nq, if64.chunk, s);
         }
@@ -1817,6 +1825,32 @@ int pqrr_dev_load_lists(pqrr_dev_index* h, const uint64_t* offsets, const uint32
         ix.next_id = max_id + 1;
         ix.id_lo = min_id;
         finalize(ix);
+    });
+}
+
+// Kernel seam of the two-phase LUT pass's tensor-core bound (k_bound.cu), for
+// tests: lower bounds of sum_j min_c l2_sq(x_q - C_l, B_j[c]) of the pairs
+// (q, probes[q w + r]) with r >= R1, into out[q w + r] (other slots untouched).
+int pqrr_dev_pair_bounds(int device, const float* queries, size_t nq, uint32_t d, const float* coarse,
+                         uint32_t c, const float* books, uint32_t m, uint32_t ks, const uint32_t* probes,
+                         uint32_t w, uint32_t R1, float* out) {
+    return guarded([&] {
+        if (!far_bound_supported(d, m, ks)) throw UnsupportedError("pair bounds need d = 128, m = 8, ks = 256");
+        if (R1 > w) throw ArgError("R1 must be <= w");
+        for (size_t i = 0; i < nq * (size_t)w; ++i)
+            if (probes[i] >= c) throw ArgError("probe out of range");
+        if (nq == 0 || w == R1) return;
+        Session se(device);
+        Workspace ws(se.s);
+        const float* dq = se.upload(ws, queries, nq * d);
+        const float* dc = se.upload(ws, coarse, (size_t)c * d);
+        const float* db = se.upload(ws, books, (size_t)ks * d);
+        const uint32_t* dp = se.upload(ws, probes, nq * (size_t)w);
+        float* o = ws.alloc<float>(nq * (size_t)w);
+        PQRR_CUDA(cudaMemsetAsync(o, 0, nq * (size_t)w * 4, se.s));
+        launch_far_bound(dq, dc, db, dp, nq, w, R1, o, se.s);
+        se.download(out, o, nq * (size_t)w);
+        se.sync();
     });
 }
 

@@ -671,3 +671,34 @@ def test_export_lists_subset(pq, golden_ivf):
         np.testing.assert_array_equal(si[so[i]:so[i + 1]], ids[a:b])
         np.testing.assert_array_equal(sc[so[i]:so[i + 1]], codes[a:b])
         np.testing.assert_array_equal(sr[so[i]:so[i + 1]], rc[a:b])
+
+
+def test_far_pair_bound_is_a_certified_lower_bound(pq, oracle, mid_instance):
+    """k_bound.cu (two-phase LUT pass): the tensor-core bound never exceeds the
+    exact fp32 sum of the LUT minima (the quantity the live-pair test uses),
+    for u8 and fractional queries, and stays tight (it only selects work)."""
+    from paper_1102_3828_b200._lib import check, lib
+
+    mi = mid_instance
+    coarse, books = mi["coarse"], mi["books"]
+    rng = np.random.default_rng(5)
+    for qs in (mi["queries"][:24].astype(np.float32),
+               (mi["queries"][:24] + rng.standard_normal((24, 128)) * 3.7).astype(np.float32)):
+        nq, w, R1 = len(qs), 40, 5
+        probes, _ = oracle.coarse_probe(coarse, qs, w)
+        out = np.zeros(nq * w, np.float32)
+        check(lib.pqrr_dev_pair_bounds(0, np.ascontiguousarray(qs), nq, 128, coarse, coarse.shape[0],
+                                       np.ascontiguousarray(books, np.float32).reshape(-1), 8, 256,
+                                       np.ascontiguousarray(probes, np.uint32).reshape(-1), w, R1, out))
+        out = out.reshape(nq, w)
+        ratios = []
+        for q in range(nq):
+            for r in range(R1, w):
+                lut = oracle.build_lut(books, qs[q] - coarse[probes[q, r]], 8).reshape(8, 256)
+                sm = np.float32(0)
+                for j in range(8):
+                    sm = np.float32(sm + lut[j].min())
+                assert out[q, r] <= sm, (q, r, out[q, r], sm)
+                ratios.append(out[q, r] / sm)
+        assert np.all(out[:, :R1] == 0)
+        assert np.median(ratios) > 0.98
