@@ -610,7 +610,7 @@ __global__ void split_pairs_kernel(const uint32_t* __restrict__ probes, size_t n
 ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_ids, size_t np,
                      uint32_t c, const uint32_t* list_len, uint32_t qt, cudaStream_t s,
                      const ItemSet* share = nullptr, uint32_t chunk = 1u << 30, uint32_t w = 1,
-                     const float* D = nullptr, const uint32_t* probes = nullptr) {
+                     const float* D = nullptr, const uint32_t* probes = nullptr, bool counts_only = false) {
     ItemSet it;
     it.c = c;
     it.qt = qt;
@@ -619,6 +619,11 @@ ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_
         it.pair_sorted = share->pair_sorted;
         it.list_cnt = share->list_cnt;
         it.list_first = share->list_first;
+    } else if (counts_only) {  // per-list pair counts / first pair only (two-phase K4f bases)
+        it.list_cnt = ws.zeros<uint32_t>(c + 1);
+        launch_histogram(lists, np, c, it.list_cnt, s);
+        it.list_first = ws.alloc<uint32_t>(c + 1);
+        exclusive_scan_u32(it.list_cnt, it.list_first, c + 1, s);
     } else {
         uint32_t* sorted_keys = ws.alloc<uint32_t>(np);
         it.pair_sorted = ws.alloc<uint32_t>(np);
@@ -722,11 +727,6 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // LUT pass (and the exact scan), 64-query items for the K4f filter
     uint32_t* pair_ids = ws.alloc<uint32_t>(P);
     launch_iota(pair_ids, P, s);
-    ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w, D);
-    // small batches (few query-list pairs per SM): K4f items split long lists
-    // into chunks so one list does not serialise on one SM
-    const uint32_t fchunk = P < (size_t)64 * sm_count() ? 16384u : (1u << 30);
-    ItemSet if64 = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kFQ, s, &im, fchunk);
     // Two-phase LUT pass (w >= 32): the near probes (rank < w/8, the sampling
     // tier 0, where the shortlist lives at C3-C5) get the full LUT pass with
     // sampling, which fixes tau; the far probes get a bound pass (exact LUTs,
@@ -742,6 +742,14 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     const bool two_phase = filter_ok && !old_lut_env0 && !one_phase_env && w >= kTwoPhaseW &&
                            lut_pass_supported(ix.d, ix.m, ix.ks);
     const uint32_t R1 = two_phase ? (w + 7) / 8 : w;
+    // all pairs: the single-phase LUT pass items, or (two-phase) only the
+    // per-list counts that place the K4f live pairs
+    ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w, D,
+                              probes, two_phase);
+    // small batches (few query-list pairs per SM): K4f items split long lists
+    // into chunks so one list does not serialise on one SM
+    const uint32_t fchunk = P < (size_t)64 * sm_count() ? 16384u : (1u << 30);
+    ItemSet if64 = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kFQ, s, &im, fchunk);
     ItemSet im_near, im_far;
     if (two_phase) {
         const size_t pn = nq * (size_t)R1, pf = nq * (size_t)(w - R1);
@@ -798,7 +806,14 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         }
         use_filter = ix.q8_cache.bytes() >= need;
     }
-    items_phase2(ws, im, c, ix.list_len.p, s);
+    if (two_phase && !use_filter) {
+        // rare (no room for the 8-bit LUT cache): the exact scan needs the
+        // sorted all-pairs items after all
+        im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w, D);
+        PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaStreamSynchronize(s));
+    }
+    if (!two_phase || !use_filter) items_phase2(ws, im, c, ix.list_len.p, s);
     if (use_filter) items_phase2(ws, if64, c, ix.list_len.p, s);
     if (two_phase) {
         items_phase2(ws, im_near, c, ix.list_len.p, s);
