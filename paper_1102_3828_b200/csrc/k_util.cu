@@ -75,10 +75,53 @@ void launch_iota(uint32_t* out, size_t n, cudaStream_t s) {
     count_launch();
 }
 
+// Small sorts (the work-item inversions of small batches): one CTA, bitonic
+// sort of (key << 32 | index) in shared memory — stable like the radix sort,
+// one launch instead of CUB's several.
+constexpr int kSmallSort = 4096;
+__global__ __launch_bounds__(1024) void small_sort_pairs_kernel(const uint32_t* __restrict__ keys_in,
+                                                               uint32_t* __restrict__ keys_out,
+                                                               const uint32_t* __restrict__ vals_in,
+                                                               uint32_t* __restrict__ vals_out, uint32_t n) {
+    __shared__ unsigned long long sk[kSmallSort];
+    uint32_t n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x)
+        sk[i] = i < n ? (((unsigned long long)keys_in[i] << 32) | i) : ~0ull;
+    __syncthreads();
+    for (uint32_t size = 2; size <= n2; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+                const uint32_t jx = i ^ stride;
+                if (jx > i) {
+                    const bool up = (i & size) == 0;
+                    const unsigned long long a = sk[i], b = sk[jx];
+                    if ((a > b) == up) {
+                        sk[i] = b;
+                        sk[jx] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned long long v = sk[i];
+        keys_out[i] = (uint32_t)(v >> 32);
+        vals_out[i] = vals_in[(uint32_t)v];
+    }
+}
+
 void sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
                 uint32_t* vals_out, size_t n, int bits, cudaStream_t s) {
     if (n == 0) return;
     if (bits < 1) bits = 1;
+    if (n <= (size_t)kSmallSort) {
+        small_sort_pairs_kernel<<<1, 1024, 0, s>>>(keys_in, keys_out, vals_in, vals_out, (uint32_t)n);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        return;
+    }
     size_t tmp = 0;
     PQRR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys_in, keys_out, vals_in, vals_out,
                                               (int64_t)n, 0, bits, s));

@@ -739,7 +739,10 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     constexpr uint32_t kTwoPhaseW = 32;
     static const bool old_lut_env0 = getenv("PQRR_LUTPASS") && std::string(getenv("PQRR_LUTPASS")) == "old";
     static const bool one_phase_env = getenv("PQRR_LUT_ONE_PHASE") != nullptr;  // A/B switch
+    // (large batches only: for a few hundred pairs the extra item sets and
+    // launches cost more than the LUT builds they save)
     const bool two_phase = filter_ok && !old_lut_env0 && !one_phase_env && w >= kTwoPhaseW &&
+                           P >= (size_t)64 * sm_count() &&
                            lut_pass_supported(ix.d, ix.m, ix.ks);
     const uint32_t R1 = two_phase ? (w + 7) / 8 : w;
     // all pairs: the single-phase LUT pass items, or (two-phase) only the
