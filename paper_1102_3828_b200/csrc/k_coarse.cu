@@ -267,7 +267,7 @@ __global__ __launch_bounds__(TW_THREADS) void topw_radix_kernel(const float* __r
     uint32_t* bits = tw_smem;                                 // [nc]
     u64* sel = reinterpret_cast<u64*>(tw_smem + ((nc + 1) & ~1u));  // [w2]
     __shared__ uint32_t hist[2048];
-    __shared__ uint32_t s_bin, s_rank, s_cnt, s_out, s_total, s_warp[TW_THREADS / 32];
+    __shared__ uint32_t s_bin, s_rank, s_out, s_total, s_warp[TW_THREADS / 32];
     const size_t q = blockIdx.x;
     const uint32_t* row = reinterpret_cast<const uint32_t*>(D + q * nc);
     for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) bits[i] = row[i];
@@ -306,7 +306,6 @@ __global__ __launch_bounds__(TW_THREADS) void topw_radix_kernel(const float* __r
                     if (r <= cacc + h) {
                         s_bin = lane * 64 + b;
                         s_rank = r - cacc;
-                        s_cnt = h;
                         break;
                     }
                     cacc += h;
