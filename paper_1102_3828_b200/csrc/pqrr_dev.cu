@@ -739,7 +739,8 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // least as large as the full one (never under-full; exactness is still
     // checked) and equal to it when the near probes hold the entries below it.
     // far probes are bounded on the tensor cores (k_bound.cu): pays from w = 32
-    constexpr uint32_t kTwoPhaseW = 32;
+    static const uint32_t kTwoPhaseW = getenv("PQRR_TWO_PHASE_W") ? (uint32_t)atoi(getenv("PQRR_TWO_PHASE_W")) : 32u;
+    static const uint32_t kR1Div = getenv("PQRR_R1_DIV") ? (uint32_t)atoi(getenv("PQRR_R1_DIV")) : 8u;  // tuning hooks
     static const bool old_lut_env0 = getenv("PQRR_LUTPASS") && std::string(getenv("PQRR_LUTPASS")) == "old";
     static const bool one_phase_env = getenv("PQRR_LUT_ONE_PHASE") != nullptr;  // A/B switch
     // (large batches only: for a few hundred pairs the extra item sets and
@@ -747,7 +748,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     const bool two_phase = filter_ok && !old_lut_env0 && !one_phase_env && w >= kTwoPhaseW &&
                            P >= (size_t)64 * sm_count() &&
                            lut_pass_supported(ix.d, ix.m, ix.ks);
-    const uint32_t R1 = two_phase ? (w + 7) / 8 : w;
+    const uint32_t R1 = two_phase ? (w + kR1Div - 1) / kR1Div : w;
     // all pairs: the single-phase LUT pass items, or (two-phase) only the
     // per-list counts that place the K4f live pairs
     ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w, D,
