@@ -565,32 +565,17 @@ def run_sweep(args, cfg, rank, world):
 
 
 def recall_and_parity(pq, cfg, queries, res_ids, ix, coarse, P, rq):
-    """recall@1/10/100 vs exact GT on a query sample + oracle parity on a subsample."""
-    import torch
-
+    """recall@1/10/100 against exact ground truth on a query sample: the
+    product's compute_groundtruth over the device-generated base set (k_exact.cu,
+    integer tensor cores, exact for u8)."""
     out = {}
     nq_gt = min(1000, len(queries))
-    qs = torch.from_numpy(queries[:nq_gt]).cuda().float()
-    best_d = torch.full((nq_gt,), float("inf"), device="cuda")
-    best_i = torch.zeros(nq_gt, dtype=torch.int64, device="cuda")
-    qn = (qs * qs).sum(1, keepdim=True)
-    chunk = 2_000_000
-    for s in range(0, cfg["n"], chunk):
-        n = min(chunk, cfg["n"] - s)
-        b = torch.from_numpy(pq.synth(2, s, n, cfg["clusters"], seed=SEED)).cuda()
-        bf = b.float()
-        # u8 data: every term is an exact integer < 2^24, so bf16 products with
-        # fp32 accumulation give the exact squared distance
-        dots = (qs.bfloat16() @ bf.bfloat16().T).float()
-        dd = qn + (bf * bf).sum(1)[None, :] - 2 * dots
-        v, i = dd.min(1)  # first occurrence = lowest id on ties
-        upd = v < best_d
-        best_d = torch.where(upd, v, best_d)
-        best_i = torch.where(upd, i + s, best_i)
-    gt = best_i.cpu().numpy()
+    t0 = time.time()
+    gt = pq.groundtruth_synthetic(SEED, cfg["clusters"], cfg["n"], queries[:nq_gt], 1)
     for r in (1, 10, 100):
-        out[f"recall@{r}"] = float(np.mean([gt[q] in res_ids[q, :r] for q in range(nq_gt)]))
+        out[f"recall@{r}"] = float(np.mean([gt.nearest(q) in res_ids[q, :r] for q in range(nq_gt)]))
     out["recall_queries"] = nq_gt
+    log(f"[recall] exact ground truth of {nq_gt} queries over {cfg['n']} vectors in {time.time() - t0:.1f}s")
     return out
 
 

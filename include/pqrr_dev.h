@@ -204,6 +204,20 @@ int pqrr_dev_pair_bounds(int device, const float* queries, size_t nq, uint32_t d
                          uint32_t c, const float* books, uint32_t m, uint32_t ks, const uint32_t* probes,
                          uint32_t w, uint32_t R1, float* out);
 
+/* ------------------------------------------------------------------ ground truth
+ * compute_groundtruth / exact_search (eval.hpp:13-19) for u8 vectors, d = 128:
+ * per query the min(k, n) nearest base rows, ascending (dist, id) (exact: u8
+ * distances are integers < 2^24, computed with integer tensor-core MMA).
+ * Rows [k * q, k * q + k) of out_ids / out_dists, out_counts[q] valid.
+ * _u8: base rows from host memory (ids 0..n-1); _synthetic: rows
+ * [row0, row0 + n) of the synthetic base set generated on the device (the
+ * bench's 1B ground truth), ids = row index.  1 <= k <= 16384.              */
+int pqrr_dev_exact_knn_u8(int device, const uint8_t* base, size_t n, const uint8_t* queries, size_t nq,
+                          uint32_t d, uint32_t k, uint32_t* out_ids, float* out_dists, uint32_t* out_counts);
+int pqrr_dev_exact_knn_synthetic(int device, uint64_t seed, uint32_t clusters, uint64_t row0, size_t n,
+                                 const uint8_t* queries, size_t nq, uint32_t k, uint32_t* out_ids,
+                                 float* out_dists, uint32_t* out_counts);
+
 /* ------------------------------------------------------------------ ADC / ADC+R
  * Exhaustive first stage (adc_index.hpp:13-31) and its re-ranking
  * (refine.hpp:30-53).  An ADC index is an index handle with one all-zero

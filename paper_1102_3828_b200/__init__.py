@@ -21,4 +21,7 @@ from .storage import (  # noqa: F401
     load_quantizer, probe_index_kind, save_adc_index, save_codebook, save_ivf_index,
     save_quantizer,
 )
-from . import adc, ivf, kernels, sharded, storage  # noqa: F401
+from .eval import (  # noqa: F401
+    GroundTruth, compute_groundtruth, exact_search, groundtruth_synthetic, recall_at_r,
+)
+from . import adc, eval, ivf, kernels, sharded, storage  # noqa: F401

@@ -110,6 +110,8 @@ _sig("pqrr_dev_adc_index_create", [_int, _u32, _u32, _f32p, _u32, _vp, _u32, C.P
 _sig("pqrr_dev_refine_train", [_int, _f32p, _u32, _u32, _u32, _f32p, _sz, _u32, _u32, _u64, _f32p])
 _sig("pqrr_dev_residual", [_int, _f32p, _u32, _u32, _u32, _f32p, _sz, _f32p])
 _sig("pqrr_dev_export_codebooks", [_vp, _vp, _vp, _vp])
+_sig("pqrr_dev_exact_knn_u8", [_int, _vp, _sz, _u8p, _sz, _u32, _u32, _u32p, _f32p, _u32p])
+_sig("pqrr_dev_exact_knn_synthetic", [_int, _u64, _u32, _u64, _sz, _u8p, _sz, _u32, _u32p, _f32p, _u32p])
 _sig("pqrr_dev_pair_bounds", [_int, _f32p, _sz, _u32, _f32p, _u32, _f32p, _u32, _u32, _u32p, _u32, _u32,
                               _f32p])
 _sig("pqrr_dev_export_lists_subset", [_vp, _u32p, _u32, _u64p, _vp, _vp, _vp])
@@ -138,7 +140,7 @@ EXPORTED = [
     "pqrr_dev_merge_topk", "pqrr_dev_merge_topk_device", "pqrr_dev_rerank_owned_u8_device",
     "pqrr_dev_adc_index_create", "pqrr_dev_refine_train", "pqrr_dev_residual",
     "pqrr_dev_reconstruct_codes", "pqrr_dev_export_codebooks", "pqrr_dev_export_lists_subset",
-    "pqrr_dev_pair_bounds", "pqrr_dev_save_quantizer",
+    "pqrr_dev_pair_bounds", "pqrr_dev_exact_knn_u8", "pqrr_dev_exact_knn_synthetic", "pqrr_dev_save_quantizer",
     "pqrr_dev_load_quantizer", "pqrr_dev_save_index", "pqrr_dev_load_index",
     "pqrr_dev_save_adc_index", "pqrr_dev_load_adc_index", "pqrr_dev_probe_index_kind",
 ]

@@ -6,6 +6,7 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <functional>
 #include <stdexcept>
 #include <string>
 
@@ -25,6 +26,13 @@ struct ArgError : std::invalid_argument {
             throw ::pqrr_b200::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 #define PQRR_LAUNCH_CHECK() PQRR_CUDA(cudaGetLastError())
+
+// Exact k-NN of u8 vectors (k_exact.cu): d = 128; the base arrives in chunks
+// through fetch(row0, n, device dst); ids are id_base + row.
+bool exact_knn_supported(uint32_t d);
+void exact_knn_u8(const uint8_t* d_queries, size_t nq, size_t n, uint64_t id_base, uint32_t k,
+                  const std::function<void(uint64_t, uint32_t, uint8_t*)>& fetch, uint32_t* out_ids,
+                  float* out_dists, uint32_t* out_cnt, cudaStream_t s);
 
 // Sets the calling thread's pqrr_dev_last_error() text; returns `code`.
 int report_error(int code, const std::string& msg);

@@ -1877,6 +1877,54 @@ int pqrr_dev_pair_bounds(int device, const float* queries, size_t nq, uint32_t d
     });
 }
 
+// compute_groundtruth / exact_search (eval.hpp:13-19) for u8 vectors: the
+// exact k nearest base rows of every query under (dist, id), on the integer
+// tensor cores (k_exact.cu).  Base rows from host memory, or generated on the
+// device (the synthetic base set, rows [row0, row0 + n), ids = row index).
+static int exact_knn_impl(int device, const uint8_t* base, uint64_t seed, uint32_t clusters, uint64_t row0,
+                          size_t n, const uint8_t* queries, size_t nq, uint32_t d, uint32_t k,
+                          uint32_t* out_ids, float* out_dists, uint32_t* out_counts) {
+    return guarded([&] {
+        if (!exact_knn_supported(d)) throw UnsupportedError("exact k-NN on the device needs d = 128");
+        if (k == 0 || k > 16384) throw UnsupportedError("exact k-NN supports 1 <= k <= 16384");
+        if (n > 0xffffffffull || row0 + n > 0x100000000ull) throw ArgError("ids exceed the 32-bit id space");
+        if (nq == 0) return;
+        Session se(device);
+        Workspace ws(se.s);
+        const uint8_t* dq = se.upload(ws, queries, nq * d);
+        double* centers = nullptr;
+        if (!base) {
+            if (clusters == 0) throw ArgError("clusters must be positive");
+            centers = ws.alloc<double>((size_t)clusters * d);
+            launch_synth_centers(seed, clusters, d, centers, se.s);
+        }
+        auto fetch = [&](uint64_t r0, uint32_t nb, uint8_t* dst) {
+            if (base)
+                PQRR_CUDA(cudaMemcpyAsync(dst, base + r0 * d, (size_t)nb * d, cudaMemcpyHostToDevice, se.s));
+            else
+                launch_synth_rows(seed, 2, row0 + r0, nb, d, centers, clusters, dst, se.s);
+        };
+        if (n == 0) {
+            for (size_t q = 0; q < nq; ++q) out_counts[q] = 0;
+            return;
+        }
+        exact_knn_u8(dq, nq, n, base ? 0 : row0, k, fetch, out_ids, out_dists, out_counts, se.s);
+    });
+}
+
+int pqrr_dev_exact_knn_u8(int device, const uint8_t* base, size_t n, const uint8_t* queries, size_t nq,
+                          uint32_t d, uint32_t k, uint32_t* out_ids, float* out_dists, uint32_t* out_counts) {
+    if (!base && n) return report_error(PQRR_EINVAL, "base is NULL");
+    return exact_knn_impl(device, base, 0, 0, 0, n, queries, nq, d, k, out_ids, out_dists, out_counts);
+}
+
+int pqrr_dev_exact_knn_synthetic(int device, uint64_t seed, uint32_t clusters, uint64_t row0, size_t n,
+                                 const uint8_t* queries, size_t nq, uint32_t k, uint32_t* out_ids,
+                                 float* out_dists, uint32_t* out_counts) {
+    return exact_knn_impl(device, nullptr, seed, clusters, row0, n, queries, nq, 128, k, out_ids, out_dists,
+                          out_counts);
+}
+
 // ---------------------------------------------------------------- ADC / ADC+R
 // The exhaustive index (adc_index.hpp:13-31) is the IVF machinery with ONE
 // all-zero coarse centroid: y - 0 = y and x - 0 = x exactly in fp32, and

@@ -702,3 +702,36 @@ def test_far_pair_bound_is_a_certified_lower_bound(pq, oracle, mid_instance):
                 ratios.append(out[q, r] / sm)
         assert np.all(out[:, :R1] == 0)
         assert np.median(ratios) > 0.98
+
+
+def test_exact_knn_groundtruth(pq, oracle, mid_instance):
+    """compute_groundtruth / exact_search (eval.hpp:13-19) on the integer tensor
+    cores == a float64 brute force under (dist, id), incl. duplicated base rows
+    (ties broken by id), k > n, and the device-generated base set."""
+    mi = mid_instance
+    base, q = mi["base"][:30000].copy(), mi["queries"][:40]
+    base[777] = base[5]  # exact ties
+    base[20001] = q[3]   # distance 0
+    gt = pq.compute_groundtruth(base, q, 50)
+    bf, qf = base.astype(np.float64), q.astype(np.float64)
+    d = (qf * qf).sum(1)[:, None] + (bf * bf).sum(1)[None, :] - 2 * qf @ bf.T
+    for i in range(len(q)):
+        order = np.lexsort((np.arange(len(base)), d[i]))[:50]
+        np.testing.assert_array_equal(gt.ids[i], order)
+        np.testing.assert_array_equal(gt.dists[i], d[i, order].astype(np.float32))
+    nn, _ = oracle.exact_nearest(base.astype(np.float32), q.astype(np.float32))
+    np.testing.assert_array_equal(gt.ids[:, 0], nn)
+    g1 = pq.compute_groundtruth(base, q, 1)  # k = 1: the fused-argmin path
+    np.testing.assert_array_equal(g1.ids[:, 0], nn)
+    np.testing.assert_array_equal(g1.dists[:, 0], gt.dists[:, 0])
+    assert pq.groundtruth_synthetic(0, 256, 120_000, q, 1).ids[:, 0].tolist() == \
+        pq.compute_groundtruth(mi["base"], q, 1).ids[:, 0].tolist()
+    one = pq.exact_search(base, q[7], 3)
+    np.testing.assert_array_equal(one.ids, gt.ids[7, :3])
+    small = pq.compute_groundtruth(base[:20], q[:2], 50)  # k > n returns n entries
+    assert small.k == 20
+    gs = pq.groundtruth_synthetic(0, 256, 120_000, q, 10)
+    full = pq.compute_groundtruth(mi["base"], q, 10)
+    np.testing.assert_array_equal(gs.ids, full.ids)
+    res = [pq.SearchResult(full.ids[i, :10].astype(np.uint32), full.dists[i, :10]) for i in range(len(q))]
+    assert pq.recall_at_r(res, full, 1) == 1.0
