@@ -701,14 +701,16 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     Workspace ws(s);
 
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[0], s));
-    // ---- K1: coarse distances + top-w probes.  Kc >= 2048: tensor-core
+    // ---- K1: coarse distances + top-w probes.  Kc >= 1024: tensor-core
     // distances with a certified candidate set recomputed exactly
     // (k_coarse_tc.cu); a query whose candidate set overflows restarts the
     // batch on the exact CUDA-core path (checked at the first readback below)
     float* D = ws.alloc<float>(nq * (size_t)c);
     uint32_t* probes = ws.alloc<uint32_t>(P);
     static const bool exact_coarse_env = getenv("PQRR_COARSE") && std::string(getenv("PQRR_COARSE")) == "exact";
-    const bool coarse_tc = !exact_coarse && !exact_coarse_env && c >= 2048 && coarse_tc_supported(ix.d, w);
+    static const uint32_t tc_min_c = getenv("PQRR_COARSE_TC_MIN") ? (uint32_t)atoi(getenv("PQRR_COARSE_TC_MIN"))
+                                                                   : 1024u;  // tuning hook
+    const bool coarse_tc = !exact_coarse && !exact_coarse_env && c >= tc_min_c && coarse_tc_supported(ix.d, w);
     uint32_t* coarse_ovf = ws.zeros<uint32_t>(1);
     if (coarse_tc) {
         if (!ix.cnorm.p) {

@@ -300,9 +300,9 @@ def test_large_coarse_radix_probe_selection(pq, oracle):
             np.testing.assert_array_equal(bits(dd[i, :oc[i]]), bits(od[i, :oc[i]]))
 
 
-@pytest.mark.parametrize("kc", [2048, 4096])
+@pytest.mark.parametrize("kc", [1024, 2048, 4096])
 def test_tensor_core_coarse_certified_probes(pq, oracle, kc):
-    """Kc >= 2048 with d = 128 takes the TF32 coarse GEMM + certify path
+    """Kc >= 1024 with d = 128 takes the TF32 coarse GEMM + certify path
     (k_coarse_tc.cu).  Fractional centroids make the TF32 rounding real, a
     ragged batch spans several 64-query GEMM tiles, and centroid pairs that
     differ by one ulp in one coordinate put near-ties inside the error bound;
@@ -311,7 +311,7 @@ def test_tensor_core_coarse_certified_probes(pq, oracle, kc):
     base = rng.integers(0, 120, (30000, 128)).astype(np.uint8)
     coarse = (base[rng.choice(30000, kc, replace=False)].astype(np.float32)
               + rng.standard_normal((kc, 128)).astype(np.float32) * 3.3)
-    for a, b in [(11, 900), (12, 901), (13, 1500)]:
+    for a, b in [(11, 900), (12, 901), (13, 1000)]:
         coarse[b] = coarse[a]
         coarse[b, a % 128] = np.nextafter(coarse[a, a % 128], np.float32(np.inf))
     books = (rng.standard_normal((8, 256, 16)) * 6).astype(np.float32)
