@@ -408,7 +408,10 @@ def main():
                           "lookups_per_clk_per_sm": lk_per_clk,
                           "fp32_gather_bound_lookups_per_clk": 32.0,
                           "vs_fp32_gather_bound": lk_per_clk / 32.0, "sm_count": n_sm,
-                          "sm_clock_mhz": f_sm / 1e6},
+                          "sm_clock_mhz": f_sm / 1e6,
+                          "note": "algorithmic lookups: 8 per (probed entry, query); K4f executes only "
+                                  "those of live (query, list) pairs (sum of LUT minima <= tau), the "
+                                  "others are settled without a lookup"},
         "filter": {"candidates_per_query": float(np.mean([s["candidates"] for s in stats])) / nq,
                    "exact_le_tau_per_query": float(np.mean([s["exact_candidates"] for s in stats])) / nq}
         if filt else None,
