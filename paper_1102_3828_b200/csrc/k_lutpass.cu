@@ -226,11 +226,13 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 const uint32_t slot = n % RING;
                 bool stop = false;
                 if (n >= RING) {
-                    while (!mbar_try(&bempty[slot], ((n / RING) - 1) & 1u))
+                    while (!mbar_try(&bempty[slot], ((n / RING) - 1) & 1u)) {
                         if (s_stop) {
                             stop = true;
                             break;
                         }
+                        __nanosleep(64);  // leave the issue slots to the consumer warps
+                    }
                 } else {
                     stop = s_stop != 0;
                 }
