@@ -973,10 +973,13 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
             put("cand_le.bin", cand_le, nq * 4);
             put("q8_param.bin", ix.q8_param.p, (size_t)n_items * kQT * 8);
             put("q8_cache.bin", ix.q8_cache.p, (size_t)n_items * 8 * 256 * kQT);
-            put("item_list.bin", im.item_list, n_items * 4);
-            put("item_start.bin", im.item_start, n_items * 4);
-            put("item_nq.bin", im.item_nq, n_items * 4);
-            put("pair_sorted.bin", im.pair_sorted, P * 4);
+            // the LUT-pass items (the near set of a two-phase search)
+            const ItemSet& lp = two_phase ? im_near : im;
+            const size_t np_lp = two_phase ? nq * (size_t)R1 : P;
+            put("item_list.bin", lp.item_list, lp.n_items * 4);
+            put("item_start.bin", lp.item_start, lp.n_items * 4);
+            put("item_nq.bin", lp.item_nq, lp.n_items * 4);
+            put("pair_sorted.bin", lp.pair_sorted, np_lp * 4);
             put("cand_pos.bin", cand_pos, nq * (size_t)cap * 4);
             put("cand_dist.bin", cand_dist, nq * (size_t)cap * 4);
         }
