@@ -1007,6 +1007,15 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
                                                 reinterpret_cast<unsigned long long*>(maxn + 4));
     PQRR_LAUNCH_CHECK();
     count_launch();
+    // the unsorted selection (a re-rank follows) needs no host-side count:
+    // queue it before the readback so the GPU stays busy during the round
+    // trip (rows that fail the check are redone and overwritten below)
+    const bool early_select = !sorted;
+    if (early_select) {
+        launch_select_topk(cand_dist, cand_pos, cand_cnt, cap, cap, nq, ix.ids.p, kprime, sorted,
+                           reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s);
+        if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[6], s));
+    }
     std::vector<uint8_t> h_fail(nq);
     unsigned h_maxn[6] = {0, 0, 0, 0, 0, 0};
     PQRR_CUDA(cudaMemcpyAsync(h_fail.data(), fail, nq, cudaMemcpyDeviceToHost, s));
@@ -1019,11 +1028,13 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     std::memcpy(&total_cand, h_maxn + 2, 8);
     std::memcpy(&total_le, h_maxn + 4, 8);
 
-    // ---- exact top-k' selection
-    launch_select_topk(cand_dist, cand_pos, cand_cnt, cap, h_maxn[0], nq, ix.ids.p, kprime, sorted,
-                       reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s);
-    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[6], s));
-    PQRR_CUDA(cudaStreamSynchronize(s));
+    // ---- exact top-k' selection (sorted: smem sized by the largest count)
+    if (!early_select) {
+        launch_select_topk(cand_dist, cand_pos, cand_cnt, cap, h_maxn[0], nq, ix.ids.p, kprime, sorted,
+                           reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s);
+        if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[6], s));
+        PQRR_CUDA(cudaStreamSynchronize(s));
+    }
     if (timed) {
         st.candidates += total_cand;
         st.exact_candidates += use_filter ? total_le : total_cand;
