@@ -78,7 +78,7 @@ void launch_iota(uint32_t* out, size_t n, cudaStream_t s) {
 // Small sorts (the work-item inversions of small batches): one CTA, bitonic
 // sort of (key << 32 | index) in shared memory — stable like the radix sort,
 // one launch instead of CUB's several.
-constexpr int kSmallSort = 4096;
+constexpr int kSmallSort = 1024;  // above ~1k the bitonic stages cost more than CUB's passes
 __global__ __launch_bounds__(1024) void small_sort_pairs_kernel(const uint32_t* __restrict__ keys_in,
                                                                uint32_t* __restrict__ keys_out,
                                                                const uint32_t* __restrict__ vals_in,
