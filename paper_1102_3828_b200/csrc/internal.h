@@ -269,7 +269,7 @@ void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,
                         const uint32_t* list_len, uint32_t nlists, const uint32_t* item_off,
                         uint32_t* item_list, uint32_t* item_start, uint32_t* item_nq,
                         uint32_t* item_e0, uint32_t* item_e1, uint32_t* sort_key, uint32_t qt,
-                        cudaStream_t s, uint32_t chunk = 1u << 30);
+                        cudaStream_t s, uint32_t chunk, uint32_t n_items);
 void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, uint32_t nlists,
                            uint32_t* items, uint32_t qt, cudaStream_t s, uint32_t chunk = 1u << 30);
 // Per query: N_q = sum of probed list lengths; per pair sample counts.

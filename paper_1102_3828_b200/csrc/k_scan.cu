@@ -429,6 +429,8 @@ __global__ void items_per_list_kernel(const uint32_t* __restrict__ cnt,
     if (l == nlists) items[l] = 0;
 }
 
+// One thread per item: its list by binary search over item_off (items of a
+// list are contiguous: groups of qt pairs x entry chunks).
 __global__ void items_build_kernel(const uint32_t* __restrict__ cnt,
                                    const uint32_t* __restrict__ first,
                                    const uint32_t* __restrict__ len, uint32_t nlists,
@@ -437,22 +439,25 @@ __global__ void items_build_kernel(const uint32_t* __restrict__ cnt,
                                    uint32_t* __restrict__ item_nq, uint32_t* __restrict__ item_e0,
                                    uint32_t* __restrict__ item_e1, uint32_t* __restrict__ sort_key,
                                    uint32_t qt, uint32_t chunk) {
-    uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= nlists) return;
-    const uint32_t c = cnt[l], L = len[l];
-    const uint32_t chunks = max(1u, (L + chunk - 1) / chunk);
-    uint32_t o = item_off[l];
-    for (uint32_t s = 0; s < c; s += qt) {
-        for (uint32_t ch = 0; ch < chunks; ++ch, ++o) {
-            const uint32_t e0 = ch * chunk, e1 = min(L, e0 + chunk);
-            item_list[o] = l;
-            item_start[o] = first[l] + s;
-            item_nq[o] = min(qt, c - s);
-            item_e0[o] = e0;
-            item_e1[o] = e1;
-            sort_key[o] = 0xffffffffu - (e1 - e0);  // ascending sort = longest first
-        }
+    const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= item_off[nlists]) return;
+    uint32_t lo = 0, hi = nlists;  // last list with item_off[l] <= o
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (item_off[mid] <= o) lo = mid;
+        else hi = mid;
     }
+    const uint32_t l = lo, c = cnt[l], L = len[l];
+    const uint32_t chunks = max(1u, (L + chunk - 1) / chunk);
+    const uint32_t k = o - item_off[l];
+    const uint32_t grp = k / chunks, ch = k % chunks;
+    const uint32_t e0 = ch * chunk, e1 = min(L, e0 + chunk);
+    item_list[o] = l;
+    item_start[o] = first[l] + grp * qt;
+    item_nq[o] = min(qt, c - grp * qt);
+    item_e0[o] = e0;
+    item_e1[o] = e1;
+    sort_key[o] = 0xffffffffu - (e1 - e0);  // ascending sort = longest first
 }
 
 template <int DSUB>
@@ -492,10 +497,11 @@ void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,
                         const uint32_t* list_len, uint32_t nlists, const uint32_t* item_off,
                         uint32_t* item_list, uint32_t* item_start, uint32_t* item_nq,
                         uint32_t* item_e0, uint32_t* item_e1, uint32_t* sort_key, uint32_t qt,
-                        cudaStream_t s, uint32_t chunk) {
-    items_build_kernel<<<(nlists + 255) / 256, 256, 0, s>>>(list_cnt, list_first, list_len, nlists,
-                                                            item_off, item_list, item_start, item_nq,
-                                                            item_e0, item_e1, sort_key, qt, chunk);
+                        cudaStream_t s, uint32_t chunk, uint32_t n_items) {
+    if (n_items == 0) return;
+    items_build_kernel<<<(n_items + 255) / 256, 256, 0, s>>>(list_cnt, list_first, list_len, nlists,
+                                                             item_off, item_list, item_start, item_nq,
+                                                             item_e0, item_e1, sort_key, qt, chunk);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

@@ -660,7 +660,7 @@ void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_l
     uint32_t* iota = ws.alloc<uint32_t>(n);
     it.item_order = ws.alloc<uint32_t>(n);
     launch_items_build(it.list_cnt, it.list_first, list_len, c, it.item_off, it.item_list,
-                       it.item_start, it.item_nq, it.item_e0, it.item_e1, key, it.qt, s, it.chunk);
+                       it.item_start, it.item_nq, it.item_e0, it.item_e1, key, it.qt, s, it.chunk, n);
     launch_iota(iota, n, s);
     sort_pairs(key, key2, iota, it.item_order, n, 32, s);
 }
