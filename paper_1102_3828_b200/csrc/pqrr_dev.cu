@@ -582,10 +582,11 @@ __global__ void pair_key_kernel(const uint32_t* __restrict__ lists, const uint32
     const size_t q = p / w;
     const float gap = fmaxf(__fsub_rn(D[q * c + lists[i]], D[q * c + probes[q * w]]), 0.f);
     // the sampling tier of the probe rank first (a 16-query block then shares
-    // one sampling stride in the LUT pass), then the gap (bits 30..17 of a
-    // non-negative float: 14 bits, monotone)
+    // one sampling stride in the LUT pass), then the gap (bits 30..19 of a
+    // non-negative float: exponent + 4 mantissa bits, monotone): 14 key bits
+    // below the list, so Kc = 1024 sorts in 3 radix passes
     const uint32_t tier = sample_tier(p % w, w, 1);
-    key[i] = (lists[i] << 16) | (tier << 14) | (__float_as_uint(gap) >> 17);
+    key[i] = (lists[i] << 14) | (tier << 12) | (__float_as_uint(gap) >> 19);
 }
 
 // Two-phase LUT pass: pairs of probe rank r < R1 (near) and r >= R1 (far).
@@ -627,12 +628,12 @@ ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_
     } else {
         uint32_t* sorted_keys = ws.alloc<uint32_t>(np);
         it.pair_sorted = ws.alloc<uint32_t>(np);
-        if (D && bits_for(c) <= 16) {
+        if (D && bits_for(c) <= 18) {
             uint32_t* key = ws.alloc<uint32_t>(np);
             pair_key_kernel<<<nblk(np), 256, 0, s>>>(lists, pair_ids, np, w, D, c, probes ? probes : lists, key);
             PQRR_LAUNCH_CHECK();
             count_launch();
-            sort_pairs(key, sorted_keys, pair_ids, it.pair_sorted, np, 16 + bits_for(c), s);
+            sort_pairs(key, sorted_keys, pair_ids, it.pair_sorted, np, 14 + bits_for(c), s);
         } else {
             sort_pairs(lists, sorted_keys, pair_ids, it.pair_sorted, np, bits_for(c), s);
         }
