@@ -539,8 +539,11 @@ __device__ __forceinline__ uint32_t warp_weighted_select(uint32_t n, uint32_t ra
     int consumed = __clz(kmin ^ kmax);
     uint32_t prefix = consumed ? kmin >> (32 - consumed) : 0u;
     uint32_t r = rank;
+    // the threshold is an estimate (exactness is checked downstream): stop with
+    // <= 8 low bits undecided and return the bin's upper edge (a relative
+    // over-estimate below 2^-15), saving the last pass over the samples
 #pragma unroll 1
-    while (consumed < 32) {
+    while (consumed < 24) {
         const int wd = min(8, 32 - consumed);
         const int sh = 32 - consumed - wd;
         const uint32_t msk = (1u << wd) - 1u;
@@ -596,7 +599,9 @@ __device__ __forceinline__ uint32_t warp_weighted_select(uint32_t n, uint32_t ra
         consumed += wd;
         __syncwarp();
     }
-    return prefix;
+    if (consumed >= 32) return prefix;
+    const int rest = 32 - consumed;
+    return (prefix << rest) | ((1u << rest) - 1u);
 }
 
 // tau_q (one query per warp): the distance at which the weighted count of the
