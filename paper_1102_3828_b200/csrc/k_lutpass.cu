@@ -407,12 +407,17 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
             // a warp's stores cover 4 lanes x 32 contiguous bytes
             uint32_t* block = reinterpret_cast<uint32_t*>(a.q8_cache + (size_t)it * Q8_BYTES);
             const int g = t & 3;
-            const float4 inv = *reinterpret_cast<const float4*>(s_inv + 4 * g);
+            // 1/s with the (1 - 2^-20) shrink folded in: fsub, rcp, this product
+            // and the per-entry product are 4 roundings, (1 + 2^-24)^4 (1 - 2^-20) < 1,
+            // so v8 = floor(x) <= (L - m) / s as before
             const float shrink = 0.99999904632568359375f;  // 1 - 2^-20
+            const float4 inv0 = *reinterpret_cast<const float4*>(s_inv + 4 * g);
+            const float4 inv = make_float4(__fmul_rn(inv0.x, shrink), __fmul_rn(inv0.y, shrink),
+                                           __fmul_rn(inv0.z, shrink), __fmul_rn(inv0.w, shrink));
             // floor(x) for 0 <= x <= 255 without the quarter-rate F2I:
             // x + 2^23 rounded down has ulp 1, so its low byte is floor(x)
-            auto q8 = [&](float L, float m, float iv) -> uint32_t {
-                const float x = fminf(__fmul_rn(__fmul_rn(__fsub_rn(L, m), iv), shrink), 255.f);
+            auto q8 = [&](float L, float m, float ivs) -> uint32_t {
+                const float x = fminf(__fmul_rn(__fsub_rn(L, m), ivs), 255.f);
                 return __float_as_uint(__fadd_rd(x, 8388608.f));
             };
 #pragma unroll 2
