@@ -262,7 +262,7 @@ void launch_recheck(const float* xq, uint32_t d, uint32_t m, const float* coarse
                     const float* books, const uint32_t* probes, uint32_t w, const uint8_t* codes,
                     const uint32_t* cand_cnt, uint32_t cap, const uint32_t* cand_pos,
                     float* cand_dist, const float* tau, size_t nq, uint32_t* cand_le,
-                    cudaStream_t s);
+                    cudaStream_t s, uint32_t* cand_mm = nullptr);
 
 // Build the scan work items from the probes.
 void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,
@@ -286,7 +286,8 @@ void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_of
 void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
                         uint32_t cap, uint32_t max_n, size_t nq, const uint32_t* ids,
                         uint32_t kprime, bool sorted, uint64_t* sl_key, uint32_t* sl_pos,
-                        uint32_t* sl_cnt, cudaStream_t s);
+                        uint32_t* sl_cnt, cudaStream_t s,
+                        const uint32_t* cand_mm = nullptr);
 // Re-rank the shortlist with the 3-term reconstruction, keep the k best.
 void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_t* sl_cnt,
                    uint32_t sl_stride, size_t nq, const float* xq, uint32_t d,
@@ -310,7 +311,8 @@ bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32
                       float* out_dist, cudaStream_t s);
 void launch_select_warp(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
                         uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime,
-                        uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s);
+                        uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s,
+                        const uint32_t* cand_mm = nullptr);
 void launch_threshold_warp(const float* sample_dist, const uint64_t* sample_off, uint32_t w, size_t nq,
                            const uint8_t* query_sampled, float alpha_k, uint32_t stride, int tiered,
                            float* tau, cudaStream_t s);

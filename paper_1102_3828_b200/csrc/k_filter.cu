@@ -414,12 +414,12 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
     const u64* __restrict__ codes, const uint32_t* __restrict__ cand_cnt, uint32_t cap,
     const uint32_t* __restrict__ cand_pos, float* __restrict__ cand_dist,
     const float* __restrict__ tau, size_t nq, uint32_t* __restrict__ cand_le,
-    uint32_t* __restrict__ counter, const u64 nz) {
+    uint32_t* __restrict__ counter, const u64 nz, uint32_t* __restrict__ cand_mm) {
     constexpr int CH = DSUB / 4;  // 16-byte chunks per subspace row
     extern __shared__ float4 smem_k[];
     float4* bk = smem_k;                      // [M][KS][CH], swizzled
     float4* res = smem_k + M * KS * CH;       // [w][d / 4], swizzled
-    __shared__ uint32_t s_q, s_le;
+    __shared__ uint32_t s_q, s_le, s_mn, s_mx;
     // per-warp exchange of the 8 sub-space terms of 4 x 4 candidates:
     // [round u][slot][j], rows of 36 floats (conflict-free writes and reads)
     __shared__ __align__(16) float s_x[16][4 * 36];
@@ -439,6 +439,8 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
         if (threadIdx.x == 0) {
             s_q = atomicAdd(counter, 1u);
             s_le = 0;
+            s_mn = 0xffffffffu;
+            s_mx = 0u;
         }
         __syncthreads();
         const size_t q = s_q;
@@ -448,6 +450,7 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
             if (threadIdx.x == 0) cand_le[q] = 0;
             continue;
         }
+        uint32_t dmn = 0xffffffffu, dmx = 0u;  // the exact distances' range (select_warp)
         for (uint32_t i = threadIdx.x; i < w * dch; i += blockDim.x) {
             const uint32_t r = i / dch, c = i % dch;
             const uint32_t l = probes[q * w + r];
@@ -555,13 +558,32 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
                 if (i < n) {
                     cand_dist[q * cap + i] = acc;
                     le += acc <= tq ? 1u : 0u;
+                    dmn = min(dmn, __float_as_uint(acc));
+                    dmx = max(dmx, __float_as_uint(acc));
                 }
             }
             __syncwarp();
         }
         if (le) atomicAdd(&s_le, le);
+        if (cand_mm) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                dmn = min(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+                dmx = max(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+            }
+            if (lane == 0) {
+                atomicMin(&s_mn, dmn);
+                atomicMax(&s_mx, dmx);
+            }
+        }
         __syncthreads();
-        if (threadIdx.x == 0) cand_le[q] = s_le;
+        if (threadIdx.x == 0) {
+            cand_le[q] = s_le;
+            if (cand_mm) {
+                cand_mm[2 * q] = s_mn;
+                cand_mm[2 * q + 1] = s_mx;
+            }
+        }
     }
 }
 
@@ -680,7 +702,7 @@ template <int DSUB>
 bool recheck_smem_t(const float* xq, uint32_t d, const float* coarse, const float* books,
                     const uint32_t* probes, uint32_t w, const uint8_t* codes, const uint32_t* cand_cnt,
                     uint32_t cap, const uint32_t* cand_pos, float* cand_dist, const float* tau,
-                    size_t nq, uint32_t* cand_le, cudaStream_t s) {
+                    size_t nq, uint32_t* cand_le, cudaStream_t s, uint32_t* cand_mm) {
     const size_t smem = (size_t)M * KS * DSUB * sizeof(float) + (size_t)w * d * sizeof(float);
     if (smem > 216 * 1024) return false;  // + ~9.3 KiB static (s_x) <= 227 KiB
     PQRR_CUDA(cudaFuncSetAttribute(recheck_smem_kernel<DSUB>,
@@ -690,7 +712,7 @@ bool recheck_smem_t(const float* xq, uint32_t d, const float* coarse, const floa
     PQRR_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), s));
     recheck_smem_kernel<DSUB><<<sm_count(), 512, smem, s>>>(
         xq, d, coarse, books, probes, w, reinterpret_cast<const u64*>(codes), cand_cnt, cap, cand_pos,
-        cand_dist, tau, nq, cand_le, counter, kNegZero2);
+        cand_dist, tau, nq, cand_le, counter, kNegZero2, cand_mm);
     PQRR_LAUNCH_CHECK();
     PQRR_CUDA(cudaFreeAsync(counter, s));
     count_launch();
@@ -701,16 +723,16 @@ void launch_recheck(const float* xq, uint32_t d, uint32_t m, const float* coarse
                     const float* books, const uint32_t* probes, uint32_t w, const uint8_t* codes,
                     const uint32_t* cand_cnt, uint32_t cap, const uint32_t* cand_pos,
                     float* cand_dist, const float* tau, size_t nq, uint32_t* cand_le,
-                    cudaStream_t s) {
+                    cudaStream_t s, uint32_t* cand_mm) {
     if (!nq) return;
     static const bool plain = getenv("PQRR_RECHECK") && std::string(getenv("PQRR_RECHECK")) == "global";
     if (!plain && d / m == 16 &&
         recheck_smem_t<16>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist,
-                           tau, nq, cand_le, s))
+                           tau, nq, cand_le, s, cand_mm))
         return;
     if (!plain && d / m == 8 &&
         recheck_smem_t<8>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist,
-                          tau, nq, cand_le, s))
+                          tau, nq, cand_le, s, cand_mm))
         return;
     switch (d / m) {
         case 16: return recheck_t<16>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s);

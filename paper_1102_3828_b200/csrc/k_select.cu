@@ -995,11 +995,13 @@ void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_of
 void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
                         uint32_t cap, uint32_t max_n, size_t nq, const uint32_t* ids,
                         uint32_t kprime, bool sorted, uint64_t* sl_key, uint32_t* sl_pos,
-                        uint32_t* sl_cnt, cudaStream_t s) {
+                        uint32_t* sl_cnt, cudaStream_t s,
+                        const uint32_t* cand_mm) {
     if (nq == 0) return;
     static const bool old_select = getenv("PQRR_SELECT") && std::string(getenv("PQRR_SELECT")) == "cta";
     if (!sorted && !old_select) {  // unsorted shortlist (re-ranked next): warp per query
-        launch_select_warp(cand_dist, cand_pos, cand_cnt, cap, nq, ids, kprime, sl_key, sl_pos, sl_cnt, s);
+        launch_select_warp(cand_dist, cand_pos, cand_cnt, cap, nq, ids, kprime, sl_key, sl_pos, sl_cnt, s,
+                           cand_mm);
         return;
     }
     uint32_t kp2 = 1;

@@ -30,11 +30,14 @@ constexpr uint32_t TIE_CAP = 256;  // boundary ties sorted in shared memory
 template <class KeyF>
 __device__ __forceinline__ void warp_radix_select(uint32_t n, uint32_t rank, KeyF key,
                                                   uint32_t* __restrict__ hist, uint32_t& kth,
-                                                  uint32_t& r_eq) {
+                                                  uint32_t& r_eq, uint32_t kmin0 = 0xffffffffu,
+                                                  uint32_t kmax0 = 0u) {
     const int lane = threadIdx.x & 31;
     constexpr int U = 8;  // loads in flight per lane
-    uint32_t kmin = 0xffffffffu, kmax = 0u;
-    for (uint32_t base = 0; base < n; base += 32 * U) {
+    // the key range, when the producer already knows it (K4r), saves a pass
+    const bool known = kmin0 <= kmax0 && kmax0 != 0xffffffffu;  // (all-ones = not provided)
+    uint32_t kmin = known ? kmin0 : 0xffffffffu, kmax = known ? kmax0 : 0u;
+    for (uint32_t base = 0; !known && base < n; base += 32 * U) {
         uint32_t v[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
@@ -336,7 +339,7 @@ __global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
     const float* __restrict__ cand_dist, const uint32_t* __restrict__ cand_pos,
     const uint32_t* __restrict__ cand_cnt, uint32_t cap, size_t nq, const uint32_t* __restrict__ ids,
     uint32_t kprime, u64* __restrict__ sl_key, uint32_t* __restrict__ sl_pos,
-    uint32_t* __restrict__ sl_cnt) {
+    uint32_t* __restrict__ sl_cnt, const uint32_t* __restrict__ cand_mm) {
     __shared__ uint32_t hist_all[WS_WARPS][256];
     __shared__ u64 tie_all[WS_WARPS][TIE_CAP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -358,7 +361,8 @@ __global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
         return;
     }
     uint32_t kth, r_eq;
-    warp_radix_select(n, kprime, [&](uint32_t i) { return dq[i]; }, hist_all[warp], kth, r_eq);
+    warp_radix_select(n, kprime, [&](uint32_t i) { return dq[i]; }, hist_all[warp], kth, r_eq,
+                      cand_mm ? cand_mm[2 * q] : 0xffffffffu, cand_mm ? cand_mm[2 * q + 1] : 0u);
     // one pass, 8 chunks of 32 per iteration (loads hoisted): entries strictly
     // below the boundary go out directly; entries at the boundary distance go
     // to a per-warp tie buffer as (id, pos) (exact ADC ties are common: equal
@@ -660,11 +664,12 @@ bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32
 
 void launch_select_warp(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
                         uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime,
-                        uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s) {
+                        uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s,
+                        const uint32_t* cand_mm) {
     if (nq == 0) return;
     select_warp_kernel<<<(unsigned)((nq + WS_WARPS - 1) / WS_WARPS), WS_WARPS * 32, 0, s>>>(
         cand_dist, cand_pos, cand_cnt, cap, nq, ids, kprime, reinterpret_cast<u64*>(sl_key), sl_pos,
-        sl_cnt);
+        sl_cnt, cand_mm);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

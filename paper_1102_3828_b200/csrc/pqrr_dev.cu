@@ -905,6 +905,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     uint32_t* cand_pos = ws.alloc<uint32_t>(nq * (size_t)cap);
     uint32_t* cand_cnt = ws.zeros<uint32_t>(nq);
     uint32_t* cand_le = nullptr;
+    uint32_t* cand_mm = nullptr;
     if (use_filter) {
         FilterArgs f{};
         f.codes = ix.codes.p;
@@ -953,8 +954,11 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         launch_ivf_filter(f, s);
         if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[9], s));
         cand_le = ws.alloc<uint32_t>(nq);
+        // exact distances' range per query (K4r smem variant; all-ones = unknown)
+        cand_mm = ws.alloc<uint32_t>(2 * nq);
+        PQRR_CUDA(cudaMemsetAsync(cand_mm, 0xff, 2 * nq * sizeof(uint32_t), s));
         launch_recheck(xq, ix.d, ix.m, ix.coarse.p, ix.books.p, probes, w, ix.codes.p, cand_cnt, cap,
-                       cand_pos, cand_dist, tau, nq, cand_le, s);
+                       cand_pos, cand_dist, tau, nq, cand_le, s, cand_mm);
         static const char* dump = getenv("PQRR_DEBUG_DUMP");  // debug hook: raw filter state
         if (dump && depth == 0) {
             PQRR_CUDA(cudaStreamSynchronize(s));
@@ -1014,7 +1018,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     const bool early_select = !sorted;
     if (early_select) {
         launch_select_topk(cand_dist, cand_pos, cand_cnt, cap, cap, nq, ix.ids.p, kprime, sorted,
-                           reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s);
+                           reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s, cand_mm);
         if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[6], s));
     }
     std::vector<uint8_t> h_fail(nq);
