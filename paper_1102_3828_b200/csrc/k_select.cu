@@ -795,7 +795,7 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
             __syncwarp();
             const int cc = lane >> 2, k = lane & 3;
             float sacc = 0.f;
-#pragma unroll 8
+#pragma unroll
             for (int gg = 0; gg < 32; ++gg) sacc = __fadd_rn(sacc, tile[cc * RC_TLD + 4 * gg + k]);
             const float s1 = __shfl_down_sync(0xffffffffu, sacc, 1);
             const float pair = __fadd_rn(sacc, s1);  // lanes k = 0: s0+s1, k = 2: s2+s3
