@@ -766,12 +766,17 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
             const uint4 lq0 = reinterpret_cast<const uint4*>(m_list)[sb >> 2];
             const uint4 lq1 = reinterpret_cast<const uint4*>(m_list)[(sb >> 2) + 1];
             const uint32_t lids[8] = {lq0.x, lq0.y, lq0.z, lq0.w, lq1.x, lq1.y, lq1.z, lq1.w};
+            // runs of one list are long: a sub-batch changes list at most once
+            // in the common case, to the list of its last candidate, whose
+            // coarse row is fetched up front so the change does not stall
+            float4 cvn = cv;
+            if (lids[7] != cur_l) cvn = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)lids[7] * D) + g);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 const uint32_t ci = sb + c;
                 const uint32_t l = lids[c];
                 if (l != cur_l) {
-                    cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + g);
+                    cv = l == lids[7] ? cvn : __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + g);
                     cur_l = l;
                 }
                 float4 bv, rv;
