@@ -140,10 +140,10 @@ __host__ __device__ inline uint32_t sample_tier(uint32_t r, uint32_t w, int tier
     const uint32_t r8 = 8 * r;
     return r8 < w ? 0u : (r8 < 2 * w ? 1u : (r8 < 4 * w ? 2u : 3u));
 }
-// Stride shift of tier t: x2 per tier, x4 per tier when w >= 32 (many far
+// Stride shift of tier t: x2 per tier, x4 per tier when w >= 16 (many far
 // probes: at C3-C5 the shortlist lives in the first few probes, and the far
 // half would otherwise hold most samples).
-__host__ __device__ inline uint32_t tier_shift(uint32_t t, uint32_t w) { return w >= 32 ? 2 * t : t; }
+__host__ __device__ inline uint32_t tier_shift(uint32_t t, uint32_t w) { return w >= 16 ? 2 * t : t; }
 static const int kQT = 16;        // queries per scan work item
 static const int kScanThreads = 512;
 
