@@ -103,6 +103,16 @@ __device__ __forceinline__ bool pair_live(float tau, float summ) {
     return __fsub_rn(__fmul_rn(tau, e_up), __fmul_rn(summ, e_dn)) >= 0.f;
 }
 
+// Position of threshold sample si at stride st in a list of len entries.  The
+// list order pairs entries by code parity (pair_perm_kernel), so an even
+// stride alone would only ever sample one side of the pairs (a biased
+// sample: measured as frequent under-full retries at even strides).  A
+// Thue-Morse jitter popc(si) & 1 balances both sides on every sub-grid
+// si = k 2^s that the per-lane tiers of the LUT pass take.
+__device__ __forceinline__ uint32_t sample_pos(uint32_t si, uint32_t st, uint32_t len) {
+    return min(si * st + ((uint32_t)__popc(si) & 1u), len - 1u);
+}
+
 // 8-bit LUT block of a LUT-pass item (K2 -> K4f): LANE-major, 16 query lanes
 // x (M * KS) row bytes, so K4f can copy any lane's 2 KiB column with
 // coalesced 16-byte loads.  r0..r3 hold rows 4 rq .. 4 rq + 3, each the bytes

@@ -327,7 +327,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 const uint32_t ns = (e1 + smin - 1) / smin;
                 const u64* lcodes = reinterpret_cast<const u64*>(a.codes) + a.list_off[l];
                 for (uint32_t si = lane; si < min(ns, (uint32_t)SCAP); si += 32)
-                    cp8(scodes + b * SCAP + si, lcodes + (size_t)si * smin);
+                    cp8(scodes + b * SCAP + si, lcodes + sample_pos(si, smin, e1));
             }
             cp_commit();
             cp_wait<0>();
@@ -457,7 +457,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 sh[kk] = mt.sshift[qq];
             }
             for (uint32_t si = warp * 8 + slot; si < ns; si += NCW * 8) {
-                const u64 code = si < (uint32_t)SCAP ? sc[si] : __ldg(lcodes + (size_t)si * smin);
+                const u64 code = si < (uint32_t)SCAP ? sc[si] : __ldg(lcodes + sample_pos(si, smin, mt.e1));
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int j = 0; j < M; ++j) {

@@ -355,7 +355,7 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
 #pragma unroll
             for (int k = 0; k < PF; ++k) {
                 const uint32_t si = wbase + k * S + slot;
-                cbuf[k] = si < ns ? __ldg(lcodes + (size_t)(i0 + si) * a.stride) : 0ull;
+                cbuf[k] = si < ns ? __ldg(lcodes + sample_pos(i0 + si, a.stride, a.list_len[l])) : 0ull;
             }
             for (uint32_t wb = wbase; wb < ns; wb += PF * S) {
 #pragma unroll
@@ -365,7 +365,7 @@ __global__ __launch_bounds__(NT, 1) void ivf_scan_kernel(const ScanArgs a, const
                     const uint32_t si = sb + slot;
                     const u64 code = cbuf[kk];
                     const uint32_t sn = si + PF * S;
-                    cbuf[kk] = sn < ns ? __ldg(lcodes + (size_t)(i0 + sn) * a.stride) : 0ull;
+                    cbuf[kk] = sn < ns ? __ldg(lcodes + sample_pos(i0 + sn, a.stride, a.list_len[l])) : 0ull;
                     if (si >= ns) continue;
                     float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll

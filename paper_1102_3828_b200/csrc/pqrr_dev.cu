@@ -689,14 +689,16 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // >= 4k' for the exact scan, >= 8k' for the filter's superset; beyond
     // 8192 the selector streams candidates from global memory
     const uint32_t cap_mul = filter_ok ? 8 : 4;
-    const uint32_t cap = std::max<uint32_t>(8192, ((cap_mul * kprime + 1023) / 1024) * 1024) << cap_shift;
+    // (16k floor: a query whose sampled threshold lands high overflows into
+    // a retry, ~0.35 ms per batch; the buffer costs 8 B per slot)
+    const uint32_t cap = std::max<uint32_t>(16384, ((cap_mul * kprime + 1023) / 1024) * 1024) << cap_shift;
     // sample density: ~64 samples expected below the alpha*k'-th distance
     // tuning hook (read per search): expected samples below the target rank
-    // large k' (C4: 1e4): 2x the samples buy a 1.5 k' target instead of 2 k'
-    // (fewer survivors to recheck and select; measured 44.1 -> 40.7 ms at C4,
-    // a loss at k' = 1000 where the sampling dominates)
+    // Targets: 1.8 k' with 96 samples below it (C2 5.63 -> 5.50 ms, no
+    // retries; the samples are unbiased since sample_pos); large k' (C4: 1e4):
+    // 1.5 k' with 128 (44.1 -> 40.7 ms): fewer survivors to recheck and select
     const char* spq_env = getenv("PQRR_SAMPLES");
-    const double spq = spq_env ? std::max(1.0, atof(spq_env)) : (kprime >= 4096 ? 128.0 : 64.0);
+    const double spq = spq_env ? std::max(1.0, atof(spq_env)) : (kprime >= 4096 ? 128.0 : 96.0);
     uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / spq));
     stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
     Workspace ws(s);
@@ -1099,7 +1101,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
 // tuning hook PQRR_ALPHA (read per search).
 double default_alpha(uint32_t kprime) {
     const char* e = getenv("PQRR_ALPHA");
-    return e ? std::max(1.05, atof(e)) : (kprime >= 4096 ? 1.5 : 2.0);
+    return e ? std::max(1.05, atof(e)) : (kprime >= 4096 ? 1.5 : 1.8);
 }
 
 void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t kprime_sz,
@@ -1129,9 +1131,9 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
     {
         const double avg_len = ix.c ? (double)ix.n / ix.c : 0.0;
         const double stride = std::max(1.0, std::floor(default_alpha(kprime) * kprime /
-                                                        (kprime >= 4096 ? 128.0 : 64.0)));
+                                                        (kprime >= 4096 ? 128.0 : 96.0)));
         const double per_q = 2.0 * w * avg_len / stride * 4.0 + (w / 16.0 + 1.0) * 32768.0 +
-                             std::max(8192.0, 8.0 * kprime) * 8.0 + ix.c * 4.0 + w * 64.0;
+                             std::max(16384.0, 8.0 * kprime) * 8.0 + ix.c * 4.0 + w * 64.0;
         // cudaMemGetInfo costs ~1 ms with a large resident index: query it
         // only when the batch needs a sizeable share of the device
         static size_t dev_total = 0;
