@@ -666,6 +666,24 @@ void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_l
     sort_pairs(key, key2, iota, it.item_order, n, 32, s);
 }
 
+// Threshold target (alpha k' entries) and samples expected below it, tuned
+// per regime (tuning hooks PQRR_ALPHA / PQRR_SAMPLES, read per search):
+//   k' >= 4096 (C4): 1.5 / 128 — fewer survivors to recheck and select
+//     (44.1 -> 40.7 ms at C4);
+//   512 <= k' < 4096 and w < 32 (C2): 1.8 / 96 (5.63 -> 5.50 ms, no retries);
+//   otherwise 2.0 / 64 (small k' would sample every entry; w >= 32 takes
+//     tau from the near probes only).
+double default_alpha(uint32_t kprime, uint32_t w) {
+    const char* e = getenv("PQRR_ALPHA");
+    if (e) return std::max(1.05, atof(e));
+    return kprime >= 4096 ? 1.5 : (kprime >= 512 && w < 32 ? 1.8 : 2.0);
+}
+double default_spq(uint32_t kprime, uint32_t w) {
+    const char* e = getenv("PQRR_SAMPLES");
+    if (e) return std::max(1.0, atof(e));
+    return kprime >= 4096 ? 128.0 : (kprime >= 512 && w < 32 ? 96.0 : 64.0);
+}
+
 // Builds the exact top-kprime shortlist of every query into `out` (device,
 // [nq][kprime]).  alpha scales the sampled threshold rank (expected
 // candidates ~ alpha * kprime).
@@ -691,14 +709,11 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     const uint32_t cap_mul = filter_ok ? 8 : 4;
     // (16k floor: a query whose sampled threshold lands high overflows into
     // a retry, ~0.35 ms per batch; the buffer costs 8 B per slot)
-    const uint32_t cap = std::max<uint32_t>(16384, ((cap_mul * kprime + 1023) / 1024) * 1024) << cap_shift;
+    const uint32_t cap_floor = kprime >= 512 ? 16384u : 8192u;
+    const uint32_t cap = std::max<uint32_t>(cap_floor, ((cap_mul * kprime + 1023) / 1024) * 1024) << cap_shift;
     // sample density: ~64 samples expected below the alpha*k'-th distance
     // tuning hook (read per search): expected samples below the target rank
-    // Targets: 1.8 k' with 96 samples below it (C2 5.63 -> 5.50 ms, no
-    // retries; the samples are unbiased since sample_pos); large k' (C4: 1e4):
-    // 1.5 k' with 128 (44.1 -> 40.7 ms): fewer survivors to recheck and select
-    const char* spq_env = getenv("PQRR_SAMPLES");
-    const double spq = spq_env ? std::max(1.0, atof(spq_env)) : (kprime >= 4096 ? 128.0 : 96.0);
+    const double spq = default_spq(kprime, w);  // samples expected below the target rank
     uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / spq));
     stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
     Workspace ws(s);
@@ -1099,11 +1114,6 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
 
 // Target candidates per query = alpha * k' (the sampled threshold rank);
 // tuning hook PQRR_ALPHA (read per search).
-double default_alpha(uint32_t kprime) {
-    const char* e = getenv("PQRR_ALPHA");
-    return e ? std::max(1.05, atof(e)) : (kprime >= 4096 ? 1.5 : 1.8);
-}
-
 void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t kprime_sz,
                    size_t k_sz, uint32_t* out_ids, float* out_dists, uint32_t* out_cnt) {
     if (w < 1 || w > ix.c) throw ArgError("v must satisfy 1 <= v <= c");
@@ -1130,10 +1140,11 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
     // the candidate buffers and the coarse distance row.
     {
         const double avg_len = ix.c ? (double)ix.n / ix.c : 0.0;
-        const double stride = std::max(1.0, std::floor(default_alpha(kprime) * kprime /
-                                                        (kprime >= 4096 ? 128.0 : 96.0)));
+        const double stride = std::max(1.0, std::floor(default_alpha(kprime, w) * kprime /
+                                                        default_spq(kprime, w)));
         const double per_q = 2.0 * w * avg_len / stride * 4.0 + (w / 16.0 + 1.0) * 32768.0 +
-                             std::max(16384.0, 8.0 * kprime) * 8.0 + ix.c * 4.0 + w * 64.0;
+                             std::max(kprime >= 512 ? 16384.0 : 8192.0, 8.0 * kprime) * 8.0 + ix.c * 4.0 +
+                             w * 64.0;
         // cudaMemGetInfo costs ~1 ms with a large resident index: query it
         // only when the batch needs a sizeable share of the device
         static size_t dev_total = 0;
@@ -1150,7 +1161,7 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
         for (size_t c0 = 0; c0 < nq; c0 += chunk) {
             const size_t nc = std::min(chunk, nq - c0);
             ShortlistDev part{sl.key + c0 * kprime, sl.pos + c0 * kprime, sl.cnt + c0};
-            shortlist_core(ix, xq + c0 * ix.d, nc, w, kprime, k == 0, default_alpha(kprime), 1, part, 0, true);
+            shortlist_core(ix, xq + c0 * ix.d, nc, w, kprime, k == 0, default_alpha(kprime, w), 1, part, 0, true);
         }
     }
     if (k > 0) {
