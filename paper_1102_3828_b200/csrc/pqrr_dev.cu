@@ -707,10 +707,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // >= 4k' for the exact scan, >= 8k' for the filter's superset; beyond
     // 8192 the selector streams candidates from global memory
     const uint32_t cap_mul = filter_ok ? 8 : 4;
-    // (16k floor: a query whose sampled threshold lands high overflows into
-    // a retry, ~0.35 ms per batch; the buffer costs 8 B per slot)
-    const uint32_t cap_floor = kprime >= 512 ? 16384u : 8192u;
-    const uint32_t cap = std::max<uint32_t>(cap_floor, ((cap_mul * kprime + 1023) / 1024) * 1024) << cap_shift;
+    const uint32_t cap = std::max<uint32_t>(8192, ((cap_mul * kprime + 1023) / 1024) * 1024) << cap_shift;
     // sample density: ~64 samples expected below the alpha*k'-th distance
     // tuning hook (read per search): expected samples below the target rank
     const double spq = default_spq(kprime, w);  // samples expected below the target rank
@@ -1143,8 +1140,7 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
         const double stride = std::max(1.0, std::floor(default_alpha(kprime, w) * kprime /
                                                         default_spq(kprime, w)));
         const double per_q = 2.0 * w * avg_len / stride * 4.0 + (w / 16.0 + 1.0) * 32768.0 +
-                             std::max(kprime >= 512 ? 16384.0 : 8192.0, 8.0 * kprime) * 8.0 + ix.c * 4.0 +
-                             w * 64.0;
+                             std::max(8192.0, 8.0 * kprime) * 8.0 + ix.c * 4.0 + w * 64.0;
         // cudaMemGetInfo costs ~1 ms with a large resident index: query it
         // only when the batch needs a sizeable share of the device
         static size_t dev_total = 0;
