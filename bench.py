@@ -1,19 +1,29 @@
 """IVFADC+R search benchmark (BASELINE.json metric) — one JSON line on rank 0.
 
-Workload (default): BASELINE.json configs[1] ("C2"): n = 10M SIFT-like uint8
-vectors (4096-component mixture, seed 0), 1M training vectors, 10k queries,
-d = 128, Kc = 1024, m = 8, m' = 16, w = 16, k' = 1000, top-100.  A step is one
-fused batched search of all queries (coarse probe -> LUT -> ADC scan ->
-exact top-k' -> residual-PQ re-rank -> top-k).
+Workload (default): BASELINE.json configs[3] ("C4"), the largest config that
+fits one B200: n = 1B SIFT-like uint8 vectors (4096-component mixture, seed
+0), 1M training vectors, 10k queries, d = 128, Kc = 8192, m = 8, m' = 32,
+w = 64, k' = 10000, top-100 (the paper's 1B IVFADC+R row).
+`--config C1|C2|C3` selects the other configs, `--config C5` the batch sweep.
+A step is one fused batched search of all queries (coarse probe -> LUT ->
+ADC scan -> exact top-k' -> residual-PQ re-rank -> top-k).
 
   value : queries/s with queries resident in HBM, device-timed (CUDA events on
           the index stream), L2 flushed between steps.
   e2e   : same metric through the public host API (pqrr_dev_search_u8 via
           ctypes) from pinned host memory, H2D of the queries and D2H of the
           results inside the timed region.
-  --impl reference : the reference's CPU implementation of the path
-          (oracle/_ref: kernels.cpp scan_topk + headers' TopK/l2_sq) on the
-          host cores, on a bounded sample of the same queries.
+  roofline : the dominant kernel of the step (per-kernel CUDA events on the
+          index stream), its algorithmic bytes against its bound.
+  cpu_baseline : the reference's CPU implementation (oracle/_ref: the
+          reference's kernels.cpp scan_topk / assign / encode + headers' TopK /
+          l2_sq) on the host cores, with the parity evidence of the same run:
+          n <= 10M ("full"): the whole index rebuilt on the CPU (codebooks,
+          lists, codes, refinement codes compared byte for byte) and every
+          query searched; larger n ("sample"): the first --ref-queries queries
+          over their probed lists exported from the device index, plus a
+          random-id re-encode of the add path.
+  --impl reference : the reference's CPU path alone, on the same config.
 
 Multi-GPU (torchrun): the database is sharded by id range; each rank searches
 its shard with the full query batch; per-rank top-k lists are all-gathered and
@@ -148,86 +158,129 @@ def build_index(pq, cfg, coarse, P, rq, device, shard, nshards):
     ix = pq.IvfIndex(coarse, P, rq, device)
     ix.add_synthetic(SEED, cfg["clusters"], lo, hi - lo, id_base=lo)
     ix.finalize()
-    log(f"[setup] added ids [{lo}, {hi}) on device {device} in {time.time() - t0:.1f}s")
-    return ix, lo, hi
+    dt = time.time() - t0
+    log(f"[setup] added ids [{lo}, {hi}) on device {device} in {dt:.1f}s")
+    return ix, lo, hi, dt
 
 
 # ---------------------------------------------------------------- reference arm
+REF_SAMPLE = {"C1": 1000, "C2": 1024, "C3": 64, "C4": 32, "C5": 32}
+
+
 def run_reference(args, cfg, rank, world):
-    """The reference's CPU implementation (oracle/_ref) on this host's cores."""
+    """The reference's CPU implementation of the path (oracle/_ref) on this
+    host's cores, on a bounded query sample per step.
+
+    n <= 10M (C1, C2): the index is built on the host too (oracle k-means for
+    the codebooks, the reference's assign_batch / encode_batch for the lists):
+    no device code is loaded.  C3-C5 (100M-1B vectors) cannot be built on the
+    host in a bench run (the assignment alone is ~1e15 element operations,
+    hours on 16 cores): the index is built on the device (setup only, untimed,
+    `index_build` says so), the add path is checked on a random id sample
+    against the reference's own encoder, and each step exports the lists its
+    queries probe and times the reference search over them."""
     if rank != 0:
         return
-    from oracle.oracle_py import Oracle, RefLib, build, ref_available
+    from oracle.oracle_py import RefLib, build, ref_available
+    from oracle import ref_harness as H
 
     if not ref_available():
         build()
     ref = RefLib()
-    cores = os.cpu_count() or 1
+    cores = H.host_cores()
     ref.set_threads(cores)
-    import paper_1102_3828_b200 as pq  # setup only (bit-identical index build), see DESIGN.md
-
-    use_gpu = pq.device_count() > 0
-    if use_gpu:
-        coarse, P, rq = train_codebooks(pq, cfg, 0)
-        ix, _, _ = build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
-        offs, ids, codes, rcodes = ix.export_lists()
-        coarse_c, books, rbooks = coarse.centroids, P.flat(), rq.pq.flat()
-        queries = pq.synth(3, 0, cfg["nq"], cfg["clusters"], seed=SEED)
-        ix.close()
-    else:  # no GPU: the oracle builds the same index on the host (slow)
-        o = Oracle()
-        centers = o.synth_centers(SEED, cfg["clusters"], 128)
-        tr = o.synth_rows(SEED, 1, 0, cfg["train"], centers).astype(np.float32)
-        coarse_c, books = o.ivf_train(tr, cfg["kc"], cfg["m"], iterations=25, seed=SEED)
-        rbooks = o.ivf_refine_train(coarse_c, books, cfg["m"], tr, cfg["mprime"], iterations=25,
-                                    seed=SEED)
-        base = o.synth_rows(SEED, 2, 0, cfg["n"], centers).astype(np.float32)
-        oix = o.ivf_build(coarse_c, books, cfg["m"], base)
-        oix.refine_encode(rbooks, cfg["mprime"], base)
-        offs, ids, codes = oix.flat()
-        rcodes = oix.rcodes[ids]
-        queries = o.synth_rows(SEED, 3, 0, cfg["nq"], centers)
-    n = len(ids)
-    list_of_id = np.zeros(n, np.uint32)
-    codes_by_id = np.zeros((n, cfg["m"]), np.uint8)
-    rcodes_by_id = np.zeros((n, cfg["mprime"]), np.uint8)
-    for l in range(cfg["kc"]):
-        seg = ids[offs[l]:offs[l + 1]]
-        list_of_id[seg] = l
-    codes_by_id[ids] = codes
-    rcodes_by_id[ids] = rcodes
-    qf = queries.astype(np.float32)
-    # bounded sample per step: ~10-20 s of CPU work
-    sample = max(cores * 4, 64)
+    sample = REF_SAMPLE[args.config]
     W, K = args.warmup, args.steps
+    nq = cfg["nq"]
+    extra = {}
+    t_setup = time.time()
+    if cfg["n"] <= CPU_BUILD_MAX:
+        from oracle.oracle_py import Oracle
 
-    def step(i):
-        qs = qf[(i * sample) % cfg["nq"]:][:sample]
-        sl_i, _, sl_c = ref.ivf_search(coarse_c, books, cfg["m"], offs, ids, codes, qs, cfg["w"],
-                                       cfg["kprime"])
-        ref.ivf_rerank(coarse_c, books, rbooks, cfg["m"], cfg["mprime"], list_of_id, codes_by_id,
-                       rcodes_by_id, qs, sl_i, sl_c, cfg["k"])
-        return len(qs)
+        hx = H.cpu_build(cfg, SEED, log)
+        centers = Oracle().synth_centers(SEED, cfg["clusters"], 128)
+        queries = Oracle().synth_rows(SEED, H.SYNTH_QUERY, 0, nq, centers)
+        index_build = "host: oracle k-means + reference assign_batch/encode_batch (no device code)"
 
+        def step(i):
+            qs = queries[(i * sample) % nq:][:sample]
+            t0 = time.perf_counter()
+            H.ref_search(ref, hx, qs, cfg["w"], cfg["kprime"], cfg["k"])
+            return len(qs), time.perf_counter() - t0
+
+        def one_thread(qs):
+            return H.ref_search(ref, hx, qs, cfg["w"], cfg["kprime"], cfg["k"])
+    else:
+        import paper_1102_3828_b200 as pq
+
+        coarse, P, rq = train_codebooks(pq, cfg, 0)
+        ix, _, _, _ = build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
+        queries = pq.synth(3, 0, nq, cfg["clusters"], seed=SEED)
+        cb = (coarse.centroids, P.flat(), rq.pq.flat())
+        # the index the reference searches, checked against the reference's
+        # own encoder on random ids (the add path, kernels.cpp:21-46)
+        starts, block = H.sample_ids(cfg["n"], nblocks=64)
+        extra["index_check"] = add_check(H, cfg, ix, cb, starts, block)
+        index_build = ("device (libpqrr_b200.so, setup only, untimed): a host build of "
+                       f"{cfg['n']:.0e} vectors is ~1e15 assign operations; lists exported per step")
+
+        def step(i):
+            qs = queries[(i * sample) % nq:][:sample]
+            _, _, ts, _ = H.probed_reference(ref, ix.export_lists_subset, *cb, cfg["m"], cfg["mprime"],
+                                             cfg["kc"], qs, cfg["w"], cfg["kprime"], cfg["k"], batch=sample)
+            return len(qs), ts
+
+        def one_thread(qs):
+            return H.probed_reference(ref, ix.export_lists_subset, *cb, cfg["m"], cfg["mprime"],
+                                      cfg["kc"], qs, cfg["w"], cfg["kprime"], cfg["k"], batch=len(qs))
+    t_setup = time.time() - t_setup
     for i in range(min(W, 1)):
         step(i)
-    t0 = time.perf_counter()
-    done = 0
+    done, dt = 0, 0.0
     for i in range(K):
-        done += step(i + 1)
-    dt = time.perf_counter() - t0
+        n_i, t_i = step(i + 1)
+        done += n_i
+        dt += t_i
     v = done / dt
+    # single-thread time per query (eval.hpp:49,63: BenchRow.time_per_query)
+    ref.set_threads(1)
+    n1 = 4
+    t0 = time.perf_counter()
+    one_thread(queries[:n1])
+    t1q = (time.perf_counter() - t0) / n1
+    ref.set_threads(cores)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": dt / K * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config, **cfg, "parallelism": "cpu-openmp"},
+        "config": {"workload": args.config, **cfg, "parallelism": f"cpu-openmp x{cores}"},
         "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "reference",
-                         "sample": f"{sample} queries per step (of {cfg['nq']}) on the "
-                                   f"{'device-built' if use_gpu else 'host-built'} index"},
+                         "cpu_model": H.cpu_model(),
+                         "sample": f"{sample} queries per step (of {nq}), OpenMP over queries",
+                         "time_per_query_1thread_s": t1q, "index_build": index_build,
+                         "setup_s": round(t_setup, 1)},
         "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        **extra,
     }
     print(json.dumps(line), flush=True)
+
+
+CPU_BUILD_MAX = 10_000_000  # host-built index (reference arm, full parity) up to C2
+
+
+def add_check(H, cfg, ix, cb, starts, block):
+    """Random-id sample of the device add path against the reference's own
+    assign / encode on host-generated rows: list, code and refinement code
+    byte for byte (ivf_index.hpp:54-56,72-73)."""
+    t0 = time.time()
+    ids, a, c, rc = H.reencode_sample(cfg, *cb, starts, block, seed=SEED)
+    dl, dc, drc = ix.lookup_ids(ids)
+    out = {"ids": int(len(ids)), "list_match": float(np.mean(dl == a)),
+           "codes_match": float(np.mean(np.all(dc == c, axis=1))),
+           "rcodes_match": float(np.mean(np.all(drc == rc, axis=1))) if rc is not None else None,
+           "sample": f"{len(starts)} random runs of {block} consecutive ids"}
+    log(f"[parity] add-path re-encode of {len(ids)} ids in {time.time() - t0:.1f}s: {out}")
+    return out
 
 
 # ---------------------------------------------------------------- our arm
@@ -237,9 +290,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recall", action="store_true")
+    ap.add_argument("--parity", default="auto", choices=["auto", "full", "sample"],
+                    help="full: host-built index + every query (n <= 10M); sample: probed-list "
+                         "reference on --ref-queries queries + add-path re-encode sample")
+    ap.add_argument("--ref-queries", type=int, default=256)
     ap.add_argument("--shard-mode", default="local", choices=["local", "exact"],
                     help="N>1: per-shard shortlists (north star) or the single-index-exact flow")
     args = ap.parse_args()
@@ -261,7 +318,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = local
     coarse, P, rq = train_codebooks(pq, cfg, device)
-    ix, lo, hi = build_index(pq, cfg, coarse, P, rq, device, rank, world)
+    ix, lo, hi, add_s = build_index(pq, cfg, coarse, P, rq, device, rank, world)
     nq, k, kp, w = cfg["nq"], cfg["k"], cfg["kprime"], cfg["w"]
     queries = pq.synth(3, 0, nq, cfg["clusters"], seed=SEED, device=device)
     d_q = torch.from_numpy(queries).cuda()
@@ -281,6 +338,7 @@ def main():
         if sharded is not None:  # shard search + NCCL all-gather + K7 merge
             oi, od, oc = sharded.search(d_q, stream)
             d_ids.copy_(oi)
+            d_dist.copy_(od)
             return
         ix.search_device(d_q.data_ptr(), nq, w, kp, k, d_ids.data_ptr(), d_dist.data_ptr(),
                          d_cnt.data_ptr(), stream.cuda_stream)
@@ -289,7 +347,7 @@ def main():
         run_once()
     torch.cuda.synchronize()
     launches0 = pq.launch_count()
-    step_ms, scan_ms, stats = [], [], []
+    step_ms, stats = [], []
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -303,9 +361,7 @@ def main():
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
-            st = ix.last_stats()
-            stats.append(st)
-            scan_ms.append(st["ms_filter"] if st["ms_filter"] > 0 else st["ms_scan"])
+            stats.append(ix.last_stats())
     torch.cuda.synchronize()
     launches = pq.launch_count() - launches0
     total_ms = float(np.sum(step_ms))
@@ -314,6 +370,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     value = nq * args.steps / (total_ms / 1e3)
+    res_ids = d_ids.cpu().numpy().view(np.uint32)
+    res_dists = d_dist.cpu().numpy()
 
     # ---- e2e through the host API from pinned memory
     pinned_q = torch.from_numpy(queries).pin_memory()
@@ -331,7 +389,7 @@ def main():
             dist.barrier()
         t0 = time.perf_counter()
         if sharded is None:
-            ids_h, d_h, c_h = ix.search(hq, w, kp, k, out=h_out)  # public host API (C ABI)
+            ix.search(hq, w, kp, k, out=h_out)  # public host API (C ABI)
         else:
             dq = pinned_q.cuda(non_blocking=True)
             oi, od, oc = sharded.search(dq, stream)
@@ -346,44 +404,16 @@ def main():
         e2e_total = float(t.item())
     e2e_val = nq * args.steps / e2e_total
 
-    # ---- parity / recall evidence
-    res_ids = d_ids.cpu().numpy().view(np.uint32)
+    # ---- recall (exact ground truth) + parity against the reference
     extra = {}
+    gt = None
     if not args.no_recall and world == 1:
-        extra.update(recall_and_parity(pq, cfg, queries, res_ids, ix, coarse, P, rq))
-
-    # ---- roofline of the dominant kernel: the main ADC scan (K4f filter; the
-    # fp32 exact scan when the filter is disabled)
-    st = stats[-1]
-    filt = st["ms_filter"] > 0
-    scanned = float(np.mean([s["scanned_entries"] for s in stats]))
-    bytes_per_step = scanned * (cfg["m"] + 4)
-    scan_s = float(np.mean(scan_ms)) / 1e3
-    peak, kind = measured_peak_gbs()
-    achieved = bytes_per_step / scan_s / 1e9
+        gt = ground_truth(pq, cfg, queries)
+        for r in (1, 10, 100):
+            extra[f"recall@{r}"] = float(np.mean([gt[q] in res_ids[q, :r] for q in range(len(gt))]))
+        extra["recall_queries"] = int(len(gt))
     clocks = clk.summary()
-    # The scan is list-major: its physical DRAM traffic is small and its real
-    # bound is shared-memory LUT gathers: m lookups per scanned
-    # (entry, query).  K4f gathers 1-byte (5-bit) table entries, 16 queries per
-    # LDS.128, against the 128 B/clk/SM shared-memory pipe; the exact fp32 scan
-    # gathers 4 bytes per lookup (32 lookups/clk/SM).
-    import torch as _t
-
-    n_sm = _t.cuda.get_device_properties(local).multi_processor_count
-    f_sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
-    lookups = scanned * cfg["m"]
-    lk_per_clk = lookups / scan_s / (n_sm * f_sm)
-    lut_bytes = 1.0 if filt else 4.0
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "scan_traffic.json")) as f:
-            tj = json.load(f)
-        if tj.get("config") == args.config and tj.get("kernel", "").startswith(
-                "ivf_filter" if filt else "ivf_scan"):
-            traffic = tj["dram_bytes_per_launch"]
-    except Exception:
-        pass
-    kname = "ivf_filter_kernel (K4f, 5-bit LUT filter)" if filt else "ivf_scan_kernel (exact main pass)"
+    roof, kernels = rooflines(cfg, stats, clocks, local, args.config)
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -395,40 +425,116 @@ def main():
         "e2e": {"value": e2e_val, "unit": "queries/s", "h2d_bytes_per_step": int(queries.nbytes),
                 "d2h_bytes_per_step": int(nq * k * 8 + nq * 4)},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": kind,
-                     "kernel": kname,
-                     "algorithmic_bytes_per_launch": bytes_per_step,
-                     "kernel_ms": scan_s * 1e3,
-                     "note": "list-major scan: B_q = sum len*(m+4) per query (SURVEY §8d); "
-                             "frac > 1 = reuse across the batch; true bound = smem gathers"},
-        "roofline_smem": {"bound": "smem LUT gathers", "achieved": lk_per_clk * lut_bytes,
-                          "peak": 128.0, "unit": "B/clk/SM", "frac": lk_per_clk * lut_bytes / 128.0,
-                          "lookups_per_launch": lookups, "bytes_per_lookup": lut_bytes,
-                          "lookups_per_clk_per_sm": lk_per_clk,
-                          "fp32_gather_bound_lookups_per_clk": 32.0,
-                          "vs_fp32_gather_bound": lk_per_clk / 32.0, "sm_count": n_sm,
-                          "sm_clock_mhz": f_sm / 1e6,
-                          "note": "algorithmic lookups: 8 per (probed entry, query); K4f executes only "
-                                  "those of live (query, list) pairs (sum of LUT minima <= tau), the "
-                                  "others are settled without a lookup"},
-        "filter": {"candidates_per_query": float(np.mean([s["candidates"] for s in stats])) / nq,
-                   "exact_le_tau_per_query": float(np.mean([s["exact_candidates"] for s in stats])) / nq}
-        if filt else None,
+        "roofline": roof,
+        "kernels": kernels,
+        "scan": scan_summary(cfg, stats),
+        "add": {"vectors": int(hi - lo), "seconds": round(add_s, 2),
+                "vectors_per_s": (hi - lo) / add_s if add_s > 0 else None,
+                "note": "device add path (coarse assign + PQ + refinement PQ + list layout), "
+                        "synthetic rows generated on the device; setup, outside the timed steps"},
         "stages_ms": {k2: round(float(np.mean([s[k2] for s in stats])), 4)
                       for k2 in ["ms_coarse", "ms_invert", "ms_sample_scan", "ms_threshold",
-                                 "ms_filter", "ms_scan", "ms_select", "ms_rerank", "ms_total"]},
-        "search_stats": {k2: st[k2] for k2 in ["work_items", "retries", "stride", "kernels",
-                                               "scanned_entries", "sampled_entries"]},
+                                 "ms_filter", "ms_recheck", "ms_scan", "ms_select", "ms_rerank_dist",
+                                 "ms_rerank", "ms_total"]},
+        "search_stats": {k2: stats[-1][k2] for k2 in ["work_items", "retries", "stride", "kernels",
+                                                     "scanned_entries", "sampled_entries",
+                                                     "candidates", "rerank_candidates",
+                                                     "filter_live_entries"]},
         "clocks": clocks,
         **extra,
     }
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(cfg, ix, coarse, P, rq, queries)
+        line["cpu_baseline"] = parity_and_baseline(args, cfg, pq, ix, coarse, P, rq, queries,
+                                                   res_ids, res_dists, gt, extra)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- roofline
+def rooflines(cfg, stats, clocks, device, config):
+    """Per-kernel rooflines (mean over the timed steps; kernel times are CUDA
+    events on the index stream around each launch).  Algorithmic work per
+    launch, SURVEY.md §8(d):
+      K5 re-rank distances: k'·(m + m' + 8) B per query from HBM (code,
+        refinement code, shortlist key) — bound: HBM;
+      K4f filter: 8 one-byte LUT lookups per (live (query, list) pair, entry)
+        it tests — bound: the shared-memory pipe (128 B/clk/SM);
+      K4r recheck: 8 code-book rows of d/m floats per surviving candidate
+        — bound: the shared-memory pipe.
+    The dominant (longest) one is `roofline`; all are in `kernels`."""
+    import torch
+
+    peak_hbm, kind = measured_peak_gbs()
+    props = torch.cuda.get_device_properties(device)
+    n_sm = props.multi_processor_count
+    f_sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    smem_peak_gbs = 128.0 * n_sm * f_sm / 1e9
+    mean = lambda k: float(np.mean([s[k] for s in stats]))  # noqa: E731
+    m, mp, d = cfg["m"], cfg["mprime"], 128
+    traffic = ncu_traffic(config)
+    ks = []
+    t = mean("ms_rerank_dist")
+    if t > 0:
+        b = mean("rerank_candidates") * (m + mp + 8)
+        ks.append({"kernel": "rerank_coop_kernel (K5 refined distances)", "bound": "hbm",
+                   "kernel_ms": t, "algorithmic_bytes_per_launch": b,
+                   "achieved": b / (t / 1e3) / 1e9, "peak": peak_hbm, "unit": "GB/s",
+                   "peak_kind": kind, "traffic": traffic.get("rerank_coop_kernel")})
+    t = mean("ms_filter")
+    if t > 0:
+        b = mean("filter_live_entries") * m
+        ks.append({"kernel": "ivf_filter_kernel (K4f 5-bit LUT filter, incl. live-pair compaction)",
+                   "bound": "smem", "kernel_ms": t, "algorithmic_bytes_per_launch": b,
+                   "achieved": b / (t / 1e3) / 1e9, "peak": smem_peak_gbs, "unit": "GB/s",
+                   "peak_kind": f"128 B/clk/SM x {n_sm} SMs x {f_sm / 1e6:.0f} MHz",
+                   "traffic": traffic.get("ivf_filter_kernel")})
+    t = mean("ms_recheck")
+    if t > 0:
+        b = mean("candidates") * m * (d // m) * 4
+        ks.append({"kernel": "recheck_smem_kernel (K4r exact ADC of the survivors)", "bound": "smem",
+                   "kernel_ms": t, "algorithmic_bytes_per_launch": b,
+                   "achieved": b / (t / 1e3) / 1e9, "peak": smem_peak_gbs, "unit": "GB/s",
+                   "peak_kind": f"128 B/clk/SM x {n_sm} SMs x {f_sm / 1e6:.0f} MHz",
+                   "traffic": traffic.get("recheck_smem_kernel")})
+    for e in ks:
+        e["frac"] = e["achieved"] / e["peak"]
+    if not ks:
+        return None, []
+    top = max(ks, key=lambda e: e["kernel_ms"])
+    share = top["kernel_ms"] / mean("ms_total") if mean("ms_total") > 0 else None
+    return {**top, "share_of_step": share}, ks
+
+
+def scan_summary(cfg, stats):
+    """The scan in the north star's terms: scan-equivalent GB/s = Σ_q B_q
+    (B_q = Σ_probed len·(m + 4)) over the filter + recheck time.
+    The list-major scan reads each list once per work item of up to 64
+    queries and skips dead (query, list) pairs, so this is NOT physical DRAM
+    traffic (that is the ncu figure in profiles/) and not a roofline fraction."""
+    mean = lambda k: float(np.mean([s[k] for s in stats]))  # noqa: E731
+    t = mean("ms_scan")
+    b = mean("scanned_entries") * (cfg["m"] + 4)
+    return {"scan_equivalent_gbs": b / (t / 1e3) / 1e9 if t > 0 else None, "scan_ms": t,
+            "probed_entries_per_query": mean("scanned_entries") / cfg["nq"],
+            "live_entry_share": mean("filter_live_entries") / mean("scanned_entries")
+            if mean("scanned_entries") else None,
+            "filter_candidates_per_query": mean("candidates") / cfg["nq"],
+            "exact_le_tau_per_query": mean("exact_candidates") / cfg["nq"]}
+
+
+def ncu_traffic(config):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of each hot
+    kernel, from the ncu --set full capture of this commit's code committed
+    under profiles/ (null when the capture is missing or from older code)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tj = json.load(f)
+    except Exception:
+        return {}
+    ent = tj.get(config, {})
+    return {k: v.get("dram_bytes") for k, v in ent.items() if isinstance(v, dict)}
 
 
 def run_sweep(args, cfg, rank, world):
@@ -446,7 +552,7 @@ def run_sweep(args, cfg, rank, world):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     coarse, P, rq = train_codebooks(pq, cfg, local)
-    ix, _, _ = build_index(pq, cfg, coarse, P, rq, local, rank, world)
+    ix, _, _, _ = build_index(pq, cfg, coarse, P, rq, local, rank, world)
     k, kp, w = cfg["k"], cfg["kprime"], cfg["w"]
     if world > 1:
         from paper_1102_3828_b200.sharded import DeviceShardedSearch
@@ -567,104 +673,95 @@ def run_sweep(args, cfg, rank, world):
         dist.destroy_process_group()
 
 
-def recall_and_parity(pq, cfg, queries, res_ids, ix, coarse, P, rq):
-    """recall@1/10/100 against exact ground truth on a query sample: the
-    product's compute_groundtruth over the device-generated base set (k_exact.cu,
-    integer tensor cores, exact for u8)."""
-    out = {}
-    nq_gt = min(1000, len(queries))
+
+def ground_truth(pq, cfg, queries, nq_gt=1000):
+    """Exact nearest neighbour (eval.hpp:13-19) of the first nq_gt queries: the
+    product's compute_groundtruth over the device-generated base set
+    (k_exact.cu, integer tensor cores: u8 distances are exact integers)."""
     t0 = time.time()
+    nq_gt = min(nq_gt, len(queries))
     gt = pq.groundtruth_synthetic(SEED, cfg["clusters"], cfg["n"], queries[:nq_gt], 1)
-    for r in (1, 10, 100):
-        out[f"recall@{r}"] = float(np.mean([gt.nearest(q) in res_ids[q, :r] for q in range(nq_gt)]))
-    out["recall_queries"] = nq_gt
     log(f"[recall] exact ground truth of {nq_gt} queries over {cfg['n']} vectors in {time.time() - t0:.1f}s")
-    return out
+    return np.array([gt.nearest(q) for q in range(nq_gt)], np.int64)
 
 
-def cpu_baseline(cfg, ix, coarse, P, rq, queries):
-    """oracle/_ref (reference kernels.cpp + headers) on a bounded query sample."""
+def parity_and_baseline(args, cfg, pq, ix, coarse, P, rq, queries, res_ids, res_dists, gt, ours):
+    """cpu_baseline: the reference's CPU path (oracle/_ref) on this host's
+    cores, timed on the same workload, plus the parity evidence of this run
+    (ids and distance bits against the GPU's results of the timed steps,
+    recall of both arms on the same queries, add-path codes)."""
     from oracle.oracle_py import RefLib, ref_available
+    from oracle import ref_harness as H
 
     if not ref_available():
         return {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
                 "sample": "unavailable: oracle/_ref not built"}
-    if cfg["n"] > 200_000_000:
-        # the whole 1B index does not fit the reference's host layout: export
-        # only the lists the sample queries probe (enough for their results)
-        return cpu_baseline_probed(cfg, ix, coarse, P, rq, queries)
     ref = RefLib()
-    cores = os.cpu_count() or 1
+    cores = H.host_cores()
     ref.set_threads(cores)
-    offs, ids, codes, rcodes = ix.export_lists()
-    n = len(ids)
-    list_of_id = np.zeros(n, np.uint32)
-    for l in range(cfg["kc"]):
-        list_of_id[ids[offs[l]:offs[l + 1]]] = l
-    codes_by_id = np.zeros((n, cfg["m"]), np.uint8)
-    codes_by_id[ids] = codes
-    rcodes_by_id = np.zeros((n, cfg["mprime"]), np.uint8)
-    rcodes_by_id[ids] = rcodes
-    sample = min(len(queries), max(64, cores * 4))
-    qf = queries[:sample].astype(np.float32)
+    nq, w, kp, k = cfg["nq"], cfg["w"], cfg["kprime"], cfg["k"]
+    cb = (coarse.centroids, P.flat(), rq.pq.flat())
+    mode = args.parity
+    if mode == "auto":
+        mode = "full" if cfg["n"] <= CPU_BUILD_MAX else "sample"
+    out = {"unit": "queries/s", "cores": cores, "kind": "reference", "cpu_model": H.cpu_model(),
+           "parity_mode": mode}
+    if mode == "full":
+        # the whole index rebuilt on the host with no device code
+        t0 = time.time()
+        c_coarse, c_books, c_rbooks, _ = H.cpu_train(cfg, SEED, log)
+        out["codebooks_match"] = bool(np.array_equal(c_coarse.view(np.uint32), cb[0].view(np.uint32))
+                                      and np.array_equal(c_books.view(np.uint32), cb[1].view(np.uint32))
+                                      and np.array_equal(c_rbooks.view(np.uint32), cb[2].view(np.uint32)))
+        hx = H.cpu_build(cfg, SEED, log, codebooks=(c_coarse, c_books, c_rbooks))
+        out["host_build_s"] = round(time.time() - t0, 1)
+        offs, ids, codes, rcodes = ix.export_lists()
+        out["offsets_match"] = bool(np.array_equal(offs, hx.offs))
+        out["ids_match"] = float(np.mean(ids == hx.ids))
+        out["codes_match"] = float(np.mean(np.all(codes == hx.codes, axis=1)))
+        out["rcodes_match"] = float(np.mean(np.all(rcodes == hx.rcodes_list_order(), axis=1)))
+        del offs, ids, codes, rcodes
+        qs = queries
+        t0 = time.perf_counter()
+        ri, rd, _ = H.ref_search(ref, hx, qs, w, kp, k)
+        t = time.perf_counter() - t0
+        out["sample"] = f"all {nq} queries, OpenMP over queries, host-built index"
+        one = lambda q: H.ref_search(ref, hx, q, w, kp, k)  # noqa: E731
+    else:
+        nr = min(args.ref_queries, nq)
+        qs = queries[:nr]
+        ri, rd, t, nl = H.probed_reference(ref, ix.export_lists_subset, *cb, cfg["m"], cfg["mprime"],
+                                           cfg["kc"], qs, w, kp, k, batch=32)
+        out["sample"] = (f"first {nr} queries in batches of 32, OpenMP over queries, over the lists "
+                         f"they probe exported from the device index ({nl} list exports)")
+        one = lambda q: H.probed_reference(ref, ix.export_lists_subset, *cb, cfg["m"],  # noqa: E731
+                                           cfg["mprime"], cfg["kc"], q, w, kp, k, batch=len(q))
+        starts, block = H.sample_ids(cfg["n"])
+        out["add_check"] = add_check(H, cfg, ix, cb, starts, block)
+    out["value"] = len(qs) / t
+    nqs = len(qs)
+    out["id_match"] = float(np.mean(res_ids[:nqs] == ri))
+    out["dist_bits_match"] = float(np.mean(res_dists[:nqs].view(np.uint32) == rd.view(np.uint32)))
+    out["queries_compared"] = int(nqs)
+    if gt is not None:
+        ng = min(len(gt), nqs)
+        for r in (1, 10, 100):
+            rc = H.recall_at(ri[:ng], gt[:ng], r)
+            rg = H.recall_at(res_ids[:ng], gt[:ng], r)
+            out[f"recall@{r}"] = rc
+            out[f"recall@{r}_gpu_same_queries"] = rg
+        out["recall_queries"] = int(ng)
+        out["recall_delta_max"] = max(abs(out[f"recall@{r}"] - out[f"recall@{r}_gpu_same_queries"])
+                                      for r in (1, 10, 100))
+    # single-thread time per query (eval.hpp:49,63 BenchRow.time_per_query)
+    ref.set_threads(1)
+    n1 = 4
     t0 = time.perf_counter()
-    sl_i, _, sl_c = ref.ivf_search(coarse.centroids, P.flat(), cfg["m"], offs, ids, codes, qf,
-                                   cfg["w"], cfg["kprime"])
-    rr, _ = ref.ivf_rerank(coarse.centroids, P.flat(), rq.pq.flat(), cfg["m"], cfg["mprime"],
-                           list_of_id, codes_by_id, rcodes_by_id, qf, sl_i, sl_c, cfg["k"])
-    dt = time.perf_counter() - t0
-    ours, _, _ = ix.search(queries[:sample], cfg["w"], cfg["kprime"], cfg["k"])
-    match = float(np.mean(ours == rr))
-    return {"value": sample / dt, "unit": "queries/s", "cores": cores, "kind": "reference",
-            "sample": f"first {sample} queries, OpenMP over queries",
-            "oracle_id_match": match}
-
-
-def cpu_baseline_probed(cfg, ix, coarse, P, rq, queries, sample=16):
-    """Reference CPU search (oracle/_ref) + oracle id check on a sample of
-    queries against a 1B-vector device index: the coarse probes of the sample
-    are computed by the CPU oracle, only the union of probed lists is exported
-    (id-ascending), and ids are renumbered monotonically (rank among the
-    exported entries) so the reference's id-indexed arrays stay small while
-    every (dist, id) order is preserved.  The sample's results are exactly the
-    full index's: a query only ever reads its probed lists."""
-    from oracle.oracle_py import Oracle, RefLib
-
-    ref = RefLib()
-    cores = os.cpu_count() or 1
+    one(queries[:n1])
+    out["time_per_query_1thread_s"] = (time.perf_counter() - t0) / n1
     ref.set_threads(cores)
-    qs = queries[:sample]
-    qf = qs.astype(np.float32)
-    probes, _ = Oracle().coarse_probe(coarse.centroids, qf, cfg["w"])
-    U = np.unique(probes).astype(np.uint32)
-    offs_u, ids_u, codes_u, rc_u = ix.export_lists_subset(U)
-    lens = np.zeros(cfg["kc"], np.uint64)
-    lens[U] = np.diff(offs_u)
-    full_offs = np.zeros(cfg["kc"] + 1, np.uint64)
-    full_offs[1:] = np.cumsum(lens)
-    order = np.argsort(ids_u, kind="stable")
-    gid_sorted = ids_u[order]
-    local = np.empty(len(ids_u), np.uint32)
-    local[order] = np.arange(len(ids_u), dtype=np.uint32)
-    list_of_local = np.empty(len(ids_u), np.uint32)
-    list_of_local[local] = np.repeat(U, np.diff(offs_u).astype(np.int64))
-    codes_by_local = np.empty_like(codes_u)
-    codes_by_local[local] = codes_u
-    rc_by_local = np.empty_like(rc_u)
-    rc_by_local[local] = rc_u
-    t0 = time.perf_counter()
-    sl_i, _, sl_c = ref.ivf_search(coarse.centroids, P.flat(), cfg["m"], full_offs, local, codes_u, qf,
-                                   cfg["w"], cfg["kprime"])
-    rr, rd = ref.ivf_rerank(coarse.centroids, P.flat(), rq.pq.flat(), cfg["m"], cfg["mprime"],
-                            list_of_local, codes_by_local, rc_by_local, qf, sl_i, sl_c, cfg["k"])
-    dt = time.perf_counter() - t0
-    ours_i, ours_d, _ = ix.search(qs, cfg["w"], cfg["kprime"], cfg["k"])
-    rr_g = gid_sorted[rr]
-    return {"value": len(qs) / dt, "unit": "queries/s", "cores": cores, "kind": "reference",
-            "sample": (f"first {len(qs)} queries, OpenMP over queries, over the {len(U)} lists they "
-                       f"probe ({len(ids_u)} entries exported from the device index)"),
-            "oracle_id_match": float(np.mean(ours_i == rr_g)),
-            "oracle_dist_bits_match": float(np.mean(ours_d.view(np.uint32) == rd.view(np.uint32)))}
+    log(f"[parity] {json.dumps(out)}")
+    return out
 
 
 if __name__ == "__main__":

@@ -193,6 +193,12 @@ int pqrr_dev_rerank_owned_u8_device(pqrr_dev_index* ix, const uint8_t* d_queries
                                     const uint32_t* d_sl_ids, const uint32_t* d_sl_counts,
                                     size_t sl_stride, size_t k, uint32_t* d_out_ids,
                                     float* d_out_dists, uint32_t* d_out_counts, void* stream);
+/* list_of_id / code_of_id (ivf_index.hpp:33-40) and RefineCodes::code
+ * (refine.hpp:27) of n ids: out_list[i] (UINT32_MAX if id i was never
+ * added), out_codes[i * m ..], out_rcodes[i * mprime ..] (NULL = skip).
+ * The add-path parity check compares these with a CPU re-encode.           */
+int pqrr_dev_lookup_ids(pqrr_dev_index* ix, const uint32_t* ids, size_t n, uint32_t* out_list,
+                        uint8_t* out_codes, uint8_t* out_rcodes);
 /* ivf_reconstruct (ivf_index.hpp:75-77): coarse + decode + refine decode. */
 int pqrr_dev_reconstruct(pqrr_dev_index* ix, const uint32_t* ids, size_t n, float* out);
 
@@ -284,6 +290,10 @@ typedef struct {
     uint32_t kernels;
     float ms_filter;           /* K4f alone (ms_scan = K4f + K4r, or the exact scan) */
     uint64_t exact_candidates; /* candidates with exact ADC <= tau (K4f path) */
+    float ms_recheck;          /* K4r alone (exact ADC of the filter's survivors) */
+    float ms_rerank_dist;      /* K5 refined distances alone (ms_rerank = K5 + top-k) */
+    uint64_t rerank_candidates;/* shortlist entries re-ranked (sum of the k' rows) */
+    uint64_t filter_live_entries; /* (live (query, list) pair, entry) combinations K4f tests */
 } pqrr_dev_search_stats;
 int pqrr_dev_last_search_stats(pqrr_dev_index* ix, pqrr_dev_search_stats* out);
 

@@ -54,7 +54,9 @@ class SearchStats(C.Structure):
                 ("sampled_entries", C.c_uint64), ("candidates", C.c_uint64),
                 ("work_items", C.c_uint32), ("retries", C.c_uint32), ("stride", C.c_uint32),
                 ("kernels", C.c_uint32), ("ms_filter", C.c_float),
-                ("exact_candidates", C.c_uint64)]
+                ("exact_candidates", C.c_uint64), ("ms_recheck", C.c_float),
+                ("ms_rerank_dist", C.c_float), ("rerank_candidates", C.c_uint64),
+                ("filter_live_entries", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -101,6 +103,7 @@ _sig("pqrr_dev_search_u8_device", [_vp, _vp, _sz, _u32, _sz, _sz, _vp, _vp, _vp,
 _sig("pqrr_dev_rerank_u8", [_vp, _u8p, _sz, _u32p, _u32p, _sz, _sz, _u32p, _f32p])
 _sig("pqrr_dev_rerank_f32", [_vp, _f32p, _sz, _u32p, _u32p, _sz, _sz, _u32p, _f32p])
 _sig("pqrr_dev_reconstruct", [_vp, _u32p, _sz, _f32p])
+_sig("pqrr_dev_lookup_ids", [_vp, _u32p, _sz, _vp, _vp, _vp])
 _sig("pqrr_dev_rerank_owned_u8_device", [_vp, _vp, _sz, _vp, _vp, _sz, _sz, _vp, _vp, _vp, _vp])
 _sig("pqrr_dev_last_search_stats", [_vp, C.POINTER(SearchStats)])
 _sig("pqrr_dev_load_lists", [_vp, _u64p, _u32p, _u8p, _vp])
@@ -136,7 +139,7 @@ EXPORTED = [
     "pqrr_dev_add_synthetic", "pqrr_dev_finalize", "pqrr_dev_index_get_info",
     "pqrr_dev_export_lists", "pqrr_dev_search_u8", "pqrr_dev_search_f32",
     "pqrr_dev_search_u8_device", "pqrr_dev_rerank_u8", "pqrr_dev_rerank_f32",
-    "pqrr_dev_reconstruct", "pqrr_dev_last_search_stats", "pqrr_dev_load_lists",
+    "pqrr_dev_reconstruct", "pqrr_dev_lookup_ids", "pqrr_dev_last_search_stats", "pqrr_dev_load_lists",
     "pqrr_dev_merge_topk", "pqrr_dev_merge_topk_device", "pqrr_dev_rerank_owned_u8_device",
     "pqrr_dev_adc_index_create", "pqrr_dev_refine_train", "pqrr_dev_residual",
     "pqrr_dev_reconstruct_codes", "pqrr_dev_export_codebooks", "pqrr_dev_export_lists_subset",

@@ -254,7 +254,8 @@ struct PairSet {
 void launch_live_pairs(const FilterArgs& a, PairSet s0, PairSet s1, const uint32_t* all_first,
                        const uint32_t* all_cnt, uint32_t nlists, uint32_t* live_slot,
                        uint32_t* live_pair, uint32_t* live_cnt, const uint32_t* item_off,
-                       uint32_t* item_start, uint32_t* item_nq, uint32_t chunk, cudaStream_t s);
+                       uint32_t* item_start, uint32_t* item_nq, uint32_t chunk, cudaStream_t s,
+                       unsigned long long* live_entries = nullptr);
 // K4r: exact ADC distance of every filter candidate (reference order), and
 // the per-query count of candidates at or below tau.
 bool recheck_supported(uint32_t d, uint32_t m, uint32_t w);
@@ -294,7 +295,8 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
                    const uint16_t* block_list, const float* coarse,
                    const uint8_t* codes, const float* books, uint32_t m, const uint8_t* rcodes,
                    const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
-                   uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s);
+                   uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s,
+                   cudaEvent_t ev_dist_done = nullptr);
 // Merge per-shard ranked lists [parts][nq][width] into the top-k (K7).
 void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* counts, size_t nq,
                        uint32_t parts, uint32_t width, uint32_t k, uint32_t* out_ids,

@@ -612,7 +612,8 @@ __global__ __launch_bounds__(256) void live_pairs_kernel(const FilterArgs a, Pai
                                                          const uint32_t* __restrict__ all_first,
                                                          uint32_t* __restrict__ live_slot,
                                                          uint32_t* __restrict__ live_pair,
-                                                         uint32_t* __restrict__ live_cnt) {
+                                                         uint32_t* __restrict__ live_cnt,
+                                                         unsigned long long* __restrict__ live_entries) {
     __shared__ uint32_t s_wc[8];
     const uint32_t l = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -647,7 +648,11 @@ __global__ __launch_bounds__(256) void live_pairs_kernel(const FilterArgs a, Pai
             __syncthreads();
         }
     }
-    if (threadIdx.x == 0) live_cnt[l] = o;
+    if (threadIdx.x == 0) {
+        live_cnt[l] = o;
+        // (live pair, entry) lookups K4f executes for this list (measurement)
+        if (live_entries && o) atomicAdd(live_entries, (unsigned long long)o * a.list_len[l]);
+    }
 }
 
 // The K4f items of a list (groups of FQ pairs x entry chunks, items_build
@@ -682,8 +687,10 @@ void launch_ivf_filter(const FilterArgs& a, cudaStream_t s) {
 void launch_live_pairs(const FilterArgs& a, PairSet s0, PairSet s1, const uint32_t* all_first,
                        const uint32_t* all_cnt, uint32_t nlists, uint32_t* live_slot,
                        uint32_t* live_pair, uint32_t* live_cnt, const uint32_t* item_off,
-                       uint32_t* item_start, uint32_t* item_nq, uint32_t chunk, cudaStream_t s) {
-    live_pairs_kernel<<<nlists, 256, 0, s>>>(a, s0, s1, all_first, live_slot, live_pair, live_cnt);
+                       uint32_t* item_start, uint32_t* item_nq, uint32_t chunk, cudaStream_t s,
+                       unsigned long long* live_entries) {
+    live_pairs_kernel<<<nlists, 256, 0, s>>>(a, s0, s1, all_first, live_slot, live_pair, live_cnt,
+                                             live_entries);
     PQRR_LAUNCH_CHECK();
     live_items_kernel<<<(nlists + 255) / 256, 256, 0, s>>>(a, all_cnt, all_first, live_cnt, nlists, item_off,
                                                           item_start, item_nq, chunk);

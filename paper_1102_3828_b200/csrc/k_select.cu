@@ -522,101 +522,6 @@ __global__ __launch_bounds__(256, 3) void rerank_kernel(
     if (threadIdx.x == 0) out_cnt[q] = cnt;
 }
 
-// Warp-cooperative re-ranker for d = 128 (dsub, dsub' multiples of 4): lane t
-// owns dims 4t..4t+3, so the centroid / code-book rows of one candidate are
-// read as coalesced 512 B / 64 B / 32 B segments instead of 32 scattered rows.
-// The exact reference order of l2_sq (s_k += t_{4g+k}^2 for g = 0..31 in
-// order, distance.hpp:16-33) is kept by transposing the squared differences of
-// 32 candidates through shared memory: lane c then sums candidate c's 32
-// groups sequentially.
-constexpr int RW_WARPS = 4;
-constexpr int RW_LD = 33;  // padded float4 row of the transpose tile
-
-__global__ __launch_bounds__(RW_WARPS * 32) void rerank_warp_kernel(
-    const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
-    const uint32_t* __restrict__ sl_cnt, uint32_t sl_stride, const float* __restrict__ xq,
-    const uint16_t* __restrict__ block_list, const float* __restrict__ coarse,
-    const uint8_t* __restrict__ codes, const float* __restrict__ books, uint32_t m,
-    const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks, uint32_t mprime,
-    uint32_t ks, uint32_t k, uint32_t* __restrict__ out_ids, float* __restrict__ out_dists,
-    uint32_t* __restrict__ out_cnt) {
-    constexpr uint32_t D = 128;
-    extern __shared__ float4 rw_smem[];
-    float4* tiles = rw_smem;                                            // [warps][32][RW_LD]
-    u64* keys = reinterpret_cast<u64*>(rw_smem + RW_WARPS * 32 * RW_LD);  // [n2]
-    const size_t q = blockIdx.x;
-    const uint32_t n = sl_cnt[q];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float4* tile = tiles + warp * 32 * RW_LD;
-    uint32_t n2 = 1;
-    while (n2 < n) n2 <<= 1;
-    for (uint32_t i = n + threadIdx.x; i < n2; i += blockDim.x) keys[i] = ~0ull;
-    const float4 x4 = reinterpret_cast<const float4*>(xq + q * D)[lane];
-    const uint32_t ds = D / m, dsr = D / mprime;
-    const uint32_t t0 = 4 * lane;
-    const uint32_t jj = t0 / ds, jr = t0 / dsr;
-    const uint32_t bo = t0 - jj * ds, ro = t0 - jr * dsr;
-    // per-warp staging of the batch's candidate metadata (list, code bytes)
-    __shared__ uint32_t s_list[RW_WARPS][32];
-    __shared__ __align__(16) uint8_t s_code[RW_WARPS][32][8];
-    __shared__ __align__(16) uint8_t s_rcode[RW_WARPS][32][32];
-    for (uint32_t b = warp * 32; b < n; b += RW_WARPS * 32) {
-        const uint32_t c = b + lane;
-        uint32_t my_id = 0;
-        if (c < n) {
-            const uint32_t pos = sl_pos[q * sl_stride + c];
-            my_id = key_id(sl_key[q * sl_stride + c]);
-            s_list[warp][lane] = block_list[pos >> 4];
-            *reinterpret_cast<u64*>(s_code[warp][lane]) = *reinterpret_cast<const u64*>(codes + (size_t)pos * 8);
-            for (uint32_t w8 = 0; w8 < mprime; w8 += 8)
-                *reinterpret_cast<u64*>(&s_rcode[warp][lane][w8]) =
-                    *reinterpret_cast<const u64*>(rcodes + (size_t)pos * mprime + w8);
-        }
-        __syncwarp();
-        const uint32_t nb = min(32u, n - b);
-#pragma unroll 4
-        for (uint32_t cc = 0; cc < nb; ++cc) {
-            const uint32_t l = s_list[warp][cc];
-            const uint32_t code = s_code[warp][cc][jj];
-            const uint32_t rcode = s_rcode[warp][cc][jr];
-            const float4 cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D + t0));
-            const float4 bv = __ldg(reinterpret_cast<const float4*>(
-                books + ((size_t)jj * ks + code) * ds + bo));
-            const float4 rv = __ldg(reinterpret_cast<const float4*>(
-                rbooks + ((size_t)jr * ks + rcode) * dsr + ro));
-            const float d0 = __fsub_rn(x4.x, __fadd_rn(__fadd_rn(cv.x, bv.x), rv.x));
-            const float d1 = __fsub_rn(x4.y, __fadd_rn(__fadd_rn(cv.y, bv.y), rv.y));
-            const float d2 = __fsub_rn(x4.z, __fadd_rn(__fadd_rn(cv.z, bv.z), rv.z));
-            const float d3 = __fsub_rn(x4.w, __fadd_rn(__fadd_rn(cv.w, bv.w), rv.w));
-            tile[cc * RW_LD + lane] =
-                make_float4(__fmul_rn(d0, d0), __fmul_rn(d1, d1), __fmul_rn(d2, d2), __fmul_rn(d3, d3));
-        }
-        __syncwarp();
-        if (c < n) {
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll 8
-            for (int g = 0; g < 32; ++g) {
-                const float4 v = tile[lane * RW_LD + g];
-                s0 = __fadd_rn(s0, v.x);
-                s1 = __fadd_rn(s1, v.y);
-                s2 = __fadd_rn(s2, v.z);
-                s3 = __fadd_rn(s3, v.w);
-            }
-            keys[c] = nb_key(__fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3)), my_id);
-        }
-        __syncwarp();
-    }
-    __syncthreads();
-    bitonic_sort_kv(keys, nullptr, n2);
-    const uint32_t cnt = min(n, k);
-    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
-        const bool live = i < cnt;
-        out_ids[q * k + i] = live ? key_id(keys[i]) : 0xffffffffu;
-        out_dists[q * k + i] = live ? key_dist(keys[i]) : __int_as_float(0x7f800000);
-    }
-    if (threadIdx.x == 0) out_cnt[q] = cnt;
-}
-
 // K5a (cooperative, d = 128, m = 8, ks = 256): refined distances of every
 // shortlist entry.  Persistent CTAs keep the PQ code book (128 KiB) in shared
 // memory; a warp takes 32 candidates of one query at a time.  Lane g owns
@@ -636,7 +541,7 @@ constexpr int RC_TLD = 132;  // tile row stride (floats): conflict-free transpos
 // m' >= 16 the refinement rows are the smaller, more numerous segments (m' = 32:
 // 32 separate 16-B rows per candidate), so keeping them on-chip saves the most
 // L1 wavefronts.
-template <int DSR, bool RB_SMEM>
+template <int DSR>
 __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
     const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
     const uint32_t* __restrict__ sl_cnt, uint32_t stride, size_t nq, const float* __restrict__ xq,
@@ -645,6 +550,7 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
     const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks,
     float* __restrict__ rdist, uint32_t* __restrict__ rid) {
     constexpr int D = 128, MP = D / DSR;  // m' = D / DSR
+    constexpr bool RB_SMEM = true;
     constexpr int META = 32 + 64 + 8 * MP;  // words per warp: list[32], code[32] u64, rcode[32][MP] B
     extern __shared__ float4 rc_smem[];
     float4* bk = rc_smem;                                            // [8][256][4] float4
@@ -810,29 +716,6 @@ __global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
             __syncwarp();
         }
     }
-}
-
-// K5a: refined distances of every shortlist entry, one thread per candidate
-// (no shared memory, full occupancy: the random code / code-book gathers are
-// latency bound).  Rows shorter than the stride are padded with +inf keys.
-template <bool FAST>
-__global__ __launch_bounds__(256) void rerank_dist_kernel(
-    const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
-    const uint32_t* __restrict__ sl_cnt, uint32_t stride, size_t nq, const float* __restrict__ xq,
-    uint32_t d, const uint16_t* __restrict__ block_list, const float* __restrict__ coarse,
-    const uint8_t* __restrict__ codes, const float* __restrict__ books, uint32_t m,
-    const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks, uint32_t mprime,
-    uint32_t ks, float* __restrict__ rdist, uint32_t* __restrict__ rid, u64 nz) {
-    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nq * stride) return;
-    const size_t q = t / stride;
-    const uint32_t i = (uint32_t)(t % stride);
-    if (i >= sl_cnt[q]) return;
-    const uint32_t p = sl_pos[t];
-    const uint32_t l = block_list[p >> 4];
-    rid[t] = key_id(sl_key[t]);
-    rdist[t] = rerank_dist<FAST>(xq + q * d, d, coarse + (size_t)l * d, books, codes + (size_t)p * m,
-                                 d / m, rbooks, rcodes + (size_t)p * mprime, d / mprime, ks, nz);
 }
 
 // K5b: top-k of (rdist, rid) rows under (dist, id): radix select on the
@@ -1045,24 +928,17 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
                    const uint16_t* block_list, const float* coarse,
                    const uint8_t* codes, const float* books, uint32_t m, const uint8_t* rcodes,
                    const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
-                   uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s) {
+                   uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s,
+                   cudaEvent_t ev_dist_done) {
     if (nq == 0) return;
     uint32_t n2 = 1;
     while (n2 < sl_stride) n2 <<= 1;
-    const size_t smem = ((d + 3) & ~3u) * sizeof(float) + (size_t)n2 * sizeof(u64);
-    if (smem > 200 * 1024) throw ArgError("shortlist too large for the device re-ranker");
-    const bool fast = d % 4 == 0 && (d / m) % 4 == 0 && (d / mprime) % 4 == 0;
-    // default: cooperative distances (d = 128, m = 8, ks = 256) + radix top-k;
-    // PQRR_RERANK=cta|split|warp select the older kernels (A/B runs)
-    static const std::string impl = [] {
-        const char* e = getenv("PQRR_RERANK");
-        return std::string(e ? e : "coop");
-    }();
-    const bool want_warp = impl == "warp";
     uint32_t k2 = 1;
     while (k2 < k) k2 <<= 1;
     const uint32_t dsr = mprime ? d / mprime : 0;
-    const bool coop_ok = impl == "coop" && d == 128 && m == 8 && ks == 256 && mprime * dsr == d &&
+    // every BASELINE shape (d = 128, m = 8, ks = 256, m' in {8, 16, 32}):
+    // cooperative distances + per-query top-k; other shapes: CTA per query
+    const bool coop_ok = d == 128 && m == 8 && ks == 256 && mprime * dsr == d &&
                          (dsr == 4 || dsr == 8 || dsr == 16) && (size_t)k2 * 8 <= 200 * 1024;
     if (coop_ok) {
         const size_t tot = nq * (size_t)sl_stride;
@@ -1080,19 +956,12 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
                 reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, nq, xq, block_list,
                 coarse, codes, books, rcodes, rbooks, rd, ri);
         };
-        static const bool rb_smem = !(getenv("PQRR_RERANK_TABLE") &&
-                                      std::string(getenv("PQRR_RERANK_TABLE")) == "pq");
-        if (rb_smem) {
-            if (dsr == 8) go(rerank_coop_kernel<8, true>);
-            else if (dsr == 4) go(rerank_coop_kernel<4, true>);
-            else go(rerank_coop_kernel<16, true>);
-        } else {
-            if (dsr == 8) go(rerank_coop_kernel<8, false>);
-            else if (dsr == 4) go(rerank_coop_kernel<4, false>);
-            else go(rerank_coop_kernel<16, false>);
-        }
+        if (dsr == 8) go(rerank_coop_kernel<8>);
+        else if (dsr == 4) go(rerank_coop_kernel<4>);
+        else go(rerank_coop_kernel<16>);
         PQRR_LAUNCH_CHECK();
         count_launch();
+        if (ev_dist_done) PQRR_CUDA(cudaEventRecord(ev_dist_done, s));
         if (!launch_rerank_topk_warp(rd, ri, sl_cnt, sl_stride, nq, k, out_ids, out_dists, out_cnt, s)) {
             set_smem((const void*)rerank_topk_kernel, (size_t)k2 * 8);
             rerank_topk_kernel<<<(unsigned)nq, SEL_THREADS, (size_t)k2 * 8, s>>>(
@@ -1104,53 +973,21 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
         PQRR_CUDA(cudaFreeAsync(ri, s));
         return;
     }
-    if (impl == "split" && (size_t)k2 * 8 <= 200 * 1024) {
-        const size_t tot = nq * (size_t)sl_stride;
-        float* rd = nullptr;
-        uint32_t* ri = nullptr;
-        PQRR_CUDA(cudaMallocAsync(&rd, tot * sizeof(float), s));
-        PQRR_CUDA(cudaMallocAsync(&ri, tot * sizeof(uint32_t), s));
-        const unsigned g = (unsigned)((tot + 255) / 256);
-        if (fast)
-            rerank_dist_kernel<true><<<g, 256, 0, s>>>(
-                reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, nq, xq, d,
-                block_list, coarse, codes, books, m, rcodes, rbooks, mprime, ks, rd, ri, kNegZero2);
-        else
-            rerank_dist_kernel<false><<<g, 256, 0, s>>>(
-                reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, nq, xq, d,
-                block_list, coarse, codes, books, m, rcodes, rbooks, mprime, ks, rd, ri, kNegZero2);
-        PQRR_LAUNCH_CHECK();
-        set_smem((const void*)rerank_topk_kernel, (size_t)k2 * 8);
-        rerank_topk_kernel<<<(unsigned)nq, SEL_THREADS, (size_t)k2 * 8, s>>>(
-            rd, ri, sl_cnt, sl_stride, k, k2, out_ids, out_dists, out_cnt);
-        PQRR_LAUNCH_CHECK();
-        PQRR_CUDA(cudaFreeAsync(rd, s));
-        PQRR_CUDA(cudaFreeAsync(ri, s));
-        count_launch(2);
-        return;
-    }
-    if (want_warp && fast && d == 128 && m == 8 && mprime % 8 == 0 && mprime <= 32) {
-        const size_t wsmem = (size_t)RW_WARPS * 32 * RW_LD * sizeof(float4) + (size_t)n2 * sizeof(u64);
-        if (wsmem > 220 * 1024) throw ArgError("shortlist too large for the device re-ranker");
-        set_smem((const void*)rerank_warp_kernel, wsmem);
-        rerank_warp_kernel<<<(unsigned)nq, RW_WARPS * 32, wsmem, s>>>(
-            reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, block_list,
-            coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists, out_cnt);
-    } else if (fast) {
-        set_smem((const void*)rerank_kernel<true>, smem);
-        rerank_kernel<true><<<(unsigned)nq, 256, smem, s>>>(
+    const size_t smem = ((d + 3) & ~3u) * sizeof(float) + (size_t)n2 * sizeof(u64);
+    if (smem > 200 * 1024) throw ArgError("shortlist too large for the device re-ranker");
+    const bool fast = d % 4 == 0 && (d / m) % 4 == 0 && (d / mprime) % 4 == 0;
+    auto go = [&](auto kern) {
+        set_smem((const void*)kern, smem);
+        kern<<<(unsigned)nq, 256, smem, s>>>(
             reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, d, block_list,
             coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists,
             out_cnt, kNegZero2);
-    } else {
-        set_smem((const void*)rerank_kernel<false>, smem);
-        rerank_kernel<false><<<(unsigned)nq, 256, smem, s>>>(
-            reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, xq, d, block_list,
-            coarse, codes, books, m, rcodes, rbooks, mprime, ks, k, out_ids, out_dists,
-            out_cnt, kNegZero2);
-    }
+    };
+    if (fast) go(rerank_kernel<true>);
+    else go(rerank_kernel<false>);
     PQRR_LAUNCH_CHECK();
     count_launch();
+    if (ev_dist_done) PQRR_CUDA(cudaEventRecord(ev_dist_done, s));
 }
 
 void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* counts, size_t nq,

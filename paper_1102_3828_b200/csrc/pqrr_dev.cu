@@ -165,10 +165,46 @@ __global__ void scatter_shortlist(const u64* __restrict__ skey, const uint32_t* 
     if (j == 0) cnt[q] = scnt[r];
 }
 
+// flag[0]: some row holds fewer than k entries ("shortlist too small");
+// flag[2..3]: the total shortlist entries (u64), the re-ranker's candidates
 __global__ void min_count_kernel(const uint32_t* __restrict__ cnt, size_t nq, uint32_t k,
                                  unsigned* __restrict__ flag) {
     size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q < nq && cnt[q] < k) atomicOr(flag, 1u);
+    const unsigned long long c = q < nq ? cnt[q] : 0ull;
+    unsigned long long v = c;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), v);
+}
+
+// code_of_id (ivf_index.hpp:33-40) + RefineCodes::code (refine.hpp:27): per id
+// its list, first-stage code and refinement code (list = UINT32_MAX if absent)
+__global__ void lookup_ids_kernel(const uint32_t* __restrict__ ids, size_t n, uint32_t id_lo,
+                                  uint32_t map_n, const uint32_t* __restrict__ map,
+                                  const uint64_t* __restrict__ off, uint32_t nlists,
+                                  const uint8_t* __restrict__ codes, uint32_t m,
+                                  const uint8_t* __restrict__ rcodes, uint32_t mprime,
+                                  uint32_t* __restrict__ o_list, uint8_t* __restrict__ o_codes,
+                                  uint8_t* __restrict__ o_rcodes) {
+    const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const uint32_t id = ids[v];
+    const uint32_t p = (id >= id_lo && id - id_lo < map_n) ? map[id - id_lo] : 0xffffffffu;
+    if (p == 0xffffffffu) {
+        if (o_list) o_list[v] = 0xffffffffu;
+        if (o_codes) for (uint32_t j = 0; j < m; ++j) o_codes[v * m + j] = 0;
+        if (o_rcodes) for (uint32_t j = 0; j < mprime; ++j) o_rcodes[v * mprime + j] = 0;
+        return;
+    }
+    uint32_t lo = 0, hi = nlists;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (off[mid] <= p) lo = mid;
+        else hi = mid;
+    }
+    if (o_list) o_list[v] = lo;
+    if (o_codes) for (uint32_t j = 0; j < m; ++j) o_codes[v * m + j] = codes[(size_t)p * m + j];
+    if (o_rcodes) for (uint32_t j = 0; j < mprime; ++j) o_rcodes[v * mprime + j] = rcodes[(size_t)p * mprime + j];
 }
 
 __global__ void id_to_pos_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
@@ -340,7 +376,7 @@ struct DevIndex {
     DBuf<uint32_t> st_assign, st_ids;
     DBuf<uint8_t> st_codes, st_rcodes;
     pqrr_dev_search_stats stats{};
-    cudaEvent_t ev[12] = {};
+    cudaEvent_t ev[13] = {};
 
     ~DevIndex() {
         for (auto& e : ev)
@@ -915,6 +951,9 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[11], s));
 
     // ---- K4 main scan: candidates (d <= tau, or the filter's superset)
+    // exactness-check readback: [0..1] max count / fail, [2..5] u64 candidate
+    // totals, [6..7] u64 (live pair, entry) lookups of K4f
+    unsigned* maxn = ws.zeros<unsigned>(8);
     float* cand_dist = ws.alloc<float>(nq * (size_t)cap);
     uint32_t* cand_pos = ws.alloc<uint32_t>(nq * (size_t)cap);
     uint32_t* cand_cnt = ws.zeros<uint32_t>(nq);
@@ -963,7 +1002,8 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
             if (two_phase) p1 = PairSet{im_far.pair_sorted, im_far.list_cnt, im_far.list_first, im_far.item_off,
                                         im_near.n_items, pair_bound};
             launch_live_pairs(f, p0, p1, im.list_first, im.list_cnt, c, live_slot, live_pair, live_cnt,
-                              if64.item_off, if64.item_start, if64.item_nq, if64.chunk, s);
+                              if64.item_off, if64.item_start, if64.item_nq, if64.chunk, s,
+                              reinterpret_cast<unsigned long long*>(maxn + 6));
         }
         launch_ivf_filter(f, s);
         if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[9], s));
@@ -1020,7 +1060,6 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
 
     // ---- exactness check of the threshold
     uint8_t* fail = ws.alloc<uint8_t>(nq);
-    unsigned* maxn = ws.zeros<unsigned>(6);
     check_fail_kernel<<<nblk(nq), 256, 0, s>>>(sampled, cand_cnt, cand_le, nq, kprime, cap, fail,
                                                 maxn, reinterpret_cast<unsigned long long*>(maxn + 2),
                                                 reinterpret_cast<unsigned long long*>(maxn + 4));
@@ -1036,16 +1075,17 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[6], s));
     }
     std::vector<uint8_t> h_fail(nq);
-    unsigned h_maxn[6] = {0, 0, 0, 0, 0, 0};
+    unsigned h_maxn[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     PQRR_CUDA(cudaMemcpyAsync(h_fail.data(), fail, nq, cudaMemcpyDeviceToHost, s));
-    PQRR_CUDA(cudaMemcpyAsync(h_maxn, maxn, 24, cudaMemcpyDeviceToHost, s));
+    PQRR_CUDA(cudaMemcpyAsync(h_maxn, maxn, 32, cudaMemcpyDeviceToHost, s));
     PQRR_CUDA(cudaStreamSynchronize(s));
     static const bool force_retry = getenv("PQRR_FORCE_RETRY") != nullptr;  // test hook
     if (force_retry && depth == 0)
         for (size_t q = 0; q < nq; ++q) h_fail[q] = (uint8_t)(1 + (q & 1));
-    uint64_t total_cand = 0, total_le = 0;
+    uint64_t total_cand = 0, total_le = 0, live_entries = 0;
     std::memcpy(&total_cand, h_maxn + 2, 8);
     std::memcpy(&total_le, h_maxn + 4, 8);
+    std::memcpy(&live_entries, h_maxn + 6, 8);
 
     // ---- exact top-k' selection (sorted: smem sized by the largest count)
     if (!early_select) {
@@ -1070,7 +1110,11 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         st.ms_threshold += el(3, 4);
         st.ms_scan += el(11, 5);
         st.ms_select += el(5, 6);
-        if (use_filter) st.ms_filter += el(11, 9);
+        if (use_filter) {
+            st.ms_filter += el(11, 9);
+            st.ms_recheck += el(9, 5);
+            st.filter_live_entries += live_entries;
+        }
         st.work_items += n_items;
         st.sampled_entries += total_samples;
         st.scanned_entries += h_grand[0];
@@ -1161,18 +1205,19 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
         }
     }
     if (k > 0) {
-        unsigned* flag = ws.zeros<unsigned>(1);
+        unsigned* flag = ws.zeros<unsigned>(4);
         min_count_kernel<<<nblk(nq), 256, 0, s>>>(sl.cnt, nq, k, flag);
         PQRR_LAUNCH_CHECK();
         count_launch();
-        unsigned h_flag = 0;
-        PQRR_CUDA(cudaMemcpyAsync(&h_flag, flag, 4, cudaMemcpyDeviceToHost, s));
+        unsigned h_flag[4] = {0, 0, 0, 0};
+        PQRR_CUDA(cudaMemcpyAsync(h_flag, flag, 16, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaStreamSynchronize(s));
-        if (h_flag) throw ShortlistError();
+        if (h_flag[0]) throw ShortlistError();
+        std::memcpy(&ix.stats.rerank_candidates, h_flag + 2, 8);
         PQRR_CUDA(cudaEventRecord(ix.ev[7], s));
         launch_rerank(reinterpret_cast<uint64_t*>(sl.key), sl.pos, sl.cnt, kprime, nq, xq, ix.d,
                       ix.block_list.p, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
-                      ix.rbooks.p, ix.mprime, ix.ks, k, out_ids, out_dists, out_cnt, s);
+                      ix.rbooks.p, ix.mprime, ix.ks, k, out_ids, out_dists, out_cnt, s, ix.ev[12]);
     } else {
         PQRR_CUDA(cudaEventRecord(ix.ev[7], s));
         launch_unpack_keys(reinterpret_cast<uint64_t*>(sl.key), sl.cnt, nq, kprime, out_ids, out_dists, s);
@@ -1187,6 +1232,7 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
     };
     auto& st = ix.stats;
     st.ms_rerank = el(7, 8);
+    if (k > 0) st.ms_rerank_dist = el(7, 12);
     st.ms_total = el(10, 8);
     st.kernels = (uint32_t)(launch_count() - l0);
 }
@@ -1762,6 +1808,33 @@ int pqrr_dev_rerank_f32(pqrr_dev_index* h, const float* queries, size_t nq, cons
                         const uint32_t* sl_counts, size_t sl_stride, size_t k, uint32_t* out_ids,
                         float* out_dists) {
     return rerank_host(h, queries, nullptr, nq, sl_ids, sl_counts, sl_stride, k, out_ids, out_dists);
+}
+
+int pqrr_dev_lookup_ids(pqrr_dev_index* h, const uint32_t* ids, size_t n, uint32_t* out_list,
+                        uint8_t* out_codes, uint8_t* out_rcodes) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        if (n == 0) return;
+        ensure_id_map(ix);
+        cudaStream_t s = ix.stream;
+        Workspace ws(s);
+        uint32_t* d_ids = ws.alloc<uint32_t>(n);
+        PQRR_CUDA(cudaMemcpyAsync(d_ids, ids, n * 4, cudaMemcpyHostToDevice, s));
+        uint32_t* o_l = out_list ? ws.alloc<uint32_t>(n) : nullptr;
+        uint8_t* o_c = out_codes ? ws.alloc<uint8_t>(n * ix.m) : nullptr;
+        uint8_t* o_r = (out_rcodes && ix.mprime) ? ws.alloc<uint8_t>(n * ix.mprime) : nullptr;
+        lookup_ids_kernel<<<nblk(n), 256, 0, s>>>(d_ids, n, (uint32_t)id_lo_of(ix), (uint32_t)ix.id_map.n,
+                                                  ix.id_map.p, ix.list_off.p, ix.c, ix.codes.p, ix.m,
+                                                  ix.rcodes.p, ix.mprime, o_l, o_c, o_r);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        if (o_l) PQRR_CUDA(cudaMemcpyAsync(out_list, o_l, n * 4, cudaMemcpyDeviceToHost, s));
+        if (o_c) PQRR_CUDA(cudaMemcpyAsync(out_codes, o_c, n * ix.m, cudaMemcpyDeviceToHost, s));
+        if (o_r) PQRR_CUDA(cudaMemcpyAsync(out_rcodes, o_r, n * ix.mprime, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaStreamSynchronize(s));
+    });
 }
 
 int pqrr_dev_reconstruct(pqrr_dev_index* h, const uint32_t* ids, size_t n, float* out) {

@@ -401,6 +401,20 @@ class IvfIndex:
                                                   d_sl_counts_ptr, sl_stride, k, d_ids_ptr,
                                                   d_dists_ptr, d_counts_ptr, stream_ptr or None))
 
+    def lookup_ids(self, ids):
+        """(list_of_id, codes [n, m], rcodes [n, m'] or None) of the given ids
+        (code_of_id, ivf_index.hpp:33-40; RefineCodes::code, refine.hpp:27);
+        list = 0xffffffff for ids never added."""
+        ids = np.ascontiguousarray(ids, np.uint32)
+        n = len(ids)
+        mp = self.info()["mprime"]
+        lst = np.zeros(n, np.uint32)
+        codes = np.zeros((n, self.pq.m), np.uint8)
+        rc = np.zeros((n, mp), np.uint8) if mp else None
+        check(lib.pqrr_dev_lookup_ids(self.h, ids, n, lst.ctypes.data, codes.ctypes.data,
+                                      rc.ctypes.data if rc is not None else None))
+        return lst, codes, rc
+
     def last_stats(self) -> dict:
         st = _lib.SearchStats()
         check(lib.pqrr_dev_last_search_stats(self.h, C.byref(st)))
