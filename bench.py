@@ -297,7 +297,7 @@ def main():
                     help="full: host-built index + every query (n <= 10M); sample: probed-list "
                          "reference on --ref-queries queries + add-path re-encode sample")
     ap.add_argument("--ref-queries", type=int, default=256)
-    ap.add_argument("--shard-mode", default="local", choices=["local", "exact"],
+    ap.add_argument("--shard-mode", default="exact", choices=["local", "exact"],
                     help="N>1: per-shard shortlists (north star) or the single-index-exact flow")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])

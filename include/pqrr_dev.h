@@ -280,6 +280,13 @@ int pqrr_dev_merge_topk_device(int device, const uint32_t* ids, const float* dis
                                const uint32_t* counts, size_t nq, uint32_t parts, uint32_t width,
                                uint32_t k, uint32_t* out_ids, float* out_dists,
                                uint32_t* out_counts, void* stream);
+/* K7 on ONE all-gathered buffer: `packed` holds `parts` consecutive blocks of
+ * 2 * nq * width + nq 32-bit words, each [ids nq x width | dists nq x width |
+ * counts nq] -- the layout a shard's search writes straight into its slice,
+ * so a merge needs one all-gather (device pointers, stream-ordered).        */
+int pqrr_dev_merge_packed_device(int device, const void* packed, size_t nq, uint32_t parts,
+                                 uint32_t width, uint32_t k, uint32_t* d_out_ids,
+                                 float* d_out_dists, uint32_t* d_out_counts, void* stream);
 
 /* Per-stage device times (CUDA events on the index stream) of the last search. */
 typedef struct {

@@ -7,13 +7,20 @@
 // top of the C ABI in include/pqrr_dev.h.  A maintainer adds this file and
 // libpqrr_b200.so to the reference build; callers keep using pqrr::ivf_*.
 //
-// The device index behind a host IvfIndex is created lazily and cached, keyed
-// by the IvfIndex's list storage (and the RefineCodes buffer when re-ranking);
-// IvfIndex objects are immutable after build, so the cache never
-// goes stale while the object lives.
+// The device index behind a host IvfIndex is created lazily and cached.  A
+// cache entry is found by the addresses of the IvfIndex's list storage (and
+// the RefineCodes buffer when re-ranking) and is only reused when its content
+// signature still matches: n, every list length, the coarse / PQ / refine
+// code books in full, the first and last (id, code) of every list, a strided
+// sample of all entries and of the refinement codes.  A new IvfIndex that
+// reuses a freed address therefore gets a fresh device index.  The cache is
+// LRU-bounded (PQRR_INDEX_CACHE entries, default 2); evicted device indexes
+// are destroyed once no call still uses them, and
+// pqrr::b200::release_device_indexes() drops them all.
 #include <cstdlib>
 #include <cstring>
-#include <map>
+#include <list>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -65,30 +72,133 @@ ProductQuantizer make_pq(std::uint32_t d, std::uint32_t m, std::uint32_t ks, con
     return pq;
 }
 
+using Handle = std::shared_ptr<pqrr_dev_index>;
+
+Handle own(pqrr_dev_index* h) {
+    return Handle(h, [](pqrr_dev_index* p) { pqrr_dev_index_destroy(p); });
+}
+
+// FNV-1a over byte ranges
+struct Fnv {
+    std::uint64_t h = 1469598103934665603ull;
+    void add(const void* p, std::size_t n) {
+        const auto* b = static_cast<const std::uint8_t*>(p);
+        for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    }
+    template <class T>
+    void pod(const T& v) { add(&v, sizeof(T)); }
+};
+
+struct Signature {
+    std::uint64_t n = 0, books = 0, entries = 0, refine = 0;
+    std::vector<std::uint64_t> lens;
+    bool operator==(const Signature&) const = default;
+};
+
+Signature signature(const IvfIndex& ix, const RefineQuantizer* rq, const RefineCodes* codes) {
+    Signature s;
+    s.n = ix.n;
+    s.lens.reserve(ix.c());
+    Fnv b, e;
+    b.add(ix.coarse.centroids.data(), ix.coarse.centroids.size() * 4);
+    for (const Codebook& cb : ix.pq.books) b.add(cb.centroids.data(), cb.centroids.size() * 4);
+    const std::uint32_t m = ix.pq.m;
+    std::uint64_t total = 0;
+    for (const IvfList& L : ix.lists) {
+        s.lens.push_back(L.ids.size());
+        total += L.ids.size();
+        if (!L.ids.empty()) {
+            e.pod(L.ids.front());
+            e.pod(L.ids.back());
+            e.add(L.codes.data(), m);
+            e.add(L.codes.data() + (L.ids.size() - 1) * m, m);
+        }
+    }
+    const std::uint64_t stride = std::max<std::uint64_t>(1, total / 65536);
+    std::uint64_t base = 0;
+    for (const IvfList& L : ix.lists) {  // every stride-th entry of the list-order concatenation
+        for (std::uint64_t g = (base + stride - 1) / stride * stride; g < base + L.ids.size(); g += stride) {
+            e.pod(L.ids[g - base]);
+            e.add(L.codes.data() + (g - base) * m, m);
+        }
+        base += L.ids.size();
+    }
+    s.books = b.h;
+    s.entries = e.h;
+    if (rq && codes) {
+        Fnv r;
+        for (const Codebook& cb : rq->pq.books) r.add(cb.centroids.data(), cb.centroids.size() * 4);
+        r.pod(codes->m);
+        const std::size_t nb = codes->bytes.size();
+        r.pod(nb);
+        const std::size_t st = std::max<std::size_t>(1, nb / 65536);
+        for (std::size_t i = 0; i < nb; i += st) r.pod(codes->bytes[i]);
+        if (nb) r.pod(codes->bytes[nb - 1]);
+        s.refine = r.h;
+    }
+    return s;
+}
+
+struct Entry {
+    std::pair<const void*, const void*> key;
+    Signature sig;
+    Handle h;
+};
+
 struct Cache {
     std::mutex mu;
-    std::map<std::pair<const void*, const void*>, pqrr_dev_index*> map;
+    std::list<Entry> lru;  // most recently used first
+    std::size_t cap() const {
+        const char* e = std::getenv("PQRR_INDEX_CACHE");
+        const long v = e ? std::atol(e) : 2;
+        return v > 0 ? std::size_t(v) : 1;
+    }
+    void put(Entry en) {  // caller holds mu
+        for (auto it = lru.begin(); it != lru.end(); ++it)
+            if (it->key == en.key) {
+                lru.erase(it);
+                break;
+            }
+        lru.push_front(std::move(en));
+        while (lru.size() > cap()) lru.pop_back();
+    }
 };
 Cache& cache() {
     static Cache c;
     return c;
 }
 
-// Device index for (index[, refinement]); built from the host lists once.
-pqrr_dev_index* device_index(const IvfIndex& ix, const RefineQuantizer* rq, const RefineCodes* codes) {
-    auto key = std::make_pair(static_cast<const void*>(ix.lists.data()),
-                              static_cast<const void*>(codes ? codes->bytes.data() : nullptr));
+std::pair<const void*, const void*> cache_key(const IvfIndex& ix, const RefineCodes* codes) {
+    return {static_cast<const void*>(ix.lists.data()),
+            static_cast<const void*>(codes ? codes->bytes.data() : nullptr)};
+}
+
+// Device index for (index[, refinement]); built from the host lists on a
+// cache miss or a signature mismatch.
+Handle device_index(const IvfIndex& ix, const RefineQuantizer* rq, const RefineCodes* codes) {
+    const auto key = cache_key(ix, codes);
+    Signature sig = signature(ix, rq, codes);
     auto& c = cache();
-    std::lock_guard<std::mutex> lk(c.mu);
-    auto it = c.map.find(key);
-    if (it != c.map.end()) return it->second;
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (auto it = c.lru.begin(); it != c.lru.end(); ++it)
+            if (it->key == key) {
+                if (it->sig == sig) {
+                    c.lru.splice(c.lru.begin(), c.lru, it);
+                    return it->h;
+                }
+                c.lru.erase(it);  // a different index now lives at this address
+                break;
+            }
+    }
     const std::uint32_t mp = rq ? rq->pq.m : 0;
     auto books = flat_books(ix.pq);
     std::vector<float> rbooks;
     if (rq) rbooks = flat_books(rq->pq);
-    pqrr_dev_index* h = nullptr;
+    pqrr_dev_index* raw = nullptr;
     check(pqrr_dev_index_create(device(), ix.pq.d, ix.c(), ix.coarse.centroids.data(), ix.pq.m,
-                                books.data(), mp, rq ? rbooks.data() : nullptr, ix.pq.ks, &h));
+                                books.data(), mp, rq ? rbooks.data() : nullptr, ix.pq.ks, &raw));
+    Handle h = own(raw);
     std::vector<std::uint64_t> off(ix.c() + 1, 0);
     for (std::uint32_t l = 0; l < ix.c(); ++l) off[l + 1] = off[l] + ix.lists[l].size();
     std::vector<std::uint32_t> ids(off.back());
@@ -101,8 +211,9 @@ pqrr_dev_index* device_index(const IvfIndex& ix, const RefineQuantizer* rq, cons
             for (std::size_t i = 0; i < L.ids.size(); ++i)
                 std::memcpy(rcs.data() + (off[l] + i) * mp, codes->code(L.ids[i]), mp);
     }
-    check(pqrr_dev_load_lists(h, off.data(), ids.data(), cds.data(), mp ? rcs.data() : nullptr));
-    c.map[key] = h;
+    check(pqrr_dev_load_lists(h.get(), off.data(), ids.data(), cds.data(), mp ? rcs.data() : nullptr));
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.put(Entry{key, std::move(sig), h});
     return h;
 }
 
@@ -226,19 +337,20 @@ IvfIndex ivf_build(Codebook coarse, ProductQuantizer pq, const VectorSet& base) 
         }
     }
     auto& c = cache();
+    Entry en{cache_key(ix, nullptr), signature(ix, nullptr, nullptr), own(h)};
     std::lock_guard<std::mutex> lk(c.mu);
-    c.map[{ix.lists.data(), nullptr}] = h;
+    c.put(std::move(en));
     return ix;
 }
 
 std::vector<SearchResult> ivf_search_batch(const IvfIndex& index, const VectorSet& queries,
                                            const IvfSearchParams& params) {
     if (queries.d != index.pq.d) throw std::invalid_argument("dimension mismatch");
-    pqrr_dev_index* h = device_index(index, nullptr, nullptr);
+    Handle h = device_index(index, nullptr, nullptr);
     const std::size_t nq = queries.n(), kp = params.kprime;
     std::vector<std::uint32_t> ids(nq * kp), cnt(nq);
     std::vector<float> d(nq * kp);
-    check(pqrr_dev_search_f32(h, queries.data.data(), nq, params.v, kp, 0, ids.data(), d.data(),
+    check(pqrr_dev_search_f32(h.get(), queries.data.data(), nq, params.v, kp, 0, ids.data(), d.data(),
                               cnt.data()));
     std::vector<SearchResult> out(nq);
     for (std::size_t q = 0; q < nq; ++q) out[q] = to_result(&ids[q * kp], &d[q * kp], cnt[q]);
@@ -274,25 +386,34 @@ RefineCodes ivf_refine_encode(const IvfIndex& index, const RefineQuantizer& rq, 
 
 std::vector<float> ivf_reconstruct(const IvfIndex& index, const RefineQuantizer& rq, std::uint32_t id,
                                    const RefineCodes& codes) {
-    pqrr_dev_index* h = device_index(index, &rq, &codes);
+    Handle h = device_index(index, &rq, &codes);
     std::vector<float> out(index.pq.d);
-    check(pqrr_dev_reconstruct(h, &id, 1, out.data()));
+    check(pqrr_dev_reconstruct(h.get(), &id, 1, out.data()));
     return out;
 }
 
 SearchResult ivf_rerank(std::span<const float> x, const SearchResult& shortlist, const IvfIndex& index,
                         const RefineQuantizer& rq, const RefineCodes& codes, std::size_t k) {
     if (k > shortlist.size()) throw std::invalid_argument("shortlist too small");
-    pqrr_dev_index* h = device_index(index, &rq, &codes);
+    Handle h = device_index(index, &rq, &codes);
     std::vector<std::uint32_t> sl(shortlist.size());
     for (std::size_t i = 0; i < sl.size(); ++i) sl[i] = shortlist[i].id;
     const std::uint32_t cnt = std::uint32_t(sl.size());
     std::vector<std::uint32_t> ids(std::max<std::size_t>(k, 1));
     std::vector<float> d(std::max<std::size_t>(k, 1));
-    check(pqrr_dev_rerank_f32(h, x.data(), 1, sl.data(), &cnt, std::max<std::size_t>(sl.size(), 1), k,
+    check(pqrr_dev_rerank_f32(h.get(), x.data(), 1, sl.data(), &cnt, std::max<std::size_t>(sl.size(), 1), k,
                               ids.data(), d.data()));
     return to_result(ids.data(), d.data(), std::uint32_t(k));
 }
+
+// Drops every cached device index (each is destroyed once no call uses it).
+namespace b200 {
+void release_device_indexes() {
+    auto& c = cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.lru.clear();
+}
+}  // namespace b200
 
 // ------------------------------------------------------------------ kernel seam (kernels.hpp:13-43)
 namespace kernels {

@@ -15,6 +15,10 @@
 
 using namespace pqrr;
 
+namespace pqrr::b200 {
+void release_device_indexes();  // integration/pqrr_ivf_b200.cpp
+}
+
 static int checks = 0, failures = 0;
 #define EXPECT(cond, what)                                      \
     do {                                                        \
@@ -108,6 +112,36 @@ int main() {
         threw = std::strcmp(e.what(), "shortlist too small") == 0;
     }
     EXPECT(threw, "shortlist too small");
+
+    // device-index cache: a different index in the SAME list storage (what a
+    // new IvfIndex at a freed address looks like) must not reuse the cached
+    // device index of the old one
+    {
+        std::vector<uint8_t> u(n * d);
+        orc_synth_rows(8, 2, 0, n, d, centers.data(), 64, u.data());
+        VectorSet base2(d, n);
+        for (size_t i = 0; i < u.size(); ++i) base2.data[i] = float(u[i]);
+        IvfIndex ix2 = ivf_build(coarse, pq, base2);
+        const void* storage = ix.lists.data();
+        for (uint32_t l = 0; l < c; ++l) ix.lists[l] = ix2.lists[l];
+        ix.list_of_id = ix2.list_of_id;
+        ix.pos_of_id = ix2.pos_of_id;
+        EXPECT(ix.lists.data() == storage, "same list storage");
+        orc_ivf* ox2 = orc_ivf_build(oc.data(), c, ob.data(), d, m, ks, base2.data.data(), n);
+        auto res2 = ivf_search_batch(ix, queries, prm);
+        orc_ivf_search_batch(ox2, queries.data.data(), nq, prm.v, prm.kprime, oi.data(), od.data(),
+                             ocnt.data());
+        bool ok = true;
+        for (size_t q = 0; q < nq; ++q) {
+            ok = ok && res2[q].size() == ocnt[q];
+            for (size_t i = 0; ok && i < res2[q].size(); ++i)
+                ok = res2[q][i].id == oi[q * prm.kprime + i] &&
+                     std::memcmp(&res2[q][i].dist, &od[q * prm.kprime + i], 4) == 0;
+        }
+        EXPECT(ok, "cache: index replaced in the same storage");
+        orc_ivf_free(ox2);
+        b200::release_device_indexes();
+    }
 
     // kernel seam: scan_topk against the serial oracle
     std::mt19937 g(5);

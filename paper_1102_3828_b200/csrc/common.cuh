@@ -108,9 +108,12 @@ __device__ __forceinline__ bool pair_live(float tau, float summ) {
 // stride alone would only ever sample one side of the pairs (a biased
 // sample: measured as frequent under-full retries at even strides).  A
 // Thue-Morse jitter popc(si) & 1 balances both sides on every sub-grid
-// si = k 2^s that the per-lane tiers of the LUT pass take.
+// si = k 2^s that the per-lane tiers of the LUT pass take.  At stride 1 every
+// entry is sampled exactly once (the exact case the retry ladder ends in), so
+// no jitter applies there; at stride >= 2 the jittered positions stay distinct.
 __device__ __forceinline__ uint32_t sample_pos(uint32_t si, uint32_t st, uint32_t len) {
-    return min(si * st + ((uint32_t)__popc(si) & 1u), len - 1u);
+    const uint32_t jit = st > 1u ? ((uint32_t)__popc(si) & 1u) : 0u;
+    return min(si * st + jit, len - 1u);
 }
 
 // 8-bit LUT block of a LUT-pass item (K2 -> K4f): LANE-major, 16 query lanes

@@ -297,10 +297,13 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
                    const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
                    uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s,
                    cudaEvent_t ev_dist_done = nullptr);
-// Merge per-shard ranked lists [parts][nq][width] into the top-k (K7).
+// Merge per-shard ranked lists into the top-k (K7).  Part p's rows are
+// ids/dists + p * ps (nq x width) and counts + p * cs (nq); ps = cs = 0 means
+// the stacked layout [parts][nq][width] + [parts][nq].
 void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* counts, size_t nq,
                        uint32_t parts, uint32_t width, uint32_t k, uint32_t* out_ids,
-                       float* out_dists, uint32_t* out_cnt, cudaStream_t s);
+                       float* out_dists, uint32_t* out_cnt, cudaStream_t s, size_t ps = 0,
+                       size_t cs = 0);
 // K1 on the tensor cores with certified exact top-w (k_coarse_tc.cu).
 bool coarse_tc_supported(uint32_t d, uint32_t w);
 void launch_coarse_norms(const float* c, uint32_t n, uint32_t d, float* out, cudaStream_t s);

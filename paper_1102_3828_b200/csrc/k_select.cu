@@ -771,8 +771,8 @@ __global__ __launch_bounds__(SEL_THREADS) void rerank_topk_kernel(
 // the global top-k under (dist, id) — one CTA per query, bitonic in smem.
 __global__ __launch_bounds__(256) void merge_topk_kernel(
     const uint32_t* __restrict__ ids, const float* __restrict__ dists,
-    const uint32_t* __restrict__ counts, size_t nq, uint32_t parts, uint32_t width, uint32_t k,
-    uint32_t n2, uint32_t* __restrict__ out_ids, float* __restrict__ out_dists,
+    const uint32_t* __restrict__ counts, size_t nq, uint32_t parts, uint32_t width, size_t ps,
+    size_t cs, uint32_t k, uint32_t n2, uint32_t* __restrict__ out_ids, float* __restrict__ out_dists,
     uint32_t* __restrict__ out_cnt) {
     extern __shared__ u64 mkeys[];
     const size_t q = blockIdx.x;
@@ -783,9 +783,9 @@ __global__ __launch_bounds__(256) void merge_topk_kernel(
         u64 key = ~0ull;
         if (i < parts * width) {
             const uint32_t p = i / width, j = i % width;
-            const size_t row = (size_t)p * nq + q;
-            if (j < counts[row]) {
-                key = nb_key(dists[row * width + j], ids[row * width + j]);
+            const size_t e = p * ps + q * width + j;
+            if (j < counts[p * cs + q]) {
+                key = nb_key(dists[e], ids[e]);
                 atomicAdd(&s_total, 1u);
             }
         }
@@ -806,18 +806,18 @@ __global__ __launch_bounds__(256) void merge_topk_kernel(
 // valid entries of all parts contiguously for select_large_kernel.
 __global__ void merge_pack_kernel(const uint32_t* __restrict__ ids, const float* __restrict__ dists,
                                   const uint32_t* __restrict__ counts, size_t nq, uint32_t parts,
-                                  uint32_t width, float* __restrict__ cd, uint32_t* __restrict__ cp,
+                                  uint32_t width, size_t ps, size_t cs, float* __restrict__ cd, uint32_t* __restrict__ cp,
                                   uint32_t* __restrict__ cid, uint32_t* __restrict__ ccnt) {
     const size_t q = blockIdx.x;
     const size_t cap = (size_t)parts * width;
     uint32_t off = 0;
     for (uint32_t p = 0; p < parts; ++p) {
-        const size_t row = (size_t)p * nq + q;
-        const uint32_t c = min(counts[row], width);
+        const size_t row = p * ps + q * width;
+        const uint32_t c = min(counts[p * cs + q], width);
         for (uint32_t j = threadIdx.x; j < c; j += blockDim.x) {
             const size_t o = q * cap + off + j;
-            cd[o] = dists[row * width + j];
-            cid[o] = ids[row * width + j];
+            cd[o] = dists[row + j];
+            cid[o] = ids[row + j];
             cp[o] = (uint32_t)o;
         }
         off += c;
@@ -992,8 +992,10 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
 
 void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* counts, size_t nq,
                        uint32_t parts, uint32_t width, uint32_t k, uint32_t* out_ids,
-                       float* out_dists, uint32_t* out_cnt, cudaStream_t s) {
+                       float* out_dists, uint32_t* out_cnt, cudaStream_t s, size_t ps, size_t cs) {
     if (nq == 0) return;
+    if (!ps) ps = nq * width;  // [parts, nq, width] + [parts, nq] by default
+    if (!cs) cs = nq;
     uint32_t n2 = 1;
     while (n2 < parts * width) n2 <<= 1;
     const size_t smem = (size_t)n2 * sizeof(u64);
@@ -1015,7 +1017,7 @@ void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* 
         PQRR_CUDA(cudaMallocAsync(&ccnt, nq * 4, s));
         PQRR_CUDA(cudaMallocAsync(&skey, nq * k * 8, s));
         PQRR_CUDA(cudaMallocAsync(&spos, nq * k * 4, s));
-        merge_pack_kernel<<<(unsigned)nq, 256, 0, s>>>(ids, dists, counts, nq, parts, width, cd, cp,
+        merge_pack_kernel<<<(unsigned)nq, 256, 0, s>>>(ids, dists, counts, nq, parts, width, ps, cs, cd, cp,
                                                        cid, ccnt);
         PQRR_LAUNCH_CHECK();
         count_launch();
@@ -1033,7 +1035,7 @@ void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* 
         return;
     }
     set_smem((const void*)merge_topk_kernel, smem);
-    merge_topk_kernel<<<(unsigned)nq, 256, smem, s>>>(ids, dists, counts, nq, parts, width, k, n2,
+    merge_topk_kernel<<<(unsigned)nq, 256, smem, s>>>(ids, dists, counts, nq, parts, width, ps, cs, k, n2,
                                                       out_ids, out_dists, out_cnt);
     PQRR_LAUNCH_CHECK();
     count_launch();

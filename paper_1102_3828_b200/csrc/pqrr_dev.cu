@@ -1940,6 +1940,23 @@ int pqrr_dev_load_lists(pqrr_dev_index* h, const uint64_t* offsets, const uint32
                 min_id = std::min<uint64_t>(min_id, ids[i]);
             }
         }
+        // every id once across all lists (the partition invariant of
+        // ivf_index.hpp:27-36), code bytes inside the code books
+        {
+            std::vector<uint64_t> seen((max_id - min_id) / 64 + 1, 0);
+            for (uint64_t i = 0; i < n; ++i) {
+                const uint64_t b = ids[i] - min_id;
+                if (seen[b >> 6] >> (b & 63) & 1) throw ArgError("corrupt file");
+                seen[b >> 6] |= 1ull << (b & 63);
+            }
+        }
+        if (ix.ks < 256) {
+            for (uint64_t i = 0; i < n * ix.m; ++i)
+                if (codes[i] >= ix.ks) throw ArgError("corrupt file");
+            if (ix.mprime)
+                for (uint64_t i = 0; i < n * ix.mprime; ++i)
+                    if (rcodes[i] >= ix.ks) throw ArgError("corrupt file");
+        }
         grow_staging(ix, n);
         cudaStream_t s = ix.stream;
         PQRR_CUDA(cudaMemcpyAsync(ix.st_assign.p, assign.data(), n * 4, cudaMemcpyHostToDevice, s));
@@ -2136,6 +2153,21 @@ int pqrr_dev_merge_topk_device(int device, const uint32_t* ids, const float* dis
                                void* stream) {
     return merge_impl(device, ids, dists, counts, nq, parts, width, k, out_ids, out_dists, out_counts,
                       true, stream);
+}
+
+int pqrr_dev_merge_packed_device(int device, const void* packed, size_t nq, uint32_t parts,
+                                 uint32_t width, uint32_t k, uint32_t* out_ids, float* out_dists,
+                                 uint32_t* out_counts, void* stream) {
+    return guarded([&] {
+        if (nq == 0 || k == 0) return;
+        if (parts == 0 || width == 0) throw ArgError("parts and width must be positive");
+        DeviceGuard g(device);
+        const uint32_t* base = static_cast<const uint32_t*>(packed);
+        const size_t blk = 2 * nq * width + nq;
+        launch_merge_topk(base, reinterpret_cast<const float*>(base + nq * width), base + 2 * nq * width,
+                          nq, parts, width, k, out_ids, out_dists, out_counts,
+                          static_cast<cudaStream_t>(stream), blk, blk);
+    });
 }
 
 int pqrr_dev_last_search_stats(pqrr_dev_index* h, pqrr_dev_search_stats* out) {

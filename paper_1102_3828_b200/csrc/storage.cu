@@ -25,6 +25,8 @@
 #include <string>
 #include <vector>
 
+#include <sys/stat.h>
+
 #include "../../include/pqrr_dev.h"
 #include "internal.h"
 
@@ -43,46 +45,62 @@ struct IoError : std::runtime_error {
     explicit IoError(const std::string& s) : std::runtime_error(s) {}
 };
 
+// Streaming writer: sections go straight to the file (no whole-file buffer;
+// a 1B-vector index is ~44 GB).
 struct Writer {
-    std::vector<uint8_t> buf;
+    FILE* f = nullptr;
+    std::string path;
+    explicit Writer(const char* p) : path(p) {
+        f = std::fopen(p, "wb");
+        if (!f) throw IoError(std::string("cannot open file for writing: ") + p);
+        std::setvbuf(f, nullptr, _IOFBF, 1 << 22);
+    }
+    ~Writer() {
+        if (f) std::fclose(f);
+    }
     void put(const void* p, size_t n) {
-        const uint8_t* b = static_cast<const uint8_t*>(p);
-        buf.insert(buf.end(), b, b + n);
+        if (n && std::fwrite(p, 1, n, f) != n) throw IoError("write failed: " + path);
     }
     template <class T>
     void pod(T v) { put(&v, sizeof(T)); }
-    void flush(const char* path) {
-        FILE* f = std::fopen(path, "wb");
-        if (!f) throw IoError(std::string("cannot open file for writing: ") + path);
-        const size_t w = buf.empty() ? 0 : std::fwrite(buf.data(), 1, buf.size(), f);
+    void close() {
         const int c = std::fclose(f);
-        if (w != buf.size() || c != 0) throw IoError(std::string("write failed: ") + path);
+        f = nullptr;
+        if (c != 0) throw IoError("write failed: " + path);
     }
 };
 
+// Streaming reader: the file size comes from fstat and every section is read
+// straight into its destination array.
 struct Reader {
-    std::vector<uint8_t> buf;
-    size_t pos = 0;
+    FILE* f = nullptr;
+    uint64_t size = 0, pos = 0;
     explicit Reader(const char* path) {
-        FILE* f = std::fopen(path, "rb");
+        f = std::fopen(path, "rb");
         if (!f) throw IoError(std::string("cannot open file: ") + path);
-        uint8_t tmp[1 << 16];
-        size_t r;
-        while ((r = std::fread(tmp, 1, sizeof tmp, f)) > 0) buf.insert(buf.end(), tmp, tmp + r);
-        std::fclose(f);
+        struct stat st;
+        if (fstat(fileno(f), &st) != 0) throw IoError(std::string("cannot stat file: ") + path);
+        size = (uint64_t)st.st_size;
+        std::setvbuf(f, nullptr, _IOFBF, 1 << 22);
     }
-    size_t left() const { return buf.size() - pos; }
-    const uint8_t* take(size_t n) {
+    ~Reader() {
+        if (f) std::fclose(f);
+    }
+    uint64_t left() const { return size - pos; }
+    void read(void* dst, uint64_t n) {
         if (n > left()) throw Corrupt();
-        const uint8_t* p = buf.data() + pos;
+        if (n && std::fread(dst, 1, n, f) != n) throw Corrupt();
         pos += n;
-        return p;
     }
     template <class T>
     T pod() {
         T v;
-        std::memcpy(&v, take(sizeof(T)), sizeof(T));
+        read(&v, sizeof(T));
         return v;
+    }
+    void rewind() {
+        std::fseek(f, 0, SEEK_SET);
+        pos = 0;
     }
     void end() const {
         if (left()) throw Corrupt();
@@ -91,12 +109,7 @@ struct Reader {
 
 struct QBlock {
     uint32_t d = 0, m = 0, ks = 0;
-    const float* books = nullptr;  // points into the reader's buffer (unaligned-safe copy below)
-    std::vector<float> copy() const {
-        std::vector<float> v((size_t)ks * d);
-        std::memcpy(v.data(), books, v.size() * 4);
-        return v;
-    }
+    std::vector<float> books;  // m * ks * (d / m) floats
 };
 
 void put_qblock(Writer& w, uint32_t d, uint32_t m, uint32_t ks, const float* books) {
@@ -109,7 +122,8 @@ void put_qblock(Writer& w, uint32_t d, uint32_t m, uint32_t ks, const float* boo
 }
 
 QBlock get_qblock(Reader& r) {
-    const uint8_t* mg = r.take(4);
+    char mg[4];
+    r.read(mg, 4);
     if (std::memcmp(mg, kMagic, 4) != 0) throw Corrupt();
     if (r.pod<uint8_t>() != kVersion) throw Corrupt();
     QBlock q;
@@ -118,27 +132,9 @@ QBlock get_qblock(Reader& r) {
     q.ks = r.pod<uint32_t>();
     if (q.d == 0 || q.m == 0 || q.ks == 0 || q.d % q.m) throw Corrupt();
     if ((uint64_t)q.ks * q.d * 4 > r.left()) throw Corrupt();
-    q.books = reinterpret_cast<const float*>(r.take((size_t)q.ks * q.d * 4));
+    q.books.resize((size_t)q.ks * q.d);
+    r.read(q.books.data(), q.books.size() * 4);
     return q;
-}
-
-// Optional refinement section: refine quantizer block, m' u32, n*m' bytes.
-struct RBlock {
-    bool present = false;
-    QBlock q;
-    const uint8_t* codes = nullptr;
-};
-
-RBlock get_rblock(Reader& r, uint64_t n, uint32_t d) {
-    RBlock b;
-    if (r.left() == 0) return b;
-    b.present = true;
-    b.q = get_qblock(r);
-    if (b.q.d != d || b.q.ks > 256) throw Corrupt();
-    if (r.pod<uint32_t>() != b.q.m) throw Corrupt();
-    if (n * b.q.m > r.left()) throw Corrupt();
-    b.codes = r.take((size_t)(n * b.q.m));
-    return b;
 }
 
 void ck(int rc) {
@@ -156,30 +152,92 @@ int run(const std::function<void()>& f) {
     }
 }
 
-// Parsed index file (pointers into the reader's buffer).
+// pos_by_rank[r] = list position of the r-th smallest id.  Ids that form a
+// dense range (every id-range shard written by this library) take a direct
+// scatter (4 B per entry); anything else is sorted.  Duplicate ids are
+// "corrupt file" (the partition invariant, ivf_index.hpp:27-36).
+std::vector<uint32_t> pos_by_rank(const std::vector<uint32_t>& ids) {
+    const size_t n = ids.size();
+    std::vector<uint32_t> out(n);
+    if (!n) return out;
+    uint32_t lo = ids[0], hi = ids[0];
+    for (uint32_t v : ids) {
+        lo = std::min(lo, v);
+        hi = std::max(hi, v);
+    }
+    if ((uint64_t)hi - lo + 1 == n) {
+        std::vector<uint8_t> seen(n, 0);
+        for (size_t i = 0; i < n; ++i) {
+            const uint32_t r = ids[i] - lo;
+            if (seen[r]) throw Corrupt();
+            seen[r] = 1;
+            out[r] = (uint32_t)i;
+        }
+        return out;
+    }
+    std::vector<uint64_t> ord(n);
+    for (size_t i = 0; i < n; ++i) ord[i] = ((uint64_t)ids[i] << 32) | i;
+    std::sort(ord.begin(), ord.end());
+    for (size_t k = 0; k < n; ++k) {
+        if (k && (ord[k] >> 32) == (ord[k - 1] >> 32)) throw Corrupt();  // duplicate id
+        out[k] = (uint32_t)(ord[k] & 0xffffffffu);
+    }
+    return out;
+}
+
+// Parsed index file, lists in file order (ids ascending per list).
 struct IndexFile {
     QBlock pq;
     uint32_t c = 0;
-    const float* coarse = nullptr;
+    std::vector<float> coarse;
     std::vector<uint64_t> offsets;  // c + 1
     std::vector<uint32_t> ids;      // list order
     std::vector<uint8_t> codes;     // list order
-    RBlock rb;
+    bool refine = false;
+    QBlock rq;
+    std::vector<uint8_t> rcodes;    // list order
     uint64_t n = 0;
 };
+
+// Optional refinement section: refine quantizer block, m' u32, n*m' bytes in
+// ascending id order, scattered to list order as it streams in.
+void get_rblock(Reader& r, IndexFile& f, bool id_is_pos) {
+    if (r.left() == 0) return;
+    f.refine = true;
+    f.rq = get_qblock(r);
+    if (f.rq.d != f.pq.d || f.rq.ks > 256) throw Corrupt();
+    const uint32_t mp = f.rq.m;
+    if (r.pod<uint32_t>() != mp) throw Corrupt();
+    if (f.n * mp > r.left()) throw Corrupt();
+    f.rcodes.resize(f.n * mp);
+    if (id_is_pos) {
+        r.read(f.rcodes.data(), f.rcodes.size());
+        return;
+    }
+    const std::vector<uint32_t> pbr = pos_by_rank(f.ids);
+    constexpr size_t CH = 1 << 16;
+    std::vector<uint8_t> buf(CH * mp);
+    for (uint64_t k0 = 0; k0 < f.n; k0 += CH) {
+        const size_t nk = (size_t)std::min<uint64_t>(CH, f.n - k0);
+        r.read(buf.data(), nk * mp);
+        for (size_t k = 0; k < nk; ++k)
+            std::memcpy(&f.rcodes[(size_t)pbr[k0 + k] * mp], &buf[k * mp], mp);
+    }
+}
 
 void parse_adc(Reader& r, IndexFile& f) {
     f.pq = get_qblock(r);
     if (f.pq.ks > 256) throw Corrupt();
     f.n = r.pod<uint64_t>();
     if (f.n > 0xffffffffull || f.n * f.pq.m > r.left()) throw Corrupt();
-    const uint8_t* codes = r.take((size_t)(f.n * f.pq.m));
+    f.codes.resize(f.n * f.pq.m);
+    r.read(f.codes.data(), f.codes.size());
     f.c = 1;
+    f.coarse.assign(f.pq.d, 0.f);
     f.offsets = {0, f.n};
     f.ids.resize(f.n);
     for (uint64_t i = 0; i < f.n; ++i) f.ids[i] = (uint32_t)i;
-    f.codes.assign(codes, codes + f.n * f.pq.m);
-    f.rb = get_rblock(r, f.n, f.pq.d);
+    get_rblock(r, f, true);
     r.end();
 }
 
@@ -188,7 +246,8 @@ void parse_ivf(Reader& r, IndexFile& f) {
     if (f.pq.ks > 256) throw Corrupt();
     f.c = r.pod<uint32_t>();
     if (f.c == 0 || (uint64_t)f.c * f.pq.d * 4 > r.left()) throw Corrupt();
-    f.coarse = reinterpret_cast<const float*>(r.take((size_t)f.c * f.pq.d * 4));
+    f.coarse.resize((size_t)f.c * f.pq.d);
+    r.read(f.coarse.data(), f.coarse.size() * 4);
     if ((uint64_t)f.c * 8 > r.left()) throw Corrupt();
     f.offsets.assign(f.c + 1, 0);
     for (uint32_t l = 0; l < f.c; ++l) {
@@ -197,19 +256,25 @@ void parse_ivf(Reader& r, IndexFile& f) {
         f.offsets[l + 1] = f.offsets[l] + len;
     }
     f.n = f.offsets[f.c];
-    const size_t rec = 4 + f.pq.m;
+    const uint32_t m = f.pq.m;
+    const size_t rec = 4 + m;
     if (f.n > 0xffffffffull || f.n * rec > r.left()) throw Corrupt();
     f.ids.resize(f.n);
-    f.codes.resize(f.n * f.pq.m);
-    for (uint64_t i = 0; i < f.n; ++i) {
-        const uint8_t* e = r.take(rec);
-        std::memcpy(&f.ids[i], e, 4);
-        std::memcpy(&f.codes[i * f.pq.m], e + 4, f.pq.m);
+    f.codes.resize(f.n * m);
+    constexpr size_t CH = 1 << 16;
+    std::vector<uint8_t> buf(CH * rec);
+    for (uint64_t i0 = 0; i0 < f.n; i0 += CH) {
+        const size_t ni = (size_t)std::min<uint64_t>(CH, f.n - i0);
+        r.read(buf.data(), ni * rec);
+        for (size_t i = 0; i < ni; ++i) {
+            std::memcpy(&f.ids[i0 + i], &buf[i * rec], 4);
+            std::memcpy(&f.codes[(i0 + i) * m], &buf[i * rec + 4], m);
+        }
     }
     for (uint32_t l = 0; l < f.c; ++l)
         for (uint64_t i = f.offsets[l] + 1; i < f.offsets[l + 1]; ++i)
             if (f.ids[i] <= f.ids[i - 1]) throw Corrupt();  // ids ascending per list
-    f.rb = get_rblock(r, f.n, f.pq.d);
+    get_rblock(r, f, false);
     r.end();
 }
 
@@ -240,46 +305,30 @@ Exported export_index(pqrr_dev_index* ix) {
     return e;
 }
 
-// refinement codes of all entries in ascending id order (id-aligned when the
-// ids are 0..n-1, refine.hpp:21-28)
-std::vector<uint8_t> rcodes_by_id(const Exported& e) {
+// refinement section: codes of all entries in ascending id order (id-aligned
+// when the ids are 0..n-1, refine.hpp:21-28), streamed in chunks
+void put_rblock(Writer& w, const Exported& e, bool id_is_pos) {
     const uint32_t mp = e.info.mprime;
-    std::vector<uint64_t> ord(e.ids.size());
-    for (size_t i = 0; i < ord.size(); ++i) ord[i] = ((uint64_t)e.ids[i] << 32) | i;
-    std::sort(ord.begin(), ord.end());
-    std::vector<uint8_t> out(e.ids.size() * mp);
-    for (size_t k = 0; k < ord.size(); ++k)
-        std::memcpy(&out[k * mp], &e.rcodes[(ord[k] & 0xffffffffu) * mp], mp);
-    return out;
-}
-
-void put_rblock(Writer& w, const Exported& e) {
-    if (!e.info.mprime) return;
-    put_qblock(w, e.info.d, e.info.mprime, e.info.ks, e.rbooks.data());
-    w.pod<uint32_t>(e.info.mprime);
-    const auto rc = rcodes_by_id(e);
-    w.put(rc.data(), rc.size());
-}
-
-// list-order refinement codes from the id-ordered file section
-std::vector<uint8_t> rcodes_list_order(const IndexFile& f) {
-    const uint32_t mp = f.rb.q.m;
-    std::vector<uint64_t> ord(f.ids.size());
-    for (size_t i = 0; i < ord.size(); ++i) ord[i] = ((uint64_t)f.ids[i] << 32) | i;
-    std::sort(ord.begin(), ord.end());
-    std::vector<uint8_t> out(f.ids.size() * mp);
-    for (size_t k = 0; k < ord.size(); ++k) {
-        if (k && (ord[k] >> 32) == (ord[k - 1] >> 32)) throw Corrupt();  // duplicate id
-        std::memcpy(&out[(ord[k] & 0xffffffffu) * mp], f.rb.codes + k * mp, mp);
+    if (!mp) return;
+    put_qblock(w, e.info.d, mp, e.info.ks, e.rbooks.data());
+    w.pod<uint32_t>(mp);
+    if (id_is_pos) {
+        w.put(e.rcodes.data(), e.rcodes.size());
+        return;
     }
-    return out;
+    const std::vector<uint32_t> pbr = pos_by_rank(e.ids);
+    constexpr size_t CH = 1 << 16;
+    std::vector<uint8_t> buf(CH * mp);
+    for (size_t k0 = 0; k0 < pbr.size(); k0 += CH) {
+        const size_t nk = std::min(CH, pbr.size() - k0);
+        for (size_t k = 0; k < nk; ++k) std::memcpy(&buf[k * mp], &e.rcodes[(size_t)pbr[k0 + k] * mp], mp);
+        w.put(buf.data(), nk * mp);
+    }
 }
 
 void load_into(pqrr_dev_index* ix, const IndexFile& f) {
-    std::vector<uint8_t> rc;
-    if (f.rb.present) rc = rcodes_list_order(f);
     ck(pqrr_dev_load_lists(ix, f.offsets.data(), f.ids.data(), f.codes.data(),
-                           f.rb.present ? rc.data() : nullptr));
+                           f.refine ? f.rcodes.data() : nullptr));
 }
 
 }  // namespace
@@ -293,9 +342,9 @@ int pqrr_dev_save_quantizer(const char* path, uint32_t d, uint32_t m, uint32_t k
                             const float* books) {
     return run([&] {
         if (m == 0 || d % m) throw ArgError("dimension not divisible");
-        Writer w;
+        Writer w(path);
         put_qblock(w, d, m, ks, books);
-        w.flush(path);
+        w.close();
     });
 }
 
@@ -308,7 +357,7 @@ int pqrr_dev_load_quantizer(const char* path, uint32_t* d, uint32_t* m, uint32_t
         *d = q.d;
         *m = q.m;
         *ks = q.ks;
-        if (books) std::memcpy(books, q.books, (size_t)q.ks * q.d * 4);
+        if (books) std::memcpy(books, q.books.data(), q.books.size() * 4);
     });
 }
 
@@ -316,17 +365,24 @@ int pqrr_dev_save_index(pqrr_dev_index* ix, const char* path) {
     return run([&] {
         Exported e = export_index(ix);
         const auto& in = e.info;
-        Writer w;
+        Writer w(path);
         put_qblock(w, in.d, in.m, in.ks, e.books.data());
         w.pod<uint32_t>(in.c);
         w.put(e.coarse.data(), e.coarse.size() * 4);
         for (uint32_t l = 0; l < in.c; ++l) w.pod<uint64_t>(e.offsets[l + 1] - e.offsets[l]);
-        for (uint64_t i = 0; i < in.n; ++i) {
-            w.pod<uint32_t>(e.ids[i]);
-            w.put(&e.codes[i * in.m], in.m);
+        const size_t rec = 4 + in.m;
+        constexpr size_t CH = 1 << 16;
+        std::vector<uint8_t> buf(CH * rec);
+        for (uint64_t i0 = 0; i0 < in.n; i0 += CH) {
+            const size_t ni = (size_t)std::min<uint64_t>(CH, in.n - i0);
+            for (size_t i = 0; i < ni; ++i) {
+                std::memcpy(&buf[i * rec], &e.ids[i0 + i], 4);
+                std::memcpy(&buf[i * rec + 4], &e.codes[(i0 + i) * in.m], in.m);
+            }
+            w.put(buf.data(), ni * rec);
         }
-        put_rblock(w, e);
-        w.flush(path);
+        put_rblock(w, e, false);
+        w.close();
     });
 }
 
@@ -339,12 +395,12 @@ int pqrr_dev_save_adc_index(pqrr_dev_index* ix, const char* path) {
             if (v != 0.f) throw ArgError("not an ADC index (non-zero coarse centroid)");
         for (uint64_t i = 0; i < in.n; ++i)
             if (e.ids[i] != i) throw ArgError("ADC files hold ids 0..n-1");
-        Writer w;
+        Writer w(path);
         put_qblock(w, in.d, in.m, in.ks, e.books.data());
         w.pod<uint64_t>(in.n);
         w.put(e.codes.data(), e.codes.size());
-        put_rblock(w, e);
-        w.flush(path);
+        put_rblock(w, e, true);
+        w.close();
     });
 }
 
@@ -354,15 +410,12 @@ int pqrr_dev_load_index(int device, const char* path, pqrr_dev_index** out) {
         Reader r(path);
         IndexFile f;
         parse_ivf(r, f);
+        if (f.refine && f.rq.ks != f.pq.ks) throw Corrupt();
         pqrr_dev_index* ix = nullptr;
-        std::vector<float> books = f.pq.copy(), rb = f.rb.present ? f.rb.q.copy() : std::vector<float>();
-        std::vector<float> coarse((size_t)f.c * f.pq.d);
-        std::memcpy(coarse.data(), f.coarse, coarse.size() * 4);
-        ck(pqrr_dev_index_create(device, f.pq.d, f.c, coarse.data(), f.pq.m, books.data(),
-                                 f.rb.present ? f.rb.q.m : 0, f.rb.present ? rb.data() : nullptr,
+        ck(pqrr_dev_index_create(device, f.pq.d, f.c, f.coarse.data(), f.pq.m, f.pq.books.data(),
+                                 f.refine ? f.rq.m : 0, f.refine ? f.rq.books.data() : nullptr,
                                  f.pq.ks, &ix));
         std::unique_ptr<pqrr_dev_index, int (*)(pqrr_dev_index*)> g(ix, pqrr_dev_index_destroy);
-        if (f.rb.present && f.rb.q.ks != f.pq.ks) throw Corrupt();
         load_into(ix, f);
         *out = g.release();
     });
@@ -374,11 +427,10 @@ int pqrr_dev_load_adc_index(int device, const char* path, pqrr_dev_index** out) 
         Reader r(path);
         IndexFile f;
         parse_adc(r, f);
-        if (f.rb.present && f.rb.q.ks != f.pq.ks) throw Corrupt();
+        if (f.refine && f.rq.ks != f.pq.ks) throw Corrupt();
         pqrr_dev_index* ix = nullptr;
-        std::vector<float> books = f.pq.copy(), rb = f.rb.present ? f.rb.q.copy() : std::vector<float>();
-        ck(pqrr_dev_adc_index_create(device, f.pq.d, f.pq.m, books.data(),
-                                     f.rb.present ? f.rb.q.m : 0, f.rb.present ? rb.data() : nullptr,
+        ck(pqrr_dev_adc_index_create(device, f.pq.d, f.pq.m, f.pq.books.data(),
+                                     f.refine ? f.rq.m : 0, f.refine ? f.rq.books.data() : nullptr,
                                      f.pq.ks, &ix));
         std::unique_ptr<pqrr_dev_index, int (*)(pqrr_dev_index*)> g(ix, pqrr_dev_index_destroy);
         load_into(ix, f);
@@ -396,7 +448,7 @@ int pqrr_dev_probe_index_kind(const char* path, int* kind) {
             return;
         } catch (const Corrupt&) {
         }
-        r.pos = 0;
+        r.rewind();
         IndexFile g;
         parse_ivf(r, g);  // throws "corrupt file" when neither layout fits
         *kind = PQRR_INDEX_IVF;

@@ -162,9 +162,27 @@ def _check_shortlist(sl_c, k):
         raise ValueError("shortlist too small")  # SPEC.md:256, as one index would
 
 
+def _packed(nq, width, dev):
+    """One rank's search output as ONE buffer, [ids nq x width | dists nq x
+    width | counts nq] 32-bit words, so a merge needs a single all-gather
+    (pqrr_dev_merge_packed_device); returns (buffer, ids, dists, counts) views."""
+    import torch
+
+    buf = torch.empty(2 * nq * width + nq, dtype=torch.int32, device=dev)
+    ids = buf[:nq * width].view(nq, width)
+    dists = buf[nq * width:2 * nq * width].view(torch.float32).view(nq, width)
+    counts = buf[2 * nq * width:]
+    return buf, ids, dists, counts
+
+
 class DeviceShardedSearch:
-    """GPU rank: device-resident queries, NCCL all-gather into one buffer and
-    the K7 merge kernel on the same stream (mode as in the module docstring)."""
+    """GPU rank: device-resident queries; each search writes its rows straight
+    into a packed buffer, ONE NCCL all-gather per merge, and the K7 merge
+    kernel on the same stream (mode as in the module docstring).  The
+    collectives run with `stream` current, so they are ordered after the
+    shard's search whichever stream the caller passes.  Exact mode's
+    "shortlist too small" check reads the shortlist counts back only after
+    the whole batch is enqueued."""
 
     def __init__(self, index, k: int, kprime: int, w: int, group=None, mode: str = "local"):
         import torch
@@ -177,29 +195,45 @@ class DeviceShardedSearch:
         self.world = dist.get_world_size(group)
         self.torch = torch
 
-    def _gather_merge(self, loc_i, loc_d, loc_c, k, stream):
+    def _gather_merge(self, buf, nq, width, k, stream):
         torch = self.torch
-        nq, width = loc_i.shape
-        dev = loc_i.device
-        all_i = torch.empty((self.world, nq, width), dtype=torch.int32, device=dev)
-        all_d = torch.empty((self.world, nq, width), dtype=torch.float32, device=dev)
-        all_c = torch.empty((self.world, nq), dtype=torch.int32, device=dev)
-        self.dist.all_gather_into_tensor(all_i, loc_i, group=self.group)
-        self.dist.all_gather_into_tensor(all_d, loc_d, group=self.group)
-        self.dist.all_gather_into_tensor(all_c, loc_c, group=self.group)
-        return _merge_device(all_i, all_d, all_c, k, stream)
+        dev = buf.device
+        allb = torch.empty((self.world, buf.numel()), dtype=torch.int32, device=dev)
+        with torch.cuda.stream(stream):
+            self.dist.all_gather_into_tensor(allb, buf, group=self.group)
+        out_i = torch.empty((nq, k), dtype=torch.int32, device=dev)
+        out_d = torch.empty((nq, k), dtype=torch.float32, device=dev)
+        out_c = torch.empty(nq, dtype=torch.int32, device=dev)
+        from ._lib import check, lib
+
+        check(lib.pqrr_dev_merge_packed_device(dev.index, allb.data_ptr(), nq, self.world, width, k,
+                                               out_i.data_ptr(), out_d.data_ptr(), out_c.data_ptr(),
+                                               stream.cuda_stream))
+        return out_i, out_d, out_c
 
     def search(self, d_queries, stream=None):
         """d_queries: uint8 CUDA tensor [nq, d] -> (ids, dists, counts) CUDA tensors."""
         stream = stream or self.torch.cuda.current_stream(d_queries.device)
+        nq, dev = d_queries.shape[0], d_queries.device
         if self.mode == "local":
-            loc = _local_search(self.ix, d_queries, self.w, self.kprime, self.k, stream)
-            return self._gather_merge(*loc, self.k, stream)
-        loc = _local_search(self.ix, d_queries, self.w, self.kprime, 0, stream)
-        sl_i, _, sl_c = self._gather_merge(*loc, self.kprime, stream)
-        _check_shortlist(sl_c, self.k)
-        r = _rerank_owned(self.ix, d_queries, sl_i, sl_c, self.k, stream)
-        return self._gather_merge(*r, self.k, stream)
+            buf, i, d, c = _packed(nq, self.k, dev)
+            self.ix.search_device(d_queries.data_ptr(), nq, self.w, self.kprime, self.k, i.data_ptr(),
+                                  d.data_ptr(), c.data_ptr(), stream.cuda_stream)
+            return self._gather_merge(buf, nq, self.k, self.k, stream)
+        buf, i, d, c = _packed(nq, self.kprime, dev)
+        self.ix.search_device(d_queries.data_ptr(), nq, self.w, self.kprime, 0, i.data_ptr(),
+                              d.data_ptr(), c.data_ptr(), stream.cuda_stream)
+        sl_i, _, sl_c = self._gather_merge(buf, nq, self.kprime, self.kprime, stream)
+        buf2, i2, d2, c2 = _packed(nq, self.k, dev)
+        self.ix.rerank_owned_device(d_queries.data_ptr(), nq, sl_i.data_ptr(), sl_c.data_ptr(),
+                                    self.kprime, self.k, i2.data_ptr(), d2.data_ptr(), c2.data_ptr(),
+                                    stream.cuda_stream)
+        out = self._gather_merge(buf2, nq, self.k, self.k, stream)
+        with self.torch.cuda.stream(stream):
+            short = (sl_c.min() < self.k) if sl_c.numel() else None
+        if short is not None and bool(short):
+            raise ValueError("shortlist too small")  # SPEC.md:256, as one index would
+        return out
 
 
 class MultiShardSearch:
