@@ -61,6 +61,13 @@ uint64_t pqrr_dev_launch_count(void);
 int pqrr_dev_assign_batch(int device, const float* points, size_t n, uint32_t dim,
                           const float* centroids, uint32_t k, uint32_t* out_assign,
                           float* out_dist);
+/* assign_batch of u8 rows without distances: the add path's assignment
+ * (ivf_index.hpp:54-56).  d = 128 and k % 128 == 0 run the certified
+ * tensor-core kernel (k_assign_tc.cu: tcgen05 + TMEM + TMA, ambiguous rows
+ * recomputed exactly); other shapes the exact CUDA-core argmin.  Either way
+ * out_assign equals kernels::assign_batch on the widened rows.              */
+int pqrr_dev_assign_u8(int device, const uint8_t* points, size_t n, uint32_t dim,
+                       const float* centroids, uint32_t k, uint32_t* out_assign);
 /* kernels::encode_batch (kernels.hpp:28-29) with pq_encode_into semantics. */
 int pqrr_dev_encode_batch(int device, const float* books, uint32_t d, uint32_t m, uint32_t ks,
                           const float* data, size_t n, uint8_t* out_codes);

@@ -109,6 +109,7 @@ _sig("pqrr_dev_last_search_stats", [_vp, C.POINTER(SearchStats)])
 _sig("pqrr_dev_load_lists", [_vp, _u64p, _u32p, _u8p, _vp])
 _sig("pqrr_dev_merge_topk", [_int, _u32p, _f32p, _u32p, _sz, _u32, _u32, _u32, _u32p, _f32p, _u32p])
 _sig("pqrr_dev_merge_topk_device", [_int, _vp, _vp, _vp, _sz, _u32, _u32, _u32, _vp, _vp, _vp, _vp])
+_sig("pqrr_dev_assign_u8", [_int, _u8p, _sz, _u32, _f32p, _u32, _u32p])
 _sig("pqrr_dev_merge_packed_device", [_int, _vp, _sz, _u32, _u32, _u32, _vp, _vp, _vp, _vp])
 _sig("pqrr_dev_adc_index_create", [_int, _u32, _u32, _f32p, _u32, _vp, _u32, C.POINTER(_vp)])
 _sig("pqrr_dev_refine_train", [_int, _f32p, _u32, _u32, _u32, _f32p, _sz, _u32, _u32, _u64, _f32p])
@@ -133,7 +134,7 @@ _sig("pqrr_dev_reconstruct_codes", [_int, _f32p, _u32, _u32, _f32p, _u32, _u32, 
 # Symbols include/pqrr_dev.h declares (checked by the CPU test suite).
 EXPORTED = [
     "pqrr_dev_last_error", "pqrr_dev_device_count", "pqrr_dev_launch_count",
-    "pqrr_dev_assign_batch", "pqrr_dev_encode_batch", "pqrr_dev_decode_batch",
+    "pqrr_dev_assign_batch", "pqrr_dev_assign_u8", "pqrr_dev_encode_batch", "pqrr_dev_decode_batch",
     "pqrr_dev_build_lut", "pqrr_dev_scan_topk", "pqrr_dev_kmeans_train", "pqrr_dev_pq_train",
     "pqrr_dev_ivf_train", "pqrr_dev_ivf_refine_train", "pqrr_dev_synth",
     "pqrr_dev_index_create", "pqrr_dev_index_destroy", "pqrr_dev_add_u8", "pqrr_dev_add_f32",

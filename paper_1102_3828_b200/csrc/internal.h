@@ -297,6 +297,32 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
                    const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
                    uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s,
                    cudaEvent_t ev_dist_done = nullptr);
+// Add-path coarse assignment on the tensor cores (k_assign_tc.cu): u8 rows,
+// d = 128, nc % 128 == 0; certified equal to launch_argmin's result.
+bool assign_tc_supported(uint32_t d, uint32_t nc);
+struct AssignTc {
+    bool ready = false, usable = false;
+    uint32_t nc = 0;
+    float cmax = 0.f;
+    void* hi = nullptr;
+    void* lo = nullptr;
+    float* cn = nullptr;
+    AssignTc() = default;
+    AssignTc(const AssignTc&) = delete;
+    AssignTc& operator=(const AssignTc&) = delete;
+    ~AssignTc();
+    // one-time split of the centroids (false: keep the exact CUDA-core path)
+    bool prepare(const float* coarse, uint32_t nc, cudaStream_t s);
+    void assign(const uint8_t* y, size_t n, const float* coarse, uint32_t* out, cudaStream_t s);
+};
+// K5a on CTA pairs (k_rerank.cu): refined distance + id of every shortlist
+// entry (rows of `stride`, sl_cnt[q] valid) into rdist / rid.
+bool rerank_pair_supported(uint32_t d, uint32_t m, uint32_t ks, uint32_t mprime);
+void launch_rerank_pair(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_t* sl_cnt,
+                        uint32_t stride, size_t nq, const float* xq, const uint16_t* block_list,
+                        const float* coarse, const uint8_t* codes, const float* books,
+                        const uint8_t* rcodes, const float* rbooks, uint32_t mprime, float* rdist,
+                        uint32_t* rid, cudaStream_t s);
 // Merge per-shard ranked lists into the top-k (K7).  Part p's rows are
 // ids/dists + p * ps (nq x width) and counts + p * cs (nq); ps = cs = 0 means
 // the stacked layout [parts][nq][width] + [parts][nq].

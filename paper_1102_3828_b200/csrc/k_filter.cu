@@ -417,7 +417,7 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
     uint32_t* __restrict__ counter, const u64 nz, uint32_t* __restrict__ cand_mm) {
     constexpr int CH = DSUB / 4;  // 16-byte chunks per subspace row
     extern __shared__ float4 smem_k[];
-    float4* bk = smem_k;                      // [M][KS][CH], swizzled
+    float4* bk = smem_k;                      // [KS][M][CH]: code-major, chunks rotated
     float4* res = smem_k + M * KS * CH;       // [w][d / 4], swizzled
     __shared__ uint32_t s_q, s_le, s_mn, s_mx;
     // per-warp exchange of the 8 sub-space terms of 4 x 4 candidates:
@@ -428,11 +428,17 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
     const uint32_t dch = d / 4;
     // swizzled chunk index within a row of subspace j (CH chunks per subspace)
     auto sw = [](uint32_t c) { return CH >= 4 ? (c ^ ((c >> 3) & 3)) : c; };
+    // Code-major book: row `code` holds all M sub-spaces' centroids for that
+    // code (the candidate's 8 lanes read 8 different rows), and sub-space j's
+    // chunk p sits at chunk (p + j / 2) mod CH of its slot, so at any p the 8
+    // lanes of a quarter warp land in 8 distinct 16-byte bank groups whatever
+    // the codes: 4 (j & 1) + ((p + j / 2) & 3).
+    auto bslot = [](uint32_t code, uint32_t jj, uint32_t p) {
+        return code * (M * CH) + jj * CH + ((p + (jj >> 1)) & (CH - 1));
+    };
     for (uint32_t i = threadIdx.x; i < (uint32_t)(M * KS * CH); i += blockDim.x) {
-        const uint32_t row = i / CH, c = i % CH;  // row = j * KS + code
-        const uint32_t jj = row / KS;
-        const uint32_t lc = jj * CH + c;  // logical chunk within a d-row
-        bk[row * CH + (sw(lc) - jj * CH)] = reinterpret_cast<const float4*>(books)[i];
+        const uint32_t row = i / CH, p = i % CH;  // row = j * KS + code
+        bk[bslot(row % KS, row / KS, p)] = reinterpret_cast<const float4*>(books)[i];
     }
     for (;;) {
         __syncthreads();  // previous query done (and books staged)
@@ -483,8 +489,8 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
             }
         };
         // 16-byte loads: a quarter-warp is one candidate's 8 sub-spaces, so the
-        // swizzled residual chunks sit in 8 distinct bank groups and the
-        // code-book rows collide only by row parity
+        // swizzled residual chunks and the code-major book rows (bslot) sit in
+        // 8 distinct bank groups
         const ulonglong2* res128 = reinterpret_cast<const ulonglong2*>(res);
         const ulonglong2* bk128 = reinterpret_cast<const ulonglong2*>(bk);
         u64 xa[CH], xb[CH];  // residual chunk halves (t, t+1) / (t+2, t+3)
@@ -528,11 +534,10 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
                     }
                 }
                 const uint32_t c = (uint32_t)(code[u] >> (8 * j)) & 0xffu;
-                const ulonglong2* brow = bk128 + (size_t)(j * KS + c) * CH;
                 u64 sa = 0, sb = 0;
 #pragma unroll
                 for (int p = 0; p < CH; ++p) {
-                    const ulonglong2 bv = brow[sw(j * CH + p) - j * CH];
+                    const ulonglong2 bv = bk128[bslot(c, j, p)];
                     if (p == 0) {  // 0 + x == x for the rounded square x >= +0
                         sa = sq2(sub2(xa[p], bv.x), nz);
                         sb = sq2(sub2(xb[p], bv.y), nz);

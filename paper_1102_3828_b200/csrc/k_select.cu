@@ -522,201 +522,6 @@ __global__ __launch_bounds__(256, 3) void rerank_kernel(
     if (threadIdx.x == 0) out_cnt[q] = cnt;
 }
 
-// K5a (cooperative, d = 128, m = 8, ks = 256): refined distances of every
-// shortlist entry.  Persistent CTAs keep the PQ code book (128 KiB) in shared
-// memory; a warp takes 32 candidates of one query at a time.  Lane g owns
-// dims 4g..4g+3: the coarse row (512 B) and refinement rows are read as
-// coalesced segments, the code-book row from shared memory, and
-//   yhat = (C_l + B(code)) + R(rcode),  sq = (x - yhat)^2
-// goes to a padded 8-candidate tile.  Lanes (candidate, k) then sum
-// sq[4g + k] for g = 0..31 sequentially — the reference 4-accumulator order of
-// l2_sq (distance.hpp:16-33) — and (s0 + s1) + (s2 + s3) is formed by
-// shuffles.  Metadata (position, id, list, code bytes) of the 32 candidates is
-// loaded by all lanes at once so its dependent latency is paid once per 32.
-constexpr int RC_WARPS = 16;
-constexpr int RC_TLD = 132;  // tile row stride (floats): conflict-free transposed reads
-
-// RB_SMEM: the refinement code book (m' rows of d/m' floats per candidate)
-// is the shared-memory table and the PQ code book is read through L1 — for
-// m' >= 16 the refinement rows are the smaller, more numerous segments (m' = 32:
-// 32 separate 16-B rows per candidate), so keeping them on-chip saves the most
-// L1 wavefronts.
-template <int DSR>
-__global__ __launch_bounds__(RC_WARPS * 32, 1) void rerank_coop_kernel(
-    const u64* __restrict__ sl_key, const uint32_t* __restrict__ sl_pos,
-    const uint32_t* __restrict__ sl_cnt, uint32_t stride, size_t nq, const float* __restrict__ xq,
-    const uint16_t* __restrict__ block_list, const float* __restrict__ coarse,
-    const uint8_t* __restrict__ codes, const float* __restrict__ books,
-    const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks,
-    float* __restrict__ rdist, uint32_t* __restrict__ rid) {
-    constexpr int D = 128, MP = D / DSR;  // m' = D / DSR
-    constexpr bool RB_SMEM = true;
-    constexpr int META = 32 + 64 + 8 * MP;  // words per warp: list[32], code[32] u64, rcode[32][MP] B
-    extern __shared__ float4 rc_smem[];
-    float4* bk = rc_smem;                                            // [8][256][4] float4
-    float* tiles = reinterpret_cast<float*>(rc_smem + 8 * 256 * 4);  // [warps][8][RC_TLD]
-    uint32_t* meta = reinterpret_cast<uint32_t*>(tiles + RC_WARPS * 8 * RC_TLD);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* m_list = meta + warp * META;
-    u64* m_code = reinterpret_cast<u64*>(m_list + 32);
-    uint8_t* m_rcode = reinterpret_cast<uint8_t*>(m_list + 32 + 64);
-    float* tile = tiles + warp * 8 * RC_TLD;
-    for (uint32_t i = threadIdx.x; i < 8 * 256 * 4; i += blockDim.x)
-        bk[i] = __ldg(reinterpret_cast<const float4*>(RB_SMEM ? rbooks : books) + i);
-    __syncthreads();
-
-    const uint32_t g = lane;
-    const uint32_t jj = g / 4, bo = g % 4;                  // book row part (float4 index)
-    const uint32_t jr = (4 * g) / DSR, ro = (4 * g) % DSR;  // refinement row, float offset
-    const uint32_t cpq = (stride + 31) / 32;
-    const size_t total = nq * (size_t)cpq;
-    const size_t tw = (size_t)gridDim.x * RC_WARPS;
-    // chunk metadata (id, list, code, refinement code) is prefetched into
-    // registers one chunk ahead: its dependent gather chain (position ->
-    // block list / codes / refinement codes) overlaps the current chunk
-    constexpr int RCV = MP % 16 == 0 ? MP / 16 : 1;
-    auto next_valid = [&](size_t c) -> size_t {
-        for (; c < total; c += tw)
-            if ((uint32_t)(c % cpq) * 32 < sl_cnt[c / cpq]) break;
-        return c;
-    };
-    uint32_t p_id = 0, p_list = 0;
-    u64 p_code = 0;
-    uint4 p_rc[RCV];
-    auto prefetch = [&](size_t c) {
-        const size_t q = c / cpq;
-        const uint32_t i0 = (uint32_t)(c % cpq) * 32;
-        const uint32_t nb = min(32u, sl_cnt[q] - i0);
-        const size_t t0 = q * stride + i0;
-        if ((uint32_t)lane < nb) {
-            const uint32_t pos = sl_pos[t0 + lane];
-            p_id = key_id(sl_key[t0 + lane]);
-            p_list = block_list[pos >> 4];
-            p_code = *reinterpret_cast<const u64*>(codes + (size_t)pos * 8);
-            if constexpr (MP % 16 == 0) {
-                const uint4* rsrc = reinterpret_cast<const uint4*>(rcodes + (size_t)pos * MP);
-#pragma unroll
-                for (int v = 0; v < RCV; ++v) p_rc[v] = rsrc[v];
-            } else {
-                const u64 r = *reinterpret_cast<const u64*>(rcodes + (size_t)pos * MP);
-                p_rc[0] = make_uint4((uint32_t)r, (uint32_t)(r >> 32), 0u, 0u);
-            }
-        }
-    };
-    size_t nch = next_valid((size_t)blockIdx.x * RC_WARPS + warp);
-    if (nch < total) prefetch(nch);
-    for (size_t ch = nch; ch < total; ch = nch) {
-        const size_t q = ch / cpq;
-        const uint32_t i0 = (uint32_t)(ch % cpq) * 32;
-        const uint32_t n = sl_cnt[q];
-        const uint32_t nb = min(32u, n - i0);
-        const size_t t0 = q * stride + i0;
-        __syncwarp();  // the previous chunk's metadata reads are done
-        if ((uint32_t)lane < nb) rid[t0 + lane] = p_id;
-        {
-            // slots past nb repeat the last candidate, so the sub-batch loop
-            // reads 8 valid entries without clamping (duplicates are not stored)
-            const int src = min(lane, (int)nb - 1);
-            const uint32_t pl = __shfl_sync(0xffffffffu, p_list, src);
-            const u64 pc = ((u64)__shfl_sync(0xffffffffu, (uint32_t)(p_code >> 32), src) << 32) |
-                           __shfl_sync(0xffffffffu, (uint32_t)p_code, src);
-            m_list[lane] = pl;
-            m_code[lane] = pc;
-            uint4 rc[RCV];
-#pragma unroll
-            for (int v = 0; v < RCV; ++v)
-                rc[v] = make_uint4(__shfl_sync(0xffffffffu, p_rc[v].x, src), __shfl_sync(0xffffffffu, p_rc[v].y, src),
-                                   __shfl_sync(0xffffffffu, p_rc[v].z, src), __shfl_sync(0xffffffffu, p_rc[v].w, src));
-            if constexpr (MP % 16 == 0) {
-#pragma unroll
-                for (int v = 0; v < RCV; ++v) reinterpret_cast<uint4*>(m_rcode + lane * MP)[v] = rc[v];
-            } else {
-                *reinterpret_cast<u64*>(m_rcode + lane * MP) = ((u64)rc[0].y << 32) | rc[0].x;
-            }
-        }
-        nch = next_valid(ch + tw);
-        if (nch < total) prefetch(nch);
-        const float4 x = reinterpret_cast<const float4*>(xq + q * D)[g];
-        __syncwarp();
-        // shortlists arrive grouped by inverted list (the filter emits per
-        // (query, list) and the selections keep index order): the coarse row
-        // stays in registers until the list changes (warp-uniform branch)
-        uint32_t cur_l = 0xffffffffu;
-        float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
-        // the L1 / L2 gathers (the code-book rows not held in shared memory)
-        // of a sub-batch of 8 candidates are issued one sub-batch ahead, so
-        // their latency overlaps the previous sub-batch's sequential sums
-        // 8 candidates' codes with 4 LDS.128 (m_code is 16-byte aligned)
-        auto gload8 = [&](uint32_t sb0, float4* out) {
-            if constexpr (RB_SMEM) {
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const ulonglong2 cc2 = reinterpret_cast<const ulonglong2*>(m_code)[(sb0 >> 1) + h];
-                    const uint32_t c0 = (uint32_t)(cc2.x >> (8 * jj)) & 0xffu;
-                    const uint32_t c1 = (uint32_t)(cc2.y >> (8 * jj)) & 0xffu;
-                    out[2 * h] = __ldg(reinterpret_cast<const float4*>(books + ((size_t)jj * 256 + c0) * 16) + bo);
-                    out[2 * h + 1] = __ldg(reinterpret_cast<const float4*>(books + ((size_t)jj * 256 + c1) * 16) + bo);
-                }
-            } else {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const uint32_t rcode = m_rcode[(sb0 + c) * MP + jr];
-                    out[c] = __ldg(reinterpret_cast<const float4*>(rbooks + ((size_t)jr * 256 + rcode) * DSR + ro));
-                }
-            }
-        };
-        float4 gv[8];
-        gload8(0, gv);
-        for (uint32_t sb = 0; sb < nb; sb += 8) {
-            // the sub-batch's 8 list ids with 2 LDS.128
-            const uint4 lq0 = reinterpret_cast<const uint4*>(m_list)[sb >> 2];
-            const uint4 lq1 = reinterpret_cast<const uint4*>(m_list)[(sb >> 2) + 1];
-            const uint32_t lids[8] = {lq0.x, lq0.y, lq0.z, lq0.w, lq1.x, lq1.y, lq1.z, lq1.w};
-            // runs of one list are long: a sub-batch changes list at most once
-            // in the common case, to the list of its last candidate, whose
-            // coarse row is fetched up front so the change does not stall
-            float4 cvn = cv;
-            if (lids[7] != cur_l) cvn = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)lids[7] * D) + g);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const uint32_t ci = sb + c;
-                const uint32_t l = lids[c];
-                if (l != cur_l) {
-                    cv = l == lids[7] ? cvn : __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + g);
-                    cur_l = l;
-                }
-                float4 bv, rv;
-                if constexpr (RB_SMEM) {
-                    const uint32_t rcode = m_rcode[ci * MP + jr];
-                    bv = gv[c];
-                    rv = bk[((jr * 256 + rcode) * DSR + ro) / 4];
-                } else {
-                    const uint32_t code = (uint32_t)(m_code[ci] >> (8 * jj)) & 0xffu;
-                    bv = bk[(jj * 256 + code) * 4 + bo];
-                    rv = gv[c];
-                }
-                const float d0 = __fsub_rn(x.x, __fadd_rn(__fadd_rn(cv.x, bv.x), rv.x));
-                const float d1 = __fsub_rn(x.y, __fadd_rn(__fadd_rn(cv.y, bv.y), rv.y));
-                const float d2 = __fsub_rn(x.z, __fadd_rn(__fadd_rn(cv.z, bv.z), rv.z));
-                const float d3 = __fsub_rn(x.w, __fadd_rn(__fadd_rn(cv.w, bv.w), rv.w));
-                *reinterpret_cast<float4*>(tile + c * RC_TLD + 4 * g) =
-                    make_float4(__fmul_rn(d0, d0), __fmul_rn(d1, d1), __fmul_rn(d2, d2), __fmul_rn(d3, d3));
-            }
-            if (sb + 8 < nb) gload8(sb + 8, gv);
-            __syncwarp();
-            const int cc = lane >> 2, k = lane & 3;
-            float sacc = 0.f;
-#pragma unroll
-            for (int gg = 0; gg < 32; ++gg) sacc = __fadd_rn(sacc, tile[cc * RC_TLD + 4 * gg + k]);
-            const float s1 = __shfl_down_sync(0xffffffffu, sacc, 1);
-            const float pair = __fadd_rn(sacc, s1);  // lanes k = 0: s0+s1, k = 2: s2+s3
-            const float p23 = __shfl_down_sync(0xffffffffu, pair, 2);
-            const float dist = __fadd_rn(pair, p23);
-            if (k == 0 && sb + cc < nb) rdist[t0 + sb + cc] = dist;
-            __syncwarp();
-        }
-    }
-}
 
 // K5b: top-k of (rdist, rid) rows under (dist, id): radix select on the
 // distance bits (rows streamed from L2), ties at the boundary broken by id,
@@ -935,32 +740,17 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
     while (n2 < sl_stride) n2 <<= 1;
     uint32_t k2 = 1;
     while (k2 < k) k2 <<= 1;
-    const uint32_t dsr = mprime ? d / mprime : 0;
     // every BASELINE shape (d = 128, m = 8, ks = 256, m' in {8, 16, 32}):
-    // cooperative distances + per-query top-k; other shapes: CTA per query
-    const bool coop_ok = d == 128 && m == 8 && ks == 256 && mprime * dsr == d &&
-                         (dsr == 4 || dsr == 8 || dsr == 16) && (size_t)k2 * 8 <= 200 * 1024;
-    if (coop_ok) {
+    // refined distances on CTA pairs (k_rerank.cu) + per-query top-k; other
+    // shapes: CTA per query
+    if (rerank_pair_supported(d, m, ks, mprime) && (size_t)k2 * 8 <= 200 * 1024) {
         const size_t tot = nq * (size_t)sl_stride;
         float* rd = nullptr;
         uint32_t* ri = nullptr;
         PQRR_CUDA(cudaMallocAsync(&rd, tot * sizeof(float), s));
         PQRR_CUDA(cudaMallocAsync(&ri, tot * sizeof(uint32_t), s));
-        const uint32_t mp = d / dsr;
-        const size_t csmem = (size_t)8 * 256 * 16 * sizeof(float) +
-                             (size_t)RC_WARPS * 8 * RC_TLD * sizeof(float) +
-                             (size_t)RC_WARPS * (32 + 64 + 8 * mp) * sizeof(uint32_t);
-        auto go = [&](auto kern) {
-            set_smem((const void*)kern, csmem);
-            kern<<<sm_count(), RC_WARPS * 32, csmem, s>>>(
-                reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, sl_stride, nq, xq, block_list,
-                coarse, codes, books, rcodes, rbooks, rd, ri);
-        };
-        if (dsr == 8) go(rerank_coop_kernel<8>);
-        else if (dsr == 4) go(rerank_coop_kernel<4>);
-        else go(rerank_coop_kernel<16>);
-        PQRR_LAUNCH_CHECK();
-        count_launch();
+        launch_rerank_pair(sl_key, sl_pos, sl_cnt, sl_stride, nq, xq, block_list, coarse, codes, books,
+                           rcodes, rbooks, mprime, rd, ri, s);
         if (ev_dist_done) PQRR_CUDA(cudaEventRecord(ev_dist_done, s));
         if (!launch_rerank_topk_warp(rd, ri, sl_cnt, sl_stride, nq, k, out_ids, out_dists, out_cnt, s)) {
             set_smem((const void*)rerank_topk_kernel, (size_t)k2 * 8);

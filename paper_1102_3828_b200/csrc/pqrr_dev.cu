@@ -364,6 +364,7 @@ struct DevIndex {
     DBuf<uint16_t> block_list;  // list of each 16-entry block of positions
     DBuf<float> cnorm;          // |C_l|^2 (tensor-core K1), cnorm_max their maximum
     float cnorm_max = 0.f;
+    AssignTc atc;               // tensor-core add-path assignment (u8 rows)
     DBuf<uint8_t> q8_cache;     // per LUT-pass item 8-bit LUT (32 KiB) for the K4f filter
     DBuf<float> q8_param;       // per LUT-pass item and query lane: (scale, sum of minima)
     uint64_t next_id = 0;
@@ -439,7 +440,12 @@ void stage_chunk(DevIndex& ix, const float* xf, const uint8_t* xu, size_t n, uin
         x = tmp;
     }
     uint32_t* a = ix.st_assign.p + ix.st_n;
-    launch_argmin(x, n, ix.coarse.p, ix.c, ix.d, a, nullptr, s);
+    // u8 rows: certified tensor-core assignment (k_assign_tc.cu); float rows
+    // (not exact in fp16) keep the exact CUDA-core argmin
+    if (xu && assign_tc_supported(ix.d, ix.c) && ix.atc.prepare(ix.coarse.p, ix.c, s))
+        ix.atc.assign(xu, n, ix.coarse.p, a, s);
+    else
+        launch_argmin(x, n, ix.coarse.p, ix.c, ix.d, a, nullptr, s);
     launch_ivf_encode(x, nullptr, n, ix.d, a, ix.coarse.p, ix.books.p, ix.m, ix.rbooks.p, ix.mprime,
                       ix.ks, ix.st_codes.p + ix.st_n * ix.m,
                       ix.mprime ? ix.st_rcodes.p + ix.st_n * ix.mprime : nullptr, s);
@@ -1333,6 +1339,29 @@ int pqrr_dev_assign_batch(int device, const float* points, size_t n, uint32_t di
         launch_argmin(p, n, c, k, dim, a, dd, se.s);
         se.download(out_assign, a, n);
         if (out_dist) se.download(out_dist, dd, n);
+        se.sync();
+    });
+}
+
+int pqrr_dev_assign_u8(int device, const uint8_t* points, size_t n, uint32_t dim,
+                       const float* centroids, uint32_t k, uint32_t* out_assign) {
+    return guarded([&] {
+        if (k == 0) throw ArgError("k must be positive");
+        if (n == 0) return;
+        Session se(device);
+        Workspace ws(se.s);
+        const uint8_t* p = se.upload(ws, points, n * dim);
+        const float* c = se.upload(ws, centroids, (size_t)k * dim);
+        uint32_t* a = ws.alloc<uint32_t>(n);
+        AssignTc tc;
+        if (assign_tc_supported(dim, k) && tc.prepare(c, k, se.s)) {
+            tc.assign(p, n, c, a, se.s);
+        } else {
+            float* x = ws.alloc<float>(n * dim);
+            launch_widen_u8(p, x, n * dim, se.s);
+            launch_argmin(x, n, c, k, dim, a, nullptr, se.s);
+        }
+        se.download(out_assign, a, n);
         se.sync();
     });
 }

@@ -29,6 +29,17 @@ def assign_batch(points, centroids, device: int = DEFAULT_DEVICE):
     return a, d
 
 
+def assign_u8(points, centroids, device: int = DEFAULT_DEVICE) -> np.ndarray:
+    """The add path's assignment of u8 rows (ivf_index.hpp:54-56): equal to
+    assign_batch's indices; d = 128, k % 128 == 0 run on the tensor cores
+    (certified, pqrr_dev_assign_u8)."""
+    p = np.ascontiguousarray(points, np.uint8)
+    c = _f32(_vectorset(centroids, p.shape[1]))
+    a = np.zeros(p.shape[0], np.uint32)
+    check(lib.pqrr_dev_assign_u8(device, p, p.shape[0], p.shape[1], c, c.shape[0], a))
+    return a
+
+
 def encode_batch(pq: ProductQuantizer, data, device: int = DEFAULT_DEVICE) -> np.ndarray:
     """kernels.hpp:28-29."""
     x = _f32(_vectorset(data, pq.d))

@@ -735,3 +735,47 @@ def test_exact_knn_groundtruth(pq, oracle, mid_instance):
     np.testing.assert_array_equal(gs.ids, full.ids)
     res = [pq.SearchResult(full.ids[i, :10].astype(np.uint32), full.dists[i, :10]) for i in range(len(q))]
     assert pq.recall_at_r(res, full, 1) == 1.0
+
+
+# ------------------------------------------------------------------ round 2: tensor-core add path
+def _near_tie_centroids(rng, rows, k):
+    """Centroids that put many rows inside the certification window: pairs of
+    centroids mirrored about a row (equal distances, or within a few ulps),
+    exact duplicates, and ordinary k-means-like means."""
+    cen = rng.uniform(0, 120, (k, 128)).astype(np.float32)
+    for j in range(0, k // 4, 2):  # mirrored pairs around row j: exact or near ties
+        r = rows[j].astype(np.float32)
+        delta = rng.uniform(-3, 3, 128).astype(np.float32)
+        cen[j] = r + delta
+        cen[j + 1] = r - delta
+        if j % 4 == 2:
+            cen[j + 1] = np.nextafter(cen[j + 1], np.float32(1e9))
+    cen[k // 2] = cen[k // 2 + 1]  # exact duplicate: ties go to the lower index
+    cen[k // 2 + 2:k // 2 + 8] = cen[k // 2 + 2]  # 6 copies: overflow path
+    return cen
+
+
+@pytest.mark.parametrize("k", [128, 1024, 8192])
+def test_assign_u8_tensor_core_equals_reference(pq, reflib, k):
+    """tcgen05 add-path assignment (k_assign_tc.cu) vs the reference's own
+    kernels::assign_batch (kernels.cpp:21-39) on the widened rows."""
+    rng = np.random.default_rng(100 + k)
+    n = 20_000 + 77  # ragged last tile
+    rows = rng.integers(0, 256, (n, 128)).astype(np.uint8)
+    rows[:300] = rows[0]  # repeated rows
+    cen = _near_tie_centroids(rng, rows, k)
+    # rows sitting exactly between the mirrored pairs
+    for j in range(0, k // 4, 2):
+        rows[1000 + j] = np.clip(np.rint((cen[j] + cen[j + 1]) / 2), 0, 255).astype(np.uint8)
+    # rows equal to the duplicated centroids (rounded): many candidates
+    rows[2000:2100] = np.clip(np.rint(cen[k // 2 + 2]), 0, 255).astype(np.uint8)
+    got = pq.kernels.assign_u8(rows, cen)
+    want, _ = reflib.assign(rows.astype(np.float32), cen)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_assign_u8_other_shapes_exact(pq, reflib):
+    rng = np.random.default_rng(5)
+    rows = rng.integers(0, 256, (3000, 64)).astype(np.uint8)
+    cen = rng.uniform(0, 255, (100, 64)).astype(np.float32)
+    np.testing.assert_array_equal(pq.kernels.assign_u8(rows, cen), reflib.assign(rows.astype(np.float32), cen)[0])
