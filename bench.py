@@ -164,7 +164,85 @@ def build_index(pq, cfg, coarse, P, rq, device, shard, nshards):
 
 
 # ---------------------------------------------------------------- reference arm
-REF_SAMPLE = {"C1": 1000, "C2": 1024, "C3": 64, "C4": 32, "C5": 32}
+REF_SAMPLE = {"C1": 1000, "C2": 1024, "C3": 64, "C4": 8, "C5": 8}
+
+
+class FileLists:
+    """export_subset() over the probed lists a setup process wrote to disk
+    (np.load with mmap): the reference arm reads the device-built index
+    without loading any product code."""
+
+    def __init__(self, d):
+        self.d = d
+        self.U = np.load(os.path.join(d, "lists.npy"))
+        self.offs = np.load(os.path.join(d, "offs.npy"))
+        self.ids = np.load(os.path.join(d, "ids.npy"), mmap_mode="r")
+        self.codes = np.load(os.path.join(d, "codes.npy"), mmap_mode="r")
+        rp = os.path.join(d, "rcodes.npy")
+        self.rcodes = np.load(rp, mmap_mode="r") if os.path.exists(rp) else None
+        self.where = {int(l): i for i, l in enumerate(self.U)}
+
+    def __call__(self, lists):
+        idx = [self.where[int(l)] for l in lists]
+        lens = np.array([self.offs[i + 1] - self.offs[i] for i in idx], np.uint64)
+        offs = np.zeros(len(idx) + 1, np.uint64)
+        offs[1:] = np.cumsum(lens)
+        sl = [slice(int(self.offs[i]), int(self.offs[i + 1])) for i in idx]
+        ids = np.concatenate([self.ids[s] for s in sl]) if sl else np.zeros(0, np.uint32)
+        codes = np.concatenate([self.codes[s] for s in sl]) if sl else np.zeros((0, 8), np.uint8)
+        rc = np.concatenate([self.rcodes[s] for s in sl]) if self.rcodes is not None else None
+        return offs, ids, codes, rc
+
+    def nbytes(self):
+        return int(sum(os.path.getsize(os.path.join(self.d, f)) for f in os.listdir(self.d)))
+
+
+def ref_tmpdir(need_bytes):
+    """A scratch directory with room for the exported lists (page cache backed)."""
+    import shutil
+    import tempfile
+
+    for base in (os.environ.get("PQRR_REF_TMP"), "/dev/shm", "/tmp", ROOT):
+        if base and os.path.isdir(base) and os.access(base, os.W_OK):
+            try:
+                if shutil.disk_usage(base).free > 1.2 * need_bytes:
+                    return tempfile.mkdtemp(prefix="pqrr_ref_", dir=base)
+            except OSError:
+                pass
+    raise RuntimeError("no scratch directory with room for the exported lists")
+
+
+def export_reference_input(args, cfg):
+    """Setup process of the reference arm at n > 10M (C3-C5): builds the index
+    on the device (the host cannot: ~1e15 assign operations), exports the lists
+    the reference's sample queries probe (id-ascending, ivf_index.hpp:15-16) and
+    the device codes of a random id sample for the add-path check, to
+    --export-dir.  The timed reference process never loads libpqrr_b200.so."""
+    import paper_1102_3828_b200 as pq
+    from oracle.oracle_py import Oracle
+    from oracle import ref_harness as H
+
+    d = args.export_dir
+    coarse, P, rq = train_codebooks(pq, cfg, 0)
+    ix, _, _, add_s = build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
+    o = Oracle()
+    o.set_threads(0)
+    centers = o.synth_centers(SEED, cfg["clusters"], 128)
+    qs = o.synth_rows(SEED, H.SYNTH_QUERY, 0, args.ref_queries, centers).astype(np.float32)
+    probes, _ = o.coarse_probe(coarse.centroids, qs, cfg["w"])
+    U = np.unique(probes).astype(np.uint32)
+    offs, ids, codes, rc = ix.export_lists_subset(U)
+    for name, arr in (("lists", U), ("offs", offs), ("ids", ids), ("codes", codes), ("rcodes", rc),
+                      ("coarse", coarse.centroids), ("books", P.flat()), ("rbooks", rq.pq.flat())):
+        if arr is not None:
+            np.save(os.path.join(d, name + ".npy"), arr)
+    starts, block = H.sample_ids(cfg["n"], nblocks=64)
+    sid = np.concatenate([np.arange(s, s + block, dtype=np.uint32) for s in starts])
+    dl, dc, drc = ix.lookup_ids(sid)
+    np.savez(os.path.join(d, "add_sample.npz"), starts=starts, block=block, lists=dl, codes=dc,
+             rcodes=drc if drc is not None else np.zeros(0, np.uint8), add_s=add_s)
+    ix.close()
+    log(f"[setup] exported {len(U)} probed lists ({len(ids)} entries) for {args.ref_queries} queries")
 
 
 def run_reference(args, cfg, rank, world):
@@ -172,16 +250,16 @@ def run_reference(args, cfg, rank, world):
     host's cores, on a bounded query sample per step.
 
     n <= 10M (C1, C2): the index is built on the host too (oracle k-means for
-    the codebooks, the reference's assign_batch / encode_batch for the lists):
-    no device code is loaded.  C3-C5 (100M-1B vectors) cannot be built on the
-    host in a bench run (the assignment alone is ~1e15 element operations,
-    hours on 16 cores): the index is built on the device (setup only, untimed,
-    `index_build` says so), the add path is checked on a random id sample
-    against the reference's own encoder, and each step exports the lists its
-    queries probe and times the reference search over them."""
+    the codebooks, the reference's assign_batch / encode_batch for the lists).
+    C3-C5 (100M-1B vectors) cannot be built on the host in a bench run (the
+    assignment alone is ~1e15 element operations): a separate setup process
+    builds it on the device and exports the lists the sample queries probe to
+    scratch files (export_reference_input).  This process reads them and
+    never loads product code; the add path is checked on a random id sample
+    against the reference's own encoder."""
     if rank != 0:
         return
-    from oracle.oracle_py import RefLib, build, ref_available
+    from oracle.oracle_py import Oracle, RefLib, build, ref_available
     from oracle import ref_harness as H
 
     if not ref_available():
@@ -194,12 +272,11 @@ def run_reference(args, cfg, rank, world):
     nq = cfg["nq"]
     extra = {}
     t_setup = time.time()
+    o = Oracle()
+    centers = o.synth_centers(SEED, cfg["clusters"], 128)
     if cfg["n"] <= CPU_BUILD_MAX:
-        from oracle.oracle_py import Oracle
-
         hx = H.cpu_build(cfg, SEED, log)
-        centers = Oracle().synth_centers(SEED, cfg["clusters"], 128)
-        queries = Oracle().synth_rows(SEED, H.SYNTH_QUERY, 0, nq, centers)
+        queries = o.synth_rows(SEED, H.SYNTH_QUERY, 0, nq, centers)
         index_build = "host: oracle k-means + reference assign_batch/encode_batch (no device code)"
 
         def step(i):
@@ -211,40 +288,68 @@ def run_reference(args, cfg, rank, world):
         def one_thread(qs):
             return H.ref_search(ref, hx, qs, cfg["w"], cfg["kprime"], cfg["k"])
     else:
-        import paper_1102_3828_b200 as pq
+        nref = (min(W, 1) + K) * sample
+        per_list = cfg["n"] / cfg["kc"] * (cfg["m"] + cfg["mprime"] + 4)
+        d = ref_tmpdir(min(cfg["kc"], nref * cfg["w"]) * per_list)
+        try:
+            cmd = [sys.executable, os.path.abspath(__file__), "--config", args.config, "--export-dir", d,
+                   "--ref-queries", str(nref)]
+            subprocess.run(cmd, check=True, stdout=sys.stderr)
+            fl = FileLists(d)
+            cb = (np.load(os.path.join(d, "coarse.npy")), np.load(os.path.join(d, "books.npy")),
+                  np.load(os.path.join(d, "rbooks.npy")))
+            queries = o.synth_rows(SEED, H.SYNTH_QUERY, 0, nref, centers)
+            a = np.load(os.path.join(d, "add_sample.npz"))
+            ids, al, ac, arc = H.reencode_sample(cfg, *cb, a["starts"], int(a["block"]), seed=SEED)
+            extra["index_check"] = {
+                "ids": int(len(ids)), "list_match": float(np.mean(a["lists"] == al)),
+                "codes_match": float(np.mean(np.all(a["codes"] == ac, axis=1))),
+                "rcodes_match": float(np.mean(np.all(a["rcodes"] == arc, axis=1))),
+                "sample": f"{len(a['starts'])} random runs of {int(a['block'])} consecutive ids, "
+                          "reference assign/encode on host-generated rows vs the device index"}
+            index_build = (f"device, in a separate setup process (bench.py --export-dir): a host build of "
+                           f"{cfg['n']:.0e} vectors is ~1e15 assign operations; the {len(fl.U)} lists the "
+                           f"{nref} sample queries probe ({fl.nbytes() / 1e9:.1f} GB) exported to scratch "
+                           "files; this process loads no product code")
 
-        coarse, P, rq = train_codebooks(pq, cfg, 0)
-        ix, _, _, _ = build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
-        queries = pq.synth(3, 0, nq, cfg["clusters"], seed=SEED)
-        cb = (coarse.centroids, P.flat(), rq.pq.flat())
-        # the index the reference searches, checked against the reference's
-        # own encoder on random ids (the add path, kernels.cpp:21-46)
-        starts, block = H.sample_ids(cfg["n"], nblocks=64)
-        extra["index_check"] = add_check(H, cfg, ix, cb, starts, block)
-        index_build = ("device (libpqrr_b200.so, setup only, untimed): a host build of "
-                       f"{cfg['n']:.0e} vectors is ~1e15 assign operations; lists exported per step")
+            def step(i):
+                qs = queries[i * sample:(i + 1) * sample]
+                _, _, ts, _ = H.probed_reference(ref, fl, *cb, cfg["m"], cfg["mprime"], cfg["kc"], qs,
+                                                 cfg["w"], cfg["kprime"], cfg["k"], batch=sample)
+                return len(qs), ts
 
-        def step(i):
-            qs = queries[(i * sample) % nq:][:sample]
-            _, _, ts, _ = H.probed_reference(ref, ix.export_lists_subset, *cb, cfg["m"], cfg["mprime"],
-                                             cfg["kc"], qs, cfg["w"], cfg["kprime"], cfg["k"], batch=sample)
-            return len(qs), ts
+            def one_thread(qs):
+                return H.probed_reference(ref, fl, *cb, cfg["m"], cfg["mprime"], cfg["kc"], qs, cfg["w"],
+                                          cfg["kprime"], cfg["k"], batch=len(qs))
+            # all timed steps run before the scratch files go away
+            t_setup = time.time() - t_setup
+            return _reference_line(args, cfg, world, ref, cores, sample, step, one_thread, queries,
+                                   index_build, t_setup, extra)
+        finally:
+            import shutil
 
-        def one_thread(qs):
-            return H.probed_reference(ref, ix.export_lists_subset, *cb, cfg["m"], cfg["mprime"],
-                                      cfg["kc"], qs, cfg["w"], cfg["kprime"], cfg["k"], batch=len(qs))
+            shutil.rmtree(d, ignore_errors=True)
     t_setup = time.time() - t_setup
+    return _reference_line(args, cfg, world, ref, cores, sample, step, one_thread, queries, index_build,
+                           t_setup, extra)
+
+
+def _reference_line(args, cfg, world, ref, cores, sample, step, one_thread, queries, index_build, t_setup,
+                    extra):
+    from oracle import ref_harness as H
+
+    W, K = args.warmup, args.steps
     for i in range(min(W, 1)):
         step(i)
     done, dt = 0, 0.0
     for i in range(K):
-        n_i, t_i = step(i + 1)
+        n_i, t_i = step(i + min(W, 1))
         done += n_i
         dt += t_i
     v = done / dt
     # single-thread time per query (eval.hpp:49,63: BenchRow.time_per_query)
     ref.set_threads(1)
-    n1 = 4
+    n1 = 2 if cfg["n"] > CPU_BUILD_MAX else 4
     t0 = time.perf_counter()
     one_thread(queries[:n1])
     t1q = (time.perf_counter() - t0) / n1
@@ -256,7 +361,7 @@ def run_reference(args, cfg, rank, world):
         "config": {"workload": args.config, **cfg, "parallelism": f"cpu-openmp x{cores}"},
         "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "reference",
                          "cpu_model": H.cpu_model(),
-                         "sample": f"{sample} queries per step (of {nq}), OpenMP over queries",
+                         "sample": f"{sample} queries per step (of {cfg['nq']}), OpenMP over queries",
                          "time_per_query_1thread_s": t1q, "index_build": index_build,
                          "setup_s": round(t_setup, 1)},
         "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -297,11 +402,14 @@ def main():
                     help="full: host-built index + every query (n <= 10M); sample: probed-list "
                          "reference on --ref-queries queries + add-path re-encode sample")
     ap.add_argument("--ref-queries", type=int, default=256)
+    ap.add_argument("--export-dir", default=None, help=argparse.SUPPRESS)  # reference-arm setup process
     ap.add_argument("--shard-mode", default="exact", choices=["local", "exact"],
                     help="N>1: per-shard shortlists (north star) or the single-index-exact flow")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     rank, world, local = dist_env()
+    if args.export_dir:
+        return export_reference_input(args, cfg)
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
     if args.config == "C5":
