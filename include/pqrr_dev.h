@@ -295,6 +295,29 @@ int pqrr_dev_merge_packed_device(int device, const void* packed, size_t nq, uint
                                  uint32_t width, uint32_t k, uint32_t* d_out_ids,
                                  float* d_out_dists, uint32_t* d_out_counts, void* stream);
 
+/* ------------------------------------------------------------------ multi-GPU group
+ * One process driving G id-range shards: shards[r] is an
+ * index handle (any device) holding the ids of shard r over all c lists.
+ * group_search broadcasts the host queries, searches every shard on its own
+ * device, and merges with ONE all-gather per merge of every shard's packed
+ * rows (pqrr_dev_merge_packed_device): NCCL (ncclCommInitAll, ncclAllGather in
+ * a group call) when the shards sit on distinct devices, device copies when
+ * shards share one.  PQRR_GROUP_EXACT (default): global IVFADC top-k', each
+ * shard re-ranks the entries it holds -> bit-identical to one index holding
+ * every id (ivf_search_batch + ivf_rerank); fails with PQRR_ESHORTLIST exactly
+ * when that index would.  PQRR_GROUP_LOCAL: every shard's fused top-k merged
+ * (re-ranks up to G k' candidates).  Outputs as pqrr_dev_search_u8.         */
+typedef struct pqrr_dev_group pqrr_dev_group;
+enum { PQRR_GROUP_EXACT = 0, PQRR_GROUP_LOCAL = 1 };
+int pqrr_dev_index_device(pqrr_dev_index* ix, int* device);
+int pqrr_dev_group_create(uint32_t G, pqrr_dev_index* const* shards, pqrr_dev_group** out);
+int pqrr_dev_group_search_u8(pqrr_dev_group* g, const uint8_t* queries, size_t nq, uint32_t w,
+                             size_t kprime, size_t k, int mode, uint32_t* out_ids,
+                             float* out_dists, uint32_t* out_counts);
+/* shards in the group and whether its all-gathers run on NCCL */
+int pqrr_dev_group_size(pqrr_dev_group* g, uint32_t* shards, int* uses_nccl);
+int pqrr_dev_group_destroy(pqrr_dev_group* g);
+
 /* Per-stage device times (CUDA events on the index stream) of the last search. */
 typedef struct {
     float ms_total, ms_coarse, ms_invert, ms_sample_scan, ms_threshold, ms_scan, ms_select,

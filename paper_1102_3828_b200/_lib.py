@@ -110,6 +110,11 @@ _sig("pqrr_dev_load_lists", [_vp, _u64p, _u32p, _u8p, _vp])
 _sig("pqrr_dev_merge_topk", [_int, _u32p, _f32p, _u32p, _sz, _u32, _u32, _u32, _u32p, _f32p, _u32p])
 _sig("pqrr_dev_merge_topk_device", [_int, _vp, _vp, _vp, _sz, _u32, _u32, _u32, _vp, _vp, _vp, _vp])
 _sig("pqrr_dev_assign_u8", [_int, _u8p, _sz, _u32, _f32p, _u32, _u32p])
+_sig("pqrr_dev_index_device", [_vp, C.POINTER(_int)])
+_sig("pqrr_dev_group_create", [_u32, C.POINTER(_vp), C.POINTER(_vp)])
+_sig("pqrr_dev_group_search_u8", [_vp, _u8p, _sz, _u32, _sz, _sz, _int, _u32p, _f32p, _u32p])
+_sig("pqrr_dev_group_size", [_vp, C.POINTER(_u32), C.POINTER(_int)])
+_sig("pqrr_dev_group_destroy", [_vp])
 _sig("pqrr_dev_merge_packed_device", [_int, _vp, _sz, _u32, _u32, _u32, _vp, _vp, _vp, _vp])
 _sig("pqrr_dev_adc_index_create", [_int, _u32, _u32, _f32p, _u32, _vp, _u32, C.POINTER(_vp)])
 _sig("pqrr_dev_refine_train", [_int, _f32p, _u32, _u32, _u32, _f32p, _sz, _u32, _u32, _u64, _f32p])
@@ -143,6 +148,8 @@ EXPORTED = [
     "pqrr_dev_search_u8_device", "pqrr_dev_rerank_u8", "pqrr_dev_rerank_f32",
     "pqrr_dev_reconstruct", "pqrr_dev_lookup_ids", "pqrr_dev_last_search_stats", "pqrr_dev_load_lists",
     "pqrr_dev_merge_topk", "pqrr_dev_merge_topk_device", "pqrr_dev_merge_packed_device",
+    "pqrr_dev_index_device", "pqrr_dev_group_create", "pqrr_dev_group_search_u8", "pqrr_dev_group_size",
+    "pqrr_dev_group_destroy",
     "pqrr_dev_rerank_owned_u8_device",
     "pqrr_dev_adc_index_create", "pqrr_dev_refine_train", "pqrr_dev_residual",
     "pqrr_dev_reconstruct_codes", "pqrr_dev_export_codebooks", "pqrr_dev_export_lists_subset",

@@ -16,10 +16,10 @@
 // bank group g mod 8, so every book gather is conflict-free whatever the
 // codes.  Both CTAs walk the same chunks (32 candidates of one query); a warp
 // handles 2 candidates per step (half warp each, lane g = one dim quad), the
-// squares go to a padded 8-candidate tile, and lanes (candidate, k) add the 16
+// squares go to a padded 16-candidate tile, and lanes (candidate, k) add the 16
 // terms of s_k of their half in ascending t.  CTA 0's partial sums (16 B per
-// candidate) are stored straight into CTA 1's shared memory (st.shared::cluster)
-// and handed over with a remote mbarrier arrive; CTA 1 continues the same four
+// candidate) are stored straight into CTA 1's shared memory (distributed shared memory)
+// with st.async, which completes CTA 1's mbarrier; CTA 1 continues the same four
 // chains over dims 64..127 — the reference's sequential order across the whole
 // vector — and forms (s0 + s1) + (s2 + s3).  Per-warp full / empty barriers
 // with a 2-slot ring let CTA 0 run a chunk ahead.
@@ -44,8 +44,14 @@ __device__ __forceinline__ unsigned peer_addr(unsigned a, unsigned rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
     return r;
 }
-__device__ __forceinline__ void st_peer(unsigned a, float v) {
-    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+// Asynchronous remote store that completes `bytes` of the peer's mbarrier
+// transaction count (no fence on the producer side).
+__device__ __forceinline__ void st_peer_async(unsigned a, float v, unsigned peer_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(a),
+                 "r"(__float_as_uint(v)), "r"(peer_bar) : "memory");
+}
+__device__ __forceinline__ void expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void arrive_peer(unsigned a) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
@@ -66,7 +72,7 @@ template <int DSR>
 struct RpSmem {
     static constexpr int HB = (128 / DSR) / 2;  // refinement code bytes per half
     static constexpr size_t books = 2 * 256 * 64 * 4;
-    static constexpr size_t tiles = (size_t)RP_WARPS * 8 * RP_TLD * 4;
+    static constexpr size_t tiles = (size_t)RP_WARPS * 16 * RP_TLD * 4;
     static constexpr size_t part = (size_t)RP_WARPS * 2 * 32 * 4 * 4;
     static constexpr size_t mlist = (size_t)RP_WARPS * 32 * 4;
     static constexpr size_t mcode = (size_t)RP_WARPS * 4 * RP_MLD;
@@ -89,7 +95,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
     uint8_t* base = reinterpret_cast<uint8_t*>(rp_smem);
     const float4* bookP = reinterpret_cast<const float4*>(base);            // [256][16] float4
     const float4* bookR = bookP + 256 * 16;                                 // [256][16] float4
-    float* tiles = reinterpret_cast<float*>(base + L::books);                // [warps][8][TLD]
+    float* tiles = reinterpret_cast<float*>(base + L::books);                // [warps][16][TLD]
     float* part = reinterpret_cast<float*>(base + L::books + L::tiles);      // [warps][2][32][4]
     uint32_t* mlist = reinterpret_cast<uint32_t*>(base + L::books + L::tiles + L::part);
     uint8_t* mcode = reinterpret_cast<uint8_t*>(mlist) + L::mlist;         // [warps][4][MLD]
@@ -109,19 +115,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
         }
     }
     if (threadIdx.x < RP_WARPS * 2)
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_addr(bars + threadIdx.x)), "r"(32) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_addr(bars + threadIdx.x)), "r"(1) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     cluster_sync();
 
-    float* tile = tiles + warp * 8 * RP_TLD;
+    float* tile = tiles + warp * 16 * RP_TLD;
     float* wpart = part + warp * 2 * 32 * 4;
     uint32_t* wlist = mlist + warp * 32;
     uint8_t* wcode = mcode + warp * 4 * RP_MLD;
     uint8_t* wrc = mrc + warp * HB * RP_MLD;
     const unsigned bar0 = s_addr(bars + warp * 2);
-    // rank 0 writes partials into, and arrives on, the peer's "full" barriers;
-    // rank 1 arrives on the peer's "empty" barriers
+    // rank 0 writes partials into the peer's shared memory with st.async, each
+    // store completing bytes of the peer's "full" barrier (armed by rank 1 with
+    // the chunk's byte count); rank 1 releases the slot with one arrive on the
+    // peer's "empty" barrier
     const unsigned peer_bar0 = peer_addr(bar0, r ^ 1u);
     const unsigned peer_part = peer_addr(s_addr(wpart), 1u);
 
@@ -137,16 +145,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
             if ((uint32_t)(c % cpq) * 32 < sl_cnt[c / cpq]) break;
         return c;
     };
-    // chunk metadata prefetched one chunk ahead (lane = candidate)
-    uint32_t p_id = 0, p_list = 0, p_code = 0;
+    // chunk metadata, software-pipelined two deep (lane = candidate): the
+    // positions of chunk i + 2 and the position-dependent gathers (list, code
+    // and refinement-code bytes) of chunk i + 1 are in flight while chunk i
+    // computes, so no warp waits on a dependent DRAM round trip
+    uint32_t p_id = 0, p_list = 0, p_code = 0, n_pos = 0;
     uint32_t p_rc[(HB + 3) / 4];
-    auto prefetch = [&](size_t c) {
+    auto rows_of = [&](size_t c, size_t& t0, uint32_t& nb) {
         const size_t q = c / cpq;
         const uint32_t i0 = (uint32_t)(c % cpq) * 32;
-        const uint32_t nb = min(32u, sl_cnt[q] - i0);
-        const size_t t0 = q * stride + i0;
+        nb = min(32u, sl_cnt[q] - i0);
+        t0 = q * stride + i0;
+    };
+    auto load_pos = [&](size_t c) {
+        size_t t0;
+        uint32_t nb;
+        rows_of(c, t0, nb);
+        if ((uint32_t)lane < nb) n_pos = sl_pos[t0 + lane];
+    };
+    auto load_meta = [&](size_t c, uint32_t pos) {
+        size_t t0;
+        uint32_t nb;
+        rows_of(c, t0, nb);
         if ((uint32_t)lane < nb) {
-            const uint32_t pos = sl_pos[t0 + lane];
             if (r) p_id = key_id(sl_key[t0 + lane]);
             p_list = block_list[pos >> 4];
             p_code = *reinterpret_cast<const uint32_t*>(codes + (size_t)pos * 8 + 4 * r);
@@ -163,7 +184,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
         }
     };
     size_t nch = next_valid((size_t)(blockIdx.x >> 1) * RP_WARPS + warp);
-    if (nch < total) prefetch(nch);
+    size_t nch2 = nch < total ? next_valid(nch + tw) : total;
+    if (nch < total) {
+        load_pos(nch);
+        load_meta(nch, n_pos);
+    }
+    if (nch2 < total) load_pos(nch2);
     uint32_t it = 0;
     for (size_t ch = nch; ch < total; ch = nch, ++it) {
         const size_t q = ch / cpq;
@@ -188,63 +214,86 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
             }
             if (r && (uint32_t)lane < nb) rid[t0 + lane] = p_id;
         }
-        nch = next_valid(ch + tw);
-        if (nch < total) prefetch(nch);
+        nch = nch2;
+        if (nch < total) {
+            load_meta(nch, n_pos);
+            nch2 = next_valid(nch + tw);
+            if (nch2 < total) load_pos(nch2);
+        }
         const float4 x = __ldg(reinterpret_cast<const float4*>(xq + q * 128 + 64 * r) + g);
         const u64 x01 = pk2(x.x, x.y), x23 = pk2(x.z, x.w);
         if (r == 0 && use > 0) wait_parity(bar0 + 8 * slot, (use - 1) & 1u);  // peer done with the slot
+        if (r == 1 && lane == 0) expect_tx(bar0 + 8 * slot, 256u * ((nb + 15) / 16));  // partials to come
         __syncwarp();
         uint32_t cur_l = 0xffffffffu;
         float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (uint32_t sb = 0; sb < nb; sb += 8) {
-            const uint4 lq0 = reinterpret_cast<const uint4*>(wlist)[sb >> 2];
-            const uint4 lq1 = reinterpret_cast<const uint4*>(wlist)[(sb >> 2) + 1];
-            const uint32_t la[4] = {h ? lq0.y : lq0.x, h ? lq0.w : lq0.z, h ? lq1.y : lq1.x, h ? lq1.w : lq1.z};
-            const u64 cb = *reinterpret_cast<const u64*>(wcode + jl * RP_MLD + sb);
-            const u64 rb = *reinterpret_cast<const u64*>(wrc + jrl * RP_MLD + sb);
-            float4 bv[4], rv[4];
+        // sub-batches of 16 candidates: squares of 8 steps (2 candidates per
+        // step), then every summing lane runs TWO independent chains
+        // (candidates cc and cc + 8) interleaved
+        for (uint32_t sb = 0; sb < nb; sb += 16) {
 #pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                const uint32_t c = 2 * s + h;
-                bv[s] = bookP[((uint32_t)(cb >> (8 * c)) & 0xffu) * 16 + g];
-                rv[s] = bookR[((uint32_t)(rb >> (8 * c)) & 0xffu) * 16 + g];
-            }
+            for (int half = 0; half < 2; ++half) {
+                const uint32_t s0 = sb + 8 * half;
+                const uint4 lq0 = reinterpret_cast<const uint4*>(wlist)[s0 >> 2];
+                const uint4 lq1 = reinterpret_cast<const uint4*>(wlist)[(s0 >> 2) + 1];
+                const uint32_t la[4] = {h ? lq0.y : lq0.x, h ? lq0.w : lq0.z, h ? lq1.y : lq1.x, h ? lq1.w : lq1.z};
+                const u64 cb = *reinterpret_cast<const u64*>(wcode + jl * RP_MLD + s0);
+                const u64 rb = *reinterpret_cast<const u64*>(wrc + jrl * RP_MLD + s0);
+                float4 bv[4], rv[4];
 #pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                if (la[s] != cur_l) {  // candidates arrive grouped by list: rare
-                    cur_l = la[s];
-                    cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)cur_l * 128 + 64 * r) + g);
+                for (int st = 0; st < 4; ++st) {
+                    const uint32_t c = 2 * st + h;
+                    bv[st] = bookP[((uint32_t)(cb >> (8 * c)) & 0xffu) * 16 + g];
+                    rv[st] = bookR[((uint32_t)(rb >> (8 * c)) & 0xffu) * 16 + g];
                 }
-                const u64 y01 = add2(add2(pk2(cv.x, cv.y), pk2(bv[s].x, bv[s].y)), pk2(rv[s].x, rv[s].y));
-                const u64 y23 = add2(add2(pk2(cv.z, cv.w), pk2(bv[s].z, bv[s].w)), pk2(rv[s].z, rv[s].w));
-                const u64 q01 = sq2(sub2(x01, y01), nz), q23 = sq2(sub2(x23, y23), nz);
-                *reinterpret_cast<float4*>(tile + (2 * s + h) * RP_TLD + 4 * g) =
-                    make_float4(lo2(q01), hi2(q01), lo2(q23), hi2(q23));
+#pragma unroll
+                for (int st = 0; st < 4; ++st) {
+                    if (la[st] != cur_l) {  // candidates arrive grouped by list: rare
+                        cur_l = la[st];
+                        cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)cur_l * 128 + 64 * r) + g);
+                    }
+                    const u64 y01 = add2(add2(pk2(cv.x, cv.y), pk2(bv[st].x, bv[st].y)), pk2(rv[st].x, rv[st].y));
+                    const u64 y23 = add2(add2(pk2(cv.z, cv.w), pk2(bv[st].z, bv[st].w)), pk2(rv[st].z, rv[st].w));
+                    const u64 q01 = sq2(sub2(x01, y01), nz), q23 = sq2(sub2(x23, y23), nz);
+                    *reinterpret_cast<float4*>(tile + (8 * half + 2 * st + h) * RP_TLD + 4 * g) =
+                        make_float4(lo2(q01), hi2(q01), lo2(q23), hi2(q23));
+                }
             }
             __syncwarp();
-            float t[16];
+            float ta[16], tb[16];
 #pragma unroll
-            for (int gg = 0; gg < 16; ++gg) t[gg] = tile[cc * RP_TLD + 4 * gg + kk];
-            float sacc = 0.f;  // l2_sq's accumulators start at +0 (distance.hpp:16-33)
-            const int pi = (slot * 32 + sb + cc) * 4 + kk;
+            for (int gg = 0; gg < 16; ++gg) {
+                ta[gg] = tile[cc * RP_TLD + 4 * gg + kk];
+                tb[gg] = tile[(cc + 8) * RP_TLD + 4 * gg + kk];
+            }
+            float sa = 0.f, sb2 = 0.f;  // l2_sq's accumulators start at +0 (distance.hpp:16-33)
+            const int pa = (slot * 32 + sb + cc) * 4 + kk, pb = pa + 32;
             if (r) {
                 if (sb == 0) wait_parity(bar0 + 8 * slot, use & 1u);  // peer's partials landed
-                sacc = wpart[pi];
+                sa = wpart[pa];
+                sb2 = wpart[pb];
             }
 #pragma unroll
-            for (int gg = 0; gg < 16; ++gg) sacc = __fadd_rn(sacc, t[gg]);
+            for (int gg = 0; gg < 16; ++gg) {
+                sa = __fadd_rn(sa, ta[gg]);
+                sb2 = __fadd_rn(sb2, tb[gg]);
+            }
             if (r == 0) {
-                st_peer(peer_part + 4u * pi, sacc);
+                st_peer_async(peer_part + 4u * pa, sa, peer_bar0 + 8 * slot);
+                st_peer_async(peer_part + 4u * pb, sb2, peer_bar0 + 8 * slot);
             } else {
-                const float s1 = __shfl_down_sync(0xffffffffu, sacc, 1);
-                const float pair = __fadd_rn(sacc, s1);  // kk = 0: s0 + s1, kk = 2: s2 + s3
-                const float p23 = __shfl_down_sync(0xffffffffu, pair, 2);
-                if (kk == 0 && sb + cc < nb) rdist[t0 + sb + cc] = __fadd_rn(pair, p23);
+                const float a1 = __shfl_down_sync(0xffffffffu, sa, 1), b1 = __shfl_down_sync(0xffffffffu, sb2, 1);
+                const float pa2 = __fadd_rn(sa, a1), pb2 = __fadd_rn(sb2, b1);  // kk = 0: s0 + s1, kk = 2: s2 + s3
+                const float a3 = __shfl_down_sync(0xffffffffu, pa2, 2), b3 = __shfl_down_sync(0xffffffffu, pb2, 2);
+                if (kk == 0 && sb + cc < nb) rdist[t0 + sb + cc] = __fadd_rn(pa2, a3);
+                if (kk == 0 && sb + 8 + cc < nb) rdist[t0 + sb + 8 + cc] = __fadd_rn(pb2, b3);
             }
             __syncwarp();
         }
-        // hand the slot over: rank 0 -> partials ready; rank 1 -> slot free
-        arrive_peer(peer_bar0 + 8 * slot);
+        // rank 1 hands the slot back once its partials are consumed (rank 0's
+        // st.async stores completed the full barrier themselves)
+        __syncwarp();
+        if (r == 1 && lane == 0) arrive_peer(peer_bar0 + 8 * slot);
     }
     cluster_sync();  // no CTA leaves while its peer may still touch its shared memory
 }

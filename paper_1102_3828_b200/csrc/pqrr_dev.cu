@@ -2184,6 +2184,10 @@ int pqrr_dev_merge_topk_device(int device, const uint32_t* ids, const float* dis
                       true, stream);
 }
 
+int pqrr_dev_index_device(pqrr_dev_index* h, int* device) {
+    return guarded([&] { *device = h->ix.device; });
+}
+
 int pqrr_dev_merge_packed_device(int device, const void* packed, size_t nq, uint32_t parts,
                                  uint32_t width, uint32_t k, uint32_t* out_ids, float* out_dists,
                                  uint32_t* out_counts, void* stream) {

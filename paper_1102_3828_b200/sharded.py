@@ -265,3 +265,60 @@ class MultiShardSearch:
         _check_shortlist(sl_c, self.k)
         return self._stack_merge([_rerank_owned(ix, d_queries, sl_i, sl_c, self.k, stream)
                                   for ix in self.ixs], self.k, stream)
+
+
+class IndexGroup:
+    """One process driving several id-range shards (pqrr_dev_group_*): NCCL
+    all-gathers when the shards sit on distinct GPUs, device copies when they
+    share one.  mode "exact" (default) is bit-identical to one index holding
+    every id; "local" merges each shard's fused top-k."""
+
+    MODES = {"exact": 0, "local": 1}
+
+    def __init__(self, shards, mode: str = "exact"):
+        import ctypes as C
+
+        from ._lib import check, lib
+
+        if mode not in self.MODES:
+            raise ValueError(f"unknown group mode {mode!r}")
+        self.shards, self.mode = list(shards), mode
+        arr = (C.c_void_p * len(self.shards))(*[s.h.value for s in self.shards])
+        self.h = C.c_void_p()
+        check(lib.pqrr_dev_group_create(len(self.shards), arr, C.byref(self.h)))
+
+    def uses_nccl(self) -> bool:
+        import ctypes as C
+
+        from ._lib import check, lib
+
+        n, u = C.c_uint32(), C.c_int()
+        check(lib.pqrr_dev_group_size(self.h, C.byref(n), C.byref(u)))
+        return bool(u.value)
+
+    def search(self, queries, v: int, kprime: int, k: int = 0, out=None):
+        """u8 host queries [nq, d] -> (ids, dists, counts), rows of k (k' if k = 0)."""
+        from ._lib import check, lib
+
+        q = np.ascontiguousarray(queries, np.uint8)
+        nq, width = q.shape[0], (k or kprime)
+        if out is None:
+            out = (np.zeros((nq, width), np.uint32), np.zeros((nq, width), np.float32),
+                   np.zeros(nq, np.uint32))
+        ids, dists, counts = out
+        check(lib.pqrr_dev_group_search_u8(self.h, q, nq, v, kprime, k, self.MODES[self.mode], ids, dists,
+                                           counts))
+        return ids, dists, counts
+
+    def close(self):
+        from ._lib import lib
+
+        if getattr(self, "h", None) and self.h.value:
+            lib.pqrr_dev_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

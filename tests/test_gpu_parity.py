@@ -199,7 +199,10 @@ def mid_instance(pq, oracle):
 
 
 @pytest.mark.parametrize("v,kprime,k", [(24, 1000, 100), (8, 100, 10), (40, 300, 300), (3, 2000, 1),
-                                        (64, 5000, 100), (40, 10000, 100)])
+                                        (64, 5000, 100), (40, 10000, 100),
+                                        # k' <= 16 over ~15k-38k probed entries (> the 8192 candidate
+                                        # buffer): the sampled threshold at stride 1, every entry sampled
+                                        (16, 16, 10), (40, 8, 8)])
 def test_search_matches_oracle(mid_instance, v, kprime, k):
     oix, dix, q = mid_instance["oix"], mid_instance["dix"], mid_instance["queries"]
     qf = q.astype(np.float32)
@@ -779,3 +782,50 @@ def test_assign_u8_other_shapes_exact(pq, reflib):
     rows = rng.integers(0, 256, (3000, 64)).astype(np.uint8)
     cen = rng.uniform(0, 255, (100, 64)).astype(np.float32)
     np.testing.assert_array_equal(pq.kernels.assign_u8(rows, cen), reflib.assign(rows.astype(np.float32), cen)[0])
+
+
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_index_group_exact_equals_single_index(pq, mid_instance, nshards):
+    """pqrr_dev_group_* (one process, several id-range shards; here all on one
+    GPU, so the all-gathers are device copies): exact mode equals the
+    single-index oracle bit for bit; local mode equals MultiShardSearch's."""
+    import torch
+
+    from paper_1102_3828_b200.sharded import IndexGroup, MultiShardSearch, shard_range
+
+    mi = mid_instance
+    base, q = mi["base"], mi["queries"]
+    shards = []
+    for r in range(nshards):
+        lo, hi = shard_range(len(base), r, nshards)
+        ix = pq.IvfIndex(pq.Codebook(mi["coarse"]), pqobj(pq, mi["books"], 8),
+                         pq.RefineQuantizer(pqobj(pq, mi["rbooks"], 16)))
+        ix.add(base[lo:hi], id_base=lo)
+        ix.finalize()
+        shards.append(ix)
+    qf = q.astype(np.float32)
+    for v, kprime, k in [(8, 300, 50), (32, 2000, 100)]:
+        g = IndexGroup(shards, "exact")
+        assert not g.uses_nccl()
+        gi, gd, gc = g.search(q, v, kprime, k)
+        si, _, sc = mi["oix"].search(qf, v, kprime)
+        ri, rd = mi["oix"].rerank(qf, si, sc, k)
+        np.testing.assert_array_equal(gi, ri)
+        np.testing.assert_array_equal(bits(gd), bits(rd))
+        assert (gc == k).all()
+        # shortlists only (k = 0): the global IVFADC top-k'
+        si2, sd2, sc2 = g.search(q, v, kprime, 0)
+        np.testing.assert_array_equal(sc2, sc)
+        for r in range(len(q)):
+            np.testing.assert_array_equal(si2[r, :sc[r]], si[r, :sc[r]])
+        g.close()
+        lg = IndexGroup(shards, "local")
+        li, ld, lc = lg.search(q, v, kprime, k)
+        mi_, md_, mc_ = MultiShardSearch(shards, k, kprime, v, mode="local").search(torch.from_numpy(q).cuda())
+        np.testing.assert_array_equal(li, mi_.cpu().numpy().view(np.uint32))
+        np.testing.assert_array_equal(bits(ld), bits(md_.cpu().numpy()))
+        lg.close()
+    g = IndexGroup(shards, "exact")
+    with pytest.raises(ValueError, match="shortlist too small"):
+        g.search(q[:4], 1, 5, 100)
+    g.close()
