@@ -12,6 +12,7 @@
 #include "../oracle/pqrr_oracle.h"
 #include "pqrr/ivf_index.hpp"
 #include "pqrr/kernels.hpp"
+#include "pqrr_dev.h"
 
 using namespace pqrr;
 
@@ -141,6 +142,37 @@ int main() {
         EXPECT(ok, "cache: index replaced in the same storage");
         orc_ivf_free(ox2);
         b200::release_device_indexes();
+    }
+
+    // multi-GPU group API (C ABI, one process): 2 and 3 id-range shards on
+    // device 0 (device-copy all-gathers), exact mode == one index bit for bit
+    {
+        std::vector<uint8_t> qu(nq * d);
+        for (size_t i = 0; i < qu.size(); ++i) qu[i] = uint8_t(queries.data[i]);
+        const uint32_t kp = 300, kk = 20;
+        std::vector<uint32_t> oi(nq * kp), ocnt(nq), ri(nq * kk);
+        std::vector<float> od(nq * kp), rd(nq * kk);
+        orc_ivf_search_batch(ox, queries.data.data(), nq, 6, kp, oi.data(), od.data(), ocnt.data());
+        orc_ivf_rerank_batch(ox, queries.data.data(), nq, oi.data(), ocnt.data(), kp, kk, ri.data(), rd.data());
+        for (uint32_t G : {2u, 3u}) {
+            std::vector<pqrr_dev_index*> sh(G);
+            for (uint32_t r = 0; r < G; ++r) {
+                const size_t lo = n * r / G, hi = n * (r + 1) / G;
+                pqrr_dev_index_create(0, d, c, oc.data(), m, ob.data(), mp, orb.data(), ks, &sh[r]);
+                pqrr_dev_add_f32(sh[r], base.row(lo), hi - lo, uint32_t(lo));
+            }
+            pqrr_dev_group* grp = nullptr;
+            EXPECT(pqrr_dev_group_create(G, sh.data(), &grp) == PQRR_OK, "group_create");
+            std::vector<uint32_t> gi(nq * kk), gc(nq);
+            std::vector<float> gd(nq * kk);
+            const int grc = pqrr_dev_group_search_u8(grp, qu.data(), nq, 6, kp, kk, PQRR_GROUP_EXACT, gi.data(),
+                                                     gd.data(), gc.data());
+            if (grc != PQRR_OK) std::fprintf(stderr, "group_search(G=%u): %s\n", G, pqrr_dev_last_error());
+            EXPECT(grc == PQRR_OK, "group_search");
+            EXPECT(gi == ri && std::memcmp(gd.data(), rd.data(), rd.size() * 4) == 0, "group exact == one index");
+            pqrr_dev_group_destroy(grp);
+            for (auto h : sh) pqrr_dev_index_destroy(h);
+        }
     }
 
     // kernel seam: scan_topk against the serial oracle

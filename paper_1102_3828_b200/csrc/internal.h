@@ -44,6 +44,12 @@ unsigned long long launch_count();
 // Number of SMs of the current device (cached).
 int sm_count();
 
+// Raises a kernel's dynamic shared-memory limit to at least `bytes` (never
+// lowers it): the attribute is per function and process-wide, so a
+// per-launch setting would race between host threads searching different
+// indexes (a lowered limit fails the other thread's launch).
+void set_max_smem(const void* kernel, size_t bytes);
+
 // -------------------------------------------------------------- synth (k_synth.cu)
 void launch_synth_centers(uint64_t seed, uint32_t clusters, uint32_t d, double* centers,
                           cudaStream_t s);

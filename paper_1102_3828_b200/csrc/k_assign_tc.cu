@@ -433,7 +433,7 @@ void AssignTc::assign(const uint8_t* y, size_t n, const float* coarse, uint32_t*
     uint32_t* ovf = nullptr;
     PQRR_CUDA(cudaMallocAsync(&ovf, (n + 1) * sizeof(uint32_t), s));
     PQRR_CUDA(cudaMemsetAsync(ovf + n, 0, sizeof(uint32_t), s));
-    PQRR_CUDA(cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    set_max_smem((const void*)assign_tc_kernel, (size_t)((int)SMEM_BYTES));
     const size_t ntiles = (n + AT_M - 1) / AT_M;
     const unsigned grid = (unsigned)std::min<size_t>(ntiles, (size_t)sm_count());
     assign_tc_kernel<<<grid, AT_THREADS, SMEM_BYTES, s>>>(mh, ml, y, n, coarse, cn, nc, cmax, out, ovf, ovf + n);

@@ -161,7 +161,7 @@ void launch_far_bound(const float* xq, const float* coarse, const float* books, 
     if (nq == 0 || w <= R1) return;
     const size_t smem = (size_t)M * KS * DS * 4 + (size_t)M * KS * 4 + (size_t)BW * 16 * RLD * 4 +
                         (size_t)BW * 16 * M * 4;
-    PQRR_CUDA(cudaFuncSetAttribute(far_bound_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem((const void*)far_bound_kernel, (size_t)((int)smem));
     far_bound_kernel<<<sm_count(), BW * 32, smem, s>>>(xq, coarse, books, probes, nq, w, R1, pair_bound);
     PQRR_LAUNCH_CHECK();
     count_launch();

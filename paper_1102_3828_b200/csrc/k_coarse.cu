@@ -360,8 +360,7 @@ void pair_dists_t(const float* x, size_t nx, const float* c, uint32_t nc, float*
     size_t smem = 2 * TB * (D + 4) * sizeof(float);
     static bool attr = false;
     if (!attr) {
-        PQRR_CUDA(cudaFuncSetAttribute(pair_dists_kernel<D>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set_max_smem((const void*)pair_dists_kernel<D>, (size_t)((int)smem));
         attr = true;
     }
     dim3 grid((unsigned)((nx + TB - 1) / TB), (nc + TB - 1) / TB);
@@ -376,8 +375,7 @@ void argmin_t(const float* x, size_t nx, const float* c, uint32_t nc, uint32_t* 
     size_t smem = 2 * TB * (D + 4) * sizeof(float);
     static bool attr = false;
     if (!attr) {
-        PQRR_CUDA(cudaFuncSetAttribute(argmin_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
+        set_max_smem((const void*)argmin_kernel<D>, (size_t)((int)smem));
         attr = true;
     }
     argmin_kernel<D><<<(unsigned)((nx + TB - 1) / TB), 256, smem, s>>>(x, nx, c, nc, out_idx,
@@ -444,8 +442,7 @@ void launch_topw(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* o
         while (w2 < w) w2 <<= 1;
         const size_t smem = (size_t)((nc + 1) & ~1u) * 4 + (size_t)w2 * 8;
         if (smem <= 200 * 1024) {
-            PQRR_CUDA(cudaFuncSetAttribute(topw_radix_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            set_max_smem((const void*)topw_radix_kernel, (size_t)((int)smem));
             topw_radix_kernel<<<(unsigned)nq, TW_THREADS, smem, s>>>(D, nc, w, w2, out_idx, out_dist);
             PQRR_LAUNCH_CHECK();
             count_launch();
@@ -458,8 +455,7 @@ void launch_topw(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* o
     if (smem > 200 * 1024) throw ArgError("coarse quantizer too large for device top-w (c > 16384)");
     static size_t attr = 0;
     if (smem > attr) {
-        PQRR_CUDA(cudaFuncSetAttribute(topw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       200 * 1024));
+        set_max_smem((const void*)topw_kernel, (size_t)(200 * 1024));
         attr = 200 * 1024;
     }
     topw_kernel<<<(unsigned)nq, 512, smem, s>>>(D, nc, n2, w, out_idx, out_dist);

@@ -356,8 +356,7 @@ void launch_coarse_tc(const float* x, size_t nq, const float* c, uint32_t nc, co
     const size_t smem = (size_t)(GM + GN) * GLD * sizeof(float);
     static bool attr = false;
     if (!attr) {
-        PQRR_CUDA(cudaFuncSetAttribute(coarse_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
+        set_max_smem((const void*)coarse_gemm_kernel, (size_t)((int)smem));
         attr = true;
     }
     dim3 grid((nc + GN - 1) / GN, (unsigned)((nq + GM - 1) / GM));

@@ -198,8 +198,7 @@ void ivf_encode_t(const float* xf, const uint8_t* xu, size_t n, uint32_t d, cons
                   uint32_t mprime, uint32_t ks, uint8_t* codes, uint8_t* rcodes, cudaStream_t s) {
     size_t smem = (size_t)EV * (d + 1) * sizeof(float) + EV * (m + mprime);
     smem = (smem + 15) & ~size_t(15);
-    PQRR_CUDA(cudaFuncSetAttribute(ivf_encode_kernel<DS, DSR>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem((const void*)ivf_encode_kernel<DS, DSR>, (size_t)((int)smem));
     ivf_encode_kernel<DS, DSR><<<(unsigned)((n + EV - 1) / EV), EV * EW, smem, s>>>(
         xf, xu, n, d, assign, coarse, books, m, rbooks, mprime, ks, codes, rcodes, kNegZero2);
     PQRR_LAUNCH_CHECK();
@@ -245,8 +244,7 @@ void launch_pq_encode(const float* data, size_t n, uint32_t d, const float* book
     const unsigned grid = (unsigned)((n + EV - 1) / EV);
 #define PQE(DS)                                                                                  \
     do {                                                                                         \
-        PQRR_CUDA(cudaFuncSetAttribute(pq_encode_kernel<DS>,                                     \
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        set_max_smem((const void*)pq_encode_kernel<DS>, smem);                                  \
         pq_encode_kernel<DS><<<grid, EV * EW, smem, s>>>(data, n, d, books, m, ks, codes,         \
                                                          kNegZero2);                             \
     } while (0)

@@ -598,8 +598,7 @@ void recheck_t(const float* xq, uint32_t d, const float* coarse, const float* bo
                uint32_t cap, const uint32_t* cand_pos, float* cand_dist, const float* tau, size_t nq,
                uint32_t* cand_le, cudaStream_t s) {
     const size_t smem = (size_t)w * d * sizeof(float);
-    PQRR_CUDA(cudaFuncSetAttribute(recheck_kernel<DSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)std::max<size_t>(smem, 1)));
+    set_max_smem((const void*)recheck_kernel<DSUB>, (size_t)((int)std::max<size_t>(smem, 1)));
     recheck_kernel<DSUB><<<(unsigned)nq, 256, smem, s>>>(
         xq, d, coarse, books, probes, w, reinterpret_cast<const u64*>(codes), cand_cnt, cap, cand_pos,
         cand_dist, tau, cand_le, kNegZero2);
@@ -683,7 +682,7 @@ void launch_ivf_filter(const FilterArgs& a, cudaStream_t s) {
     // + 1 KiB: 32 staged 2052-byte lane columns (the LUT build) exceed the
     // 64 KiB candidate stage
     const int smem = LUT8_BYTES + STAGE * (int)sizeof(uint32_t) + 1024;
-    PQRR_CUDA(cudaFuncSetAttribute(ivf_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    set_max_smem((const void*)ivf_filter_kernel, (size_t)(smem));
     ivf_filter_kernel<<<sm_count(), FT, smem, s>>>(a);
     PQRR_LAUNCH_CHECK();
     count_launch();
@@ -717,8 +716,7 @@ bool recheck_smem_t(const float* xq, uint32_t d, const float* coarse, const floa
                     size_t nq, uint32_t* cand_le, cudaStream_t s, uint32_t* cand_mm) {
     const size_t smem = (size_t)M * KS * DSUB * sizeof(float) + (size_t)w * d * sizeof(float);
     if (smem > 216 * 1024) return false;  // + ~9.3 KiB static (s_x) <= 227 KiB
-    PQRR_CUDA(cudaFuncSetAttribute(recheck_smem_kernel<DSUB>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem((const void*)recheck_smem_kernel<DSUB>, (size_t)((int)smem));
     uint32_t* counter = nullptr;
     PQRR_CUDA(cudaMallocAsync(&counter, sizeof(uint32_t), s));
     PQRR_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), s));

@@ -484,8 +484,7 @@ void lut_pass_t(const ScanArgs& a, cudaStream_t s) {
     const size_t ring = (size_t)RING * KS * DSUB * sizeof(float);
     const size_t smem = (size_t)LUT_FLOATS * sizeof(float) + 2 * (size_t)xbuf((int)a.d + 4) * sizeof(float) +
                         (size_t)(QT + 1) * a.d * sizeof(float) + 2 * (size_t)SCAP * sizeof(u64) + ring;
-    PQRR_CUDA(cudaFuncSetAttribute(lut_pass_kernel<DSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+    set_max_smem((const void*)lut_pass_kernel<DSUB>, (size_t)((int)smem));
     lut_pass_kernel<DSUB><<<sm_count(), NTH, smem, s>>>(a, kNegZero2);
     PQRR_LAUNCH_CHECK();
     count_launch();

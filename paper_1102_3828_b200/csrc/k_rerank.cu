@@ -16,7 +16,7 @@
 // bank group g mod 8, so every book gather is conflict-free whatever the
 // codes.  Both CTAs walk the same chunks (32 candidates of one query); a warp
 // handles 2 candidates per step (half warp each, lane g = one dim quad), the
-// squares go to a padded 16-candidate tile, and lanes (candidate, k) add the 16
+// squares go to a padded 8-candidate tile, and lanes (candidate, k) add the 16
 // terms of s_k of their half in ascending t.  CTA 0's partial sums (16 B per
 // candidate) are stored straight into CTA 1's shared memory (distributed shared memory)
 // with st.async, which completes CTA 1's mbarrier; CTA 1 continues the same four
@@ -53,14 +53,17 @@ __device__ __forceinline__ void st_peer_async(unsigned a, float v, unsigned peer
 __device__ __forceinline__ void expect_tx(unsigned bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// Remote arrive / local wait with the default (CTA-scope) semantics, as the
+// cross-CTA TMA pipelines use them: a cluster-scope acquire would invalidate
+// L1 (CCTL.IVALL) and a cluster-scope release fence the GPU on every chunk.
 __device__ __forceinline__ void arrive_peer(unsigned a) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
 }
 __device__ __forceinline__ void wait_parity(unsigned a, unsigned parity) {
     unsigned done = 0;
     while (!done)
         asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
             "selp.u32 %0, 1, 0, p; }"
             : "=r"(done) : "r"(a), "r"(parity) : "memory");
 }
@@ -72,7 +75,7 @@ template <int DSR>
 struct RpSmem {
     static constexpr int HB = (128 / DSR) / 2;  // refinement code bytes per half
     static constexpr size_t books = 2 * 256 * 64 * 4;
-    static constexpr size_t tiles = (size_t)RP_WARPS * 16 * RP_TLD * 4;
+    static constexpr size_t tiles = (size_t)RP_WARPS * 8 * RP_TLD * 4;
     static constexpr size_t part = (size_t)RP_WARPS * 2 * 32 * 4 * 4;
     static constexpr size_t mlist = (size_t)RP_WARPS * 32 * 4;
     static constexpr size_t mcode = (size_t)RP_WARPS * 4 * RP_MLD;
@@ -95,7 +98,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
     uint8_t* base = reinterpret_cast<uint8_t*>(rp_smem);
     const float4* bookP = reinterpret_cast<const float4*>(base);            // [256][16] float4
     const float4* bookR = bookP + 256 * 16;                                 // [256][16] float4
-    float* tiles = reinterpret_cast<float*>(base + L::books);                // [warps][16][TLD]
+    float* tiles = reinterpret_cast<float*>(base + L::books);                // [warps][8][TLD]
     float* part = reinterpret_cast<float*>(base + L::books + L::tiles);      // [warps][2][32][4]
     uint32_t* mlist = reinterpret_cast<uint32_t*>(base + L::books + L::tiles + L::part);
     uint8_t* mcode = reinterpret_cast<uint8_t*>(mlist) + L::mlist;         // [warps][4][MLD]
@@ -120,7 +123,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
     __syncthreads();
     cluster_sync();
 
-    float* tile = tiles + warp * 16 * RP_TLD;
+    float* tile = tiles + warp * 8 * RP_TLD;
     float* wpart = part + warp * 2 * 32 * 4;
     uint32_t* wlist = mlist + warp * 32;
     uint8_t* wcode = mcode + warp * 4 * RP_MLD;
@@ -140,33 +143,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
     const uint32_t cpq = (stride + 31) / 32;
     const size_t total = nq * (size_t)cpq;
     const size_t tw = (size_t)(gridDim.x >> 1) * RP_WARPS;
-    auto next_valid = [&](size_t c) -> size_t {
-        for (; c < total; c += tw)
-            if ((uint32_t)(c % cpq) * 32 < sl_cnt[c / cpq]) break;
-        return c;
-    };
-    // chunk metadata, software-pipelined two deep (lane = candidate): the
-    // positions of chunk i + 2 and the position-dependent gathers (list, code
-    // and refinement-code bytes) of chunk i + 1 are in flight while chunk i
-    // computes, so no warp waits on a dependent DRAM round trip
-    uint32_t p_id = 0, p_list = 0, p_code = 0, n_pos = 0;
+    // chunk metadata, software-pipelined (lane = candidate): while chunk i
+    // computes, the positions and row counts of chunk i + 2 and the
+    // position-dependent gathers (list, code and refinement-code bytes) of
+    // chunk i + 1 are in flight, so no warp waits on a dependent DRAM round
+    // trip.  Chunk indices advance by the grid stride; chunks past a query's
+    // count carry nb = 0 and are skipped by both CTAs alike.
+    uint32_t p_id = 0, p_list = 0, p_code = 0;
     uint32_t p_rc[(HB + 3) / 4];
-    auto rows_of = [&](size_t c, size_t& t0, uint32_t& nb) {
+    uint32_t n_pos = 0, n_cnt = 0;  // chunk i + 1: position of the lane's entry, row count
+    auto load_pos = [&](size_t c) {  // no dependency: rows are allocated k' wide
         const size_t q = c / cpq;
+        n_cnt = sl_cnt[q];
+        n_pos = sl_pos[q * stride + (uint32_t)(c % cpq) * 32 + min((uint32_t)lane, stride - 1 - (uint32_t)(c % cpq) * 32)];
+    };
+    auto nb_of = [&](size_t c, uint32_t cnt) -> uint32_t {
         const uint32_t i0 = (uint32_t)(c % cpq) * 32;
-        nb = min(32u, sl_cnt[q] - i0);
-        t0 = q * stride + i0;
+        return cnt > i0 ? min(32u, cnt - i0) : 0u;
     };
-    auto load_pos = [&](size_t c) {
-        size_t t0;
-        uint32_t nb;
-        rows_of(c, t0, nb);
-        if ((uint32_t)lane < nb) n_pos = sl_pos[t0 + lane];
-    };
-    auto load_meta = [&](size_t c, uint32_t pos) {
-        size_t t0;
-        uint32_t nb;
-        rows_of(c, t0, nb);
+    auto load_meta = [&](size_t c, uint32_t pos, uint32_t nb) {
+        const size_t t0 = (c / cpq) * stride + (uint32_t)(c % cpq) * 32;
         if ((uint32_t)lane < nb) {
             if (r) p_id = key_id(sl_key[t0 + lane]);
             p_list = block_list[pos >> 4];
@@ -183,22 +179,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
             }
         }
     };
-    size_t nch = next_valid((size_t)(blockIdx.x >> 1) * RP_WARPS + warp);
-    size_t nch2 = nch < total ? next_valid(nch + tw) : total;
-    if (nch < total) {
-        load_pos(nch);
-        load_meta(nch, n_pos);
+    const size_t start = (size_t)(blockIdx.x >> 1) * RP_WARPS + warp;
+    uint32_t cur_cnt = 0;
+    if (start < total) {
+        load_pos(start);
+        cur_cnt = n_cnt;
+        load_meta(start, n_pos, nb_of(start, cur_cnt));
+        if (start + tw < total) load_pos(start + tw);
     }
-    if (nch2 < total) load_pos(nch2);
     uint32_t it = 0;
-    for (size_t ch = nch; ch < total; ch = nch, ++it) {
+    for (size_t ch = start; ch < total; ch += tw) {
         const size_t q = ch / cpq;
         const uint32_t i0 = (uint32_t)(ch % cpq) * 32;
-        const uint32_t nb = min(32u, sl_cnt[q] - i0);
+        const uint32_t nb = nb_of(ch, cur_cnt);
         const size_t t0 = q * stride + i0;
         const uint32_t slot = it & 1u, use = it >> 1;
         __syncwarp();  // the previous chunk's metadata reads are done
-        {
+        if (nb) {
             // lanes past nb repeat the last candidate, so sub-batches run
             // without bounds checks (duplicates are never stored)
             const int src = min(lane, (int)nb - 1);
@@ -214,79 +211,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
             }
             if (r && (uint32_t)lane < nb) rid[t0 + lane] = p_id;
         }
-        nch = nch2;
-        if (nch < total) {
-            load_meta(nch, n_pos);
-            nch2 = next_valid(nch + tw);
-            if (nch2 < total) load_pos(nch2);
+        if (ch + tw < total) {
+            cur_cnt = n_cnt;
+            load_meta(ch + tw, n_pos, nb_of(ch + tw, cur_cnt));
+            if (ch + 2 * tw < total) load_pos(ch + 2 * tw);
         }
+        if (!nb) continue;
+        ++it;
         const float4 x = __ldg(reinterpret_cast<const float4*>(xq + q * 128 + 64 * r) + g);
         const u64 x01 = pk2(x.x, x.y), x23 = pk2(x.z, x.w);
         if (r == 0 && use > 0) wait_parity(bar0 + 8 * slot, (use - 1) & 1u);  // peer done with the slot
-        if (r == 1 && lane == 0) expect_tx(bar0 + 8 * slot, 256u * ((nb + 15) / 16));  // partials to come
+        if (r == 1 && lane == 0) expect_tx(bar0 + 8 * slot, 128u * ((nb + 7) / 8));  // partials to come
         __syncwarp();
         uint32_t cur_l = 0xffffffffu;
         float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
-        // sub-batches of 16 candidates: squares of 8 steps (2 candidates per
-        // step), then every summing lane runs TWO independent chains
-        // (candidates cc and cc + 8) interleaved
-        for (uint32_t sb = 0; sb < nb; sb += 16) {
+        for (uint32_t sb = 0; sb < nb; sb += 8) {
+            const uint4 lq0 = reinterpret_cast<const uint4*>(wlist)[sb >> 2];
+            const uint4 lq1 = reinterpret_cast<const uint4*>(wlist)[(sb >> 2) + 1];
+            const uint32_t la[4] = {h ? lq0.y : lq0.x, h ? lq0.w : lq0.z, h ? lq1.y : lq1.x, h ? lq1.w : lq1.z};
+            const u64 cb = *reinterpret_cast<const u64*>(wcode + jl * RP_MLD + sb);
+            const u64 rb = *reinterpret_cast<const u64*>(wrc + jrl * RP_MLD + sb);
+            float4 bv[4], rv[4];
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const uint32_t s0 = sb + 8 * half;
-                const uint4 lq0 = reinterpret_cast<const uint4*>(wlist)[s0 >> 2];
-                const uint4 lq1 = reinterpret_cast<const uint4*>(wlist)[(s0 >> 2) + 1];
-                const uint32_t la[4] = {h ? lq0.y : lq0.x, h ? lq0.w : lq0.z, h ? lq1.y : lq1.x, h ? lq1.w : lq1.z};
-                const u64 cb = *reinterpret_cast<const u64*>(wcode + jl * RP_MLD + s0);
-                const u64 rb = *reinterpret_cast<const u64*>(wrc + jrl * RP_MLD + s0);
-                float4 bv[4], rv[4];
+            for (int st = 0; st < 4; ++st) {
+                const uint32_t c = 2 * st + h;
+                bv[st] = bookP[((uint32_t)(cb >> (8 * c)) & 0xffu) * 16 + g];
+                rv[st] = bookR[((uint32_t)(rb >> (8 * c)) & 0xffu) * 16 + g];
+            }
 #pragma unroll
-                for (int st = 0; st < 4; ++st) {
-                    const uint32_t c = 2 * st + h;
-                    bv[st] = bookP[((uint32_t)(cb >> (8 * c)) & 0xffu) * 16 + g];
-                    rv[st] = bookR[((uint32_t)(rb >> (8 * c)) & 0xffu) * 16 + g];
+            for (int st = 0; st < 4; ++st) {
+                if (la[st] != cur_l) {  // candidates arrive grouped by list: rare
+                    cur_l = la[st];
+                    cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)cur_l * 128 + 64 * r) + g);
                 }
-#pragma unroll
-                for (int st = 0; st < 4; ++st) {
-                    if (la[st] != cur_l) {  // candidates arrive grouped by list: rare
-                        cur_l = la[st];
-                        cv = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)cur_l * 128 + 64 * r) + g);
-                    }
-                    const u64 y01 = add2(add2(pk2(cv.x, cv.y), pk2(bv[st].x, bv[st].y)), pk2(rv[st].x, rv[st].y));
-                    const u64 y23 = add2(add2(pk2(cv.z, cv.w), pk2(bv[st].z, bv[st].w)), pk2(rv[st].z, rv[st].w));
-                    const u64 q01 = sq2(sub2(x01, y01), nz), q23 = sq2(sub2(x23, y23), nz);
-                    *reinterpret_cast<float4*>(tile + (8 * half + 2 * st + h) * RP_TLD + 4 * g) =
-                        make_float4(lo2(q01), hi2(q01), lo2(q23), hi2(q23));
-                }
+                const u64 y01 = add2(add2(pk2(cv.x, cv.y), pk2(bv[st].x, bv[st].y)), pk2(rv[st].x, rv[st].y));
+                const u64 y23 = add2(add2(pk2(cv.z, cv.w), pk2(bv[st].z, bv[st].w)), pk2(rv[st].z, rv[st].w));
+                const u64 q01 = sq2(sub2(x01, y01), nz), q23 = sq2(sub2(x23, y23), nz);
+                *reinterpret_cast<float4*>(tile + (2 * st + h) * RP_TLD + 4 * g) =
+                    make_float4(lo2(q01), hi2(q01), lo2(q23), hi2(q23));
             }
             __syncwarp();
-            float ta[16], tb[16];
+            float t[16];
 #pragma unroll
-            for (int gg = 0; gg < 16; ++gg) {
-                ta[gg] = tile[cc * RP_TLD + 4 * gg + kk];
-                tb[gg] = tile[(cc + 8) * RP_TLD + 4 * gg + kk];
-            }
-            float sa = 0.f, sb2 = 0.f;  // l2_sq's accumulators start at +0 (distance.hpp:16-33)
-            const int pa = (slot * 32 + sb + cc) * 4 + kk, pb = pa + 32;
+            for (int gg = 0; gg < 16; ++gg) t[gg] = tile[cc * RP_TLD + 4 * gg + kk];
+            float sacc = 0.f;  // l2_sq's accumulators start at +0 (distance.hpp:16-33)
+            const int pi = (slot * 32 + sb + cc) * 4 + kk;
             if (r) {
                 if (sb == 0) wait_parity(bar0 + 8 * slot, use & 1u);  // peer's partials landed
-                sa = wpart[pa];
-                sb2 = wpart[pb];
+                sacc = wpart[pi];
             }
 #pragma unroll
-            for (int gg = 0; gg < 16; ++gg) {
-                sa = __fadd_rn(sa, ta[gg]);
-                sb2 = __fadd_rn(sb2, tb[gg]);
-            }
+            for (int gg = 0; gg < 16; ++gg) sacc = __fadd_rn(sacc, t[gg]);
             if (r == 0) {
-                st_peer_async(peer_part + 4u * pa, sa, peer_bar0 + 8 * slot);
-                st_peer_async(peer_part + 4u * pb, sb2, peer_bar0 + 8 * slot);
+                st_peer_async(peer_part + 4u * pi, sacc, peer_bar0 + 8 * slot);
             } else {
-                const float a1 = __shfl_down_sync(0xffffffffu, sa, 1), b1 = __shfl_down_sync(0xffffffffu, sb2, 1);
-                const float pa2 = __fadd_rn(sa, a1), pb2 = __fadd_rn(sb2, b1);  // kk = 0: s0 + s1, kk = 2: s2 + s3
-                const float a3 = __shfl_down_sync(0xffffffffu, pa2, 2), b3 = __shfl_down_sync(0xffffffffu, pb2, 2);
-                if (kk == 0 && sb + cc < nb) rdist[t0 + sb + cc] = __fadd_rn(pa2, a3);
-                if (kk == 0 && sb + 8 + cc < nb) rdist[t0 + sb + 8 + cc] = __fadd_rn(pb2, b3);
+                const float s1 = __shfl_down_sync(0xffffffffu, sacc, 1);
+                const float pair = __fadd_rn(sacc, s1);  // kk = 0: s0 + s1, kk = 2: s2 + s3
+                const float p23 = __shfl_down_sync(0xffffffffu, pair, 2);
+                if (kk == 0 && sb + cc < nb) rdist[t0 + sb + cc] = __fadd_rn(pair, p23);
             }
             __syncwarp();
         }
@@ -299,7 +281,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
 }
 
 void set_smem_attr(const void* f, size_t bytes) {
-    PQRR_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    set_max_smem((const void*)f, (size_t)((int)bytes));
 }
 
 }  // namespace

@@ -465,8 +465,7 @@ void scan_t(const ScanArgs& a, cudaStream_t s) {
     // the sub-codebook ring doubles as the 32 KiB q8 staging buffer
     const size_t ring = std::max<size_t>(2 * (size_t)KS * DSUB * sizeof(float), (size_t)M * KS * QT);
     const size_t smem = (size_t)LUT_FLOATS * sizeof(float) + (size_t)QT * (a.d + 4) * sizeof(float) + ring;
-    PQRR_CUDA(cudaFuncSetAttribute(ivf_scan_kernel<DSUB>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem((const void*)ivf_scan_kernel<DSUB>, (size_t)((int)smem));
     ivf_scan_kernel<DSUB><<<sm_count(), NT, smem, s>>>(a, kNegZero2);
     PQRR_LAUNCH_CHECK();
     count_launch();

@@ -647,7 +647,7 @@ __global__ void unpack_keys_kernel(const u64* __restrict__ keys, const uint32_t*
 }
 
 void set_smem(const void* f, size_t bytes) {
-    PQRR_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    set_max_smem((const void*)f, (size_t)((int)bytes));
 }
 
 }  // namespace

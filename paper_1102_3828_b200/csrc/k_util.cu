@@ -8,6 +8,10 @@
 #include <cub/device/device_segmented_radix_sort.cuh>
 
 #include "common.cuh"
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "internal.h"
 
 namespace pqrr_b200 {
@@ -25,6 +29,18 @@ int sm_count() {
     PQRR_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
     if (dev < 64) cached[dev] = n;
     return n;
+}
+
+void set_max_smem(const void* kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> set;  // (device, kernel) -> limit
+    int dev = 0;
+    PQRR_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = set[{dev, kernel}];
+    if (bytes <= cur) return;
+    PQRR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur = bytes;
 }
 
 namespace {

@@ -682,8 +682,7 @@ bool launch_rerank_topk_warp(const float* rdist, const uint32_t* rid, const uint
     const size_t smem = (size_t)WS_WARPS * k2 * sizeof(u64);
     if (k2 > 1024 || smem > 96 * 1024) return false;
     if (smem > 48 * 1024)
-        PQRR_CUDA(cudaFuncSetAttribute(rerank_topk_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
+        set_max_smem((const void*)rerank_topk_warp_kernel, (size_t)((int)smem));
     rerank_topk_warp_kernel<<<(unsigned)((nq + WS_WARPS - 1) / WS_WARPS), WS_WARPS * 32, smem, s>>>(
         rdist, rid, cnt, stride, nq, k, k2, out_ids, out_dists, out_cnt);
     PQRR_LAUNCH_CHECK();
