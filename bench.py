@@ -564,14 +564,21 @@ def main():
 def rooflines(cfg, stats, clocks, device, config):
     """Per-kernel rooflines (mean over the timed steps; kernel times are CUDA
     events on the index stream around each launch).  Algorithmic work per
-    launch, SURVEY.md §8(d):
-      K5 re-rank distances: k'·(m + m' + 8) B per query from HBM (code,
-        refinement code, shortlist key) — bound: HBM;
-      K4f filter: 8 one-byte LUT lookups per (live (query, list) pair, entry)
-        it tests — bound: the shared-memory pipe (128 B/clk/SM);
-      K4r recheck: 8 code-book rows of d/m floats per surviving candidate
-        — bound: the shared-memory pipe.
-    The dominant (longest) one is `roofline`; all are in `kernels`."""
+    launch, SURVEY.md §8(d), and the resource that bounds it:
+      K5a re-rank distances (rerank_pair_kernel, CTA pairs): per shortlist
+        entry the 8 PQ rows and m' refinement rows it must gather from on-chip
+        memory, 512 B + 512 B (the coarse row is amortised over runs of one
+        list) -- bound: the shared-memory pipe; its HBM side, k'(m + m' + 8) B
+        per query (code, refinement code, shortlist key / position), is
+        reported beside it;
+      K4f filter: 1 B per (live (query, list) pair, entry, sub-space) LUT
+        lookup it performs -- bound: the shared-memory pipe;
+      K4r recheck: 8 code-book rows of d/m floats (512 B) per surviving
+        candidate -- bound: the shared-memory pipe.
+    Shared-memory peak: 128 B/clk/SM x SMs x the SM clock sampled under load.
+    `traffic` is ncu dram__bytes_read.sum + dram__bytes_write.sum per launch
+    of the same kernel on the same commit (profiles/ncu_traffic.json), or null.
+    The dominant (longest) kernel is `roofline`; all are in `kernels`."""
     import torch
 
     peak_hbm, kind = measured_peak_gbs()
@@ -579,33 +586,36 @@ def rooflines(cfg, stats, clocks, device, config):
     n_sm = props.multi_processor_count
     f_sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
     smem_peak_gbs = 128.0 * n_sm * f_sm / 1e9
+    smem_kind = f"128 B/clk/SM x {n_sm} SMs x {f_sm / 1e6:.0f} MHz"
     mean = lambda k: float(np.mean([s[k] for s in stats]))  # noqa: E731
     m, mp, d = cfg["m"], cfg["mprime"], 128
     traffic = ncu_traffic(config)
     ks = []
     t = mean("ms_rerank_dist")
     if t > 0:
-        b = mean("rerank_candidates") * (m + mp + 8)
-        ks.append({"kernel": "rerank_coop_kernel (K5 refined distances)", "bound": "hbm",
+        nc = mean("rerank_candidates")
+        b = nc * (d // m * 4 * m + d // mp * 4 * mp)
+        hb = nc * (m + mp + 8)
+        ks.append({"kernel": "rerank_pair_kernel (K5a refined distances, CTA pairs)", "bound": "smem",
                    "kernel_ms": t, "algorithmic_bytes_per_launch": b,
-                   "achieved": b / (t / 1e3) / 1e9, "peak": peak_hbm, "unit": "GB/s",
-                   "peak_kind": kind, "traffic": traffic.get("rerank_coop_kernel")})
+                   "achieved": b / (t / 1e3) / 1e9, "peak": smem_peak_gbs, "unit": "GB/s",
+                   "peak_kind": smem_kind, "traffic": traffic.get("rerank_pair_kernel"),
+                   "hbm": {"algorithmic_bytes_per_launch": hb, "achieved": hb / (t / 1e3) / 1e9,
+                           "peak": peak_hbm, "frac": hb / (t / 1e3) / 1e9 / peak_hbm, "peak_kind": kind}})
     t = mean("ms_filter")
     if t > 0:
         b = mean("filter_live_entries") * m
         ks.append({"kernel": "ivf_filter_kernel (K4f 5-bit LUT filter, incl. live-pair compaction)",
                    "bound": "smem", "kernel_ms": t, "algorithmic_bytes_per_launch": b,
                    "achieved": b / (t / 1e3) / 1e9, "peak": smem_peak_gbs, "unit": "GB/s",
-                   "peak_kind": f"128 B/clk/SM x {n_sm} SMs x {f_sm / 1e6:.0f} MHz",
-                   "traffic": traffic.get("ivf_filter_kernel")})
+                   "peak_kind": smem_kind, "traffic": traffic.get("ivf_filter_kernel")})
     t = mean("ms_recheck")
     if t > 0:
         b = mean("candidates") * m * (d // m) * 4
         ks.append({"kernel": "recheck_smem_kernel (K4r exact ADC of the survivors)", "bound": "smem",
                    "kernel_ms": t, "algorithmic_bytes_per_launch": b,
                    "achieved": b / (t / 1e3) / 1e9, "peak": smem_peak_gbs, "unit": "GB/s",
-                   "peak_kind": f"128 B/clk/SM x {n_sm} SMs x {f_sm / 1e6:.0f} MHz",
-                   "traffic": traffic.get("recheck_smem_kernel")})
+                   "peak_kind": smem_kind, "traffic": traffic.get("recheck_smem_kernel")})
     for e in ks:
         e["frac"] = e["achieved"] / e["peak"]
     if not ks:

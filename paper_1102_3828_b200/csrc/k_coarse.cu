@@ -432,12 +432,11 @@ void launch_argmin(const float* x, size_t nx, const float* c, uint32_t nc, uint3
 void launch_topw(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* out_idx,
                  float* out_dist, cudaStream_t s) {
     if (nq == 0) return;
-    static const bool force_sort = getenv("PQRR_TOPW") != nullptr;
     // default: warp-per-query radix select (w <= 64)
-    if (!force_sort && launch_topw_warp(D, nq, nc, w, out_idx, out_dist, s)) return;
+    if (launch_topw_warp(D, nq, nc, w, out_idx, out_dist, s)) return;
     // radix select wins for large Kc (8192: 5.65 -> 2.33 ms per 10k queries);
     // the full bitonic sort is faster for Kc <= 2048 (measured 0.54 vs 0.61 ms)
-    if (w < nc && nc > 2048 && !force_sort) {
+    if (w < nc && nc > 2048) {
         uint32_t w2 = 1;
         while (w2 < w) w2 <<= 1;
         const size_t smem = (size_t)((nc + 1) & ~1u) * 4 + (size_t)w2 * 8;

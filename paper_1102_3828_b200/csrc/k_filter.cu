@@ -735,12 +735,13 @@ void launch_recheck(const float* xq, uint32_t d, uint32_t m, const float* coarse
                     float* cand_dist, const float* tau, size_t nq, uint32_t* cand_le,
                     cudaStream_t s, uint32_t* cand_mm) {
     if (!nq) return;
-    static const bool plain = getenv("PQRR_RECHECK") && std::string(getenv("PQRR_RECHECK")) == "global";
-    if (!plain && d / m == 16 &&
+    // shared-memory code book (the recheck kernels below stay for shapes or
+    // residual sets it does not hold)
+    if (d / m == 16 &&
         recheck_smem_t<16>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist,
                            tau, nq, cand_le, s, cand_mm))
         return;
-    if (!plain && d / m == 8 &&
+    if (d / m == 8 &&
         recheck_smem_t<8>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist,
                           tau, nq, cand_le, s, cand_mm))
         return;

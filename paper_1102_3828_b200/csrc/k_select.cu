@@ -669,10 +669,9 @@ void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_of
                              uint32_t stride, int tiered, uint32_t max_samples, float* tau,
                              cudaStream_t s) {
     if (nq == 0) return;
-    static const bool cta = getenv("PQRR_THRESHOLD") && std::string(getenv("PQRR_THRESHOLD")) == "cta";
     // warp per query when the batch fills the GPU with warps; a small batch
     // (C5 latency points) spreads each query's samples over a CTA instead
-    if (!cta && nq >= (size_t)2 * sm_count() * 8) {
+    if (nq >= (size_t)2 * sm_count() * 8) {
         launch_threshold_warp(sample_dist, sample_off, w, nq, query_sampled, alpha_k, stride, tiered, tau, s);
         return;
     }
@@ -691,8 +690,7 @@ void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const 
                         uint32_t* sl_cnt, cudaStream_t s,
                         const uint32_t* cand_mm) {
     if (nq == 0) return;
-    static const bool old_select = getenv("PQRR_SELECT") && std::string(getenv("PQRR_SELECT")) == "cta";
-    if (!sorted && !old_select) {  // unsorted shortlist (re-ranked next): warp per query
+    if (!sorted) {  // unsorted shortlist (re-ranked next): warp per query
         launch_select_warp(cand_dist, cand_pos, cand_cnt, cap, nq, ids, kprime, sl_key, sl_pos, sl_cnt, s,
                            cand_mm);
         return;

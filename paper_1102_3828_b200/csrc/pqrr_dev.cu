@@ -764,10 +764,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // batch on the exact CUDA-core path (checked at the first readback below)
     float* D = ws.alloc<float>(nq * (size_t)c);
     uint32_t* probes = ws.alloc<uint32_t>(P);
-    static const bool exact_coarse_env = getenv("PQRR_COARSE") && std::string(getenv("PQRR_COARSE")) == "exact";
-    static const uint32_t tc_min_c = getenv("PQRR_COARSE_TC_MIN") ? (uint32_t)atoi(getenv("PQRR_COARSE_TC_MIN"))
-                                                                   : 1024u;  // tuning hook
-    const bool coarse_tc = !exact_coarse && !exact_coarse_env && c >= tc_min_c && coarse_tc_supported(ix.d, w);
+    const bool coarse_tc = !exact_coarse && c >= 1024u && coarse_tc_supported(ix.d, w);
     uint32_t* coarse_ovf = ws.zeros<uint32_t>(1);
     if (coarse_tc) {
         if (!ix.cnorm.p) {
@@ -798,13 +795,10 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // least as large as the full one (never under-full; exactness is still
     // checked) and equal to it when the near probes hold the entries below it.
     // far probes are bounded on the tensor cores (k_bound.cu): pays from w = 32
-    static const uint32_t kTwoPhaseW = getenv("PQRR_TWO_PHASE_W") ? (uint32_t)atoi(getenv("PQRR_TWO_PHASE_W")) : 32u;
-    static const uint32_t kR1Div = getenv("PQRR_R1_DIV") ? (uint32_t)atoi(getenv("PQRR_R1_DIV")) : 8u;  // tuning hooks
-    static const bool old_lut_env0 = getenv("PQRR_LUTPASS") && std::string(getenv("PQRR_LUTPASS")) == "old";
-    static const bool one_phase_env = getenv("PQRR_LUT_ONE_PHASE") != nullptr;  // A/B switch
+    constexpr uint32_t kTwoPhaseW = 32u, kR1Div = 8u;
     // (large batches only: for a few hundred pairs the extra item sets and
     // launches cost more than the LUT builds they save)
-    const bool two_phase = filter_ok && !old_lut_env0 && !one_phase_env && w >= kTwoPhaseW &&
+    const bool two_phase = filter_ok && w >= kTwoPhaseW &&
                            P >= (size_t)64 * sm_count() &&
                            lut_pass_supported(ix.d, ix.m, ix.ks);
     const uint32_t R1 = two_phase ? (w + kR1Div - 1) / kR1Div : w;
@@ -834,9 +828,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
     uint64_t* grand = ws.zeros<uint64_t>(2);
     // importance-weighted sampling needs the warp-specialised LUT pass
-    static const bool old_lut_env = getenv("PQRR_LUTPASS") && std::string(getenv("PQRR_LUTPASS")) == "old";
-    static const bool uniform_env = getenv("PQRR_SAMPLING") && std::string(getenv("PQRR_SAMPLING")) == "uniform";
-    const int tiered = (!old_lut_env && !uniform_env && w >= 8 && lut_pass_supported(ix.d, ix.m, ix.ks)) ? 1 : 0;
+    const int tiered = (w >= 8 && lut_pass_supported(ix.d, ix.m, ix.ks)) ? 1 : 0;
     launch_query_sizes(probes, nq, w, ix.list_len.p, stride, tiered, cap, n_entries, sampled,
                        pair_samples, grand, s, R1);
     uint64_t* sample_off = ws.alloc<uint64_t>(P + 1);
@@ -917,16 +909,14 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         a.sample_dist = total_samples ? sample_dist : nullptr;
         a.tau = tau;  // unused in the LUT pass
         a.item_counter = counter;
-        static const bool old_lut = getenv("PQRR_LUTPASS") && std::string(getenv("PQRR_LUTPASS")) == "old";
-        if (!old_lut && lut_pass_supported(ix.d, ix.m, ix.ks)) launch_lut_pass(a, s);
+        if (lut_pass_supported(ix.d, ix.m, ix.ks)) launch_lut_pass(a, s);
         else launch_ivf_scan(a, s);
     }
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[3], s));
     launch_sample_threshold(sample_dist, sample_off, w, nq, sampled, (float)(alpha * kprime), stride,
                             tiered, (uint32_t)h_grand[1], tau, s);
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[4], s));
-    static const bool fma_bound_env = getenv("PQRR_FAR_BOUND") && std::string(getenv("PQRR_FAR_BOUND")) == "fma";
-    float* pair_bound = (two_phase && use_filter && !fma_bound_env && far_bound_supported(ix.d, ix.m, ix.ks))
+    float* pair_bound = (two_phase && use_filter && far_bound_supported(ix.d, ix.m, ix.ks))
                             ? ws.alloc<float>(P) : nullptr;
     if (two_phase && use_filter && im_far.n_items) {
         // far probes: bound pass (per-lane sum of minima), then the 8-bit
@@ -1019,35 +1009,6 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         PQRR_CUDA(cudaMemsetAsync(cand_mm, 0xff, 2 * nq * sizeof(uint32_t), s));
         launch_recheck(xq, ix.d, ix.m, ix.coarse.p, ix.books.p, probes, w, ix.codes.p, cand_cnt, cap,
                        cand_pos, cand_dist, tau, nq, cand_le, s, cand_mm);
-        static const char* dump = getenv("PQRR_DEBUG_DUMP");  // debug hook: raw filter state
-        if (dump && depth == 0) {
-            PQRR_CUDA(cudaStreamSynchronize(s));
-            auto put = [&](const char* name, const void* src, size_t bytes) {
-                std::vector<char> h(bytes);
-                if (bytes) PQRR_CUDA(cudaMemcpy(h.data(), src, bytes, cudaMemcpyDeviceToHost));
-                std::string path = std::string(dump) + "/" + name;
-                FILE* fp = fopen(path.c_str(), "wb");
-                if (fp) {
-                    fwrite(h.data(), 1, bytes, fp);
-                    fclose(fp);
-                }
-            };
-            put("tau.bin", tau, nq * 4);
-            put("probes.bin", probes, P * 4);
-            put("cand_cnt.bin", cand_cnt, nq * 4);
-            put("cand_le.bin", cand_le, nq * 4);
-            put("q8_param.bin", ix.q8_param.p, (size_t)n_items * kQT * 8);
-            put("q8_cache.bin", ix.q8_cache.p, (size_t)n_items * 8 * 256 * kQT);
-            // the LUT-pass items (the near set of a two-phase search)
-            const ItemSet& lp = two_phase ? im_near : im;
-            const size_t np_lp = two_phase ? nq * (size_t)R1 : P;
-            put("item_list.bin", lp.item_list, lp.n_items * 4);
-            put("item_start.bin", lp.item_start, lp.n_items * 4);
-            put("item_nq.bin", lp.item_nq, lp.n_items * 4);
-            put("pair_sorted.bin", lp.pair_sorted, np_lp * 4);
-            put("cand_pos.bin", cand_pos, nq * (size_t)cap * 4);
-            put("cand_dist.bin", cand_dist, nq * (size_t)cap * 4);
-        }
     } else {
         im.apply(a);
         a.pass = 0;

@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+for i in 1 2; do ./integration/build/test_shim > gpurun_out/r2j_shim$i.log 2>&1; echo "rc=$?" >> gpurun_out/r2j_shim$i.log; done
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/r2j_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r2j_tests.log
+timeout 900 python bench.py --config C2 --no-cpu-baseline --no-recall > gpurun_out/r2j_c2.json 2> gpurun_out/r2j_c2.err
+timeout 1200 python bench.py --config C4 --no-cpu-baseline --no-recall > gpurun_out/r2j_c4.json 2> gpurun_out/r2j_c4.err
+echo done
