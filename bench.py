@@ -164,7 +164,7 @@ def build_index(pq, cfg, coarse, P, rq, device, shard, nshards):
 
 
 # ---------------------------------------------------------------- reference arm
-REF_SAMPLE = {"C1": 1000, "C2": 1024, "C3": 64, "C4": 8, "C5": 8}
+REF_SAMPLE = {"C1": 1000, "C2": 1024, "C3": 64, "C4": 32, "C5": 32}
 
 
 class FileLists:

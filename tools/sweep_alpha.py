@@ -13,7 +13,7 @@ ap.add_argument("--grid", default="2.0:64,1.7:64,1.5:64,1.5:128,1.3:128,1.3:256"
 args = ap.parse_args()
 cfg = dict(bench.CONFIGS[args.config])
 coarse, P, rq = bench.train_codebooks(pq, cfg, 0)
-ix, _, _ = bench.build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
+ix, _, _, _ = bench.build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
 q = pq.synth(3, 0, cfg["nq"], cfg["clusters"], seed=bench.SEED)
 ref = None
 for g in args.grid.split(","):
