@@ -265,12 +265,11 @@ void launch_live_pairs(const FilterArgs& a, PairSet s0, PairSet s1, const uint32
 // K4r: exact ADC distance of every filter candidate (reference order), and
 // the per-query count of candidates at or below tau.
 bool recheck_supported(uint32_t d, uint32_t m, uint32_t w);
-// Returns true when cand_list (non-null) received every candidate's list id.
-bool launch_recheck(const float* xq, uint32_t d, uint32_t m, const float* coarse,
+void launch_recheck(const float* xq, uint32_t d, uint32_t m, const float* coarse,
                     const float* books, const uint32_t* probes, uint32_t w, const uint8_t* codes,
                     const uint32_t* cand_cnt, uint32_t cap, const uint32_t* cand_pos,
                     float* cand_dist, const float* tau, size_t nq, uint32_t* cand_le,
-                    cudaStream_t s, uint32_t* cand_mm = nullptr, uint16_t* cand_list = nullptr);
+                    cudaStream_t s, uint32_t* cand_mm = nullptr);
 
 // Build the scan work items from the probes.
 void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,
@@ -295,8 +294,7 @@ void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const 
                         uint32_t cap, uint32_t max_n, size_t nq, const uint32_t* ids,
                         uint32_t kprime, bool sorted, uint64_t* sl_key, uint32_t* sl_pos,
                         uint32_t* sl_cnt, cudaStream_t s,
-                        const uint32_t* cand_mm = nullptr, const uint16_t* cand_list = nullptr,
-                        uint16_t* sl_list = nullptr);
+                        const uint32_t* cand_mm = nullptr);
 // Re-rank the shortlist with the 3-term reconstruction, keep the k best.
 void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_t* sl_cnt,
                    uint32_t sl_stride, size_t nq, const float* xq, uint32_t d,
@@ -304,7 +302,7 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
                    const uint8_t* codes, const float* books, uint32_t m, const uint8_t* rcodes,
                    const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
                    uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s,
-                   cudaEvent_t ev_dist_done = nullptr, const uint16_t* sl_list = nullptr);
+                   cudaEvent_t ev_dist_done = nullptr);
 // Add-path coarse assignment on the tensor cores (k_assign_tc.cu): u8 rows,
 // d = 128, nc % 128 == 0; certified equal to launch_argmin's result.
 bool assign_tc_supported(uint32_t d, uint32_t nc);
@@ -330,7 +328,7 @@ void launch_rerank_pair(const uint64_t* sl_key, const uint32_t* sl_pos, const ui
                         uint32_t stride, size_t nq, const float* xq, const uint16_t* block_list,
                         const float* coarse, const uint8_t* codes, const float* books,
                         const uint8_t* rcodes, const float* rbooks, uint32_t mprime, float* rdist,
-                        uint32_t* rid, cudaStream_t s, const uint16_t* sl_list = nullptr);
+                        uint32_t* rid, cudaStream_t s);
 // Merge per-shard ranked lists into the top-k (K7).  Part p's rows are
 // ids/dists + p * ps (nq x width) and counts + p * cs (nq); ps = cs = 0 means
 // the stacked layout [parts][nq][width] + [parts][nq].
@@ -351,8 +349,7 @@ bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32
 void launch_select_warp(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
                         uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime,
                         uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s,
-                        const uint32_t* cand_mm = nullptr, const uint16_t* cand_list = nullptr,
-                        uint16_t* sl_list = nullptr);
+                        const uint32_t* cand_mm = nullptr);
 void launch_threshold_warp(const float* sample_dist, const uint64_t* sample_off, uint32_t w, size_t nq,
                            const uint8_t* query_sampled, float alpha_k, uint32_t stride, int tiered,
                            float* tau, cudaStream_t s);

@@ -414,8 +414,7 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
     const u64* __restrict__ codes, const uint32_t* __restrict__ cand_cnt, uint32_t cap,
     const uint32_t* __restrict__ cand_pos, float* __restrict__ cand_dist,
     const float* __restrict__ tau, size_t nq, uint32_t* __restrict__ cand_le,
-    uint32_t* __restrict__ counter, const u64 nz, uint32_t* __restrict__ cand_mm,
-    uint16_t* __restrict__ cand_list) {
+    uint32_t* __restrict__ counter, const u64 nz, uint32_t* __restrict__ cand_mm) {
     constexpr int CH = DSUB / 4;  // 16-byte chunks per subspace row
     extern __shared__ float4 smem_k[];
     float4* bk = smem_k;                      // [KS][M][CH]: code-major, chunks rotated
@@ -563,10 +562,6 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
                 const uint32_t i = base + j * 4 + slot;
                 if (i < n) {
                     cand_dist[q * cap + i] = acc;
-                    if (cand_list) {  // the candidate's list, carried into the shortlist for K5a
-                        const uint32_t rj = j == 0 ? rr[0] : j == 1 ? rr[1] : j == 2 ? rr[2] : rr[3];
-                        cand_list[q * cap + i] = (uint16_t)probes[q * w + rj];
-                    }
                     le += acc <= tq ? 1u : 0u;
                     dmn = min(dmn, __float_as_uint(acc));
                     dmx = max(dmx, __float_as_uint(acc));
@@ -718,7 +713,7 @@ template <int DSUB>
 bool recheck_smem_t(const float* xq, uint32_t d, const float* coarse, const float* books,
                     const uint32_t* probes, uint32_t w, const uint8_t* codes, const uint32_t* cand_cnt,
                     uint32_t cap, const uint32_t* cand_pos, float* cand_dist, const float* tau,
-                    size_t nq, uint32_t* cand_le, cudaStream_t s, uint32_t* cand_mm, uint16_t* cand_list) {
+                    size_t nq, uint32_t* cand_le, cudaStream_t s, uint32_t* cand_mm) {
     const size_t smem = (size_t)M * KS * DSUB * sizeof(float) + (size_t)w * d * sizeof(float);
     if (smem > 216 * 1024) return false;  // + ~9.3 KiB static (s_x) <= 227 KiB
     set_max_smem((const void*)recheck_smem_kernel<DSUB>, (size_t)((int)smem));
@@ -727,37 +722,36 @@ bool recheck_smem_t(const float* xq, uint32_t d, const float* coarse, const floa
     PQRR_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), s));
     recheck_smem_kernel<DSUB><<<sm_count(), 512, smem, s>>>(
         xq, d, coarse, books, probes, w, reinterpret_cast<const u64*>(codes), cand_cnt, cap, cand_pos,
-        cand_dist, tau, nq, cand_le, counter, kNegZero2, cand_mm, cand_list);
+        cand_dist, tau, nq, cand_le, counter, kNegZero2, cand_mm);
     PQRR_LAUNCH_CHECK();
     PQRR_CUDA(cudaFreeAsync(counter, s));
     count_launch();
     return true;
 }
 
-bool launch_recheck(const float* xq, uint32_t d, uint32_t m, const float* coarse,
+void launch_recheck(const float* xq, uint32_t d, uint32_t m, const float* coarse,
                     const float* books, const uint32_t* probes, uint32_t w, const uint8_t* codes,
                     const uint32_t* cand_cnt, uint32_t cap, const uint32_t* cand_pos,
                     float* cand_dist, const float* tau, size_t nq, uint32_t* cand_le,
-                    cudaStream_t s, uint32_t* cand_mm, uint16_t* cand_list) {
-    if (!nq) return false;
+                    cudaStream_t s, uint32_t* cand_mm) {
+    if (!nq) return;
     // shared-memory code book (the recheck kernels below stay for shapes or
     // residual sets it does not hold)
     if (d / m == 16 &&
         recheck_smem_t<16>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist,
-                           tau, nq, cand_le, s, cand_mm, cand_list))
-        return cand_list != nullptr;
+                           tau, nq, cand_le, s, cand_mm))
+        return;
     if (d / m == 8 &&
         recheck_smem_t<8>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist,
-                          tau, nq, cand_le, s, cand_mm, cand_list))
-        return cand_list != nullptr;
-    switch (d / m) {  // these variants do not record the list ids
-        case 16: recheck_t<16>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s); return false;
-        case 8: recheck_t<8>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s); return false;
-        case 4: recheck_t<4>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s); return false;
-        case 32: recheck_t<32>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s); return false;
+                          tau, nq, cand_le, s, cand_mm))
+        return;
+    switch (d / m) {
+        case 16: return recheck_t<16>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s);
+        case 8: return recheck_t<8>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s);
+        case 4: return recheck_t<4>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s);
+        case 32: return recheck_t<32>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist, tau, nq, cand_le, s);
         default: throw ArgError("recheck supports d/m in {4, 8, 16, 32}");
     }
-    return false;
 }
 
 }  // namespace pqrr_b200

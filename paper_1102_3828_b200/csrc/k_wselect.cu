@@ -339,8 +339,7 @@ __global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
     const float* __restrict__ cand_dist, const uint32_t* __restrict__ cand_pos,
     const uint32_t* __restrict__ cand_cnt, uint32_t cap, size_t nq, const uint32_t* __restrict__ ids,
     uint32_t kprime, u64* __restrict__ sl_key, uint32_t* __restrict__ sl_pos,
-    uint32_t* __restrict__ sl_cnt, const uint32_t* __restrict__ cand_mm,
-    const uint16_t* __restrict__ cand_list, uint16_t* __restrict__ sl_list) {
+    uint32_t* __restrict__ sl_cnt, const uint32_t* __restrict__ cand_mm) {
     __shared__ uint32_t hist_all[WS_WARPS][256];
     __shared__ u64 tie_all[WS_WARPS][TIE_CAP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -351,16 +350,12 @@ __global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
     const uint32_t* pq = cand_pos + q * cap;
     u64* ok = sl_key + q * kprime;
     uint32_t* op = sl_pos + q * kprime;
-    // the candidates' list ids travel with them when K4r recorded them
-    const uint16_t* lq = cand_list ? cand_list + q * cap : nullptr;
-    uint16_t* ol = sl_list ? sl_list + q * kprime : nullptr;
     const unsigned lt_mask = (1u << lane) - 1u;
     if (n <= kprime) {
         for (uint32_t i = lane; i < n; i += 32) {
             const uint32_t p = pq[i];
             ok[i] = ((u64)dq[i] << 32) | ids[p];
             op[i] = p;
-            if (ol) ol[i] = lq[i];
         }
         if (lane == 0) sl_cnt[q] = n;
         return;
@@ -397,11 +392,10 @@ __global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
                 const uint32_t o = n_out + __popc(mlt & lt_mask);
                 ok[o] = ((u64)u[k] << 32) | id[k];
                 op[o] = p[k];
-                if (ol) ol[o] = lq[base + k * 32 + lane];
             }
-            if (eq) {  // (id, candidate index): ties sort by id
+            if (eq) {
                 const uint32_t t = n_eq + __popc(meq & lt_mask);
-                if (t < TIE_CAP) tie[t] = ((u64)id[k] << 32) | (base + k * 32 + lane);
+                if (t < TIE_CAP) tie[t] = ((u64)id[k] << 32) | p[k];
             }
             n_out += __popc(mlt);
             n_eq += __popc(meq);
@@ -417,10 +411,8 @@ __global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
             warp_bitonic(tie, t2);
         }
         for (uint32_t t = lane; t < r_eq; t += 32) {
-            const uint32_t ci = (uint32_t)tie[t];
             ok[n_out + t] = ((u64)kth << 32) | (uint32_t)(tie[t] >> 32);
-            op[n_out + t] = pq[ci];
-            if (ol) ol[n_out + t] = lq[ci];
+            op[n_out + t] = (uint32_t)tie[t];
         }
     } else {
         // many ties (duplicate vectors): radix-select the r_eq-th smallest id
@@ -442,7 +434,6 @@ __global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
                 const uint32_t o = n_out + nt + __popc(m & lt_mask);
                 ok[o] = ((u64)kth << 32) | idd;
                 op[o] = pp;
-                if (ol) ol[o] = lq[i];
             }
             nt += __popc(m);
         }
@@ -674,11 +665,11 @@ bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32
 void launch_select_warp(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
                         uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime,
                         uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s,
-                        const uint32_t* cand_mm, const uint16_t* cand_list, uint16_t* sl_list) {
+                        const uint32_t* cand_mm) {
     if (nq == 0) return;
     select_warp_kernel<<<(unsigned)((nq + WS_WARPS - 1) / WS_WARPS), WS_WARPS * 32, 0, s>>>(
         cand_dist, cand_pos, cand_cnt, cap, nq, ids, kprime, reinterpret_cast<u64*>(sl_key), sl_pos,
-        sl_cnt, cand_mm, cand_list, sl_list);
+        sl_cnt, cand_mm);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

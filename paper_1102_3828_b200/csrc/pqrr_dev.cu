@@ -581,10 +581,6 @@ struct ShortlistDev {
     u64* key;
     uint32_t* pos;
     uint32_t* cnt;
-    // list id of every entry (K4r -> selection -> K5a), or null; *list_ok is
-    // cleared when some row's lists were not recorded (exact-scan path, retry)
-    uint16_t* list = nullptr;
-    bool* list_ok = nullptr;
 };
 
 // Work items of one pair set (see k_scan.cu): pairs (list, pair id = q*w+r)
@@ -959,7 +955,6 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     uint32_t* cand_cnt = ws.zeros<uint32_t>(nq);
     uint32_t* cand_le = nullptr;
     uint32_t* cand_mm = nullptr;
-    uint16_t* cand_list = nullptr;
     if (use_filter) {
         FilterArgs f{};
         f.codes = ix.codes.p;
@@ -1012,10 +1007,8 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         // exact distances' range per query (K4r smem variant; all-ones = unknown)
         cand_mm = ws.alloc<uint32_t>(2 * nq);
         PQRR_CUDA(cudaMemsetAsync(cand_mm, 0xff, 2 * nq * sizeof(uint32_t), s));
-        cand_list = out.list ? ws.alloc<uint16_t>(nq * (size_t)cap) : nullptr;
-        if (!launch_recheck(xq, ix.d, ix.m, ix.coarse.p, ix.books.p, probes, w, ix.codes.p, cand_cnt, cap,
-                            cand_pos, cand_dist, tau, nq, cand_le, s, cand_mm, cand_list))
-            cand_list = nullptr;
+        launch_recheck(xq, ix.d, ix.m, ix.coarse.p, ix.books.p, probes, w, ix.codes.p, cand_cnt, cap,
+                       cand_pos, cand_dist, tau, nq, cand_le, s, cand_mm);
     } else {
         im.apply(a);
         a.pass = 0;
@@ -1043,11 +1036,9 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // queue it before the readback so the GPU stays busy during the round
     // trip (rows that fail the check are redone and overwritten below)
     const bool early_select = !sorted;
-    if (out.list_ok && (!early_select || !cand_list)) *out.list_ok = false;
     if (early_select) {
         launch_select_topk(cand_dist, cand_pos, cand_cnt, cap, cap, nq, ix.ids.p, kprime, sorted,
-                           reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s, cand_mm, cand_list,
-                           cand_list ? out.list : nullptr);
+                           reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s, cand_mm);
         if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[6], s));
     }
     std::vector<uint8_t> h_fail(nq);
@@ -1105,7 +1096,6 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
             if (h_fail[q] == kind) rows.push_back((uint32_t)q);
         if (rows.empty()) continue;
         if (depth >= 8) throw std::runtime_error("shortlist threshold did not converge");
-        if (out.list_ok) *out.list_ok = false;  // the retried rows carry no list ids
         st.retries += (uint32_t)rows.size();
         Workspace ws2(s);
         uint32_t* d_rows = ws2.alloc<uint32_t>(rows.size());
@@ -1152,11 +1142,6 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
     Workspace ws(s);
     ShortlistDev sl{ws.alloc<u64>(nq * (size_t)kprime), ws.alloc<uint32_t>(nq * (size_t)kprime),
                     ws.alloc<uint32_t>(nq)};
-    bool lists_ok = k > 0;
-    if (k > 0) {
-        sl.list = ws.alloc<uint16_t>(nq * (size_t)kprime);
-        sl.list_ok = &lists_ok;
-    }
     // Large batches run in chunks sized to the free device memory: per query
     // the sampled distances (~2 w avg_len / stride floats: uniform sampling of
     // the k'-quantile needs many samples when k' << N_q), the 8-bit LUT blocks,
@@ -1182,8 +1167,7 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
         }
         for (size_t c0 = 0; c0 < nq; c0 += chunk) {
             const size_t nc = std::min(chunk, nq - c0);
-            ShortlistDev part{sl.key + c0 * kprime, sl.pos + c0 * kprime, sl.cnt + c0,
-                              sl.list ? sl.list + c0 * kprime : nullptr, sl.list_ok};
+            ShortlistDev part{sl.key + c0 * kprime, sl.pos + c0 * kprime, sl.cnt + c0};
             shortlist_core(ix, xq + c0 * ix.d, nc, w, kprime, k == 0, default_alpha(kprime, w), 1, part, 0, true);
         }
     }
@@ -1200,8 +1184,7 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
         PQRR_CUDA(cudaEventRecord(ix.ev[7], s));
         launch_rerank(reinterpret_cast<uint64_t*>(sl.key), sl.pos, sl.cnt, kprime, nq, xq, ix.d,
                       ix.block_list.p, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
-                      ix.rbooks.p, ix.mprime, ix.ks, k, out_ids, out_dists, out_cnt, s, ix.ev[12],
-                      lists_ok ? sl.list : nullptr);
+                      ix.rbooks.p, ix.mprime, ix.ks, k, out_ids, out_dists, out_cnt, s, ix.ev[12]);
     } else {
         PQRR_CUDA(cudaEventRecord(ix.ev[7], s));
         launch_unpack_keys(reinterpret_cast<uint64_t*>(sl.key), sl.cnt, nq, kprime, out_ids, out_dists, s);
