@@ -320,6 +320,8 @@ struct AssignTc {
     // one-time split of the centroids (false: keep the exact CUDA-core path)
     bool prepare(const float* coarse, uint32_t nc, cudaStream_t s);
     void assign(const uint8_t* y, size_t n, const float* coarse, uint32_t* out, cudaStream_t s);
+    // search side: D~ rows of n u8-valued f32 queries (+ per-row min / max keys)
+    void dtilde(const float* x, size_t n, float* Dt, uint32_t* kmm, cudaStream_t s);
 };
 // K5a on CTA pairs (k_rerank.cu): refined distance + id of every shortlist
 // entry (rows of `stride`, sl_cnt[q] valid) into rdist / rid.
@@ -339,9 +341,12 @@ void launch_merge_topk(const uint32_t* ids, const float* dists, const uint32_t* 
 // K1 on the tensor cores with certified exact top-w (k_coarse_tc.cu).
 bool coarse_tc_supported(uint32_t d, uint32_t w);
 void launch_coarse_norms(const float* c, uint32_t n, uint32_t d, float* out, cudaStream_t s);
+// atc (prepared, non-null) and u8-valued queries: D~ on tcgen05 (k_assign_tc.cu)
+// with the certification window 2^-13 (|x|^2 + max |c|^2); otherwise mma.sync TF32.
+struct AssignTc;
 void launch_coarse_tc(const float* x, size_t nq, const float* c, uint32_t nc, const float* cnorm,
                       float cnorm_max, uint32_t w, float* Dt, uint32_t* out_idx, uint32_t* overflow,
-                      cudaStream_t s);
+                      cudaStream_t s, AssignTc* atc = nullptr);
 // Warp-per-query selections (k_wselect.cu); the bool variants return false
 // outside their envelope (caller falls back to the CTA kernels).
 bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* out_idx,

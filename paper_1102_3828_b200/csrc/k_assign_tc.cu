@@ -310,6 +310,186 @@ __global__ void __launch_bounds__(AT_THREADS, 1) assign_tc_kernel(
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
 }
 
+// Search-side coarse distances on the same machinery: rows
+// are queries already widened to f32 whose components are u8 integers (exact
+// in fp16); the epilogue writes D~[q][c] = |x|^2 + |c|^2 - 2 <x, c>~ row-major
+// for the certified top-w selection (k_coarse_tc.cu) and the per-row minimum
+// and maximum as the certify kernel's order-preserving keys, so it skips its
+// first pass over the row.
+__device__ __forceinline__ uint32_t signed_key(float v) {
+    const uint32_t u = __float_as_uint(v);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
+    const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
+    const float* __restrict__ x, size_t n, const float* __restrict__ cnorm, uint32_t nc,
+    float* __restrict__ Dt, uint32_t* __restrict__ kmm) {
+    extern __shared__ uint8_t at_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>(((uintptr_t)at_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* As = sm;
+    uint8_t* Bs = sm + 2 * A_BYTES;
+    float* nx = reinterpret_cast<float*>(Bs + 2 * B_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(nx + 2 * AT_M);
+    const unsigned bar0 = su32(bars);
+    auto BAR = [&](int kind, int i) { return bar0 + 8u * (2 * kind + i); };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nblocks = nc / AT_N;
+    const size_t ntiles = (n + AT_M - 1) / AT_M;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            bar_init(BAR(0, i), 64);
+            bar_init(BAR(1, i), 1);
+            bar_init(BAR(2, i), 1);
+            bar_init(BAR(3, i), 1);
+            bar_init(BAR(4, i), 1);
+            bar_init(BAR(5, i), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&map_hi) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&map_lo) : "memory");
+            uint32_t g = 0;
+            for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+                for (uint32_t b = 0; b < nblocks; ++b, ++g) {
+                    const uint32_t st = g & 1u, use = g >> 1;
+                    if (use) bar_wait(BAR(3, st), (use - 1) & 1u);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(BAR(2, st)),
+                                 "r"(B_BYTES) : "memory");
+                    const unsigned dst = su32(Bs + st * B_BYTES);
+                    const int row = (int)(b * AT_N);
+                    tma_2d(dst, &map_hi, 0, row, BAR(2, st));
+                    tma_2d(dst + 16384, &map_hi, 64, row, BAR(2, st));
+                    tma_2d(dst + 32768, &map_lo, 0, row, BAR(2, st));
+                    tma_2d(dst + 49152, &map_lo, 64, row, BAR(2, st));
+                }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            uint32_t g = 0, i = 0;
+            for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+                const uint32_t a = i & 1u;
+                bar_wait(BAR(0, a), (i >> 1) & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const unsigned abase = su32(As + a * A_BYTES);
+                for (uint32_t b = 0; b < nblocks; ++b, ++g) {
+                    const uint32_t st = g & 1u, acc = g & 1u, use = g >> 1;
+                    bar_wait(BAR(2, st), use & 1u);
+                    if (use) bar_wait(BAR(5, acc), (use - 1) & 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const unsigned bbase = su32(Bs + st * B_BYTES);
+                    const unsigned d = tmem + acc * AT_N;
+#pragma unroll
+                    for (int kk = 0; kk < AT_D / 16; ++kk) {
+                        const unsigned off = (unsigned)(kk >> 2) * 16384u + (unsigned)(kk & 3) * 32u;
+                        const uint64_t ad = sw128_desc(abase + off);
+                        mma_f16(d, ad, sw128_desc(bbase + off), kk > 0 ? 1u : 0u);
+                        mma_f16(d, ad, sw128_desc(bbase + 32768u + off), 1u);
+                    }
+                    mma_commit(BAR(3, st));
+                    mma_commit(BAR(4, acc));
+                }
+                mma_commit(BAR(1, a));
+            }
+        }
+    } else if (warp < 4) {
+        const int cw = warp - 2;
+        uint32_t i = 0;
+        for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const uint32_t a = i & 1u;
+            if (i >= 2) bar_wait(BAR(1, a), ((i >> 1) - 1) & 1u);
+            uint8_t* A = As + a * A_BYTES;
+            for (int r = cw; r < AT_M; r += 2) {
+                const size_t row = t * AT_M + r;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (row < n) v = __ldg(reinterpret_cast<const float4*>(x + row * AT_D) + lane);
+                const int k = 4 * lane, h = k >> 6, ch = ((k & 63) >> 3) ^ (r & 7);
+                const __half2 lo = __floats2half2_rn(v.x, v.y);  // u8 integers: exact
+                const __half2 hi = __floats2half2_rn(v.z, v.w);
+                uint2 pk;
+                pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+                pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+                *reinterpret_cast<uint2*>(A + h * 16384 + (r >> 3) * 1024 + (r & 7) * 128 + ch * 16 + (k & 7) * 2) = pk;
+                float s2 = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, __fmaf_rn(v.z, v.z, v.w * v.w)));
+#pragma unroll
+                for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+                if (lane == 0) nx[a * AT_M + r] = s2;  // exact: integer sum < 2^24
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bar_arrive(BAR(0, a));
+        }
+    } else {
+        const int ew = warp - 4;
+        const int r = 32 * ew + lane;
+        const unsigned lane_off = (unsigned)(32 * ew) << 16;
+        uint32_t g = 0, i = 0;
+        for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const uint32_t a = i & 1u;
+            bar_wait(BAR(0, a), (i >> 1) & 1u);
+            const float xn = nx[a * AT_M + r];
+            const size_t row = t * AT_M + r;
+            const bool live = row < n;
+            float* out = Dt + (live ? row : 0) * (size_t)nc;
+            uint32_t kmin = 0xffffffffu, kmax = 0u;
+            for (uint32_t b = 0; b < nblocks; ++b, ++g) {
+                const uint32_t acc = g & 1u;
+                bar_wait(BAR(4, acc), (g >> 1) & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+                for (int c4 = 0; c4 < AT_N / 32; ++c4) {
+                    uint32_t u[32];
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+                          "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+                          "=r"(u[14]), "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]),
+                          "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]),
+                          "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+                        : "r"(tmem + lane_off + acc * AT_N + 32 * c4));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (c4 == AT_N / 32 - 1) {
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        bar_arrive(BAR(5, acc));
+                    }
+                    const uint32_t k0 = b * AT_N + 32 * c4;
+                    const float4* cn4 = reinterpret_cast<const float4*>(cnorm + k0);
+#pragma unroll
+                    for (int q4 = 0; q4 < 8; ++q4) {
+                        const float4 cn = __ldg(cn4 + q4);
+                        float4 dv;
+                        dv.x = __fmaf_rn(-2.f, __uint_as_float(u[4 * q4 + 0]), __fadd_rn(xn, cn.x));
+                        dv.y = __fmaf_rn(-2.f, __uint_as_float(u[4 * q4 + 1]), __fadd_rn(xn, cn.y));
+                        dv.z = __fmaf_rn(-2.f, __uint_as_float(u[4 * q4 + 2]), __fadd_rn(xn, cn.z));
+                        dv.w = __fmaf_rn(-2.f, __uint_as_float(u[4 * q4 + 3]), __fadd_rn(xn, cn.w));
+                        kmin = min(kmin, min(min(signed_key(dv.x), signed_key(dv.y)),
+                                             min(signed_key(dv.z), signed_key(dv.w))));
+                        kmax = max(kmax, max(max(signed_key(dv.x), signed_key(dv.y)),
+                                             max(signed_key(dv.z), signed_key(dv.w))));
+                        if (live) __stcs(reinterpret_cast<float4*>(out + k0) + q4, dv);
+                    }
+                }
+            }
+            if (live) reinterpret_cast<uint2*>(kmm)[row] = make_uint2(kmin, kmax);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
 // Rows whose certification window held 4+ centroids: exact argmin, one warp
 // per row, strict < in ascending index (kernels.cpp:29-35).
 __global__ void assign_overflow_kernel(const uint8_t* __restrict__ y, const float* __restrict__ coarse,
@@ -386,6 +566,18 @@ CUtensorMap make_map(const __half* base, uint32_t rows) {
 }  // namespace
 
 bool assign_tc_supported(uint32_t d, uint32_t nc) { return d == AT_D && nc >= AT_N && nc % AT_N == 0; }
+
+void AssignTc::dtilde(const float* x, size_t n, float* Dt, uint32_t* kmm, cudaStream_t s) {
+    if (n == 0) return;
+    const CUtensorMap mh = make_map(static_cast<const __half*>(hi), nc);
+    const CUtensorMap ml = make_map(static_cast<const __half*>(lo), nc);
+    set_max_smem((const void*)dtilde_tc_kernel, SMEM_BYTES);
+    const size_t ntiles = (n + AT_M - 1) / AT_M;
+    const unsigned grid = (unsigned)std::min<size_t>(ntiles, (size_t)sm_count());
+    dtilde_tc_kernel<<<grid, AT_THREADS, SMEM_BYTES, s>>>(mh, ml, x, n, cn, nc, Dt, kmm);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+}
 
 AssignTc::~AssignTc() {
     if (hi) cudaFree(hi);

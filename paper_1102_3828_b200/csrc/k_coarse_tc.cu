@@ -165,7 +165,7 @@ __device__ __forceinline__ void wbitonic(u64* keys, uint32_t n2) {
 __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
     const float* __restrict__ Dt, size_t nq, uint32_t nc, uint32_t w, const float* __restrict__ x,
     const float* __restrict__ c, float cnorm_max, uint32_t* __restrict__ out_idx,
-    uint32_t* __restrict__ overflow, const u64 nz) {
+    uint32_t* __restrict__ overflow, const u64 nz, const uint32_t* __restrict__ kmm, float dscale_tc) {
     constexpr int D = 128;
     __shared__ uint32_t hist_all[CW][256];
     __shared__ __align__(16) u64 cand_all[CW][CCAP];
@@ -184,9 +184,13 @@ __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
         const uint32_t u = __ldg(row + i);
         return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
     };
-    // ---- pass 1: min / max of the keys
+    // ---- pass 1: min / max of the keys (given by the tcgen05 epilogue when kmm)
     uint32_t kmin = 0xffffffffu, kmax = 0u;
-    for (uint32_t base = 0; base < nc; base += 32 * U) {
+    if (kmm) {
+        kmin = kmm[2 * q];
+        kmax = kmm[2 * q + 1];
+    }
+    for (uint32_t base = 0; !kmm && base < nc; base += 32 * U) {
         uint32_t v[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
@@ -284,7 +288,9 @@ __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
     // 2^-10 when the query is exact in TF32 (u8 queries); 2^-9 when its
     // components round too (float queries through pqrr_dev_search_f32); + 1%
     // slack for this sum and an absolute floor for underflowing products
-    const float dscale = __all_sync(0xffffffffu, tf32_exact) ? 9.765625e-04f : 1.953125e-03f;
+    // (the tcgen05 path passes its own, 2^-13: fp16 hi/lo centroid split)
+    const float dscale = dscale_tc > 0.f ? dscale_tc
+                                         : (__all_sync(0xffffffffu, tf32_exact) ? 9.765625e-04f : 1.953125e-03f);
     const float delta_max = dscale * (nx + cnorm_max) * 1.01f + 0x1p-100f;
     const float bound = __uint_as_float(tu) + 2.f * delta_max;
     // ---- pass 3: candidates D~ <= bound (index order)
@@ -351,8 +357,21 @@ void launch_coarse_norms(const float* c, uint32_t n, uint32_t d, float* out, cud
 
 void launch_coarse_tc(const float* x, size_t nq, const float* c, uint32_t nc, const float* cnorm,
                       float cnorm_max, uint32_t w, float* Dt, uint32_t* out_idx, uint32_t* overflow,
-                      cudaStream_t s) {
+                      cudaStream_t s, AssignTc* atc) {
     if (!nq) return;
+    if (atc) {
+        // D~ on the 5th-generation tensor cores; the window shrinks from
+        // 2^-10 to 2^-13 (|x|^2 + max |c|^2), the min / max pass is folded in
+        uint32_t* kmm = nullptr;
+        PQRR_CUDA(cudaMallocAsync(&kmm, nq * 2 * sizeof(uint32_t), s));
+        atc->dtilde(x, nq, Dt, kmm, s);
+        topw_certify_kernel<<<(unsigned)((nq + CW - 1) / CW), CW * 32, 0, s>>>(
+            Dt, nq, nc, w, x, c, atc->cmax, out_idx, overflow, kNegZero2, kmm, 0x1p-13f);
+        PQRR_LAUNCH_CHECK();
+        count_launch();
+        PQRR_CUDA(cudaFreeAsync(kmm, s));
+        return;
+    }
     const size_t smem = (size_t)(GM + GN) * GLD * sizeof(float);
     static bool attr = false;
     if (!attr) {
@@ -363,7 +382,8 @@ void launch_coarse_tc(const float* x, size_t nq, const float* c, uint32_t nc, co
     coarse_gemm_kernel<<<grid, GW * 32, smem, s>>>(x, nq, c, nc, cnorm, Dt);
     PQRR_LAUNCH_CHECK();
     topw_certify_kernel<<<(unsigned)((nq + CW - 1) / CW), CW * 32, 0, s>>>(Dt, nq, nc, w, x, c, cnorm_max,
-                                                                           out_idx, overflow, kNegZero2);
+                                                                           out_idx, overflow, kNegZero2,
+                                                                           nullptr, 0.f);
     PQRR_LAUNCH_CHECK();
     count_launch(2);
 }

@@ -407,6 +407,14 @@ __global__ __launch_bounds__(256) void recheck_kernel(
 // at ~2 wavefronts.  Each lane computes l2_sq(residual_j, B_j[c_j]) in the
 // reference order; the 8 values are gathered by shuffles and summed
 // j-ascending — the same fp32 operations as the exact scan's LUT + ADC.
+// A survivor's 8 code bytes: a random sector never reused on this SM, read
+// without allocating in L1.
+__device__ __forceinline__ u64 ld_code_na(const u64* p) {
+    u64 v;
+    asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+
 template <int DSUB>
 __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
     const float* __restrict__ xq, uint32_t d, const float* __restrict__ coarse,
@@ -500,7 +508,7 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
         u64 ncode[U];
         fetch(warp * 4 * U);
 #pragma unroll
-        for (int u = 0; u < U; ++u) ncode[u] = __ldg(codes + npos[u]);
+        for (int u = 0; u < U; ++u) ncode[u] = ld_code_na(codes + npos[u]);
         uint32_t cpos_r[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) cpos_r[u] = nr[u];
@@ -516,7 +524,7 @@ __global__ __launch_bounds__(512, 1) void recheck_smem_kernel(
             if (base + STEP < n) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    ncode[u] = __ldg(codes + npos[u]);
+                    ncode[u] = ld_code_na(codes + npos[u]);
                     cpos_r[u] = nr[u];
                 }
                 if (base + 2 * STEP < n) fetch(base + 2 * STEP);

@@ -67,6 +67,30 @@ __device__ __forceinline__ void wait_parity(unsigned a, unsigned parity) {
             "selp.u32 %0, 1, 0, p; }"
             : "=r"(done) : "r"(a), "r"(parity) : "memory");
 }
+// Random gathers with no L1 allocation: a candidate's sectors are never
+// reused on this SM (the sibling CTA reads the other half), so they would only
+// evict the coarse rows and queries L1 does reuse.
+__device__ __forceinline__ uint32_t ld_na_u32(const void* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_na_u16(const void* p) {
+    unsigned short v;
+    asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_na_v2(const void* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_na_v4(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -165,17 +189,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
         const size_t t0 = (c / cpq) * stride + (uint32_t)(c % cpq) * 32;
         if ((uint32_t)lane < nb) {
             if (r) p_id = key_id(sl_key[t0 + lane]);
-            p_list = block_list[pos >> 4];
-            p_code = *reinterpret_cast<const uint32_t*>(codes + (size_t)pos * 8 + 4 * r);
+            p_list = ld_na_u16(block_list + (pos >> 4));
+            p_code = ld_na_u32(codes + (size_t)pos * 8 + 4 * r);
             const uint8_t* rs = rcodes + (size_t)pos * MP + r * HB;
             if constexpr (HB == 16) {
-                const uint4 v = *reinterpret_cast<const uint4*>(rs);
+                const uint4 v = ld_na_v4(rs);
                 p_rc[0] = v.x, p_rc[1] = v.y, p_rc[2] = v.z, p_rc[3] = v.w;
             } else if constexpr (HB == 8) {
-                const uint2 v = *reinterpret_cast<const uint2*>(rs);
+                const uint2 v = ld_na_v2(rs);
                 p_rc[0] = v.x, p_rc[1] = v.y;
             } else {
-                p_rc[0] = *reinterpret_cast<const uint32_t*>(rs);
+                p_rc[0] = ld_na_u32(rs);
             }
         }
     };

@@ -364,7 +364,8 @@ struct DevIndex {
     DBuf<uint16_t> block_list;  // list of each 16-entry block of positions
     DBuf<float> cnorm;          // |C_l|^2 (tensor-core K1), cnorm_max their maximum
     float cnorm_max = 0.f;
-    AssignTc atc;               // tensor-core add-path assignment (u8 rows)
+    AssignTc atc;               // tcgen05 coarse distances (add path; u8 queries)
+    bool q_u8 = false;          // the search in flight has u8-valued queries
     DBuf<uint8_t> q8_cache;     // per LUT-pass item 8-bit LUT (32 KiB) for the K4f filter
     DBuf<float> q8_param;       // per LUT-pass item and query lane: (scale, sum of minima)
     uint64_t next_id = 0;
@@ -775,7 +776,11 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
             PQRR_CUDA(cudaStreamSynchronize(s));
             ix.cnorm_max = *std::max_element(h.begin(), h.end());
         }
-        launch_coarse_tc(xq, nq, ix.coarse.p, c, ix.cnorm.p, ix.cnorm_max, w, D, probes, coarse_ovf, s);
+        // u8 queries (exact in fp16): D~ on tcgen05 with the add path's
+        // centroid split; float queries: mma.sync TF32
+        AssignTc* atc = (ix.q_u8 && assign_tc_supported(ix.d, c) && ix.atc.prepare(ix.coarse.p, c, s))
+                            ? &ix.atc : nullptr;
+        launch_coarse_tc(xq, nq, ix.coarse.p, c, ix.cnorm.p, ix.cnorm_max, w, D, probes, coarse_ovf, s, atc);
     } else {
         launch_pair_dists(xq, nq, ix.coarse.p, c, ix.d, D, s);
         launch_topw(D, nq, c, w, probes, nullptr, s);
@@ -1653,7 +1658,9 @@ static int search_host(pqrr_dev_index* h, const float* qf, const uint8_t* qu, si
         uint32_t* oi = ws.alloc<uint32_t>(nq * width);
         float* od = ws.alloc<float>(nq * width);
         uint32_t* oc = ws.alloc<uint32_t>(nq);
+        ix.q_u8 = qf == nullptr;
         search_device(ix, xq, nq, w, kprime, k, oi, od, oc);
+        ix.q_u8 = false;
         PQRR_CUDA(cudaMemcpyAsync(out_ids, oi, nq * width * 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaMemcpyAsync(out_dists, od, nq * width * 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaMemcpyAsync(out_counts, oc, nq * 4, cudaMemcpyDeviceToHost, s));
@@ -1696,7 +1703,9 @@ int pqrr_dev_search_u8_device(pqrr_dev_index* h, const uint8_t* d_queries, size_
         Workspace ws(s);
         float* xq = ws.alloc<float>(nq * ix.d);
         launch_widen_u8(d_queries, xq, nq * ix.d, s);
+        ix.q_u8 = true;
         search_device(ix, xq, nq, w, kprime, k, d_out_ids, d_out_dists, d_out_counts);
+        ix.q_u8 = false;
         stream_join(s, user);
     });
 }
