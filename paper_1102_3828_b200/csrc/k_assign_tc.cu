@@ -324,7 +324,7 @@ __device__ __forceinline__ uint32_t signed_key(float v) {
 __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
     const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
     const float* __restrict__ x, size_t n, const float* __restrict__ cnorm, uint32_t nc,
-    float* __restrict__ Dt, uint32_t* __restrict__ kmm) {
+    float* __restrict__ Dt, uint32_t* __restrict__ kmm, uint32_t nsplit) {
     extern __shared__ uint8_t at_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>(((uintptr_t)at_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* As = sm;
@@ -335,8 +335,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
     auto BAR = [&](int kind, int i) { return bar0 + 8u * (2 * kind + i); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t nblocks = nc / AT_N;
+    // work unit = (128-query tile, a 1/nsplit range of the centroid blocks):
+    // small batches spread one tile's centroids over several SMs
+    const uint32_t nblocks_all = nc / AT_N;
     const size_t ntiles = (n + AT_M - 1) / AT_M;
+    const size_t nunits = ntiles * nsplit;
+    auto unit = [&](size_t u, size_t& t, uint32_t& b0, uint32_t& b1) {
+        t = u / nsplit;
+        const uint32_t sp = (uint32_t)(u % nsplit);
+        b0 = (uint32_t)((uint64_t)nblocks_all * sp / nsplit);
+        b1 = (uint32_t)((uint64_t)nblocks_all * (sp + 1) / nsplit);
+    };
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             bar_init(BAR(0, i), 64);
@@ -363,8 +372,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
             asm volatile("prefetch.tensormap [%0];" ::"l"(&map_hi) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(&map_lo) : "memory");
             uint32_t g = 0;
-            for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-                for (uint32_t b = 0; b < nblocks; ++b, ++g) {
+            for (size_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+                size_t t;
+                uint32_t bb0, bb1;
+                unit(u, t, bb0, bb1);
+                for (uint32_t b = bb0; b < bb1; ++b, ++g) {
                     const uint32_t st = g & 1u, use = g >> 1;
                     if (use) bar_wait(BAR(3, st), (use - 1) & 1u);
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(BAR(2, st)),
@@ -376,16 +388,20 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
                     tma_2d(dst + 32768, &map_lo, 0, row, BAR(2, st));
                     tma_2d(dst + 49152, &map_lo, 64, row, BAR(2, st));
                 }
+            }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             uint32_t g = 0, i = 0;
-            for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            for (size_t u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+                size_t t;
+                uint32_t bb0, bb1;
+                unit(u, t, bb0, bb1);
                 const uint32_t a = i & 1u;
                 bar_wait(BAR(0, a), (i >> 1) & 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const unsigned abase = su32(As + a * A_BYTES);
-                for (uint32_t b = 0; b < nblocks; ++b, ++g) {
+                for (uint32_t b = bb0; b < bb1; ++b, ++g) {
                     const uint32_t st = g & 1u, acc = g & 1u, use = g >> 1;
                     bar_wait(BAR(2, st), use & 1u);
                     if (use) bar_wait(BAR(5, acc), (use - 1) & 1u);
@@ -408,7 +424,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
     } else if (warp < 4) {
         const int cw = warp - 2;
         uint32_t i = 0;
-        for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        for (size_t u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+            const size_t t = u / nsplit;
             const uint32_t a = i & 1u;
             if (i >= 2) bar_wait(BAR(1, a), ((i >> 1) - 1) & 1u);
             uint8_t* A = As + a * A_BYTES;
@@ -436,7 +453,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
         const int r = 32 * ew + lane;
         const unsigned lane_off = (unsigned)(32 * ew) << 16;
         uint32_t g = 0, i = 0;
-        for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        for (size_t u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+            size_t t;
+            uint32_t bb0, bb1;
+            unit(u, t, bb0, bb1);
             const uint32_t a = i & 1u;
             bar_wait(BAR(0, a), (i >> 1) & 1u);
             const float xn = nx[a * AT_M + r];
@@ -444,7 +464,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
             const bool live = row < n;
             float* out = Dt + (live ? row : 0) * (size_t)nc;
             uint32_t kmin = 0xffffffffu, kmax = 0u;
-            for (uint32_t b = 0; b < nblocks; ++b, ++g) {
+            for (uint32_t b = bb0; b < bb1; ++b, ++g) {
                 const uint32_t acc = g & 1u;
                 bar_wait(BAR(4, acc), (g >> 1) & 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -483,7 +503,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
                     }
                 }
             }
-            if (live) reinterpret_cast<uint2*>(kmm)[row] = make_uint2(kmin, kmax);
+            if (live) {  // kmm = [min keys n][max keys n], combined over the splits
+                if (nsplit == 1) {
+                    kmm[row] = kmin;
+                    kmm[n + row] = kmax;
+                } else {
+                    atomicMin(kmm + row, kmin);
+                    atomicMax(kmm + n + row, kmax);
+                }
+            }
         }
     }
     __syncthreads();
@@ -573,8 +601,15 @@ void AssignTc::dtilde(const float* x, size_t n, float* Dt, uint32_t* kmm, cudaSt
     const CUtensorMap ml = make_map(static_cast<const __half*>(lo), nc);
     set_max_smem((const void*)dtilde_tc_kernel, SMEM_BYTES);
     const size_t ntiles = (n + AT_M - 1) / AT_M;
-    const unsigned grid = (unsigned)std::min<size_t>(ntiles, (size_t)sm_count());
-    dtilde_tc_kernel<<<grid, AT_THREADS, SMEM_BYTES, s>>>(mh, ml, x, n, cn, nc, Dt, kmm);
+    const uint32_t nblocks = nc / AT_N, sms = (uint32_t)sm_count();
+    // fewer tiles than SMs: split each tile's centroid blocks over the idle SMs
+    const uint32_t nsplit = ntiles >= sms ? 1u : std::min<uint32_t>(nblocks, (uint32_t)(sms / ntiles));
+    if (nsplit > 1) {
+        PQRR_CUDA(cudaMemsetAsync(kmm, 0xff, n * sizeof(uint32_t), s));
+        PQRR_CUDA(cudaMemsetAsync(kmm + n, 0, n * sizeof(uint32_t), s));
+    }
+    const unsigned grid = (unsigned)std::min<size_t>(ntiles * nsplit, (size_t)sms);
+    dtilde_tc_kernel<<<grid, AT_THREADS, SMEM_BYTES, s>>>(mh, ml, x, n, cn, nc, Dt, kmm, nsplit);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

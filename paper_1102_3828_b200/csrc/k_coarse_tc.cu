@@ -186,9 +186,9 @@ __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
     };
     // ---- pass 1: min / max of the keys (given by the tcgen05 epilogue when kmm)
     uint32_t kmin = 0xffffffffu, kmax = 0u;
-    if (kmm) {
-        kmin = kmm[2 * q];
-        kmax = kmm[2 * q + 1];
+    if (kmm) {  // [min keys nq][max keys nq]
+        kmin = kmm[q];
+        kmax = kmm[nq + q];
     }
     for (uint32_t base = 0; !kmm && base < nc; base += 32 * U) {
         uint32_t v[U];
