@@ -8,9 +8,10 @@
 // LUT (98,304 FP32 operations) need not be built.  This kernel bounds m_j
 // from below without building it:
 //     L~_jc = |r_j|^2 + |B_jc|^2 - 2 <r_j, B_jc>,
-// the dot products on the tensor cores (mma.sync m16n8k8 TF32, fp32
-// accumulation: 16 pairs x 8 codes x 16 dims per sub-space and code tile).
-// Both operands round to TF32 (relative 2^-11 each); with
+// the dot products on the 5th-generation tensor cores (tcgen05.mma kind::f16,
+// fp32 accumulation in TMEM: 128 pairs x 256 codes x the 16 dims of a
+// sub-space per instruction).  Both operands round to fp16 (relative 2^-11
+// each, like TF32 with round-to-nearest); with
 // sum_t |r_t b_t| <= (|r_j|^2 + |B_jc|^2) / 2 every error term of L~ (operand
 // rounding, fp32 accumulation, the norms, the epilogue) and of the reference's
 // own fp32 l2_sq (< 40 u) is below 2^-9 (|r_j|^2 + |B_jc|^2) (the bound used
@@ -20,7 +21,10 @@
 // A pair with bound > tau is dead; the others get the exact LUT pass, whose
 // sum of minima then decides exactly.  The bound only selects work: the
 // exact path decides every result.
+#include <cuda_fp16.h>
 #include <float.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "internal.h"
@@ -28,128 +32,232 @@
 namespace pqrr_b200 {
 namespace {
 
-constexpr int BW = 8;      // warps per CTA: one 16-pair tile each
-constexpr int RLD = 144;   // residual tile row stride (floats): conflict-free fragment loads
 constexpr int M = 8, KS = 256, DS = 16, D = 128;
+constexpr int TM = 128;                  // far pairs per tile (TMEM lanes)
+constexpr int FB_THREADS = 256;          // warp 0 book / setup, 1 MMA, 2-3 residuals, 4-7 epilogue
+constexpr uint32_t A_BYTES = TM * D * 2;     // 32 KiB: residual rows, fp16, K-major 128-byte swizzle
+constexpr uint32_t B_BYTES = KS * D * 2;     // 64 KiB: the code-major book [code][128 dims], fp16
+constexpr uint32_t SMEM_BYTES = 1024 + 2 * A_BYTES + B_BYTES + M * KS * 4 + 2 * TM * M * 4 + 16 * 8 + 16;
 
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(unsigned a, unsigned n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
 }
-__device__ __forceinline__ void mma_tf32(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
+__device__ __forceinline__ void bar_arrive(unsigned a) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void bar_wait(unsigned a, unsigned parity) {
+    unsigned done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(done) : "r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ uint64_t sw128_desc(unsigned addr) {
+    return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// kind::f16, D f32, A / B f16 K-major, M = 128, N = 256
+constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(KS >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+__device__ __forceinline__ void mma_f16(unsigned dtmem, uint64_t ad, uint64_t bd) {
     asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+        "{ .reg .pred p; setp.ne.b32 p, 0, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
+        ::"r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc));
+}
+__device__ __forceinline__ void mma_commit(unsigned bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+// byte offset of element (row, k) in a K-major, 128-byte-swizzled fp16 tile
+// of `rows` rows (two K halves of rows x 64 elements)
+__device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t k, uint32_t rows) {
+    return (k >> 6) * rows * 128 + (row >> 3) * 1024 + (row & 7) * 128 + ((((k & 63) >> 3) ^ (row & 7)) << 4) +
+           (k & 7) * 2;
 }
 
-// Lane (g, tig) of a k-step pair (the 16 dims of a sub-space) carries dims
-// 4 tig .. 4 tig + 3 of its A row and B column: k-step 0 puts dim 4 tig at
-// k = tig and 4 tig + 2 at k = tig + 4, k-step 1 dims 4 tig + 1 and 4 tig + 3
-// — the same permutation for A and B, so the dot products are unchanged and
-// each operand is one LDS.128.
-__global__ __launch_bounds__(BW * 32, 1) void far_bound_kernel(
+// Far-pair bound on the 5th-generation tensor cores.  Rows = 128 far pairs,
+// K = the 16 dims of one sub-space, N = the 256 codes: sub-space j is ONE
+// tcgen05.mma (M = 128, N = 256, K = 16) of the residual tile against the
+// code-major book at K step j, into one of two TMEM accumulators (256 columns
+// each), so the epilogue of sub-space j overlaps the MMA of j + 1.  Operands
+// round to fp16 (relative 2^-11 each, as TF32 with round-to-nearest; plus an
+// absolute 2^-25 per subnormal element, covered by subtracting 2^-10); the
+// bound arithmetic is the mma.sync version's:
+//     lb_jc = (|r_j|^2 + |B_jc|^2)(1 - 2^-8) - 2 <r_j, B_jc>~ - 2^-10,
+//     bound = sum_j max(0, min_c lb_jc), summed rounding down, x (1 - 2^-16).
+__global__ void __launch_bounds__(FB_THREADS, 1) far_bound_tc_kernel(
     const float* __restrict__ xq, const float* __restrict__ coarse, const float* __restrict__ books,
-    const uint32_t* __restrict__ probes, size_t nq, uint32_t w, uint32_t R1,
-    float* __restrict__ pair_bound) {
-    extern __shared__ float4 bsm[];
-    uint4* bk = reinterpret_cast<uint4*>(bsm);                          // [M][KS][4] tf32 bits
-    float* bn2 = reinterpret_cast<float*>(bsm + M * KS * 4);            // [M][KS] |B_jc|^2 (1 - 2^-8)
-    float* tiles = bn2 + M * KS;                                        // [BW][16][RLD]
-    float* rn2s = tiles + BW * 16 * RLD;                                // [BW][16][M]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t* __restrict__ probes, size_t nq, uint32_t w, uint32_t R1, float* __restrict__ pair_bound) {
+    extern __shared__ uint8_t fb_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>(((uintptr_t)fb_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* As = sm;                                                  // [2][A_BYTES]
+    uint8_t* Bs = sm + 2 * A_BYTES;                                    // [B_BYTES]
+    float* bn2 = reinterpret_cast<float*>(Bs + B_BYTES);               // [M][KS] |B_jc|^2 (1 - 2^-8)
+    float* rn2 = bn2 + M * KS;                                         // [2][TM][M] |r_j|^2 (1 - 2^-8)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rn2 + 2 * TM * M);  // a_full[2] a_empty[2] t_full[2] t_empty[2]
+    const unsigned bar0 = su32(bars);
+    auto BAR = [&](int kind, int i) { return bar0 + 8u * (2 * kind + i); };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float shrink = 0.99609375f;  // 1 - 2^-8
-    for (uint32_t i = threadIdx.x; i < M * KS * 4; i += blockDim.x) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(books) + i);
-        bk[i] = make_uint4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
+    const uint32_t wf = w - R1;
+    const size_t nfar = nq * (size_t)wf;
+    const size_t ntiles = (nfar + TM - 1) / TM;
+
+    // the code-major book (fp16, swizzled) and |B_jc|^2, once per CTA
+    for (uint32_t i = threadIdx.x; i < (uint32_t)(KS * D / 4); i += blockDim.x) {
+        const uint32_t c = i / (D / 4), k = 4 * (i % (D / 4)), j = k / DS;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(books + ((size_t)j * KS + c) * DS + (k % DS)));
+        const __half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(Bs + sw128_off(c, k, KS)) = pk;
     }
     for (uint32_t rc = threadIdx.x; rc < M * KS; rc += blockDim.x) {
         const float* b = books + (size_t)rc * DS;
-        float s = 0.f;
+        float s2 = 0.f;
 #pragma unroll
-        for (int t = 0; t < DS; ++t) s = __fmaf_rn(b[t], b[t], s);
-        bn2[rc] = __fmul_rn(s, shrink);
+        for (int t = 0; t < DS; ++t) s2 = __fmaf_rn(b[t], b[t], s2);
+        bn2[rc] = __fmul_rn(s2, shrink);
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            bar_init(BAR(0, i), 64);   // a_full: the residual warps
+            bar_init(BAR(1, i), 1);    // a_empty: MMA commit
+            bar_init(BAR(2, i), 1);    // t_full: MMA commit
+            bar_init(BAR(3, i), 128);  // t_empty: epilogue threads
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
 
-    const uint32_t wf = w - R1;
-    const size_t nfar = nq * (size_t)wf;
-    const size_t ntiles = (nfar + 15) / 16;
-    float* tile = tiles + warp * 16 * RLD;
-    float* rn2 = rn2s + warp * 16 * M;
-    const int g = lane >> 2, tig = lane & 3;
-    for (size_t tl = (size_t)blockIdx.x * BW + warp; tl < ntiles; tl += (size_t)gridDim.x * BW) {
-        // residuals r = x - C_l of the tile's 16 far pairs (rows past the end: 0)
-        for (int i = lane; i < 16 * (D / 4); i += 32) {
-            const int row = i / (D / 4), c4 = i % (D / 4);
-            const size_t k = tl * 16 + row;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (k < nfar) {
-                const size_t q = k / wf;
-                const uint32_t l = probes[q * w + R1 + (uint32_t)(k % wf)];
-                const float4 x = __ldg(reinterpret_cast<const float4*>(xq + q * D) + c4);
-                const float4 cc = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + c4);
-                v = make_float4(__fsub_rn(x.x, cc.x), __fsub_rn(x.y, cc.y), __fsub_rn(x.z, cc.z),
-                                __fsub_rn(x.w, cc.w));
+    if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            uint32_t g = 0, i = 0;
+            const unsigned bbase = su32(Bs);
+            for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+                const uint32_t a = i & 1u;
+                bar_wait(BAR(0, a), (i >> 1) & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const unsigned abase = su32(As + a * A_BYTES);
+                for (int j = 0; j < M; ++j, ++g) {
+                    const uint32_t acc = g & 1u, use = g >> 1;
+                    if (use) bar_wait(BAR(3, acc), (use - 1) & 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const unsigned ka = (unsigned)(j >> 2) * (TM * 128) + (unsigned)(j & 3) * 32u;
+                    const unsigned kb = (unsigned)(j >> 2) * (KS * 128) + (unsigned)(j & 3) * 32u;
+                    mma_f16(tmem + acc * KS, sw128_desc(abase + ka), sw128_desc(bbase + kb));
+                    mma_commit(BAR(2, acc));
+                }
+                mma_commit(BAR(1, a));
             }
-            *reinterpret_cast<float4*>(tile + row * RLD + 4 * c4) = v;
         }
-        __syncwarp();
-        // |r_j|^2 (1 - 2^-8) per (pair, sub-space)
-        for (int i = lane; i < 16 * M; i += 32) {
-            const int row = i / M, j = i % M;
-            const float* r = tile + row * RLD + j * DS;
-            float s = 0.f;
-#pragma unroll
-            for (int t = 0; t < DS; ++t) s = __fmaf_rn(r[t], r[t], s);
-            rn2[row * M + j] = __fmul_rn(s, shrink);
-        }
-        __syncwarp();
-        float sum0 = 0.f, sum1 = 0.f;  // rows g and g + 8
-#pragma unroll 1
-        for (int j = 0; j < M; ++j) {
-            const float4 ra = *reinterpret_cast<const float4*>(tile + g * RLD + j * DS + 4 * tig);
-            const float4 rb = *reinterpret_cast<const float4*>(tile + (g + 8) * RLD + j * DS + 4 * tig);
-            const uint32_t a00 = to_tf32(ra.x), a01 = to_tf32(rb.x), a02 = to_tf32(ra.z), a03 = to_tf32(rb.z);
-            const uint32_t a10 = to_tf32(ra.y), a11 = to_tf32(rb.y), a12 = to_tf32(ra.w), a13 = to_tf32(rb.w);
-            const float r0 = rn2[g * M + j], r1 = rn2[(g + 8) * M + j];
-            float mn0 = FLT_MAX, mn1 = FLT_MAX;
-#pragma unroll 4
-            for (int nt = 0; nt < KS / 8; ++nt) {
-                const uint4 bv = bk[(j * KS + nt * 8 + g) * 4 + tig];
-                float c[4] = {0.f, 0.f, 0.f, 0.f};
-                // k-step 0: dims 4 tig + {0, 2}; k-step 1: 4 tig + {1, 3}
-                mma_tf32(c, a00, a01, a02, a03, bv.x, bv.z);
-                mma_tf32(c, a10, a11, a12, a13, bv.y, bv.w);
-                const float2 bb = *reinterpret_cast<const float2*>(bn2 + j * KS + nt * 8 + 2 * tig);
-                mn0 = fminf(mn0, fminf(__fmaf_rn(-2.f, c[0], __fadd_rn(r0, bb.x)),
-                                       __fmaf_rn(-2.f, c[1], __fadd_rn(r0, bb.y))));
-                mn1 = fminf(mn1, fminf(__fmaf_rn(-2.f, c[2], __fadd_rn(r1, bb.x)),
-                                       __fmaf_rn(-2.f, c[3], __fadd_rn(r1, bb.y))));
-            }
-            mn0 = fminf(mn0, __shfl_xor_sync(0xffffffffu, mn0, 1));
-            mn0 = fminf(mn0, __shfl_xor_sync(0xffffffffu, mn0, 2));
-            mn1 = fminf(mn1, __shfl_xor_sync(0xffffffffu, mn1, 1));
-            mn1 = fminf(mn1, __shfl_xor_sync(0xffffffffu, mn1, 2));
-            sum0 = __fadd_rd(sum0, fmaxf(mn0, 0.f));
-            sum1 = __fadd_rd(sum1, fmaxf(mn1, 0.f));
-        }
-        if (tig == 0) {
-            const float keep = 0.9999847412109375f;  // 1 - 2^-16
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const size_t k = tl * 16 + g + 8 * h;
+    } else if (warp == 2 || warp == 3) {
+        // ------------------------------------------------ residual rows
+        const int cw = warp - 2;
+        uint32_t i = 0;
+        for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const uint32_t a = i & 1u;
+            if (i >= 2) bar_wait(BAR(1, a), ((i >> 1) - 1) & 1u);
+            uint8_t* A = As + a * A_BYTES;
+            for (int r = cw; r < TM; r += 2) {
+                const size_t k = t * TM + r;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (k < nfar) {
                     const size_t q = k / wf;
-                    pair_bound[q * w + R1 + (uint32_t)(k % wf)] = __fmul_rd(h ? sum1 : sum0, keep);
+                    const uint32_t l = probes[q * w + R1 + (uint32_t)(k % wf)];
+                    const float4 x = __ldg(reinterpret_cast<const float4*>(xq + q * D) + lane);
+                    const float4 cc = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + lane);
+                    v = make_float4(__fsub_rn(x.x, cc.x), __fsub_rn(x.y, cc.y), __fsub_rn(x.z, cc.z),
+                                    __fsub_rn(x.w, cc.w));
                 }
+                const __half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
+                uint2 pk;
+                pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+                pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+                *reinterpret_cast<uint2*>(A + sw128_off(r, 4 * lane, TM)) = pk;
+                // |r_j|^2 of the fp32 residual: lanes 4j .. 4j + 3 hold sub-space j
+                float s2 = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, __fmaf_rn(v.z, v.z, __fmul_rn(v.w, v.w))));
+                s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+                if ((lane & 3) == 0) rn2[(a * TM + r) * M + (lane >> 2)] = __fmul_rn(s2, shrink);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bar_arrive(BAR(0, a));
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ epilogue: min over codes, sum over j
+        const int ew = warp - 4;
+        const int r = 32 * ew + lane;
+        const unsigned lane_off = (unsigned)(32 * ew) << 16;
+        uint32_t g = 0, i = 0;
+        for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const uint32_t a = i & 1u;
+            bar_wait(BAR(0, a), (i >> 1) & 1u);  // rn2 of this tile is written
+            // read now: the residual warps refill this buffer (tile i + 2) once
+            // the tile's last MMA retired, while sub-spaces 6-7 still drain
+            float rjs[M];
+#pragma unroll
+            for (int j = 0; j < M; ++j) rjs[j] = rn2[(a * TM + r) * M + j];
+            float sum = 0.f;
+#pragma unroll
+            for (int j = 0; j < M; ++j, ++g) {
+                const uint32_t acc = g & 1u;
+                bar_wait(BAR(2, acc), (g >> 1) & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const float rj = rjs[j];
+                float mn = FLT_MAX;
+#pragma unroll 1
+                for (int c32 = 0; c32 < KS / 32; ++c32) {
+                    uint32_t u[32];
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+                          "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+                          "=r"(u[14]), "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]),
+                          "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]),
+                          "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+                        : "r"(tmem + lane_off + acc * KS + 32 * c32));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (c32 == KS / 32 - 1) {
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        bar_arrive(BAR(3, acc));
+                    }
+                    const float4* b4 = reinterpret_cast<const float4*>(bn2 + j * KS + 32 * c32);
+#pragma unroll
+                    for (int q4 = 0; q4 < 8; ++q4) {
+                        const float4 bb = b4[q4];
+                        mn = fminf(mn, fminf(fminf(__fmaf_rn(-2.f, __uint_as_float(u[4 * q4]), __fadd_rn(rj, bb.x)),
+                                                   __fmaf_rn(-2.f, __uint_as_float(u[4 * q4 + 1]), __fadd_rn(rj, bb.y))),
+                                             fminf(__fmaf_rn(-2.f, __uint_as_float(u[4 * q4 + 2]), __fadd_rn(rj, bb.z)),
+                                                   __fmaf_rn(-2.f, __uint_as_float(u[4 * q4 + 3]), __fadd_rn(rj, bb.w)))));
+                    }
+                }
+                sum = __fadd_rd(sum, fmaxf(__fsub_rd(mn, 0x1p-10f), 0.f));
+            }
+            const size_t k = t * TM + r;
+            if (k < nfar) {
+                const size_t q = k / wf;
+                pair_bound[q * w + R1 + (uint32_t)(k % wf)] = __fmul_rd(sum, 0.9999847412109375f);  // 1 - 2^-16
             }
         }
-        __syncwarp();
     }
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
 }  // namespace
@@ -159,10 +267,10 @@ bool far_bound_supported(uint32_t d, uint32_t m, uint32_t ks) { return d == D &&
 void launch_far_bound(const float* xq, const float* coarse, const float* books, const uint32_t* probes,
                       size_t nq, uint32_t w, uint32_t R1, float* pair_bound, cudaStream_t s) {
     if (nq == 0 || w <= R1) return;
-    const size_t smem = (size_t)M * KS * DS * 4 + (size_t)M * KS * 4 + (size_t)BW * 16 * RLD * 4 +
-                        (size_t)BW * 16 * M * 4;
-    set_max_smem((const void*)far_bound_kernel, (size_t)((int)smem));
-    far_bound_kernel<<<sm_count(), BW * 32, smem, s>>>(xq, coarse, books, probes, nq, w, R1, pair_bound);
+    set_max_smem((const void*)far_bound_tc_kernel, SMEM_BYTES);
+    const size_t nfar = nq * (size_t)(w - R1);
+    const unsigned grid = (unsigned)std::min<size_t>((nfar + TM - 1) / TM, (size_t)sm_count());
+    far_bound_tc_kernel<<<grid, FB_THREADS, SMEM_BYTES, s>>>(xq, coarse, books, probes, nq, w, R1, pair_bound);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

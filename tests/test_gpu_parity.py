@@ -829,3 +829,27 @@ def test_index_group_exact_equals_single_index(pq, mid_instance, nshards):
     with pytest.raises(ValueError, match="shortlist too small"):
         g.search(q[:4], 1, 5, 100)
     g.close()
+
+
+def test_two_phase_search_large_batch_matches_oracle(pq, mid_instance, oracle):
+    """A batch large enough for the two-phase LUT pass (query-list pairs >=
+    64 x SMs): far probes go through the tcgen05 far-pair bound (k_bound.cu)
+    and, at Kc = 128, the coarse distances through the tcgen05 D~ kernel;
+    shortlists and re-ranked lists must equal the oracle's bit for bit."""
+    from oracle.oracle_py import Oracle
+
+    o = Oracle()
+    centers = o.synth_centers(0, 256, 128)
+    q = o.synth_rows(0, 3, 1000, 320, centers)
+    oix, dix = mid_instance["oix"], mid_instance["dix"]
+    qf = q.astype(np.float32)
+    for v, kprime, k in [(40, 1000, 100), (96, 300, 50)]:
+        oi, od, oc = oix.search(qf, v, kprime)
+        ri, rd = oix.rerank(qf, oi, oc, k)
+        di, dd, dc = dix.search(q, v, kprime, k)
+        np.testing.assert_array_equal(di, ri)
+        np.testing.assert_array_equal(bits(dd), bits(rd))
+        si, sd, sc = dix.search(q, v, kprime, 0)
+        np.testing.assert_array_equal(sc, oc)
+        for i in range(len(q)):
+            np.testing.assert_array_equal(si[i, :oc[i]], oi[i, :oc[i]])
