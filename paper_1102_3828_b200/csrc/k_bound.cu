@@ -34,10 +34,10 @@ namespace {
 
 constexpr int M = 8, KS = 256, DS = 16, D = 128;
 constexpr int TM = 128;                  // far pairs per tile (TMEM lanes)
-constexpr int FB_THREADS = 256;          // warp 0 book / setup, 1 MMA, 2-3 residuals, 4-7 epilogue
+constexpr int FB_THREADS = 384;          // warp 1 MMA, 2-3 residuals, 4-11 epilogue (two per TMEM quadrant)
 constexpr uint32_t A_BYTES = TM * D * 2;     // 32 KiB: residual rows, fp16, K-major 128-byte swizzle
 constexpr uint32_t B_BYTES = KS * D * 2;     // 64 KiB: the code-major book [code][128 dims], fp16
-constexpr uint32_t SMEM_BYTES = 1024 + 2 * A_BYTES + B_BYTES + M * KS * 4 + 2 * TM * M * 4 + 16 * 8 + 16;
+constexpr uint32_t SMEM_BYTES = 1024 + 2 * A_BYTES + B_BYTES + M * KS * 4 + 3 * TM * M * 4 + 16 * 8 + 16;
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_init(unsigned a, unsigned n) {
@@ -96,7 +96,8 @@ __global__ void __launch_bounds__(FB_THREADS, 1) far_bound_tc_kernel(
     uint8_t* Bs = sm + 2 * A_BYTES;                                    // [B_BYTES]
     float* bn2 = reinterpret_cast<float*>(Bs + B_BYTES);               // [M][KS] |B_jc|^2 (1 - 2^-8)
     float* rn2 = bn2 + M * KS;                                         // [2][TM][M] |r_j|^2 (1 - 2^-8)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(rn2 + 2 * TM * M);  // a_full[2] a_empty[2] t_full[2] t_empty[2]
+    float* xmin = rn2 + 2 * TM * M;                                    // [TM][M] upper-half minima
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xmin + TM * M);       // a_full[2] a_empty[2] t_full[2] t_empty[2]
     const unsigned bar0 = su32(bars);
     auto BAR = [&](int kind, int i) { return bar0 + 8u * (2 * kind + i); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1) far_bound_tc_kernel(
             bar_init(BAR(0, i), 64);   // a_full: the residual warps
             bar_init(BAR(1, i), 1);    // a_empty: MMA commit
             bar_init(BAR(2, i), 1);    // t_full: MMA commit
-            bar_init(BAR(3, i), 128);  // t_empty: epilogue threads
+            bar_init(BAR(3, i), 256);  // t_empty: epilogue threads
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -173,46 +174,72 @@ __global__ void __launch_bounds__(FB_THREADS, 1) far_bound_tc_kernel(
             const uint32_t a = i & 1u;
             if (i >= 2) bar_wait(BAR(1, a), ((i >> 1) - 1) & 1u);
             uint8_t* A = As + a * A_BYTES;
-            for (int r = cw; r < TM; r += 2) {
-                const size_t k = t * TM + r;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            // this warp's 64 rows r = cw + 2 i: the list ids first (lane i holds
+            // rows i and i + 32), then 4 rows at a time with all loads in flight
+            uint32_t lid[2], qid[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const size_t k = t * TM + cw + 2 * (lane + 32 * h);
+                lid[h] = 0;
+                qid[h] = 0xffffffffu;
                 if (k < nfar) {
-                    const size_t q = k / wf;
-                    const uint32_t l = probes[q * w + R1 + (uint32_t)(k % wf)];
-                    const float4 x = __ldg(reinterpret_cast<const float4*>(xq + q * D) + lane);
-                    const float4 cc = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + lane);
-                    v = make_float4(__fsub_rn(x.x, cc.x), __fsub_rn(x.y, cc.y), __fsub_rn(x.z, cc.z),
-                                    __fsub_rn(x.w, cc.w));
+                    qid[h] = (uint32_t)(k / wf);
+                    lid[h] = probes[(size_t)qid[h] * w + R1 + (uint32_t)(k % wf)];
                 }
-                const __half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
-                uint2 pk;
-                pk.x = *reinterpret_cast<const uint32_t*>(&lo);
-                pk.y = *reinterpret_cast<const uint32_t*>(&hi);
-                *reinterpret_cast<uint2*>(A + sw128_off(r, 4 * lane, TM)) = pk;
-                // |r_j|^2 of the fp32 residual: lanes 4j .. 4j + 3 hold sub-space j
-                float s2 = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, __fmaf_rn(v.z, v.z, __fmul_rn(v.w, v.w))));
-                s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
-                s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
-                if ((lane & 3) == 0) rn2[(a * TM + r) * M + (lane >> 2)] = __fmul_rn(s2, shrink);
+            }
+#pragma unroll 1
+            for (int i0 = 0; i0 < TM / 2; i0 += 4) {
+                float4 xv[4], cv[4];
+                uint32_t qq[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u, h = i >> 5;
+                    qq[u] = __shfl_sync(0xffffffffu, h ? qid[1] : qid[0], i & 31);
+                    const uint32_t l = __shfl_sync(0xffffffffu, h ? lid[1] : lid[0], i & 31);
+                    xv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    cv[u] = xv[u];
+                    if (qq[u] != 0xffffffffu) {
+                        xv[u] = __ldg(reinterpret_cast<const float4*>(xq + (size_t)qq[u] * D) + lane);
+                        cv[u] = __ldg(reinterpret_cast<const float4*>(coarse + (size_t)l * D) + lane);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int r = cw + 2 * (i0 + u);
+                    const float4 v = make_float4(__fsub_rn(xv[u].x, cv[u].x), __fsub_rn(xv[u].y, cv[u].y),
+                                                 __fsub_rn(xv[u].z, cv[u].z), __fsub_rn(xv[u].w, cv[u].w));
+                    const __half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
+                    uint2 pk;
+                    pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+                    pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+                    *reinterpret_cast<uint2*>(A + sw128_off(r, 4 * lane, TM)) = pk;
+                    // |r_j|^2 of the fp32 residual: lanes 4j .. 4j + 3 hold sub-space j
+                    float s2 = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, __fmaf_rn(v.z, v.z, __fmul_rn(v.w, v.w))));
+                    s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+                    s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+                    if ((lane & 3) == 0) rn2[(a * TM + r) * M + (lane >> 2)] = __fmul_rn(s2, shrink);
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             bar_arrive(BAR(0, a));
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue: min over codes, sum over j
-        const int ew = warp - 4;
-        const int r = 32 * ew + lane;
-        const unsigned lane_off = (unsigned)(32 * ew) << 16;
+        // warps 4 + qd and 8 + qd share TMEM lanes 32 qd .. + 31 (rows) and
+        // take code columns 0..127 / 128..255; the upper half's minima meet
+        // the lower half's in shared memory at the end of the tile
+        const int ew = warp - 4, qd = ew & 3, hf = ew >> 2;
+        const int r = 32 * qd + lane;
+        const unsigned lane_off = (unsigned)(32 * qd) << 16;
         uint32_t g = 0, i = 0;
         for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
             const uint32_t a = i & 1u;
             bar_wait(BAR(0, a), (i >> 1) & 1u);  // rn2 of this tile is written
             // read now: the residual warps refill this buffer (tile i + 2) once
             // the tile's last MMA retired, while sub-spaces 6-7 still drain
-            float rjs[M];
+            float rjs[M], mns[M];
 #pragma unroll
             for (int j = 0; j < M; ++j) rjs[j] = rn2[(a * TM + r) * M + j];
-            float sum = 0.f;
 #pragma unroll
             for (int j = 0; j < M; ++j, ++g) {
                 const uint32_t acc = g & 1u;
@@ -221,7 +248,8 @@ __global__ void __launch_bounds__(FB_THREADS, 1) far_bound_tc_kernel(
                 const float rj = rjs[j];
                 float mn = FLT_MAX;
 #pragma unroll 1
-                for (int c32 = 0; c32 < KS / 32; ++c32) {
+                for (int c32 = 0; c32 < KS / 64; ++c32) {
+                    const int col = 128 * hf + 32 * c32;
                     uint32_t u[32];
                     asm volatile(
                         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
@@ -231,13 +259,13 @@ __global__ void __launch_bounds__(FB_THREADS, 1) far_bound_tc_kernel(
                           "=r"(u[14]), "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]),
                           "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]),
                           "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
-                        : "r"(tmem + lane_off + acc * KS + 32 * c32));
+                        : "r"(tmem + lane_off + acc * KS + col));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (c32 == KS / 32 - 1) {
+                    if (c32 == KS / 64 - 1) {
                         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                         bar_arrive(BAR(3, acc));
                     }
-                    const float4* b4 = reinterpret_cast<const float4*>(bn2 + j * KS + 32 * c32);
+                    const float4* b4 = reinterpret_cast<const float4*>(bn2 + j * KS + col);
 #pragma unroll
                     for (int q4 = 0; q4 < 8; ++q4) {
                         const float4 bb = b4[q4];
@@ -247,13 +275,25 @@ __global__ void __launch_bounds__(FB_THREADS, 1) far_bound_tc_kernel(
                                                    __fmaf_rn(-2.f, __uint_as_float(u[4 * q4 + 3]), __fadd_rn(rj, bb.w)))));
                     }
                 }
-                sum = __fadd_rd(sum, fmaxf(__fsub_rd(mn, 0x1p-10f), 0.f));
+                mns[j] = mn;
             }
-            const size_t k = t * TM + r;
-            if (k < nfar) {
-                const size_t q = k / wf;
-                pair_bound[q * w + R1 + (uint32_t)(k % wf)] = __fmul_rd(sum, 0.9999847412109375f);  // 1 - 2^-16
+            if (hf) {
+#pragma unroll
+                for (int j = 0; j < M; ++j) xmin[r * M + j] = mns[j];
             }
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
+            if (!hf) {
+                float sum = 0.f;
+#pragma unroll
+                for (int j = 0; j < M; ++j)
+                    sum = __fadd_rd(sum, fmaxf(__fsub_rd(fminf(mns[j], xmin[r * M + j]), 0x1p-10f), 0.f));
+                const size_t k = t * TM + r;
+                if (k < nfar) {
+                    const size_t q = k / wf;
+                    pair_bound[q * w + R1 + (uint32_t)(k % wf)] = __fmul_rd(sum, 0.9999847412109375f);  // 1 - 2^-16
+                }
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // xmin is free for the next tile
         }
     }
     __syncthreads();
