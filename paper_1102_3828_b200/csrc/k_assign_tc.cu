@@ -46,7 +46,9 @@ constexpr int AT_M = 128, AT_N = 128, AT_D = 128;
 constexpr int AT_THREADS = 256;
 constexpr uint32_t A_BYTES = AT_M * AT_D * 2;       // 32 KiB: two K halves of 16 KiB
 constexpr uint32_t B_BYTES = 2 * AT_N * AT_D * 2;   // 64 KiB: hi halves, lo halves
-constexpr uint32_t SMEM_BYTES = 1024 + 2 * A_BYTES + 2 * B_BYTES + 2 * AT_M * 4 + 16 * 8 + 16;
+constexpr uint32_t CN_SMEM = 8192;  // centroids whose |c|^2 are staged in shared memory
+constexpr uint32_t SMEM_BASE = 1024 + 2 * A_BYTES + 2 * B_BYTES + 2 * AT_M * 4 + 16 * 8 + 16;
+constexpr uint32_t SMEM_BYTES = SMEM_BASE + CN_SMEM * 4;
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_init(unsigned a, unsigned n) {
@@ -144,6 +146,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1) assign_tc_kernel(
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    // |c|^2 of every centroid in shared memory (the epilogue reads 128 per
+    // block as broadcast LDS instead of global loads)
+    const float* cns = cnorm;
+    if (nc <= CN_SMEM) {
+        float* dst = reinterpret_cast<float*>(tmem_slot + 4);
+        for (uint32_t k = threadIdx.x; k < nc; k += blockDim.x) dst[k] = __ldg(cnorm + k);
+        __syncthreads();
+        cns = dst;
+    }
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
@@ -202,10 +213,18 @@ __global__ void __launch_bounds__(AT_THREADS, 1) assign_tc_kernel(
             const uint32_t a = i & 1u;
             if (i >= 2) bar_wait(BAR(1, a), ((i >> 1) - 1) & 1u);
             uint8_t* A = As + a * A_BYTES;
-            for (int r = cw; r < AT_M; r += 2) {
-                const size_t row = t * AT_M + r;
-                uint32_t v = 0;
-                if (row < n) v = __ldg(reinterpret_cast<const uint32_t*>(y + row * AT_D) + lane);
+            uint32_t pre[4];
+#pragma unroll 1
+            for (int r0 = cw; r0 < AT_M; r0 += 8) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // 4 rows' loads in flight
+                const size_t rr = t * AT_M + r0 + 2 * u;
+                pre[u] = rr < n ? __ldg(reinterpret_cast<const uint32_t*>(y + rr * AT_D) + lane) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int r = r0 + 2 * u;
+                const uint32_t v = pre[u];
                 // dims 4 lane .. 4 lane + 3: chunk (k & 63) / 8 of K half k / 64, swizzled by row
                 const int k = 4 * lane, h = k >> 6, ch = ((k & 63) >> 3) ^ (r & 7);
                 const __half2 lo = __halves2half2(__uint2half_rn(v & 0xff), __uint2half_rn((v >> 8) & 0xff));
@@ -219,6 +238,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) assign_tc_kernel(
 #pragma unroll
                 for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
                 if (lane == 0) nx[a * AT_M + r] = (float)s;  // exact: < 2^24
+            }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             bar_arrive(BAR(0, a));
@@ -257,16 +277,26 @@ __global__ void __launch_bounds__(AT_THREADS, 1) assign_tc_kernel(
                         bar_arrive(BAR(5, acc));
                     }
                     const uint32_t k0 = b * AT_N + 32 * c4;
-                    const float4* cn4 = reinterpret_cast<const float4*>(cnorm + k0);
+                    const float4* cn4 = reinterpret_cast<const float4*>(cns + k0);
+                    // the chunk's 32 estimates (independent ops), then the
+                    // insertion only when one of them beats the 4th smallest
+                    float dts[32];
+                    float cmin = __int_as_float(0x7f800000);
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        const float4 cn = __ldg(cn4 + q);
-                        const float cv[4] = {cn.x, cn.y, cn.z, cn.w};
+                        const float4 cn = cn4[q];
+                        dts[4 * q + 0] = __fmaf_rn(-2.f, __uint_as_float(u[4 * q + 0]), __fadd_rn(xn, cn.x));
+                        dts[4 * q + 1] = __fmaf_rn(-2.f, __uint_as_float(u[4 * q + 1]), __fadd_rn(xn, cn.y));
+                        dts[4 * q + 2] = __fmaf_rn(-2.f, __uint_as_float(u[4 * q + 2]), __fadd_rn(xn, cn.z));
+                        dts[4 * q + 3] = __fmaf_rn(-2.f, __uint_as_float(u[4 * q + 3]), __fadd_rn(xn, cn.w));
+                        cmin = fminf(cmin, fminf(fminf(dts[4 * q], dts[4 * q + 1]), fminf(dts[4 * q + 2], dts[4 * q + 3])));
+                    }
+                    if (cmin < v3) {
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float dt = __fmaf_rn(-2.f, __uint_as_float(u[4 * q + e]), __fadd_rn(xn, cv[e]));
-                            if (dt < v3) {  // insert (rare after the first blocks)
-                                const uint32_t k = k0 + 4 * q + e;
+                        for (int e = 0; e < 32; ++e) {
+                            const float dt = dts[e];
+                            if (dt < v3) {
+                                const uint32_t k = k0 + e;
                                 if (dt < v2) {
                                     v3 = v2;
                                     if (dt < v1) {
@@ -366,6 +396,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    // |c|^2 of every centroid in shared memory (the epilogue reads 128 per
+    // block as broadcast LDS instead of global loads)
+    const float* cns = cnorm;
+    if (nc <= CN_SMEM) {
+        float* dst = reinterpret_cast<float*>(tmem_slot + 4);
+        for (uint32_t k = threadIdx.x; k < nc; k += blockDim.x) dst[k] = __ldg(cnorm + k);
+        __syncthreads();
+        cns = dst;
+    }
 
     if (warp == 0) {
         if (lane == 0) {
@@ -429,10 +468,19 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
             const uint32_t a = i & 1u;
             if (i >= 2) bar_wait(BAR(1, a), ((i >> 1) - 1) & 1u);
             uint8_t* A = As + a * A_BYTES;
-            for (int r = cw; r < AT_M; r += 2) {
-                const size_t row = t * AT_M + r;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (row < n) v = __ldg(reinterpret_cast<const float4*>(x + row * AT_D) + lane);
+            float4 pre[4];
+#pragma unroll 1
+            for (int r0 = cw; r0 < AT_M; r0 += 8) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // 4 rows' loads in flight
+                const size_t rr = t * AT_M + r0 + 2 * u;
+                pre[u] = rr < n ? __ldg(reinterpret_cast<const float4*>(x + rr * AT_D) + lane)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int r = r0 + 2 * u;
+                const float4 v = pre[u];
                 const int k = 4 * lane, h = k >> 6, ch = ((k & 63) >> 3) ^ (r & 7);
                 const __half2 lo = __floats2half2_rn(v.x, v.y);  // u8 integers: exact
                 const __half2 hi = __floats2half2_rn(v.z, v.w);
@@ -444,6 +492,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
 #pragma unroll
                 for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
                 if (lane == 0) nx[a * AT_M + r] = s2;  // exact: integer sum < 2^24
+            }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             bar_arrive(BAR(0, a));
@@ -486,10 +535,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
                         bar_arrive(BAR(5, acc));
                     }
                     const uint32_t k0 = b * AT_N + 32 * c4;
-                    const float4* cn4 = reinterpret_cast<const float4*>(cnorm + k0);
+                    const float4* cn4 = reinterpret_cast<const float4*>(cns + k0);
 #pragma unroll
                     for (int q4 = 0; q4 < 8; ++q4) {
-                        const float4 cn = __ldg(cn4 + q4);
+                        const float4 cn = cn4[q4];
                         float4 dv;
                         dv.x = __fmaf_rn(-2.f, __uint_as_float(u[4 * q4 + 0]), __fadd_rn(xn, cn.x));
                         dv.y = __fmaf_rn(-2.f, __uint_as_float(u[4 * q4 + 1]), __fadd_rn(xn, cn.y));
