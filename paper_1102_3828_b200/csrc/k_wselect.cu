@@ -563,15 +563,9 @@ __device__ __forceinline__ uint32_t warp_weighted_select(uint32_t n, uint32_t ra
             }
 #pragma unroll
             for (int k = 0; k < U; ++k) {
-                // warp-aggregated increments: the samples of a query crowd a
-                // few bins, and 32 lanes adding to one shared-memory counter
-                // serialise; lanes with equal bins sum their weights first
                 const uint32_t i = base + k * 32 + lane;
-                const bool in = i < n && (consumed == 0 || (v[k] >> (sh + wd)) == prefix);
-                const uint32_t bin = in ? ((v[k] >> sh) & msk) : 0xffffffffu;
-                const unsigned grp = __match_any_sync(0xffffffffu, bin);
-                const uint32_t tot = __reduce_add_sync(grp, in ? wt(i) : 0u);
-                if (in && lane == __ffs(grp) - 1) atomicAdd(&hist[bin], tot);
+                if (i < n && (consumed == 0 || (v[k] >> (sh + wd)) == prefix))
+                    atomicAdd(&hist[(v[k] >> sh) & msk], wt(i));
             }
         }
         __syncwarp();
