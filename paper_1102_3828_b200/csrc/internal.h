@@ -294,7 +294,7 @@ void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const 
                         uint32_t cap, uint32_t max_n, size_t nq, const uint32_t* ids,
                         uint32_t kprime, bool sorted, uint64_t* sl_key, uint32_t* sl_pos,
                         uint32_t* sl_cnt, cudaStream_t s,
-                        const uint32_t* cand_mm = nullptr);
+                        const uint32_t* cand_mm = nullptr, bool need_ids = true);
 // Re-rank the shortlist with the 3-term reconstruction, keep the k best.
 void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_t* sl_cnt,
                    uint32_t sl_stride, size_t nq, const float* xq, uint32_t d,
@@ -302,7 +302,7 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
                    const uint8_t* codes, const float* books, uint32_t m, const uint8_t* rcodes,
                    const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
                    uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s,
-                   cudaEvent_t ev_dist_done = nullptr);
+                   cudaEvent_t ev_dist_done = nullptr, const uint32_t* ids_for_keys = nullptr);
 // Add-path coarse assignment on the tensor cores (k_assign_tc.cu): u8 rows,
 // d = 128, nc % 128 == 0; certified equal to launch_argmin's result.
 bool assign_tc_supported(uint32_t d, uint32_t nc);
@@ -330,7 +330,7 @@ void launch_rerank_pair(const uint64_t* sl_key, const uint32_t* sl_pos, const ui
                         uint32_t stride, size_t nq, const float* xq, const uint16_t* block_list,
                         const float* coarse, const uint8_t* codes, const float* books,
                         const uint8_t* rcodes, const float* rbooks, uint32_t mprime, float* rdist,
-                        uint32_t* rid, cudaStream_t s);
+                        uint32_t* rid, cudaStream_t s, const uint32_t* ids = nullptr);
 // Merge per-shard ranked lists into the top-k (K7).  Part p's rows are
 // ids/dists + p * ps (nq x width) and counts + p * cs (nq); ps = cs = 0 means
 // the stacked layout [parts][nq][width] + [parts][nq].
@@ -354,7 +354,7 @@ bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32
 void launch_select_warp(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
                         uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime,
                         uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s,
-                        const uint32_t* cand_mm = nullptr);
+                        const uint32_t* cand_mm = nullptr, bool need_ids = true);
 void launch_threshold_warp(const float* sample_dist, const uint64_t* sample_off, uint32_t w, size_t nq,
                            const uint8_t* query_sampled, float alpha_k, uint32_t stride, int tiered,
                            float* tau, cudaStream_t s);

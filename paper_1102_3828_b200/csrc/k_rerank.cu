@@ -115,7 +115,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
     const uint16_t* __restrict__ block_list, const float* __restrict__ coarse,
     const uint8_t* __restrict__ codes, const float* __restrict__ books,
     const uint8_t* __restrict__ rcodes, const float* __restrict__ rbooks, float* __restrict__ rdist,
-    uint32_t* __restrict__ rid, u64 nz) {
+    uint32_t* __restrict__ rid, const uint32_t* __restrict__ ids, u64 nz) {
     using L = RpSmem<DSR>;
     constexpr int MP = 128 / DSR, HB = L::HB;
     extern __shared__ float4 rp_smem[];
@@ -188,7 +188,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
     auto load_meta = [&](size_t c, uint32_t pos, uint32_t nb) {
         const size_t t0 = (c / cpq) * stride + (uint32_t)(c % cpq) * 32;
         if ((uint32_t)lane < nb) {
-            if (r) p_id = key_id(sl_key[t0 + lane]);
+            // rank 1 writes the ids: from the shortlist keys, or from the id
+            // array when the selection left them out of the keys (ids = non-null)
+            if (r) p_id = ids ? ld_na_u32(ids + pos) : key_id(sl_key[t0 + lane]);
             p_list = ld_na_u16(block_list + (pos >> 4));
             p_code = ld_na_u32(codes + (size_t)pos * 8 + 4 * r);
             const uint8_t* rs = rcodes + (size_t)pos * MP + r * HB;
@@ -318,7 +320,7 @@ void launch_rerank_pair(const uint64_t* sl_key, const uint32_t* sl_pos, const ui
                         uint32_t stride, size_t nq, const float* xq, const uint16_t* block_list,
                         const float* coarse, const uint8_t* codes, const float* books,
                         const uint8_t* rcodes, const float* rbooks, uint32_t mprime, float* rdist,
-                        uint32_t* rid, cudaStream_t s) {
+                        uint32_t* rid, cudaStream_t s, const uint32_t* ids) {
     auto go = [&](auto kern, size_t smem) {
         static int clusters = 0;  // per instantiation: max co-resident clusters
         set_smem_attr((const void*)kern, smem);
@@ -339,7 +341,7 @@ void launch_rerank_pair(const uint64_t* sl_key, const uint32_t* sl_pos, const ui
         }
         kern<<<2 * (unsigned)clusters, RP_WARPS * 32, smem, s>>>(
             reinterpret_cast<const u64*>(sl_key), sl_pos, sl_cnt, stride, nq, xq, block_list, coarse,
-            codes, books, rcodes, rbooks, rdist, rid, kNegZero2);
+            codes, books, rcodes, rbooks, rdist, rid, ids, kNegZero2);
         PQRR_LAUNCH_CHECK();
         count_launch();
     };

@@ -688,11 +688,11 @@ void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const 
                         uint32_t cap, uint32_t max_n, size_t nq, const uint32_t* ids,
                         uint32_t kprime, bool sorted, uint64_t* sl_key, uint32_t* sl_pos,
                         uint32_t* sl_cnt, cudaStream_t s,
-                        const uint32_t* cand_mm) {
+                        const uint32_t* cand_mm, bool need_ids) {
     if (nq == 0) return;
     if (!sorted) {  // unsorted shortlist (re-ranked next): warp per query
         launch_select_warp(cand_dist, cand_pos, cand_cnt, cap, nq, ids, kprime, sl_key, sl_pos, sl_cnt, s,
-                           cand_mm);
+                           cand_mm, need_ids);
         return;
     }
     uint32_t kp2 = 1;
@@ -732,7 +732,7 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
                    const uint8_t* codes, const float* books, uint32_t m, const uint8_t* rcodes,
                    const float* rbooks, uint32_t mprime, uint32_t ks, uint32_t k,
                    uint32_t* out_ids, float* out_dists, uint32_t* out_cnt, cudaStream_t s,
-                   cudaEvent_t ev_dist_done) {
+                   cudaEvent_t ev_dist_done, const uint32_t* ids_for_keys) {
     if (nq == 0) return;
     uint32_t n2 = 1;
     while (n2 < sl_stride) n2 <<= 1;
@@ -748,7 +748,7 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
         PQRR_CUDA(cudaMallocAsync(&rd, tot * sizeof(float), s));
         PQRR_CUDA(cudaMallocAsync(&ri, tot * sizeof(uint32_t), s));
         launch_rerank_pair(sl_key, sl_pos, sl_cnt, sl_stride, nq, xq, block_list, coarse, codes, books,
-                           rcodes, rbooks, mprime, rd, ri, s);
+                           rcodes, rbooks, mprime, rd, ri, s, ids_for_keys);
         if (ev_dist_done) PQRR_CUDA(cudaEventRecord(ev_dist_done, s));
         if (!launch_rerank_topk_warp(rd, ri, sl_cnt, sl_stride, nq, k, out_ids, out_dists, out_cnt, s)) {
             set_smem((const void*)rerank_topk_kernel, (size_t)k2 * 8);

@@ -339,7 +339,7 @@ __global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
     const float* __restrict__ cand_dist, const uint32_t* __restrict__ cand_pos,
     const uint32_t* __restrict__ cand_cnt, uint32_t cap, size_t nq, const uint32_t* __restrict__ ids,
     uint32_t kprime, u64* __restrict__ sl_key, uint32_t* __restrict__ sl_pos,
-    uint32_t* __restrict__ sl_cnt, const uint32_t* __restrict__ cand_mm) {
+    uint32_t* __restrict__ sl_cnt, const uint32_t* __restrict__ cand_mm, int need_ids) {
     __shared__ uint32_t hist_all[WS_WARPS][256];
     __shared__ u64 tie_all[WS_WARPS][TIE_CAP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -354,7 +354,7 @@ __global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
     if (n <= kprime) {
         for (uint32_t i = lane; i < n; i += 32) {
             const uint32_t p = pq[i];
-            ok[i] = ((u64)dq[i] << 32) | ids[p];
+            ok[i] = ((u64)dq[i] << 32) | (need_ids ? ids[p] : 0u);
             op[i] = p;
         }
         if (lane == 0) sl_cnt[q] = n;
@@ -383,7 +383,9 @@ __global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
             p[k] = (i < n && u[k] <= kth) ? pq[i] : 0u;
         }
 #pragma unroll
-        for (int k = 0; k < U; ++k) id[k] = u[k] <= kth ? ids[p[k]] : 0u;
+        // ids only where they decide (the boundary ties) unless the caller
+        // needs them in the keys (the re-ranker with records reads its own)
+        for (int k = 0; k < U; ++k) id[k] = (u[k] == kth || (need_ids && u[k] < kth)) ? ids[p[k]] : 0u;
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             const bool lt = u[k] < kth, eq = u[k] == kth;  // padding lanes carry 0xffffffff
@@ -665,11 +667,11 @@ bool launch_topw_warp(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32
 void launch_select_warp(const float* cand_dist, const uint32_t* cand_pos, const uint32_t* cand_cnt,
                         uint32_t cap, size_t nq, const uint32_t* ids, uint32_t kprime,
                         uint64_t* sl_key, uint32_t* sl_pos, uint32_t* sl_cnt, cudaStream_t s,
-                        const uint32_t* cand_mm) {
+                        const uint32_t* cand_mm, bool need_ids) {
     if (nq == 0) return;
     select_warp_kernel<<<(unsigned)((nq + WS_WARPS - 1) / WS_WARPS), WS_WARPS * 32, 0, s>>>(
         cand_dist, cand_pos, cand_cnt, cap, nq, ids, kprime, reinterpret_cast<u64*>(sl_key), sl_pos,
-        sl_cnt, cand_mm);
+        sl_cnt, cand_mm, need_ids ? 1 : 0);
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

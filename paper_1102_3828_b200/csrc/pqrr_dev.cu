@@ -366,6 +366,7 @@ struct DevIndex {
     float cnorm_max = 0.f;
     AssignTc atc;               // tcgen05 coarse distances (add path; u8 queries)
     bool q_u8 = false;          // the search in flight has u8-valued queries
+    bool keys_need_ids = true;  // the shortlist keys must carry ids (see search_device)
     DBuf<uint8_t> q8_cache;     // per LUT-pass item 8-bit LUT (32 KiB) for the K4f filter
     DBuf<float> q8_param;       // per LUT-pass item and query lane: (scale, sum of minima)
     uint64_t next_id = 0;
@@ -562,6 +563,7 @@ void finalize(DevIndex& ix) {
     ix.st_n = 0;
     ix.id_map_valid = false;
 }
+
 
 uint64_t id_lo_of(const DevIndex& ix) { return ix.id_lo == ~0ull ? 0 : ix.id_lo; }
 
@@ -1043,7 +1045,8 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     const bool early_select = !sorted;
     if (early_select) {
         launch_select_topk(cand_dist, cand_pos, cand_cnt, cap, cap, nq, ix.ids.p, kprime, sorted,
-                           reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s, cand_mm);
+                           reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s, cand_mm,
+                           ix.keys_need_ids);
         if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[6], s));
     }
     std::vector<uint8_t> h_fail(nq);
@@ -1144,6 +1147,13 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
     for (auto& e : ix.ev)
         if (!e) PQRR_CUDA(cudaEventCreate(&e));
     PQRR_CUDA(cudaEventRecord(ix.ev[10], s));
+    // large shortlists (k' >= 4096) ahead of the CTA-pair re-ranker: the keys
+    // carry no ids, the selection gathers ids only for its boundary ties and
+    // the re-ranker's rank 1 reads the ids of the entries it writes (C4:
+    // selection 2.59 -> 1.41 ms, re-ranker +0.5 ms; at k' = 1000 the
+    // selection's gathers are cheap and the re-ranker's extra load is not)
+    const bool pair = k > 0 && kprime >= 4096 && rerank_pair_supported(ix.d, ix.m, ix.ks, ix.mprime);
+    ix.keys_need_ids = !pair;
     Workspace ws(s);
     ShortlistDev sl{ws.alloc<u64>(nq * (size_t)kprime), ws.alloc<uint32_t>(nq * (size_t)kprime),
                     ws.alloc<uint32_t>(nq)};
@@ -1189,7 +1199,8 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
         PQRR_CUDA(cudaEventRecord(ix.ev[7], s));
         launch_rerank(reinterpret_cast<uint64_t*>(sl.key), sl.pos, sl.cnt, kprime, nq, xq, ix.d,
                       ix.block_list.p, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
-                      ix.rbooks.p, ix.mprime, ix.ks, k, out_ids, out_dists, out_cnt, s, ix.ev[12]);
+                      ix.rbooks.p, ix.mprime, ix.ks, k, out_ids, out_dists, out_cnt, s, ix.ev[12],
+                      pair ? ix.ids.p : nullptr);
     } else {
         PQRR_CUDA(cudaEventRecord(ix.ev[7], s));
         launch_unpack_keys(reinterpret_cast<uint64_t*>(sl.key), sl.cnt, nq, kprime, out_ids, out_dists, s);
@@ -1470,6 +1481,9 @@ int pqrr_dev_index_create(int device, uint32_t d, uint32_t c, const float* coars
         ix.mprime = mprime;
         ix.ks = ks;
         PQRR_CUDA(cudaStreamCreateWithFlags(&ix.stream, cudaStreamNonBlocking));
+        // the search's random gathers (codes, refinement codes, ids, block
+        // table) use 4-32 B of each miss: fetch 32-B sectors, not wider lines
+        PQRR_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32));
         cudaMemPool_t pool;
         PQRR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
         uint64_t thr = UINT64_MAX;

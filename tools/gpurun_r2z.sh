@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python bench.py --config C2 --no-cpu-baseline --no-recall > gpurun_out/r2z_c2.json 2> gpurun_out/r2z_c2.err
+timeout 1200 python bench.py --config C4 --no-cpu-baseline --no-recall > gpurun_out/r2z_c4.json 2> gpurun_out/r2z_c4.err
+echo done
