@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) dtilde_tc_kernel(
     // |c|^2 of every centroid in shared memory (the epilogue reads 128 per
     // block as broadcast LDS instead of global loads)
     const float* cns = cnorm;
-    if (nc <= CN_SMEM) {
+    if (nc <= CN_SMEM && nsplit == 1) {  // split small batches read their few blocks' |c|^2 directly
         float* dst = reinterpret_cast<float*>(tmem_slot + 4);
         for (uint32_t k = threadIdx.x; k < nc; k += blockDim.x) dst[k] = __ldg(cnorm + k);
         __syncthreads();

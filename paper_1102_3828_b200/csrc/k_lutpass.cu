@@ -252,6 +252,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
 
     if (warp == NCW) {
         // ---------------------------------------------------------- producer
+        uint32_t live_mask = 0, my_c = 0;  // skip_dead: claimed items found live
         for (uint32_t k = 0;; ++k) {
             const int b = k & 1;
             if (k >= 2) mbar_wait(&empty_bar[b], ((k >> 1) - 1) & 1);
@@ -260,8 +261,42 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
             int q;
             for (;;) {
                 c = 0;
-                if (lane == 0) c = atomicAdd(a.item_counter, 1u);
-                c = __shfl_sync(0xffffffffu, c, 0);
+                if (a.skip_dead) {
+                    // round 2 of the two-phase pass skips most far items: the
+                    // lanes claim 32 items at once and test one item each (the
+                    // dependent loads of 32 items overlap instead of running one
+                    // item after the other); live items are then taken in order
+                    while (!live_mask) {
+                        uint32_t cb = 0;
+                        if (lane == 0) cb = atomicAdd(a.item_counter, 32u);
+                        cb = __shfl_sync(0xffffffffu, cb, 0);
+                        if (cb >= n_items) break;
+                        my_c = cb + lane;
+                        bool lv = false;
+                        if (my_c < n_items) {
+                            const uint32_t it2 = a.item_order[my_c];
+                            const uint32_t st2 = a.item_start[it2], nq2 = a.item_nq[it2];
+                            for (uint32_t j = 0; j < nq2 && j < (uint32_t)QT && !lv; ++j) {
+                                const uint32_t p2 = a.pair_sorted[st2 + j];
+                                const int q2 = (int)(p2 / a.w);
+                                const float sm2 = a.pair_bound ? a.pair_bound[p2]
+                                                               : a.q8_param[((size_t)it2 * QT + j) * 2 + 1];
+                                lv = pair_live(a.tau[q2], sm2);
+                            }
+                        }
+                        live_mask = __ballot_sync(0xffffffffu, lv);
+                    }
+                    if (!live_mask) {
+                        c = n_items;
+                        break;
+                    }
+                    const int src = __ffs(live_mask) - 1;
+                    live_mask &= live_mask - 1u;
+                    c = __shfl_sync(0xffffffffu, my_c, src);
+                } else {
+                    if (lane == 0) c = atomicAdd(a.item_counter, 1u);
+                    c = __shfl_sync(0xffffffffu, c, 0);
+                }
                 if (c >= n_items) break;
                 it = a.item_order[c];  // longest items first
                 l = a.item_list[it];
@@ -275,13 +310,7 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                     p = a.pair_sorted[start + lane];
                     q = (int)(p / a.w);
                 }
-                if (!a.skip_dead) break;
-                // round 2 of the two-phase pass: only items with a lane that
-                // can reach tau (its bound-pass sum of minima, pair_live)
-                const float summ = a.pair_bound ? (q >= 0 ? a.pair_bound[p] : 0.f)
-                                                : a.q8_param[((size_t)it * QT + lane) * 2 + 1];
-                const bool live = q >= 0 && pair_live(a.tau[q], summ);
-                if (__any_sync(0xffffffffu, live)) break;
+                break;  // (skip_dead: the item was found live above)
             }
             if (c >= n_items) {
                 if (lane == 0) {

@@ -1186,16 +1186,16 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
             shortlist_core(ix, xq + c0 * ix.d, nc, w, kprime, k == 0, default_alpha(kprime, w), 1, part, 0, true);
         }
     }
+    // "shortlist too small" is checked after the re-rank, with the
+    // final synchronisation: no host round trip between selection and re-rank
+    // (a failing batch's outputs are not returned)
+    unsigned h_flag[4] = {0, 0, 0, 0};
     if (k > 0) {
         unsigned* flag = ws.zeros<unsigned>(4);
         min_count_kernel<<<nblk(nq), 256, 0, s>>>(sl.cnt, nq, k, flag);
         PQRR_LAUNCH_CHECK();
         count_launch();
-        unsigned h_flag[4] = {0, 0, 0, 0};
         PQRR_CUDA(cudaMemcpyAsync(h_flag, flag, 16, cudaMemcpyDeviceToHost, s));
-        PQRR_CUDA(cudaStreamSynchronize(s));
-        if (h_flag[0]) throw ShortlistError();
-        std::memcpy(&ix.stats.rerank_candidates, h_flag + 2, 8);
         PQRR_CUDA(cudaEventRecord(ix.ev[7], s));
         launch_rerank(reinterpret_cast<uint64_t*>(sl.key), sl.pos, sl.cnt, kprime, nq, xq, ix.d,
                       ix.block_list.p, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
@@ -1208,6 +1208,8 @@ void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t 
     }
     PQRR_CUDA(cudaEventRecord(ix.ev[8], s));
     PQRR_CUDA(cudaEventSynchronize(ix.ev[8]));
+    if (h_flag[0]) throw ShortlistError();
+    std::memcpy(&ix.stats.rerank_candidates, h_flag + 2, 8);
     auto el = [&](int a, int b) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ix.ev[a], ix.ev[b]);

@@ -39,3 +39,24 @@ def test_ref_harness_matches_oracle(reflib):
     sid, a, c, rc = H.reencode_sample(cfg, hx.coarse, hx.books, hx.rbooks, starts, block)
     assert np.array_equal(a, hx.list_of_id[sid]) and np.array_equal(c, hx.codes_by_id[sid]) and np.array_equal(rc, hx.rcodes_by_id[sid])
     assert H.host_cores() >= 1 and H.cpu_model()
+
+
+def test_reference_arm_file_lists(tmp_path):
+    """bench.FileLists: the reference arm's view of the lists a setup process
+    exported (no product code loaded) returns each requested list's rows."""
+    import bench
+
+    U = np.array([3, 7, 9], np.uint32)
+    offs = np.array([0, 2, 5, 6], np.uint64)
+    ids = np.array([1, 4, 2, 3, 8, 5], np.uint32)
+    codes = np.arange(48, dtype=np.uint8).reshape(6, 8)
+    rc = np.arange(96, dtype=np.uint8).reshape(6, 16)
+    for name, a in (("lists", U), ("offs", offs), ("ids", ids), ("codes", codes), ("rcodes", rc)):
+        np.save(tmp_path / f"{name}.npy", a)
+    fl = bench.FileLists(str(tmp_path))
+    o, i, c, r = fl(np.array([9, 3], np.uint32))
+    np.testing.assert_array_equal(o, [0, 1, 3])
+    np.testing.assert_array_equal(i, [5, 1, 4])
+    np.testing.assert_array_equal(c[:, 0], [40, 0, 8])
+    np.testing.assert_array_equal(r[:, 0], [80, 0, 16])
+    assert fl.nbytes() > 0
