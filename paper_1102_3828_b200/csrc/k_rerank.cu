@@ -91,6 +91,9 @@ __device__ __forceinline__ uint4 ld_na_v4(const void* p) {
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_addr(smem)), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -105,7 +108,8 @@ struct RpSmem {
     static constexpr size_t mcode = (size_t)RP_WARPS * 4 * RP_MLD;
     static constexpr size_t mrc = (size_t)RP_WARPS * HB * RP_MLD;
     static constexpr size_t bars = (size_t)RP_WARPS * 2 * 8;
-    static constexpr size_t total = books + tiles + part + mlist + mcode + mrc + bars;
+    static constexpr size_t pos = (size_t)RP_WARPS * 33 * 4;
+    static constexpr size_t total = books + tiles + part + mlist + mcode + mrc + bars + pos;
 };
 
 template <int DSR>
@@ -128,6 +132,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
     uint8_t* mcode = reinterpret_cast<uint8_t*>(mlist) + L::mlist;         // [warps][4][MLD]
     uint8_t* mrc = mcode + L::mcode;                                        // [warps][HB][MLD]
     u64* bars = reinterpret_cast<u64*>(mrc + L::mrc);  // [warps][2]: full (rank 1) / empty (rank 0)
+    uint32_t* posbuf = reinterpret_cast<uint32_t*>(bars + RP_WARPS * 2);  // [warps][32 positions + count]
 
     const unsigned r = cta_rank();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -175,11 +180,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
     // count carry nb = 0 and are skipped by both CTAs alike.
     uint32_t p_id = 0, p_list = 0, p_code = 0;
     uint32_t p_rc[(HB + 3) / 4];
+    // the positions and row count of chunk i + 2 travel by cp.async into a
+    // per-warp smem slot: a register load here would be the warp's 7th
+    // outstanding global load and wait for a free scoreboard (one DRAM round
+    // trip per chunk, ncu: 18% of K5a's stall samples at C4)
     uint32_t n_pos = 0, n_cnt = 0;  // chunk i + 1: position of the lane's entry, row count
+    uint32_t* wpos = posbuf + warp * 33;
     auto load_pos = [&](size_t c) {  // no dependency: rows are allocated k' wide
         const size_t q = c / cpq;
-        n_cnt = sl_cnt[q];
-        n_pos = sl_pos[q * stride + (uint32_t)(c % cpq) * 32 + min((uint32_t)lane, stride - 1 - (uint32_t)(c % cpq) * 32)];
+        const uint32_t i0 = (uint32_t)(c % cpq) * 32;
+        cp_async4(wpos + lane, sl_pos + q * stride + i0 + min((uint32_t)lane, stride - 1 - i0));
+        if (lane == 0) cp_async4(wpos + 32, sl_cnt + q);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto take_pos = [&]() {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        n_pos = wpos[lane];
+        n_cnt = wpos[32];
+        __syncwarp();  // read before the next cp.async overwrites the slot
     };
     auto nb_of = [&](size_t c, uint32_t cnt) -> uint32_t {
         const uint32_t i0 = (uint32_t)(c % cpq) * 32;
@@ -209,6 +228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
     uint32_t cur_cnt = 0;
     if (start < total) {
         load_pos(start);
+        take_pos();
         cur_cnt = n_cnt;
         load_meta(start, n_pos, nb_of(start, cur_cnt));
         if (start + tw < total) load_pos(start + tw);
@@ -238,6 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RP_WARPS * 32, 1) re
             if (r && (uint32_t)lane < nb) rid[t0 + lane] = p_id;
         }
         if (ch + tw < total) {
+            take_pos();
             cur_cnt = n_cnt;
             load_meta(ch + tw, n_pos, nb_of(ch + tw, cur_cnt));
             if (ch + 2 * tw < total) load_pos(ch + 2 * tw);
