@@ -573,8 +573,10 @@ def rooflines(cfg, stats, clocks, device, config):
         reported beside it;
       K4f filter: 1 B per (live (query, list) pair, entry, sub-space) LUT
         lookup it performs -- bound: the shared-memory pipe;
-      K4r recheck: 8 code-book rows of d/m floats (512 B) per surviving
-        candidate -- bound: the shared-memory pipe.
+      K4r recheck (recheck_lut_kernel): per surviving candidate its probe
+        rank and 8 code bytes read and its exact distance written back,
+        16 B -- bound: HBM (the 8 lookups into the pair's exact LUT, 32 B of
+        shared memory per candidate, are reported beside it).
     Shared-memory peak: 128 B/clk/SM x SMs x the SM clock sampled under load.
     `traffic` is ncu dram__bytes_read.sum + dram__bytes_write.sum per launch
     of the same kernel on the same commit (profiles/ncu_traffic.json), or null.
@@ -611,11 +613,15 @@ def rooflines(cfg, stats, clocks, device, config):
                    "peak_kind": smem_kind, "traffic": traffic.get("ivf_filter_kernel")})
     t = mean("ms_recheck")
     if t > 0:
-        b = mean("candidates") * m * (d // m) * 4
-        ks.append({"kernel": "recheck_smem_kernel (K4r exact ADC of the survivors)", "bound": "smem",
-                   "kernel_ms": t, "algorithmic_bytes_per_launch": b,
-                   "achieved": b / (t / 1e3) / 1e9, "peak": smem_peak_gbs, "unit": "GB/s",
-                   "peak_kind": smem_kind, "traffic": traffic.get("recheck_smem_kernel")})
+        nc = mean("candidates")
+        b, sb = nc * 16, nc * m * 4
+        ks.append({"kernel": "recheck_lut_kernel (K4r exact ADC of the survivors, per-pair LUTs)",
+                   "bound": "hbm", "kernel_ms": t, "algorithmic_bytes_per_launch": b,
+                   "achieved": b / (t / 1e3) / 1e9, "peak": peak_hbm, "unit": "GB/s", "peak_kind": kind,
+                   "traffic": traffic.get("recheck_lut_kernel"),
+                   "smem": {"algorithmic_bytes_per_launch": sb, "achieved": sb / (t / 1e3) / 1e9,
+                            "peak": smem_peak_gbs, "frac": sb / (t / 1e3) / 1e9 / smem_peak_gbs,
+                            "peak_kind": smem_kind}})
     for e in ks:
         e["frac"] = e["achieved"] / e["peak"]
     if not ks:

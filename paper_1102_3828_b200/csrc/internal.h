@@ -238,6 +238,12 @@ struct FilterArgs {
     uint32_t* cand_pos;
     uint32_t* cand_cnt;
     uint32_t cap;
+    // optional: each candidate's 8 code bytes next to its position, read from
+    // the list K4f just streamed (L2) so K4r needs no random DRAM gather
+    uint64_t* cand_code;
+    // optional: per query a 256-bit mask of the probe ranks that got a
+    // candidate (zeroed by the caller; K4r builds LUTs for exactly those)
+    uint32_t* cand_used;
     int pass_all;  // debug: every probed entry is a candidate
     float band_div;  // Delta target = (tau - sum of minima) / band_div
 };
@@ -269,7 +275,8 @@ void launch_recheck(const float* xq, uint32_t d, uint32_t m, const float* coarse
                     const float* books, const uint32_t* probes, uint32_t w, const uint8_t* codes,
                     const uint32_t* cand_cnt, uint32_t cap, const uint32_t* cand_pos,
                     float* cand_dist, const float* tau, size_t nq, uint32_t* cand_le,
-                    cudaStream_t s, uint32_t* cand_mm = nullptr);
+                    cudaStream_t s, uint32_t* cand_mm = nullptr, const uint64_t* cand_code = nullptr,
+                    const uint32_t* cand_used = nullptr);
 
 // Build the scan work items from the probes.
 void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,

@@ -100,7 +100,9 @@ __device__ __forceinline__ void append_direct(int slot, uint32_t pos, const int*
     if (o < a.cap) {
         a.cand_pos[(size_t)q * a.cap + o] = pos;
         a.cand_aux[(size_t)q * a.cap + o] = s_r[slot];
+        if (a.cand_code) a.cand_code[(size_t)q * a.cap + o] = __ldg(reinterpret_cast<const u64*>(a.codes) + pos);
     }
+    if (a.cand_used) atomicOr(a.cand_used + (size_t)q * 8 + (s_r[slot] >> 5), 1u << (s_r[slot] & 31));
 }
 
 // Writes the staged candidates (entry << 6 | slot) of the item to the
@@ -118,6 +120,10 @@ __device__ __forceinline__ void flush_stage(const FilterArgs& a, const uint32_t*
         const uint32_t cnt = s_scnt[threadIdx.x];
         s_sbase[threadIdx.x] = cnt ? atomicAdd(a.cand_cnt + s_q[threadIdx.x], cnt) : 0u;
         s_scnt[threadIdx.x] = 0;
+        if (cnt && a.cand_used) {
+            const uint32_t r = s_r[threadIdx.x];
+            atomicOr(a.cand_used + (size_t)s_q[threadIdx.x] * 8 + (r >> 5), 1u << (r & 31));
+        }
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < nst; i += FT) {
@@ -126,8 +132,10 @@ __device__ __forceinline__ void flush_stage(const FilterArgs& a, const uint32_t*
         const uint32_t o = s_sbase[sl] + atomicAdd(&s_scnt[sl], 1u);
         if (o < a.cap) {
             const size_t q = (size_t)s_q[sl];
-            a.cand_pos[q * a.cap + o] = off32 + (v >> 6);
+            const uint32_t pos = off32 + (v >> 6);
+            a.cand_pos[q * a.cap + o] = pos;
             a.cand_aux[q * a.cap + o] = s_r[sl];
+            if (a.cand_code) a.cand_code[q * a.cap + o] = __ldg(reinterpret_cast<const u64*>(a.codes) + pos);
         }
     }
     __syncthreads();
@@ -717,6 +725,217 @@ bool recheck_supported(uint32_t d, uint32_t m, uint32_t w) {
     return (size_t)w * d * sizeof(float) <= 200 * 1024;
 }
 
+// K4r with per-pair LUTs (d = 128, m = 8, ks = 256).  A query's survivors
+// come from few (query, list) pairs (at C4 ~8 of the 64 probes), each with
+// hundreds to thousands of survivors, so the CTA builds the exact LUT of every
+// pair that has survivors -- L_j[c] = l2_sq(x - C_l restricted to sub-space
+// j, B_j[c]), 2048 values in the reference order, 8 KiB in shared memory --
+// and each survivor's exact ADC distance is then 8 shared-memory lookups
+// summed j-ascending (adc_distance, product_quantizer.hpp:53-57): the same
+// fp32 values in the same order as recomputing the 8 terms per survivor.
+// Pairs are taken LUT_SLOTS at a time (a query with more such pairs makes one
+// pass over its survivors per batch).  The pairs with survivors come from
+// K4f's per-query rank mask (cand_used) or, without it, from a pass over the
+// survivors' ranks.  Survivors are handled 4 per thread with vector loads and
+// two groups' loads in flight before the first store (the kernel is bound by
+// load latency, not by its shared-memory lookups).
+constexpr int LUT_SLOTS = 16;
+
+__device__ __forceinline__ float subspace_l2(const float* __restrict__ r, const float* __restrict__ b, u64 nz) {
+    // l2_sq(r[0..16), b[0..16)) in the reference order (distance.hpp:16-33)
+    const ulonglong2* r2 = reinterpret_cast<const ulonglong2*>(r);
+    const ulonglong2* b2 = reinterpret_cast<const ulonglong2*>(b);
+    u64 sa = 0, sb = 0;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const ulonglong2 rv = r2[p], bv = b2[p];
+        if (p == 0) {  // 0 + x == x for the rounded square x >= +0
+            sa = sq2(sub2(rv.x, bv.x), nz);
+            sb = sq2(sub2(rv.y, bv.y), nz);
+        } else {
+            sa = acc_sq2(sa, rv.x, bv.x, nz);
+            sb = acc_sq2(sb, rv.y, bv.y, nz);
+        }
+    }
+    return __fadd_rn(__fadd_rn(lo2(sa), hi2(sa)), __fadd_rn(lo2(sb), hi2(sb)));
+}
+
+// One group of 4 survivors (i0 .. i0+3 of the query's buffer): ranks and codes.
+struct SurvGroup {
+    uint32_t r[4];
+    u64 c[4];
+    uint32_t cnt;  // valid survivors in the group (0..4)
+};
+
+__device__ __forceinline__ SurvGroup load_group(const uint32_t* aux, const u64* cq, const uint32_t* pq,
+                                                const u64* codes, uint32_t i0, uint32_t n) {
+    SurvGroup g;
+    g.cnt = i0 < n ? min(4u, n - i0) : 0u;
+    if (g.cnt == 4) {
+        const uint4 a4 = *reinterpret_cast<const uint4*>(aux + i0);
+        g.r[0] = a4.x, g.r[1] = a4.y, g.r[2] = a4.z, g.r[3] = a4.w;
+        if (cq) {
+            const ulonglong2 c01 = *reinterpret_cast<const ulonglong2*>(cq + i0);
+            const ulonglong2 c23 = *reinterpret_cast<const ulonglong2*>(cq + i0 + 2);
+            g.c[0] = c01.x, g.c[1] = c01.y, g.c[2] = c23.x, g.c[3] = c23.y;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) g.c[u] = __ldg(codes + pq[i0 + u]);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool v = (uint32_t)u < g.cnt;
+            g.r[u] = v ? aux[i0 + u] : 0u;
+            g.c[u] = v ? (cq ? cq[i0 + u] : __ldg(codes + pq[i0 + u])) : 0ull;
+        }
+    }
+    return g;
+}
+
+__global__ __launch_bounds__(512, 1) void recheck_lut_kernel(
+    const float* __restrict__ xq, const float* __restrict__ coarse, const float* __restrict__ books,
+    const uint32_t* __restrict__ probes, uint32_t w, const u64* __restrict__ codes,
+    const uint32_t* __restrict__ cand_cnt, uint32_t cap, const uint32_t* __restrict__ cand_pos,
+    float* cand_dist, const float* __restrict__ tau, size_t nq, uint32_t* __restrict__ cand_le,
+    uint32_t* __restrict__ counter, const u64 nz, uint32_t* __restrict__ cand_mm,
+    const u64* __restrict__ cand_code, const uint32_t* __restrict__ cand_used, float* __restrict__ scratch) {
+    constexpr int D = 128, DS = 16;
+    extern __shared__ float4 lut4[];
+    float* lut = reinterpret_cast<float*>(lut4);  // [LUT_SLOTS][M * KS]
+    __shared__ __align__(16) float res[LUT_SLOTS][D];
+    __shared__ uint8_t slot_of[256];
+    __shared__ uint32_t used[8], s_rank[256];
+    __shared__ uint32_t s_q, s_le, s_mn, s_mx, s_nused;
+    const int tid = threadIdx.x;
+    for (;;) {
+        __syncthreads();  // previous query done
+        if (tid == 0) {
+            s_q = atomicAdd(counter, 1u);
+            s_le = 0;
+            s_mn = 0xffffffffu;
+            s_mx = 0u;
+        }
+        __syncthreads();
+        const size_t q = s_q;
+        if (q >= nq) break;
+        const uint32_t n = min(cand_cnt[q], cap);
+        if (n == 0) {
+            if (tid == 0) {
+                cand_le[q] = 0;
+                if (cand_mm) cand_mm[2 * q] = 0xffffffffu, cand_mm[2 * q + 1] = 0u;
+            }
+            continue;
+        }
+        uint32_t* aux = reinterpret_cast<uint32_t*>(cand_dist) + q * cap;  // probe ranks (K4f)
+        float* dq = cand_dist + q * cap;
+        const uint32_t* pq = cand_pos + q * cap;
+        const u64* cq = cand_code ? cand_code + q * cap : nullptr;
+        // the probe ranks that have survivors
+        if (tid < 8) used[tid] = cand_used ? cand_used[q * 8 + tid] : 0u;
+        __syncthreads();
+        if (!cand_used) {
+            for (uint32_t i = tid; i < n; i += blockDim.x) {
+                const uint32_t r = aux[i];
+                if (!((used[r >> 5] >> (r & 31)) & 1u)) atomicOr(&used[r >> 5], 1u << (r & 31));
+            }
+            __syncthreads();
+        }
+        if (tid < 256 && ((used[tid >> 5] >> (tid & 31)) & 1u)) {
+            uint32_t before = __popc(used[tid >> 5] & ((1u << (tid & 31)) - 1u));
+            for (int k = 0; k < (tid >> 5); ++k) before += __popc(used[k]);
+            slot_of[tid] = (uint8_t)before;
+            s_rank[before] = tid;
+        }
+        if (tid == 0) {
+            uint32_t t = 0;
+            for (int k = 0; k < 8; ++k) t += __popc(used[k]);
+            s_nused = t;
+        }
+        __syncthreads();
+        const uint32_t nused = s_nused;
+        const float tq = tau[q];
+        uint32_t le = 0, dmn = 0xffffffffu, dmx = 0u;
+        // several batches: the ranks are read again by every batch, so the
+        // distances go to the CTA's scratch row and are copied over at the end
+        float* out = nused > (uint32_t)LUT_SLOTS ? scratch + (size_t)blockIdx.x * cap : dq;
+        for (uint32_t b0 = 0; b0 < nused; b0 += LUT_SLOTS) {
+            const uint32_t nb = min((uint32_t)LUT_SLOTS, nused - b0);
+            if (b0) __syncthreads();  // the previous batch's lookups are done
+            // residuals x - C_l of the batch's pairs, then their exact LUTs
+            for (uint32_t i = tid; i < nb * D; i += blockDim.x) {
+                const uint32_t sl = i / D, t = i % D;
+                const uint32_t l = probes[q * w + s_rank[b0 + sl]];
+                res[sl][t] = __fsub_rn(xq[q * D + t], coarse[(size_t)l * D + t]);
+            }
+            __syncthreads();
+            for (uint32_t v = tid; v < nb * M * KS; v += blockDim.x) {
+                const uint32_t sl = v / (M * KS), jc = v % (M * KS), j = jc / KS, c = jc % KS;
+                lut[v] = subspace_l2(&res[sl][j * DS], books + ((size_t)j * KS + c) * DS, nz);
+            }
+            __syncthreads();
+            // survivors of the batch: 8 lookups each, summed j-ascending
+            auto run = [&](const SurvGroup& g, uint32_t i0) {
+                float d4[4];
+                bool done[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t sl = slot_of[g.r[u]] - b0;  // wraps for earlier batches
+                    done[u] = (uint32_t)u < g.cnt && sl < nb;
+                    const float* L = lut + min(sl, (uint32_t)LUT_SLOTS - 1) * (M * KS);
+                    const u64 code = g.c[u];
+                    float acc = L[(uint32_t)(code & 0xffu)];  // 0 + L_0 == L_0
+#pragma unroll
+                    for (int j = 1; j < M; ++j) acc = __fadd_rn(acc, L[j * KS + (uint32_t)((code >> (8 * j)) & 0xffu)]);
+                    d4[u] = acc;
+                    if (done[u]) {
+                        le += acc <= tq ? 1u : 0u;
+                        dmn = min(dmn, __float_as_uint(acc));
+                        dmx = max(dmx, __float_as_uint(acc));
+                    }
+                }
+                if (done[0] && done[1] && done[2] && done[3]) {
+                    *reinterpret_cast<float4*>(out + i0) = make_float4(d4[0], d4[1], d4[2], d4[3]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (done[u]) out[i0 + u] = d4[u];
+                }
+            };
+            const uint32_t step = 4 * blockDim.x;
+            for (uint32_t i0 = 4 * tid; i0 < n; i0 += 2 * step) {
+                const SurvGroup g0 = load_group(aux, cq, pq, codes, i0, n);
+                const SurvGroup g1 = load_group(aux, cq, pq, codes, i0 + step, n);
+                run(g0, i0);
+                if (g1.cnt) run(g1, i0 + step);
+            }
+        }
+        if (out != dq) {
+            __syncthreads();
+            for (uint32_t i = tid; i < n; i += blockDim.x) dq[i] = out[i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            le += __shfl_xor_sync(0xffffffffu, le, o);
+            dmn = min(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+            dmx = max(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+        }
+        if ((tid & 31) == 0) {
+            if (le) atomicAdd(&s_le, le);
+            atomicMin(&s_mn, dmn);
+            atomicMax(&s_mx, dmx);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            cand_le[q] = s_le;
+            if (cand_mm) {
+                cand_mm[2 * q] = s_mn;
+                cand_mm[2 * q + 1] = s_mx;
+            }
+        }
+    }
+}
+
 template <int DSUB>
 bool recheck_smem_t(const float* xq, uint32_t d, const float* coarse, const float* books,
                     const uint32_t* probes, uint32_t w, const uint8_t* codes, const uint32_t* cand_cnt,
@@ -741,10 +960,30 @@ void launch_recheck(const float* xq, uint32_t d, uint32_t m, const float* coarse
                     const float* books, const uint32_t* probes, uint32_t w, const uint8_t* codes,
                     const uint32_t* cand_cnt, uint32_t cap, const uint32_t* cand_pos,
                     float* cand_dist, const float* tau, size_t nq, uint32_t* cand_le,
-                    cudaStream_t s, uint32_t* cand_mm) {
+                    cudaStream_t s, uint32_t* cand_mm, const uint64_t* cand_code,
+                    const uint32_t* cand_used) {
     if (!nq) return;
-    // shared-memory code book (the recheck kernels below stay for shapes or
-    // residual sets it does not hold)
+    // per-pair LUTs (the common shape), else the shared-memory code book, else
+    // the generic recheck kernels
+    if (d == 128 && m == M && d / m == 16 && w <= 256) {
+        const size_t smem = (size_t)LUT_SLOTS * M * KS * sizeof(float);
+        set_max_smem((const void*)recheck_lut_kernel, smem);
+        uint32_t* counter = nullptr;
+        float* scratch = nullptr;
+        PQRR_CUDA(cudaMallocAsync(&counter, sizeof(uint32_t), s));
+        PQRR_CUDA(cudaMallocAsync(&scratch, (size_t)sm_count() * cap * sizeof(float), s));
+        PQRR_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), s));
+        recheck_lut_kernel<<<sm_count(), 512, smem, s>>>(xq, coarse, books, probes, w,
+                                                        reinterpret_cast<const u64*>(codes), cand_cnt, cap,
+                                                        cand_pos, cand_dist, tau, nq, cand_le, counter,
+                                                        kNegZero2, cand_mm,
+                                                        reinterpret_cast<const u64*>(cand_code), cand_used, scratch);
+        PQRR_LAUNCH_CHECK();
+        PQRR_CUDA(cudaFreeAsync(scratch, s));
+        PQRR_CUDA(cudaFreeAsync(counter, s));
+        count_launch();
+        return;
+    }
     if (d / m == 16 &&
         recheck_smem_t<16>(xq, d, coarse, books, probes, w, codes, cand_cnt, cap, cand_pos, cand_dist,
                            tau, nq, cand_le, s, cand_mm))

@@ -986,6 +986,11 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         f.cand_pos = cand_pos;
         f.cand_cnt = cand_cnt;
         f.cap = cap;
+        // candidates' codes next to them (K4r then reads no random DRAM sectors)
+        uint64_t* cand_code = ws.alloc<uint64_t>(nq * (size_t)cap);
+        f.cand_code = cand_code;
+        uint32_t* cand_used = ws.zeros<uint32_t>(nq * 8);
+        f.cand_used = w <= 256 ? cand_used : nullptr;
         static const bool pass_all = getenv("PQRR_FILTER_ALL") != nullptr;  // debug hook
         f.pass_all = pass_all ? 1 : 0;
         const char* bd_env = getenv("PQRR_BANDDIV");  // tuning hook (read per search)
@@ -1015,7 +1020,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         cand_mm = ws.alloc<uint32_t>(2 * nq);
         PQRR_CUDA(cudaMemsetAsync(cand_mm, 0xff, 2 * nq * sizeof(uint32_t), s));
         launch_recheck(xq, ix.d, ix.m, ix.coarse.p, ix.books.p, probes, w, ix.codes.p, cand_cnt, cap,
-                       cand_pos, cand_dist, tau, nq, cand_le, s, cand_mm);
+                       cand_pos, cand_dist, tau, nq, cand_le, s, cand_mm, cand_code, f.cand_used);
     } else {
         im.apply(a);
         a.pass = 0;

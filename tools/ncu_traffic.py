@@ -8,7 +8,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["rerank_pair_kernel", "ivf_filter_kernel", "recheck_smem_kernel", "lut_pass_kernel",
+KERNELS = ["rerank_pair_kernel", "ivf_filter_kernel", "recheck_smem_kernel", "recheck_lut_kernel", "lut_pass_kernel",
            "select_large_kernel", "assign_tc_kernel"]
 
 

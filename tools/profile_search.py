@@ -24,7 +24,7 @@ def main():
     if args.nq:
         cfg["nq"] = args.nq
     coarse, P, rq = bench.train_codebooks(pq, cfg, 0)
-    ix, _, _ = bench.build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
+    ix, _, _, _ = bench.build_index(pq, cfg, coarse, P, rq, 0, 0, 1)
     q = pq.synth(3, 0, cfg["nq"], cfg["clusters"], seed=bench.SEED)
     tolerate = bool(os.environ.get("PQRR_LIB_PATH"))  # timing variants may compute garbage
     try:
