@@ -151,7 +151,12 @@ __device__ __forceinline__ void flush_stage(const FilterArgs& a, const uint32_t*
 // step: the two lanes of a quarter warp that read the same quad position get
 // the two entries of a parity pair, so every LDS.128 stays conflict-free
 // exactly as in the 64-slot layout.
-template <int NQD>
+// NQD = 0 (items with <= 4 or <= 8 live pairs): the LUT row is the pairs'
+// bytes as NW = 1 / 2 words, replicated to fill the 64-byte row; a lane reads
+// copy (eoff / 2) mod (16 / NW), so the two lanes of a parity pair share a copy
+// index and land 16 banks apart -- one LDS.32 per (entry, j) serves the warp
+// in one wavefront, one LDS.64 in two (vs 4 for an LDS.128).
+template <int NQD, int NW = 1>
 __device__ __forceinline__ void filter_scan(const FilterArgs& a, const uint4* __restrict__ lut8v,
                                             const uint8_t* s_t, const int* s_q, const uint32_t* s_r,
                                             uint32_t* s_nst, uint32_t* stage, uint32_t* s_scnt,
@@ -159,9 +164,11 @@ __device__ __forceinline__ void filter_scan(const FilterArgs& a, const uint4* __
                                             uint32_t off32, bool stage_ok) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c = lane & 3, h = (lane >> 2) & 1, p = lane >> 3;
-    const int grp = c % NQD;  // the lane's slot group
-    const uint32_t eoff = 2 * (p * (4 / NQD) + c / NQD) + h;
-    constexpr uint32_t EPW = 32 / NQD;  // entries per warp step
+    constexpr int NQ = NQD ? NQD : 1;
+    const int grp = c % NQ;  // the lane's slot group
+    const uint32_t eoff = 2 * (p * (4 / NQ) + c / NQ) + h;
+    constexpr uint32_t EPW = 32 / NQ;  // entries per warp step
+    const uint32_t* lut32 = reinterpret_cast<const uint32_t*>(lut8v) + NW * ((eoff >> 1) % (16 / NW));
     const uint4 tb = reinterpret_cast<const uint4*>(s_t)[grp];
     const uint4 th = make_uint4(tb.x | 0x80808080u, tb.y | 0x80808080u, tb.z | 0x80808080u,
                                 tb.w | 0x80808080u);
@@ -197,22 +204,38 @@ __device__ __forceinline__ void filter_scan(const FilterArgs& a, const uint4* __
         for (int j = 0; j < M; ++j) {
             const uint32_t ca = ((j < 4 ? cAl : cAh) >> (8 * (j & 3))) & 0xffu;
             const uint32_t cb = ((j < 4 ? cBl : cBh) >> (8 * (j & 3))) & 0xffu;
-            const uint4 va = lut8v[(j * KS + ca) * NSUB + c];
-            const uint4 vb = lut8v[(j * KS + cb) * NSUB + c];
-            a0 += va.x; a1 += va.y; a2 += va.z; a3 += va.w;
-            b0 += vb.x; b1 += vb.y; b2 += vb.z; b3 += vb.w;
+            if (NQD == 0 && NW == 1) {
+                a0 += lut32[(j * KS + ca) * 16];
+                b0 += lut32[(j * KS + cb) * 16];
+            } else if (NQD == 0) {
+                const uint2 va = *reinterpret_cast<const uint2*>(lut32 + (j * KS + ca) * 16);
+                const uint2 vb = *reinterpret_cast<const uint2*>(lut32 + (j * KS + cb) * 16);
+                a0 += va.x; a1 += va.y;
+                b0 += vb.x; b1 += vb.y;
+            } else {
+                const uint4 va = lut8v[(j * KS + ca) * NSUB + c];
+                const uint4 vb = lut8v[(j * KS + cb) * NSUB + c];
+                a0 += va.x; a1 += va.y; a2 += va.z; a3 += va.w;
+                b0 += vb.x; b1 += vb.y; b2 += vb.z; b3 += vb.w;
+            }
         }
         // pass bits sit at bit 7 of each byte; gather them into one lane mask
         // (bit 16 s + 4 t + b: step s, word t, byte b -> slot grp * 16 + 4 t
         // + b).  (x >> 7) * 0x00204081 moves bits 0/8/16/24 to bits 21..24
         // without carries.
         auto m4 = [](uint32_t x) { return (((x >> 7) * 0x00204081u) >> 21) & 0xfu; };
-        const uint32_t mA = vA ? (m4(le_bytes(a0, tb.x, th.x)) | (m4(le_bytes(a1, tb.y, th.y)) << 4) |
-                                  (m4(le_bytes(a2, tb.z, th.z)) << 8) | (m4(le_bytes(a3, tb.w, th.w)) << 12))
-                               : 0u;
-        const uint32_t mB = vB ? (m4(le_bytes(b0, tb.x, th.x)) | (m4(le_bytes(b1, tb.y, th.y)) << 4) |
-                                  (m4(le_bytes(b2, tb.z, th.z)) << 8) | (m4(le_bytes(b3, tb.w, th.w)) << 12))
-                               : 0u;
+        uint32_t mA, mB;
+        if (NQD == 0) {
+            mA = vA ? m4(le_bytes(a0, tb.x, th.x)) | (NW == 2 ? m4(le_bytes(a1, tb.y, th.y)) << 4 : 0u) : 0u;
+            mB = vB ? m4(le_bytes(b0, tb.x, th.x)) | (NW == 2 ? m4(le_bytes(b1, tb.y, th.y)) << 4 : 0u) : 0u;
+        } else {
+            mA = vA ? (m4(le_bytes(a0, tb.x, th.x)) | (m4(le_bytes(a1, tb.y, th.y)) << 4) |
+                       (m4(le_bytes(a2, tb.z, th.z)) << 8) | (m4(le_bytes(a3, tb.w, th.w)) << 12))
+                    : 0u;
+            mB = vB ? (m4(le_bytes(b0, tb.x, th.x)) | (m4(le_bytes(b1, tb.y, th.y)) << 4) |
+                       (m4(le_bytes(b2, tb.z, th.z)) << 8) | (m4(le_bytes(b3, tb.w, th.w)) << 12))
+                    : 0u;
+        }
         uint32_t mask = mA | (mB << 16);
         while (mask) {
             const int bpos = __ffs(mask) - 1;
@@ -289,7 +312,9 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
         }
         __syncthreads();
         // NQD = 1 / 2 / 4 quads of 16 slots per entry (filter_scan)
-        const int nqd = nqi <= 16 ? 1 : (nqi <= 32 ? 2 : 4);
+        // 0: narrow (<= 4 / <= 8 pairs: nw replicated words per row); else quads per entry
+        const int nqd = nqi <= 8 ? 0 : (nqi <= 16 ? 1 : (nqi <= 32 ? 2 : 4));
+        const int nw = nqi <= 4 ? 1 : 2;
 
         // ---- 5-bit LUT of the item: the live slots' 8-bit lane columns
         // (lane-major LUT-pass blocks, q8_put_rows) are staged 32 at a time in
@@ -300,7 +325,7 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
             uint8_t* colbuf = reinterpret_cast<uint8_t*>(stage);  // [32][2052]
             uint32_t* colw = stage;
             constexpr int CST = M * KS + 4;  // bytes per staged column
-            const int nsl = 16 * nqd;
+            const int nsl = nqd ? 16 * nqd : 4 * nw;
             for (int h = 0; 32 * h < nsl; ++h) {
                 const int ns = min(32, nsl - 32 * h);
                 for (int x = threadIdx.x; x < ns * (M * KS / 16); x += FT) {
@@ -316,7 +341,32 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
                 }
                 __syncthreads();
                 const int sq = threadIdx.x & 7;
-                if (4 * sq < ns) {
+                if (nqd == 0) {
+                    // every thread converts whole rows: the pairs' nw words, replicated
+                    uint32_t mu[8], ad[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        mu[k] = s_mult[k];
+                        ad[k] = s_add[k];
+                    }
+                    for (int row = threadIdx.x; row < M * KS; row += FT) {
+                        const uint8_t* cb = colbuf + row;
+                        const uint32_t word = (uint32_t)cb[0] | ((uint32_t)cb[CST] << 8) |
+                                              ((uint32_t)cb[2 * CST] << 16) | ((uint32_t)cb[3 * CST] << 24);
+                        const uint32_t v5 = v5_of(word, mu, ad);
+                        uint32_t v5b = v5;
+                        if (nw == 2) {
+                            const uint8_t* cc = cb + 4 * CST;
+                            const uint32_t w2 = (uint32_t)cc[0] | ((uint32_t)cc[CST] << 8) |
+                                                ((uint32_t)cc[2 * CST] << 16) | ((uint32_t)cc[3 * CST] << 24);
+                            v5b = v5_of(w2, mu + 4, ad + 4);
+                        }
+                        const uint4 v4 = make_uint4(v5, v5b, nw == 2 ? v5 : v5b, v5b);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)  // rotated: the 8 lanes of a phase hit 8 bank groups
+                            reinterpret_cast<uint4*>(lut8 + row * FQ)[(i + (row >> 1)) & 3] = v4;
+                    }
+                } else if (4 * sq < ns) {
                     const int s0 = 32 * h + 4 * sq;  // first slot of this thread's word
                     uint32_t mu[4], ad[4];
 #pragma unroll
@@ -344,7 +394,11 @@ __global__ __launch_bounds__(FT, 1) void ivf_filter_kernel(const FilterArgs a) {
         const uint32_t off32 = (uint32_t)off;
         const bool stage_ok = len < (1u << 26);
         const u64* codes = reinterpret_cast<const u64*>(a.codes) + off;
-        if (nqd == 1)
+        if (nqd == 0 && nw == 1)
+            filter_scan<0, 1>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, s_scnt, s_sbase, codes, len, off32, stage_ok);
+        else if (nqd == 0)
+            filter_scan<0, 2>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, s_scnt, s_sbase, codes, len, off32, stage_ok);
+        else if (nqd == 1)
             filter_scan<1>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, s_scnt, s_sbase, codes, len, off32, stage_ok);
         else if (nqd == 2)
             filter_scan<2>(a, lut8v, s_t, s_q, s_r, &s_nst, stage, s_scnt, s_sbase, codes, len, off32, stage_ok);
