@@ -176,10 +176,32 @@ int pqrr_dev_search_f32(pqrr_dev_index* ix, const float* queries, size_t nq, uin
                         uint32_t* out_counts);
 /* Device-resident variant: all pointers are device pointers on the index's
  * device; `stream` is a cudaStream_t (NULL = the legacy default stream). The
- * call is stream-ordered but may synchronise internally.                    */
+ * call is stream-ordered and returns after the results are complete (small
+ * batches: one graph launch and one synchronisation; large batches read
+ * counts back between stages).                                              */
 int pqrr_dev_search_u8_device(pqrr_dev_index* ix, const uint8_t* d_queries, size_t nq,
                               uint32_t w, size_t kprime, size_t k, uint32_t* d_out_ids,
                               float* d_out_dists, uint32_t* d_out_counts, void* stream);
+/* Enqueue-only variant for small batches (serving; eval.hpp:49's per-query
+ * time is the latency it targets).  The whole search is one CUDA graph,
+ * captured on the first call of a (shape, buffers) combination and replayed
+ * afterwards: _enqueue returns once the graph is launched, ordered after
+ * `stream`'s earlier work, and `stream` waits for the results; no host
+ * synchronisation happens inside.  _finish waits for the enqueued search and
+ * returns its error code (PQRR_ESHORTLIST as above); in the rare case that a
+ * sampled threshold failed its on-device exactness check it redoes the batch
+ * on the synchronising path, so the results are the same bits either way.
+ * One search may be pending per index.  PQRR_EUNSUPPORTED: the batch is
+ * outside the envelope (more than 1024 queries, or bounds too large for the
+ * device) — use pqrr_dev_search_u8_device.                                   */
+int pqrr_dev_search_u8_enqueue(pqrr_dev_index* ix, const uint8_t* d_queries, size_t nq,
+                               uint32_t w, size_t kprime, size_t k, uint32_t* d_out_ids,
+                               float* d_out_dists, uint32_t* d_out_counts, void* stream);
+int pqrr_dev_search_finish(pqrr_dev_index* ix);
+/* enabled = 0: every search of this index takes the synchronising path (per
+ * stage times in pqrr_dev_last_search_stats; graph replays report only the
+ * total); 1 (default): batches of up to 1024 queries replay captured graphs. */
+int pqrr_dev_index_set_graph(pqrr_dev_index* ix, int enabled);
 
 /* ivf_rerank (ivf_index.hpp:79-81) of an explicit shortlist: sl_ids row q
  * holds sl_counts[q] ids (stride sl_stride); outputs k per query. */

@@ -100,6 +100,9 @@ _sig("pqrr_dev_export_lists", [_vp, _vp, _vp, _vp, _vp])
 _sig("pqrr_dev_search_u8", [_vp, _u8p, _sz, _u32, _sz, _sz, _u32p, _f32p, _u32p])
 _sig("pqrr_dev_search_f32", [_vp, _f32p, _sz, _u32, _sz, _sz, _u32p, _f32p, _u32p])
 _sig("pqrr_dev_search_u8_device", [_vp, _vp, _sz, _u32, _sz, _sz, _vp, _vp, _vp, _vp])
+_sig("pqrr_dev_search_u8_enqueue", [_vp, _vp, _sz, _u32, _sz, _sz, _vp, _vp, _vp, _vp])
+_sig("pqrr_dev_search_finish", [_vp])
+_sig("pqrr_dev_index_set_graph", [_vp, _int])
 _sig("pqrr_dev_rerank_u8", [_vp, _u8p, _sz, _u32p, _u32p, _sz, _sz, _u32p, _f32p])
 _sig("pqrr_dev_rerank_f32", [_vp, _f32p, _sz, _u32p, _u32p, _sz, _sz, _u32p, _f32p])
 _sig("pqrr_dev_reconstruct", [_vp, _u32p, _sz, _f32p])
@@ -145,7 +148,8 @@ EXPORTED = [
     "pqrr_dev_index_create", "pqrr_dev_index_destroy", "pqrr_dev_add_u8", "pqrr_dev_add_f32",
     "pqrr_dev_add_synthetic", "pqrr_dev_finalize", "pqrr_dev_index_get_info",
     "pqrr_dev_export_lists", "pqrr_dev_search_u8", "pqrr_dev_search_f32",
-    "pqrr_dev_search_u8_device", "pqrr_dev_rerank_u8", "pqrr_dev_rerank_f32",
+    "pqrr_dev_search_u8_device", "pqrr_dev_search_u8_enqueue", "pqrr_dev_search_finish",
+    "pqrr_dev_index_set_graph", "pqrr_dev_rerank_u8", "pqrr_dev_rerank_f32",
     "pqrr_dev_reconstruct", "pqrr_dev_lookup_ids", "pqrr_dev_last_search_stats", "pqrr_dev_load_lists",
     "pqrr_dev_merge_topk", "pqrr_dev_merge_topk_device", "pqrr_dev_merge_packed_device",
     "pqrr_dev_index_device", "pqrr_dev_group_create", "pqrr_dev_group_search_u8", "pqrr_dev_group_size",

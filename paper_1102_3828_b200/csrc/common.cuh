@@ -131,4 +131,29 @@ __device__ __forceinline__ void q8_put_rows(uint32_t* __restrict__ block, int g,
     block[(4 * g + 3) * LANE_WORDS + rq] = __byte_perm(hi01, hi23, 0x7632);
 }
 
+// Upper bound of the R-th smallest value a CTA holds, without atomics: every
+// thread passes the minimum of the values it read (all threads must have read
+// at least one); the R-th smallest of those minima has at least R values at or
+// below it.  A histogram-based select then only counts the values <= the
+// bound — the low tail — instead of serialising its shared-memory atomics on
+// the few bins that hold nearly every value.  blockDim.x must be a power of
+// two, R <= blockDim.x; s_mins holds blockDim.x words.  All threads call.
+__device__ __forceinline__ uint32_t cta_tail_bound(uint32_t my_min, uint32_t R, uint32_t* s_mins) {
+    s_mins[threadIdx.x] = my_min;
+    __syncthreads();
+    for (uint32_t size = 2; size <= blockDim.x; size <<= 1)
+        for (uint32_t st = size >> 1; st > 0; st >>= 1) {
+            const uint32_t i = threadIdx.x, jx = i ^ st;
+            if (jx > i) {
+                const uint32_t a = s_mins[i], b = s_mins[jx];
+                if ((a > b) == ((i & size) == 0)) {
+                    s_mins[i] = b;
+                    s_mins[jx] = a;
+                }
+            }
+            __syncthreads();
+        }
+    return s_mins[R - 1];
+}
+
 }  // namespace pqrr_b200

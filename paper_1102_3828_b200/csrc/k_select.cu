@@ -25,25 +25,33 @@ __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t n
                                    int tiered, uint32_t cap, uint64_t* __restrict__ n_entries,
                                    uint8_t* __restrict__ sampled, uint64_t* __restrict__ pair_samples,
                                    unsigned long long* __restrict__ grand_total, uint32_t max_rank) {
-    size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per query: the probes' list lengths are dependent loads
+    const size_t q = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (q >= nq) return;
-    uint64_t tot = 0;
-    for (uint32_t r = 0; r < w; ++r) tot += list_len[probes[q * w + r]];
-    n_entries[q] = tot;
-    atomicAdd(grand_total, (unsigned long long)tot);
+    unsigned long long tot = 0;
+    for (uint32_t r = lane; r < w; r += 32) tot += list_len[probes[q * w + r]];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
     // every query whose candidates may not fit the buffer gets a threshold
     // (stride 1 samples every entry: still exact, only slower)
     const bool samp = tot > cap;
-    sampled[q] = samp ? 1 : 0;
     unsigned long long ssum = 0;
-    for (uint32_t r = 0; r < w; ++r) {
+    for (uint32_t r = lane; r < w; r += 32) {
         const uint32_t len = list_len[probes[q * w + r]];
         const uint32_t st = stride << tier_shift(sample_tier(r, w, tiered), w);
         const uint64_t ns = (samp && r < max_rank) ? (len + st - 1) / st : 0;
         pair_samples[q * w + r] = ns;
         ssum += ns;
     }
-    atomicMax(grand_total + 1, ssum);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+    if (lane == 0) {
+        n_entries[q] = tot;
+        atomicAdd(grand_total, tot);
+        sampled[q] = samp ? 1 : 0;
+        atomicMax(grand_total + 1, ssum);
+    }
 }
 
 // Block-wide search of the bin holding the rank-th element (1-based) of a
@@ -111,7 +119,8 @@ __device__ __forceinline__ void for_each_u32(const uint32_t* __restrict__ src, u
 // straight from global memory, the selected bin is compacted into shared
 // memory when it fits stage_cap (with each element's tier), and the remaining
 // passes run over that small set only.
-__global__ __launch_bounds__(SEL_THREADS, 4) void sample_threshold_kernel(
+constexpr int THR_THREADS_MAX = 1024;
+__global__ __launch_bounds__(THR_THREADS_MAX, 1) void sample_threshold_kernel(
     const float* __restrict__ sample, const uint64_t* __restrict__ sample_off, uint32_t w,
     const uint8_t* __restrict__ sampled, float alpha_k, uint32_t stride, int tiered,
     uint32_t stage_cap, float* __restrict__ tau) {
@@ -119,6 +128,7 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void sample_threshold_kernel(
     uint8_t* stage_t = reinterpret_cast<uint8_t*>(stage + stage_cap);
     __shared__ uint32_t hist[NBINS];
     __shared__ uint32_t s_bin, s_rank, s_fill;
+    __shared__ uint32_t s_mins[THR_THREADS_MAX];
     __shared__ unsigned long long s_seg[5];
     const size_t q = blockIdx.x;
     if (!sampled[q]) {
@@ -147,24 +157,28 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void sample_threshold_kernel(
     for (int b = threadIdx.x; b < NBINS; b += blockDim.x) hist[b] = 0;
     if (threadIdx.x == 0) s_fill = 0;
     __syncthreads();
-    for (int t = 0; t < 4; ++t) {
-        const uint32_t wt = stride << tier_shift(t, w);
-        const uint32_t n = (uint32_t)(s_seg[t + 1] - s_seg[t]);
-        if (n) for_each_u32(gsrc + s_seg[t], n, [&](uint32_t u) { atomicAdd(&hist[u >> 21], wt); });
-    }
-    __syncthreads();
-    find_bin(hist, rank, &s_bin, &s_rank);
-    __syncthreads();
-    uint32_t prefix = s_bin, r = s_rank;
-    // optimistic compaction of the selected bin (with each element's tier);
-    // an overfull stage falls back to reading global memory
-    {
-        const uint32_t top = prefix;
+    // The target rank sits in the far lower tail (~64-128 samples of 10^4-10^6),
+    // and a histogram over all samples serialises its shared-memory atomics on
+    // the two or three bins that hold nearly everything.  So first bound the
+    // answer from above without atomics: each thread keeps the minimum of the
+    // tier-0 samples it reads (tier 0 carries the smallest weight, `stride`);
+    // the R0-th smallest of those minima, R0 = ceil(rank / stride), has at
+    // least R0 tier-0 samples at or below it, i.e. weight >= rank.  Only the
+    // samples <= that bound (a few hundred) are staged, and the exact weighted
+    // select runs over the stage.  Same tau as the full radix select.
+    const uint32_t n0 = (uint32_t)(s_seg[1] - s_seg[0]);
+    const uint32_t R0 = (rank + stride - 1) / stride;
+    bool staged = false;
+    uint32_t cnt = 0, prefix = 0, r = rank;
+    if (R0 <= blockDim.x / 2 && n0 >= 8 * blockDim.x) {
+        uint32_t mn = 0xffffffffu;
+        for_each_u32(gsrc + s_seg[0], n0, [&](uint32_t u) { mn = min(mn, u); });
+        const uint32_t T0 = cta_tail_bound(mn, R0, s_mins);
         for (int t = 0; t < 4; ++t) {
             const uint32_t n = (uint32_t)(s_seg[t + 1] - s_seg[t]);
             if (n)
                 for_each_u32(gsrc + s_seg[t], n, [&](uint32_t u) {
-                    if ((u >> 21) == top) {
+                    if (u <= T0) {
                         const uint32_t k = atomicAdd(&s_fill, 1u);
                         if (k < stage_cap) {
                             stage[k] = u;
@@ -173,13 +187,57 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void sample_threshold_kernel(
                     }
                 });
         }
+        __syncthreads();
+        cnt = s_fill;
+        staged = cnt <= stage_cap;
+        __syncthreads();
+        if (!staged && threadIdx.x == 0) s_fill = 0;
+        __syncthreads();
     }
-    __syncthreads();
-    const uint32_t cnt = s_fill;
-    const bool staged = cnt <= stage_cap;
-    if (cnt == 1) {  // the bin holds a single value: it is the answer
-        if (threadIdx.x == 0) tau[q] = __uint_as_float(stage[0]);
-        return;
+    if (staged) {  // top 11 bits over the stage
+        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x)
+            atomicAdd(&hist[stage[i] >> 21], stride << tier_shift(stage_t[i], w));
+        __syncthreads();
+        find_bin(hist, rank, &s_bin, &s_rank);
+        __syncthreads();
+        prefix = s_bin;
+        r = s_rank;
+    } else {
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t wt = stride << tier_shift(t, w);
+            const uint32_t n = (uint32_t)(s_seg[t + 1] - s_seg[t]);
+            if (n) for_each_u32(gsrc + s_seg[t], n, [&](uint32_t u) { atomicAdd(&hist[u >> 21], wt); });
+        }
+        __syncthreads();
+        find_bin(hist, rank, &s_bin, &s_rank);
+        __syncthreads();
+        prefix = s_bin;
+        r = s_rank;
+        // optimistic compaction of the selected bin (with each element's tier);
+        // an overfull stage falls back to reading global memory
+        {
+            const uint32_t top = prefix;
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t n = (uint32_t)(s_seg[t + 1] - s_seg[t]);
+                if (n)
+                    for_each_u32(gsrc + s_seg[t], n, [&](uint32_t u) {
+                        if ((u >> 21) == top) {
+                            const uint32_t k = atomicAdd(&s_fill, 1u);
+                            if (k < stage_cap) {
+                                stage[k] = u;
+                                stage_t[k] = (uint8_t)t;
+                            }
+                        }
+                    });
+            }
+        }
+        __syncthreads();
+        cnt = s_fill;
+        staged = cnt <= stage_cap;
+        if (cnt == 1) {  // the bin holds a single value: it is the answer
+            if (threadIdx.x == 0) tau[q] = __uint_as_float(stage[0]);
+            return;
+        }
     }
     const int shifts[2] = {10, 0};
     const int widths[2] = {11, 10};
@@ -240,6 +298,7 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void select_topk_kernel(
     __shared__ uint32_t hist[NBINS];
     __shared__ uint32_t s_bin, s_rank, s_out, s_bincnt;
     __shared__ u64 s_kth;
+    __shared__ u64 s_mm[2 * SEL_THREADS / 32];
     const size_t q = blockIdx.x;
     const uint32_t n = min(cand_cnt[q], cap);
     uint32_t* spos = reinterpret_cast<uint32_t*>(skeys + slots);
@@ -252,9 +311,31 @@ __global__ __launch_bounds__(SEL_THREADS, 4) void select_topk_kernel(
     __syncthreads();
     u64 kth = ~0ull;
     if (n > kprime) {
-        u64 prefix = 0;
+        // the candidates' distances share their leading bits (all are <= tau and
+        // >= the nearest entry): start below the common prefix of the smallest
+        // and the largest key, or the first pass would put every atomic on one bin
+        u64 kmin = ~0ull, kmax = 0ull;
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+            kmin = min(kmin, skeys[i]);
+            kmax = max(kmax, skeys[i]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            s_mm[2 * (threadIdx.x >> 5)] = kmin;
+            s_mm[2 * (threadIdx.x >> 5) + 1] = kmax;
+        }
+        __syncthreads();
+        for (uint32_t i = 0; i < blockDim.x / 32; ++i) {
+            kmin = min(kmin, s_mm[2 * i]);
+            kmax = max(kmax, s_mm[2 * i + 1]);
+        }
+        int consumed = kmin == kmax ? 0 : __clzll((long long)(kmin ^ kmax));
+        u64 prefix = consumed ? kmin >> (64 - consumed) : 0ull;
         uint32_t r = kprime;
-        int consumed = 0;
         while (consumed < 64) {
             const int wd = min(RADIX_BITS, 64 - consumed);
             const int sh = 64 - consumed - wd;
@@ -657,7 +738,7 @@ void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uin
                         uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
                         cudaStream_t s, uint32_t max_rank) {
     if (nq == 0) return;
-    query_sizes_kernel<<<(unsigned)((nq + 127) / 128), 128, 0, s>>>(
+    query_sizes_kernel<<<(unsigned)((nq + 3) / 4), 128, 0, s>>>(
         probes, nq, w, list_len, stride, tiered, cap, nq_entries, query_sampled, pair_samples,
         reinterpret_cast<unsigned long long*>(grand_total), max_rank);
     PQRR_LAUNCH_CHECK();
@@ -678,7 +759,9 @@ void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_of
     const uint32_t stage_cap = std::min<uint32_t>(max_samples, 8 * 1024);
     const size_t smem = (size_t)std::max<uint32_t>(stage_cap, 1) * (sizeof(uint32_t) + 1) + 16;
     set_smem((const void*)sample_threshold_kernel, smem);
-    sample_threshold_kernel<<<(unsigned)nq, SEL_THREADS, smem, s>>>(
+    // few queries: 1024 threads each (the passes over a query's samples are latency bound)
+    const int thr = nq <= (size_t)2 * sm_count() ? THR_THREADS_MAX : SEL_THREADS;
+    sample_threshold_kernel<<<(unsigned)nq, thr, smem, s>>>(
         sample_dist, sample_off, w, query_sampled, alpha_k, stride, tiered, stage_cap, tau);
     PQRR_LAUNCH_CHECK();
     count_launch();
@@ -690,10 +773,17 @@ void launch_select_topk(const float* cand_dist, const uint32_t* cand_pos, const 
                         uint32_t* sl_cnt, cudaStream_t s,
                         const uint32_t* cand_mm, bool need_ids) {
     if (nq == 0) return;
-    if (!sorted) {  // unsorted shortlist (re-ranked next): warp per query
-        launch_select_warp(cand_dist, cand_pos, cand_cnt, cap, nq, ids, kprime, sl_key, sl_pos, sl_cnt, s,
-                           cand_mm, need_ids);
-        return;
+    if (!sorted) {
+        // unsorted shortlist (re-ranked next): warp per query; a batch too
+        // small to fill the GPU with warps gives each query a CTA (C5 batch 1:
+        // 0.052 -> 0.012 ms)
+        const bool cta = nq < (size_t)2 * sm_count() && need_ids && (size_t)cap * 12 <= 96 * 1024;
+        if (!cta) {
+            launch_select_warp(cand_dist, cand_pos, cand_cnt, cap, nq, ids, kprime, sl_key, sl_pos, sl_cnt, s,
+                               cand_mm, need_ids);
+            return;
+        }
+        max_n = cap;
     }
     uint32_t kp2 = 1;
     while (kp2 < kprime) kp2 <<= 1;
@@ -750,7 +840,9 @@ void launch_rerank(const uint64_t* sl_key, const uint32_t* sl_pos, const uint32_
         launch_rerank_pair(sl_key, sl_pos, sl_cnt, sl_stride, nq, xq, block_list, coarse, codes, books,
                            rcodes, rbooks, mprime, rd, ri, s, ids_for_keys);
         if (ev_dist_done) PQRR_CUDA(cudaEventRecord(ev_dist_done, s));
-        if (!launch_rerank_topk_warp(rd, ri, sl_cnt, sl_stride, nq, k, out_ids, out_dists, out_cnt, s)) {
+        // (a batch too small to fill the GPU with warps gives each query a CTA)
+        if (nq < (size_t)2 * sm_count() ||
+            !launch_rerank_topk_warp(rd, ri, sl_cnt, sl_stride, nq, k, out_ids, out_dists, out_cnt, s)) {
             set_smem((const void*)rerank_topk_kernel, (size_t)k2 * 8);
             rerank_topk_kernel<<<(unsigned)nq, SEL_THREADS, (size_t)k2 * 8, s>>>(
                 rd, ri, sl_cnt, sl_stride, k, k2, out_ids, out_dists, out_cnt);

@@ -123,15 +123,23 @@ __global__ void iota_base_kernel(uint32_t* out, size_t n, uint32_t base) {
     if (i < n) out[i] = base + (uint32_t)i;
 }
 
+// Status word of an enqueue-only search (no host round trip inside the batch):
+// a set bit means the batch must be redone on the synchronising path.
+constexpr uint32_t kStatusCoarseOverflow = 1u;  // a certified coarse candidate set overflowed
+constexpr uint32_t kStatusThreshold = 2u;       // a query's sampled threshold failed its exactness check
+
 // le (optional): per query, how many candidates have an exact distance <= tau
 // (the filter path keeps a superset of those in the buffer).
 __global__ void check_fail_kernel(const uint8_t* __restrict__ sampled, const uint32_t* __restrict__ cnt,
                                   const uint32_t* __restrict__ le, size_t nq, uint32_t kprime,
                                   uint32_t cap, uint8_t* __restrict__ fail, unsigned* __restrict__ max_n,
                                   unsigned long long* __restrict__ total,
-                                  unsigned long long* __restrict__ total_le) {
+                                  unsigned long long* __restrict__ total_le,
+                                  const uint32_t* __restrict__ coarse_ovf, uint32_t* __restrict__ status) {
     size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
+    // enqueue-only search: the host reads one status word after the batch
+    if (status && q == 0 && coarse_ovf && *coarse_ovf) atomicOr(status, kStatusCoarseOverflow);
     atomicMax(max_n, min(cnt[q], cap));
     atomicAdd(total, (unsigned long long)cnt[q]);
     if (le) atomicAdd(total_le, (unsigned long long)le[q]);
@@ -143,6 +151,7 @@ __global__ void check_fail_kernel(const uint8_t* __restrict__ sampled, const uin
         if (exact < kprime) f = 1;  // threshold too tight: shortlist may be incomplete
     }
     fail[q] = f;
+    if (status && f) atomicOr(status, kStatusThreshold);
 }
 
 __global__ void gather_rows_f32(const float* __restrict__ x, uint32_t d, const uint32_t* __restrict__ rows,
@@ -359,6 +368,8 @@ struct DevIndex {
     DBuf<uint32_t> list_len;
     std::vector<uint64_t> h_off;
     std::vector<uint32_t> h_len;
+    std::vector<uint32_t> h_len_desc;  // list lengths, longest first (bounds of the enqueue-only search)
+    uint64_t h_len_desc_n = ~0ull;
     DBuf<uint8_t> codes, rcodes;
     DBuf<uint32_t> ids;
     DBuf<uint16_t> block_list;  // list of each 16-entry block of positions
@@ -380,8 +391,52 @@ struct DevIndex {
     DBuf<uint8_t> st_codes, st_rcodes;
     pqrr_dev_search_stats stats{};
     cudaEvent_t ev[13] = {};
+    // enqueue-only search: cached graphs, the device status block
+    // ([0..3] min_count flag, [4] status bits) and its pinned host copy,
+    // staging buffers with stable addresses for the host-buffer API
+    struct SearchGraph {
+        const void* xq = nullptr;
+        size_t nq = 0, kprime = 0, k = 0;
+        uint32_t w = 0;
+        const void *oi = nullptr, *od = nullptr, *oc = nullptr;
+        bool q_u8 = false;
+        uint64_t sig = 0;
+        cudaGraphExec_t exec = nullptr;
+        uint32_t kernels = 0;
+        uint64_t used = 0;
+    };
+    std::vector<SearchGraph> graphs;
+    uint64_t graph_clock = 0;
+    bool graph_enabled = true;  // pqrr_dev_index_set_graph
+    DBuf<uint32_t> d_stat;
+    uint32_t* h_stat = nullptr;
+    DBuf<uint8_t> sg_qu8;
+    DBuf<float> sg_xq, sg_od;
+    DBuf<uint32_t> sg_oi, sg_oc;
+    cudaEvent_t ev_fast[2] = {};
+    // the enqueued search pqrr_dev_search_finish completes
+    struct Pending {
+        bool on = false;
+        const uint8_t* d_queries = nullptr;
+        size_t nq = 0, kprime = 0, k = 0;
+        uint32_t w = 0;
+        uint32_t* oi = nullptr;
+        float* od = nullptr;
+        uint32_t* oc = nullptr;
+        cudaStream_t user = nullptr;
+    } pending;
+
+    void drop_graphs() {
+        for (auto& g : graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        graphs.clear();
+    }
 
     ~DevIndex() {
+        drop_graphs();
+        if (h_stat) cudaFreeHost(h_stat);
+        for (auto& e : ev_fast)
+            if (e) cudaEventDestroy(e);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
@@ -694,7 +749,11 @@ ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_
     return it;
 }
 
-void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_len, cudaStream_t s) {
+// n_items may be an upper bound (enqueue-only search, `padded`): the slots
+// past the real count keep an all-ones sort key, so they sort last and no
+// kernel reaches them (every kernel reads the real count from item_off[c]).
+void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_len, cudaStream_t s,
+                  bool padded = false) {
     const uint32_t n = it.n_items;
     it.item_list = ws.alloc<uint32_t>(n);
     it.item_start = ws.alloc<uint32_t>(n);
@@ -705,6 +764,7 @@ void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_l
     uint32_t* key2 = ws.alloc<uint32_t>(n);
     uint32_t* iota = ws.alloc<uint32_t>(n);
     it.item_order = ws.alloc<uint32_t>(n);
+    if (padded) PQRR_CUDA(cudaMemsetAsync(key, 0xff, (size_t)std::max<uint32_t>(n, 1) * 4, s));
     launch_items_build(it.list_cnt, it.list_first, list_len, c, it.item_off, it.item_list,
                        it.item_start, it.item_nq, it.item_e0, it.item_e1, key, it.qt, s, it.chunk, n);
     launch_iota(iota, n, s);
@@ -729,15 +789,73 @@ double default_spq(uint32_t kprime, uint32_t w) {
     return kprime >= 4096 ? 128.0 : (kprime >= 512 && w < 32 ? 96.0 : 64.0);
 }
 
+// ---- enqueue-only search (no host round trip inside the batch) ----
+// The synchronising path reads four kinds of counts back before it sizes its
+// buffers: work items per item set, threshold samples, the coarse overflow
+// flag and the per-query exactness check.  The enqueue-only path replaces the
+// counts by host-side upper bounds (from the list lengths the host holds) and
+// folds the two flags into one device status word that the caller reads with
+// the results; a set bit sends the batch to the synchronising path.  Every
+// kernel takes its real counts from device memory, so both paths run the same
+// kernels on the same data and return the same bits.
+struct FastBounds {
+    bool two_phase = false;
+    uint32_t R1 = 0, fchunk = 1u << 30;
+    uint32_t items_all = 0, items_f64 = 0, items_near = 0, items_far = 0;
+    uint64_t samples = 0;
+    size_t q8_items = 0;
+    double bytes = 0;  // scratch the bounds ask for
+};
+
+uint32_t items_bound(size_t np, uint32_t c, uint32_t qt) {
+    // sum over lists of ceil(cnt / qt) with sum cnt = np
+    const size_t lists = std::min<size_t>(np, c);
+    return (uint32_t)std::min<size_t>(np, lists + np / qt);
+}
+
+const std::vector<uint32_t>& lens_desc(DevIndex& ix) {
+    if (ix.h_len_desc_n != ix.n || ix.h_len_desc.size() != ix.h_len.size()) {
+        ix.h_len_desc = ix.h_len;
+        std::sort(ix.h_len_desc.begin(), ix.h_len_desc.end(), std::greater<uint32_t>());
+        ix.h_len_desc_n = ix.n;
+    }
+    return ix.h_len_desc;
+}
+
 // Builds the exact top-kprime shortlist of every query into `out` (device,
 // [nq][kprime]).  alpha scales the sampled threshold rank (expected
 // candidates ~ alpha * kprime).
-void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32_t kprime,
-                    bool sorted, double alpha, uint32_t stride_div, ShortlistDev out, int depth,
-                    bool timed, uint32_t cap_shift = 0, bool exact_coarse = false) {
-    cudaStream_t s = ix.stream;
-    auto& st = ix.stats;
+// Lazy state of the tensor-core coarse stage (|C_l|^2 and their maximum, the
+// fp16 hi/lo centroid split); synchronises on first use, so the enqueue-only
+// path calls it before it starts capturing.
+AssignTc* prepare_coarse_tc(DevIndex& ix, uint32_t w) {
     const uint32_t c = ix.c;
+    cudaStream_t s = ix.stream;
+    if (!(c >= 1024u && coarse_tc_supported(ix.d, w))) return nullptr;
+    if (!ix.cnorm.p) {
+        ix.cnorm.alloc(c);
+        launch_coarse_norms(ix.coarse.p, c, ix.d, ix.cnorm.p, s);
+        std::vector<float> h(c);
+        PQRR_CUDA(cudaMemcpyAsync(h.data(), ix.cnorm.p, c * sizeof(float), cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaStreamSynchronize(s));
+        ix.cnorm_max = *std::max_element(h.begin(), h.end());
+    }
+    // u8 queries (exact in fp16): D~ on tcgen05 with the add path's
+    // centroid split; float queries: mma.sync TF32
+    return (ix.q_u8 && assign_tc_supported(ix.d, c) && ix.atc.prepare(ix.coarse.p, c, s)) ? &ix.atc : nullptr;
+}
+
+// Shape decisions of one shortlist batch (shared by the synchronising and the
+// enqueue-only path).
+struct Plan {
+    bool filter_ok, coarse_tc, two_phase;
+    uint32_t cap, stride, R1, fchunk;
+    int tiered;
+};
+
+Plan make_plan(const DevIndex& ix, size_t nq, uint32_t w, uint32_t kprime, double alpha,
+               uint32_t stride_div, uint32_t cap_shift, bool exact_coarse) {
+    Plan pl{};
     const size_t P = nq * (size_t)w;
     // K4f (filter + exact recheck) unless disabled or out of its envelope:
     // m = 8, ks = 256, w*d residuals in shared memory, and an 8-bit LUT cache
@@ -747,52 +865,21 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         const char* e = getenv("PQRR_SCAN");
         return e && std::string(e) == "exact";
     }();
-    const bool filter_ok = !exact_env && ix.m == 8 && ix.ks == 256 && recheck_supported(ix.d, ix.m, w);
+    pl.filter_ok = !exact_env && ix.m == 8 && ix.ks == 256 && recheck_supported(ix.d, ix.m, w);
     // candidate buffer per query: the sampled threshold targets ~2k' entries;
     // >= 4k' for the exact scan, >= 8k' for the filter's superset; beyond
     // 8192 the selector streams candidates from global memory
-    const uint32_t cap_mul = filter_ok ? 8 : 4;
-    const uint32_t cap = std::max<uint32_t>(8192, ((cap_mul * kprime + 1023) / 1024) * 1024) << cap_shift;
+    const uint32_t cap_mul = pl.filter_ok ? 8 : 4;
+    pl.cap = std::max<uint32_t>(8192, ((cap_mul * kprime + 1023) / 1024) * 1024) << cap_shift;
     // sample density: ~64 samples expected below the alpha*k'-th distance
     // tuning hook (read per search): expected samples below the target rank
     const double spq = default_spq(kprime, w);  // samples expected below the target rank
     uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / spq));
-    stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
-    Workspace ws(s);
-
-    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[0], s));
-    // ---- K1: coarse distances + top-w probes.  Kc >= 1024: tensor-core
-    // distances with a certified candidate set recomputed exactly
-    // (k_coarse_tc.cu); a query whose candidate set overflows restarts the
-    // batch on the exact CUDA-core path (checked at the first readback below)
-    float* D = ws.alloc<float>(nq * (size_t)c);
-    uint32_t* probes = ws.alloc<uint32_t>(P);
-    const bool coarse_tc = !exact_coarse && c >= 1024u && coarse_tc_supported(ix.d, w);
-    uint32_t* coarse_ovf = ws.zeros<uint32_t>(1);
-    if (coarse_tc) {
-        if (!ix.cnorm.p) {
-            ix.cnorm.alloc(c);
-            launch_coarse_norms(ix.coarse.p, c, ix.d, ix.cnorm.p, s);
-            std::vector<float> h(c);
-            PQRR_CUDA(cudaMemcpyAsync(h.data(), ix.cnorm.p, c * sizeof(float), cudaMemcpyDeviceToHost, s));
-            PQRR_CUDA(cudaStreamSynchronize(s));
-            ix.cnorm_max = *std::max_element(h.begin(), h.end());
-        }
-        // u8 queries (exact in fp16): D~ on tcgen05 with the add path's
-        // centroid split; float queries: mma.sync TF32
-        AssignTc* atc = (ix.q_u8 && assign_tc_supported(ix.d, c) && ix.atc.prepare(ix.coarse.p, c, s))
-                            ? &ix.atc : nullptr;
-        launch_coarse_tc(xq, nq, ix.coarse.p, c, ix.cnorm.p, ix.cnorm_max, w, D, probes, coarse_ovf, s, atc);
-    } else {
-        launch_pair_dists(xq, nq, ix.coarse.p, c, ix.d, D, s);
-        launch_topw(D, nq, c, w, probes, nullptr, s);
-    }
-    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[1], s));
-
-    // ---- invert probes into list-major work items: 16-query items for the
-    // LUT pass (and the exact scan), 64-query items for the K4f filter
-    uint32_t* pair_ids = ws.alloc<uint32_t>(P);
-    launch_iota(pair_ids, P, s);
+    pl.stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
+    // (up to 64 queries the exact CUDA-core distances cost one 64-row tile
+    // pass over the centroids and need no certification: C5 batch 1 coarse
+    // stage 0.11 -> 0.03 ms)
+    pl.coarse_tc = !exact_coarse && nq > 64 && ix.c >= 1024u && coarse_tc_supported(ix.d, w);
     // Two-phase LUT pass (w >= 32): the near probes (rank < w/8, the sampling
     // tier 0, where the shortlist lives at C3-C5) get the full LUT pass with
     // sampling, which fixes tau; the far probes get a bound pass (exact LUTs,
@@ -805,18 +892,113 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     constexpr uint32_t kTwoPhaseW = 32u, kR1Div = 8u;
     // (large batches only: for a few hundred pairs the extra item sets and
     // launches cost more than the LUT builds they save)
-    const bool two_phase = filter_ok && w >= kTwoPhaseW &&
-                           P >= (size_t)64 * sm_count() &&
-                           lut_pass_supported(ix.d, ix.m, ix.ks);
-    const uint32_t R1 = two_phase ? (w + kR1Div - 1) / kR1Div : w;
-    // all pairs: the single-phase LUT pass items, or (two-phase) only the
-    // per-list counts that place the K4f live pairs
-    ItemSet im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w, D,
-                              probes, two_phase);
+    pl.two_phase = pl.filter_ok && w >= kTwoPhaseW && P >= (size_t)64 * sm_count() &&
+                   lut_pass_supported(ix.d, ix.m, ix.ks);
+    pl.R1 = pl.two_phase ? (w + kR1Div - 1) / kR1Div : w;
     // small batches (few query-list pairs per SM): K4f items split long lists
     // into chunks so one list does not serialise on one SM
-    const uint32_t fchunk = P < (size_t)64 * sm_count() ? 16384u : (1u << 30);
-    ItemSet if64 = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kFQ, s, &im, fchunk);
+    pl.fchunk = P < (size_t)64 * sm_count() ? 16384u : (1u << 30);
+    // importance-weighted sampling needs the warp-specialised LUT pass
+    pl.tiered = (w >= 8 && lut_pass_supported(ix.d, ix.m, ix.ks)) ? 1 : 0;
+    return pl;
+}
+
+FastBounds fast_bounds(DevIndex& ix, const Plan& pl, size_t nq, uint32_t w, uint32_t kprime) {
+    FastBounds b;
+    const size_t P = nq * (size_t)w;
+    const uint32_t c = ix.c;
+    b.two_phase = pl.two_phase;
+    b.R1 = pl.R1;
+    b.fchunk = pl.fchunk;
+    const auto& ld = lens_desc(ix);
+    const uint32_t max_len = ld.empty() ? 0u : ld[0];
+    b.items_all = items_bound(P, c, kQT);
+    const uint32_t chunks = std::max<uint32_t>(1, (uint32_t)(((uint64_t)max_len + pl.fchunk - 1) / pl.fchunk));
+    b.items_f64 = items_bound(P, c, kFQ) * chunks;
+    if (pl.two_phase) {
+        b.items_near = items_bound(nq * (size_t)pl.R1, c, kQT);
+        b.items_far = items_bound(nq * (size_t)(w - pl.R1), c, kQT);
+    }
+    // threshold samples of one query: its probes' lists sampled at the stride
+    // of their rank tier; the longest lists at the densest tiers bound any probe set
+    uint64_t per_q = 0;
+    for (uint32_t r = 0; r < pl.R1 && r < ld.size(); ++r) {
+        const uint64_t st = (uint64_t)pl.stride << tier_shift(sample_tier(r, w, pl.tiered), w);
+        per_q += (ld[r] + st - 1) / st;
+    }
+    b.samples = per_q * nq;
+    b.q8_items = pl.filter_ok ? (size_t)(pl.two_phase ? b.items_near + b.items_far : b.items_all) : 0;
+    const double items = (double)b.items_all + b.items_f64 + b.items_near + b.items_far;
+    b.bytes = (double)b.samples * 4.0 + (double)b.q8_items * (8.0 * 256 * kQT + kQT * 8.0) + items * 40.0 +
+              (double)nq * ((double)pl.cap * 16.0 + c * 4.0 + (double)kprime * 16.0) + (double)P * 64.0;
+    return b;
+}
+
+void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32_t kprime,
+                    bool sorted, double alpha, uint32_t stride_div, ShortlistDev out, int depth,
+                    bool timed, uint32_t cap_shift = 0, bool exact_coarse = false,
+                    uint32_t* fast_status = nullptr) {
+    cudaStream_t s = ix.stream;
+    auto& st = ix.stats;
+    const uint32_t c = ix.c;
+    const size_t P = nq * (size_t)w;
+    const Plan pl = make_plan(ix, nq, w, kprime, alpha, stride_div, cap_shift, exact_coarse);
+    const bool filter_ok = pl.filter_ok;
+    const uint32_t cap = pl.cap, stride = pl.stride;
+    // enqueue-only: host-side bounds stand in for the counts read back below
+    const bool fast = fast_status != nullptr;
+    FastBounds fb;
+    if (fast) fb = fast_bounds(ix, pl, nq, w, kprime);
+    Workspace ws(s);
+
+    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[0], s));
+    // ---- K1: coarse distances + top-w probes.  Kc >= 1024: tensor-core
+    // distances with a certified candidate set recomputed exactly
+    // (k_coarse_tc.cu); a query whose candidate set overflows restarts the
+    // batch on the exact CUDA-core path (checked at the first readback below)
+    float* D = ws.alloc<float>(nq * (size_t)c);
+    uint32_t* probes = ws.alloc<uint32_t>(P);
+    const bool coarse_tc = pl.coarse_tc;
+    uint32_t* coarse_ovf = ws.zeros<uint32_t>(1);
+    if (coarse_tc) {
+        AssignTc* atc = prepare_coarse_tc(ix, w);
+        launch_coarse_tc(xq, nq, ix.coarse.p, c, ix.cnorm.p, ix.cnorm_max, w, D, probes, coarse_ovf, s, atc);
+    } else {
+        launch_pair_dists(xq, nq, ix.coarse.p, c, ix.d, D, s);
+        launch_topw(D, nq, c, w, probes, nullptr, s);
+    }
+    if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[1], s));
+
+    // ---- invert probes into list-major work items: 16-query items for the
+    // LUT pass (and the exact scan), 64-query items for the K4f filter
+    // (small batches: the whole inversion in two single-CTA launches, k_invert.cu)
+    const bool small_inv = !pl.two_phase && invert_small_supported(P, c);
+    uint32_t* pair_ids = ws.alloc<uint32_t>(P);
+    if (!small_inv) launch_iota(pair_ids, P, s);
+    // two-phase LUT pass: see make_plan
+    const bool two_phase = pl.two_phase;
+    const uint32_t R1 = pl.R1;
+    // all pairs: the single-phase LUT pass items, or (two-phase) only the
+    // per-list counts that place the K4f live pairs
+    const uint32_t fchunk = pl.fchunk;
+    ItemSet im, if64;
+    if (small_inv) {
+        im.c = if64.c = c;
+        im.qt = kQT;
+        if64.qt = kFQ;
+        if64.chunk = fchunk;
+        im.pair_sorted = if64.pair_sorted = ws.alloc<uint32_t>(P);
+        im.list_cnt = if64.list_cnt = ws.alloc<uint32_t>(c + 1);
+        im.list_first = if64.list_first = ws.alloc<uint32_t>(c + 1);
+        im.item_off = ws.alloc<uint32_t>(c + 1);
+        if64.item_off = ws.alloc<uint32_t>(c + 1);
+        launch_invert_small(probes, (uint32_t)P, w, D, c, ix.list_len.p, kQT, kFQ, fchunk, im.pair_sorted,
+                            im.list_cnt, im.list_first, im.item_off, if64.item_off, s);
+    } else {
+        im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w, D, probes,
+                          two_phase);
+        if64 = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kFQ, s, &im, fchunk);
+    }
     ItemSet im_near, im_far;
     if (two_phase) {
         const size_t pn = nq * (size_t)R1, pf = nq * (size_t)(w - R1);
@@ -834,24 +1016,34 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     uint8_t* sampled = ws.alloc<uint8_t>(nq);
     uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
     uint64_t* grand = ws.zeros<uint64_t>(2);
-    // importance-weighted sampling needs the warp-specialised LUT pass
-    const int tiered = (w >= 8 && lut_pass_supported(ix.d, ix.m, ix.ks)) ? 1 : 0;
+    const int tiered = pl.tiered;
     launch_query_sizes(probes, nq, w, ix.list_len.p, stride, tiered, cap, n_entries, sampled,
                        pair_samples, grand, s, R1);
     uint64_t* sample_off = ws.alloc<uint64_t>(P + 1);
     exclusive_scan_u64(pair_samples, sample_off, P + 1, s);
     uint64_t total_samples = 0, h_grand[2] = {0, 0};
-    PQRR_CUDA(cudaMemcpyAsync(h_grand, grand, 16, cudaMemcpyDeviceToHost, s));
-    PQRR_CUDA(cudaMemcpyAsync(&total_samples, sample_off + P, 8, cudaMemcpyDeviceToHost, s));
-    PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
-    PQRR_CUDA(cudaMemcpyAsync(&if64.n_items, if64.item_off + c, 4, cudaMemcpyDeviceToHost, s));
-    if (two_phase) {
-        PQRR_CUDA(cudaMemcpyAsync(&im_near.n_items, im_near.item_off + c, 4, cudaMemcpyDeviceToHost, s));
-        PQRR_CUDA(cudaMemcpyAsync(&im_far.n_items, im_far.item_off + c, 4, cudaMemcpyDeviceToHost, s));
-    }
     uint32_t h_ovf = 0;
-    if (coarse_tc) PQRR_CUDA(cudaMemcpyAsync(&h_ovf, coarse_ovf, 4, cudaMemcpyDeviceToHost, s));
-    PQRR_CUDA(cudaStreamSynchronize(s));
+    if (fast) {
+        // bounds instead of the readback; the kernels read the real counts on
+        // the device, the coarse overflow flag joins the status word
+        total_samples = fb.samples;
+        h_grand[1] = 8192;  // the threshold kernel's staging capacity
+        im.n_items = fb.items_all;
+        if64.n_items = fb.items_f64;
+        im_near.n_items = fb.items_near;
+        im_far.n_items = fb.items_far;
+    } else {
+        PQRR_CUDA(cudaMemcpyAsync(h_grand, grand, 16, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaMemcpyAsync(&total_samples, sample_off + P, 8, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaMemcpyAsync(&if64.n_items, if64.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+        if (two_phase) {
+            PQRR_CUDA(cudaMemcpyAsync(&im_near.n_items, im_near.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+            PQRR_CUDA(cudaMemcpyAsync(&im_far.n_items, im_far.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+        }
+        if (coarse_tc) PQRR_CUDA(cudaMemcpyAsync(&h_ovf, coarse_ovf, 4, cudaMemcpyDeviceToHost, s));
+        PQRR_CUDA(cudaStreamSynchronize(s));
+    }
     if (h_ovf) {  // rare: a certified candidate set did not fit; redo on the exact path
         shortlist_core(ix, xq, nq, w, kprime, sorted, alpha, stride_div, out, depth, timed, cap_shift, true);
         return;
@@ -861,6 +1053,8 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     bool use_filter = filter_ok;
     if (use_filter) {
         const size_t need = (size_t)n_items * 8 * 256 * kQT;
+        // (enqueue-only: ensure_fast sized the cache to the bound before the capture)
+        if (fast && ix.q8_cache.bytes() < need) throw std::runtime_error("enqueue-only search: LUT cache not prepared");
         if (ix.q8_cache.bytes() < need) {
             size_t free_b = 0, total_b = 0;
             PQRR_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -871,6 +1065,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         }
         use_filter = ix.q8_cache.bytes() >= need;
     }
+    if (two_phase && !use_filter && fast) throw std::runtime_error("enqueue-only search: LUT cache not prepared");
     if (two_phase && !use_filter) {
         // rare (no room for the 8-bit LUT cache): the exact scan needs the
         // sorted all-pairs items after all
@@ -878,11 +1073,30 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaStreamSynchronize(s));
     }
-    if (!two_phase || !use_filter) items_phase2(ws, im, c, ix.list_len.p, s);
-    if (use_filter) items_phase2(ws, if64, c, ix.list_len.p, s);
+    if (small_inv && im.n_items <= kInvertSmallMaxItems &&
+        (!use_filter || if64.n_items <= kInvertSmallMaxItems)) {
+        auto prep = [&](ItemSet& it) {
+            const uint32_t n = std::max<uint32_t>(it.n_items, 1);
+            it.item_list = ws.alloc<uint32_t>(n);
+            it.item_start = ws.alloc<uint32_t>(n);
+            it.item_nq = ws.alloc<uint32_t>(n);
+            it.item_e0 = ws.alloc<uint32_t>(n);
+            it.item_e1 = ws.alloc<uint32_t>(n);
+            it.item_order = ws.alloc<uint32_t>(n);
+            return SmallItems{it.item_off, it.item_list, it.item_start, it.item_nq, it.item_e0, it.item_e1,
+                              it.item_order, it.qt, it.chunk, it.n_items};
+        };
+        const SmallItems sa = prep(im);
+        SmallItems sb{};
+        if (use_filter) sb = prep(if64);
+        launch_items_finish_small(im.list_cnt, im.list_first, ix.list_len.p, c, sa, use_filter ? &sb : nullptr, s);
+    } else {
+        if (!two_phase || !use_filter) items_phase2(ws, im, c, ix.list_len.p, s, fast);
+        if (use_filter) items_phase2(ws, if64, c, ix.list_len.p, s, fast);
+    }
     if (two_phase) {
-        items_phase2(ws, im_near, c, ix.list_len.p, s);
-        items_phase2(ws, im_far, c, ix.list_len.p, s);
+        items_phase2(ws, im_near, c, ix.list_len.p, s, fast);
+        items_phase2(ws, im_far, c, ix.list_len.p, s, fast);
     }
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[2], s));
 
@@ -1041,7 +1255,8 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     uint8_t* fail = ws.alloc<uint8_t>(nq);
     check_fail_kernel<<<nblk(nq), 256, 0, s>>>(sampled, cand_cnt, cand_le, nq, kprime, cap, fail,
                                                 maxn, reinterpret_cast<unsigned long long*>(maxn + 2),
-                                                reinterpret_cast<unsigned long long*>(maxn + 4));
+                                                reinterpret_cast<unsigned long long*>(maxn + 4),
+                                                coarse_tc ? coarse_ovf : nullptr, fast_status);
     PQRR_LAUNCH_CHECK();
     count_launch();
     // the unsorted selection (a re-rank follows) needs no host-side count:
@@ -1053,6 +1268,15 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
                            reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s, cand_mm,
                            ix.keys_need_ids);
         if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[6], s));
+    }
+    if (fast) {
+        // no readback: failed rows are flagged in the status word (the caller
+        // redoes the batch on the synchronising path); the sorted selection
+        // sizes its staging by the buffer capacity instead of the largest count
+        if (!early_select)
+            launch_select_topk(cand_dist, cand_pos, cand_cnt, cap, cap, nq, ix.ids.p, kprime, sorted,
+                               reinterpret_cast<uint64_t*>(out.key), out.pos, out.cnt, s);
+        return;
     }
     std::vector<uint8_t> h_fail(nq);
     unsigned h_maxn[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1133,22 +1357,218 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     }
 }
 
+// ---- enqueue-only search: one CUDA graph per (shape, buffers) ----
+// Small batches are launch- and round-trip-bound (C5 batch 1: 37 kernels and
+// three host synchronisations for 0.2 ms of device work), so the whole search
+// is captured once per shape into a graph (host-side bounds instead of
+// readbacks, see FastBounds) and replayed with one launch.  Larger batches
+// stay on the synchronising path: their two round trips are noise against
+// tens of milliseconds, and a failed threshold there retries only its row.
+constexpr size_t kFastMaxQueries = 1024;
+
+uint64_t index_signature(const DevIndex& ix) {
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+    auto mix = [&](uint64_t v) { h = (h ^ v) * 0xbf58476d1ce4e5b9ull; h ^= h >> 29; };
+    for (const void* p : {(const void*)ix.codes.p, (const void*)ix.rcodes.p, (const void*)ix.ids.p,
+                          (const void*)ix.list_off.p, (const void*)ix.list_len.p, (const void*)ix.coarse.p,
+                          (const void*)ix.books.p, (const void*)ix.rbooks.p, (const void*)ix.block_list.p,
+                          (const void*)ix.q8_cache.p, (const void*)ix.q8_param.p, (const void*)ix.cnorm.p,
+                          (const void*)ix.atc.hi, (const void*)ix.d_stat.p})
+        mix((uint64_t)(uintptr_t)p);
+    mix(ix.n);
+    mix(ix.slots);
+    return h;
+}
+
+// Whether the batch may take the enqueue-only path; allocates what the
+// capture must not (status block, LUT cache sized to the bounds, lazy coarse state).
+bool ensure_fast(DevIndex& ix, size_t nq, uint32_t w, uint32_t kprime, uint32_t k) {
+    if (!ix.graph_enabled || nq == 0 || nq > kFastMaxQueries) return false;
+    static size_t dev_total = 0;
+    if (!dev_total) {
+        size_t f = 0;
+        PQRR_CUDA(cudaMemGetInfo(&f, &dev_total));
+    }
+    const Plan pl = make_plan(ix, nq, w, kprime, default_alpha(kprime, w), 1, 0, false);
+    const FastBounds fb = fast_bounds(ix, pl, nq, w, kprime);
+    if (fb.bytes > 0.125 * (double)dev_total) return false;
+    if (!ix.d_stat.p) {
+        ix.d_stat.alloc(8);
+        PQRR_CUDA(cudaMallocHost(&ix.h_stat, 8 * sizeof(uint32_t)));
+        for (auto& e : ix.ev_fast) PQRR_CUDA(cudaEventCreate(&e));
+    }
+    if (pl.filter_ok) {
+        const size_t need = fb.q8_items * 8 * 256 * kQT;
+        if (ix.q8_cache.bytes() < need) {
+            // (the stream may still read the old cache)
+            PQRR_CUDA(cudaStreamSynchronize(ix.stream));
+            ix.q8_cache.alloc(need);
+            ix.q8_param.alloc(fb.q8_items * kQT * 2);
+        }
+    }
+    if (pl.coarse_tc) prepare_coarse_tc(ix, w);
+    (void)k;
+    return true;
+}
+
+void search_body_fast(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32_t kprime, uint32_t k,
+                      uint32_t* out_ids, float* out_dists, uint32_t* out_cnt) {
+    cudaStream_t s = ix.stream;
+    const bool pair = k > 0 && kprime >= 4096 && rerank_pair_supported(ix.d, ix.m, ix.ks, ix.mprime);
+    ix.keys_need_ids = !pair;
+    PQRR_CUDA(cudaMemsetAsync(ix.d_stat.p, 0, 8 * sizeof(uint32_t), s));
+    Workspace ws(s);
+    ShortlistDev sl{ws.alloc<u64>(nq * (size_t)kprime), ws.alloc<uint32_t>(nq * (size_t)kprime),
+                    ws.alloc<uint32_t>(nq)};
+    shortlist_core(ix, xq, nq, w, kprime, k == 0, default_alpha(kprime, w), 1, sl, 0, false, 0, false,
+                   ix.d_stat.p + 4);
+    min_count_kernel<<<nblk(nq), 256, 0, s>>>(sl.cnt, nq, k, ix.d_stat.p);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+    if (k > 0) {
+        launch_rerank(reinterpret_cast<uint64_t*>(sl.key), sl.pos, sl.cnt, kprime, nq, xq, ix.d,
+                      ix.block_list.p, ix.coarse.p, ix.codes.p, ix.books.p, ix.m, ix.rcodes.p,
+                      ix.rbooks.p, ix.mprime, ix.ks, k, out_ids, out_dists, out_cnt, s, nullptr,
+                      pair ? ix.ids.p : nullptr);
+    } else {
+        launch_unpack_keys(reinterpret_cast<uint64_t*>(sl.key), sl.cnt, nq, kprime, out_ids, out_dists, s);
+        PQRR_CUDA(cudaMemcpyAsync(out_cnt, sl.cnt, nq * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    PQRR_CUDA(cudaMemcpyAsync(ix.h_stat, ix.d_stat.p, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+}
+
+// Enqueues the whole search on ix.stream without blocking the host (graph
+// replay; the first call of a shape captures it).  `widen_from` (optional):
+// u8 queries on the device, widened into xq inside the graph.  Returns false
+// if the shape cannot take this path.
+bool search_enqueue(DevIndex& ix, const uint8_t* widen_from, float* xq, size_t nq, uint32_t w,
+                    uint32_t kprime, uint32_t k, uint32_t* out_ids, float* out_dists, uint32_t* out_cnt) {
+    if (!ensure_fast(ix, nq, w, kprime, k)) return false;
+    cudaStream_t s = ix.stream;
+    const uint64_t sig = index_signature(ix);
+    const void* qkey = widen_from ? (const void*)widen_from : (const void*)xq;
+    DevIndex::SearchGraph* g = nullptr;
+    for (auto& c : ix.graphs)
+        if (c.xq == qkey && c.nq == nq && c.w == w && c.kprime == kprime && c.k == k && c.oi == out_ids &&
+            c.od == out_dists && c.oc == out_cnt && c.q_u8 == ix.q_u8) {
+            g = &c;
+            break;
+        }
+    if (g && g->sig != sig) {  // the index moved or grew under the graph
+        if (g->exec) cudaGraphExecDestroy(g->exec);
+        g->exec = nullptr;
+    }
+    if (g && !g->exec && g->sig == sig) return false;  // this shape failed to capture before
+    if (!g || !g->exec) {
+        if (!g) {
+            if (ix.graphs.size() >= 16) {  // evict the least recently used
+                size_t lru = 0;
+                for (size_t i = 1; i < ix.graphs.size(); ++i)
+                    if (ix.graphs[i].used < ix.graphs[lru].used) lru = i;
+                if (ix.graphs[lru].exec) cudaGraphExecDestroy(ix.graphs[lru].exec);
+                ix.graphs.erase(ix.graphs.begin() + lru);
+            }
+            ix.graphs.emplace_back();
+            g = &ix.graphs.back();
+            g->xq = qkey; g->nq = nq; g->w = w; g->kprime = kprime; g->k = k;
+            g->oi = out_ids; g->od = out_dists; g->oc = out_cnt; g->q_u8 = ix.q_u8;
+        }
+        g->sig = sig;
+        cudaGraph_t graph = nullptr;
+        const unsigned long long l0 = launch_count();
+        PQRR_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        bool ok = true;
+        std::string why;
+        try {
+            if (widen_from) launch_widen_u8(widen_from, xq, nq * ix.d, s);
+            search_body_fast(ix, xq, nq, w, kprime, k, out_ids, out_dists, out_cnt);
+        } catch (const std::exception& e) {
+            ok = false;
+            why = e.what();
+        }
+        const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+        if (ce != cudaSuccess || !graph) ok = false;
+        if (ok && cudaGraphInstantiate(&g->exec, graph, 0) != cudaSuccess) {
+            ok = false;
+            g->exec = nullptr;
+        }
+        if (graph) cudaGraphDestroy(graph);
+        if (!ok) {
+            cudaGetLastError();  // clear a capture error; the shape stays on the synchronising path
+            g->exec = nullptr;
+            return false;
+        }
+        g->kernels = (uint32_t)(launch_count() - l0);
+    }
+    g->used = ++ix.graph_clock;
+    PQRR_CUDA(cudaEventRecord(ix.ev_fast[0], s));
+    PQRR_CUDA(cudaGraphLaunch(g->exec, s));
+    PQRR_CUDA(cudaEventRecord(ix.ev_fast[1], s));
+    ix.stats = pqrr_dev_search_stats{};
+    ix.stats.nq = nq;
+    ix.stats.kernels = g->kernels;
+    return true;
+}
+
+// After the enqueued search finished: 0 = results valid, 1 = the batch must be
+// redone on the synchronising path; throws "shortlist too small".
+int search_fast_outcome(DevIndex& ix, uint32_t k) {
+    static const bool force_retry = getenv("PQRR_FORCE_RETRY") != nullptr;  // test hook: take the fallback
+    if (ix.h_stat[4] || force_retry) return 1;
+    if (k > 0 && ix.h_stat[0]) throw ShortlistError();
+    std::memcpy(&ix.stats.rerank_candidates, ix.h_stat + 2, 8);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ix.ev_fast[0], ix.ev_fast[1]);
+    ix.stats.ms_total = ms;
+    return 0;
+}
+
 // Target candidates per query = alpha * k' (the sampled threshold rank);
 // tuning hook PQRR_ALPHA (read per search).
-void search_device(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t kprime_sz,
-                   size_t k_sz, uint32_t* out_ids, float* out_dists, uint32_t* out_cnt) {
+void search_sync(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t kprime_sz, size_t k_sz,
+                 uint32_t* out_ids, float* out_dists, uint32_t* out_cnt);
+
+void validate_search(DevIndex& ix, uint32_t w, size_t kprime_sz, size_t k_sz) {
     if (w < 1 || w > ix.c) throw ArgError("v must satisfy 1 <= v <= c");
     if (kprime_sz < 1) throw ArgError("kprime must be positive");
     if (kprime_sz > 16384) throw UnsupportedError("kprime above 16384 is not supported on the device");
     if (k_sz > kprime_sz) throw ShortlistError();
     if (k_sz > 0 && ix.mprime == 0) throw ArgError("re-ranking needs refinement codes (mprime > 0)");
     finalize(ix);
+}
+
+// `widen_from` (optional): the queries as u8 on the device; xq is then the
+// staging buffer they are widened into (inside the graph on the enqueue-only
+// path).  Small batches replay a captured graph and synchronise once; a batch
+// whose status word is set, and every large batch, runs the synchronising path.
+void search_device(DevIndex& ix, float* xq, size_t nq, uint32_t w, size_t kprime_sz,
+                   size_t k_sz, uint32_t* out_ids, float* out_dists, uint32_t* out_cnt,
+                   const uint8_t* widen_from = nullptr) {
+    validate_search(ix, w, kprime_sz, k_sz);
+    const uint32_t kprime = (uint32_t)kprime_sz, k = (uint32_t)k_sz;
+    cudaStream_t s = ix.stream;
+    if (nq == 0) {
+        ix.stats = pqrr_dev_search_stats{};
+        return;
+    }
+    if (search_enqueue(ix, widen_from, xq, nq, w, kprime, k, out_ids, out_dists, out_cnt)) {
+        PQRR_CUDA(cudaStreamSynchronize(s));
+        if (search_fast_outcome(ix, k) == 0) return;
+        // redo the batch with per-row retries (xq is already widened)
+    } else if (widen_from) {
+        launch_widen_u8(widen_from, xq, nq * ix.d, s);
+    }
+    search_sync(ix, xq, nq, w, kprime_sz, k_sz, out_ids, out_dists, out_cnt);
+}
+
+// The synchronising path: counts read back, per-row threshold retries, stage times.
+void search_sync(DevIndex& ix, const float* xq, size_t nq, uint32_t w, size_t kprime_sz, size_t k_sz,
+                 uint32_t* out_ids, float* out_dists, uint32_t* out_cnt) {
     const uint32_t kprime = (uint32_t)kprime_sz, k = (uint32_t)k_sz;
     cudaStream_t s = ix.stream;
     const unsigned long long l0 = launch_count();
     ix.stats = pqrr_dev_search_stats{};
     ix.stats.nq = nq;
-    if (nq == 0) return;
     for (auto& e : ix.ev)
         if (!e) PQRR_CUDA(cudaEventCreate(&e));
     PQRR_CUDA(cudaEventRecord(ix.ev[10], s));
@@ -1664,23 +2084,35 @@ static int search_host(pqrr_dev_index* h, const float* qf, const uint8_t* qu, si
         DeviceGuard g(ix.device);
         if (nq == 0) return;
         cudaStream_t s = ix.stream;
-        Workspace ws(s);
-        float* xq = ws.alloc<float>(nq * ix.d);
+        // index-owned staging with stable addresses (the captured graphs of
+        // small batches bake them in); grows, never shrinks
+        const size_t width = k ? k : kprime;
+        auto grow = [&](auto& b, size_t n) {
+            if (b.n < n) {
+                PQRR_CUDA(cudaStreamSynchronize(s));
+                b.alloc(n + n / 2);
+            }
+        };
+        grow(ix.sg_xq, nq * ix.d);
+        grow(ix.sg_oi, nq * width);
+        grow(ix.sg_od, nq * width);
+        grow(ix.sg_oc, nq);
+        float* xq = ix.sg_xq.p;
+        const uint8_t* dq = nullptr;
         if (qf) {
             for (size_t i = 0; i < nq * ix.d; ++i)
                 if (!std::isfinite(qf[i])) throw ArgError("VectorSet: non-finite value");
             PQRR_CUDA(cudaMemcpyAsync(xq, qf, nq * ix.d * 4, cudaMemcpyHostToDevice, s));
         } else {
-            uint8_t* dq = ws.alloc<uint8_t>(nq * ix.d);
-            PQRR_CUDA(cudaMemcpyAsync(dq, qu, nq * ix.d, cudaMemcpyHostToDevice, s));
-            launch_widen_u8(dq, xq, nq * ix.d, s);
+            grow(ix.sg_qu8, nq * ix.d);
+            PQRR_CUDA(cudaMemcpyAsync(ix.sg_qu8.p, qu, nq * ix.d, cudaMemcpyHostToDevice, s));
+            dq = ix.sg_qu8.p;
         }
-        const size_t width = k ? k : kprime;
-        uint32_t* oi = ws.alloc<uint32_t>(nq * width);
-        float* od = ws.alloc<float>(nq * width);
-        uint32_t* oc = ws.alloc<uint32_t>(nq);
+        uint32_t* oi = ix.sg_oi.p;
+        float* od = ix.sg_od.p;
+        uint32_t* oc = ix.sg_oc.p;
         ix.q_u8 = qf == nullptr;
-        search_device(ix, xq, nq, w, kprime, k, oi, od, oc);
+        search_device(ix, xq, nq, w, kprime, k, oi, od, oc, dq);
         ix.q_u8 = false;
         PQRR_CUDA(cudaMemcpyAsync(out_ids, oi, nq * width * 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaMemcpyAsync(out_dists, od, nq * width * 4, cudaMemcpyDeviceToHost, s));
@@ -1721,16 +2153,86 @@ int pqrr_dev_search_u8_device(pqrr_dev_index* h, const uint8_t* d_queries, size_
         cudaStream_t user = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
         cudaStream_t s = ix.stream;
         stream_join(user, s);
-        Workspace ws(s);
-        float* xq = ws.alloc<float>(nq * ix.d);
-        launch_widen_u8(d_queries, xq, nq * ix.d, s);
+        if (ix.sg_xq.n < nq * ix.d) {
+            PQRR_CUDA(cudaStreamSynchronize(s));
+            ix.sg_xq.alloc(nq * ix.d + nq * ix.d / 2);
+        }
         ix.q_u8 = true;
-        search_device(ix, xq, nq, w, kprime, k, d_out_ids, d_out_dists, d_out_counts);
+        search_device(ix, ix.sg_xq.p, nq, w, kprime, k, d_out_ids, d_out_dists, d_out_counts, d_queries);
         ix.q_u8 = false;
         stream_join(s, user);
     });
 }
 
+
+int pqrr_dev_search_u8_enqueue(pqrr_dev_index* h, const uint8_t* d_queries, size_t nq, uint32_t w,
+                               size_t kprime, size_t k, uint32_t* d_out_ids, float* d_out_dists,
+                               uint32_t* d_out_counts, void* stream) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        if (ix.pending.on) throw ArgError("an enqueued search is pending: call pqrr_dev_search_finish first");
+        validate_search(ix, w, kprime, k);
+        if (nq == 0) return;
+        cudaStream_t user = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+        cudaStream_t s = ix.stream;
+        if (ix.sg_xq.n < nq * ix.d) {
+            PQRR_CUDA(cudaStreamSynchronize(s));
+            ix.sg_xq.alloc(nq * ix.d + nq * ix.d / 2);
+        }
+        stream_join(user, s);
+        ix.q_u8 = true;
+        bool ok = false;
+        try {
+            ok = search_enqueue(ix, d_queries, ix.sg_xq.p, nq, w, (uint32_t)kprime, (uint32_t)k, d_out_ids,
+                                d_out_dists, d_out_counts);
+        } catch (...) {
+            ix.q_u8 = false;
+            throw;
+        }
+        ix.q_u8 = false;
+        if (!ok) throw UnsupportedError("batch shape outside the enqueue-only path: use pqrr_dev_search_u8_device");
+        stream_join(s, user);
+        ix.pending = DevIndex::Pending{true, d_queries, nq, kprime, k, w, d_out_ids, d_out_dists, d_out_counts, user};
+    });
+}
+
+int pqrr_dev_index_set_graph(pqrr_dev_index* h, int enabled) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        ix.graph_enabled = enabled != 0;
+    });
+}
+
+int pqrr_dev_search_finish(pqrr_dev_index* h) {
+    return guarded([&] {
+        DevIndex& ix = h->ix;
+        std::lock_guard<std::mutex> lk(ix.mu);
+        DeviceGuard g(ix.device);
+        if (!ix.pending.on) return;
+        const DevIndex::Pending p = ix.pending;
+        ix.pending.on = false;
+        cudaStream_t s = ix.stream;
+        PQRR_CUDA(cudaStreamSynchronize(s));
+        if (search_fast_outcome(ix, (uint32_t)p.k) == 0) return;
+        // rare: a threshold failed its exactness check (or a coarse candidate
+        // set overflowed); redo the batch with per-row retries, ordered after
+        // whatever the caller queued behind the first attempt
+        stream_join(p.user, s);
+        ix.q_u8 = true;
+        try {
+            launch_widen_u8(p.d_queries, ix.sg_xq.p, p.nq * ix.d, s);
+            search_sync(ix, ix.sg_xq.p, p.nq, p.w, p.kprime, p.k, p.oi, p.od, p.oc);
+        } catch (...) {
+            ix.q_u8 = false;
+            throw;
+        }
+        ix.q_u8 = false;
+        stream_join(s, p.user);
+    });
+}
 
 int pqrr_dev_rerank_owned_u8_device(pqrr_dev_index* h, const uint8_t* d_queries, size_t nq,
                                     const uint32_t* d_sl_ids, const uint32_t* d_sl_counts,

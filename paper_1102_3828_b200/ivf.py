@@ -392,6 +392,22 @@ class IvfIndex:
         check(lib.pqrr_dev_search_u8_device(self.h, d_queries_ptr, nq, v, kprime, k, d_ids_ptr,
                                             d_dists_ptr, d_counts_ptr, stream_ptr or None))
 
+    def search_enqueue(self, d_queries_ptr: int, nq: int, v: int, kprime: int, k: int,
+                       d_ids_ptr: int, d_dists_ptr: int, d_counts_ptr: int, stream_ptr: int = 0):
+        """Small-batch search as one captured CUDA graph, launched without
+        blocking the host (pqrr_dev_search_u8_enqueue); ``search_finish`` waits
+        and raises what the blocking call would."""
+        check(lib.pqrr_dev_search_u8_enqueue(self.h, d_queries_ptr, nq, v, kprime, k, d_ids_ptr,
+                                             d_dists_ptr, d_counts_ptr, stream_ptr or None))
+
+    def search_finish(self):
+        check(lib.pqrr_dev_search_finish(self.h))
+
+    def set_graph(self, enabled: bool):
+        """False: every search takes the synchronising path (per-stage times in
+        ``last_stats``); True (default): batches of <= 1024 queries replay graphs."""
+        check(lib.pqrr_dev_index_set_graph(self.h, 1 if enabled else 0))
+
     def rerank_owned_device(self, d_queries_ptr: int, nq: int, d_sl_ids_ptr: int,
                             d_sl_counts_ptr: int, sl_stride: int, k: int, d_ids_ptr: int,
                             d_dists_ptr: int, d_counts_ptr: int, stream_ptr: int = 0):

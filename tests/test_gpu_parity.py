@@ -219,6 +219,16 @@ def test_search_matches_oracle(mid_instance, v, kprime, k):
     np.testing.assert_array_equal(di, ri)
     np.testing.assert_array_equal(bits(dd), bits(rd))
     st = dix.last_stats()
+    assert st["kernels"] > 5 and st["ms_total"] > 0  # a graph replay (64 queries) reports only the total
+    # the synchronising path returns the same bits and per-stage statistics
+    dix.set_graph(False)
+    try:
+        si, sd, sc = dix.search(q, v, kprime, k)
+        st = dix.last_stats()
+    finally:
+        dix.set_graph(True)
+    np.testing.assert_array_equal(si, ri)
+    np.testing.assert_array_equal(bits(sd), bits(rd))
     assert st["kernels"] > 5 and st["ms_scan"] > 0
     # K4f keeps a superset of the exact candidates (<= tau)
     assert st["exact_candidates"] <= st["candidates"]
@@ -853,3 +863,83 @@ def test_two_phase_search_large_batch_matches_oracle(pq, mid_instance, oracle):
         np.testing.assert_array_equal(sc, oc)
         for i in range(len(q)):
             np.testing.assert_array_equal(si[i, :oc[i]], oi[i, :oc[i]])
+
+
+@pytest.mark.parametrize("nq,v,kprime,k", [(1, 24, 1000, 100), (5, 8, 100, 10), (64, 64, 5000, 100),
+                                           (300, 40, 1000, 100), (16, 40, 8, 8), (7, 16, 300, 0)])
+def test_graph_replay_equals_oracle(pq, mid_instance, oracle, nq, v, kprime, k):
+    """Small batches run as one captured CUDA graph (host-side bounds instead
+    of count readbacks, a device status word instead of the retry round trip).
+    The capture call and the replays — with different queries in the same
+    buffers — must equal the oracle bit for bit, and the graph must hold the
+    whole search (no kernel launched outside it on a replay)."""
+    from oracle.oracle_py import Oracle
+
+    o = Oracle()
+    centers = o.synth_centers(0, 256, 128)
+    oix, dix = mid_instance["oix"], mid_instance["dix"]
+    for rep in range(3):
+        q = o.synth_rows(0, 3, 5000 + 1000 * rep, nq, centers)
+        qf = q.astype(np.float32)
+        oi, od, oc = oix.search(qf, v, kprime)
+        l0 = pq.launch_count()
+        di, dd, dc = dix.search(q, v, kprime, k)
+        launched = pq.launch_count() - l0
+        # replays launch nothing outside the graph (a batch whose status word
+        # flags a failed threshold is redone on the synchronising path, which
+        # reports stage times)
+        if rep and dix.last_stats()["ms_scan"] == 0:
+            assert launched == 0, launched
+        if k:
+            ri, rd = oix.rerank(qf, oi, oc, k)
+            np.testing.assert_array_equal(di, ri)
+            np.testing.assert_array_equal(bits(dd), bits(rd))
+        else:
+            np.testing.assert_array_equal(dc, oc)
+            for i in range(nq):
+                np.testing.assert_array_equal(di[i, :oc[i]], oi[i, :oc[i]])
+                np.testing.assert_array_equal(bits(dd[i, :oc[i]]), bits(od[i, :oc[i]]))
+        st = dix.last_stats()
+        assert st["ms_total"] > 0  # (a graph replay times only the total; a flagged batch is redone with stage times)
+
+
+def test_enqueue_finish_device_api(pq, mid_instance, oracle):
+    """pqrr_dev_search_u8_enqueue launches the captured search without blocking;
+    pqrr_dev_search_finish returns the blocking call's outcome: the same bits,
+    'shortlist too small' when k exceeds a row's candidates, and
+    NotImplementedError for a batch outside the envelope."""
+    import torch
+
+    oix, dix, q = mid_instance["oix"], mid_instance["dix"], mid_instance["queries"]
+    v, kprime, k = 24, 1000, 100
+    qf = q.astype(np.float32)
+    oi, od, oc = oix.search(qf, v, kprime)
+    ri, rd = oix.rerank(qf, oi, oc, k)
+    dq = torch.from_numpy(q).cuda()
+    ids = torch.zeros((len(q), k), dtype=torch.int32, device="cuda")
+    dists = torch.zeros((len(q), k), dtype=torch.float32, device="cuda")
+    cnt = torch.zeros(len(q), dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    for _ in range(3):
+        ids.zero_()
+        dix.search_enqueue(dq.data_ptr(), len(q), v, kprime, k, ids.data_ptr(), dists.data_ptr(),
+                           cnt.data_ptr(), st)
+        with pytest.raises(ValueError, match="pending"):
+            dix.search_enqueue(dq.data_ptr(), len(q), v, kprime, k, ids.data_ptr(), dists.data_ptr(),
+                               cnt.data_ptr(), st)
+        dix.search_finish()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(ids.cpu().numpy().view(np.uint32), ri)
+        np.testing.assert_array_equal(bits(dists.cpu().numpy()), bits(rd))
+    dix.search_finish()  # nothing pending: a no-op
+    # a row with fewer than k candidates: the error arrives at finish
+    big = torch.zeros((len(q), 3000), dtype=torch.int32, device="cuda")
+    bigd = torch.zeros((len(q), 3000), dtype=torch.float32, device="cuda")
+    dix.search_enqueue(dq.data_ptr(), len(q), 1, 3000, 3000, big.data_ptr(), bigd.data_ptr(),
+                       cnt.data_ptr(), st)
+    with pytest.raises(ValueError, match="shortlist too small"):
+        dix.search_finish()
+    many = torch.zeros((2000, 128), dtype=torch.uint8, device="cuda")
+    with pytest.raises(NotImplementedError):
+        dix.search_enqueue(many.data_ptr(), 2000, v, kprime, 0, ids.data_ptr(), dists.data_ptr(),
+                           cnt.data_ptr(), st)
