@@ -131,28 +131,68 @@ __device__ __forceinline__ void q8_put_rows(uint32_t* __restrict__ block, int g,
     block[(4 * g + 3) * LANE_WORDS + rq] = __byte_perm(hi01, hi23, 0x7632);
 }
 
+// Ascending bitonic sort of a[0, n2) in shared memory by the whole CTA (n2 a
+// power of two >= 32, blockDim.x a multiple of 32).  Element i lives with
+// thread i % blockDim.x, so partners at distance < 32 sit in one warp: those
+// steps run in registers through shuffles, and only the steps at distance
+// >= 32 go through shared memory and a block barrier (n2 = 1024: 21 barriers
+// instead of 55 — single-CTA sorts of small batches are barrier bound).
+template <class T>
+__device__ __forceinline__ void cta_bitonic_sort(T* a, uint32_t n2) {
+    for (uint32_t k = 2; k <= n2; k <<= 1) {
+        uint32_t j = k >> 1;
+        if (k <= 32) {
+            if (k != 2) continue;  // k = 2..32 are done together below
+        } else {
+            for (; j >= 32; j >>= 1) {
+                for (uint32_t i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+                    const uint32_t lo = 2 * i - (i & (j - 1)), hi = lo + j;
+                    const bool up = (lo & k) == 0;
+                    const T x = a[lo], y = a[hi];
+                    if ((x > y) == up) {
+                        a[lo] = y;
+                        a[hi] = x;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+            T v = a[i];
+            if (k == 2) {
+#pragma unroll
+                for (uint32_t kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+                    for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+                        const T o = __shfl_xor_sync(0xffffffffu, v, jj);
+                        const bool keep_min = ((i & jj) == 0) == ((i & kk) == 0);
+                        v = (keep_min == (v < o)) ? v : o;
+                    }
+            } else {
+#pragma unroll
+                for (uint32_t jj = 16; jj > 0; jj >>= 1) {
+                    const T o = __shfl_xor_sync(0xffffffffu, v, jj);
+                    const bool keep_min = ((i & jj) == 0) == ((i & k) == 0);
+                    v = (keep_min == (v < o)) ? v : o;
+                }
+            }
+            a[i] = v;
+        }
+        __syncthreads();
+    }
+}
+
 // Upper bound of the R-th smallest value a CTA holds, without atomics: every
 // thread passes the minimum of the values it read (all threads must have read
 // at least one); the R-th smallest of those minima has at least R values at or
 // below it.  A histogram-based select then only counts the values <= the
 // bound — the low tail — instead of serialising its shared-memory atomics on
 // the few bins that hold nearly every value.  blockDim.x must be a power of
-// two, R <= blockDim.x; s_mins holds blockDim.x words.  All threads call.
+// two >= 32, R <= blockDim.x; s_mins holds blockDim.x words.  All threads call.
 __device__ __forceinline__ uint32_t cta_tail_bound(uint32_t my_min, uint32_t R, uint32_t* s_mins) {
     s_mins[threadIdx.x] = my_min;
     __syncthreads();
-    for (uint32_t size = 2; size <= blockDim.x; size <<= 1)
-        for (uint32_t st = size >> 1; st > 0; st >>= 1) {
-            const uint32_t i = threadIdx.x, jx = i ^ st;
-            if (jx > i) {
-                const uint32_t a = s_mins[i], b = s_mins[jx];
-                if ((a > b) == ((i & size) == 0)) {
-                    s_mins[i] = b;
-                    s_mins[jx] = a;
-                }
-            }
-            __syncthreads();
-        }
+    cta_bitonic_sort(s_mins, blockDim.x);
     return s_mins[R - 1];
 }
 

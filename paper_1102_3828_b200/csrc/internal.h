@@ -285,23 +285,21 @@ void launch_items_build(const uint32_t* list_cnt, const uint32_t* list_first,
                         uint32_t* item_e0, uint32_t* item_e1, uint32_t* sort_key, uint32_t qt,
                         cudaStream_t s, uint32_t chunk, uint32_t n_items);
 // Small-batch probe inversion in shared memory (k_invert.cu): one launch for
-// the sorted pairs, per-list counts / first pair and the item offsets of two
-// item sets (qt_a queries per item, whole lists; qt_b queries per item, lists
-// cut into chunk_b entries), one launch for the items and their order.
+// the sorted pairs, per-list counts / first pair, and for two item sets (qt
+// queries per item, lists cut into `chunk` entries) the item offsets, the
+// items and their longest-first order.
 static const size_t kInvertSmallMaxPairs = 4096;
 static const uint32_t kInvertSmallMaxItems = 4096;
 bool invert_small_supported(size_t np, uint32_t c);
-void launch_invert_small(const uint32_t* probes, uint32_t np, uint32_t w, const float* D, uint32_t c,
-                         const uint32_t* list_len, uint32_t qt_a, uint32_t qt_b, uint32_t chunk_b,
-                         uint32_t* pair_sorted, uint32_t* list_cnt, uint32_t* list_first,
-                         uint32_t* item_off_a, uint32_t* item_off_b, cudaStream_t s);
 struct SmallItems {
-    const uint32_t* item_off;
+    uint32_t* item_off;  // [c + 1]
     uint32_t *item_list, *item_start, *item_nq, *item_e0, *item_e1, *item_order;
-    uint32_t qt, chunk, bound;  // bound >= the real item count (<= kInvertSmallMaxItems)
+    uint32_t qt, chunk;
+    uint32_t bound;  // >= the real item count, <= kInvertSmallMaxItems; 0: offsets only
 };
-void launch_items_finish_small(const uint32_t* list_cnt, const uint32_t* list_first, const uint32_t* list_len,
-                               uint32_t nlists, const SmallItems& a, const SmallItems* b, cudaStream_t s);
+void launch_invert_small(const uint32_t* probes, uint32_t np, uint32_t w, const float* D, uint32_t c,
+                         const uint32_t* list_len, uint32_t* pair_sorted, uint32_t* list_cnt,
+                         uint32_t* list_first, const SmallItems& a, const SmallItems& b, cudaStream_t s);
 void launch_items_per_list(const uint32_t* list_cnt, const uint32_t* list_len, uint32_t nlists,
                            uint32_t* items, uint32_t qt, cudaStream_t s, uint32_t chunk = 1u << 30);
 // Per query: N_q = sum of probed list lengths; per pair sample counts.

@@ -235,6 +235,7 @@ __global__ __launch_bounds__(512) void topw_kernel(const float* __restrict__ D, 
 // equal to D* (ties -> lowest centroid index) are compacted and
 // only those w keys are sorted.  Replaces a full sort of Kc keys per query.
 constexpr int TW_THREADS = 256;
+constexpr uint32_t TW_TAIL = 1024;  // keys of the sorted-tail shortcut (the 2048-word histogram)
 
 __device__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t* s_total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -266,7 +267,7 @@ __global__ __launch_bounds__(TW_THREADS) void topw_radix_kernel(const float* __r
     extern __shared__ uint32_t tw_smem[];
     uint32_t* bits = tw_smem;                                 // [nc]
     u64* sel = reinterpret_cast<u64*>(tw_smem + ((nc + 1) & ~1u));  // [w2]
-    __shared__ uint32_t hist[2048];
+    __shared__ __align__(16) uint32_t hist[2048];
     __shared__ uint32_t s_bin, s_rank, s_out, s_total, s_warp[TW_THREADS / 32];
     const size_t q = blockIdx.x;
     const uint32_t* row = reinterpret_cast<const uint32_t*>(D + q * nc);
@@ -285,6 +286,35 @@ __global__ __launch_bounds__(TW_THREADS) void topw_radix_kernel(const float* __r
     uint32_t T0 = 0xffffffffu;
     if (w <= blockDim.x / 2 && nc >= blockDim.x) T0 = cta_tail_bound(mn, w, hist);
     __syncthreads();
+    // the tail itself (a little over w entries) usually fits a small buffer:
+    // sort it by (distance, index) and take the first w — no radix passes
+    if (T0 != 0xffffffffu) {
+        u64* tail = reinterpret_cast<u64*>(hist);  // 2048 words = TW_TAIL keys
+        for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+            const uint32_t u = bits[i];
+            if (u <= T0) {
+                const uint32_t k = atomicAdd(&s_out, 1u);
+                if (k < TW_TAIL) tail[k] = ((u64)u << 32) | i;
+            }
+        }
+        __syncthreads();
+        const uint32_t cnt = s_out;
+        __syncthreads();
+        if (cnt <= TW_TAIL) {
+            uint32_t n2 = 32;
+            while (n2 < cnt) n2 <<= 1;
+            for (uint32_t i = cnt + threadIdx.x; i < n2; i += blockDim.x) tail[i] = ~0ull;
+            __syncthreads();
+            cta_bitonic_sort(tail, n2);
+            for (uint32_t i = threadIdx.x; i < w; i += blockDim.x) {
+                out_idx[q * w + i] = key_id(tail[i]);
+                if (out_dist) out_dist[q * w + i] = key_dist(tail[i]);
+            }
+            return;
+        }
+        if (threadIdx.x == 0) s_out = 0;
+        __syncthreads();
+    }
     uint32_t prefix = 0, r = w;
     const int shifts[3] = {21, 10, 0}, widths[3] = {11, 11, 10};
     for (int pass = 0; pass < 3; ++pass) {
@@ -344,21 +374,8 @@ __global__ __launch_bounds__(TW_THREADS) void topw_radix_kernel(const float* __r
     for (uint32_t i = lo; i < hi && k < r; ++i)
         if (bits[i] == dstar) sel[base_lt + k++] = ((u64)dstar << 32) | i;
     __syncthreads();
-    // sort the w selected keys (w2 = next pow2)
-    for (uint32_t kk = 2; kk <= w2; kk <<= 1) {
-        for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
-            for (uint32_t i = threadIdx.x; i < w2 / 2; i += blockDim.x) {
-                const uint32_t a0 = 2 * i - (i & (j - 1)), a1 = a0 + j;
-                const bool up = (a0 & kk) == 0;
-                const u64 x = sel[a0], y = sel[a1];
-                if ((x > y) == up) {
-                    sel[a0] = y;
-                    sel[a1] = x;
-                }
-            }
-            __syncthreads();
-        }
-    }
+    // sort the w selected keys (w2 = next pow2, >= 32)
+    cta_bitonic_sort(sel, w2);
     for (uint32_t i = threadIdx.x; i < w; i += blockDim.x) {
         out_idx[q * w + i] = key_id(sel[i]);
         if (out_dist) out_dist[q * w + i] = key_dist(sel[i]);
@@ -449,7 +466,7 @@ void launch_topw(const float* D, size_t nq, uint32_t nc, uint32_t w, uint32_t* o
     // radix select wins for large Kc (8192: 5.65 -> 2.33 ms per 10k queries);
     // the full bitonic sort is faster for Kc <= 2048 (measured 0.54 vs 0.61 ms)
     if (w < nc && nc > 2048) {
-        uint32_t w2 = 1;
+        uint32_t w2 = 32;
         while (w2 < w) w2 <<= 1;
         const size_t smem = (size_t)((nc + 1) & ~1u) * 4 + (size_t)w2 * 8;
         if (smem <= 200 * 1024) {

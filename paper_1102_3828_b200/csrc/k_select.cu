@@ -58,11 +58,13 @@ __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t n
 // 2048-bin histogram; returns bin and rank within the bin.
 __device__ void find_bin(const uint32_t* hist, uint32_t rank, uint32_t* s_bin, uint32_t* s_rank,
                          uint32_t* s_cnt = nullptr) {
-    // one warp: lane l owns bins [64 l, 64 l + 64)
+    // one warp: lane l owns bins [64 l, 64 l + 64); it reads them rotated by
+    // l so the 32 lanes hit 32 banks (unrotated, lane * 64 + b is one bank)
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         uint32_t sum = 0;
-        for (int b = 0; b < 64; ++b) sum += hist[lane * 64 + b];
+#pragma unroll 8
+        for (int b = 0; b < 64; ++b) sum += hist[lane * 64 + ((b + lane) & 63)];
         uint32_t incl = sum;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -72,17 +74,24 @@ __device__ void find_bin(const uint32_t* hist, uint32_t rank, uint32_t* s_bin, u
         const uint32_t excl = incl - sum;
         const bool mine = excl < rank && rank <= incl;
         const unsigned who = __ballot_sync(0xffffffffu, mine);
-        if (mine && lane == __ffs(who) - 1) {
-            uint32_t c = excl;
-            for (int b = 0; b < 64; ++b) {
-                const uint32_t h = hist[lane * 64 + b];
-                if (rank <= c + h) {
-                    *s_bin = lane * 64 + b;
-                    *s_rank = rank - c;
-                    if (s_cnt) *s_cnt = h;
-                    break;
-                }
-                c += h;
+        if (who) {
+            // the owner's 64 bins, two per lane, scanned by the whole warp
+            const int owner = __ffs(who) - 1;
+            const uint32_t base = __shfl_sync(0xffffffffu, excl, owner);
+            const uint32_t h0 = hist[owner * 64 + 2 * lane], h1 = hist[owner * 64 + 2 * lane + 1];
+            uint32_t inc2 = h0 + h1;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                uint32_t v = __shfl_up_sync(0xffffffffu, inc2, off);
+                if (lane >= off) inc2 += v;
+            }
+            const uint32_t c0 = base + inc2 - h0 - h1;  // entries before this lane's two bins
+            const bool hit0 = c0 < rank && rank <= c0 + h0;
+            const bool hit1 = c0 + h0 < rank && rank <= c0 + h0 + h1;
+            if (hit0 || hit1) {  // exactly one lane
+                *s_bin = owner * 64 + 2 * lane + (hit0 ? 0 : 1);
+                *s_rank = rank - (hit0 ? c0 : c0 + h0);
+                if (s_cnt) *s_cnt = hit0 ? h0 : h1;
             }
         }
     }

@@ -399,6 +399,7 @@ struct DevIndex {
         size_t nq = 0, kprime = 0, k = 0;
         uint32_t w = 0;
         const void *oi = nullptr, *od = nullptr, *oc = nullptr;
+        const void* h_in = nullptr;  // host-staged variant (copies inside the graph)
         bool q_u8 = false;
         uint64_t sig = 0;
         cudaGraphExec_t exec = nullptr;
@@ -411,8 +412,13 @@ struct DevIndex {
     DBuf<uint32_t> d_stat;
     uint32_t* h_stat = nullptr;
     DBuf<uint8_t> sg_qu8;
-    DBuf<float> sg_xq, sg_od;
-    DBuf<uint32_t> sg_oi, sg_oc;
+    DBuf<float> sg_xq;
+    DBuf<uint32_t> sg_out;  // [ids | dists | counts] of the host-buffer API
+    // pinned host staging of small batches: the graph copies queries in and
+    // results out itself, the API call only memcpy's on the CPU
+    void* h_in = nullptr;
+    void* h_out = nullptr;
+    size_t h_in_bytes = 0, h_out_bytes = 0;
     cudaEvent_t ev_fast[2] = {};
     // the enqueued search pqrr_dev_search_finish completes
     struct Pending {
@@ -435,6 +441,8 @@ struct DevIndex {
     ~DevIndex() {
         drop_graphs();
         if (h_stat) cudaFreeHost(h_stat);
+        if (h_in) cudaFreeHost(h_in);
+        if (h_out) cudaFreeHost(h_out);
         for (auto& e : ev_fast)
             if (e) cudaEventDestroy(e);
         for (auto& e : ev)
@@ -971,8 +979,27 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
 
     // ---- invert probes into list-major work items: 16-query items for the
     // LUT pass (and the exact scan), 64-query items for the K4f filter
-    // (small batches: the whole inversion in two single-CTA launches, k_invert.cu)
+    // (small batches: the whole inversion in one single-CTA launch, k_invert.cu;
+    // its buffers are sized by host-side bounds in both search modes)
     const bool small_inv = !pl.two_phase && invert_small_supported(P, c);
+    if (small_inv && !fast) fb = fast_bounds(ix, pl, nq, w, kprime);
+    // room for the 8-bit LUT blocks of n_items LUT-pass items (index-owned cache)
+    auto ensure_q8 = [&](uint32_t n_items) {
+        const size_t need = (size_t)n_items * 8 * 256 * kQT;
+        // (enqueue-only: ensure_fast sized the cache to the bound before the capture)
+        if (fast && ix.q8_cache.bytes() < need) throw std::runtime_error("enqueue-only search: LUT cache not prepared");
+        if (ix.q8_cache.bytes() < need) {
+            size_t free_b = 0, total_b = 0;
+            PQRR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            if (need - ix.q8_cache.bytes() < free_b / 2) {
+                PQRR_CUDA(cudaStreamSynchronize(s));  // (the stream may still read the old cache)
+                ix.q8_cache.alloc(need);
+                ix.q8_param.alloc((size_t)n_items * kQT * 2);
+            }
+        }
+        return ix.q8_cache.bytes() >= need;
+    };
+    bool use_filter = filter_ok;
     uint32_t* pair_ids = ws.alloc<uint32_t>(P);
     if (!small_inv) launch_iota(pair_ids, P, s);
     // two-phase LUT pass: see make_plan
@@ -992,8 +1019,28 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         im.list_first = if64.list_first = ws.alloc<uint32_t>(c + 1);
         im.item_off = ws.alloc<uint32_t>(c + 1);
         if64.item_off = ws.alloc<uint32_t>(c + 1);
-        launch_invert_small(probes, (uint32_t)P, w, D, c, ix.list_len.p, kQT, kFQ, fchunk, im.pair_sorted,
-                            im.list_cnt, im.list_first, im.item_off, if64.item_off, s);
+        im.n_items = fb.items_all;
+        if64.n_items = fb.items_f64;
+        if (use_filter) use_filter = ensure_q8(im.n_items);
+        // item sets within the shared-memory sort are finished in the same
+        // launch; a larger one (long lists cut into many chunks) goes through
+        // items_phase2 with its bound
+        auto prep = [&](ItemSet& it, bool wanted) {
+            SmallItems o{it.item_off, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, it.qt, it.chunk, 0u};
+            if (!wanted || it.n_items > kInvertSmallMaxItems) return o;
+            const uint32_t n = std::max<uint32_t>(it.n_items, 1);
+            o.item_list = it.item_list = ws.alloc<uint32_t>(n);
+            o.item_start = it.item_start = ws.alloc<uint32_t>(n);
+            o.item_nq = it.item_nq = ws.alloc<uint32_t>(n);
+            o.item_e0 = it.item_e0 = ws.alloc<uint32_t>(n);
+            o.item_e1 = it.item_e1 = ws.alloc<uint32_t>(n);
+            o.item_order = it.item_order = ws.alloc<uint32_t>(n);
+            o.bound = n;
+            return o;
+        };
+        const SmallItems sa = prep(im, true), sb = prep(if64, use_filter);
+        launch_invert_small(probes, (uint32_t)P, w, D, c, ix.list_len.p, im.pair_sorted, im.list_cnt,
+                            im.list_first, sa, sb, s);
     } else {
         im = items_phase1(ws, probes, pair_ids, P, c, ix.list_len.p, kQT, s, nullptr, 1u << 30, w, D, probes,
                           two_phase);
@@ -1035,8 +1082,10 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     } else {
         PQRR_CUDA(cudaMemcpyAsync(h_grand, grand, 16, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaMemcpyAsync(&total_samples, sample_off + P, 8, cudaMemcpyDeviceToHost, s));
-        PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
-        PQRR_CUDA(cudaMemcpyAsync(&if64.n_items, if64.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+        if (!small_inv) {
+            PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+            PQRR_CUDA(cudaMemcpyAsync(&if64.n_items, if64.item_off + c, 4, cudaMemcpyDeviceToHost, s));
+        }
         if (two_phase) {
             PQRR_CUDA(cudaMemcpyAsync(&im_near.n_items, im_near.item_off + c, 4, cudaMemcpyDeviceToHost, s));
             PQRR_CUDA(cudaMemcpyAsync(&im_far.n_items, im_far.item_off + c, 4, cudaMemcpyDeviceToHost, s));
@@ -1050,21 +1099,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     }
     const uint32_t n_items = two_phase ? im_near.n_items + im_far.n_items : im.n_items;
 
-    bool use_filter = filter_ok;
-    if (use_filter) {
-        const size_t need = (size_t)n_items * 8 * 256 * kQT;
-        // (enqueue-only: ensure_fast sized the cache to the bound before the capture)
-        if (fast && ix.q8_cache.bytes() < need) throw std::runtime_error("enqueue-only search: LUT cache not prepared");
-        if (ix.q8_cache.bytes() < need) {
-            size_t free_b = 0, total_b = 0;
-            PQRR_CUDA(cudaMemGetInfo(&free_b, &total_b));
-            if (need - ix.q8_cache.bytes() < free_b / 2) {
-                ix.q8_cache.alloc(need);
-                ix.q8_param.alloc((size_t)n_items * kQT * 2);
-            }
-        }
-        use_filter = ix.q8_cache.bytes() >= need;
-    }
+    if (use_filter && !small_inv) use_filter = ensure_q8(n_items);
     if (two_phase && !use_filter && fast) throw std::runtime_error("enqueue-only search: LUT cache not prepared");
     if (two_phase && !use_filter) {
         // rare (no room for the 8-bit LUT cache): the exact scan needs the
@@ -1073,27 +1108,10 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         PQRR_CUDA(cudaMemcpyAsync(&im.n_items, im.item_off + c, 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaStreamSynchronize(s));
     }
-    if (small_inv && im.n_items <= kInvertSmallMaxItems &&
-        (!use_filter || if64.n_items <= kInvertSmallMaxItems)) {
-        auto prep = [&](ItemSet& it) {
-            const uint32_t n = std::max<uint32_t>(it.n_items, 1);
-            it.item_list = ws.alloc<uint32_t>(n);
-            it.item_start = ws.alloc<uint32_t>(n);
-            it.item_nq = ws.alloc<uint32_t>(n);
-            it.item_e0 = ws.alloc<uint32_t>(n);
-            it.item_e1 = ws.alloc<uint32_t>(n);
-            it.item_order = ws.alloc<uint32_t>(n);
-            return SmallItems{it.item_off, it.item_list, it.item_start, it.item_nq, it.item_e0, it.item_e1,
-                              it.item_order, it.qt, it.chunk, it.n_items};
-        };
-        const SmallItems sa = prep(im);
-        SmallItems sb{};
-        if (use_filter) sb = prep(if64);
-        launch_items_finish_small(im.list_cnt, im.list_first, ix.list_len.p, c, sa, use_filter ? &sb : nullptr, s);
-    } else {
-        if (!two_phase || !use_filter) items_phase2(ws, im, c, ix.list_len.p, s, fast);
-        if (use_filter) items_phase2(ws, if64, c, ix.list_len.p, s, fast);
-    }
+    // (small_inv: the sets finished by invert_small_kernel have their items;
+    // their counts are bounds, so a set finished here is padded)
+    if ((!two_phase || !use_filter) && !im.item_order) items_phase2(ws, im, c, ix.list_len.p, s, fast || small_inv);
+    if (use_filter && !if64.item_order) items_phase2(ws, if64, c, ix.list_len.p, s, fast || small_inv);
     if (two_phase) {
         items_phase2(ws, im_near, c, ix.list_len.p, s, fast);
         items_phase2(ws, im_far, c, ix.list_len.p, s, fast);
@@ -1437,12 +1455,24 @@ void search_body_fast(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint
     PQRR_CUDA(cudaMemcpyAsync(ix.h_stat, ix.d_stat.p, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
 }
 
+// Host-staged small batch: the graph starts with the H2D copy of the queries
+// from pinned staging and ends with one D2H copy of [ids | dists | counts].
+struct HostStage {
+    const void* h_in;
+    void* d_in;
+    size_t in_bytes;
+    void* h_out;
+    const void* d_out;
+    size_t out_bytes;
+};
+
 // Enqueues the whole search on ix.stream without blocking the host (graph
 // replay; the first call of a shape captures it).  `widen_from` (optional):
 // u8 queries on the device, widened into xq inside the graph.  Returns false
 // if the shape cannot take this path.
 bool search_enqueue(DevIndex& ix, const uint8_t* widen_from, float* xq, size_t nq, uint32_t w,
-                    uint32_t kprime, uint32_t k, uint32_t* out_ids, float* out_dists, uint32_t* out_cnt) {
+                    uint32_t kprime, uint32_t k, uint32_t* out_ids, float* out_dists, uint32_t* out_cnt,
+                    const HostStage* hs = nullptr) {
     if (!ensure_fast(ix, nq, w, kprime, k)) return false;
     cudaStream_t s = ix.stream;
     const uint64_t sig = index_signature(ix);
@@ -1450,7 +1480,7 @@ bool search_enqueue(DevIndex& ix, const uint8_t* widen_from, float* xq, size_t n
     DevIndex::SearchGraph* g = nullptr;
     for (auto& c : ix.graphs)
         if (c.xq == qkey && c.nq == nq && c.w == w && c.kprime == kprime && c.k == k && c.oi == out_ids &&
-            c.od == out_dists && c.oc == out_cnt && c.q_u8 == ix.q_u8) {
+            c.od == out_dists && c.oc == out_cnt && c.q_u8 == ix.q_u8 && c.h_in == (hs ? hs->h_in : nullptr)) {
             g = &c;
             break;
         }
@@ -1459,7 +1489,9 @@ bool search_enqueue(DevIndex& ix, const uint8_t* widen_from, float* xq, size_t n
         g->exec = nullptr;
     }
     if (g && !g->exec && g->sig == sig) return false;  // this shape failed to capture before
+    bool captured_now = false;
     if (!g || !g->exec) {
+        captured_now = true;
         if (!g) {
             if (ix.graphs.size() >= 16) {  // evict the least recently used
                 size_t lru = 0;
@@ -1472,6 +1504,7 @@ bool search_enqueue(DevIndex& ix, const uint8_t* widen_from, float* xq, size_t n
             g = &ix.graphs.back();
             g->xq = qkey; g->nq = nq; g->w = w; g->kprime = kprime; g->k = k;
             g->oi = out_ids; g->od = out_dists; g->oc = out_cnt; g->q_u8 = ix.q_u8;
+            g->h_in = hs ? hs->h_in : nullptr;
         }
         g->sig = sig;
         cudaGraph_t graph = nullptr;
@@ -1480,8 +1513,10 @@ bool search_enqueue(DevIndex& ix, const uint8_t* widen_from, float* xq, size_t n
         bool ok = true;
         std::string why;
         try {
+            if (hs) PQRR_CUDA(cudaMemcpyAsync(hs->d_in, hs->h_in, hs->in_bytes, cudaMemcpyHostToDevice, s));
             if (widen_from) launch_widen_u8(widen_from, xq, nq * ix.d, s);
             search_body_fast(ix, xq, nq, w, kprime, k, out_ids, out_dists, out_cnt);
+            if (hs) PQRR_CUDA(cudaMemcpyAsync(hs->h_out, hs->d_out, hs->out_bytes, cudaMemcpyDeviceToHost, s));
         } catch (const std::exception& e) {
             ok = false;
             why = e.what();
@@ -1501,6 +1536,9 @@ bool search_enqueue(DevIndex& ix, const uint8_t* widen_from, float* xq, size_t n
         g->kernels = (uint32_t)(launch_count() - l0);
     }
     g->used = ++ix.graph_clock;
+    // (launch accounting: the capture call counted its kernels as they were
+    // recorded; a replay launches the same kernels)
+    if (!captured_now) count_launch(g->kernels);
     PQRR_CUDA(cudaEventRecord(ix.ev_fast[0], s));
     PQRR_CUDA(cudaGraphLaunch(g->exec, s));
     PQRR_CUDA(cudaEventRecord(ix.ev_fast[1], s));
@@ -1541,24 +1579,28 @@ void validate_search(DevIndex& ix, uint32_t w, size_t kprime_sz, size_t k_sz) {
 // staging buffer they are widened into (inside the graph on the enqueue-only
 // path).  Small batches replay a captured graph and synchronise once; a batch
 // whose status word is set, and every large batch, runs the synchronising path.
-void search_device(DevIndex& ix, float* xq, size_t nq, uint32_t w, size_t kprime_sz,
+// `hs` (optional, host-buffer API): queries wait in pinned staging; returns
+// true if the graph also delivered the results to hs->h_out.
+bool search_device(DevIndex& ix, float* xq, size_t nq, uint32_t w, size_t kprime_sz,
                    size_t k_sz, uint32_t* out_ids, float* out_dists, uint32_t* out_cnt,
-                   const uint8_t* widen_from = nullptr) {
+                   const uint8_t* widen_from = nullptr, const HostStage* hs = nullptr) {
     validate_search(ix, w, kprime_sz, k_sz);
     const uint32_t kprime = (uint32_t)kprime_sz, k = (uint32_t)k_sz;
     cudaStream_t s = ix.stream;
     if (nq == 0) {
         ix.stats = pqrr_dev_search_stats{};
-        return;
+        return false;
     }
-    if (search_enqueue(ix, widen_from, xq, nq, w, kprime, k, out_ids, out_dists, out_cnt)) {
+    if (search_enqueue(ix, widen_from, xq, nq, w, kprime, k, out_ids, out_dists, out_cnt, hs)) {
         PQRR_CUDA(cudaStreamSynchronize(s));
-        if (search_fast_outcome(ix, k) == 0) return;
+        if (search_fast_outcome(ix, k) == 0) return hs != nullptr;
         // redo the batch with per-row retries (xq is already widened)
-    } else if (widen_from) {
-        launch_widen_u8(widen_from, xq, nq * ix.d, s);
+    } else {
+        if (hs) PQRR_CUDA(cudaMemcpyAsync(hs->d_in, hs->h_in, hs->in_bytes, cudaMemcpyHostToDevice, s));
+        if (widen_from) launch_widen_u8(widen_from, xq, nq * ix.d, s);
     }
     search_sync(ix, xq, nq, w, kprime_sz, k_sz, out_ids, out_dists, out_cnt);
+    return false;
 }
 
 // The synchronising path: counts read back, per-row threshold retries, stage times.
@@ -2093,27 +2135,59 @@ static int search_host(pqrr_dev_index* h, const float* qf, const uint8_t* qu, si
                 b.alloc(n + n / 2);
             }
         };
+        auto grow_pinned = [&](void*& p, size_t& have, size_t need) {
+            if (have >= need) return;
+            PQRR_CUDA(cudaStreamSynchronize(s));
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            have = 0;
+            PQRR_CUDA(cudaMallocHost(&p, need + need / 2));
+            have = need + need / 2;
+        };
+        const size_t out_words = 2 * nq * width + nq;
         grow(ix.sg_xq, nq * ix.d);
-        grow(ix.sg_oi, nq * width);
-        grow(ix.sg_od, nq * width);
-        grow(ix.sg_oc, nq);
+        grow(ix.sg_out, out_words);
+        if (!qf) grow(ix.sg_qu8, nq * ix.d);
         float* xq = ix.sg_xq.p;
-        const uint8_t* dq = nullptr;
-        if (qf) {
+        const uint8_t* dq = qf ? nullptr : ix.sg_qu8.p;
+        uint32_t* oi = ix.sg_out.p;
+        float* od = reinterpret_cast<float*>(ix.sg_out.p + nq * width);
+        uint32_t* oc = ix.sg_out.p + 2 * nq * width;
+        if (qf)
             for (size_t i = 0; i < nq * ix.d; ++i)
                 if (!std::isfinite(qf[i])) throw ArgError("VectorSet: non-finite value");
-            PQRR_CUDA(cudaMemcpyAsync(xq, qf, nq * ix.d * 4, cudaMemcpyHostToDevice, s));
+        // small batches: queries and results pass through pinned staging and
+        // the captured graph does both copies (one launch and one
+        // synchronisation per search instead of four copies around it)
+        const size_t in_bytes = nq * ix.d * (qf ? 4 : 1);
+        const bool staged = ix.graph_enabled && nq <= kFastMaxQueries && out_words * 4 <= (256u << 10);
+        HostStage hs{};
+        if (staged) {
+            grow_pinned(ix.h_in, ix.h_in_bytes, in_bytes);
+            grow_pinned(ix.h_out, ix.h_out_bytes, out_words * 4);
+            std::memcpy(ix.h_in, qf ? (const void*)qf : (const void*)qu, in_bytes);
+            hs = HostStage{ix.h_in, qf ? (void*)xq : (void*)ix.sg_qu8.p, in_bytes, ix.h_out, ix.sg_out.p,
+                           out_words * 4};
         } else {
-            grow(ix.sg_qu8, nq * ix.d);
-            PQRR_CUDA(cudaMemcpyAsync(ix.sg_qu8.p, qu, nq * ix.d, cudaMemcpyHostToDevice, s));
-            dq = ix.sg_qu8.p;
+            PQRR_CUDA(cudaMemcpyAsync(qf ? (void*)xq : (void*)ix.sg_qu8.p, qf ? (const void*)qf : (const void*)qu,
+                                      in_bytes, cudaMemcpyHostToDevice, s));
         }
-        uint32_t* oi = ix.sg_oi.p;
-        float* od = ix.sg_od.p;
-        uint32_t* oc = ix.sg_oc.p;
         ix.q_u8 = qf == nullptr;
-        search_device(ix, xq, nq, w, kprime, k, oi, od, oc, dq);
+        bool delivered = false;
+        try {
+            delivered = search_device(ix, xq, nq, w, kprime, k, oi, od, oc, dq, staged ? &hs : nullptr);
+        } catch (...) {
+            ix.q_u8 = false;
+            throw;
+        }
         ix.q_u8 = false;
+        if (delivered) {
+            const uint32_t* ho = static_cast<const uint32_t*>(ix.h_out);
+            std::memcpy(out_ids, ho, nq * width * 4);
+            std::memcpy(out_dists, ho + nq * width, nq * width * 4);
+            std::memcpy(out_counts, ho + 2 * nq * width, nq * 4);
+            return;
+        }
         PQRR_CUDA(cudaMemcpyAsync(out_ids, oi, nq * width * 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaMemcpyAsync(out_dists, od, nq * width * 4, cudaMemcpyDeviceToHost, s));
         PQRR_CUDA(cudaMemcpyAsync(out_counts, oc, nq * 4, cudaMemcpyDeviceToHost, s));
