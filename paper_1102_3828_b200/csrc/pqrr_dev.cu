@@ -2117,6 +2117,41 @@ int pqrr_dev_export_lists(pqrr_dev_index* h, uint64_t* offsets, uint32_t* ids, u
     });
 }
 
+// Device-pointer API, small batches: the graph works on index-owned buffers
+// (stable addresses: one graph per shape whatever pointers the caller passes,
+// e.g. fresh torch tensors every call); queries are copied in and results out
+// with device-to-device copies on the index stream around the replay.
+struct DevStage {
+    const uint8_t* dq;
+    uint32_t* oi;
+    float* od;
+    uint32_t* oc;
+    size_t width;
+};
+static DevStage stage_device_batch(DevIndex& ix, const uint8_t* d_queries, size_t nq, size_t kprime, size_t k) {
+    cudaStream_t s = ix.stream;
+    auto grow = [&](auto& b, size_t n) {
+        if (b.n < n) {
+            PQRR_CUDA(cudaStreamSynchronize(s));
+            b.alloc(n + n / 2);
+        }
+    };
+    const size_t width = k ? k : kprime;
+    grow(ix.sg_xq, nq * ix.d);
+    grow(ix.sg_qu8, nq * ix.d);
+    grow(ix.sg_out, 2 * nq * width + nq);
+    PQRR_CUDA(cudaMemcpyAsync(ix.sg_qu8.p, d_queries, nq * ix.d, cudaMemcpyDeviceToDevice, s));
+    return DevStage{ix.sg_qu8.p, ix.sg_out.p, reinterpret_cast<float*>(ix.sg_out.p + nq * width),
+                    ix.sg_out.p + 2 * nq * width, width};
+}
+static void unstage_device_batch(DevIndex& ix, const DevStage& st, size_t nq, uint32_t* d_ids, float* d_dists,
+                                 uint32_t* d_counts) {
+    cudaStream_t s = ix.stream;
+    PQRR_CUDA(cudaMemcpyAsync(d_ids, st.oi, nq * st.width * 4, cudaMemcpyDeviceToDevice, s));
+    PQRR_CUDA(cudaMemcpyAsync(d_dists, st.od, nq * st.width * 4, cudaMemcpyDeviceToDevice, s));
+    PQRR_CUDA(cudaMemcpyAsync(d_counts, st.oc, nq * 4, cudaMemcpyDeviceToDevice, s));
+}
+
 static int search_host(pqrr_dev_index* h, const float* qf, const uint8_t* qu, size_t nq, uint32_t w,
                        size_t kprime, size_t k, uint32_t* out_ids, float* out_dists,
                        uint32_t* out_counts) {
@@ -2227,12 +2262,25 @@ int pqrr_dev_search_u8_device(pqrr_dev_index* h, const uint8_t* d_queries, size_
         cudaStream_t user = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
         cudaStream_t s = ix.stream;
         stream_join(user, s);
+        const bool small = ix.graph_enabled && nq <= kFastMaxQueries;
         if (ix.sg_xq.n < nq * ix.d) {
             PQRR_CUDA(cudaStreamSynchronize(s));
             ix.sg_xq.alloc(nq * ix.d + nq * ix.d / 2);
         }
         ix.q_u8 = true;
-        search_device(ix, ix.sg_xq.p, nq, w, kprime, k, d_out_ids, d_out_dists, d_out_counts, d_queries);
+        try {
+            if (small) {
+                validate_search(ix, w, kprime, k);  // before anything is staged
+                const DevStage st = stage_device_batch(ix, d_queries, nq, kprime, k);
+                search_device(ix, ix.sg_xq.p, nq, w, kprime, k, st.oi, st.od, st.oc, st.dq);
+                unstage_device_batch(ix, st, nq, d_out_ids, d_out_dists, d_out_counts);
+            } else {
+                search_device(ix, ix.sg_xq.p, nq, w, kprime, k, d_out_ids, d_out_dists, d_out_counts, d_queries);
+            }
+        } catch (...) {
+            ix.q_u8 = false;
+            throw;
+        }
         ix.q_u8 = false;
         stream_join(s, user);
     });
@@ -2251,16 +2299,15 @@ int pqrr_dev_search_u8_enqueue(pqrr_dev_index* h, const uint8_t* d_queries, size
         if (nq == 0) return;
         cudaStream_t user = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
         cudaStream_t s = ix.stream;
-        if (ix.sg_xq.n < nq * ix.d) {
-            PQRR_CUDA(cudaStreamSynchronize(s));
-            ix.sg_xq.alloc(nq * ix.d + nq * ix.d / 2);
-        }
+        if (!ix.graph_enabled || nq > kFastMaxQueries)
+            throw UnsupportedError("batch shape outside the enqueue-only path: use pqrr_dev_search_u8_device");
         stream_join(user, s);
         ix.q_u8 = true;
         bool ok = false;
         try {
-            ok = search_enqueue(ix, d_queries, ix.sg_xq.p, nq, w, (uint32_t)kprime, (uint32_t)k, d_out_ids,
-                                d_out_dists, d_out_counts);
+            const DevStage st = stage_device_batch(ix, d_queries, nq, kprime, k);
+            ok = search_enqueue(ix, st.dq, ix.sg_xq.p, nq, w, (uint32_t)kprime, (uint32_t)k, st.oi, st.od, st.oc);
+            if (ok) unstage_device_batch(ix, st, nq, d_out_ids, d_out_dists, d_out_counts);
         } catch (...) {
             ix.q_u8 = false;
             throw;

@@ -943,3 +943,25 @@ def test_enqueue_finish_device_api(pq, mid_instance, oracle):
     with pytest.raises(NotImplementedError):
         dix.search_enqueue(many.data_ptr(), 2000, v, kprime, 0, ids.data_ptr(), dists.data_ptr(),
                            cnt.data_ptr(), st)
+
+
+def test_large_batch_warp_selections_match_oracle(pq, mid_instance, oracle):
+    """A batch that fills the GPU with warps (>= 2 x 148 x 8 queries) takes the
+    warp-per-query kernels: the single-pass threshold (each lane keeps its 8
+    smallest samples; k_wselect.cu), the warp top-w / shortlist / top-k
+    selections.  Shortlists and re-ranked lists must equal the oracle's."""
+    from oracle.oracle_py import Oracle
+
+    o = Oracle()
+    centers = o.synth_centers(0, 256, 128)
+    q = o.synth_rows(0, 3, 20000, 2400, centers)
+    oix, dix = mid_instance["oix"], mid_instance["dix"]
+    qf = q.astype(np.float32)
+    for v, kprime, k in [(24, 300, 50), (8, 1000, 100)]:
+        oi, od, oc = oix.search(qf, v, kprime)
+        ri, rd = oix.rerank(qf, oi, oc, k)
+        di, dd, dc = dix.search(q, v, kprime, k)
+        np.testing.assert_array_equal(di, ri)
+        np.testing.assert_array_equal(bits(dd), bits(rd))
+        st = dix.last_stats()
+        assert st["ms_threshold"] > 0  # the synchronising path (more than 1024 queries)
