@@ -307,6 +307,12 @@ void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uin
                         uint32_t stride, int tiered, uint32_t cap, uint64_t* nq_entries,
                         uint8_t* query_sampled, uint64_t* pair_samples, uint64_t* grand_total,
                         cudaStream_t s, uint32_t max_rank = 0xffffffffu);
+// Small batches (<= 8192 pairs): sizes and the exclusive scan of the pairs'
+// sample counts (sample_off, nq * w + 1 entries) in one single-CTA launch.
+bool launch_query_sizes_small(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
+                              uint32_t stride, int tiered, uint32_t cap, uint64_t* nq_entries,
+                              uint8_t* query_sampled, uint64_t* sample_off, uint64_t* grand_total,
+                              cudaStream_t s, uint32_t max_rank);
 // tau_q = rank-th smallest sample of query q (sampled queries), +inf otherwise.
 void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_off, uint32_t w,
                              size_t nq, const uint8_t* query_sampled, float alpha_k,

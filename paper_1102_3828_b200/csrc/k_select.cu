@@ -54,6 +54,75 @@ __global__ void query_sizes_kernel(const uint32_t* __restrict__ probes, size_t n
     }
 }
 
+// query_sizes_kernel + the exclusive scan of the pairs' sample counts in one
+// CTA, for the few thousand pairs of a small batch (two launches and the
+// library scan less on the serving path).  sample_off has nq * w + 1 entries.
+constexpr int QS_THREADS = 1024;
+__global__ __launch_bounds__(QS_THREADS) void query_sizes_small_kernel(
+    const uint32_t* __restrict__ probes, uint32_t nq, uint32_t w, const uint32_t* __restrict__ list_len,
+    uint32_t stride, int tiered, uint32_t cap, uint64_t* __restrict__ n_entries,
+    uint8_t* __restrict__ sampled, uint64_t* __restrict__ sample_off,
+    unsigned long long* __restrict__ grand_total, uint32_t max_rank) {
+    extern __shared__ uint32_t qs_ns[];  // [nq * w] samples per pair
+    __shared__ unsigned long long s_warp[QS_THREADS / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t np = nq * w;
+    for (uint32_t q = warp; q < nq; q += QS_THREADS / 32) {
+        unsigned long long tot = 0;
+        for (uint32_t r = lane; r < w; r += 32) tot += list_len[probes[q * w + r]];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        const bool samp = tot > cap;
+        unsigned long long ssum = 0;
+        for (uint32_t r = lane; r < w; r += 32) {
+            const uint32_t len = list_len[probes[q * w + r]];
+            const uint32_t st = stride << tier_shift(sample_tier(r, w, tiered), w);
+            const uint32_t ns = (samp && r < max_rank) ? (len + st - 1) / st : 0u;
+            qs_ns[q * w + r] = ns;
+            ssum += ns;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+        if (lane == 0) {
+            n_entries[q] = tot;
+            atomicAdd(grand_total, tot);
+            sampled[q] = samp ? 1 : 0;
+            atomicMax(grand_total + 1, ssum);
+        }
+    }
+    __syncthreads();
+    // exclusive scan over the pairs: contiguous chunk per thread
+    const uint32_t per = (np + QS_THREADS - 1) / QS_THREADS;
+    const uint32_t i0 = min(np, threadIdx.x * per), i1 = min(np, i0 + per);
+    unsigned long long sum = 0;
+    for (uint32_t i = i0; i < i1; ++i) sum += qs_ns[i];
+    unsigned long long incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned long long v = s_warp[lane];
+        unsigned long long wi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        s_warp[lane] = wi - v;
+    }
+    __syncthreads();
+    unsigned long long run = s_warp[warp] + incl - sum;
+    for (uint32_t i = i0; i < i1; ++i) {
+        sample_off[i] = run;
+        run += qs_ns[i];
+    }
+    if (i0 < np && i1 == np) sample_off[np] = run;  // the thread holding the last pair: the total
+}
+
 // Block-wide search of the bin holding the rank-th element (1-based) of a
 // 2048-bin histogram; returns bin and rank within the bin.
 __device__ void find_bin(const uint32_t* hist, uint32_t rank, uint32_t* s_bin, uint32_t* s_rank,
@@ -752,6 +821,20 @@ void launch_query_sizes(const uint32_t* probes, size_t nq, uint32_t w, const uin
         reinterpret_cast<unsigned long long*>(grand_total), max_rank);
     PQRR_LAUNCH_CHECK();
     count_launch();
+}
+
+bool launch_query_sizes_small(const uint32_t* probes, size_t nq, uint32_t w, const uint32_t* list_len,
+                              uint32_t stride, int tiered, uint32_t cap, uint64_t* nq_entries,
+                              uint8_t* query_sampled, uint64_t* sample_off, uint64_t* grand_total,
+                              cudaStream_t s, uint32_t max_rank) {
+    const size_t np = nq * (size_t)w;
+    if (nq == 0 || np > 8192) return false;
+    query_sizes_small_kernel<<<1, QS_THREADS, np * sizeof(uint32_t), s>>>(
+        probes, (uint32_t)nq, w, list_len, stride, tiered, cap, nq_entries, query_sampled, sample_off,
+        reinterpret_cast<unsigned long long*>(grand_total), max_rank);
+    PQRR_LAUNCH_CHECK();
+    count_launch();
+    return true;
 }
 
 void launch_sample_threshold(const float* sample_dist, const uint64_t* sample_off, uint32_t w,

@@ -614,12 +614,13 @@ __device__ __forceinline__ uint32_t warp_weighted_select(uint32_t n, uint32_t ra
 // query's samples reaches alpha*k' entries; each sample weighs its pair's
 // stride (sample_tier: the tiers are contiguous ranges of the query's slots).
 // +inf for queries scanned without sampling or with too few entries.
+constexpr int TH_CAP = 640;  // staged samples per warp (threshold_warp_kernel)
 __global__ __launch_bounds__(WS_WARPS * 32) void threshold_warp_kernel(
     const float* __restrict__ sample, const uint64_t* __restrict__ sample_off, uint32_t w,
     size_t nq, const uint8_t* __restrict__ sampled, float alpha_k, uint32_t stride, int tiered,
     float* __restrict__ tau) {
     __shared__ uint32_t hist_all[WS_WARPS][256];
-    __shared__ uint32_t stage_all[WS_WARPS][2 * 32 * 8];  // per warp: 256 staged values, then their indices
+    __shared__ uint32_t stage_all[WS_WARPS][2 * TH_CAP];  // per warp: staged values, then their indices
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t q = (size_t)blockIdx.x * WS_WARPS + warp;
     if (q >= nq) return;
@@ -650,21 +651,25 @@ __global__ __launch_bounds__(WS_WARPS * 32) void threshold_warp_kernel(
     // One pass over the samples instead of four.  The target rank sits in the
     // far lower tail (rank / stride ~ 64-128 samples of 10^4-10^5), and at
     // large batches the samples stream from HBM (C5, 65536 queries: 16.5 GB per
-    // pass).  Each lane keeps the TB smallest samples it reads (sorted
-    // registers; an insertion is rare once they are warm); the weighted select
-    // then runs over the 32 x TB staged values.  The staged set holds EVERY
-    // sample <= t if each lane's largest kept value exceeds t (or the lane kept
-    // everything it read), and then t is the select over all samples; otherwise
-    // (or if the staged weight does not reach the rank) the full select runs.
+    // pass).  The warp keeps a bound Tw >= the answer and stages (ballot
+    // compaction, no atomics) only the samples <= Tw.  When the stage fills, a
+    // weighted select over it gives a new bound — the rank-th of a subset is
+    // >= the rank-th of all — and the stage keeps only its entries <= the new
+    // bound.  Every sample dropped or skipped is above a bound, hence above the
+    // answer, so the final select over the stage is the select over all
+    // samples.  The stage fills ~4 times per query (512, 4k, 30k samples in).
     {
-        constexpr int TB = 8, U = 4;
-        uint32_t bv[TB], bi[TB];
-#pragma unroll
-        for (int k = 0; k < TB; ++k) {
-            bv[k] = 0xffffffffu;
-            bi[k] = 0xffffffffu;
-        }
-        for (uint32_t base = 0; base < n; base += 32 * U) {
+        constexpr int U = 8;
+        uint32_t* st_v = stage_all[warp];
+        uint32_t* st_i = st_v + TH_CAP;
+        auto st_wt = [&](uint32_t j) {
+            const uint32_t ix = st_i[j];
+            return stride << tier_shift((ix >= b1) + (ix >= b2) + (ix >= b3), w);
+        };
+        uint32_t Tw = 0xffffffffu, cnt = 0;
+        bool give_up = false;
+        const uint32_t lt_mask = (1u << lane) - 1u;
+        for (uint32_t base = 0; base < n && !give_up; base += 32 * U) {
             uint32_t v[U];
 #pragma unroll
             for (int k = 0; k < U; ++k) {
@@ -674,50 +679,54 @@ __global__ __launch_bounds__(WS_WARPS * 32) void threshold_warp_kernel(
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const uint32_t i = base + k * 32 + lane;
-                if (i < n && v[k] < bv[TB - 1]) {
-                    uint32_t cv = v[k], ci = i;  // sorted insert, largest falls out
-#pragma unroll
-                    for (int t2 = 0; t2 < TB; ++t2) {
-                        if (cv < bv[t2]) {
-                            const uint32_t tv = bv[t2], ti = bi[t2];
-                            bv[t2] = cv;
-                            bi[t2] = ci;
-                            cv = tv;
-                            ci = ti;
-                        }
+                const bool pass = i < n && v[k] <= Tw;
+                const uint32_t m = __ballot_sync(0xffffffffu, pass);
+                if (m) {
+                    if (pass) {
+                        const uint32_t pos = cnt + __popc(m & lt_mask);
+                        st_v[pos] = v[k];
+                        st_i[pos] = i;
                     }
+                    cnt += __popc(m);
                 }
             }
-        }
-        uint32_t* st_v = stage_all[warp];
-        uint32_t* st_i = st_v + 32 * TB;
-        unsigned long long wsum = 0;
+            if (cnt > TH_CAP - 32 * U) {  // (warp-uniform) the next round may not fit: tighten the bound
+                __syncwarp();
+                unsigned long long wsum = 0;
+                for (uint32_t j = lane; j < cnt; j += 32) wsum += st_wt(j);
 #pragma unroll
-        for (int k = 0; k < TB; ++k) {
-            st_v[k * 32 + lane] = bv[k];
-            st_i[k * 32 + lane] = bi[k];
-            if (bi[k] != 0xffffffffu)
-                wsum += (unsigned long long)stride << tier_shift((bi[k] >= b1) + (bi[k] >= b2) + (bi[k] >= b3), w);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-        __syncwarp();
-        if (wsum >= rank) {
-            // empty slots (all-ones value) carry no weight and sort last
-            const uint32_t t = warp_weighted_select(
-                32 * TB, rank, [&](uint32_t i) { return st_v[i]; },
-                [&](uint32_t i) {
-                    const uint32_t ix = st_i[i];
-                    return ix == 0xffffffffu ? 0u
-                                             : stride << tier_shift((ix >= b1) + (ix >= b2) + (ix >= b3), w);
-                },
-                hist_all[warp]);
-            // complete up to t?  (a lane with a free slot kept all it read)
-            const bool ok = bi[TB - 1] == 0xffffffffu || bv[TB - 1] > t;
-            if (__all_sync(0xffffffffu, ok)) {
-                if (lane == 0) tau[q] = __uint_as_float(t);
-                return;
+                for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+                if (wsum < rank) {
+                    give_up = true;  // (stage weight below the rank: tiny strides against a huge rank)
+                    break;
+                }
+                Tw = warp_weighted_select(cnt, rank, [&](uint32_t j) { return st_v[j]; }, st_wt, hist_all[warp]);
+                __syncwarp();
+                uint32_t kept = 0;
+                for (uint32_t j0 = 0; j0 < cnt; j0 += 32) {
+                    const uint32_t j = j0 + lane;
+                    const uint32_t vv = j < cnt ? st_v[j] : 0xffffffffu, ii = j < cnt ? st_i[j] : 0u;
+                    const bool keep = j < cnt && vv <= Tw;
+                    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+                    __syncwarp();
+                    if (keep) {
+                        const uint32_t pos = kept + __popc(m & lt_mask);
+                        st_v[pos] = vv;
+                        st_i[pos] = ii;
+                    }
+                    kept += __popc(m);
+                    __syncwarp();
+                }
+                cnt = kept;
+                if (cnt > TH_CAP / 2) give_up = true;  // (masses of equal values: the multi-pass select handles them)
             }
+        }
+        if (!give_up) {
+            __syncwarp();
+            const uint32_t t = warp_weighted_select(cnt, rank, [&](uint32_t j) { return st_v[j]; }, st_wt,
+                                                    hist_all[warp]);
+            if (lane == 0) tau[q] = __uint_as_float(t);
+            return;
         }
         __syncwarp();
     }

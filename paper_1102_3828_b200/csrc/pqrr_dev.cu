@@ -1061,13 +1061,16 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     }
     uint64_t* n_entries = ws.alloc<uint64_t>(nq);
     uint8_t* sampled = ws.alloc<uint8_t>(nq);
-    uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
     uint64_t* grand = ws.zeros<uint64_t>(2);
     const int tiered = pl.tiered;
-    launch_query_sizes(probes, nq, w, ix.list_len.p, stride, tiered, cap, n_entries, sampled,
-                       pair_samples, grand, s, R1);
     uint64_t* sample_off = ws.alloc<uint64_t>(P + 1);
-    exclusive_scan_u64(pair_samples, sample_off, P + 1, s);
+    if (!launch_query_sizes_small(probes, nq, w, ix.list_len.p, stride, tiered, cap, n_entries, sampled,
+                                  sample_off, grand, s, R1)) {
+        uint64_t* pair_samples = ws.zeros<uint64_t>(P + 1);
+        launch_query_sizes(probes, nq, w, ix.list_len.p, stride, tiered, cap, n_entries, sampled,
+                           pair_samples, grand, s, R1);
+        exclusive_scan_u64(pair_samples, sample_off, P + 1, s);
+    }
     uint64_t total_samples = 0, h_grand[2] = {0, 0};
     uint32_t h_ovf = 0;
     if (fast) {
