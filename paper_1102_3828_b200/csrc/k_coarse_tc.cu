@@ -141,6 +141,7 @@ __global__ void sq_norms_kernel(const float* __restrict__ c, uint32_t n, uint32_
 
 constexpr int CW = 8;            // queries (warps) per CTA
 constexpr uint32_t CCAP = 256;   // candidate buffer per query (more: exact path)
+constexpr uint32_t SCAP = 512;   // staged (key, index) entries of the streaming select
 
 // In-warp bitonic sort of n2 (power of two) 64-bit keys in shared memory.
 __device__ __forceinline__ void wbitonic(u64* keys, uint32_t n2) {
@@ -162,44 +163,25 @@ __device__ __forceinline__ void wbitonic(u64* keys, uint32_t n2) {
     }
 }
 
-__global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
-    const float* __restrict__ Dt, size_t nq, uint32_t nc, uint32_t w, const float* __restrict__ x,
-    const float* __restrict__ c, float cnorm_max, uint32_t* __restrict__ out_idx,
-    uint32_t* __restrict__ overflow, const u64 nz, const uint32_t* __restrict__ kmm, float dscale_tc) {
-    constexpr int D = 128;
-    __shared__ uint32_t hist_all[CW][256];
-    __shared__ __align__(16) u64 cand_all[CW][CCAP];
-    __shared__ __align__(16) float xs_all[CW][D];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const size_t q = (size_t)blockIdx.x * CW + warp;
-    if (q >= nq) return;
-    const uint32_t* row = reinterpret_cast<const uint32_t*>(Dt + q * nc);
-    uint32_t* hist = hist_all[warp];
-    u64* cand = cand_all[warp];
-    float* xs = xs_all[warp];
-    reinterpret_cast<float4*>(xs)[lane] = reinterpret_cast<const float4*>(x + q * D)[lane];
+// Upper edge of the bin (two 8-bit radix steps below the keys' common prefix)
+// that holds the rank-th smallest of n keys: a value >= that key.  One warp;
+// hist = 256 words of its shared memory.  have_mm: kmin / kmax are given.
+template <class KeyF>
+__device__ __forceinline__ uint32_t warp_rank_key(uint32_t n, uint32_t rank, KeyF key, uint32_t* hist,
+                                                  bool have_mm, uint32_t kmin, uint32_t kmax) {
+    const int lane = threadIdx.x & 31;
     constexpr int U = 4;
-    // D~ may be slightly negative: order keys as signed floats
-    auto key = [&](uint32_t i) {
-        const uint32_t u = __ldg(row + i);
-        return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-    };
-    // ---- pass 1: min / max of the keys (given by the tcgen05 epilogue when kmm)
-    uint32_t kmin = 0xffffffffu, kmax = 0u;
-    if (kmm) {  // [min keys nq][max keys nq]
-        kmin = kmm[q];
-        kmax = kmm[nq + q];
-    }
-    for (uint32_t base = 0; !kmm && base < nc; base += 32 * U) {
+    // ---- pass 1: min / max of the keys (unless given)
+    for (uint32_t base = 0; !have_mm && base < n; base += 32 * U) {
         uint32_t v[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             const uint32_t i = base + k * 32 + lane;
-            v[k] = i < nc ? key(i) : 0u;
+            v[k] = i < n ? key(i) : 0u;
         }
 #pragma unroll
         for (int k = 0; k < U; ++k)
-            if (base + k * 32 + lane < nc) {
+            if (base + k * 32 + lane < n) {
                 kmin = min(kmin, v[k]);
                 kmax = max(kmax, v[k]);
             }
@@ -215,7 +197,7 @@ __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
     if (kmin != kmax) {
         int consumed = __clz(kmin ^ kmax);
         uint32_t prefix = consumed ? kmin >> (32 - consumed) : 0u;
-        uint32_t r = w;
+        uint32_t r = rank;
 #pragma unroll 1
         for (int step = 0; step < 2 && consumed < 32; ++step) {
             const int wd = min(8, 32 - consumed);
@@ -223,16 +205,16 @@ __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
 #pragma unroll
             for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
             __syncwarp();
-            for (uint32_t base = 0; base < nc; base += 32 * U) {
+            for (uint32_t base = 0; base < n; base += 32 * U) {
                 uint32_t v[U];
 #pragma unroll
                 for (int k = 0; k < U; ++k) {
                     const uint32_t i = base + k * 32 + lane;
-                    v[k] = i < nc ? key(i) : 0u;
+                    v[k] = i < n ? key(i) : 0u;
                 }
 #pragma unroll
                 for (int k = 0; k < U; ++k)
-                    if (base + k * 32 + lane < nc && (consumed == 0 || (v[k] >> (sh + wd)) == prefix))
+                    if (base + k * 32 + lane < n && (consumed == 0 || (v[k] >> (sh + wd)) == prefix))
                         atomicAdd(&hist[(v[k] >> sh) & ((1u << wd) - 1u)], 1u);
             }
             __syncwarp();
@@ -272,10 +254,36 @@ __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
         }
         tkey = consumed >= 32 ? prefix : ((prefix << (32 - consumed)) | ((1u << (32 - consumed)) - 1u));
     }
-    // back to a float: T~ (>= the w-th smallest D~), candidate bound T~ + 2 delta_max
-    const uint32_t tu = (tkey & 0x80000000u) ? (tkey & 0x7fffffffu) : ~tkey;
+    return tkey;
+}
+
+__global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
+    const float* __restrict__ Dt, size_t nq, uint32_t nc, uint32_t w, const float* __restrict__ x,
+    const float* __restrict__ c, float cnorm_max, uint32_t* __restrict__ out_idx,
+    uint32_t* __restrict__ overflow, const u64 nz, const uint32_t* __restrict__ kmm, float dscale_tc) {
+    constexpr int D = 128;
+    __shared__ uint32_t hist_all[CW][256];
+    __shared__ __align__(16) u64 cand_all[CW][SCAP];  // the streaming stage, then the candidates
+    __shared__ __align__(16) float xs_all[CW][D];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t q = (size_t)blockIdx.x * CW + warp;
+    if (q >= nq) return;
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(Dt + q * nc);
+    uint32_t* hist = hist_all[warp];
+    u64* cand = cand_all[warp];
+    u64* stage = cand;
+    float* xs = xs_all[warp];
+    reinterpret_cast<float4*>(xs)[lane] = reinterpret_cast<const float4*>(x + q * D)[lane];
+    constexpr int U = 4;
+    // D~ may be slightly negative: order keys as signed floats
+    auto key = [&](uint32_t i) {
+        const uint32_t u = __ldg(row + i);
+        return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    };
+    // |x|^2 and the certification window first (the streaming select needs them)
     float nx = 0.f;
     bool tf32_exact = true;  // zero or normal with the low 13 mantissa bits clear
+    __syncwarp();
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         const float v = xs[4 * lane + t];
@@ -292,10 +300,86 @@ __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
     const float dscale = dscale_tc > 0.f ? dscale_tc
                                          : (__all_sync(0xffffffffu, tf32_exact) ? 9.765625e-04f : 1.953125e-03f);
     const float delta_max = dscale * (nx + cnorm_max) * 1.01f + 0x1p-100f;
-    const float bound = __uint_as_float(tu) + 2.f * delta_max;
-    // ---- pass 3: candidates D~ <= bound (index order)
-    uint32_t ncand = 0;
+    auto fkey = [](float f) {
+        const uint32_t u = __float_as_uint(f);
+        return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    };
+    auto kfloat = [](uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); };
     const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t ncand = 0;
+    // ---- one pass over the row.  The warp keeps a bound Tw >= the w-th
+    // smallest D~ and stages (ballot compaction) the entries with
+    // D~ <= Tw + 2 delta_max; when the stage fills, the w-th smallest staged
+    // key tightens Tw (the w-th of a subset is >= the w-th of the row) and the
+    // stage is filtered.  What is skipped or dropped lies above a bound + 2
+    // delta_max, so the final stage holds every certified candidate.
+    bool streamed = w + 64 <= SCAP / 2;
+    if (streamed) {
+        uint32_t bkey = 0xffffffffu;  // key of Tw + 2 delta_max
+        uint32_t cnt = 0;
+        auto tighten = [&]() {
+            const uint32_t tk = warp_rank_key(cnt, w, [&](uint32_t j) { return (uint32_t)(stage[j] >> 32); }, hist,
+                                              false, 0xffffffffu, 0u);
+            bkey = fkey(kfloat(tk) + 2.f * delta_max);
+            __syncwarp();
+            uint32_t kept = 0;
+            for (uint32_t j0 = 0; j0 < cnt; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const u64 e = j < cnt ? stage[j] : ~0ull;
+                const bool keep = j < cnt && (uint32_t)(e >> 32) <= bkey;
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                __syncwarp();
+                if (keep) stage[kept + __popc(m & lt_mask)] = e;
+                kept += __popc(m);
+                __syncwarp();
+            }
+            cnt = kept;
+        };
+        for (uint32_t base = 0; base < nc && streamed; base += 32 * U) {
+            uint32_t v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const uint32_t i = base + k * 32 + lane;
+                v[k] = i < nc ? key(i) : 0xffffffffu;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const uint32_t i = base + k * 32 + lane;
+                const bool pass = i < nc && v[k] <= bkey;
+                const unsigned m = __ballot_sync(0xffffffffu, pass);
+                if (m) {
+                    if (pass) stage[cnt + __popc(m & lt_mask)] = ((u64)v[k] << 32) | i;
+                    cnt += __popc(m);
+                }
+            }
+            if (cnt > SCAP - 32 * U) {
+                __syncwarp();
+                tighten();
+                if (cnt > SCAP / 2) streamed = false;  // (a wide window or masses of ties: the multi-pass select)
+            }
+        }
+        if (streamed && cnt >= w) {
+            __syncwarp();
+            tighten();  // final T~ and window; the stage now holds exactly the candidates
+            ncand = cnt;
+            for (uint32_t t = lane; t < ncand; t += 32) cand[t] = stage[t] & 0xffffffffull;  // indices
+            __syncwarp();
+        } else {
+            streamed = false;
+        }
+    }
+    if (!streamed) {
+    // ---- multi-pass select (fallback).  pass 1: min / max of the keys (given by the tcgen05 epilogue when kmm)
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    if (kmm) {  // [min keys nq][max keys nq]
+        kmin = kmm[q];
+        kmax = kmm[nq + q];
+    }
+    const uint32_t tkey = warp_rank_key(nc, w, key, hist, kmm != nullptr, kmin, kmax);
+    // back to a float: T~ (>= the w-th smallest D~), candidate bound T~ + 2 delta_max
+    const float bound = kfloat(tkey) + 2.f * delta_max;
+    // ---- pass 3: candidates D~ <= bound (index order)
+    ncand = 0;
     for (uint32_t base = 0; base < nc; base += 32 * U) {
         float v[U];
 #pragma unroll
@@ -312,6 +396,7 @@ __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
             if (take && o < CCAP) cand[o] = i;
             ncand += __popc(m);
         }
+    }
     }
     if (ncand > CCAP || ncand < w) {
         // the batch is redone on the exact path; emit valid probes meanwhile

@@ -475,32 +475,54 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
             const uint32_t ns = (mt.e1 + smin - 1) / smin;
             const u64* lcodes = reinterpret_cast<const u64*>(a.codes) + a.list_off[mt.l];
             const u64* sc = scodes + b * SCAP;
+            // An item of a small batch holds one or two probing queries: with
+            // <= 4 live lanes (all in quad 0) every lane of a warp takes its
+            // own sample for that quad (32 samples per warp step instead of 8
+            // samples x 4 quads, three of them dead).  Codes are loaded four
+            // steps ahead: past the staged ones they are random DRAM sectors.
+            const bool narrow = mt.nqi <= 4;
+            const int my_qd = narrow ? 0 : qd;
+            const uint32_t nslot = narrow ? 32u : 8u;
+            const uint32_t step = NCW * nslot;
             unsigned long long sbase[4];
             bool sw[4];
             uint32_t sh[4];
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-                const int qq = qd * 4 + kk;
+                const int qq = my_qd * 4 + kk;
                 sw[kk] = mt.q[qq] >= 0 && mt.samp[qq];
                 sbase[kk] = mt.sbase[qq];
                 sh[kk] = mt.sshift[qq];
             }
-            for (uint32_t si = warp * 8 + slot; si < ns; si += NCW * 8) {
-                const u64 code = si < (uint32_t)SCAP ? sc[si] : __ldg(lcodes + sample_pos(si, smin, mt.e1));
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            constexpr int SU = 4;
+            for (uint32_t si0 = warp * nslot + (narrow ? (uint32_t)lane : (uint32_t)slot); si0 < ns;
+                 si0 += SU * step) {
+                u64 code[SU];
 #pragma unroll
-                for (int j = 0; j < M; ++j) {
-                    const uint32_t cj = (uint32_t)(code >> (8 * j)) & 0xffu;
-                    const float4 v = lut4[(j * KS + cj) * (QT / 4) + qd];
-                    acc[0] = __fadd_rn(acc[0], v.x);
-                    acc[1] = __fadd_rn(acc[1], v.y);
-                    acc[2] = __fadd_rn(acc[2], v.z);
-                    acc[3] = __fadd_rn(acc[3], v.w);
+                for (int u = 0; u < SU; ++u) {
+                    const uint32_t si = si0 + u * step;
+                    code[u] = si >= ns ? 0ull
+                                       : (si < (uint32_t)SCAP ? sc[si] : __ldg(lcodes + sample_pos(si, smin, mt.e1)));
                 }
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    if (sw[kk] && (si & ((1u << sh[kk]) - 1u)) == 0u)
-                        a.sample_dist[sbase[kk] + (si >> sh[kk])] = acc[kk];
+                for (int u = 0; u < SU; ++u) {
+                    const uint32_t si = si0 + u * step;
+                    if (si >= ns) break;
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int j = 0; j < M; ++j) {
+                        const uint32_t cj = (uint32_t)(code[u] >> (8 * j)) & 0xffu;
+                        const float4 v = lut4[(j * KS + cj) * (QT / 4) + my_qd];
+                        acc[0] = __fadd_rn(acc[0], v.x);
+                        acc[1] = __fadd_rn(acc[1], v.y);
+                        acc[2] = __fadd_rn(acc[2], v.z);
+                        acc[3] = __fadd_rn(acc[3], v.w);
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        if (sw[kk] && (si & ((1u << sh[kk]) - 1u)) == 0u)
+                            a.sample_dist[sbase[kk] + (si >> sh[kk])] = acc[kk];
+                }
             }
         }
         csync();  // all consumers are done with xr[b], meta[b], scodes[b] and the LUT
