@@ -405,6 +405,7 @@ struct DevIndex {
         cudaGraphExec_t exec = nullptr;
         uint32_t kernels = 0;
         uint64_t used = 0;
+        double bytes = 0;  // scratch its memory nodes reserve (bounds)
     };
     std::vector<SearchGraph> graphs;
     uint64_t graph_clock = 0;
@@ -435,6 +436,7 @@ struct DevIndex {
     void drop_graphs() {
         for (auto& g : graphs)
             if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (!graphs.empty()) cudaDeviceGraphMemTrim(device);
         graphs.clear();
     }
 
@@ -1403,7 +1405,7 @@ uint64_t index_signature(const DevIndex& ix) {
 
 // Whether the batch may take the enqueue-only path; allocates what the
 // capture must not (status block, LUT cache sized to the bounds, lazy coarse state).
-bool ensure_fast(DevIndex& ix, size_t nq, uint32_t w, uint32_t kprime, uint32_t k) {
+bool ensure_fast(DevIndex& ix, size_t nq, uint32_t w, uint32_t kprime, uint32_t k, double* scratch_bytes = nullptr) {
     if (!ix.graph_enabled || nq == 0 || nq > kFastMaxQueries) return false;
     static size_t dev_total = 0;
     if (!dev_total) {
@@ -1413,6 +1415,7 @@ bool ensure_fast(DevIndex& ix, size_t nq, uint32_t w, uint32_t kprime, uint32_t 
     const Plan pl = make_plan(ix, nq, w, kprime, default_alpha(kprime, w), 1, 0, false);
     const FastBounds fb = fast_bounds(ix, pl, nq, w, kprime);
     if (fb.bytes > 0.125 * (double)dev_total) return false;
+    if (scratch_bytes) *scratch_bytes = fb.bytes;
     if (!ix.d_stat.p) {
         ix.d_stat.alloc(8);
         PQRR_CUDA(cudaMallocHost(&ix.h_stat, 8 * sizeof(uint32_t)));
@@ -1476,7 +1479,8 @@ struct HostStage {
 bool search_enqueue(DevIndex& ix, const uint8_t* widen_from, float* xq, size_t nq, uint32_t w,
                     uint32_t kprime, uint32_t k, uint32_t* out_ids, float* out_dists, uint32_t* out_cnt,
                     const HostStage* hs = nullptr) {
-    if (!ensure_fast(ix, nq, w, kprime, k)) return false;
+    double scratch = 0;
+    if (!ensure_fast(ix, nq, w, kprime, k, &scratch)) return false;
     cudaStream_t s = ix.stream;
     const uint64_t sig = index_signature(ix);
     const void* qkey = widen_from ? (const void*)widen_from : (const void*)xq;
@@ -1496,12 +1500,32 @@ bool search_enqueue(DevIndex& ix, const uint8_t* widen_from, float* xq, size_t n
     if (!g || !g->exec) {
         captured_now = true;
         if (!g) {
-            if (ix.graphs.size() >= 16) {  // evict the least recently used
+            // cached graphs keep the scratch of their memory nodes mapped:
+            // at most 16 graphs and a quarter of the device, least recently
+            // used evicted (and their memory trimmed) first
+            static size_t dev_total = 0;
+            if (!dev_total) {
+                size_t f = 0;
+                PQRR_CUDA(cudaMemGetInfo(&f, &dev_total));
+            }
+            auto held = [&] {
+                double b = 0;
+                for (auto& c : ix.graphs) b += c.exec ? c.bytes : 0.0;
+                return b;
+            };
+            bool trimmed = false;
+            while (!ix.graphs.empty() &&
+                   (ix.graphs.size() >= 16 || held() + scratch > 0.25 * (double)dev_total)) {
                 size_t lru = 0;
                 for (size_t i = 1; i < ix.graphs.size(); ++i)
                     if (ix.graphs[i].used < ix.graphs[lru].used) lru = i;
                 if (ix.graphs[lru].exec) cudaGraphExecDestroy(ix.graphs[lru].exec);
                 ix.graphs.erase(ix.graphs.begin() + lru);
+                trimmed = true;
+            }
+            if (trimmed) {
+                PQRR_CUDA(cudaStreamSynchronize(s));
+                cudaDeviceGraphMemTrim(ix.device);
             }
             ix.graphs.emplace_back();
             g = &ix.graphs.back();
@@ -1510,6 +1534,7 @@ bool search_enqueue(DevIndex& ix, const uint8_t* widen_from, float* xq, size_t n
             g->h_in = hs ? hs->h_in : nullptr;
         }
         g->sig = sig;
+        g->bytes = scratch;
         cudaGraph_t graph = nullptr;
         const unsigned long long l0 = launch_count();
         PQRR_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -2326,7 +2351,13 @@ int pqrr_dev_index_set_graph(pqrr_dev_index* h, int enabled) {
     return guarded([&] {
         DevIndex& ix = h->ix;
         std::lock_guard<std::mutex> lk(ix.mu);
+        if (ix.pending.on) throw ArgError("an enqueued search is pending: call pqrr_dev_search_finish first");
         ix.graph_enabled = enabled != 0;
+        if (!ix.graph_enabled && !ix.graphs.empty()) {  // release the cached graphs and their scratch
+            DeviceGuard g(ix.device);
+            PQRR_CUDA(cudaStreamSynchronize(ix.stream));
+            ix.drop_graphs();
+        }
     });
 }
 
