@@ -443,17 +443,76 @@ __global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
     if (lane == 0) sl_cnt[q] = kprime;
 }
 
+// One pass over a row for its k smallest (dist, id) keys when k << n (C4: 100
+// of 10^4): the warp keeps a bound >= the k-th smallest distance, stages by
+// ballot compaction the entries at or below it, and when the stage fills, the
+// exact k-th smallest staged distance becomes the bound (the k-th of a subset
+// is >= the k-th of the row) and the stage keeps its entries <= it.  The final
+// stage holds every entry <= the bound, so its first k keys in (dist, id)
+// order are the row's.  false: the stage cannot hold k plus a round (or masses
+// of ties); the caller runs the multi-pass select.
+constexpr uint32_t RT_CAP = 512;
+__device__ __forceinline__ bool rerank_topk_stream(uint32_t n, uint32_t k, const uint32_t* __restrict__ db,
+                                                   const uint32_t* __restrict__ ib, u64* stage, uint32_t cap,
+                                                   uint32_t* hist, uint32_t& n_out) {
+    constexpr int U = 4;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    if (cap < RT_CAP || k + 32 * U > cap / 2) return false;
+    uint32_t bound = 0xffffffffu, cnt = 0;
+    for (uint32_t base = 0; base < n; base += 32 * U) {
+        uint32_t v[U];
+#pragma unroll
+        for (int t = 0; t < U; ++t) {
+            const uint32_t i = base + t * 32 + lane;
+            v[t] = i < n ? __ldg(db + i) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int t = 0; t < U; ++t) {
+            const uint32_t i = base + t * 32 + lane;
+            const bool pass = i < n && v[t] <= bound;
+            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            if (m) {
+                if (pass) stage[cnt + __popc(m & lt_mask)] = ((u64)v[t] << 32) | __ldg(ib + i);
+                cnt += __popc(m);
+            }
+        }
+        if (cnt > cap - 32 * U) {
+            __syncwarp();
+            uint32_t kth, r_eq;
+            warp_radix_select(cnt, k, [&](uint32_t j) { return (uint32_t)(stage[j] >> 32); }, hist, kth, r_eq);
+            bound = kth;
+            __syncwarp();
+            uint32_t kept = 0;
+            for (uint32_t j0 = 0; j0 < cnt; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const u64 e = j < cnt ? stage[j] : ~0ull;
+                const bool keep = j < cnt && (uint32_t)(e >> 32) <= bound;
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                __syncwarp();
+                if (keep) stage[kept + __popc(m & lt_mask)] = e;
+                kept += __popc(m);
+                __syncwarp();
+            }
+            cnt = kept;
+            if (cnt > cap / 2) return false;
+        }
+    }
+    n_out = cnt;
+    return true;
+}
+
 // Re-rank top-k: (rdist, rid) rows of width `stride`, n = cnt[q] valid.
 __global__ __launch_bounds__(WS_WARPS * 32) void rerank_topk_warp_kernel(
     const float* __restrict__ rdist, const uint32_t* __restrict__ rid,
-    const uint32_t* __restrict__ cnt_in, uint32_t stride, size_t nq, uint32_t k, uint32_t k2,
+    const uint32_t* __restrict__ cnt_in, uint32_t stride, size_t nq, uint32_t k, uint32_t k2, uint32_t cap,
     uint32_t* __restrict__ out_ids, float* __restrict__ out_dists, uint32_t* __restrict__ out_cnt) {
-    extern __shared__ u64 wkeys[];  // [WS_WARPS][k2]
+    extern __shared__ u64 wkeys[];  // [WS_WARPS][cap], cap >= k2
     __shared__ uint32_t hist_all[WS_WARPS][256];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t q = (size_t)blockIdx.x * WS_WARPS + warp;
     if (q >= nq) return;
-    u64* keys = wkeys + (size_t)warp * k2;
+    u64* keys = wkeys + (size_t)warp * cap;
     const uint32_t n = cnt_in[q];
     const uint32_t* db = reinterpret_cast<const uint32_t*>(rdist) + q * stride;
     const uint32_t* ib = rid + q * stride;
@@ -462,6 +521,8 @@ __global__ __launch_bounds__(WS_WARPS * 32) void rerank_topk_warp_kernel(
     if (n <= k) {
         for (uint32_t i = lane; i < n; i += 32) keys[i] = ((u64)db[i] << 32) | ib[i];
         n_out = n;
+    } else if (rerank_topk_stream(n, k, db, ib, keys, cap, hist_all[warp], n_out)) {
+        // (one pass: the stage holds every entry at or below the k-th distance)
     } else {
         uint32_t kth, r_eq;
         warp_radix_select(n, k, [&](uint32_t i) { return db[i]; }, hist_all[warp], kth, r_eq);
@@ -500,9 +561,11 @@ __global__ __launch_bounds__(WS_WARPS * 32) void rerank_topk_warp_kernel(
         }
     }
     __syncwarp();
-    for (uint32_t i = n_out + lane; i < k2; i += 32) keys[i] = ~0ull;
+    uint32_t s2 = k2;  // (the streamed stage may hold more than k entries: ties and the last bound's slack)
+    while (s2 < n_out) s2 <<= 1;
+    for (uint32_t i = n_out + lane; i < s2; i += 32) keys[i] = ~0ull;
     __syncwarp();
-    warp_bitonic(keys, k2);
+    warp_bitonic(keys, s2);
     const uint32_t cnt = min(n, k);
     for (uint32_t i = lane; i < k; i += 32) {
         const bool live = i < cnt;
@@ -765,12 +828,13 @@ bool launch_rerank_topk_warp(const float* rdist, const uint32_t* rid, const uint
                              float* out_dists, uint32_t* out_cnt, cudaStream_t s) {
     uint32_t k2 = 1;
     while (k2 < k) k2 <<= 1;
-    const size_t smem = (size_t)WS_WARPS * k2 * sizeof(u64);
+    const uint32_t cap = std::max<uint32_t>(k2, RT_CAP);  // per-warp keys: the streaming stage or the k2 winners
+    const size_t smem = (size_t)WS_WARPS * cap * sizeof(u64);
     if (k2 > 1024 || smem > 96 * 1024) return false;
     if (smem > 48 * 1024)
         set_max_smem((const void*)rerank_topk_warp_kernel, (size_t)((int)smem));
     rerank_topk_warp_kernel<<<(unsigned)((nq + WS_WARPS - 1) / WS_WARPS), WS_WARPS * 32, smem, s>>>(
-        rdist, rid, cnt, stride, nq, k, k2, out_ids, out_dists, out_cnt);
+        rdist, rid, cnt, stride, nq, k, k2, cap, out_ids, out_dists, out_cnt);
     PQRR_LAUNCH_CHECK();
     count_launch();
     return true;
