@@ -274,7 +274,7 @@ __global__ __launch_bounds__(CW * 32, 4) void topw_certify_kernel(
     u64* stage = cand;
     float* xs = xs_all[warp];
     reinterpret_cast<float4*>(xs)[lane] = reinterpret_cast<const float4*>(x + q * D)[lane];
-    constexpr int U = 4;
+    constexpr int U = 8;
     // D~ may be slightly negative: order keys as signed floats
     auto key = [&](uint32_t i) {
         const uint32_t u = __ldg(row + i);

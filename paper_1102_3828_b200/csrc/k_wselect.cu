@@ -455,11 +455,30 @@ constexpr uint32_t RT_CAP = 512;
 __device__ __forceinline__ bool rerank_topk_stream(uint32_t n, uint32_t k, const uint32_t* __restrict__ db,
                                                    const uint32_t* __restrict__ ib, u64* stage, uint32_t cap,
                                                    uint32_t* hist, uint32_t& n_out) {
-    constexpr int U = 4;
+    constexpr int U = 4;  // (8 loads in flight need a 1024-entry stage: 64 KiB per CTA, measured slower)
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     if (cap < RT_CAP || k + 32 * U > cap / 2) return false;
     uint32_t bound = 0xffffffffu, cnt = 0;
+    auto tighten = [&]() {
+        __syncwarp();
+        uint32_t kth, r_eq;
+        warp_radix_select(cnt, k, [&](uint32_t j) { return (uint32_t)(stage[j] >> 32); }, hist, kth, r_eq);
+        bound = kth;
+        __syncwarp();
+        uint32_t kept = 0;
+        for (uint32_t j0 = 0; j0 < cnt; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            const u64 e = j < cnt ? stage[j] : ~0ull;
+            const bool keep = j < cnt && (uint32_t)(e >> 32) <= bound;
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            __syncwarp();
+            if (keep) stage[kept + __popc(m & lt_mask)] = e;
+            kept += __popc(m);
+            __syncwarp();
+        }
+        cnt = kept;
+    };
     for (uint32_t base = 0; base < n; base += 32 * U) {
         uint32_t v[U];
 #pragma unroll
@@ -478,26 +497,11 @@ __device__ __forceinline__ bool rerank_topk_stream(uint32_t n, uint32_t k, const
             }
         }
         if (cnt > cap - 32 * U) {
-            __syncwarp();
-            uint32_t kth, r_eq;
-            warp_radix_select(cnt, k, [&](uint32_t j) { return (uint32_t)(stage[j] >> 32); }, hist, kth, r_eq);
-            bound = kth;
-            __syncwarp();
-            uint32_t kept = 0;
-            for (uint32_t j0 = 0; j0 < cnt; j0 += 32) {
-                const uint32_t j = j0 + lane;
-                const u64 e = j < cnt ? stage[j] : ~0ull;
-                const bool keep = j < cnt && (uint32_t)(e >> 32) <= bound;
-                const unsigned m = __ballot_sync(0xffffffffu, keep);
-                __syncwarp();
-                if (keep) stage[kept + __popc(m & lt_mask)] = e;
-                kept += __popc(m);
-                __syncwarp();
-            }
-            cnt = kept;
+            tighten();
             if (cnt > cap / 2) return false;
         }
     }
+    if (cnt > 2 * k + 64) tighten();  // keep the final sort small
     n_out = cnt;
     return true;
 }
