@@ -357,6 +357,12 @@ __global__ __launch_bounds__(NTH, 1) void lut_pass_kernel(const ScanArgs a, cons
                 const u64* lcodes = reinterpret_cast<const u64*>(a.codes) + a.list_off[l];
                 for (uint32_t si = lane; si < min(ns, (uint32_t)SCAP); si += 32)
                     cp8(scodes + b * SCAP + si, lcodes + sample_pos(si, smin, e1));
+                // the samples past the staged ones are read by the consumers one
+                // item later: pull their sectors into L2 now, so those loads
+                // wait an L2 hit instead of a DRAM access (all 16 consumer warps
+                // sit in the sampling loop together, nothing else hides it)
+                for (uint32_t si = SCAP + lane; si < ns; si += 32)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(lcodes + sample_pos(si, smin, e1)));
             }
             cp_commit();
             cp_wait<0>();
