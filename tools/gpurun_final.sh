@@ -2,6 +2,7 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 P=${1:-fin}
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print(\"smoke ok\")" > gpurun_out/${P}_smoke.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${P}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${P}_tests.log
 timeout 1800 python bench.py > gpurun_out/${P}_c4.json 2> gpurun_out/${P}_c4.err
 timeout 1800 python bench.py --impl reference > gpurun_out/${P}_ref_c4.json 2> gpurun_out/${P}_ref_c4.err
