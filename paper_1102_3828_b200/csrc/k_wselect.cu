@@ -19,7 +19,7 @@ namespace pqrr_b200 {
 namespace {
 
 constexpr int WS_WARPS = 8;  // queries per CTA
-constexpr uint32_t TIE_CAP = 512;  // boundary bin / boundary ties sorted in shared memory
+constexpr uint32_t TIE_CAP = 256;  // boundary ties sorted in shared memory
 
 // Rank-th (1-based) smallest of n 32-bit keys key(i); on return `kth` is that
 // key and `r_eq` the number of entries equal to it that belong to the
@@ -335,7 +335,7 @@ __global__ __launch_bounds__(WS_WARPS * 32) void topw_warp_kernel(const float* _
 // Shortlist selection (unsorted): candidates (dist, pos) of query q, ids
 // gathered for the selected entries only.  Ties at the boundary distance are
 // resolved by id with a small warp loop (they are rare).
-__global__ __launch_bounds__(WS_WARPS * 32, 4) void select_warp_kernel(
+__global__ __launch_bounds__(WS_WARPS * 32) void select_warp_kernel(
     const float* __restrict__ cand_dist, const uint32_t* __restrict__ cand_pos,
     const uint32_t* __restrict__ cand_cnt, uint32_t cap, size_t nq, const uint32_t* __restrict__ ids,
     uint32_t kprime, u64* __restrict__ sl_key, uint32_t* __restrict__ sl_pos,
@@ -360,154 +360,6 @@ __global__ __launch_bounds__(WS_WARPS * 32, 4) void select_warp_kernel(
         if (lane == 0) sl_cnt[q] = n;
         return;
     }
-    u64* tie = tie_all[warp];
-    // Two reads of the candidates instead of four (they stream from HBM: at C4
-    // a batch holds 2 GB of them).  With the key range known (K4r), one 8-bit
-    // histogram below the common leading bits finds the bin of the k'-th
-    // key; the second pass emits every entry of a lower bin and stages the
-    // boundary bin (dist, row index), a few hundred entries, whose sort
-    // supplies the remaining rank.  A boundary bin larger than the stage (or
-    // more boundary ties than it holds) takes the multi-pass select below.
-    {
-        const uint32_t kmin0 = cand_mm ? cand_mm[2 * q] : 0xffffffffu, kmax0 = cand_mm ? cand_mm[2 * q + 1] : 0u;
-        if (kmin0 < kmax0 && kmax0 != 0xffffffffu) {
-            constexpr int U = 8;
-            uint32_t* hist = hist_all[warp];
-            const int consumed = __clz(kmin0 ^ kmax0);
-            const int wd = min(8, 32 - consumed), sh = 32 - consumed - wd;
-            const uint32_t msk = (1u << wd) - 1u;
-#pragma unroll
-            for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
-            __syncwarp();
-            for (uint32_t base = 0; base < n; base += 32 * U) {
-                uint32_t v[U];
-#pragma unroll
-                for (int k = 0; k < U; ++k) {
-                    const uint32_t i = base + k * 32 + lane;
-                    v[k] = i < n ? dq[i] : 0u;
-                }
-#pragma unroll
-                for (int k = 0; k < U; ++k)
-                    if (base + k * 32 + lane < n) atomicAdd(&hist[(v[k] >> sh) & msk], 1u);
-            }
-            __syncwarp();
-            uint32_t h[8], sum = 0;
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                h[b] = hist[lane * 8 + b];
-                sum += h[b];
-            }
-            uint32_t incl = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const uint32_t excl = incl - sum;
-            const bool mine = excl < kprime && kprime <= incl;
-            const int owner = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
-            uint32_t bin = 0, before = excl, bcnt = 0;
-            if (mine) {
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    if (kprime > before + h[b]) {
-                        before += h[b];
-                    } else {
-                        bin = lane * 8 + b;
-                        bcnt = h[b];
-                        break;
-                    }
-                }
-            }
-            bin = __shfl_sync(0xffffffffu, bin, owner);
-            before = __shfl_sync(0xffffffffu, before, owner);
-            bcnt = __shfl_sync(0xffffffffu, bcnt, owner);
-            if (bcnt <= TIE_CAP) {
-                const uint32_t rin = kprime - before;  // rank inside the boundary bin, 1-based
-                uint32_t n_out = 0, n_st = 0;
-                for (uint32_t base = 0; base < n; base += 32 * U) {
-                    uint32_t u[U], pp[U], id[U];
-#pragma unroll
-                    for (int k = 0; k < U; ++k) {
-                        const uint32_t i = base + k * 32 + lane;
-                        u[k] = i < n ? dq[i] : 0xffffffffu;
-                    }
-#pragma unroll
-                    for (int k = 0; k < U; ++k) {
-                        const uint32_t i = base + k * 32 + lane;
-                        pp[k] = (i < n && ((u[k] >> sh) & msk) < bin) ? pq[i] : 0u;
-                    }
-#pragma unroll
-                    for (int k = 0; k < U; ++k) {
-                        const uint32_t i = base + k * 32 + lane;
-                        id[k] = (need_ids && i < n && ((u[k] >> sh) & msk) < bin) ? ids[pp[k]] : 0u;
-                    }
-#pragma unroll
-                    for (int k = 0; k < U; ++k) {
-                        const uint32_t i = base + k * 32 + lane;
-                        const uint32_t b = (u[k] >> sh) & msk;
-                        const bool lt = i < n && b < bin, eq = i < n && b == bin;
-                        const unsigned mlt = __ballot_sync(0xffffffffu, lt), meq = __ballot_sync(0xffffffffu, eq);
-                        if (lt) {
-                            const uint32_t o = n_out + __popc(mlt & lt_mask);
-                            ok[o] = ((u64)u[k] << 32) | id[k];
-                            op[o] = pp[k];
-                        }
-                        if (eq) tie[n_st + __popc(meq & lt_mask)] = ((u64)u[k] << 32) | i;
-                        n_out += __popc(mlt);
-                        n_st += __popc(meq);
-                    }
-                }
-                __syncwarp();
-                // the boundary bin in (dist, row index) order
-                uint32_t t2 = 1;
-                while (t2 < n_st) t2 <<= 1;
-                for (uint32_t i = n_st + lane; i < t2; i += 32) tie[i] = ~0ull;
-                __syncwarp();
-                warp_bitonic(tie, t2);
-                const uint32_t kd = (uint32_t)(tie[rin - 1] >> 32);  // the k'-th distance
-                uint32_t c_lt = 0, c_eq = 0;
-                for (uint32_t j0 = 0; j0 < n_st; j0 += 32) {
-                    const uint32_t j = j0 + lane;
-                    const uint32_t d = j < n_st ? (uint32_t)(tie[j] >> 32) : 0xffffffffu;
-                    c_lt += __popc(__ballot_sync(0xffffffffu, j < n_st && d < kd));
-                    c_eq += __popc(__ballot_sync(0xffffffffu, j < n_st && d == kd));
-                }
-                const uint32_t r_eq2 = rin - c_lt;  // boundary ties that belong to the shortlist
-                // sorted: [0, c_lt) below kd, [c_lt, c_lt + c_eq) at kd
-                for (uint32_t j = lane; j < c_lt; j += 32) {
-                    const u64 e = tie[j];
-                    const uint32_t ppos = pq[(uint32_t)e];
-                    ok[n_out + j] = (e & 0xffffffff00000000ull) | (need_ids ? ids[ppos] : 0u);
-                    op[n_out + j] = ppos;
-                }
-                n_out += c_lt;
-                __syncwarp();
-                // the ties as (id, pos), the r_eq2 smallest ids win (types.hpp:47-50)
-                // (in place, 32 at a time: a chunk's writes land below every later read)
-                uint32_t e2 = 1;
-                while (e2 < c_eq) e2 <<= 1;
-                for (uint32_t j0 = 0; j0 < e2; j0 += 32) {
-                    const uint32_t j = j0 + lane;
-                    u64 e = ~0ull;
-                    if (j < c_eq) {
-                        const uint32_t ppos = pq[(uint32_t)tie[c_lt + j]];
-                        e = ((u64)ids[ppos] << 32) | ppos;
-                    }
-                    __syncwarp();
-                    if (j < e2) tie[j] = e;
-                    __syncwarp();
-                }
-                if (c_eq != r_eq2) warp_bitonic(tie, e2);
-                for (uint32_t t = lane; t < r_eq2; t += 32) {
-                    ok[n_out + t] = ((u64)kd << 32) | (uint32_t)(tie[t] >> 32);
-                    op[n_out + t] = (uint32_t)tie[t];
-                }
-                if (lane == 0) sl_cnt[q] = kprime;
-                return;
-            }
-        }
-    }
     uint32_t kth, r_eq;
     warp_radix_select(n, kprime, [&](uint32_t i) { return dq[i]; }, hist_all[warp], kth, r_eq,
                       cand_mm ? cand_mm[2 * q] : 0xffffffffu, cand_mm ? cand_mm[2 * q + 1] : 0u);
@@ -516,6 +368,7 @@ __global__ __launch_bounds__(WS_WARPS * 32, 4) void select_warp_kernel(
     // to a per-warp tie buffer as (id, pos) (exact ADC ties are common: equal
     // codes in one list); the r_eq smallest ids among them are taken after.
     constexpr int U = 8;
+    u64* tie = tie_all[warp];
     uint32_t n_out = 0, n_eq = 0;
     for (uint32_t base = 0; base < n; base += 32 * U) {
         uint32_t u[U], p[U], id[U];
