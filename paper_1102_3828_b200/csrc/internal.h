@@ -208,6 +208,10 @@ void launch_ivf_scan(const ScanArgs& a, cudaStream_t s);
 // K2 LUT pass (pass 1) as a warp-specialised kernel (k_lutpass.cu).
 bool lut_pass_supported(uint32_t d, uint32_t m, uint32_t ks);
 void launch_lut_pass(const ScanArgs& a, cudaStream_t s);
+// The same pass for small batches (about one probing query per list): code
+// book resident, two query lanes per LUT (k_lutnarrow.cu).  Single-phase only.
+bool lut_pass_narrow_supported(uint32_t d, uint32_t m, uint32_t ks);
+void launch_lut_pass_narrow(const ScanArgs& a, cudaStream_t s);
 
 // K4f: the main scan as a conservative 4-bit filter over 64-query items
 // (k_filter.cu).  Candidates are emitted as (position, probe rank); K4r

@@ -1153,7 +1153,12 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         a.sample_dist = total_samples ? sample_dist : nullptr;
         a.tau = tau;  // unused in the LUT pass
         a.item_counter = counter;
-        if (lut_pass_supported(ix.d, ix.m, ix.ks)) launch_lut_pass(a, s);
+        // (no more pairs than lists: about one probing query per item, where
+        // the 16-lane pass spends its time on dead lanes and its code-book ring)
+        // (two-phase: this is the near pass, nq * R1 pairs)
+        const size_t p_first = two_phase ? nq * (size_t)R1 : P;
+        if (p_first <= (size_t)c && lut_pass_narrow_supported(ix.d, ix.m, ix.ks)) launch_lut_pass_narrow(a, s);
+        else if (lut_pass_supported(ix.d, ix.m, ix.ks)) launch_lut_pass(a, s);
         else launch_ivf_scan(a, s);
     }
     if (timed) PQRR_CUDA(cudaEventRecord(ix.ev[3], s));

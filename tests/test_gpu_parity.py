@@ -965,3 +965,32 @@ def test_large_batch_warp_selections_match_oracle(pq, mid_instance, oracle):
         np.testing.assert_array_equal(bits(dd), bits(rd))
         st = dix.last_stats()
         assert st["ms_threshold"] > 0  # the synchronising path (more than 1024 queries)
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_narrow_lut_pass_many_lanes_per_list(pq, mid_instance, oracle, graph):
+    """Small batches (no more query-list pairs than lists) take the narrow LUT
+    pass (k_lutnarrow.cu: code book resident, two query lanes per LUT).  Seven
+    copies of two queries put up to 14 lanes on every probed list, so items
+    run through several lane pairs, odd lane counts included; shortlists
+    (every list sampled at k' = 8: stride 1) and re-ranked lists must equal
+    the oracle's on both search paths."""
+    oix, dix = mid_instance["oix"], mid_instance["dix"]
+    q = np.repeat(mid_instance["queries"][:2], 7, axis=0)[:13]
+    qf = q.astype(np.float32)
+    dix.set_graph(graph)
+    try:
+        for v, kprime, k in [(16, 300, 50), (19, 8, 8), (3, 2000, 100)]:
+            assert len(q) * v <= 256
+            oi, od, oc = oix.search(qf, v, kprime)
+            ri, rd = oix.rerank(qf, oi, oc, min(k, int(oc.min())))
+            di, dd, dc = dix.search(q, v, kprime, min(k, int(oc.min())))
+            np.testing.assert_array_equal(di, ri)
+            np.testing.assert_array_equal(bits(dd), bits(rd))
+            si, sd, sc = dix.search(q, v, kprime, 0)
+            np.testing.assert_array_equal(sc, oc)
+            for i in range(len(q)):
+                np.testing.assert_array_equal(si[i, :oc[i]], oi[i, :oc[i]])
+                np.testing.assert_array_equal(bits(sd[i, :oc[i]]), bits(od[i, :oc[i]]))
+    finally:
+        dix.set_graph(True)
