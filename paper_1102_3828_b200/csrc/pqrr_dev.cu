@@ -762,8 +762,11 @@ ItemSet items_phase1(Workspace& ws, const uint32_t* lists, const uint32_t* pair_
 // n_items may be an upper bound (enqueue-only search, `padded`): the slots
 // past the real count keep an all-ones sort key, so they sort last and no
 // kernel reaches them (every kernel reads the real count from item_off[c]).
+// identity_order: items keep their build order (chunked K4f items of a small
+// batch are all one chunk long but for list tails: the longest-first sort
+// would only cost its launches).
 void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_len, cudaStream_t s,
-                  bool padded = false) {
+                  bool padded = false, bool identity_order = false) {
     const uint32_t n = it.n_items;
     it.item_list = ws.alloc<uint32_t>(n);
     it.item_start = ws.alloc<uint32_t>(n);
@@ -777,6 +780,10 @@ void items_phase2(Workspace& ws, ItemSet& it, uint32_t c, const uint32_t* list_l
     if (padded) PQRR_CUDA(cudaMemsetAsync(key, 0xff, (size_t)std::max<uint32_t>(n, 1) * 4, s));
     launch_items_build(it.list_cnt, it.list_first, list_len, c, it.item_off, it.item_list,
                        it.item_start, it.item_nq, it.item_e0, it.item_e1, key, it.qt, s, it.chunk, n);
+    if (identity_order) {
+        launch_iota(it.item_order, n, s);
+        return;
+    }
     launch_iota(iota, n, s);
     sort_pairs(key, key2, iota, it.item_order, n, 32, s);
 }
@@ -1116,7 +1123,8 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
     // (small_inv: the sets finished by invert_small_kernel have their items;
     // their counts are bounds, so a set finished here is padded)
     if ((!two_phase || !use_filter) && !im.item_order) items_phase2(ws, im, c, ix.list_len.p, s, fast || small_inv);
-    if (use_filter && !if64.item_order) items_phase2(ws, if64, c, ix.list_len.p, s, fast || small_inv);
+    if (use_filter && !if64.item_order)
+        items_phase2(ws, if64, c, ix.list_len.p, s, fast || small_inv, small_inv && fchunk < (1u << 30));
     if (two_phase) {
         items_phase2(ws, im_near, c, ix.list_len.p, s, fast);
         items_phase2(ws, im_far, c, ix.list_len.p, s, fast);
