@@ -204,28 +204,61 @@ __global__ __launch_bounds__(NT, 1) void lut_pass_narrow_kernel(const ScanArgs a
             // entry sample_pos(s << sshift, smin) for the lane's slot s)
             if (sampling && mt.smin) {
                 const uint32_t smin = mt.smin;
-                for (int k = 0; k < 2 && lp + k < nqi; ++k) {
-                    if (!mt.samp[lp + k]) continue;
-                    const uint32_t sh = mt.sshift[lp + k];
+                constexpr int SU = 8;  // codes in flight per thread: random DRAM sectors, nothing else hides them
+                const bool s0 = mt.samp[lp], s1 = lp + 1 < nqi && mt.samp[lp + 1];
+                if (s0 && s1 && mt.sshift[lp] == mt.sshift[lp + 1]) {
+                    // both lanes at the same stride (two queries at the same probe
+                    // tier): one code per slot serves both
+                    const uint32_t sh = mt.sshift[lp];
                     const uint32_t st = smin << sh, ns = (len + st - 1) / st;
-                    float* out = a.sample_dist + mt.sbase[lp + k];
-                    constexpr int SU = 4;
-                    for (uint32_t s0 = t; s0 < ns; s0 += SU * NT) {
+                    float* out0 = a.sample_dist + mt.sbase[lp];
+                    float* out1 = a.sample_dist + mt.sbase[lp + 1];
+                    for (uint32_t sb = t; sb < ns; sb += SU * NT) {
                         u64 code[SU];
 #pragma unroll
                         for (int u = 0; u < SU; ++u) {
-                            const uint32_t s = s0 + u * NT;
+                            const uint32_t s = sb + u * NT;
                             code[u] = s < ns ? __ldg(lcodes + sample_pos(s << sh, smin, len)) : 0ull;
                         }
 #pragma unroll
                         for (int u = 0; u < SU; ++u) {
-                            const uint32_t s = s0 + u * NT;
+                            const uint32_t s = sb + u * NT;
                             if (s >= ns) break;
-                            float acc = 0.f;
+                            float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-                            for (int j = 0; j < M; ++j)
-                                acc = __fadd_rn(acc, lut[(j * KS + ((uint32_t)(code[u] >> (8 * j)) & 0xffu)) * 2 + k]);
-                            out[s] = acc;
+                            for (int j = 0; j < M; ++j) {
+                                const float2 v = *reinterpret_cast<const float2*>(
+                                    lut + (j * KS + ((uint32_t)(code[u] >> (8 * j)) & 0xffu)) * 2);
+                                acc0 = __fadd_rn(acc0, v.x);
+                                acc1 = __fadd_rn(acc1, v.y);
+                            }
+                            out0[s] = acc0;
+                            out1[s] = acc1;
+                        }
+                    }
+                } else {
+                    for (int k = 0; k < 2 && lp + k < nqi; ++k) {
+                        if (!mt.samp[lp + k]) continue;
+                        const uint32_t sh = mt.sshift[lp + k];
+                        const uint32_t st = smin << sh, ns = (len + st - 1) / st;
+                        float* out = a.sample_dist + mt.sbase[lp + k];
+                        for (uint32_t sb = t; sb < ns; sb += SU * NT) {
+                            u64 code[SU];
+#pragma unroll
+                            for (int u = 0; u < SU; ++u) {
+                                const uint32_t s = sb + u * NT;
+                                code[u] = s < ns ? __ldg(lcodes + sample_pos(s << sh, smin, len)) : 0ull;
+                            }
+#pragma unroll
+                            for (int u = 0; u < SU; ++u) {
+                                const uint32_t s = sb + u * NT;
+                                if (s >= ns) break;
+                                float acc = 0.f;
+#pragma unroll
+                                for (int j = 0; j < M; ++j)
+                                    acc = __fadd_rn(acc, lut[(j * KS + ((uint32_t)(code[u] >> (8 * j)) & 0xffu)) * 2 + k]);
+                                out[s] = acc;
+                            }
                         }
                     }
                 }
