@@ -994,3 +994,19 @@ def test_narrow_lut_pass_many_lanes_per_list(pq, mid_instance, oracle, graph):
                 np.testing.assert_array_equal(bits(sd[i, :oc[i]]), bits(od[i, :oc[i]]))
     finally:
         dix.set_graph(True)
+
+
+def test_graph_cache_eviction_and_recapture(pq, mid_instance, oracle):
+    """More batch shapes than the index caches graphs for (16): the least
+    recently used graph is destroyed (its graph memory trimmed) and a shape
+    that comes back is captured again; every search still equals the oracle."""
+    oix, dix, q = mid_instance["oix"], mid_instance["dix"], mid_instance["queries"]
+    v, kprime = 8, 100
+    oi, od, oc = oix.search(q.astype(np.float32), v, kprime)
+    for rnd in range(2):
+        for nq in range(1, 21):
+            di, dd, dc = dix.search(q[:nq], v, kprime, 0)
+            np.testing.assert_array_equal(dc, oc[:nq])
+            for i in range(nq):
+                np.testing.assert_array_equal(di[i, :oc[i]], oi[i, :oc[i]])
+                np.testing.assert_array_equal(bits(dd[i, :oc[i]]), bits(od[i, :oc[i]]))
