@@ -893,10 +893,11 @@ Plan make_plan(const DevIndex& ix, size_t nq, uint32_t w, uint32_t kprime, doubl
     const double spq = default_spq(kprime, w);  // samples expected below the target rank
     uint32_t stride = (uint32_t)std::max(1.0, std::floor(alpha * kprime / spq));
     pl.stride = std::max<uint32_t>(1, stride / std::max<uint32_t>(1, stride_div));
-    // (up to 64 queries the exact CUDA-core distances cost one 64-row tile
-    // pass over the centroids and need no certification: C5 batch 1 coarse
-    // stage 0.11 -> 0.03 ms)
-    pl.coarse_tc = !exact_coarse && nq > 64 && ix.c >= 1024u && coarse_tc_supported(ix.d, w);
+    // (up to 256 queries the exact CUDA-core distances cost a few 64-row tile
+    // passes over the centroids and need no certification, while the
+    // warp-per-query certify kernel would run on a handful of warps: C5 batch 1
+    // coarse stage 0.11 -> 0.03 ms, batch 256 0.11 -> 0.06 ms)
+    pl.coarse_tc = !exact_coarse && nq > 256 && ix.c >= 1024u && coarse_tc_supported(ix.d, w);
     // Two-phase LUT pass (w >= 32): the near probes (rank < w/8, the sampling
     // tier 0, where the shortlist lives at C3-C5) get the full LUT pass with
     // sampling, which fixes tau; the far probes get a bound pass (exact LUTs,
