@@ -211,7 +211,8 @@ void launch_lut_pass(const ScanArgs& a, cudaStream_t s);
 // The same pass for small batches (about one probing query per list): code
 // book resident, two query lanes per LUT (k_lutnarrow.cu).  Single-phase only.
 bool lut_pass_narrow_supported(uint32_t d, uint32_t m, uint32_t ks);
-void launch_lut_pass_narrow(const ScanArgs& a, cudaStream_t s);
+// max_items: an upper bound of the pass's items (no more than SMs: one item per CTA, undivided)
+void launch_lut_pass_narrow(const ScanArgs& a, cudaStream_t s, size_t max_items);
 
 // K4f: the main scan as a conservative 4-bit filter over 64-query items
 // (k_filter.cu).  Candidates are emitted as (position, probe rank); K4r

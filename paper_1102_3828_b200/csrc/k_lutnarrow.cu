@@ -30,7 +30,7 @@ constexpr int KS = 256;
 constexpr int QT = kQT;
 constexpr int DSUB = 16;
 constexpr int D = M * DSUB;
-constexpr int NT = 512;
+constexpr int NT = 512;  // NG groups of NT / NG threads share the resident code book, each on its own item
 constexpr int LANE_WORDS = M * KS / 4;  // one lane's 8-bit column (2 KiB)
 constexpr int Q8_BYTES = M * KS * QT;
 
@@ -45,25 +45,40 @@ struct NarrowMeta {
 // rows r .. r + 7 at one chunk index then cover 8 distinct 16-byte bank groups
 __device__ __forceinline__ int book_chunk(int r, int c) { return (c + (r >> 1)) & 3; }
 
+template <int NG>
 __global__ __launch_bounds__(NT, 1) void lut_pass_narrow_kernel(const ScanArgs a, const u64 nz) {
+    constexpr int GT = NT / NG;
     extern __shared__ float4 nl_smem[];
     float* book = reinterpret_cast<float*>(nl_smem);  // [M * KS][16], chunk-swizzled
-    float* lut = book + M * KS * DSUB;                // [M * KS][2]
-    float* xr = lut + M * KS * 2;                     // [2][D] residual queries of the lane pair
-    __shared__ NarrowMeta mt;
-    __shared__ unsigned s_mnu[M * 2], s_mxu[M * 2];
-    __shared__ float s_min[M * 2], s_inv[2];
-    const int t = threadIdx.x, lane = t & 31;
+    // NG = 2: two groups of 256 threads walk the items independently (named
+    // barriers): an item is a chain of dependent loads (claim -> item -> pairs
+    // -> rows, then the sampled codes at DRAM latency) with little arithmetic,
+    // so two items in flight per SM overlap each other's latencies (C5 batch
+    // 16: 0.494 -> 0.470 ms).  NG = 1 when there are no more items than SMs
+    // (one query: the whole CTA on its one item).
+    const int g = threadIdx.x / GT, t = threadIdx.x % GT, lane = t & 31;
+    float* lut = book + M * KS * DSUB + g * (M * KS * 2);              // per group [M * KS][2]
+    float* xr = book + M * KS * DSUB + NG * (M * KS * 2) + g * 2 * D;  // per group [2][D] residual queries
+    __shared__ NarrowMeta mt_all[NG];
+    __shared__ unsigned s_mnu_all[NG][M * 2], s_mxu_all[NG][M * 2];
+    __shared__ float s_min_all[NG][M * 2], s_inv_all[NG][2];
+    NarrowMeta& mt = mt_all[g];
+    unsigned* s_mnu = s_mnu_all[g];
+    unsigned* s_mxu = s_mxu_all[g];
+    float* s_min = s_min_all[g];
+    float* s_inv = s_inv_all[g];
+    auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(GT) : "memory"); };
     const uint32_t n_items = *a.num_items;
     // the code book, once per CTA
-    for (int i = t; i < M * KS * 4; i += NT) {
+    for (int i = threadIdx.x; i < M * KS * 4; i += NT) {
         const int r = i >> 2, c = i & 3;
         *reinterpret_cast<float4*>(book + r * DSUB + 4 * book_chunk(r & (KS - 1), c)) =
             __ldg(reinterpret_cast<const float4*>(a.books) + i);
     }
+    __syncthreads();
     const bool sampling = a.sample_dist != nullptr;
     for (;;) {
-        __syncthreads();  // the previous item is done with mt / lut / xr
+        gsync();  // the previous item is done with mt / lut / xr
         if (t < 32) {
             // ---- claim an item and gather its metadata (one warp)
             uint32_t c = 0;
@@ -100,13 +115,13 @@ __global__ __launch_bounds__(NT, 1) void lut_pass_narrow_kernel(const ScanArgs a
                 }
             }
         }
-        __syncthreads();
+        gsync();
         const uint32_t it = mt.it;
         if (it == 0xffffffffu) break;
         const uint32_t l = mt.l, len = mt.len, nqi = mt.nqi;
         const u64* lcodes = reinterpret_cast<const u64*>(a.codes) + a.list_off[l];
         for (uint32_t lp = 0; lp < nqi; lp += 2) {
-            if (lp) __syncthreads();  // the previous lane pair is done with lut / xr
+            if (lp) gsync();  // the previous lane pair is done with lut / xr
             // ---- residual queries x - C_l (ivf_index.hpp:58-59) of lanes lp, lp + 1
             if (t < 2 * D) {
                 const int k = t / D, e = t % D, q = lp + k < nqi ? mt.q[lp + k] : -1;
@@ -116,11 +131,11 @@ __global__ __launch_bounds__(NT, 1) void lut_pass_narrow_kernel(const ScanArgs a
                 s_mnu[t] = 0x7f800000u;
                 s_mxu[t] = 0u;
             }
-            __syncthreads();
-            // ---- exact LUT in the reference order: thread = 4 (j, code) entries x 2 lanes
+            gsync();
+            // ---- exact LUT in the reference order: thread = 8 (j, code) entries x 2 lanes
 #pragma unroll
-            for (int r = 0; r < M * KS / NT; ++r) {
-                const int idx = t + NT * r, j = idx >> 8, i = idx & (KS - 1);
+            for (int r = 0; r < M * KS / GT; ++r) {
+                const int idx = t + GT * r, j = idx >> 8, i = idx & (KS - 1);
                 const float* brow = book + idx * DSUB;
                 u64 sa01 = 0, sa23 = 0, sb01 = 0, sb23 = 0;
 #pragma unroll
@@ -159,7 +174,7 @@ __global__ __launch_bounds__(NT, 1) void lut_pass_narrow_kernel(const ScanArgs a
                     atomicMax(s_mxu + j * 2 + 1, __float_as_uint(mxb));
                 }
             }
-            __syncthreads();
+            gsync();
             // ---- 8-bit block of the live lanes (quantize as lut_pass_kernel)
             if (a.q8_param) {
                 if (t < 2) {
@@ -179,7 +194,7 @@ __global__ __launch_bounds__(NT, 1) void lut_pass_narrow_kernel(const ScanArgs a
                         prm[1] = sm;
                     }
                 }
-                __syncthreads();
+                gsync();
                 if (a.q8_cache) {
                     uint32_t* block = reinterpret_cast<uint32_t*>(a.q8_cache + (size_t)it * Q8_BYTES);
                     const float shrink = 0.99999904632568359375f;  // 1 - 2^-20 (see lut_pass_kernel)
@@ -188,7 +203,7 @@ __global__ __launch_bounds__(NT, 1) void lut_pass_narrow_kernel(const ScanArgs a
                         return __float_as_uint(__fadd_rd(x, 8388608.f)) & 0xffu;
                     };
                     // word rq of a lane's column = rows 4 rq .. 4 rq + 3 (row = j * KS + code)
-                    for (int wd = t; wd < 2 * LANE_WORDS; wd += NT) {
+                    for (int wd = t; wd < 2 * LANE_WORDS; wd += GT) {
                         const int k = wd / LANE_WORDS, rq = wd % LANE_WORDS;
                         if (lp + k >= nqi) continue;
                         const int j = (4 * rq) >> 8;
@@ -213,16 +228,16 @@ __global__ __launch_bounds__(NT, 1) void lut_pass_narrow_kernel(const ScanArgs a
                     const uint32_t st = smin << sh, ns = (len + st - 1) / st;
                     float* out0 = a.sample_dist + mt.sbase[lp];
                     float* out1 = a.sample_dist + mt.sbase[lp + 1];
-                    for (uint32_t sb = t; sb < ns; sb += SU * NT) {
+                    for (uint32_t sb = t; sb < ns; sb += SU * GT) {
                         u64 code[SU];
 #pragma unroll
                         for (int u = 0; u < SU; ++u) {
-                            const uint32_t s = sb + u * NT;
+                            const uint32_t s = sb + u * GT;
                             code[u] = s < ns ? __ldg(lcodes + sample_pos(s << sh, smin, len)) : 0ull;
                         }
 #pragma unroll
                         for (int u = 0; u < SU; ++u) {
-                            const uint32_t s = sb + u * NT;
+                            const uint32_t s = sb + u * GT;
                             if (s >= ns) break;
                             float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
@@ -242,16 +257,16 @@ __global__ __launch_bounds__(NT, 1) void lut_pass_narrow_kernel(const ScanArgs a
                         const uint32_t sh = mt.sshift[lp + k];
                         const uint32_t st = smin << sh, ns = (len + st - 1) / st;
                         float* out = a.sample_dist + mt.sbase[lp + k];
-                        for (uint32_t sb = t; sb < ns; sb += SU * NT) {
+                        for (uint32_t sb = t; sb < ns; sb += SU * GT) {
                             u64 code[SU];
 #pragma unroll
                             for (int u = 0; u < SU; ++u) {
-                                const uint32_t s = sb + u * NT;
+                                const uint32_t s = sb + u * GT;
                                 code[u] = s < ns ? __ldg(lcodes + sample_pos(s << sh, smin, len)) : 0ull;
                             }
 #pragma unroll
                             for (int u = 0; u < SU; ++u) {
-                                const uint32_t s = sb + u * NT;
+                                const uint32_t s = sb + u * GT;
                                 if (s >= ns) break;
                                 float acc = 0.f;
 #pragma unroll
@@ -271,12 +286,18 @@ __global__ __launch_bounds__(NT, 1) void lut_pass_narrow_kernel(const ScanArgs a
 
 bool lut_pass_narrow_supported(uint32_t d, uint32_t m, uint32_t ks) { return d == D && m == M && ks == KS; }
 
-void launch_lut_pass_narrow(const ScanArgs& a, cudaStream_t s) {
+void launch_lut_pass_narrow(const ScanArgs& a, cudaStream_t s, size_t max_items) {
     if (!lut_pass_narrow_supported(a.d, a.m, a.ks)) throw ArgError("narrow LUT pass supports d = 128, m = 8, ks = 256");
     if (a.q8_mode || a.skip_dead) throw ArgError("narrow LUT pass: single-phase only");
-    const size_t smem = ((size_t)M * KS * DSUB + (size_t)M * KS * 2 + 2 * D) * sizeof(float);
-    set_max_smem((const void*)lut_pass_narrow_kernel, smem);
-    lut_pass_narrow_kernel<<<sm_count(), NT, smem, s>>>(a, kNegZero2);
+    const int ng = max_items <= (size_t)sm_count() ? 1 : 2;
+    const size_t smem = ((size_t)M * KS * DSUB + (size_t)ng * (M * KS * 2 + 2 * D)) * sizeof(float);
+    if (ng == 1) {
+        set_max_smem((const void*)lut_pass_narrow_kernel<1>, smem);
+        lut_pass_narrow_kernel<1><<<sm_count(), NT, smem, s>>>(a, kNegZero2);
+    } else {
+        set_max_smem((const void*)lut_pass_narrow_kernel<2>, smem);
+        lut_pass_narrow_kernel<2><<<sm_count(), NT, smem, s>>>(a, kNegZero2);
+    }
     PQRR_LAUNCH_CHECK();
     count_launch();
 }

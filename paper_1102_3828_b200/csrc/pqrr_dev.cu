@@ -1166,7 +1166,7 @@ void shortlist_core(DevIndex& ix, const float* xq, size_t nq, uint32_t w, uint32
         // the 16-lane pass spends its time on dead lanes and its code-book ring)
         // (two-phase: this is the near pass, nq * R1 pairs)
         const size_t p_first = two_phase ? nq * (size_t)R1 : P;
-        if (p_first <= (size_t)c && lut_pass_narrow_supported(ix.d, ix.m, ix.ks)) launch_lut_pass_narrow(a, s);
+        if (p_first <= (size_t)c && lut_pass_narrow_supported(ix.d, ix.m, ix.ks)) launch_lut_pass_narrow(a, s, p_first);
         else if (lut_pass_supported(ix.d, ix.m, ix.ks)) launch_lut_pass(a, s);
         else launch_ivf_scan(a, s);
     }
